@@ -1,0 +1,157 @@
+/* irkdev.h -- C ABI of the B200-native IRK stage-system solve phase.
+ *
+ * Drop-in boundary for the reference's C++ solver interface (irkprec):
+ * plain pointers and sizes, no torch or C++ types.  Every entry point
+ * returns an irk_status; the message of the last failure on the calling
+ * thread is irk_last_error().  Error classes map 1:1 onto the reference's
+ * exceptions (common.hpp:16-41): IRK_EINVAL <-> std::invalid_argument
+ * (require, common.hpp:39-41), IRK_ESINGULAR <-> SingularError,
+ * IRK_ENUMERICAL <-> NumericalError.  GMRES non-convergence is NOT an error:
+ * it is reported in irk_report.converged (gmres.hpp:45-48).
+ *
+ * The library has no CPU fallback: device entry points fail with IRK_ECUDA
+ * when no CUDA device is present.
+ */
+#ifndef IRKDEV_H
+#define IRKDEV_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    IRK_OK = 0,
+    IRK_EINVAL = 1,       /* std::invalid_argument (common.hpp:39-41)     */
+    IRK_ESINGULAR = 2,    /* SingularError (common.hpp:16-24)             */
+    IRK_ENUMERICAL = 3,   /* NumericalError (common.hpp:28-37)            */
+    IRK_ECUDA = 4,        /* CUDA runtime failure / no device             */
+    IRK_EUNSUPPORTED = 5, /* valid reference option not run on the device */
+    IRK_EINTERNAL = 9
+} irk_status;
+
+const char* irk_last_error(void);
+
+/* CSR view (csr.hpp:15-32): int32 row_ptr[n_rows+1], col_idx[nnz],
+ * fp64 vals[nnz]; columns strictly increasing within a row. */
+typedef struct {
+    int n_rows, n_cols, nnz;
+    const int* row_ptr;
+    const int* col_idx;
+    const double* vals;
+} irk_csr;
+
+/* AmgParams (amg.hpp:14-29). smoother: 0 damped Jacobi (device), 1 GS. */
+typedef struct {
+    double theta;
+    int pre_sweeps, post_sweeps, smoother;
+    double jacobi_weight, prolongation_weight;
+    int prolongation_steps, max_coarse, max_levels;
+} irk_amg_params;
+void irk_amg_params_default(irk_amg_params* p);
+
+/* GmresConfig (gmres.hpp:17-21) plus the restart length of GMRES(m);
+ * restart = 0 means full GMRES (the reference's behaviour). side: 1 right. */
+typedef struct {
+    int side;
+    double rel_tol;
+    int max_iter;
+    int restart;
+} irk_gmres_cfg;
+void irk_gmres_cfg_default(irk_gmres_cfg* c); /* right, 1e-8, 500, 50 */
+
+/* SolveReport (gmres.hpp:23-38) without the history vector, which is
+ * copied into a caller buffer. */
+typedef struct {
+    int iterations, cycles, n_reorth, converged;
+    double final_rel_residual, true_rel_residual;
+    double solve_seconds, setup_seconds;
+    int history_len;
+} irk_report;
+
+/* ------------------------------------------------------ host setup ---- */
+typedef struct irk_problem irk_problem;
+/* Heat u_t = lap u on [0,1]^2, P1, zero Dirichlet, no forcing
+ * (study.cpp:190-211 minus the manufactured forcing). */
+int irk_problem_heat(int cells, irk_problem** out);
+/* Double glazing on [-1,1]^2, cells per side, P1 SUPG, East wall = 1
+ * (study.cpp:215-249, manufactured = false). */
+int irk_problem_double_glazing(int cells, double eps, irk_problem** out);
+int irk_problem_n(const irk_problem* p);
+/* which: 0 M (mass), 1 K (stiffness / SUPG operator, the reference's F). */
+int irk_problem_matrix(const irk_problem* p, int which, irk_csr* out);
+const double* irk_problem_lift(const irk_problem* p);
+/* u0 = sin(pi x) sin(pi y) + U[-noise, noise] (splitmix64(seed)). */
+int irk_problem_initial(const irk_problem* p, double noise, unsigned long long seed, double* u0);
+void irk_problem_free(irk_problem* p);
+
+/* scheme: 0 Radau IIA (s=1..7), 1 Lobatto IIIC (s=2..5)
+ * (butcher.hpp:31-40). A row-major s*s. */
+int irk_tableau(int scheme, int s, double* A, double* b, double* c, int* q);
+/* A = L diag(D) U (butcher.hpp:49-58). */
+int irk_ldu(int s, const double* A, double* L, double* D, double* U);
+/* kind: 0 Jacobi, 1 GSL, 2 DU, 3 LD (butcher.hpp:55-61).
+ * structure out: 0 diagonal, 1 lower, 2 upper. */
+int irk_precond_coeff(int scheme, int s, int kind, double* Atilde, int* structure);
+/* custom_coeff (butcher.hpp:71-73): validates and infers the structure. */
+int irk_custom_coeff(int s, const double* Atilde, int* structure);
+
+typedef struct irk_hierarchy irk_hierarchy;
+/* amg_setup (amg.hpp:52): the reference's smoothed-aggregation coarsening. */
+int irk_amg_setup(const irk_csr* A, const irk_amg_params* p, irk_hierarchy** out);
+int irk_hierarchy_levels(const irk_hierarchy* h);
+/* which: 0 A, 1 P, 2 R (amg.hpp:35-40). */
+int irk_hierarchy_level(const irk_hierarchy* h, int level, int which, irk_csr* out);
+const double* irk_hierarchy_inv_diag(const irk_hierarchy* h, int level);
+const double* irk_hierarchy_coarse_inverse(const irk_hierarchy* h, int* n);
+void irk_hierarchy_free(irk_hierarchy* h);
+
+/* ------------------------------------------------------ device solver - */
+typedef struct irkdev irkdev;
+
+/* BlockPreconditioner + StageOperator on the device
+ * (stage.hpp:56-59, stage.hpp:21-23).  A, b: Butcher matrix/weights;
+ * Atilde: preconditioner coefficients with `structure`.  When
+ * n_hier == 0 the hierarchies are built here (one per distinct Atilde_jj,
+ * stage.cpp:85-106); otherwise hiers[k] is used for the k-th distinct
+ * diagonal in first-appearance order. */
+int irkdev_create(const irk_csr* M, const irk_csr* K, int s, const double* A, const double* b,
+                  const double* Atilde, int structure, double ht, const irk_amg_params* amg,
+                  int n_hier, const irk_hierarchy* const* hiers, int device, irkdev** out);
+void irkdev_destroy(irkdev* d);
+int irkdev_info(const irkdev* d, int* n, int* s, int* n_hier, int* solver_of_block,
+                double* setup_seconds);
+/* hierarchy k, level l: sizes for the roofline byte model. */
+int irkdev_level_info(const irkdev* d, int k, int l, int* n, int* nnz_A, int* nnz_P,
+                      int* nnz_R, int* fmt_A);
+int irkdev_num_levels(const irkdev* d, int k);
+
+/* irk_step (irk.hpp:36-39): host pointers.  f_lift may be NULL (zero),
+ * k_out may be NULL; history (max_iter+1 doubles) may be NULL. */
+int irkdev_step(irkdev* d, const double* u_n, const double* f_lift, const irk_gmres_cfg* cfg,
+                double* u_next, double* k_out, irk_report* rep, double* history);
+/* Same with DEVICE pointers (inputs already resident in HBM). */
+int irkdev_step_device(irkdev* d, const double* d_u_n, const double* d_f_lift,
+                       const irk_gmres_cfg* cfg, double* d_u_next, double* d_k_out,
+                       irk_report* rep);
+
+/* Kernel-level entry points, host pointers (parity tests):
+ * StageOperator::apply (stage.cpp:28-44), BlockPreconditioner::apply
+ * (stage.cpp:138-182), amg_vcycle for hierarchy k (amg.cpp:229-237). */
+int irkdev_stage_apply(irkdev* d, const double* v, double* y);
+int irkdev_precond_apply(irkdev* d, const double* v, double* w);
+int irkdev_vcycle(irkdev* d, int k, const double* r, double* z);
+/* Deterministic device dot (the GMRES reduction tree), host pointers. */
+int irkdev_dot(irkdev* d, const double* x, const double* y, long long n, double* out);
+
+/* Roofline hook: mean ms per launch of a hot kernel, CUDA events on the
+ * solver stream.  which: 0 stage operator, 1 fine smoother SpMV,
+ * 2 preconditioner apply, 3 V-cycle. */
+int irkdev_time_kernel(irkdev* d, int which, int reps, double* ms);
+/* Kernel launches per GMRES iteration in the captured graph body, and the
+ * graph mode (1 conditional WHILE nodes, 0 host-driven). */
+int irkdev_graph_info(const irkdev* d, int* launches_per_iteration, int* graph_mode);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,399 @@
+/* TEST INFRASTRUCTURE ONLY -- CPU restatement ("oracle") of the IRK solve
+ * phase of irkprec, used by tests/ (as the checker), __graft_entry__.smoke()
+ * and bench.py's cpu_baseline leg.  The product path never links or calls it.
+ *
+ * Parity is pinned two ways:
+ *   1. against the reference itself compiled in place (oracle/_ref, built by
+ *      oracle/Makefile from /root/reference/proj/src): stage apply, V-cycle,
+ *      preconditioner apply and whole IRK steps, tests/test_oracle_vs_ref.py;
+ *   2. against the reference's own known-answer tests restated in
+ *      tests/test_oracle_kat.py (test_blocksolve.cpp, test_amg.cpp KATs).
+ *
+ * Restated algorithms (reference file:line):
+ *   or_spmv           csr.cpp:102-114       sequential row sums
+ *   or_stage_apply    stage.cpp:28-44       s F-products, s M-products, s^2 axpys
+ *   or_vcycle         amg.cpp:115-168, 229-237  V(pre,post) damped Jacobi
+ *   or_precond_apply  stage.cpp:138-182     diagonal / forward / backward sweeps
+ *   or_irk_step       irk.cpp:9-68, gmres.cpp:14-142 with the documented
+ *                     deviations of the B200 path: GMRES(m) restarts, classical
+ *                     Gram-Schmidt with the reference's 0.7071 second-pass
+ *                     rule (gmres.cpp:84), a flexible basis (x = Z y, which
+ *                     equals P^-1 V y by linearity), dense coarse inverse.
+ *
+ * Floating-point order mirrors the device kernels exactly (compiled with
+ * -ffp-contract=off; device with --fmad=false), including the fixed
+ * reduction tree of paper_2010_11377_b200/csrc/device/common.cuh, so the
+ * device result is expected to be bit-identical to this file's. */
+#include "irk_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#include <time.h>
+
+#define RED_T 256
+#define RED_PT 16
+#define CHUNK (RED_T * RED_PT)
+
+/* ------------------------------------------------------------ reductions */
+/* Warp shuffle-down tree on 32 lanes (lane 0 result). */
+static double warp_tree(double* a) {
+    for (int off = 16; off > 0; off >>= 1)
+        for (int i = 0; i < off; ++i) a[i] = a[i] + a[i + off];
+    return a[0];
+}
+
+/* 256 per-thread values -> block sum: per-warp trees, then warps in order. */
+static double block_sum(double* t) {
+    double w[8];
+    for (int k = 0; k < 8; ++k) w[k] = warp_tree(t + 32 * k);
+    double r = w[0];
+    for (int k = 1; k < 8; ++k) r += w[k];
+    return r;
+}
+
+static double chunk_partial(const double* x, const double* y, long n, long c) {
+    double t[RED_T];
+    for (int th = 0; th < RED_T; ++th) {
+        double acc = 0.0;
+        for (int u = 0; u < RED_PT / 2; ++u)
+            for (int e = 0; e < 2; ++e) {
+                const long k = c * CHUNK + (long)u * 2 * RED_T + 2 * th + e;
+                const double xv = k < n ? x[k] : 0.0, yv = k < n ? y[k] : 0.0;
+                acc += xv * yv;
+            }
+        t[th] = acc;
+    }
+    return block_sum(t);
+}
+
+static double final_sum(const double* part, long nch) {
+    double t[RED_T];
+    for (int th = 0; th < RED_T; ++th) {
+        double acc = 0.0;
+        for (long p = th; p < nch; p += RED_T) acc += part[p];
+        t[th] = acc;
+    }
+    return block_sum(t);
+}
+
+double or_dot(const double* x, const double* y, long n) {
+    long nch = (n + CHUNK - 1) / CHUNK;
+    if (nch < 1) nch = 1;
+    double* part = (double*)malloc(sizeof(double) * nch);
+#pragma omp parallel for schedule(static)
+    for (long c = 0; c < nch; ++c) part[c] = chunk_partial(x, y, n, c);
+    const double r = final_sum(part, nch);
+    free(part);
+    return r;
+}
+
+/* ------------------------------------------------------------ sparse */
+void or_spmv(const or_csr* A, const double* x, double* y) {
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < A->rows; ++i) {
+        double s = 0.0;
+        for (int k = A->ptr[i]; k < A->ptr[i + 1]; ++k) s += A->val[k] * x[A->idx[k]];
+        y[i] = s;
+    }
+}
+
+/* y_i = e(s_i) for s = A x with x = wd.*r (implicit) or x (plain). */
+enum { EPI_PLAIN, EPI_RESID, EPI_SMOOTH, EPI_PROLONG };
+
+static void spmv_epi(const or_csr* A, const double* x, const double* r, const double* wd,
+                     const double* zb, int implicit_x, int epi, double* y) {
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < A->rows; ++i) {
+        double s = 0.0;
+        for (int k = A->ptr[i]; k < A->ptr[i + 1]; ++k) {
+            const int c = A->idx[k];
+            const double xv = implicit_x ? wd[c] * r[c] : x[c];
+            s += A->val[k] * xv;
+        }
+        double out = s;
+        if (epi == EPI_RESID) out = r[i] - s;
+        else if (epi == EPI_SMOOTH) out = x[i] + wd[i] * (r[i] - s);
+        else if (epi == EPI_PROLONG) out = (zb ? zb[i] : wd[i] * r[i]) + s;
+        y[i] = out;
+    }
+}
+
+/* ------------------------------------------------------------ V-cycle */
+static void vcycle_level(const or_hier* h, double** wd, int l, const double* r, double* z) {
+    const or_csr* A = &h->A[l];
+    const int n = A->rows;
+    if (l == h->nlev - 1) {
+        for (int i = 0; i < n; ++i) {
+            double s = 0.0;
+            for (int j = 0; j < n; ++j) s += h->cinv[(long)i * n + j] * r[j];
+            z[i] = s;
+        }
+        return;
+    }
+    const int nc = h->A[l + 1].rows;
+    double* t = (double*)malloc(sizeof(double) * n);
+    double* zp = NULL;
+    double* rc = (double*)malloc(sizeof(double) * nc);
+    double* zc = (double*)malloc(sizeof(double) * nc);
+    if (h->pre > 1) {
+        /* first sweep from z = 0 gives wd.*r, then pre-1 Jacobi sweeps */
+        zp = (double*)malloc(sizeof(double) * n);
+        double* tmp = (double*)malloc(sizeof(double) * n);
+        for (int i = 0; i < n; ++i) zp[i] = wd[l][i] * r[i];
+        for (int sw = 1; sw < h->pre; ++sw) {
+            spmv_epi(A, zp, r, wd[l], NULL, 0, EPI_SMOOTH, tmp);
+            memcpy(zp, tmp, sizeof(double) * n);
+        }
+        free(tmp);
+        spmv_epi(A, zp, r, wd[l], NULL, 0, EPI_RESID, t);
+    } else {
+        spmv_epi(A, NULL, r, wd[l], NULL, 1, EPI_RESID, t);
+    }
+    or_spmv(&h->R[l], t, rc);
+    vcycle_level(h, wd, l + 1, rc, zc);
+    /* z = zp + P zc, then post-smoothing sweeps */
+    spmv_epi(&h->P[l], zc, r, wd[l], zp, 0, EPI_PROLONG, t);
+    double* cur = t;
+    double* nxt = z;
+    for (int sw = 0; sw < h->post; ++sw) {
+        spmv_epi(A, cur, r, wd[l], NULL, 0, EPI_SMOOTH, nxt);
+        double* sv = cur;
+        cur = nxt;
+        nxt = sv;
+    }
+    if (cur != z) memcpy(z, cur, sizeof(double) * n);
+    free(t);
+    free(zp);
+    free(rc);
+    free(zc);
+}
+
+void or_vcycle(const or_hier* h, const double* r, double* z) {
+    double** wd = (double**)malloc(sizeof(double*) * h->nlev);
+    for (int l = 0; l < h->nlev; ++l) {
+        const int n = h->A[l].rows;
+        wd[l] = (double*)malloc(sizeof(double) * n);
+        for (int i = 0; i < n; ++i) wd[l][i] = h->omega * h->inv_diag[l][i];
+    }
+    vcycle_level(h, wd, 0, r, z);
+    for (int l = 0; l < h->nlev; ++l) free(wd[l]);
+    free(wd);
+}
+
+/* ------------------------------------------------------------ stage system */
+void or_stage_apply(const or_sys* S, const double* v, double* y) {
+    const int n = S->n, s = S->s;
+    double* Fv = (double*)malloc(sizeof(double) * (size_t)s * n);
+    for (int j = 0; j < s; ++j) or_spmv(&S->K, v + (size_t)j * n, Fv + (size_t)j * n);
+    for (int i = 0; i < s; ++i) {
+        double* yi = y + (size_t)i * n;
+        or_spmv(&S->M, v + (size_t)i * n, yi);
+        for (int j = 0; j < s; ++j) {
+            const double c = S->ht * S->A[i * s + j];
+            const double* f = Fv + (size_t)j * n;
+            for (int k = 0; k < n; ++k) yi[k] = yi[k] + c * f[k];
+        }
+    }
+    free(Fv);
+}
+
+void or_precond_apply(const or_sys* S, const double* v, double* w) {
+    const int n = S->n, s = S->s;
+    double* Fw = (double*)malloc(sizeof(double) * (size_t)s * n);
+    double* rhs = (double*)malloc(sizeof(double) * n);
+    for (int q = 0; q < s; ++q) {
+        const int j = S->structure == 2 ? s - 1 - q : q;
+        const double* in = v + (size_t)j * n;
+        if (S->structure != 0 && q > 0) {
+            const int prev = S->structure == 2 ? j + 1 : j - 1;
+            or_spmv(&S->K, w + (size_t)prev * n, Fw + (size_t)prev * n);
+            const int k0 = S->structure == 2 ? j + 1 : 0;
+            const int k1 = S->structure == 2 ? s : j;
+            memcpy(rhs, in, sizeof(double) * n);
+            for (int k = k0; k < k1; ++k) {
+                const double a = S->At[j * s + k];
+                if (a == 0.0) continue;
+                const double e = -S->ht * a;
+                const double* f = Fw + (size_t)k * n;
+                for (int i = 0; i < n; ++i) rhs[i] = rhs[i] + e * f[i];
+            }
+            in = rhs;
+        }
+        or_vcycle(&S->h[S->sob[j]], in, w + (size_t)j * n);
+    }
+    free(Fw);
+    free(rhs);
+}
+
+/* ------------------------------------------------------------ GMRES(m) */
+static double hyp(double a, double b) {
+    a = fabs(a);
+    b = fabs(b);
+    const double mx = a > b ? a : b, mn = a > b ? b : a;
+    if (mx == 0.0) return 0.0;
+    const double r = mn / mx;
+    return mx * sqrt(1.0 + r * r);
+}
+
+int or_irk_step(const or_sys* S, const double* u, const double* lift, double rtol, int restart,
+                int max_iter, double* u_next, double* K, or_report* rep, double* hist) {
+    struct timespec ts0, ts1;
+    clock_gettime(CLOCK_MONOTONIC, &ts0);
+    const int n = S->n, s = S->s;
+    const long N = (long)s * n;
+    if (restart <= 0 || restart > max_iter) restart = max_iter;
+    const int R = restart;
+    double* b = (double*)malloc(sizeof(double) * N);
+    double* x = (double*)calloc(N, sizeof(double));
+    double* r = (double*)malloc(sizeof(double) * N);
+    double* ax = (double*)malloc(sizeof(double) * N);
+    double* V = (double*)malloc(sizeof(double) * N * (R + 1));
+    double* Z = (double*)malloc(sizeof(double) * N * (R > 0 ? R : 1));
+    double* H = (double*)calloc((size_t)(R > 0 ? R : 1) * (R + 1), sizeof(double));
+    double* g = (double*)calloc(R + 1, sizeof(double));
+    double* cs = (double*)calloc(R + 1, sizeof(double));
+    double* sn = (double*)calloc(R + 1, sizeof(double));
+    double* h = (double*)calloc(R + 2, sizeof(double));
+    double* cc = (double*)calloc(R + 2, sizeof(double));
+    double* y = (double*)calloc(R + 1, sizeof(double));
+
+    /* stage right-hand side (irk.cpp:9-33, no forcing) */
+    {
+        double* ku = (double*)malloc(sizeof(double) * n);
+        or_spmv(&S->K, u, ku);
+        for (int i = 0; i < n; ++i) {
+            double f = ku[i];
+            if (lift) f = f + lift[i];
+            for (int q = 0; q < s; ++q) b[(long)q * n + i] = -f;
+        }
+        free(ku);
+    }
+    memcpy(r, b, sizeof(double) * N);
+    const double bnorm = sqrt(or_dot(b, b, N));
+    int total = 0, cycles = 0, nre = 0, converged = 0, stop = 0;
+    double beta = bnorm, tol_c = rtol, final_rel = 1.0, true_rel = 0.0;
+    if (hist) hist[0] = 1.0;
+    if (bnorm == 0.0) {
+        converged = 1;
+        final_rel = 0.0;
+        if (hist) hist[0] = 0.0;
+    } else {
+        int budget = R < max_iter ? R : max_iter;
+        double inv = 1.0 / bnorm;
+        while (budget > 0) {
+            for (long k = 0; k < N; ++k) V[k] = r[k] * inv;
+            g[0] = beta;
+            int j = 0, m = 0;
+            stop = 0;
+            while (1) {
+                double* vj = V + (long)j * N;
+                double* zj = Z + (long)j * N;
+                double* w = V + (long)(j + 1) * N;
+                or_precond_apply(S, vj, zj);
+                or_stage_apply(S, zj, w);
+                for (int i = 0; i <= j; ++i) h[i] = or_dot(V + (long)i * N, w, N);
+                const double before = sqrt(or_dot(w, w, N));
+                for (long k = 0; k < N; ++k) {
+                    double t = w[k];
+                    for (int i = 0; i <= j; ++i) t = t - h[i] * V[(long)i * N + k];
+                    w[k] = t;
+                }
+                double hnext = sqrt(or_dot(w, w, N));
+                if (hnext < 0.70710678118654752 * before) {
+                    for (int i = 0; i <= j; ++i) cc[i] = or_dot(V + (long)i * N, w, N);
+                    for (long k = 0; k < N; ++k) {
+                        double t = w[k];
+                        for (int i = 0; i <= j; ++i) t = t - cc[i] * V[(long)i * N + k];
+                        w[k] = t;
+                    }
+                    for (int i = 0; i <= j; ++i) h[i] = h[i] + cc[i];
+                    hnext = sqrt(or_dot(w, w, N));
+                    nre += 1;
+                }
+                /* Givens (gmres.cpp:93-112) */
+                h[j + 1] = hnext;
+                for (int i = 0; i < j; ++i) {
+                    const double t = cs[i] * h[i] + sn[i] * h[i + 1];
+                    h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+                    h[i] = t;
+                }
+                const double denom = hyp(h[j], h[j + 1]);
+                double c = 1.0, sv = 0.0;
+                if (denom > 0.0) {
+                    c = h[j] / denom;
+                    sv = h[j + 1] / denom;
+                }
+                cs[j] = c;
+                sn[j] = sv;
+                h[j] = denom;
+                h[j + 1] = 0.0;
+                g[j + 1] = -sv * g[j];
+                g[j] = c * g[j];
+                for (int i = 0; i <= j + 1; ++i) H[(long)j * (R + 1) + i] = h[i];
+                total += 1;
+                m = j + 1;
+                const double res_rel = fabs(g[j + 1]) / beta;
+                const double hv = cycles == 0 ? res_rel : res_rel * beta / bnorm;
+                if (hist) hist[total] = hv;
+                final_rel = hv;
+                const int bad = !(res_rel == res_rel) || !(hnext == hnext);
+                if (res_rel <= tol_c) stop = 1;
+                else if (hnext <= 1e-14 * beta || bad) stop = 2;
+                else if (j + 1 >= budget) stop = 3;
+                else stop = 0;
+                if (stop) break;
+                const double hinv = 1.0 / hnext;
+                for (long k = 0; k < N; ++k) w[k] = w[k] * hinv;
+                j += 1;
+            }
+            /* y = H^-1 g, x += Z y (gmres.cpp:126-132, flexible form) */
+            for (int i = m - 1; i >= 0; --i) {
+                double acc = g[i];
+                for (int k = i + 1; k < m; ++k) acc -= H[(long)k * (R + 1) + i] * y[k];
+                y[i] = acc / H[(long)i * (R + 1) + i];
+            }
+            for (long k = 0; k < N; ++k) {
+                double t = x[k];
+                for (int i = 0; i < m; ++i) t = t + y[i] * Z[(long)i * N + k];
+                x[k] = t;
+            }
+            or_stage_apply(S, x, ax);
+            for (long k = 0; k < N; ++k) r[k] = b[k] - ax[k];
+            const double rn = sqrt(or_dot(r, r, N));
+            cycles += 1;
+            true_rel = rn / bnorm;
+            if (stop == 1 || stop == 2 || total >= max_iter || rn == 0.0) {
+                converged = stop == 1;
+                break;
+            }
+            beta = rn;
+            tol_c = rtol * bnorm / rn;
+            const int left = max_iter - total;
+            budget = R < left ? R : left;
+            inv = 1.0 / rn;
+        }
+    }
+    /* u_{n+1} = u_n + ht sum_i b_i K_i (irk.cpp:59-65) */
+    double hb[7];
+    for (int q = 0; q < s; ++q) hb[q] = S->ht * S->b[q];
+    for (int i = 0; i < n; ++i) {
+        double acc = u[i];
+        for (int q = 0; q < s; ++q) acc = acc + hb[q] * x[(long)q * n + i];
+        u_next[i] = acc;
+    }
+    if (K) memcpy(K, x, sizeof(double) * N);
+    clock_gettime(CLOCK_MONOTONIC, &ts1);
+    if (rep) {
+        rep->iterations = total;
+        rep->cycles = cycles;
+        rep->n_reorth = nre;
+        rep->converged = converged;
+        rep->true_rel = true_rel;
+        rep->final_rel = final_rel;
+        rep->seconds = (ts1.tv_sec - ts0.tv_sec) + 1e-9 * (ts1.tv_nsec - ts0.tv_nsec);
+    }
+    free(b); free(x); free(r); free(ax); free(V); free(Z); free(H);
+    free(g); free(cs); free(sn); free(h); free(cc); free(y);
+    return 0;
+}

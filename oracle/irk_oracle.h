@@ -1,0 +1,65 @@
+/* TEST INFRASTRUCTURE ONLY -- CPU restatement of the IRK solve phase.
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg load
+ * this (as the checker).  The product never links it.  See irk_oracle.c. */
+#ifndef IRK_ORACLE_H
+#define IRK_ORACLE_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+    int rows, cols;
+    const int* ptr;
+    const int* idx;
+    const double* val;
+} or_csr;
+
+typedef struct {
+    int nlev;
+    const or_csr* A;             /* nlev */
+    const or_csr* P;             /* nlev - 1 */
+    const or_csr* R;             /* nlev - 1 */
+    const double* const* inv_diag; /* nlev */
+    const double* cinv;          /* dense nc x nc inverse of A[nlev-1] */
+    int nc;
+    double omega;
+    int pre, post;
+} or_hier;
+
+typedef struct {
+    int n, s;
+    or_csr M, K;
+    const double* A;   /* s*s Butcher matrix */
+    const double* b;   /* s weights */
+    double ht;
+    const double* At;  /* s*s preconditioner coefficients */
+    int structure;     /* 0 diagonal, 1 lower, 2 upper */
+    int nh;
+    const or_hier* h;
+    const int* sob;    /* solver_of_block[s] */
+} or_sys;
+
+void or_spmv(const or_csr* A, const double* x, double* y);
+double or_dot(const double* x, const double* y, long n);
+void or_vcycle(const or_hier* h, const double* r, double* z);
+void or_stage_apply(const or_sys* S, const double* v, double* y);
+void or_precond_apply(const or_sys* S, const double* v, double* w);
+
+typedef struct {
+    int iterations, cycles, n_reorth, converged;
+    double true_rel, final_rel;
+    double seconds;
+} or_report;
+
+/* One IRK step: rhs, GMRES(restart) (right preconditioning, CGS with the
+ * reference's conditional second pass, flexible basis), u_next.  hist gets
+ * max_iter+1 entries (may be NULL). */
+int or_irk_step(const or_sys* S, const double* u, const double* lift, double rtol,
+                int restart, int max_iter, double* u_next, double* K, or_report* rep,
+                double* hist);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

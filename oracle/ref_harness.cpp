@@ -1,0 +1,390 @@
+// TEST INFRASTRUCTURE ONLY.  Builds into oracle/_ref/libirkref.so together
+// with the reference's own hot-path sources compiled in place from
+// /root/reference/proj/src (see oracle/Makefile).  Nothing in the product
+// links or loads this library: only tests/, __graft_entry__.smoke() and the
+// CPU-baseline / `--impl reference` legs of bench.py do, as the checker.
+//
+// What this file adds around the unmodified reference code:
+//   * a C ABI so the Python test-suite can drive the reference through ctypes;
+//   * the heat problem WITHOUT manufactured forcing (mirrors
+//     study.cpp:190-211 minus the forcing) and the
+//     double-glazing setup (mirrors study.cpp:215-249, u0 = 0);
+//   * a GMRES(m) restart wrapper around the reference's full `gmres`
+//     (gmres.cpp:14-142) -- the reference itself never restarts
+//     (gmres.hpp:20), SURVEY §8c3 item 2;
+//   * a K-returning IRK step (irk.cpp:35-68 keeps K internal; the wrapper
+//     replicates it the way run_error_study does, study.cpp:628-634).
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "irkprec/amg.hpp"
+#include "irkprec/butcher.hpp"
+#include "irkprec/csr.hpp"
+#include "irkprec/fem.hpp"
+#include "irkprec/gmres.hpp"
+#include "irkprec/irk.hpp"
+#include "irkprec/kernels.hpp"
+#include "irkprec/mesh.hpp"
+#include "irkprec/stage.hpp"
+
+using namespace irkprec;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const SingularError& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const NumericalError& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 9;
+    }
+}
+
+CsrMatrix from_arrays(int n_rows, int n_cols, const int* rp, const int* ci,
+                      const double* v) {
+    CsrMatrix A;
+    A.n_rows = n_rows;
+    A.n_cols = n_cols;
+    A.row_ptr.assign(rp, rp + n_rows + 1);
+    const int nnz = rp[n_rows];
+    A.col_idx.assign(ci, ci + nnz);
+    A.vals.assign(v, v + nnz);
+    return A;
+}
+
+struct RefProblem {
+    std::shared_ptr<const CsrMatrix> M, F;
+    Vec f_lift;
+};
+
+struct RefSolver {
+    std::shared_ptr<const CsrMatrix> M, F;
+    ButcherTable table;
+    PrecondCoeff coeff;
+    double ht = 0.0;
+    std::unique_ptr<BlockPreconditioner> P;
+    std::unique_ptr<StageOperator> op;
+};
+
+ButcherTable make_table(int scheme, int s) {
+    return scheme == 1 ? make_lobatto_iiic(s) : make_radau_iia(s);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// ---------------------------------------------------------------- problems
+// kind 0: heat on [0,1]^2 with `cells` cells per side, P1, zero Dirichlet,
+//         no forcing (study.cpp:190-211 without manufactured_problem).
+// kind 1: double glazing on [-1,1]^2 with `cells` cells per side, P1 SUPG,
+//         eps, East wall = 1 (study.cpp:215-249, manufactured = false).
+int ref_problem_create(int kind, int cells, double eps, void** out) {
+    return guard([&] {
+        auto* p = new RefProblem;
+        if (kind == 0) {
+            const Mesh2D mesh = build_structured_mesh(Domain::UnitSquare, cells);
+            const FemSpace space = make_space(mesh, 1);
+            const CsrMatrix M_full = assemble_mass(space);
+            const CsrMatrix F_full = assemble_diffusion(space, 1.0);
+            EliminatedSystem e = eliminate_dirichlet(M_full, F_full, space, {});
+            p->M = std::make_shared<const CsrMatrix>(std::move(e.M_ff));
+            p->F = std::make_shared<const CsrMatrix>(std::move(e.F_ff));
+            p->f_lift = std::move(e.f_lift);
+        } else {
+            const Mesh2D mesh = build_structured_mesh(Domain::BiUnitSquare, cells);
+            const FemSpace space = make_space(mesh, 1);
+            SupgMatrices supg =
+                assemble_advection_supg(space, make_double_glazing_wind(), eps);
+            WallValues walls;
+            walls.east = 1.0;
+            EliminatedSystem e = eliminate_dirichlet(supg.M, supg.F, space, walls);
+            p->M = std::make_shared<const CsrMatrix>(std::move(e.M_ff));
+            p->F = std::make_shared<const CsrMatrix>(std::move(e.F_ff));
+            p->f_lift = std::move(e.f_lift);
+        }
+        *out = p;
+    });
+}
+
+void ref_problem_free(void* h) { delete static_cast<RefProblem*>(h); }
+
+// which: 0 = M, 1 = F (K).  Pointers stay valid while the problem lives.
+int ref_problem_csr(void* h, int which, int* n, int* nnz, const int** rp,
+                    const int** ci, const double** v) {
+    auto* p = static_cast<RefProblem*>(h);
+    const CsrMatrix& A = which == 0 ? *p->M : *p->F;
+    *n = A.n_rows;
+    *nnz = A.nnz();
+    *rp = A.row_ptr.data();
+    *ci = A.col_idx.data();
+    *v = A.vals.data();
+    return 0;
+}
+
+const double* ref_problem_flift(void* h) {
+    return static_cast<RefProblem*>(h)->f_lift.data();
+}
+
+// ---------------------------------------------------------------- butcher
+int ref_butcher(int scheme, int s, double* A, double* b, double* c, int* q) {
+    return guard([&] {
+        const ButcherTable t = make_table(scheme, s);
+        for (int i = 0; i < s * s; ++i) A[i] = t.A.values[i];
+        for (int i = 0; i < s; ++i) {
+            b[i] = t.b[i];
+            c[i] = t.c[i];
+        }
+        *q = t.q;
+    });
+}
+
+// kind: 0 jacobi, 1 gsl, 2 du, 3 ld  (butcher.hpp:55-61 order)
+int ref_precond_coeff(int scheme, int s, int kind, double* Atilde,
+                      int* structure) {
+    return guard([&] {
+        const ButcherTable t = make_table(scheme, s);
+        const PrecondCoeff pc = precond_coeff(t, static_cast<CoeffKind>(kind));
+        for (int i = 0; i < s * s; ++i) Atilde[i] = pc.Atilde.values[i];
+        *structure = static_cast<int>(pc.structure);
+    });
+}
+
+int ref_ldu(int s, const double* A, double* L, double* D, double* U) {
+    return guard([&] {
+        DenseMatrix M(s, s);
+        for (int i = 0; i < s * s; ++i) M.values[i] = A[i];
+        const LduFactors f = ldu_factorize(M);
+        for (int i = 0; i < s * s; ++i) {
+            L[i] = f.L.values[i];
+            U[i] = f.U.values[i];
+        }
+        for (int i = 0; i < s; ++i) D[i] = f.D[i];
+    });
+}
+
+// ---------------------------------------------------------------- AMG
+int ref_amg_setup(int n, const int* rp, const int* ci, const double* v,
+                  double theta, int pre, int post, int max_coarse,
+                  int max_levels, int psteps, void** out) {
+    return guard([&] {
+        AmgParams prm;
+        prm.theta = theta;
+        prm.pre_sweeps = pre;
+        prm.post_sweeps = post;
+        prm.max_coarse = max_coarse;
+        prm.max_levels = max_levels;
+        prm.prolongation_steps = psteps;
+        auto* h = new AmgHierarchy(amg_setup(from_arrays(n, n, rp, ci, v), prm));
+        *out = h;
+    });
+}
+
+void ref_amg_free(void* h) { delete static_cast<AmgHierarchy*>(h); }
+
+int ref_amg_nlevels(void* h) { return static_cast<AmgHierarchy*>(h)->n_levels(); }
+
+// which: 0 = A, 1 = P, 2 = R.
+int ref_amg_level(void* hp, int lev, int which, int* n_rows, int* n_cols,
+                  int* nnz, const int** rp, const int** ci, const double** v) {
+    auto* h = static_cast<AmgHierarchy*>(hp);
+    if (lev < 0 || lev >= h->n_levels()) return 1;
+    const auto& L = h->levels[lev];
+    const CsrMatrix& A = which == 0 ? L.A : which == 1 ? L.P : L.R;
+    *n_rows = A.n_rows;
+    *n_cols = A.n_cols;
+    *nnz = A.nnz();
+    *rp = A.row_ptr.data();
+    *ci = A.col_idx.data();
+    *v = A.vals.data();
+    return 0;
+}
+
+const double* ref_amg_invdiag(void* hp, int lev) {
+    return static_cast<AmgHierarchy*>(hp)->levels[lev].inv_diag.data();
+}
+
+int ref_amg_vcycle(void* hp, const double* r, double* z) {
+    return guard([&] {
+        auto* h = static_cast<AmgHierarchy*>(hp);
+        const int n = h->fine_size();
+        amg_vcycle(*h, std::span<const double>(r, n), std::span<double>(z, n));
+    });
+}
+
+// ---------------------------------------------------------------- solver
+// A BlockPreconditioner + StageOperator over caller-supplied M, K.
+int ref_solver_create(int n, const int* m_rp, const int* m_ci, const double* m_v,
+                      const int* k_rp, const int* k_ci, const double* k_v,
+                      int scheme, int s, int kind, double ht, double theta,
+                      int pre, int post, int max_coarse, void** out) {
+    return guard([&] {
+        auto* S = new RefSolver;
+        S->M = std::make_shared<const CsrMatrix>(from_arrays(n, n, m_rp, m_ci, m_v));
+        S->F = std::make_shared<const CsrMatrix>(from_arrays(n, n, k_rp, k_ci, k_v));
+        S->table = make_table(scheme, s);
+        S->coeff = precond_coeff(S->table, static_cast<CoeffKind>(kind));
+        S->ht = ht;
+        AmgParams prm;
+        prm.theta = theta;
+        prm.pre_sweeps = pre;
+        prm.post_sweeps = post;
+        prm.max_coarse = max_coarse;
+        S->P = std::make_unique<BlockPreconditioner>(
+            S->M, S->F, S->coeff, ht, SubsolverKind::AmgVcycle, prm);
+        S->op = std::make_unique<StageOperator>(S->M, S->F, S->table.A, ht);
+        *out = S;
+    });
+}
+
+void ref_solver_free(void* h) { delete static_cast<RefSolver*>(h); }
+
+double ref_solver_setup_seconds(void* h) {
+    return static_cast<RefSolver*>(h)->P->setup_seconds();
+}
+
+int ref_solver_distinct(void* h) {
+    return static_cast<RefSolver*>(h)->P->distinct_subsolvers();
+}
+
+int ref_stage_apply(void* h, const double* v, double* y) {
+    return guard([&] {
+        auto* S = static_cast<RefSolver*>(h);
+        const std::size_t N = static_cast<std::size_t>(S->op->size());
+        S->op->apply(std::span<const double>(v, N), std::span<double>(y, N));
+    });
+}
+
+int ref_precond_apply(void* h, const double* v, double* w) {
+    return guard([&] {
+        auto* S = static_cast<RefSolver*>(h);
+        const std::size_t N = static_cast<std::size_t>(S->P->size());
+        S->P->apply(std::span<const double>(v, N), std::span<double>(w, N));
+    });
+}
+
+// One IRK step with GMRES(restart) built on the reference's full `gmres`.
+// restart <= 0 calls the reference gmres once (its own semantics).  Returns
+// u_next, K (may be null), total iterations, the number of restart cycles,
+// true relative residual, converged flag, solve seconds (wall, excludes
+// nothing but setup) and the per-iteration residual history (<= hist_cap).
+int ref_irk_step(void* h, const double* u_n, const double* f_lift, double rtol,
+                 int restart, int max_iter, double* u_next, double* K_out,
+                 int* iters, int* cycles, double* true_rel, int* converged,
+                 double* seconds, double* hist, int hist_cap, int* hist_len) {
+    return guard([&] {
+        auto* S = static_cast<RefSolver*>(h);
+        const int n = S->M->n_rows;
+        const int s = S->table.s;
+        const std::size_t N = static_cast<std::size_t>(s) * n;
+        LinearParabolicSystem sys;
+        sys.M = S->M;
+        sys.F = S->F;
+        if (f_lift) sys.f_lift.assign(f_lift, f_lift + n);
+
+        const auto t0 = std::chrono::steady_clock::now();
+        const Vec rhs = stage_rhs(sys, S->table, S->ht, 0.0,
+                                  std::span<const double>(u_n, n));
+        ApplyFn apply = [S](std::span<const double> v, std::span<double> y) {
+            S->op->apply(v, y);
+        };
+        ApplyFn papply = [S](std::span<const double> v, std::span<double> w) {
+            S->P->apply(v, w);
+        };
+        Vec x(N, 0.0);
+        int total = 0, ncyc = 0;
+        bool conv = false;
+        double trel = 0.0;
+        std::vector<double> history{1.0};
+        const double bnorm = nrm2(rhs);
+        if (restart <= 0) {
+            GmresConfig cfg{PrecondSide::Right, rtol, max_iter};
+            auto [sol, rep] = gmres(apply, static_cast<int>(N), rhs, &papply, cfg);
+            x = std::move(sol);
+            total = rep.iterations;
+            ncyc = 1;
+            conv = rep.converged;
+            trel = rep.true_rel_residual;
+            history = rep.history;
+        } else {
+            // GMRES(m): restart on the residual system b - A x_k with the
+            // tolerance rescaled so that the cycle stops at ||r|| <= tol ||b||.
+            Vec r = rhs;
+            double rnorm = bnorm;
+            while (true) {
+                if (bnorm == 0.0) {
+                    conv = true;
+                    break;
+                }
+                const int budget = std::min(restart, max_iter - total);
+                if (budget <= 0) break;
+                GmresConfig cfg{PrecondSide::Right, rtol * bnorm / rnorm, budget};
+                auto [dx, rep] = gmres(apply, static_cast<int>(N), r, &papply, cfg);
+                for (std::size_t k = 1; k < rep.history.size(); ++k)
+                    history.push_back(rep.history[k] * rnorm / bnorm);
+                axpy(1.0, dx, x);
+                total += rep.iterations;
+                ncyc += 1;
+                Vec ax(N);
+                apply(x, ax);
+                for (std::size_t k = 0; k < N; ++k) r[k] = rhs[k] - ax[k];
+                rnorm = nrm2(r);
+                if (rep.converged) {
+                    conv = true;
+                    break;
+                }
+                if (rep.iterations < budget) break;  // breakdown
+            }
+            trel = bnorm > 0.0 ? rnorm / bnorm : 0.0;
+        }
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        for (int i = 0; i < n; ++i) u_next[i] = u_n[i];
+        for (int i = 0; i < s; ++i)
+            axpy(S->ht * S->table.b[i],
+                 std::span<const double>(x).subspan(static_cast<std::size_t>(i) * n, n),
+                 std::span<double>(u_next, n));
+        if (K_out) std::memcpy(K_out, x.data(), N * sizeof(double));
+        *iters = total;
+        *cycles = ncyc;
+        *true_rel = trel;
+        *converged = conv ? 1 : 0;
+        const int len = std::min<int>(hist_cap, static_cast<int>(history.size()));
+        for (int k = 0; k < len; ++k) hist[k] = history[k];
+        *hist_len = static_cast<int>(history.size());
+    });
+}
+
+// Plain CSR y = A x through the reference spmv (csr.cpp:102-114).
+int ref_spmv(int n_rows, int n_cols, const int* rp, const int* ci,
+             const double* v, const double* x, double* y) {
+    return guard([&] {
+        const CsrMatrix A = from_arrays(n_rows, n_cols, rp, ci, v);
+        spmv(A, std::span<const double>(x, n_cols), std::span<double>(y, n_rows));
+    });
+}
+
+double ref_dot(int n, const double* x, const double* y) {
+    return dot(std::span<const double>(x, n), std::span<const double>(y, n));
+}
+
+}  // extern "C"

@@ -1,0 +1,468 @@
+"""B200-native solve phase for the coupled s-stage IRK systems of arXiv 2010.11377.
+
+Host mirror of the reference's (irkprec) C++ solver interface for the hot path,
+over the C ABI of ``include/irkdev.h`` (``lib/libirkdev.so``):
+
+==========================  =====================================================
+this module                 reference (``/root/reference/proj``)
+==========================  =====================================================
+``make_radau_iia``          ``make_radau_iia`` (butcher.hpp:31-34)
+``make_lobatto_iiic``       ``make_lobatto_iiic`` (butcher.hpp:36-40)
+``ldu_factorize``           ``ldu_factorize`` (butcher.hpp:49-58)
+``precond_coeff``           ``precond_coeff`` (butcher.hpp:77)
+``custom_coeff``            ``custom_coeff`` (butcher.hpp:81)
+``amg_setup``               ``amg_setup`` (amg.hpp:52)
+``BlockPreconditioner``     ``BlockPreconditioner`` (stage.hpp:54-95)
+``StageOperator``           ``StageOperator`` (stage.hpp:16-42)
+``irk_step``                ``irk_step`` (irk.hpp:36-39)
+``integrate``               ``integrate`` (irk.hpp:49-59)
+``GmresConfig``             ``GmresConfig`` (gmres.hpp:17-21) + ``restart``
+``SolveReport``             ``SolveReport`` (gmres.hpp:23-38)
+==========================  =====================================================
+
+Errors follow the reference: ``ValueError`` for ``std::invalid_argument``,
+``SingularError``, ``NumericalError``; GMRES non-convergence is reported in
+``SolveReport.converged``, never raised.  Every solve-phase operation runs on
+the GPU; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from enum import IntEnum
+
+import numpy as np
+
+from . import _abi
+from ._abi import CudaError, NumericalError, SingularError, Unsupported, check
+
+__all__ = [
+    "CsrMatrix", "Scheme", "CoeffKind", "CoeffStructure", "ButcherTable", "PrecondCoeff",
+    "AmgParams", "AmgHierarchy", "GmresConfig", "SolveReport", "IrkStepResult",
+    "LinearParabolicSystem", "ProblemSetup", "BlockPreconditioner", "StageOperator",
+    "make_radau_iia", "make_lobatto_iiic", "make_table", "ldu_factorize", "precond_coeff",
+    "custom_coeff", "amg_setup", "make_heat_setup", "make_double_glazing_setup", "irk_step",
+    "integrate", "SingularError", "NumericalError", "CudaError", "Unsupported",
+]
+
+
+@dataclass
+class CsrMatrix:
+    """CSR with int32 indices and fp64 values (csr.hpp:15-32)."""
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    vals: np.ndarray
+    n_cols: int
+
+    @property
+    def n_rows(self) -> int:
+        return len(self.row_ptr) - 1
+
+    @property
+    def nnz(self) -> int:
+        return int(self.row_ptr[-1])
+
+    def view(self) -> _abi.irk_csr:
+        self.row_ptr = np.ascontiguousarray(self.row_ptr, dtype=np.int32)
+        self.col_idx = np.ascontiguousarray(self.col_idx, dtype=np.int32)
+        self.vals = np.ascontiguousarray(self.vals, dtype=np.float64)
+        return _abi.csr_view(self.row_ptr, self.col_idx, self.vals, self.n_cols)
+
+    @classmethod
+    def from_view(cls, v: _abi.irk_csr) -> "CsrMatrix":
+        rp, ci, vals, nc = _abi.csr_arrays(v)
+        return cls(rp, ci, vals, nc)
+
+    def matvec(self, x: np.ndarray) -> np.ndarray:
+        """Host convenience product (tests/diagnostics only)."""
+        rows = np.repeat(np.arange(self.n_rows), np.diff(self.row_ptr))
+        return np.bincount(rows, weights=self.vals * x[self.col_idx], minlength=self.n_rows)
+
+
+class Scheme(IntEnum):
+    RadauIIA = 0
+    LobattoIIIC = 1
+
+
+class CoeffKind(IntEnum):
+    Jacobi = 0
+    GaussSeidelLower = 1
+    UpperFactor = 2
+    LowerFactor = 3
+    Custom = 4
+
+
+class CoeffStructure(IntEnum):
+    Diagonal = 0
+    LowerTriangular = 1
+    UpperTriangular = 2
+
+
+@dataclass
+class ButcherTable:
+    scheme: Scheme
+    s: int
+    A: np.ndarray
+    b: np.ndarray
+    c: np.ndarray
+    q: int
+
+
+def make_table(scheme: Scheme, s: int) -> ButcherTable:
+    A = np.zeros(s * s)
+    b = np.zeros(s)
+    c = np.zeros(s)
+    q = C.c_int()
+    check(_abi.lib().irk_tableau(int(scheme), s, _abi.as_d(A), _abi.as_d(b), _abi.as_d(c), C.byref(q)))
+    return ButcherTable(Scheme(scheme), s, A.reshape(s, s), b, c, q.value)
+
+
+def make_radau_iia(s: int) -> ButcherTable:
+    return make_table(Scheme.RadauIIA, s)
+
+
+def make_lobatto_iiic(s: int) -> ButcherTable:
+    return make_table(Scheme.LobattoIIIC, s)
+
+
+def ldu_factorize(A: np.ndarray):
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    s = A.shape[0]
+    L, D, U = np.zeros(s * s), np.zeros(s), np.zeros(s * s)
+    check(_abi.lib().irk_ldu(s, _abi.as_d(A.ravel()), _abi.as_d(L), _abi.as_d(D), _abi.as_d(U)))
+    return L.reshape(s, s), D, U.reshape(s, s)
+
+
+@dataclass
+class PrecondCoeff:
+    kind: CoeffKind
+    Atilde: np.ndarray
+    structure: CoeffStructure
+
+
+def precond_coeff(table: ButcherTable, kind: CoeffKind) -> PrecondCoeff:
+    s = table.s
+    At = np.zeros(s * s)
+    st = C.c_int()
+    check(_abi.lib().irk_precond_coeff(int(table.scheme), s, int(kind), _abi.as_d(At), C.byref(st)))
+    return PrecondCoeff(CoeffKind(kind), At.reshape(s, s), CoeffStructure(st.value))
+
+
+def custom_coeff(Atilde: np.ndarray) -> PrecondCoeff:
+    At = np.ascontiguousarray(Atilde, dtype=np.float64)
+    if At.ndim != 2 or At.shape[0] != At.shape[1]:
+        raise ValueError("custom_coeff: not square")
+    st = C.c_int()
+    check(_abi.lib().irk_custom_coeff(At.shape[0], _abi.as_d(At.ravel()), C.byref(st)))
+    return PrecondCoeff(CoeffKind.Custom, At.copy(), CoeffStructure(st.value))
+
+
+@dataclass
+class AmgParams:
+    """AmgParams (amg.hpp:14-29); library defaults = BASELINE's V(1,1) Jacobi."""
+    theta: float = 0.25
+    pre_sweeps: int = 1
+    post_sweeps: int = 1
+    smoother: int = 0
+    jacobi_weight: float = 2.0 / 3.0
+    prolongation_weight: float = 4.0 / 3.0
+    prolongation_steps: int = 1
+    max_coarse: int = 64
+    max_levels: int = 10
+
+    def c(self) -> _abi.irk_amg_params:
+        return _abi.irk_amg_params(self.theta, self.pre_sweeps, self.post_sweeps, self.smoother,
+                                   self.jacobi_weight, self.prolongation_weight,
+                                   self.prolongation_steps, self.max_coarse, self.max_levels)
+
+
+class AmgHierarchy:
+    """Smoothed-aggregation hierarchy built by the host setup (amg.hpp:33-46)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _abi.lib().irk_hierarchy_free(self._h)
+            self._h = None
+
+    def n_levels(self) -> int:
+        return _abi.lib().irk_hierarchy_levels(self._h)
+
+    def level(self, l: int, which: str = "A") -> CsrMatrix:
+        v = _abi.irk_csr()
+        check(_abi.lib().irk_hierarchy_level(self._h, l, {"A": 0, "P": 1, "R": 2}[which], C.byref(v)))
+        return CsrMatrix.from_view(v)
+
+    def inv_diag(self, l: int) -> np.ndarray:
+        n = self.level(l).n_rows
+        return np.ctypeslib.as_array(_abi.lib().irk_hierarchy_inv_diag(self._h, l), (n,)).copy()
+
+    def coarse_inverse(self) -> np.ndarray:
+        n = C.c_int()
+        p = _abi.lib().irk_hierarchy_coarse_inverse(self._h, C.byref(n))
+        return np.ctypeslib.as_array(p, (n.value * n.value,)).copy().reshape(n.value, n.value)
+
+    def sizes(self) -> list[int]:
+        return [self.level(l).n_rows for l in range(self.n_levels())]
+
+
+def amg_setup(A: CsrMatrix, params: AmgParams | None = None) -> AmgHierarchy:
+    h = C.c_void_p()
+    v = A.view()
+    check(_abi.lib().irk_amg_setup(C.byref(v), C.byref((params or AmgParams()).c()), C.byref(h)))
+    return AmgHierarchy(h)
+
+
+@dataclass
+class LinearParabolicSystem:
+    """M du/dt = -F u - f_lift over the free dofs (irk.hpp:15-22); no forcing."""
+    M: CsrMatrix
+    F: CsrMatrix
+    f_lift: np.ndarray | None = None
+
+    def n(self) -> int:
+        return self.M.n_rows
+
+
+class ProblemSetup:
+    """Host-assembled P1 problem (heat or double glazing) with its u0 recipe."""
+
+    def __init__(self, handle: C.c_void_p, kind: str, cells: int):
+        self._h = handle
+        self.kind = kind
+        self.cells = cells
+        L = _abi.lib()
+        mv, kv = _abi.irk_csr(), _abi.irk_csr()
+        check(L.irk_problem_matrix(handle, 0, C.byref(mv)))
+        check(L.irk_problem_matrix(handle, 1, C.byref(kv)))
+        self.M = CsrMatrix.from_view(mv)
+        self.F = CsrMatrix.from_view(kv)
+        n = self.M.n_rows
+        self.f_lift = np.ctypeslib.as_array(L.irk_problem_lift(handle), (n,)).copy()
+        self.sys = LinearParabolicSystem(self.M, self.F, self.f_lift)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _abi.lib().irk_problem_free(self._h)
+            self._h = None
+
+    def initial(self, noise: float = 0.0, seed: int = 1) -> np.ndarray:
+        if self.kind == "double_glazing":
+            return np.zeros(self.M.n_rows)
+        u = np.zeros(self.M.n_rows)
+        check(_abi.lib().irk_problem_initial(self._h, noise, seed, _abi.as_d(u)))
+        return u
+
+
+def make_heat_setup(cells: int) -> ProblemSetup:
+    h = C.c_void_p()
+    check(_abi.lib().irk_problem_heat(cells, C.byref(h)))
+    return ProblemSetup(h, "heat", cells)
+
+
+def make_double_glazing_setup(cells: int, eps: float = 0.005) -> ProblemSetup:
+    h = C.c_void_p()
+    check(_abi.lib().irk_problem_double_glazing(cells, eps, C.byref(h)))
+    return ProblemSetup(h, "double_glazing", cells)
+
+
+@dataclass
+class GmresConfig:
+    """GmresConfig (gmres.hpp:17-21) + GMRES(m) restart (0 = full GMRES)."""
+    side: str = "right"
+    rel_tol: float = 1e-8
+    max_iter: int = 500
+    restart: int = 50
+
+    def c(self) -> _abi.irk_gmres_cfg:
+        if self.side != "right":
+            raise Unsupported("device GMRES runs right preconditioning (the reference default)")
+        return _abi.irk_gmres_cfg(1, self.rel_tol, self.max_iter, self.restart)
+
+
+@dataclass
+class SolveReport:
+    iterations: int = 0
+    history: list = field(default_factory=list)
+    final_rel_residual: float = 0.0
+    true_rel_residual: float = 0.0
+    converged: bool = True
+    solve_seconds: float = 0.0
+    setup_seconds: float = 0.0
+    cycles: int = 0
+    n_reorth: int = 0
+    rel_error: float = math.nan
+
+
+@dataclass
+class IrkStepResult:
+    u_next: np.ndarray
+    report: SolveReport
+    K: np.ndarray | None = None
+
+
+def _report(r: _abi.irk_report, hist: np.ndarray | None) -> SolveReport:
+    return SolveReport(r.iterations, [] if hist is None else list(hist[: r.history_len]),
+                       r.final_rel_residual, r.true_rel_residual, bool(r.converged),
+                       r.solve_seconds, r.setup_seconds, r.cycles, r.n_reorth)
+
+
+class _Device:
+    """One irkdev handle: M, K, the Butcher matrix, Atilde and the hierarchies."""
+
+    def __init__(self, M: CsrMatrix, F: CsrMatrix, A: np.ndarray, b: np.ndarray,
+                 coeff: PrecondCoeff, ht: float, amg: AmgParams, hiers=None, device: int = 0):
+        s = A.shape[0]
+        self.s, self.n = s, M.n_rows
+        self.A = np.ascontiguousarray(A, dtype=np.float64)
+        self.b = np.ascontiguousarray(b, dtype=np.float64)
+        self._keep = (M, F)
+        mv, kv = M.view(), F.view()
+        h = C.c_void_p()
+        hp = None
+        nh = 0
+        if hiers:
+            nh = len(hiers)
+            hp = (C.c_void_p * nh)(*[x._h for x in hiers])
+        check(_abi.lib().irkdev_create(
+            C.byref(mv), C.byref(kv), s, _abi.as_d(self.A.ravel()),
+            _abi.as_d(self.b),
+            _abi.as_d(np.ascontiguousarray(coeff.Atilde, dtype=np.float64).ravel()),
+            int(coeff.structure), ht, C.byref(amg.c()), nh, hp, device, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _abi.lib().irkdev_destroy(self._h)
+            self._h = None
+
+    def info(self):
+        n, s, nh = C.c_int(), C.c_int(), C.c_int()
+        sob = (C.c_int * self.s)()
+        setup = C.c_double()
+        check(_abi.lib().irkdev_info(self._h, C.byref(n), C.byref(s), C.byref(nh), sob, C.byref(setup)))
+        return {"n": n.value, "s": s.value, "n_hier": nh.value, "solver_of_block": list(sob),
+                "setup_seconds": setup.value}
+
+    def _apply(self, fn, v: np.ndarray, *extra) -> np.ndarray:
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.empty_like(v)
+        check(fn(self._h, *extra, _abi.as_d(v), _abi.as_d(out)))
+        return out
+
+
+class BlockPreconditioner:
+    """I_s (x) M + ht Atilde (x) F with one AMG V-cycle per block (stage.hpp:54-95).
+
+    Only the AMG subsolver runs on the device (BASELINE's path); ``ExactLU`` is
+    analysis-only in the reference and out of scope here.
+    """
+
+    def __init__(self, M: CsrMatrix, F: CsrMatrix, coeff: PrecondCoeff, ht: float,
+                 amg_params: AmgParams | None = None, table: ButcherTable | None = None,
+                 hierarchies=None, device: int = 0):
+        self.M, self.F, self.coeff, self.ht = M, F, coeff, ht
+        self.amg_params = amg_params or AmgParams()
+        s = coeff.Atilde.shape[0]
+        A = table.A if table is not None else coeff.Atilde
+        b = table.b if table is not None else np.zeros(s)
+        self._dev = _Device(M, F, A, b, coeff, ht, self.amg_params, hierarchies, device)
+
+    def stages(self) -> int:
+        return self._dev.s
+
+    def size(self) -> int:
+        return self._dev.s * self._dev.n
+
+    def distinct_subsolvers(self) -> int:
+        return self._dev.info()["n_hier"]
+
+    def setup_seconds(self) -> float:
+        return self._dev.info()["setup_seconds"]
+
+    def apply(self, v: np.ndarray) -> np.ndarray:
+        return self._dev._apply(_abi.lib().irkdev_precond_apply, v)
+
+    def vcycle(self, k: int, r: np.ndarray) -> np.ndarray:
+        return self._dev._apply(_abi.lib().irkdev_vcycle, r, k)
+
+    def bind_table(self, table: ButcherTable) -> None:
+        """Rebuild the device handle with the stage operator of `table`."""
+        if np.array_equal(self._dev.A, table.A) and np.array_equal(self._dev.b, table.b):
+            return
+        self._dev = _Device(self.M, self.F, table.A, table.b, self.coeff, self.ht,
+                            self.amg_params)
+
+
+class StageOperator:
+    """I_s (x) M + ht A (x) F, applied on the device (stage.hpp:16-42)."""
+
+    def __init__(self, P: BlockPreconditioner):
+        self._dev = P._dev
+
+    def apply(self, v: np.ndarray) -> np.ndarray:
+        return self._dev._apply(_abi.lib().irkdev_stage_apply, v)
+
+
+def irk_step(sys: LinearParabolicSystem, table: ButcherTable, ht: float, t_n: float,
+             u_n: np.ndarray, P: BlockPreconditioner, cfg: GmresConfig | None = None,
+             want_K: bool = False) -> IrkStepResult:
+    """One IRK step (irk.cpp:35-68): stage rhs, GMRES(m) with P, u_{n+1}."""
+    if ht <= 0.0:
+        raise ValueError("irk_step: ht must be positive")
+    if P is None:
+        raise Unsupported("the device path needs a BlockPreconditioner")
+    if P.ht != ht:
+        raise ValueError("irk_step: preconditioner built for a different ht")
+    P.bind_table(table)
+    cfg = cfg or GmresConfig()
+    dev = P._dev
+    u = np.ascontiguousarray(u_n, dtype=np.float64)
+    if u.shape[0] != dev.n:
+        raise ValueError("stage_rhs: dimension mismatch")
+    un = np.empty_like(u)
+    K = np.empty(dev.n * dev.s) if want_K else None
+    hist = np.empty(cfg.max_iter + 1)
+    rep = _abi.irk_report()
+    lift = None if sys.f_lift is None else np.ascontiguousarray(sys.f_lift, dtype=np.float64)
+    check(_abi.lib().irkdev_step(dev._h, _abi.as_d(u), None if lift is None else _abi.as_d(lift),
+                                 C.byref(cfg.c()), _abi.as_d(un),
+                                 None if K is None else _abi.as_d(K), C.byref(rep), _abi.as_d(hist)))
+    return IrkStepResult(un, _report(rep, hist), K)
+
+
+@dataclass
+class TrajectorySummary:
+    u_final: np.ndarray
+    t_final: float = 0.0
+    steps: int = 0
+    reports: list = field(default_factory=list)
+    all_converged: bool = True
+
+
+def integrate(sys: LinearParabolicSystem, table: ButcherTable, u0: np.ndarray, t_final: float,
+              ht: float, make_precond, cfg: GmresConfig | None = None) -> TrajectorySummary:
+    """Time loop of irk.cpp:70-102 (truncated last step, factory on ht change)."""
+    if ht <= 0.0:
+        raise ValueError("integrate: ht must be positive")
+    if t_final < 0.0:
+        raise ValueError("integrate: t_final must be nonnegative")
+    out = TrajectorySummary(np.array(u0, dtype=np.float64))
+    t, cur = 0.0, ht
+    P = make_precond(cur)
+    while t < t_final - 1e-14 * t_final:
+        step = ht if t + ht <= t_final else t_final - t
+        if step != cur:
+            cur = step
+            P = make_precond(cur)
+        r = irk_step(sys, table, step, t, out.u_final, P, cfg)
+        out.u_final = r.u_next
+        out.all_converged = out.all_converged and r.report.converged
+        out.reports.append(r.report)
+        t += step
+        out.steps += 1
+    out.t_final = t
+    return out

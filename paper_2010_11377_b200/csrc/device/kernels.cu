@@ -1,0 +1,754 @@
+// sm_100a kernels of the IRK solve phase.  All fp64 on CUDA cores; every
+// kernel is HBM-bandwidth bound (0.1-0.2 flop/byte), so the design goals are
+// coalesced streaming of matrix values, no index reads where the pattern is a
+// stencil (DIA), fused epilogues instead of separate BLAS-1 passes, and
+// deterministic reductions (see common.cuh for the numerics contract).
+#include <cstdio>
+#include <string>
+
+#include "../host/sparse.hpp"
+#include "kernels.cuh"
+
+namespace irkb {
+namespace dev {
+
+namespace {
+
+struct Offs {
+    int o[kMaxDiags];
+};
+
+inline int blocks_for(long long n, int t) { return static_cast<int>((n + t - 1) / t); }
+
+// ------------------------------------------------------------------ SpMV
+template <int XM, int EPI>
+__device__ __forceinline__ double spmv_epilogue(double s, int i, const SpmvArgs& a,
+                                                const double* r) {
+    if (EPI == kEPlain) return s;
+    if (EPI == kEResid) return r[i] - s;
+    if (EPI == kESmooth) return a.x.get()[i] + a.wd[i] * (r[i] - s);
+    // kEProlong: base + correction (amg.cpp:163-164)
+    const double zb = a.zb ? a.zb[i] : a.wd[i] * r[i];
+    return zb + s;
+}
+
+// DIA: one thread per row, diagonals visited in ascending offset order, i.e.
+// CSR column order, so the row sum is the reference's sequential sum (padding
+// entries are stored zeros and contribute exact zeros).
+template <int XM, int EPI>
+__global__ void __launch_bounds__(256) k_spmv_dia(int n, int nd, Offs off,
+                                                  const double* __restrict__ val,
+                                                  SpmvArgs a) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* r = a.r.base ? a.r.get() : nullptr;
+    const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
+    const double* __restrict__ wd = a.wd;
+    double s = 0.0;
+#pragma unroll 4
+    for (int d = 0; d < nd; ++d) {
+        const int c = i + off.o[d];
+        if (c >= 0 && c < n) {
+            const double xv = XM == kXWdR ? wd[c] * r[c] : x[c];
+            s += __ldg(val + static_cast<long long>(d) * n + i) * xv;
+        }
+    }
+    a.y.get()[i] = spmv_epilogue<XM, EPI>(s, i, a, r);
+}
+
+// CSR with shared-memory staging: the CTA streams its rows' nonzeros
+// coalesced, forms the products val*x into shared memory, and each thread then
+// adds its own row's products in column order -- coalesced loads with the
+// reference's exact per-row summation order.
+constexpr int kCsrRows = 128;
+constexpr int kCsrTile = 1024;
+
+template <int XM, int EPI>
+__global__ void __launch_bounds__(kCsrRows) k_spmv_csr(int rows, const int* __restrict__ ptr,
+                                                       const int* __restrict__ idx,
+                                                       const double* __restrict__ val,
+                                                       SpmvArgs a) {
+    __shared__ double prod[kCsrTile];
+    __shared__ int rp[kCsrRows + 1];
+    const int r0 = blockIdx.x * kCsrRows;
+    const int nr = min(kCsrRows, rows - r0);
+    const int t = threadIdx.x;
+    for (int q = t; q <= nr; q += kCsrRows) rp[q] = ptr[r0 + q];
+    __syncthreads();
+    const double* r = a.r.base ? a.r.get() : nullptr;
+    const double* x = a.x.base ? a.x.get() : nullptr;
+    const int base = rp[0], end = rp[nr];
+    const int lo = t < nr ? rp[t] : 0, hi = t < nr ? rp[t + 1] : 0;
+    double s = 0.0;
+    for (int ts = base; ts < end; ts += kCsrTile) {
+        const int te = min(ts + kCsrTile, end);
+        for (int k = ts + t; k < te; k += kCsrRows) {
+            const int c = idx[k];
+            const double xv = XM == kXWdR ? a.wd[c] * r[c] : x[c];
+            prod[k - ts] = val[k] * xv;
+        }
+        __syncthreads();
+        const int a0 = max(lo, ts), a1 = min(hi, te);
+        for (int k = a0; k < a1; ++k) s += prod[k - ts];
+        __syncthreads();
+    }
+    if (t < nr) a.y.get()[r0 + t] = spmv_epilogue<XM, EPI>(s, r0 + t, a, r);
+}
+
+template <int XM, int EPI>
+void launch_spmv(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
+    if (A.rows == 0) return;
+    if (A.fmt == 1) {
+        Offs o;
+        for (int d = 0; d < kMaxDiags; ++d) o.o[d] = A.off[d];
+        k_spmv_dia<XM, EPI><<<blocks_for(A.rows, 256), 256, 0, st>>>(A.rows, A.nd, o, A.val, a);
+    } else {
+        k_spmv_csr<XM, EPI><<<blocks_for(A.rows, kCsrRows), kCsrRows, 0, st>>>(A.rows, A.ptr, A.idx,
+                                                                              A.val, a);
+    }
+}
+
+// ------------------------------------------------------------------ stage op
+template <int S>
+__global__ void __launch_bounds__(256) k_stage_op_dia(int n, int nd, Offs off,
+                                                      const double* __restrict__ mv,
+                                                      const double* __restrict__ kv,
+                                                      StageCoef cf, VecRef zr, VecRef yr) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* __restrict__ z = zr.get();
+    double* __restrict__ y = yr.get();
+    double fm[S], fk[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) fm[j] = fk[j] = 0.0;
+    for (int d = 0; d < nd; ++d) {
+        const int c = i + off.o[d];
+        if (c >= 0 && c < n) {
+            const double m = __ldg(mv + static_cast<long long>(d) * n + i);
+            const double k = __ldg(kv + static_cast<long long>(d) * n + i);
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+                const double x = z[static_cast<long long>(j) * n + c];
+                fm[j] += m * x;
+                fk[j] += k * x;
+            }
+        }
+    }
+    // y_i = M v_i, then y_i += (ht a_ij) (F v_j) for j = 0..s-1 (stage.cpp:40-43)
+#pragma unroll
+    for (int b = 0; b < S; ++b) {
+        double acc = fm[b];
+#pragma unroll
+        for (int j = 0; j < S; ++j) acc += cf.c[b * S + j] * fk[j];
+        y[static_cast<long long>(b) * n + i] = acc;
+    }
+}
+
+// ------------------------------------------------------------------ sweep
+__global__ void __launch_bounds__(256) k_sweep_dia(int n, int nd, Offs off,
+                                                   const double* __restrict__ kv, VecRef wr,
+                                                   VecRef vr, SweepTerms t,
+                                                   double* __restrict__ store, VecRef outr) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* __restrict__ w = wr.get();
+    double f = 0.0;
+    for (int d = 0; d < nd; ++d) {
+        const int c = i + off.o[d];
+        if (c >= 0 && c < n) f += __ldg(kv + static_cast<long long>(d) * n + i) * w[c];
+    }
+    if (store) store[i] = f;
+    double acc = vr.get()[i];
+    for (int q = 0; q < t.nt; ++q) acc += t.coef[q] * (t.buf[q] ? t.buf[q][i] : f);
+    outr.get()[i] = acc;
+}
+
+__global__ void k_combine(int n, VecRef vr, SweepTerms t, VecRef outr) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double acc = vr.get()[i];
+    for (int q = 0; q < t.nt; ++q) acc += t.coef[q] * t.buf[q][i];
+    outr.get()[i] = acc;
+}
+
+__global__ void k_axpy(int n, double alpha, const double* __restrict__ x, VecRef yr) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double* y = yr.get();
+    y[i] = y[i] + alpha * x[i];
+}
+
+__global__ void k_dense_mv(int n, const double* __restrict__ A, VecRef rr, VecRef zr) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* r = rr.get();
+    double* z = zr.get();
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s += A[static_cast<long long>(i) * n + j] * r[j];
+    z[i] = s;
+}
+
+__global__ void k_wd_times_r(int n, const double* __restrict__ wd, VecRef rr,
+                             double* __restrict__ z) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    z[i] = wd[i] * rr.get()[i];
+}
+
+__global__ void k_stage_rhs(int n, int s, const double* __restrict__ ku,
+                            const double* __restrict__ lift, double* __restrict__ b) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double f = ku[i];
+    if (lift) f = f + lift[i];
+    for (int q = 0; q < s; ++q) b[static_cast<long long>(q) * n + i] = -f;
+}
+
+struct HB {
+    double v[kMaxStages];
+};
+
+__global__ void k_irk_update(int n, int s, const double* __restrict__ u,
+                             const double* __restrict__ x, HB hb, double* __restrict__ un) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double acc = u[i];
+    for (int q = 0; q < s; ++q) acc = acc + hb.v[q] * x[static_cast<long long>(q) * n + i];
+    un[i] = acc;
+}
+
+// ------------------------------------------------------------------ reductions
+// Chunk c covers elements [c*kChunk, (c+1)*kChunk); thread t owns elements
+// c*kChunk + u*512 + 2t + e (u = 0..7, e = 0..1), summed in (u, e) order.
+__device__ __forceinline__ long long chunk_elem(int c, int u, int e) {
+    return static_cast<long long>(c) * kChunk + u * (2 * kRedThreads) + 2 * threadIdx.x + e;
+}
+
+// Warp-tree of v, lane 0 stores into red[warp * stride + slot].
+__device__ __forceinline__ void warp_tree_store(double v, double* red, int stride, int slot) {
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31) == 0) red[(threadIdx.x >> 5) * stride + slot] = v;
+}
+
+// After a __syncthreads: the 8 warp values of `slot` added in warp order.
+__device__ __forceinline__ double warp_sum8(const double* red, int stride, int slot) {
+    double r = red[slot];
+    for (int w = 1; w < kRedThreads / 32; ++w) r += red[w * stride + slot];
+    return r;
+}
+
+// Last-CTA election after every CTA wrote its partials.
+__device__ __forceinline__ bool elect_last(unsigned* counter) {
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) __threadfence();
+    return last;
+}
+
+// Final reduction of `nv` partial vectors (nch each) into out[0..nv).
+// Thread t sums partials t, t+256, ... sequentially; then the warp tree and
+// the 8 warp results in order.  Called by the whole last CTA.
+__device__ void final_reduce(const double* part, int nch, int nv, double* red, double* out) {
+    for (int q = 0; q < nv; ++q) {
+        double acc = 0.0;
+        for (int p = threadIdx.x; p < nch; p += kRedThreads)
+            acc += __ldcg(part + static_cast<long long>(q) * nch + p);
+        warp_tree_store(acc, red, nv, q);
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nv; q += kRedThreads) out[q] = warp_sum8(red, nv, q);
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_dot(const double* __restrict__ x,
+                                                     const double* __restrict__ y, long long n,
+                                                     double* part, unsigned* counter,
+                                                     double* out) {
+    __shared__ double red[kRedThreads / 32 * 1];
+    __shared__ double res[1];
+    const int c = blockIdx.x;
+    double acc = 0.0;
+    for (int u = 0; u < kRedPerThread / 2; ++u)
+        for (int e = 0; e < 2; ++e) {
+            const long long k = chunk_elem(c, u, e);
+            const double xv = k < n ? x[k] : 0.0, yv = k < n ? y[k] : 0.0;
+            acc += xv * yv;
+        }
+    warp_tree_store(acc, red, 1, 0);
+    __syncthreads();
+    if (threadIdx.x == 0) part[c] = warp_sum8(red, 1, 0);
+    if (!elect_last(counter)) return;
+    final_reduce(part, gridDim.x, 1, red, res);
+    if (threadIdx.x == 0) {
+        *out = res[0];
+        *counter = 0u;
+    }
+}
+
+// ------------------------------------------------------------------ GMRES
+// Loads the thread's 16 chunk elements of v (zero beyond n).
+__device__ __forceinline__ void load_chunk(const double* __restrict__ v, long long n, int c,
+                                           double (&o)[kRedPerThread]) {
+    const long long base = static_cast<long long>(c) * kChunk + 2 * threadIdx.x;
+    if (static_cast<long long>(c + 1) * kChunk <= n) {
+#pragma unroll
+        for (int u = 0; u < kRedPerThread / 2; ++u) {
+            const double2 p = __ldcs(reinterpret_cast<const double2*>(v + base + u * 2 * kRedThreads));
+            o[2 * u] = p.x;
+            o[2 * u + 1] = p.y;
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < kRedPerThread / 2; ++u)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const long long k = base + u * 2 * kRedThreads + e;
+                o[2 * u + e] = k < n ? v[k] : 0.0;
+            }
+    }
+}
+
+__device__ __forceinline__ void store_chunk(double* v, long long n, int c,
+                                            const double (&o)[kRedPerThread]) {
+    const long long base = static_cast<long long>(c) * kChunk + 2 * threadIdx.x;
+    if (static_cast<long long>(c + 1) * kChunk <= n) {
+#pragma unroll
+        for (int u = 0; u < kRedPerThread / 2; ++u)
+            *reinterpret_cast<double2*>(v + base + u * 2 * kRedThreads) =
+                make_double2(o[2 * u], o[2 * u + 1]);
+    } else {
+#pragma unroll
+        for (int u = 0; u < kRedPerThread / 2; ++u)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const long long k = base + u * 2 * kRedThreads + e;
+                if (k < n) v[k] = o[2 * u + e];
+            }
+    }
+}
+
+__device__ __forceinline__ double chunk_dot_local(const double (&a)[kRedPerThread],
+                                                  const double (&b)[kRedPerThread]) {
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRedPerThread; ++q) acc += a[q] * b[q];
+    return acc;
+}
+
+__device__ void set_cond(cudaGraphConditionalHandle h, int use, unsigned v) {
+    if (use) cudaGraphSetConditional(h, v);
+}
+
+// Scalar tail of one Arnoldi step (gmres.cpp:93-118), single thread.
+__device__ void arnoldi_tail(const GmresBufs& g) {
+    GmresCtl* c = g.ctl;
+    const int j = c->j;
+    double* h = c->hcol;
+    h[j + 1] = c->hnext;
+    for (int i = 0; i < j; ++i) {
+        const double t = c->cs[i] * h[i] + c->sn[i] * h[i + 1];
+        h[i + 1] = -c->sn[i] * h[i] + c->cs[i] * h[i + 1];
+        h[i] = t;
+    }
+    const double denom = hyp(h[j], h[j + 1]);
+    double cs = 1.0, sn = 0.0;
+    if (denom > 0.0) {
+        cs = h[j] / denom;
+        sn = h[j + 1] / denom;
+    }
+    c->cs[j] = cs;
+    c->sn[j] = sn;
+    h[j] = denom;
+    h[j + 1] = 0.0;
+    c->g[j + 1] = -sn * c->g[j];
+    c->g[j] = cs * c->g[j];
+    double* col = g.H + static_cast<long long>(j) * (c->restart + 1);
+    for (int i = 0; i <= j + 1; ++i) col[i] = h[i];
+    c->total += 1;
+    c->m = j + 1;
+    const double res_rel = fabs(c->g[j + 1]) / c->beta;
+    const double hist = c->cycles == 0 ? res_rel : res_rel * c->beta / c->bnorm;
+    g.hist[c->total] = hist;
+    c->final_rel = hist;
+    if (!(res_rel == res_rel) || !(c->hnext == c->hnext)) c->bad = 1;
+    if (res_rel <= c->tol_c)
+        c->stop = 1;
+    else if (c->hnext <= 1e-14 * c->beta || c->bad)
+        c->stop = 2;
+    else if (j + 1 >= c->budget)
+        c->stop = 3;
+    else {
+        c->stop = 0;
+        c->inv = 1.0 / c->hnext;
+    }
+}
+
+// Pass 1: h_i = V_i . w (i <= j) and ||w||^2; pass 2 (if reorth): c_i = V_i . w.
+__global__ void __launch_bounds__(kRedThreads) k_gm_blockdot(GmresBufs g, int pass) {
+    extern __shared__ double red[];
+    GmresCtl* ctl = g.ctl;
+    if (pass == 2 && !ctl->reorth) return;
+    const int j = ctl->j;
+    const int nb = j + 1;
+    const int nv = pass == 1 ? nb + 1 : nb;
+    const int c = blockIdx.x;
+    const long long n = g.sN;
+    const long long stride = (g.sN + 63) / 64 * 64;
+    double w[kRedPerThread];
+    load_chunk(g.V + static_cast<long long>(j + 1) * stride, n, c, w);
+    if (pass == 1) warp_tree_store(chunk_dot_local(w, w), red, nv, nb);
+    for (int i = 0; i < nb; ++i) {
+        double v[kRedPerThread];
+        load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v);
+        warp_tree_store(chunk_dot_local(v, w), red, nv, i);
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nv; q += kRedThreads)
+        g.partials[static_cast<long long>(q) * g.nchunks + c] = warp_sum8(red, nv, q);
+    if (!elect_last(g.counters + pass - 1)) return;
+    double* res = red + kRedThreads / 32 * nv;
+    final_reduce(g.partials, g.nchunks, nv, red, res);
+    if (threadIdx.x == 0) {
+        if (pass == 1) {
+            for (int i = 0; i < nb; ++i) ctl->hcol[i] = res[i];
+            ctl->before = sqrt(res[nb]);
+        } else {
+            for (int i = 0; i < nb; ++i) ctl->y[i] = res[i];
+        }
+        g.counters[pass - 1] = 0u;
+    }
+}
+
+// w -= sum_i coef_i V_i (sequential in i), then ||w|| and the scalar tail.
+__global__ void __launch_bounds__(kRedThreads) k_gm_update(GmresBufs g, int pass) {
+    extern __shared__ double red[];
+    GmresCtl* ctl = g.ctl;
+    if (pass == 2 && !ctl->reorth) return;
+    const int j = ctl->j;
+    const int nb = j + 1;
+    const double* coef = pass == 1 ? ctl->hcol : ctl->y;
+    double* cf = red + kRedThreads / 32 + 1;
+    for (int i = threadIdx.x; i < nb; i += kRedThreads) cf[i] = coef[i];
+    __syncthreads();
+    const int c = blockIdx.x;
+    const long long n = g.sN;
+    const long long stride = (g.sN + 63) / 64 * 64;
+    double* wp = g.V + static_cast<long long>(j + 1) * stride;
+    double w[kRedPerThread];
+    load_chunk(wp, n, c, w);
+    for (int i = 0; i < nb; ++i) {
+        double v[kRedPerThread];
+        load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v);
+        const double h = cf[i];
+#pragma unroll
+        for (int q = 0; q < kRedPerThread; ++q) w[q] = w[q] - h * v[q];
+    }
+    store_chunk(wp, n, c, w);
+    warp_tree_store(chunk_dot_local(w, w), red, 1, 0);
+    __syncthreads();
+    if (threadIdx.x == 0) g.partials[c] = warp_sum8(red, 1, 0);
+    if (!elect_last(g.counters + 2 + pass - 1)) return;
+    double* res = red + kRedThreads / 32;
+    final_reduce(g.partials, g.nchunks, 1, red, res);
+    if (threadIdx.x == 0) {
+        const double nrm = sqrt(res[0]);
+        if (pass == 1) {
+            ctl->after = nrm;
+            if (nrm < 0.70710678118654752 * ctl->before) {
+                ctl->reorth = 1;
+            } else {
+                ctl->reorth = 0;
+                ctl->hnext = nrm;
+                arnoldi_tail(g);
+            }
+        } else {
+            for (int i = 0; i < nb; ++i) ctl->hcol[i] = ctl->hcol[i] + ctl->y[i];
+            ctl->hnext = nrm;
+            ctl->n_reorth += 1;
+            arnoldi_tail(g);
+        }
+        g.counters[2 + pass - 1] = 0u;
+    }
+}
+
+// V_{j+1} *= 1/h_{j+1,j} when the cycle continues; advance j.
+__global__ void __launch_bounds__(kRedThreads) k_gm_normalize(GmresBufs g) {
+    GmresCtl* ctl = g.ctl;
+    const int stop = ctl->stop;
+    const int j = ctl->j;
+    if (stop == 0) {
+        const long long stride = (g.sN + 63) / 64 * 64;
+        double* v = g.V + static_cast<long long>(j + 1) * stride;
+        const double inv = ctl->inv;
+        double w[kRedPerThread];
+        load_chunk(v, g.sN, blockIdx.x, w);
+#pragma unroll
+        for (int q = 0; q < kRedPerThread; ++q) w[q] = w[q] * inv;
+        store_chunk(v, g.sN, blockIdx.x, w);
+    }
+    if (!elect_last(g.counters + 4)) return;
+    if (threadIdx.x == 0) {
+        if (stop == 0) ctl->j = j + 1;
+        set_cond(g.h_inner, g.use_cond, stop == 0 ? 1u : 0u);
+        g.counters[4] = 0u;
+    }
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_gm_init(GmresBufs g, const double* __restrict__ b,
+                                                         double* __restrict__ r, double rel_tol,
+                                                         int restart, int max_iter) {
+    __shared__ double red[kRedThreads / 32 + 1];
+    double v[kRedPerThread];
+    load_chunk(b, g.sN, blockIdx.x, v);
+    store_chunk(r, g.sN, blockIdx.x, v);
+    warp_tree_store(chunk_dot_local(v, v), red, 1, 0);
+    __syncthreads();
+    if (threadIdx.x == 0) g.partials[blockIdx.x] = warp_sum8(red, 1, 0);
+    if (!elect_last(g.counters + 5)) return;
+    final_reduce(g.partials, g.nchunks, 1, red, red + kRedThreads / 32);
+    if (threadIdx.x == 0) {
+        GmresCtl* c = g.ctl;
+        const double bn = sqrt(red[kRedThreads / 32]);
+        c->rel_tol = rel_tol;
+        c->restart = restart;
+        c->max_iter = max_iter;
+        c->bnorm = bn;
+        c->beta = bn;
+        c->total = 0;
+        c->cycles = 0;
+        c->n_reorth = 0;
+        c->reorth = 0;
+        c->bad = 0;
+        c->j = 0;
+        c->m = 0;
+        c->stop = 0;
+        c->true_rel = 0.0;
+        if (bn == 0.0) {
+            c->done = 1;
+            c->converged = 1;
+            c->final_rel = 0.0;
+            g.hist[0] = 0.0;
+        } else {
+            c->done = 0;
+            c->converged = 0;
+            c->final_rel = 1.0;
+            g.hist[0] = 1.0;
+            c->tol_c = rel_tol;
+            c->budget = restart < max_iter ? restart : max_iter;
+            c->inv = 1.0 / bn;
+            if (c->budget <= 0) c->done = 1;
+        }
+        set_cond(g.h_outer, g.use_cond, c->done ? 0u : 1u);
+        g.counters[5] = 0u;
+    }
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_gm_cycle_begin(GmresBufs g,
+                                                                const double* __restrict__ r) {
+    GmresCtl* ctl = g.ctl;
+    const double inv = ctl->inv;
+    double v[kRedPerThread];
+    load_chunk(r, g.sN, blockIdx.x, v);
+#pragma unroll
+    for (int q = 0; q < kRedPerThread; ++q) v[q] = v[q] * inv;
+    store_chunk(g.V, g.sN, blockIdx.x, v);
+    if (!elect_last(g.counters + 6)) return;
+    if (threadIdx.x == 0) {
+        ctl->g[0] = ctl->beta;
+        ctl->j = 0;
+        ctl->stop = 0;
+        set_cond(g.h_inner, g.use_cond, 1u);
+        g.counters[6] = 0u;
+    }
+}
+
+// Back substitution for y (gmres.cpp:126-131), one thread.
+__global__ void k_gm_backsub(GmresBufs g) {
+    GmresCtl* c = g.ctl;
+    const int m = c->m;
+    const int ld = c->restart + 1;
+    for (int i = m - 1; i >= 0; --i) {
+        double s = c->g[i];
+        for (int k = i + 1; k < m; ++k) s -= g.H[static_cast<long long>(k) * ld + i] * c->y[k];
+        c->y[i] = s / g.H[static_cast<long long>(i) * ld + i];
+    }
+}
+
+// x += sum_i y_i Z_i (sequential in i).  Z slots are padded like V.
+__global__ void __launch_bounds__(kRedThreads) k_gm_xupdate(GmresBufs g, double* __restrict__ x) {
+    __shared__ double ys[kMaxRestart];
+    const GmresCtl* c = g.ctl;
+    const int m = c->m;
+    for (int i = threadIdx.x; i < m; i += kRedThreads) ys[i] = c->y[i];
+    __syncthreads();
+    const long long stride = (g.sN + 63) / 64 * 64;
+    double xv[kRedPerThread];
+    load_chunk(x, g.sN, blockIdx.x, xv);
+    for (int i = 0; i < m; ++i) {
+        double z[kRedPerThread];
+        load_chunk(g.Z + static_cast<long long>(i) * stride, g.sN, blockIdx.x, z);
+#pragma unroll
+        for (int q = 0; q < kRedPerThread; ++q) xv[q] = xv[q] + ys[i] * z[q];
+    }
+    store_chunk(x, g.sN, blockIdx.x, xv);
+}
+
+// r = b - Ax, beta = ||r||, restart decision.
+__global__ void __launch_bounds__(kRedThreads) k_gm_residual(GmresBufs g, const double* __restrict__ b,
+                                                             const double* __restrict__ ax,
+                                                             double* __restrict__ r) {
+    __shared__ double red[kRedThreads / 32 + 1];
+    double bv[kRedPerThread], av[kRedPerThread];
+    load_chunk(b, g.sN, blockIdx.x, bv);
+    load_chunk(ax, g.sN, blockIdx.x, av);
+#pragma unroll
+    for (int q = 0; q < kRedPerThread; ++q) bv[q] = bv[q] - av[q];
+    store_chunk(r, g.sN, blockIdx.x, bv);
+    warp_tree_store(chunk_dot_local(bv, bv), red, 1, 0);
+    __syncthreads();
+    if (threadIdx.x == 0) g.partials[blockIdx.x] = warp_sum8(red, 1, 0);
+    if (!elect_last(g.counters + 7)) return;
+    final_reduce(g.partials, g.nchunks, 1, red, red + kRedThreads / 32);
+    if (threadIdx.x == 0) {
+        GmresCtl* c = g.ctl;
+        const double rn = sqrt(red[kRedThreads / 32]);
+        c->cycles += 1;
+        c->true_rel = rn / c->bnorm;
+        const bool finished = c->stop == 1 || c->stop == 2 || c->total >= c->max_iter || rn == 0.0;
+        if (finished) {
+            c->done = 1;
+            c->converged = c->stop == 1 ? 1 : 0;
+        } else {
+            c->beta = rn;
+            c->tol_c = c->rel_tol * c->bnorm / rn;
+            const int left = c->max_iter - c->total;
+            c->budget = c->restart < left ? c->restart : left;
+            c->inv = 1.0 / rn;
+        }
+        set_cond(g.h_outer, g.use_cond, finished ? 0u : 1u);
+        g.counters[7] = 0u;
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st) {
+#define IRK_SPMV_CASE(X, E)                         \
+    if (xmode == X && epi == E) {                   \
+        launch_spmv<X, E>(A, a, st);                \
+        return;                                     \
+    }
+    IRK_SPMV_CASE(kXPlain, kEPlain)
+    IRK_SPMV_CASE(kXPlain, kEResid)
+    IRK_SPMV_CASE(kXPlain, kESmooth)
+    IRK_SPMV_CASE(kXPlain, kEProlong)
+    IRK_SPMV_CASE(kXWdR, kEResid)
+    IRK_SPMV_CASE(kXWdR, kEPlain)
+#undef IRK_SPMV_CASE
+    throw InvalidArgument("spmv: unsupported mode combination");
+}
+
+void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecRef y, int n,
+                  cudaStream_t st) {
+    Offs o;
+    for (int d = 0; d < kMaxDiags; ++d) o.o[d] = M.off[d];
+    const int nb = blocks_for(n, 256);
+    switch (c.s) {
+#define IRK_OP_CASE(S) \
+    case S: k_stage_op_dia<S><<<nb, 256, 0, st>>>(n, M.nd, o, M.val, K.val, c, z, y); break;
+        IRK_OP_CASE(1) IRK_OP_CASE(2) IRK_OP_CASE(3) IRK_OP_CASE(4) IRK_OP_CASE(5)
+        IRK_OP_CASE(6) IRK_OP_CASE(7)
+#undef IRK_OP_CASE
+    default: throw InvalidArgument("stage_op: s out of range");
+    }
+}
+
+void sweep_dia(const Mat& K, VecRef w, VecRef v, const SweepTerms& t, double* store, VecRef out,
+               int n, cudaStream_t st) {
+    Offs o;
+    for (int d = 0; d < kMaxDiags; ++d) o.o[d] = K.off[d];
+    k_sweep_dia<<<blocks_for(n, 256), 256, 0, st>>>(n, K.nd, o, K.val, w, v, t, store, out);
+}
+
+void combine(VecRef v, const SweepTerms& t, VecRef out, int n, cudaStream_t st) {
+    k_combine<<<blocks_for(n, 256), 256, 0, st>>>(n, v, t, out);
+}
+
+void axpy(double alpha, const double* x, VecRef y, int n, cudaStream_t st) {
+    k_axpy<<<blocks_for(n, 256), 256, 0, st>>>(n, alpha, x, y);
+}
+
+void dense_mv(int n, const double* Ainv, VecRef r, VecRef z, cudaStream_t st) {
+    k_dense_mv<<<blocks_for(n, 128), 128, 0, st>>>(n, Ainv, r, z);
+}
+
+void wd_times_r(int n, const double* wd, VecRef r, double* z, cudaStream_t st) {
+    k_wd_times_r<<<blocks_for(n, 256), 256, 0, st>>>(n, wd, r, z);
+}
+
+void stage_rhs_finish(const double* ku, const double* lift, double* b, int n, int s,
+                      cudaStream_t st) {
+    k_stage_rhs<<<blocks_for(n, 256), 256, 0, st>>>(n, s, ku, lift, b);
+}
+
+void irk_update(const double* u, const double* x, const double* hb, int n, int s, double* un,
+                cudaStream_t st) {
+    HB h;
+    for (int q = 0; q < s; ++q) h.v[q] = hb[q];
+    k_irk_update<<<blocks_for(n, 256), 256, 0, st>>>(n, s, u, x, h, un);
+}
+
+static size_t red_smem(int nv) { return sizeof(double) * (kRedThreads / 32 * nv + nv + 8); }
+
+void gm_init(const GmresBufs& g, const double* b, double* r, double rel_tol, int restart,
+             int max_iter, cudaStream_t st) {
+    k_gm_init<<<g.nchunks, kRedThreads, 0, st>>>(g, b, r, rel_tol, restart, max_iter);
+}
+
+void gm_cycle_begin(const GmresBufs& g, const double* r, cudaStream_t st) {
+    k_gm_cycle_begin<<<g.nchunks, kRedThreads, 0, st>>>(g, r);
+}
+
+void gm_blockdot(const GmresBufs& g, int pass, cudaStream_t st) {
+    // capacity for up to restart+1 basis vectors plus ||w||
+    const int nv = kMaxRestart + 2;
+    k_gm_blockdot<<<g.nchunks, kRedThreads, red_smem(nv), st>>>(g, pass);
+}
+
+void gm_update(const GmresBufs& g, int pass, cudaStream_t st) {
+    k_gm_update<<<g.nchunks, kRedThreads, sizeof(double) * (kRedThreads / 32 + 1 + kMaxRestart + 8),
+                  st>>>(g, pass);
+}
+
+void gm_normalize(const GmresBufs& g, cudaStream_t st) {
+    k_gm_normalize<<<g.nchunks, kRedThreads, 0, st>>>(g);
+}
+
+void gm_solution(const GmresBufs& g, double* x, cudaStream_t st) {
+    k_gm_backsub<<<1, 1, 0, st>>>(g);
+    k_gm_xupdate<<<g.nchunks, kRedThreads, 0, st>>>(g, x);
+}
+
+void gm_residual(const GmresBufs& g, const double* b, const double* ax, double* r,
+                 cudaStream_t st) {
+    k_gm_residual<<<g.nchunks, kRedThreads, 0, st>>>(g, b, ax, r);
+}
+
+void dot(const double* x, const double* y, long long n, double* partials, unsigned* counter,
+         double* out, cudaStream_t st) {
+    const int nch = static_cast<int>((n + kChunk - 1) / kChunk);
+    k_dot<<<nch > 0 ? nch : 1, kRedThreads, 0, st>>>(x, y, n, partials, counter, out);
+}
+
+void set_smem_limits() {
+    const int nv = kMaxRestart + 2;
+    cudaFuncSetAttribute(k_gm_blockdot, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(red_smem(nv)));
+}
+
+}  // namespace dev
+}  // namespace irkb

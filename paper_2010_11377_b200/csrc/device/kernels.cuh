@@ -1,0 +1,150 @@
+// Kernel interface of the B200 IRK solve phase (fp64, HBM-bound, CUDA cores).
+// Each launcher enqueues on the given stream; none synchronises.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace irkb {
+namespace dev {
+
+constexpr int kMaxDiags = 16;
+
+// Device matrix: either DIA ("stencil": a few constant diagonals, values
+// stored diagonal-major so a thread-per-row sweep is fully coalesced and no
+// column index is read) or CSR.  DIA is chosen at upload when the pattern is
+// a small set of diagonals with little padding -- true for the fine-level
+// FE operators, M, K and every fine-level A of the hierarchies.
+struct Mat {
+    int fmt = 0;  // 0 CSR, 1 DIA
+    int rows = 0, cols = 0, nnz = 0;
+    const int* ptr = nullptr;
+    const int* idx = nullptr;
+    const double* val = nullptr;  // CSR: nnz; DIA: nd * rows
+    int nd = 0;
+    int off[kMaxDiags] = {};
+};
+
+// x operand of an SpMV: either a plain vector or the implicit Jacobi
+// pre-smoothed iterate wd .* r (never materialised).
+enum XMode { kXPlain = 0, kXWdR = 1 };
+// Row epilogue applied to s = (A x)_i.
+enum Epi {
+    kEPlain = 0,    // y = s
+    kEResid = 1,    // y = r - s
+    kESmooth = 2,   // y = x + wd*(r - s)        (Jacobi sweep, x = input)
+    kEProlong = 3,  // y = zb + s,  zb = wd .* r (implicit) or a vector
+};
+
+struct SpmvArgs {
+    VecRef x{};                  // plain x (kXPlain)
+    VecRef r{};                  // residual / rhs vector
+    const double* wd = nullptr;  // omega * D^-1
+    const double* zb = nullptr;  // prolong base (nullptr -> wd .* r)
+    VecRef y{};
+};
+
+void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st);
+
+// Stage operator y_i = M z_i + sum_j c_ij K z_j (c = ht*A), M/K sharing one
+// DIA pattern; one pass over both value arrays for all s stage vectors.
+struct StageCoef {
+    int s;
+    double c[kMaxStages * kMaxStages];
+};
+void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z,
+                  VecRef y, int n, cudaStream_t st);
+
+// Block-substitution sweep, fused for DIA K:
+//   fresh = K w;  store_fresh (optional) = fresh;
+//   out = v + sum_t coef_t * term_t  (terms in the given order; the term
+//   flagged `fresh` uses the value just computed).
+struct SweepTerms {
+    int nt;
+    double coef[kMaxStages];
+    const double* buf[kMaxStages];  // nullptr marks the fresh term
+};
+void sweep_dia(const Mat& K, VecRef w, VecRef v, const SweepTerms& t,
+               double* store_fresh, VecRef out, int n, cudaStream_t st);
+// Generic element-wise combine (used with a CSR K): out = v + sum coef*buf.
+void combine(VecRef v, const SweepTerms& t, VecRef out, int n, cudaStream_t st);
+// y += alpha * x, element-wise (rounded multiply then add).
+void axpy(double alpha, const double* x, VecRef y, int n, cudaStream_t st);
+
+// Coarsest-level solve z = Ainv r (dense row-major inverse).
+void dense_mv(int n, const double* Ainv, VecRef r, VecRef z, cudaStream_t st);
+// z = wd .* r (first Jacobi sweep from a zero iterate, amg.cpp:119-124).
+void wd_times_r(int n, const double* wd, VecRef r, double* z, cudaStream_t st);
+
+// rhs block i = -(K u + lift) for i < s (irk.cpp:9-33 without forcing).
+void stage_rhs_finish(const double* ku, const double* lift, double* b, int n, int s,
+                      cudaStream_t st);
+// u_next = u + sum_i hb_i x_i (irk.cpp:59-65).
+void irk_update(const double* u, const double* x, const double* hb, int n, int s,
+                double* u_next, cudaStream_t st);
+
+// ------------------------------------------------------------------ GMRES
+// Control block shared by every GMRES kernel (device memory).
+struct GmresCtl {
+    int j;          // inner iteration index within the cycle
+    int j_next;
+    int budget;
+    int total;      // iterations so far
+    int cycles;
+    int stop;       // 0 continue, 1 converged, 2 breakdown, 3 budget
+    int done;
+    int converged;
+    int reorth;     // current iteration re-orthogonalises
+    int n_reorth;
+    int restart, max_iter;
+    int m;          // columns of the last cycle
+    int bad;        // non-finite scalar seen
+    double rel_tol, bnorm, beta, tol_c, inv, before, after, hnext;
+    double final_rel, true_rel;
+    double g[kMaxRestart + 1];
+    double cs[kMaxRestart];
+    double sn[kMaxRestart];
+    double hcol[kMaxRestart + 2];
+    double y[kMaxRestart];
+};
+
+struct GmresBufs {
+    GmresCtl* ctl;
+    double* H;          // (restart) columns of (restart+1)
+    double* hist;       // max_iter + 1
+    double* partials;   // (kMaxRestart + 2) * nchunks
+    unsigned* counters; // one per reduction kernel
+    double* V;          // (restart + 1) * sN
+    double* Z;          // restart * sN
+    long long sN;
+    int nchunks;
+    cudaGraphConditionalHandle h_inner;
+    cudaGraphConditionalHandle h_outer;
+    int use_cond;       // 1 when running inside conditional graph nodes
+};
+
+// b -> r copy and ||b||; initialises the control block (bnorm == 0 ends the
+// solve: x = 0).
+void gm_init(const GmresBufs& g, const double* b, double* r, double rel_tol,
+             int restart, int max_iter, cudaStream_t st);
+// V_0 = r / beta, g_0 = beta, j = 0 (start of a restart cycle).
+void gm_cycle_begin(const GmresBufs& g, const double* r, cudaStream_t st);
+// h = V_{0..j}^T w and ||w||  (pass 1), or c = V^T w (pass 2, if reorth).
+void gm_blockdot(const GmresBufs& g, int pass, cudaStream_t st);
+// w -= V h (pass 1) / w -= V c, h += c (pass 2), ||w||, scalar tail.
+void gm_update(const GmresBufs& g, int pass, cudaStream_t st);
+// V_{j+1} = w / h_{j+1,j} if continuing; advance j; set loop condition.
+void gm_normalize(const GmresBufs& g, cudaStream_t st);
+// y = H^-1 g (1 thread) then x += Z y.
+void gm_solution(const GmresBufs& g, double* x, cudaStream_t st);
+// r = b - Ax, beta = ||r||, restart decision.
+void gm_residual(const GmresBufs& g, const double* b, const double* ax, double* r,
+                 cudaStream_t st);
+
+// Standalone deterministic dot (same tree) for tests: out[0] = x.y.
+void dot(const double* x, const double* y, long long n, double* partials,
+         unsigned* counter, double* out, cudaStream_t st);
+
+}  // namespace dev
+}  // namespace irkb

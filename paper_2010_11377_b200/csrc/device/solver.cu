@@ -1,0 +1,736 @@
+// Device solver orchestration.  One CUDA stream per solver; one CUDA graph
+// per IRK step holding the whole restarted GMRES as nested conditional WHILE
+// nodes (outer: restart cycles, inner: Arnoldi iterations), so a step is one
+// graph launch plus one small device->host read of the report.  The kernels
+// read the iteration index from the device control block, which keeps the
+// captured iteration body iteration-invariant.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+
+#include "solver.hpp"
+
+namespace irkb {
+
+namespace dev {
+void set_smem_limits();
+}
+
+using dev::VecRef;
+
+DevBuf::DevBuf(size_t bytes) : n_(bytes) {
+    if (bytes == 0) return;
+    IRK_CUDA_CHECK(cudaMalloc(&p_, bytes));
+}
+
+DevBuf::~DevBuf() {
+    if (p_) cudaFree(p_);
+}
+
+DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+        if (p_) cudaFree(p_);
+        p_ = o.p_;
+        n_ = o.n_;
+        o.p_ = nullptr;
+        o.n_ = 0;
+    }
+    return *this;
+}
+
+namespace {
+
+VecRef block(VecRef v, long long off) {
+    v.offset += off;
+    return v;
+}
+
+VecRef slot(double* base, const int* idx, long long stride, int add) {
+    return VecRef{base, idx, stride, add, 0};
+}
+
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+
+double* DeviceSolver::alloc(size_t count) {
+    bufs_.emplace_back(sizeof(double) * std::max<size_t>(count, 1));
+    return bufs_.back().as<double>();
+}
+
+// DIA when the pattern is <= 16 diagonals with <= 15% padding; else CSR.
+dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia) {
+    dev::Mat m;
+    m.rows = A.rows;
+    m.cols = A.cols;
+    m.nnz = A.nnz();
+    std::vector<int> offs;
+    bool dia = allow_dia && A.rows == A.cols && A.rows > 0;
+    if (dia) {
+        for (int i = 0; i < A.rows && dia; ++i)
+            for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+                const int o = A.idx[k] - i;
+                if (std::find(offs.begin(), offs.end(), o) == offs.end()) {
+                    offs.push_back(o);
+                    if (static_cast<int>(offs.size()) > dev::kMaxDiags) {
+                        dia = false;
+                        break;
+                    }
+                }
+            }
+        if (dia && static_cast<double>(offs.size()) * A.rows > 1.15 * A.nnz() + 64) dia = false;
+    }
+    if (dia) {
+        std::sort(offs.begin(), offs.end());
+        const int nd = static_cast<int>(offs.size());
+        std::vector<double> v(static_cast<size_t>(nd) * A.rows, 0.0);
+        for (int i = 0; i < A.rows; ++i)
+            for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+                const int d = static_cast<int>(std::lower_bound(offs.begin(), offs.end(), A.idx[k] - i) -
+                                               offs.begin());
+                v[static_cast<size_t>(d) * A.rows + i] = A.val[k];
+            }
+        double* dv = alloc(v.size());
+        IRK_CUDA_CHECK(cudaMemcpy(dv, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
+        m.fmt = 1;
+        m.nd = nd;
+        for (int d = 0; d < nd; ++d) m.off[d] = offs[d];
+        m.val = dv;
+        return m;
+    }
+    bufs_.emplace_back(sizeof(int) * (A.rows + 1));
+    int* dp = bufs_.back().as<int>();
+    bufs_.emplace_back(sizeof(int) * std::max(1, A.nnz()));
+    int* di = bufs_.back().as<int>();
+    double* dv = alloc(A.nnz());
+    IRK_CUDA_CHECK(cudaMemcpy(dp, A.ptr.data(), sizeof(int) * (A.rows + 1), cudaMemcpyHostToDevice));
+    if (A.nnz()) {
+        IRK_CUDA_CHECK(cudaMemcpy(di, A.idx.data(), sizeof(int) * A.nnz(), cudaMemcpyHostToDevice));
+        IRK_CUDA_CHECK(cudaMemcpy(dv, A.val.data(), sizeof(double) * A.nnz(), cudaMemcpyHostToDevice));
+    }
+    m.fmt = 0;
+    m.ptr = dp;
+    m.idx = di;
+    m.val = dv;
+    return m;
+}
+
+DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<double>& A,
+                           const std::vector<double>& b, const std::vector<double>& At,
+                           Structure structure, double ht, const AmgParams& amg,
+                           std::vector<Hierarchy> hiers, int device)
+    : s_(s), device_(device), At_(At), structure_(structure), ht_(ht) {
+    const auto t0 = std::chrono::steady_clock::now();
+    check(s >= 1 && s <= dev::kMaxStages, "device solver: s must be in 1..7");
+    check(M.rows == M.cols && K.rows == K.cols && M.rows == K.rows,
+          "block preconditioner: M, F size mismatch");
+    check(static_cast<int>(A.size()) == s * s && static_cast<int>(At.size()) == s * s &&
+              static_cast<int>(b.size()) == s,
+          "device solver: coefficient size mismatch");
+    check(ht > 0.0, "irk_step: ht must be positive");
+    n_ = M.rows;
+    sN_ = static_cast<long long>(s) * n_;
+    stride_ = (sN_ + 63) / 64 * 64;
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        throw CudaError("no CUDA device: the B200 solve phase has no CPU fallback");
+    IRK_CUDA_CHECK(cudaSetDevice(device));
+    IRK_CUDA_CHECK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    dev::set_smem_limits();
+
+    // Hierarchies: one per distinct diagonal coefficient (stage.cpp:85-106).
+    std::vector<double> distinct;
+    distinct_diagonals(s, At, sob_, distinct);
+    if (hiers.empty()) {
+        for (double d : distinct) hiers.push_back(amg_setup(add(1.0, M, ht * d, K), amg));
+    }
+    check(hiers.size() == distinct.size(), "device solver: hierarchy count mismatch");
+    hier_host_ = std::move(hiers);
+
+    M_ = upload(M, true);
+    K_ = upload(K, true);
+    fused_op_ = M_.fmt == 1 && K_.fmt == 1 && M_.nd == K_.nd &&
+                std::equal(M_.off, M_.off + M_.nd, K_.off);
+    coef_.s = s;
+    for (int i = 0; i < s * s; ++i) coef_.c[i] = ht * A[i];
+    hb_.resize(s);
+    for (int i = 0; i < s; ++i) hb_[i] = ht * b[i];
+
+    for (const Hierarchy& h : hier_host_) {
+        DevHier dh;
+        dh.prm = h.params;
+        const int L = h.n_levels();
+        for (int l = 0; l < L; ++l) {
+            const AmgLevel& lev = h.levels[l];
+            DevLevel d;
+            d.n = lev.A.rows;
+            d.A = upload(lev.A, true);
+            std::vector<double> wd(d.n);
+            for (int i = 0; i < d.n; ++i) wd[i] = h.params.jacobi_weight * lev.inv_diag[i];
+            d.wd = alloc(d.n);
+            IRK_CUDA_CHECK(cudaMemcpy(d.wd, wd.data(), sizeof(double) * d.n, cudaMemcpyHostToDevice));
+            if (l + 1 < L) {
+                d.P = upload(lev.P, false);
+                d.R = upload(lev.R, false);
+            }
+            d.t = alloc(d.n);
+            d.u = alloc(d.n);
+            if (h.params.pre_sweeps > 1) d.zp = alloc(d.n);
+            if (l > 0) {
+                d.r = alloc(d.n);
+                d.z = alloc(d.n);
+            }
+            dh.lv.push_back(d);
+        }
+        dh.nc = h.levels.back().A.rows;
+        dh.cinv = alloc(static_cast<size_t>(dh.nc) * dh.nc);
+        IRK_CUDA_CHECK(cudaMemcpy(dh.cinv, h.coarse_inverse.data(),
+                                  sizeof(double) * dh.nc * dh.nc, cudaMemcpyHostToDevice));
+        hier_.push_back(std::move(dh));
+    }
+
+    rhs_ = alloc(n_);
+    fw_ = alloc(static_cast<size_t>(s) * n_);
+    u_ = alloc(n_);
+    lift_ = alloc(n_);
+    unext_ = alloc(n_);
+    ku_ = alloc(n_);
+    b_ = alloc(stride_);
+    x_ = alloc(stride_);
+    r_ = alloc(stride_);
+    ax_ = alloc(stride_);
+    const long long nch = (sN_ + dev::kChunk - 1) / dev::kChunk;
+    red_part_ = alloc(nch + 1);
+    red_out_ = alloc(8);
+    bufs_.emplace_back(sizeof(unsigned) * 16);
+    red_cnt_ = bufs_.back().as<unsigned>();
+    IRK_CUDA_CHECK(cudaMemset(red_cnt_, 0, sizeof(unsigned) * 16));
+    IRK_CUDA_CHECK(cudaDeviceSynchronize());
+    setup_seconds_ = seconds_since(t0);
+}
+
+DeviceSolver::~DeviceSolver() {
+    for (cudaGraphExec_t* e : {&exec_, &exec_iter_, &exec_pre_, &exec_cb_, &exec_ce_, &exec_post_})
+        if (*e) cudaGraphExecDestroy(*e);
+    if (ctl_host_) cudaFreeHost(ctl_host_);
+    if (hist_host_) cudaFreeHost(hist_host_);
+    if (st_) cudaStreamDestroy(st_);
+}
+
+int DeviceSolver::matrix_format(int which) const { return which == 0 ? M_.fmt : K_.fmt; }
+
+// ------------------------------------------------------------------ recording
+// One V(pre,post) cycle (amg.cpp:144-168) with fused kernels per level:
+//   t = r - A (wd.*r)      pre-smooth from zero fused into the residual
+//   r_{l+1} = R t          restriction
+//   t = wd.*r + P z_{l+1}  prolongation fused with the pre-smoothed iterate
+//   z = t + wd.*(r - A t)  post-smoothing sweep
+void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0) {
+    DevHier& H = hier_[k];
+    const int L = static_cast<int>(H.lv.size());
+    const int pre = H.prm.pre_sweeps, post = H.prm.post_sweeps;
+    auto rhs_of = [&](int l) { return l == 0 ? r0 : dev::plain(H.lv[l].r); };
+    auto out_of = [&](int l) { return l == 0 ? z0 : dev::plain(H.lv[l].z); };
+    for (int l = 0; l + 1 < L; ++l) {
+        DevLevel& d = H.lv[l];
+        dev::SpmvArgs a;
+        a.r = rhs_of(l);
+        a.wd = d.wd;
+        a.y = dev::plain(d.t);
+        if (pre == 1) {
+            dev::spmv(d.A, dev::kXWdR, dev::kEResid, a, st_);
+        } else {
+            dev::wd_times_r(d.n, d.wd, a.r, d.zp, st_);
+            double* cur = d.zp;
+            double* tmp = d.u;
+            for (int sw = 1; sw < pre; ++sw) {
+                dev::SpmvArgs sa = a;
+                sa.x = dev::plain(cur);
+                sa.y = dev::plain(tmp);
+                dev::spmv(d.A, dev::kXPlain, dev::kESmooth, sa, st_);
+                std::swap(cur, tmp);
+            }
+            if (cur != d.zp)
+                IRK_CUDA_CHECK(cudaMemcpyAsync(d.zp, cur, sizeof(double) * d.n, cudaMemcpyDeviceToDevice, st_));
+            a.x = dev::plain(d.zp);
+            dev::spmv(d.A, dev::kXPlain, dev::kEResid, a, st_);
+        }
+        dev::SpmvArgs ra;
+        ra.x = dev::plain(d.t);
+        ra.y = dev::plain(H.lv[l + 1].r);
+        dev::spmv(d.R, dev::kXPlain, dev::kEPlain, ra, st_);
+    }
+    dev::dense_mv(H.nc, H.cinv, rhs_of(L - 1), out_of(L - 1), st_);
+    for (int l = L - 2; l >= 0; --l) {
+        DevLevel& d = H.lv[l];
+        dev::SpmvArgs pa;
+        pa.x = dev::plain(H.lv[l + 1].z);
+        pa.r = rhs_of(l);
+        pa.wd = d.wd;
+        pa.zb = pre == 1 ? nullptr : d.zp;
+        pa.y = dev::plain(d.t);
+        dev::spmv(d.P, dev::kXPlain, dev::kEProlong, pa, st_);
+        double* cur = d.t;
+        for (int sw = 0; sw < post; ++sw) {
+            dev::SpmvArgs sa;
+            sa.x = dev::plain(cur);
+            sa.r = rhs_of(l);
+            sa.wd = d.wd;
+            const bool last = sw == post - 1;
+            double* nxt = cur == d.t ? d.u : d.t;
+            sa.y = last ? out_of(l) : dev::plain(nxt);
+            dev::spmv(d.A, dev::kXPlain, dev::kESmooth, sa, st_);
+            cur = nxt;
+        }
+    }
+}
+
+// Block preconditioner apply (stage.cpp:138-182): diagonal, forward (LD,
+// GSL) or backward (DU) block substitution, one V-cycle per block.  The
+// off-diagonal K-products are fused into the sweep kernel that assembles the
+// next block's right-hand side.
+void DeviceSolver::record_precond(VecRef v, VecRef w) {
+    const int s = s_;
+    const long long n = n_;
+    auto e = [&](int j, int k) { return -ht_ * At_[j * s + k]; };
+    for (int q = 0; q < s; ++q) {
+        const int j = structure_ == Structure::Upper ? s - 1 - q : q;
+        VecRef in = block(v, j * n);
+        if (structure_ != Structure::Diagonal && q > 0) {
+            const int prev = structure_ == Structure::Upper ? j + 1 : j - 1;
+            const int k0 = structure_ == Structure::Upper ? j + 1 : 0;
+            const int k1 = structure_ == Structure::Upper ? s : j;
+            // later stages that still need K w_prev
+            bool later = false;
+            for (int q2 = q + 1; q2 < s; ++q2) {
+                const int j2 = structure_ == Structure::Upper ? s - 1 - q2 : q2;
+                if (At_[j2 * s + prev] != 0.0) later = true;
+            }
+            dev::SweepTerms t{};
+            bool fresh = false;
+            for (int k = k0; k < k1; ++k) {
+                if (At_[j * s + k] == 0.0) continue;
+                t.coef[t.nt] = e(j, k);
+                t.buf[t.nt] = k == prev ? nullptr : fw_ + k * n;
+                if (k == prev) fresh = true;
+                ++t.nt;
+            }
+            if (fresh || later) {
+                double* store = later ? fw_ + prev * n : nullptr;
+                if (K_.fmt == 1) {
+                    dev::sweep_dia(K_, block(w, prev * n), in, t, store, dev::plain(rhs_), n_, st_);
+                } else {
+                    dev::SpmvArgs a;
+                    a.x = block(w, prev * n);
+                    a.y = dev::plain(fw_ + prev * n);
+                    dev::spmv(K_, dev::kXPlain, dev::kEPlain, a, st_);
+                    for (int q3 = 0; q3 < t.nt; ++q3)
+                        if (!t.buf[q3]) t.buf[q3] = fw_ + prev * n;
+                    dev::combine(in, t, dev::plain(rhs_), n_, st_);
+                }
+                in = dev::plain(rhs_);
+            } else if (t.nt > 0) {
+                dev::combine(in, t, dev::plain(rhs_), n_, st_);
+                in = dev::plain(rhs_);
+            }
+        }
+        record_vcycle(sob_[j], in, block(w, j * n));
+    }
+}
+
+// Stage operator (stage.cpp:28-44): fused single pass when M and K share a
+// DIA pattern, otherwise s K-products, s M-products and s^2 axpys.
+void DeviceSolver::record_stage_op(VecRef z, VecRef y) {
+    if (fused_op_) {
+        dev::stage_op_dia(M_, K_, coef_, z, y, n_, st_);
+        return;
+    }
+    const long long n = n_;
+    for (int j = 0; j < s_; ++j) {
+        dev::SpmvArgs a;
+        a.x = block(z, j * n);
+        a.y = dev::plain(fw_ + j * n);
+        dev::spmv(K_, dev::kXPlain, dev::kEPlain, a, st_);
+    }
+    for (int i = 0; i < s_; ++i) {
+        dev::SpmvArgs a;
+        a.x = block(z, i * n);
+        a.y = block(y, i * n);
+        dev::spmv(M_, dev::kXPlain, dev::kEPlain, a, st_);
+        for (int j = 0; j < s_; ++j)
+            dev::axpy(coef_.c[i * s_ + j], fw_ + j * n, block(y, i * n), n_, st_);
+    }
+}
+
+// One Arnoldi iteration: Z_j = P^-1 V_j, V_{j+1} = A Z_j, CGS (+ conditional
+// second pass), Givens, normalisation.
+void DeviceSolver::record_iteration() {
+    const int* jp = &gb_.ctl->j;
+    record_precond(slot(gb_.V, jp, stride_, 0), slot(gb_.Z, jp, stride_, 0));
+    record_stage_op(slot(gb_.Z, jp, stride_, 0), slot(gb_.V, jp, stride_, 1));
+    dev::gm_blockdot(gb_, 1, st_);
+    dev::gm_update(gb_, 1, st_);
+    dev::gm_blockdot(gb_, 2, st_);
+    dev::gm_update(gb_, 2, st_);
+    dev::gm_normalize(gb_, st_);
+}
+
+// ------------------------------------------------------------------ GMRES
+void DeviceSolver::ensure_gmres(int restart, int max_iter) {
+    check(restart <= dev::kMaxRestart, "gmres: restart exceeds the device capacity (512)");
+    if (restart <= cap_restart_ && max_iter <= cap_iter_) return;
+    for (cudaGraphExec_t* e : {&exec_, &exec_iter_, &exec_pre_, &exec_cb_, &exec_ce_, &exec_post_})
+        if (*e) {
+            cudaGraphExecDestroy(*e);
+            *e = nullptr;
+        }
+    g_restart_ = -1;
+    cap_restart_ = std::max(restart, cap_restart_);
+    cap_iter_ = std::max(max_iter, cap_iter_);
+    V_ = DevBuf(sizeof(double) * stride_ * (cap_restart_ + 1));
+    Z_ = DevBuf(sizeof(double) * stride_ * cap_restart_);
+    H_ = DevBuf(sizeof(double) * (cap_restart_ + 1) * (cap_restart_ + 1));
+    hist_ = DevBuf(sizeof(double) * (cap_iter_ + 1));
+    const int nch = static_cast<int>((sN_ + dev::kChunk - 1) / dev::kChunk);
+    part_ = DevBuf(sizeof(double) * static_cast<size_t>(dev::kMaxRestart + 2) * nch);
+    ctl_ = DevBuf(sizeof(dev::GmresCtl));
+    cnt_ = DevBuf(sizeof(unsigned) * 16);
+    IRK_CUDA_CHECK(cudaMemset(cnt_.as<void>(), 0, sizeof(unsigned) * 16));
+    IRK_CUDA_CHECK(cudaMemset(ctl_.as<void>(), 0, sizeof(dev::GmresCtl)));
+    if (ctl_host_) cudaFreeHost(ctl_host_);
+    if (hist_host_) cudaFreeHost(hist_host_);
+    IRK_CUDA_CHECK(cudaMallocHost(&ctl_host_, sizeof(dev::GmresCtl)));
+    IRK_CUDA_CHECK(cudaMallocHost(&hist_host_, sizeof(double) * (cap_iter_ + 1)));
+    gb_.ctl = ctl_.as<dev::GmresCtl>();
+    gb_.H = H_.as<double>();
+    gb_.hist = hist_.as<double>();
+    gb_.partials = part_.as<double>();
+    gb_.counters = cnt_.as<unsigned>();
+    gb_.V = V_.as<double>();
+    gb_.Z = Z_.as<double>();
+    gb_.sN = sN_;
+    gb_.nchunks = nch;
+}
+
+namespace {
+
+struct Capture {
+    cudaStream_t st;
+    cudaGraph_t g = nullptr;
+};
+
+cudaGraphExec_t instantiate(cudaGraph_t g) {
+    cudaGraphExec_t e = nullptr;
+    IRK_CUDA_CHECK(cudaGraphInstantiate(&e, g, 0));
+    return e;
+}
+
+// Adds a WHILE conditional node at the current capture point of `st` and
+// returns its body graph; `st` continues after the node.
+cudaGraph_t add_while(cudaStream_t st, cudaGraphConditionalHandle* h, unsigned dflt) {
+    cudaStreamCaptureStatus status;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    IRK_CUDA_CHECK(cudaStreamGetCaptureInfo(st, &status, nullptr, &cg, &deps, &ndeps));
+    IRK_CUDA_CHECK(cudaGraphConditionalHandleCreate(h, cg, dflt, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = *h;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    IRK_CUDA_CHECK(cudaGraphAddNode(&node, cg, deps, ndeps, &p));
+    IRK_CUDA_CHECK(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+    return p.conditional.phGraph_out[0];
+}
+
+int count_nodes(cudaGraph_t g) {
+    size_t n = 0;
+    cudaGraphGetNodes(g, nullptr, &n);
+    return static_cast<int>(n);
+}
+
+}  // namespace
+
+void DeviceSolver::build_graph(bool lift, int restart, int max_iter, double rtol, bool use_cond) {
+    for (cudaGraphExec_t* e : {&exec_, &exec_iter_, &exec_pre_, &exec_cb_, &exec_ce_, &exec_post_})
+        if (*e) {
+            cudaGraphExecDestroy(*e);
+            *e = nullptr;
+        }
+    gb_.use_cond = use_cond ? 1 : 0;
+    auto pre = [&]() {
+        dev::SpmvArgs a;
+        a.x = dev::plain(u_);
+        a.y = dev::plain(ku_);
+        dev::spmv(K_, dev::kXPlain, dev::kEPlain, a, st_);
+        dev::stage_rhs_finish(ku_, lift ? lift_ : nullptr, b_, n_, s_, st_);
+        IRK_CUDA_CHECK(cudaMemsetAsync(x_, 0, sizeof(double) * sN_, st_));
+        dev::gm_init(gb_, b_, r_, rtol, restart, max_iter, st_);
+    };
+    auto cycle_begin = [&]() { dev::gm_cycle_begin(gb_, r_, st_); };
+    auto cycle_end = [&]() {
+        dev::gm_solution(gb_, x_, st_);
+        record_stage_op(dev::plain(x_), dev::plain(ax_));
+        dev::gm_residual(gb_, b_, ax_, r_, st_);
+    };
+    auto post = [&]() { dev::irk_update(u_, x_, hb_.data(), n_, s_, unext_, st_); };
+
+    if (use_cond) {
+        cudaStream_t s2 = nullptr, s3 = nullptr;
+        IRK_CUDA_CHECK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        IRK_CUDA_CHECK(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
+        cudaStream_t main = st_;
+        cudaGraph_t top = nullptr;
+        IRK_CUDA_CHECK(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
+        // The outer handle must exist before the init kernel is recorded.
+        cudaGraphConditionalHandle ho;
+        {
+            cudaStreamCaptureStatus status;
+            cudaGraph_t cg = nullptr;
+            IRK_CUDA_CHECK(cudaStreamGetCaptureInfo(main, &status, nullptr, &cg, nullptr, nullptr));
+            IRK_CUDA_CHECK(cudaGraphConditionalHandleCreate(&ho, cg, 0, 0));
+        }
+        gb_.h_outer = ho;
+        pre();
+        // outer WHILE node (handle created above, on the top graph)
+        cudaGraph_t outer_body;
+        {
+            cudaStreamCaptureStatus status;
+            cudaGraph_t cg = nullptr;
+            const cudaGraphNode_t* deps = nullptr;
+            size_t ndeps = 0;
+            IRK_CUDA_CHECK(cudaStreamGetCaptureInfo(main, &status, nullptr, &cg, &deps, &ndeps));
+            cudaGraphNodeParams p = {};
+            p.type = cudaGraphNodeTypeConditional;
+            p.conditional.handle = ho;
+            p.conditional.type = cudaGraphCondTypeWhile;
+            p.conditional.size = 1;
+            cudaGraphNode_t node;
+            IRK_CUDA_CHECK(cudaGraphAddNode(&node, cg, deps, ndeps, &p));
+            IRK_CUDA_CHECK(cudaStreamUpdateCaptureDependencies(main, &node, 1, cudaStreamSetCaptureDependencies));
+            outer_body = p.conditional.phGraph_out[0];
+        }
+        // outer body: cycle begin -> inner WHILE -> cycle end
+        st_ = s2;
+        IRK_CUDA_CHECK(cudaStreamBeginCaptureToGraph(s2, outer_body, nullptr, nullptr, 0,
+                                                     cudaStreamCaptureModeThreadLocal));
+        cudaGraphConditionalHandle hi;
+        {
+            cudaStreamCaptureStatus status;
+            cudaGraph_t cg = nullptr;
+            IRK_CUDA_CHECK(cudaStreamGetCaptureInfo(s2, &status, nullptr, &cg, nullptr, nullptr));
+            IRK_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hi, cg, 0, 0));
+        }
+        gb_.h_inner = hi;
+        cycle_begin();
+        cudaGraph_t inner_body;
+        {
+            cudaStreamCaptureStatus status;
+            cudaGraph_t cg = nullptr;
+            const cudaGraphNode_t* deps = nullptr;
+            size_t ndeps = 0;
+            IRK_CUDA_CHECK(cudaStreamGetCaptureInfo(s2, &status, nullptr, &cg, &deps, &ndeps));
+            cudaGraphNodeParams p = {};
+            p.type = cudaGraphNodeTypeConditional;
+            p.conditional.handle = hi;
+            p.conditional.type = cudaGraphCondTypeWhile;
+            p.conditional.size = 1;
+            cudaGraphNode_t node;
+            IRK_CUDA_CHECK(cudaGraphAddNode(&node, cg, deps, ndeps, &p));
+            IRK_CUDA_CHECK(cudaStreamUpdateCaptureDependencies(s2, &node, 1, cudaStreamSetCaptureDependencies));
+            inner_body = p.conditional.phGraph_out[0];
+        }
+        st_ = s3;
+        IRK_CUDA_CHECK(cudaStreamBeginCaptureToGraph(s3, inner_body, nullptr, nullptr, 0,
+                                                     cudaStreamCaptureModeThreadLocal));
+        record_iteration();
+        IRK_CUDA_CHECK(cudaStreamEndCapture(s3, &inner_body));
+        launches_per_iter_ = count_nodes(inner_body);
+        st_ = s2;
+        cycle_end();
+        IRK_CUDA_CHECK(cudaStreamEndCapture(s2, &outer_body));
+        st_ = main;
+        post();
+        IRK_CUDA_CHECK(cudaStreamEndCapture(main, &top));
+        exec_ = instantiate(top);
+        cudaGraphDestroy(top);
+        cudaStreamDestroy(s2);
+        cudaStreamDestroy(s3);
+    } else {
+        auto cap = [&](auto&& fn) {
+            cudaGraph_t g = nullptr;
+            IRK_CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+            fn();
+            IRK_CUDA_CHECK(cudaStreamEndCapture(st_, &g));
+            return g;
+        };
+        cudaGraph_t g;
+        g = cap(pre); exec_pre_ = instantiate(g); cudaGraphDestroy(g);
+        g = cap(cycle_begin); exec_cb_ = instantiate(g); cudaGraphDestroy(g);
+        g = cap([&] { record_iteration(); });
+        launches_per_iter_ = count_nodes(g);
+        exec_iter_ = instantiate(g); cudaGraphDestroy(g);
+        g = cap(cycle_end); exec_ce_ = instantiate(g); cudaGraphDestroy(g);
+        g = cap(post); exec_post_ = instantiate(g); cudaGraphDestroy(g);
+    }
+    graph_mode_ = use_cond ? 1 : 0;
+    g_lift_ = lift;
+    g_restart_ = restart;
+    g_iter_ = max_iter;
+    g_rtol_ = rtol;
+}
+
+SolveReport DeviceSolver::read_report(int max_iter) {
+    SolveReport rep;
+    const dev::GmresCtl& c = *ctl_host_;
+    rep.iterations = c.total;
+    rep.cycles = c.cycles;
+    rep.n_reorth = c.n_reorth;
+    rep.converged = c.converged;
+    rep.final_rel = c.final_rel;
+    rep.true_rel = c.true_rel;
+    const int len = std::min(c.total, max_iter) + 1;
+    rep.history.assign(hist_host_, hist_host_ + len);
+    return rep;
+}
+
+SolveReport DeviceSolver::step(const double* u, const double* lift, const GmresConfig& cfg,
+                               double* u_next, double* k_out) {
+    check(cfg.rel_tol > 0.0, "gmres: rel_tol must be positive");
+    check(cfg.side == 1, "device gmres: only right preconditioning runs on the device");
+    const int max_iter = cfg.max_iter;
+    int restart = cfg.restart <= 0 || cfg.restart > max_iter ? max_iter : cfg.restart;
+    if (restart < 1) restart = 1;
+    ensure_gmres(restart, std::max(max_iter, 1));
+    static const bool no_cond = std::getenv("IRK_NO_COND_GRAPH") != nullptr;
+    const bool want_cond = !no_cond;
+    if (g_restart_ != restart || g_iter_ != max_iter || g_rtol_ != cfg.rel_tol ||
+        g_lift_ != (lift != nullptr) || (graph_mode_ == 1) != want_cond) {
+        bool ok = false;
+        if (want_cond) {
+            try {
+                build_graph(lift != nullptr, restart, max_iter, cfg.rel_tol, true);
+                ok = true;
+            } catch (const CudaError&) {
+                cudaGetLastError();
+                cudaStreamCaptureStatus stc;
+                if (cudaStreamIsCapturing(st_, &stc) == cudaSuccess && stc != cudaStreamCaptureStatusNone) {
+                    cudaGraph_t junk;
+                    cudaStreamEndCapture(st_, &junk);
+                }
+            }
+        }
+        if (!ok) build_graph(lift != nullptr, restart, max_iter, cfg.rel_tol, false);
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    IRK_CUDA_CHECK(cudaMemcpyAsync(u_, u, sizeof(double) * n_, cudaMemcpyDefault, st_));
+    if (lift) IRK_CUDA_CHECK(cudaMemcpyAsync(lift_, lift, sizeof(double) * n_, cudaMemcpyDefault, st_));
+    if (graph_mode_ == 1) {
+        IRK_CUDA_CHECK(cudaGraphLaunch(exec_, st_));
+    } else {
+        IRK_CUDA_CHECK(cudaGraphLaunch(exec_pre_, st_));
+        IRK_CUDA_CHECK(cudaMemcpyAsync(ctl_host_, gb_.ctl, sizeof(dev::GmresCtl), cudaMemcpyDeviceToHost, st_));
+        IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
+        while (!ctl_host_->done) {
+            IRK_CUDA_CHECK(cudaGraphLaunch(exec_cb_, st_));
+            while (true) {
+                IRK_CUDA_CHECK(cudaGraphLaunch(exec_iter_, st_));
+                IRK_CUDA_CHECK(cudaMemcpyAsync(&ctl_host_->stop, &gb_.ctl->stop, sizeof(int),
+                                               cudaMemcpyDeviceToHost, st_));
+                IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
+                if (ctl_host_->stop != 0) break;
+            }
+            IRK_CUDA_CHECK(cudaGraphLaunch(exec_ce_, st_));
+            IRK_CUDA_CHECK(cudaMemcpyAsync(ctl_host_, gb_.ctl, sizeof(dev::GmresCtl), cudaMemcpyDeviceToHost, st_));
+            IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
+        }
+        IRK_CUDA_CHECK(cudaGraphLaunch(exec_post_, st_));
+    }
+    if (u_next) IRK_CUDA_CHECK(cudaMemcpyAsync(u_next, unext_, sizeof(double) * n_, cudaMemcpyDefault, st_));
+    if (k_out) IRK_CUDA_CHECK(cudaMemcpyAsync(k_out, x_, sizeof(double) * sN_, cudaMemcpyDefault, st_));
+    IRK_CUDA_CHECK(cudaMemcpyAsync(ctl_host_, gb_.ctl, sizeof(dev::GmresCtl), cudaMemcpyDeviceToHost, st_));
+    IRK_CUDA_CHECK(cudaMemcpyAsync(hist_host_, gb_.hist, sizeof(double) * (max_iter + 1),
+                                   cudaMemcpyDeviceToHost, st_));
+    IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
+    SolveReport rep = read_report(max_iter);
+    rep.solve_seconds = seconds_since(t0);
+    return rep;
+}
+
+SolveReport DeviceSolver::step_host(const double* u, const double* lift, const GmresConfig& cfg,
+                                    double* u_next, double* k_out) {
+    // cudaMemcpyDefault handles pageable or pinned host pointers.
+    return step(u, lift, cfg, u_next, k_out);
+}
+
+void DeviceSolver::stage_apply(const double* v, double* y) {
+    record_stage_op(dev::plain(v), dev::plain(y));
+    IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
+}
+
+void DeviceSolver::precond_apply(const double* v, double* w) {
+    record_precond(dev::plain(v), dev::plain(w));
+    IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
+}
+
+void DeviceSolver::vcycle(int k, const double* r, double* z) {
+    check(k >= 0 && k < static_cast<int>(hier_.size()), "vcycle: hierarchy index out of range");
+    record_vcycle(k, dev::plain(r), dev::plain(z));
+    IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
+}
+
+double DeviceSolver::dot(const double* x, const double* y, long long n) {
+    const long long nch = (n + dev::kChunk - 1) / dev::kChunk;
+    DevBuf part(sizeof(double) * std::max<long long>(nch, 1));
+    dev::dot(x, y, n, part.as<double>(), red_cnt_, red_out_, st_);
+    double out = 0.0;
+    IRK_CUDA_CHECK(cudaMemcpyAsync(&out, red_out_, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
+    return out;
+}
+
+double DeviceSolver::time_kernel(int which, int reps) {
+    DevBuf a(sizeof(double) * stride_), b(sizeof(double) * stride_);
+    IRK_CUDA_CHECK(cudaMemsetAsync(a.as<void>(), 0, sizeof(double) * stride_, st_));
+    auto once = [&]() {
+        switch (which) {
+        case 0: record_stage_op(dev::plain(a.as<double>()), dev::plain(b.as<double>())); break;
+        case 1: {
+            DevLevel& d = hier_[0].lv[0];
+            dev::SpmvArgs sa;
+            sa.x = dev::plain(a.as<double>());
+            sa.r = dev::plain(a.as<double>());
+            sa.wd = d.wd;
+            sa.y = dev::plain(b.as<double>());
+            dev::spmv(d.A, dev::kXPlain, dev::kESmooth, sa, st_);
+            break;
+        }
+        case 2: record_precond(dev::plain(a.as<double>()), dev::plain(b.as<double>())); break;
+        default: record_vcycle(0, dev::plain(a.as<double>()), dev::plain(b.as<double>())); break;
+        }
+    };
+    once();
+    cudaEvent_t e0, e1;
+    IRK_CUDA_CHECK(cudaEventCreate(&e0));
+    IRK_CUDA_CHECK(cudaEventCreate(&e1));
+    IRK_CUDA_CHECK(cudaEventRecord(e0, st_));
+    for (int i = 0; i < reps; ++i) once();
+    IRK_CUDA_CHECK(cudaEventRecord(e1, st_));
+    IRK_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return static_cast<double>(ms) / reps;
+}
+
+}  // namespace irkb

@@ -1,0 +1,154 @@
+// Device-resident IRK stage-system solver: the B200 replacement for the
+// reference's irk_step -> gmres -> {StageOperator, BlockPreconditioner ->
+// amg_vcycle} call stack (SURVEY.md §3 stack B).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "../host/setup.hpp"
+#include "kernels.cuh"
+
+namespace irkb {
+
+// Owns one device allocation.
+class DevBuf {
+public:
+    DevBuf() = default;
+    explicit DevBuf(size_t bytes);
+    ~DevBuf();
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    template <class T> T* as() const { return static_cast<T*>(p_); }
+    size_t bytes() const { return n_; }
+
+private:
+    void* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+struct GmresConfig {
+    int side = 1;        // 1 right (the only device mode), 0 left
+    double rel_tol = 1e-8;
+    int max_iter = 500;
+    int restart = 50;    // 0 = full GMRES (restart = max_iter)
+};
+
+struct SolveReport {
+    int iterations = 0, cycles = 0, n_reorth = 0, converged = 0;
+    double final_rel = 0.0, true_rel = 0.0;
+    double solve_seconds = 0.0;
+    std::vector<double> history;
+};
+
+struct DevLevel {
+    int n = 0;
+    dev::Mat A, P, R;
+    double* wd = nullptr;         // omega * D^-1
+    double* r = nullptr;          // level rhs (levels >= 1)
+    double* z = nullptr;          // level solution (levels >= 1)
+    double* t = nullptr;          // residual / prolongated iterate
+    double* u = nullptr;          // post-sweep ping-pong
+    double* zp = nullptr;         // pre-smoothed iterate (pre > 1 only)
+};
+
+struct DevHier {
+    std::vector<DevLevel> lv;
+    double* cinv = nullptr;
+    int nc = 0;
+    AmgParams prm;
+};
+
+class DeviceSolver {
+public:
+    // Builds (or takes) one AMG hierarchy per distinct diagonal of At and
+    // uploads everything.  `hiers` may be empty (built here with `amg`).
+    DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<double>& A,
+                 const std::vector<double>& b, const std::vector<double>& At, Structure st,
+                 double ht, const AmgParams& amg, std::vector<Hierarchy> hiers, int device);
+    ~DeviceSolver();
+
+    int n() const { return n_; }
+    int s() const { return s_; }
+    long long sN() const { return sN_; }
+    cudaStream_t stream() const { return st_; }
+    const std::vector<Hierarchy>& hierarchies() const { return hier_host_; }
+    const std::vector<int>& solver_of_block() const { return sob_; }
+    double setup_seconds() const { return setup_seconds_; }
+    bool fused_stage_op() const { return fused_op_; }
+    int matrix_format(int which) const;  // 0 M, 1 K -> 0 CSR, 1 DIA
+
+    // Device-pointer entry points (enqueue + synchronise).
+    void stage_apply(const double* v, double* y);
+    void precond_apply(const double* v, double* w);
+    void vcycle(int k, const double* r, double* z);
+    double dot(const double* x, const double* y, long long n);
+    SolveReport step(const double* u, const double* lift, const GmresConfig& cfg, double* u_next,
+                     double* k_out);
+    // Host-pointer step: H2D of u (and lift), D2H of u_next (and K).
+    SolveReport step_host(const double* u, const double* lift, const GmresConfig& cfg,
+                          double* u_next, double* k_out);
+
+    // Timing hooks for the roofline (bench.py): launches `reps` applications
+    // of the named hot kernel between CUDA events on the solver's stream and
+    // returns the mean milliseconds per launch.  which: 0 stage operator,
+    // 1 fine-level smoother SpMV, 2 preconditioner apply, 3 V-cycle.
+    double time_kernel(int which, int reps);
+    int launches_per_iteration() const { return launches_per_iter_; }
+    int graph_mode() const { return graph_mode_; }
+
+private:
+    dev::Mat upload(const Csr& A, bool allow_dia);
+    double* alloc(size_t count);
+    void record_vcycle(int k, dev::VecRef r, dev::VecRef z);
+    void record_precond(dev::VecRef v, dev::VecRef w);
+    void record_stage_op(dev::VecRef z, dev::VecRef y);
+    void record_iteration();
+    void ensure_gmres(int restart, int max_iter);
+    void build_graph(bool lift, int restart, int max_iter, double rtol, bool use_cond);
+    SolveReport read_report(int max_iter);
+
+    int n_ = 0, s_ = 0;
+    long long sN_ = 0, stride_ = 0;
+    int device_ = 0;
+    cudaStream_t st_ = nullptr;
+    std::vector<DevBuf> bufs_;
+    dev::Mat M_, K_;
+    bool fused_op_ = false;
+    dev::StageCoef coef_{};
+    std::vector<double> At_, hb_;
+    Structure structure_ = Structure::Diagonal;
+    double ht_ = 0.0;
+    std::vector<int> sob_;
+    std::vector<Hierarchy> hier_host_;
+    std::vector<DevHier> hier_;
+    double setup_seconds_ = 0.0;
+    // work vectors
+    double *rhs_ = nullptr, *fw_ = nullptr;  // fw_: s * n
+    double *u_ = nullptr, *lift_ = nullptr, *unext_ = nullptr, *ku_ = nullptr;
+    double *b_ = nullptr, *x_ = nullptr, *r_ = nullptr, *ax_ = nullptr;
+    double *red_part_ = nullptr, *red_out_ = nullptr;
+    unsigned* red_cnt_ = nullptr;
+    // GMRES
+    int cap_restart_ = 0, cap_iter_ = 0;
+    dev::GmresBufs gb_{};
+    DevBuf V_, Z_, H_, hist_, part_, ctl_, cnt_;
+    dev::GmresCtl* ctl_host_ = nullptr;  // pinned
+    double* hist_host_ = nullptr;        // pinned
+    // graph cache
+    cudaGraphExec_t exec_ = nullptr;
+    cudaGraphExec_t exec_iter_ = nullptr, exec_pre_ = nullptr, exec_cb_ = nullptr,
+                    exec_ce_ = nullptr, exec_post_ = nullptr;
+    int graph_mode_ = -1;  // 1 conditional nodes, 0 host-driven loop
+    bool g_lift_ = false;
+    int g_restart_ = -1, g_iter_ = -1;
+    double g_rtol_ = -1.0;
+    int launches_per_iter_ = 0;
+    int counting_ = 0;
+};
+
+}  // namespace irkb
