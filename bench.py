@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 IRK solve phase (BASELINE.json metric).
+
+Workload (BASELINE configs[1], "C2"): 2D heat on a 1024x1024-cell P1 grid
+(1,046,529 free dofs per stage), Radau IIA s=3 (3,139,587 unknowns),
+h_t = 1e-3, u0 = sin(pi x) sin(pi y) + U[-0.01, 0.01] (seeded), GMRES(50),
+rtol 1e-8, block LDU (P_LD) preconditioner with one AMG V(1,1) damped-Jacobi
+cycle per diagonal block, fp64.  A "step" is one IRK timestep solve (stage
+rhs -> GMRES -> u_{n+1}); timed steps advance the trajectory u_0 -> u_K.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  `value` = timestep solves/s over all ranks
+with inputs resident in HBM (irkdev_step_device); `e2e` = the same metric
+through the host-pointer C ABI (irkdev_step: H2D of u_n, D2H of u_{n+1} and
+the report inside the timed region).  Multi-GPU runs are independent replicas
+(the solve does not shard), reported as weak scaling.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "IRK timestep solves/s (2D heat, Radau IIA); solve-phase HBM GB/s vs peak"
+UNIT = "solves/s"
+CELLS, S, HT, NOISE, SEED = 1024, 3, 1e-3, 0.01, 1
+WORKLOAD = "C2: heat 1024^2 P1, Radau IIA s=3, h_t=1e-3, P_LD + AMG V(1,1) Jacobi, GMRES(50) rtol 1e-8"
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def config(extra=None):
+    c = {"workload": WORKLOAD, "grid": f"{CELLS}x{CELLS}", "dofs_per_stage": (CELLS - 1) ** 2,
+         "stages": S, "unknowns": S * (CELLS - 1) ** 2, "ht": HT, "preconditioner": "LD",
+         "gmres_restart": 50, "rel_tol": 1e-8,
+         "l2_policy": "inputs larger than L2 (>=2.8 GB streamed per GMRES iteration vs 126 MB L2)"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ byte model
+def solve_bytes(dev_info, levels, its_reorth, n, s, nnz_mk):
+    """Algorithmic HBM bytes of one IRK solve per SURVEY.md §8(d).
+
+    levels[k] = [(n_l, nnz_A, nnz_P, nnz_R), ...]; its_reorth = (iters, reorths,
+    cycles) of the solve.  Each kernel reads its operands once and writes its
+    result once; no cross-kernel cache credit.
+    """
+    N = n
+    sN = s * N
+    OP = 4 * (N + 1) + 4 * nnz_mk + 16 * nnz_mk + 8 * sN + 8 * sN
+
+    def VC(lv):
+        b = 0
+        for l in range(len(lv) - 1):
+            nl, nA, nP, nR = lv[l]
+            nc = lv[l + 1][0]
+            b += 2 * (4 * (nl + 1) + 12 * nA) + 4 * (nl + 1) + 12 * nP + 4 * (nc + 1) + 12 * nR
+            b += 104 * nl + 16 * nc
+        nL = lv[-1][0]
+        return b + 8 * nL * nL + 16 * nL
+
+    sob = dev_info["solver_of_block"]
+    PREC = sum(VC(levels[sob[i]]) for i in range(s))
+    PREC += (s - 1) * (4 * (N + 1) + 12 * nnz_mk + 16 * N) + sum(8 * N * (i + 2) for i in range(1, s))
+    iters, reorths, cycles = its_reorth
+    total = 0
+    # per-iteration ORTH with j = index within the cycle (restart 50)
+    j_list = []
+    left = iters
+    while left > 0:
+        m = min(50, left)
+        j_list.extend(range(m))
+        left -= m
+    for k, j in enumerate(j_list):
+        total += OP + PREC + 8 * sN * (2 * j + 7)
+    # re-orthogonalisation passes: assume they fire on the first `reorths` iterations' j
+    for j in j_list[:reorths]:
+        total += 8 * sN * (2 * j + 5)
+    total += 8 * sN * (iters + 1) + PREC + OP + 16 * sN + 8 * N * (s + 2) + (4 * (N + 1) + 12 * nnz_mk)
+    total += max(cycles - 1, 0) * (PREC + OP + 8 * sN * 51 + 24 * sN)
+    per_iter = (OP + PREC + sum(8 * sN * (2 * j + 7) for j in j_list) / max(len(j_list), 1))
+    return total, per_iter
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference_steps(steps, warmup, rank0=True):
+    """The reference's own CPU implementation (oracle/_ref: irkprec compiled from
+    its sources) on the same workload: setup excluded, steps timed."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    from refs import Ref, RefSolver  # noqa: E402
+    if not Ref.available():
+        raise RuntimeError("oracle/_ref/libirkref.so not built")
+    import paper_2010_11377_b200 as P
+    prob = P.make_heat_setup(CELLS)
+    u0 = prob.initial(NOISE, SEED)
+    ref_prob = Ref.problem("heat", CELLS)
+    rs = RefSolver(ref_prob["M"], ref_prob["K"], 0, S, 3, HT)
+    u = u0.copy()
+    for _ in range(warmup):
+        rs.step(u, ref_prob["f_lift"])
+    u = u0.copy()
+    secs, its = [], []
+    for _ in range(steps):
+        r = rs.step(u, ref_prob["f_lift"])
+        secs.append(r["seconds"])
+        its.append(r["iterations"])
+        u = r["u_next"]
+    return sum(secs), its
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    steps = max(1, min(args.steps, 3))
+    warm = 0 if args.warmup <= 0 else 1
+    total, its = run_reference_steps(steps, warm)
+    value = steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": 1e3 * total / steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded u0 noise, BASELINE configs[1])",
+        "config": config({"reference_iterations": its}),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "reference",
+                         "sample": f"{steps} C2 timesteps of the reference irk_step (irkprec compiled "
+                                   "from /root/reference sources, OpenMP, GMRES(50) wrapper), "
+                                   "setup excluded"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cells", type=int, default=CELLS)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    global CELLS
+    CELLS = args.cells
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2010_11377_b200 as P
+    from paper_2010_11377_b200 import _abi
+    L = _abi.lib()
+
+    t_setup = time.time()
+    prob = P.make_heat_setup(CELLS)
+    table = P.make_radau_iia(S)
+    coeff = P.precond_coeff(table, P.CoeffKind.LowerFactor)
+    Pc = P.BlockPreconditioner(prob.M, prob.F, coeff, HT, P.AmgParams(), table=table, device=local)
+    dev = Pc._dev
+    setup_s = time.time() - t_setup
+    u0 = prob.initial(NOISE, SEED)
+    n = prob.M.n_rows
+    cfg = P.GmresConfig(restart=50).c()
+
+    d_u = torch.from_numpy(u0).cuda()
+    d_un = torch.empty_like(d_u)
+    stream_ptr = C.c_void_p()
+    _abi.check(L.irkdev_stream(dev._h, C.byref(stream_ptr)))
+    st = torch.cuda.ExternalStream(stream_ptr.value)
+
+    def dstep(u_t, un_t):
+        rep = _abi.irk_report()
+        _abi.check(L.irkdev_step_device(dev._h, C.c_void_p(u_t.data_ptr()), None, C.byref(cfg),
+                                        C.c_void_p(un_t.data_ptr()), None, C.byref(rep)))
+        return rep
+
+    for _ in range(args.warmup):
+        dstep(d_u, d_un)
+    # timed: the trajectory u_0 -> u_K, inputs resident in HBM
+    cur = torch.from_numpy(u0).cuda()
+    nxt = torch.empty_like(cur)
+    reps = []
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            reps.append(dstep(cur, nxt))
+            cur, nxt = nxt, cur
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+        dist.barrier()
+    its = [r.iterations for r in reps]
+    value = world * args.steps / (ms / 1e3)
+
+    # e2e: host pointers through the public C ABI (H2D u_n, D2H u_{n+1} + report)
+    hu = torch.from_numpy(u0.copy()).pin_memory()
+    hun = torch.empty_like(hu).pin_memory()
+    hist = np.empty(501)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(st)
+    for _ in range(args.steps):
+        rep = _abi.irk_report()
+        _abi.check(L.irkdev_step(dev._h, _abi.as_d(hu.numpy()), None, C.byref(cfg),
+                                 _abi.as_d(hun.numpy()), None, C.byref(rep), _abi.as_d(hist)))
+        hu, hun = hun, hu
+    e3.record(st)
+    torch.cuda.synchronize()
+    e2e_ms = e2.elapsed_time(e3)
+    wall_e2e = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+
+    # launches inside the timed region: per-phase kernel counts of the graph
+    cnt = (C.c_int * 4)()
+    _abi.check(L.irkdev_launch_counts(dev._h, cnt))
+    launches = sum(cnt[0] + cnt[3] + cnt[1] * r.cycles + cnt[2] * r.iterations for r in reps)
+
+    # roofline of the dominant kernel: fine-level smoother SpMV (DIA, 7 diagonals)
+    info = dev.info()
+    nh = info["n_hier"]
+    levels = []
+    for k in range(nh):
+        lv = []
+        for l in range(L.irkdev_num_levels(dev._h, k)):
+            a, b_, c_, d_, f_ = (C.c_int() for _ in range(5))
+            _abi.check(L.irkdev_level_info(dev._h, k, l, C.byref(a), C.byref(b_), C.byref(c_),
+                                           C.byref(d_), C.byref(f_)))
+            lv.append((a.value, b_.value, c_.value, d_.value))
+        levels.append(lv)
+    kms = C.c_double()
+    _abi.check(L.irkdev_time_kernel(dev._h, 1, 200, C.byref(kms)))
+    nd = 7
+    # algorithmic bytes of one smoother launch: 7 diagonals of values,
+    # x, r, wd read once, y written once
+    k_bytes = 8 * nd * n + 4 * 8 * n
+    pk = peaks()
+    hbm_peak = pk.get("hbm_gbs", 6650.0)
+    k_gbs = k_bytes / (kms.value * 1e-3) / 1e9
+    # whole-solve byte model on the actual hierarchies and iterations
+    nnz_mk = prob.M.nnz
+    model = [solve_bytes(info, levels, (r.iterations, r.n_reorth, r.cycles), n, S, nnz_mk)[0]
+             for r in reps]
+    solve_gbs = sum(model) / (ms / 1e3) / 1e9 / 1.0
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded u0 noise, BASELINE configs[1])",
+        "config": config({"parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                          "gmres_iterations": its, "reorth_passes": [r.n_reorth for r in reps],
+                          "restart_cycles": [r.cycles for r in reps],
+                          "true_rel_residual": [r.true_rel_residual for r in reps],
+                          "launches_per_iteration": cnt[2], "setup_seconds": setup_s,
+                          "hierarchy_sizes": [[x[0] for x in lv] for lv in levels]}),
+        "e2e": {"value": world * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 4 * 8 + 8 * 501,
+                "wall_seconds": wall_e2e},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": "fine-level Jacobi smoother SpMV (DIA, k_spmv_dia)",
+                     "achieved": k_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": k_gbs / hbm_peak,
+                     "traffic": None, "bytes_per_launch": k_bytes,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in pk
+                     else "fallback 6650 GB/s (B200_PROFILING.md)"},
+        "solve_roofline": {"model_bytes_per_solve": sum(model) / len(model),
+                           "achieved_gbs": solve_gbs, "peak_gbs": hbm_peak,
+                           "frac": solve_gbs / hbm_peak,
+                           "definition": "SURVEY.md §8(d) per-kernel byte model on the actual "
+                                         "hierarchies and iteration counts / measured solve time"},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            total, rits = run_reference_steps(2, 0)
+            line["cpu_baseline"] = {
+                "value": 2 / total, "unit": UNIT, "cores": cpu_threads(), "kind": "reference",
+                "sample": "2 C2 timesteps of the reference irk_step (irkprec compiled from its "
+                          "own sources, OpenMP on all host threads, GMRES(50) wrapper), setup "
+                          f"excluded; reference iterations {rits}"}
+        except Exception as e:  # reported, not fatal
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": cpu_threads(),
+                                    "kind": "reference", "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -150,6 +150,12 @@ int irkdev_time_kernel(irkdev* d, int which, int reps, double* ms);
 /* Kernel launches per GMRES iteration in the captured graph body, and the
  * graph mode (1 conditional WHILE nodes, 0 host-driven). */
 int irkdev_graph_info(const irkdev* d, int* launches_per_iteration, int* graph_mode);
+/* Kernel launches of the captured step graph per phase: [0] once per step
+ * before the GMRES loop, [1] per restart cycle, [2] per Arnoldi iteration,
+ * [3] once per step after the loop. */
+int irkdev_launch_counts(const irkdev* d, int* counts4);
+/* The solver's CUDA stream (cudaStream_t) for event timing by the caller. */
+int irkdev_stream(const irkdev* d, void** stream);
 
 #ifdef __cplusplus
 }

@@ -366,6 +366,8 @@ class BlockPreconditioner:
                  hierarchies=None, device: int = 0):
         self.M, self.F, self.coeff, self.ht = M, F, coeff, ht
         self.amg_params = amg_params or AmgParams()
+        self._hiers = hierarchies
+        self._device = device
         s = coeff.Atilde.shape[0]
         A = table.A if table is not None else coeff.Atilde
         b = table.b if table is not None else np.zeros(s)
@@ -393,8 +395,9 @@ class BlockPreconditioner:
         """Rebuild the device handle with the stage operator of `table`."""
         if np.array_equal(self._dev.A, table.A) and np.array_equal(self._dev.b, table.b):
             return
+        self._dev = None  # release the old handle before allocating the new one
         self._dev = _Device(self.M, self.F, table.A, table.b, self.coeff, self.ht,
-                            self.amg_params)
+                            self.amg_params, self._hiers, self._device)
 
 
 class StageOperator:

@@ -84,6 +84,8 @@ _SIGS = {
     "irkdev_dot": (C.c_int, [V, dptr, dptr, C.c_longlong, dptr]),
     "irkdev_time_kernel": (C.c_int, [V, C.c_int, C.c_int, dptr]),
     "irkdev_graph_info": (C.c_int, [V, iptr, iptr]),
+    "irkdev_launch_counts": (C.c_int, [V, iptr]),
+    "irkdev_stream": (C.c_int, [V, C.POINTER(C.c_void_p)]),
 }
 
 _lib = None
@@ -110,7 +112,8 @@ def exported_symbols() -> list[str]:
     """Every function name irkdev.h declares."""
     import re
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"\b(irk(?:dev)?_[a-z_0-9]+)\s*\(", text)))
+    decl = r"^(?:int|void|const char\s*\*|const double\s*\*)\s*\**\s*(irk(?:dev)?_[a-z_0-9]+)\s*\("
+    return sorted(set(re.findall(decl, text, re.MULTILINE)))
 
 
 class SingularError(RuntimeError):

@@ -354,6 +354,17 @@ int irkdev_time_kernel(irkdev* d, int which, int reps, double* ms) {
     return guard([&] { *ms = d->s->time_kernel(which, reps); });
 }
 
+int irkdev_launch_counts(const irkdev* d, int* c) {
+    return guard([&] {
+        const auto& v = d->s->launch_counts();
+        for (int i = 0; i < 4; ++i) c[i] = v[i];
+    });
+}
+
+int irkdev_stream(const irkdev* d, void** stream) {
+    return guard([&] { *stream = static_cast<void*>(d->s->stream()); });
+}
+
 int irkdev_graph_info(const irkdev* d, int* lpi, int* mode) {
     return guard([&] {
         if (lpi) *lpi = d->s->launches_per_iteration();

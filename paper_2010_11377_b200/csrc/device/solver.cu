@@ -452,10 +452,31 @@ cudaGraph_t add_while(cudaStream_t st, cudaGraphConditionalHandle* h, unsigned d
     return p.conditional.phGraph_out[0];
 }
 
+// Kernel nodes of a graph (memset / conditional nodes excluded).
 int count_nodes(cudaGraph_t g) {
     size_t n = 0;
     cudaGraphGetNodes(g, nullptr, &n);
-    return static_cast<int>(n);
+    std::vector<cudaGraphNode_t> nodes(n);
+    if (n) cudaGraphGetNodes(g, nodes.data(), &n);
+    int k = 0;
+    for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType t;
+        cudaGraphNodeGetType(nd, &t);
+        if (t == cudaGraphNodeTypeKernel) ++k;
+    }
+    return k;
+}
+
+// Kernel launches recorded by fn, counted from a throw-away capture.
+template <class F>
+int count_launches(cudaStream_t st, F&& fn) {
+    cudaGraph_t g = nullptr;
+    IRK_CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    fn();
+    IRK_CUDA_CHECK(cudaStreamEndCapture(st, &g));
+    const int k = count_nodes(g);
+    cudaGraphDestroy(g);
+    return k;
 }
 
 }  // namespace
@@ -484,6 +505,10 @@ void DeviceSolver::build_graph(bool lift, int restart, int max_iter, double rtol
     };
     auto post = [&]() { dev::irk_update(u_, x_, hb_.data(), n_, s_, unext_, st_); };
 
+    launch_counts_[0] = count_launches(st_, pre);
+    launch_counts_[1] = count_launches(st_, [&] { cycle_begin(); cycle_end(); });
+    launch_counts_[2] = count_launches(st_, [&] { record_iteration(); });
+    launch_counts_[3] = count_launches(st_, post);
     if (use_cond) {
         cudaStream_t s2 = nullptr, s3 = nullptr;
         IRK_CUDA_CHECK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));

@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <memory>
 #include <vector>
 
@@ -99,6 +100,7 @@ public:
     // 1 fine-level smoother SpMV, 2 preconditioner apply, 3 V-cycle.
     double time_kernel(int which, int reps);
     int launches_per_iteration() const { return launches_per_iter_; }
+    const std::array<int, 4>& launch_counts() const { return launch_counts_; }
     int graph_mode() const { return graph_mode_; }
 
 private:
@@ -148,6 +150,7 @@ private:
     int g_restart_ = -1, g_iter_ = -1;
     double g_rtol_ = -1.0;
     int launches_per_iter_ = 0;
+    std::array<int, 4> launch_counts_{};
     int counting_ = 0;
 };
 
