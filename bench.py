@@ -222,7 +222,10 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
+    return our_arm(args)
 
+
+def our_arm(args):
     global CELLS
     CELLS = args.cells
     import torch
