@@ -184,8 +184,8 @@ class AmgHierarchy:
         self._h = handle
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _abi.lib().irk_hierarchy_free(self._h)
+        if getattr(self, "_h", None) and _abi is not None and _abi._lib is not None:
+            _abi._lib.irk_hierarchy_free(self._h)
             self._h = None
 
     def n_levels(self) -> int:
@@ -245,8 +245,8 @@ class ProblemSetup:
         self.sys = LinearParabolicSystem(self.M, self.F, self.f_lift)
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _abi.lib().irk_problem_free(self._h)
+        if getattr(self, "_h", None) and _abi is not None and _abi._lib is not None:
+            _abi._lib.irk_problem_free(self._h)
             self._h = None
 
     def initial(self, noise: float = 0.0, seed: int = 1) -> np.ndarray:
@@ -335,8 +335,8 @@ class _Device:
         self._h = h
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _abi.lib().irkdev_destroy(self._h)
+        if getattr(self, "_h", None) and _abi is not None and _abi._lib is not None:
+            _abi._lib.irkdev_destroy(self._h)
             self._h = None
 
     def info(self):
