@@ -21,99 +21,148 @@ struct Offs {
 inline int blocks_for(long long n, int t) { return static_cast<int>((n + t - 1) / t); }
 
 // ------------------------------------------------------------------ SpMV
+// Value fetch: fp64, or a code into the exact dictionary (u8: shared-memory
+// copy; u16: global, L1-resident).
+template <int VF>
+__device__ __forceinline__ double vfetch(const void* v, long long k, const double* tab) {
+    if constexpr (VF == kF64) {
+        return __ldg(static_cast<const double*>(v) + k);
+    } else if constexpr (VF == kU8) {
+        return tab[__ldg(static_cast<const unsigned char*>(v) + k)];
+    } else {
+        return __ldg(tab + __ldg(static_cast<const unsigned short*>(v) + k));
+    }
+}
+
+// Shared-memory dictionaries for u8 codes (256 entries each).
+template <int VF>
+__device__ __forceinline__ const double* load_tab(const Mat& A, double* s_tab, double* s_wd) {
+    if constexpr (VF == kU8) {
+        for (int i = threadIdx.x; i < A.ntab; i += blockDim.x) {
+            s_tab[i] = A.tab[i];
+            if (A.wdtab) s_wd[i] = A.wdtab[i];
+        }
+        __syncthreads();
+        return s_tab;
+    } else {
+        return A.tab;
+    }
+}
+
 template <int XM, int EPI>
-__device__ __forceinline__ double spmv_epilogue(double s, int i, const SpmvArgs& a,
-                                                const double* r) {
+__device__ __forceinline__ double spmv_epilogue(double s, double wdi, int i, const SpmvArgs& a,
+                                                const double* r, const double* x) {
     if (EPI == kEPlain) return s;
     if (EPI == kEResid) return r[i] - s;
-    if (EPI == kESmooth) return a.x.get()[i] + a.wd[i] * (r[i] - s);
+    if (EPI == kESmooth) return x[i] + wdi * (r[i] - s);
     // kEProlong: base + correction (amg.cpp:163-164)
-    const double zb = a.zb ? a.zb[i] : a.wd[i] * r[i];
+    const double zb = a.zb ? a.zb[i] : wdi * r[i];
     return zb + s;
 }
 
-// DIA: one thread per row, diagonals visited in ascending offset order, i.e.
-// CSR column order, so the row sum is the reference's sequential sum (padding
-// entries are stored zeros and contribute exact zeros).
-template <int XM, int EPI>
-__global__ void __launch_bounds__(256) k_spmv_dia(int n, int nd, Offs off,
-                                                  const double* __restrict__ val,
-                                                  SpmvArgs a) {
+// DIA: one thread per row, diagonals in ascending offset (= CSR column)
+// order, so the row sum is the reference's sequential sum; padding entries
+// are stored zeros and contribute exact zeros.  WDT=1: omega*D^-1 comes from
+// the dictionary of the diagonal's code (no wd array traffic).
+template <int XM, int EPI, int VF, int WDT>
+__global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
+    __shared__ double s_tab[VF == kU8 ? 256 : 1];
+    __shared__ double s_wd[VF == kU8 ? 256 : 1];
+    const double* tab = load_tab<VF>(A, s_tab, s_wd);
+    const int n = A.rows;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double* r = a.r.base ? a.r.get() : nullptr;
     const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
     const double* __restrict__ wd = a.wd;
+    const unsigned char* dcode = nullptr;
+    if constexpr (WDT == 1)
+        dcode = static_cast<const unsigned char*>(A.val) + static_cast<long long>(A.diag0) * n;
     double s = 0.0;
 #pragma unroll 4
-    for (int d = 0; d < nd; ++d) {
-        const int c = i + off.o[d];
+    for (int d = 0; d < A.nd; ++d) {
+        const int c = i + A.off[d];
         if (c >= 0 && c < n) {
-            const double xv = XM == kXWdR ? wd[c] * r[c] : x[c];
-            s += __ldg(val + static_cast<long long>(d) * n + i) * xv;
+            double xv;
+            if constexpr (XM == kXWdR) {
+                const double wdc = WDT == 1 ? s_wd[__ldg(dcode + c)] : wd[c];
+                xv = wdc * r[c];
+            } else {
+                xv = x[c];
+            }
+            s += vfetch<VF>(A.val, static_cast<long long>(d) * n + i, tab) * xv;
         }
     }
-    a.y.get()[i] = spmv_epilogue<XM, EPI>(s, i, a, r);
+    double wdi = 0.0;
+    if (EPI == kESmooth || (EPI == kEProlong && !a.zb))
+        wdi = WDT == 1 ? s_wd[__ldg(dcode + i)] : wd[i];
+    a.y.get()[i] = spmv_epilogue<XM, EPI>(s, wdi, i, a, r, x);
 }
 
-// CSR with shared-memory staging: the CTA streams its rows' nonzeros
-// coalesced, forms the products val*x into shared memory, and each thread then
-// adds its own row's products in column order -- coalesced loads with the
-// reference's exact per-row summation order.
-constexpr int kCsrRows = 128;
-constexpr int kCsrTile = 1024;
-
-template <int XM, int EPI>
-__global__ void __launch_bounds__(kCsrRows) k_spmv_csr(int rows, const int* __restrict__ ptr,
-                                                       const int* __restrict__ idx,
-                                                       const double* __restrict__ val,
-                                                       SpmvArgs a) {
-    __shared__ double prod[kCsrTile];
-    __shared__ int rp[kCsrRows + 1];
-    const int r0 = blockIdx.x * kCsrRows;
-    const int nr = min(kCsrRows, rows - r0);
-    const int t = threadIdx.x;
-    for (int q = t; q <= nr; q += kCsrRows) rp[q] = ptr[r0 + q];
-    __syncthreads();
+// SELL-32: one warp per 32-row slice, entries column-major inside the slice,
+// sequential per-row sums (same order as CSR; padding adds exact zeros).
+template <int XM, int EPI, int VF>
+__global__ void __launch_bounds__(256) k_spmv_sell(Mat A, SpmvArgs a) {
+    __shared__ double s_tab[VF == kU8 ? 256 : 1];
+    __shared__ double s_wd[1];
+    const double* tab = load_tab<VF>(A, s_tab, s_wd);
+    const int slice = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int nslices = (A.rows + 31) >> 5;
+    if (slice >= nslices) return;
     const double* r = a.r.base ? a.r.get() : nullptr;
-    const double* x = a.x.base ? a.x.get() : nullptr;
-    const int base = rp[0], end = rp[nr];
-    const int lo = t < nr ? rp[t] : 0, hi = t < nr ? rp[t + 1] : 0;
+    const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
+    const double* __restrict__ wd = a.wd;
+    const int base = __ldg(A.sptr + slice);
+    const int len = (__ldg(A.sptr + slice + 1) - base) >> 5;
+    const int* __restrict__ idx = A.idx + base + lane;
     double s = 0.0;
-    for (int ts = base; ts < end; ts += kCsrTile) {
-        const int te = min(ts + kCsrTile, end);
-        for (int k = ts + t; k < te; k += kCsrRows) {
-            const int c = idx[k];
-            const double xv = XM == kXWdR ? a.wd[c] * r[c] : x[c];
-            prod[k - ts] = val[k] * xv;
-        }
-        __syncthreads();
-        const int a0 = max(lo, ts), a1 = min(hi, te);
-        for (int k = a0; k < a1; ++k) s += prod[k - ts];
-        __syncthreads();
+#pragma unroll 4
+    for (int k = 0; k < len; ++k) {
+        const int c = __ldg(idx + k * 32);
+        const double xv = XM == kXWdR ? wd[c] * r[c] : x[c];
+        s += vfetch<VF>(A.val, base + k * 32 + lane, tab) * xv;
     }
-    if (t < nr) a.y.get()[r0 + t] = spmv_epilogue<XM, EPI>(s, r0 + t, a, r);
+    const int row = slice * 32 + lane;
+    if (row >= A.rows) return;
+    double wdi = 0.0;
+    if (EPI == kESmooth || (EPI == kEProlong && !a.zb)) wdi = wd[row];
+    a.y.get()[row] = spmv_epilogue<XM, EPI>(s, wdi, row, a, r, x);
+}
+
+template <int XM, int EPI, int VF>
+void launch_spmv_vf(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
+    if (A.fmt == kDia) {
+        if (VF == kU8 && A.wdtab && A.diag0 >= 0)
+            k_spmv_dia<XM, EPI, VF, 1><<<blocks_for(A.rows, 256), 256, 0, st>>>(A, a);
+        else
+            k_spmv_dia<XM, EPI, VF, 0><<<blocks_for(A.rows, 256), 256, 0, st>>>(A, a);
+    } else {
+        const int nslices = (A.rows + 31) / 32;
+        k_spmv_sell<XM, EPI, VF><<<blocks_for(static_cast<long long>(nslices) * 32, 256), 256, 0, st>>>(A, a);
+    }
 }
 
 template <int XM, int EPI>
 void launch_spmv(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
     if (A.rows == 0) return;
-    if (A.fmt == 1) {
-        Offs o;
-        for (int d = 0; d < kMaxDiags; ++d) o.o[d] = A.off[d];
-        k_spmv_dia<XM, EPI><<<blocks_for(A.rows, 256), 256, 0, st>>>(A.rows, A.nd, o, A.val, a);
-    } else {
-        k_spmv_csr<XM, EPI><<<blocks_for(A.rows, kCsrRows), kCsrRows, 0, st>>>(A.rows, A.ptr, A.idx,
-                                                                              A.val, a);
+    switch (A.vf) {
+    case kU8: launch_spmv_vf<XM, EPI, kU8>(A, a, st); break;
+    case kU16: launch_spmv_vf<XM, EPI, kU16>(A, a, st); break;
+    default: launch_spmv_vf<XM, EPI, kF64>(A, a, st); break;
     }
 }
 
 // ------------------------------------------------------------------ stage op
-template <int S>
-__global__ void __launch_bounds__(256) k_stage_op_dia(int n, int nd, Offs off,
-                                                      const double* __restrict__ mv,
-                                                      const double* __restrict__ kv,
-                                                      StageCoef cf, VecRef zr, VecRef yr) {
+template <int S, int VF>
+__global__ void __launch_bounds__(256) k_stage_op_dia(Mat M, Mat K, StageCoef cf, VecRef zr,
+                                                      VecRef yr) {
+    __shared__ double s_tm[VF == kU8 ? 256 : 1];
+    __shared__ double s_tk[VF == kU8 ? 256 : 1];
+    __shared__ double s_dummy[1];
+    const double* tm = load_tab<VF>(M, s_tm, s_dummy);
+    const double* tk = load_tab<VF>(K, s_tk, s_dummy);
+    const int n = M.rows;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double* __restrict__ z = zr.get();
@@ -121,11 +170,12 @@ __global__ void __launch_bounds__(256) k_stage_op_dia(int n, int nd, Offs off,
     double fm[S], fk[S];
 #pragma unroll
     for (int j = 0; j < S; ++j) fm[j] = fk[j] = 0.0;
-    for (int d = 0; d < nd; ++d) {
-        const int c = i + off.o[d];
+    for (int d = 0; d < M.nd; ++d) {
+        const int c = i + M.off[d];
         if (c >= 0 && c < n) {
-            const double m = __ldg(mv + static_cast<long long>(d) * n + i);
-            const double k = __ldg(kv + static_cast<long long>(d) * n + i);
+            const long long e = static_cast<long long>(d) * n + i;
+            const double m = vfetch<VF>(M.val, e, tm);
+            const double k = vfetch<VF>(K.val, e, tk);
 #pragma unroll
             for (int j = 0; j < S; ++j) {
                 const double x = z[static_cast<long long>(j) * n + c];
@@ -145,21 +195,26 @@ __global__ void __launch_bounds__(256) k_stage_op_dia(int n, int nd, Offs off,
 }
 
 // ------------------------------------------------------------------ sweep
-__global__ void __launch_bounds__(256) k_sweep_dia(int n, int nd, Offs off,
-                                                   const double* __restrict__ kv, VecRef wr,
-                                                   VecRef vr, SweepTerms t,
+template <int VF>
+__global__ void __launch_bounds__(256) k_sweep_dia(Mat K, VecRef wr, VecRef vr, SweepTerms t,
                                                    double* __restrict__ store, VecRef outr) {
+    __shared__ double s_tk[VF == kU8 ? 256 : 1];
+    __shared__ double s_dummy[1];
+    const double* tk = load_tab<VF>(K, s_tk, s_dummy);
+    const int n = K.rows;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double* __restrict__ w = wr.get();
     double f = 0.0;
-    for (int d = 0; d < nd; ++d) {
-        const int c = i + off.o[d];
-        if (c >= 0 && c < n) f += __ldg(kv + static_cast<long long>(d) * n + i) * w[c];
+    for (int d = 0; d < K.nd; ++d) {
+        const int c = i + K.off[d];
+        if (c >= 0 && c < n) f += vfetch<VF>(K.val, static_cast<long long>(d) * n + i, tk) * w[c];
     }
     if (store) store[i] = f;
     double acc = vr.get()[i];
-    for (int q = 0; q < t.nt; ++q) acc += t.coef[q] * (t.buf[q] ? t.buf[q][i] : f);
+#pragma unroll
+    for (int q = 0; q < kMaxStages; ++q)
+        if (q < t.nt) acc += t.coef[q] * (t.buf[q] ? t.buf[q][i] : f);
     outr.get()[i] = acc;
 }
 
@@ -167,7 +222,9 @@ __global__ void k_combine(int n, VecRef vr, SweepTerms t, VecRef outr) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double acc = vr.get()[i];
-    for (int q = 0; q < t.nt; ++q) acc += t.coef[q] * t.buf[q][i];
+#pragma unroll
+    for (int q = 0; q < kMaxStages; ++q)
+        if (q < t.nt) acc += t.coef[q] * t.buf[q][i];
     outr.get()[i] = acc;
 }
 
@@ -201,7 +258,9 @@ __global__ void k_stage_rhs(int n, int s, const double* __restrict__ ku,
     if (i >= n) return;
     double f = ku[i];
     if (lift) f = f + lift[i];
-    for (int q = 0; q < s; ++q) b[static_cast<long long>(q) * n + i] = -f;
+#pragma unroll
+    for (int q = 0; q < kMaxStages; ++q)
+        if (q < s) b[static_cast<long long>(q) * n + i] = -f;
 }
 
 struct HB {
@@ -213,7 +272,9 @@ __global__ void k_irk_update(int n, int s, const double* __restrict__ u,
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double acc = u[i];
-    for (int q = 0; q < s; ++q) acc = acc + hb.v[q] * x[static_cast<long long>(q) * n + i];
+#pragma unroll
+    for (int q = 0; q < kMaxStages; ++q)
+        if (q < s) acc = acc + hb.v[q] * x[static_cast<long long>(q) * n + i];
     un[i] = acc;
 }
 
@@ -654,24 +715,33 @@ void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st) 
 
 void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecRef y, int n,
                   cudaStream_t st) {
-    Offs o;
-    for (int d = 0; d < kMaxDiags; ++d) o.o[d] = M.off[d];
     const int nb = blocks_for(n, 256);
+    if (M.vf != K.vf || (M.vf != kF64 && M.vf != kU8))
+        throw InvalidArgument("stage_op: M and K must share a value format (f64 or u8)");
+    const bool u8 = M.vf == kU8;
     switch (c.s) {
-#define IRK_OP_CASE(S) \
-    case S: k_stage_op_dia<S><<<nb, 256, 0, st>>>(n, M.nd, o, M.val, K.val, c, z, y); break;
+#define IRK_OP_CASE(S)                                                             \
+    case S:                                                                        \
+        if (u8)                                                                    \
+            k_stage_op_dia<S, kU8><<<nb, 256, 0, st>>>(M, K, c, z, y);             \
+        else                                                                       \
+            k_stage_op_dia<S, kF64><<<nb, 256, 0, st>>>(M, K, c, z, y);            \
+        break;
         IRK_OP_CASE(1) IRK_OP_CASE(2) IRK_OP_CASE(3) IRK_OP_CASE(4) IRK_OP_CASE(5)
         IRK_OP_CASE(6) IRK_OP_CASE(7)
 #undef IRK_OP_CASE
     default: throw InvalidArgument("stage_op: s out of range");
     }
+    (void)n;
 }
 
 void sweep_dia(const Mat& K, VecRef w, VecRef v, const SweepTerms& t, double* store, VecRef out,
                int n, cudaStream_t st) {
-    Offs o;
-    for (int d = 0; d < kMaxDiags; ++d) o.o[d] = K.off[d];
-    k_sweep_dia<<<blocks_for(n, 256), 256, 0, st>>>(n, K.nd, o, K.val, w, v, t, store, out);
+    switch (K.vf) {
+    case kU8: k_sweep_dia<kU8><<<blocks_for(n, 256), 256, 0, st>>>(K, w, v, t, store, out); break;
+    case kU16: k_sweep_dia<kU16><<<blocks_for(n, 256), 256, 0, st>>>(K, w, v, t, store, out); break;
+    default: k_sweep_dia<kF64><<<blocks_for(n, 256), 256, 0, st>>>(K, w, v, t, store, out); break;
+    }
 }
 
 void combine(VecRef v, const SweepTerms& t, VecRef out, int n, cudaStream_t st) {

@@ -11,19 +11,38 @@ namespace dev {
 
 constexpr int kMaxDiags = 16;
 
-// Device matrix: either DIA ("stencil": a few constant diagonals, values
-// stored diagonal-major so a thread-per-row sweep is fully coalesced and no
-// column index is read) or CSR.  DIA is chosen at upload when the pattern is
-// a small set of diagonals with little padding -- true for the fine-level
-// FE operators, M, K and every fine-level A of the hierarchies.
+// Device matrix formats.  Both keep the reference's per-row summation order
+// (column-ascending, sequential), so results are bit-identical to a CSR row
+// sum:
+//   DIA  -- a few constant diagonals (the fine-level FE stencils: M, K and
+//           every fine-level A); entries stored diagonal-major, no indices.
+//   SELL -- SELL-32: slices of 32 consecutive rows padded to the slice's
+//           longest row, stored column-major inside the slice, so a warp
+//           streams one slice fully coalesced with one thread per row
+//           (P, R and the Galerkin coarse operators).
+// Values are fp64 or, when the matrix has few distinct values, uint8 /
+// uint16 codes into an exact fp64 dictionary (lossless; e.g. 3 distinct
+// values in the fine-level stencils, 14 in the fine prolongator).
+enum MatFmt { kSell = 0, kDia = 1 };
+enum ValFmt { kF64 = 0, kU8 = 1, kU16 = 2 };
+
 struct Mat {
-    int fmt = 0;  // 0 CSR, 1 DIA
+    int fmt = kSell;
+    int vf = kF64;
     int rows = 0, cols = 0, nnz = 0;
-    const int* ptr = nullptr;
-    const int* idx = nullptr;
-    const double* val = nullptr;  // CSR: nnz; DIA: nd * rows
+    // SELL-32
+    const int* sptr = nullptr;  // slice offsets (entries), rows/32 + 1
+    const int* idx = nullptr;   // column per stored entry
+    // values (both formats): f64 / u8 / u16 per stored entry
+    const void* val = nullptr;
+    const double* tab = nullptr;  // code dictionary (vf != kF64)
+    int ntab = 0;
+    // DIA
     int nd = 0;
     int off[kMaxDiags] = {};
+    int diag0 = -1;                 // slot of offset 0
+    const double* wdtab = nullptr;  // omega / diagonal value per code (DIA, u8)
+    size_t bytes = 0;               // device bytes of the stored operator
 };
 
 // x operand of an SpMV: either a plain vector or the implicit Jacobi

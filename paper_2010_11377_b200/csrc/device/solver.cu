@@ -64,8 +64,82 @@ double* DeviceSolver::alloc(size_t count) {
     return bufs_.back().as<double>();
 }
 
-// DIA when the pattern is <= 16 diagonals with <= 15% padding; else CSR.
-dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia) {
+namespace {
+
+// Exact value dictionary: distinct fp64 bit patterns (so +0.0 / -0.0 stay
+// distinct and decoding reproduces every stored bit).
+struct Dict {
+    int vf = dev::kF64;
+    std::vector<double> tab;
+    std::vector<unsigned char> c8;
+    std::vector<unsigned short> c16;
+};
+
+Dict encode(const std::vector<double>& v) {
+    Dict d;
+    std::vector<uint64_t> bits(v.size());
+    std::memcpy(bits.data(), v.data(), v.size() * sizeof(double));
+    std::vector<uint64_t> u = bits;
+    std::sort(u.begin(), u.end());
+    u.erase(std::unique(u.begin(), u.end()), u.end());
+    if (u.size() > 65536) return d;
+    d.tab.resize(u.size());
+    std::memcpy(d.tab.data(), u.data(), u.size() * sizeof(double));
+    auto code = [&](uint64_t b) {
+        return static_cast<size_t>(std::lower_bound(u.begin(), u.end(), b) - u.begin());
+    };
+    if (u.size() <= 256) {
+        d.vf = dev::kU8;
+        d.c8.resize(v.size());
+        for (size_t i = 0; i < v.size(); ++i) d.c8[i] = static_cast<unsigned char>(code(bits[i]));
+    } else {
+        d.vf = dev::kU16;
+        d.c16.resize(v.size());
+        for (size_t i = 0; i < v.size(); ++i) d.c16[i] = static_cast<unsigned short>(code(bits[i]));
+    }
+    return d;
+}
+
+}  // namespace
+
+template <class T>
+const T* DeviceSolver::upload_array(const std::vector<T>& h) {
+    bufs_.emplace_back(sizeof(T) * std::max<size_t>(h.size(), 1));
+    T* p = bufs_.back().as<T>();
+    if (!h.empty()) IRK_CUDA_CHECK(cudaMemcpy(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
+    return p;
+}
+
+// Stores the entry values (fp64 or dictionary codes) of an operator.
+void DeviceSolver::upload_values(dev::Mat& m, const std::vector<double>& vals, double omega) {
+    Dict d = compress_values_ ? encode(vals) : Dict{};
+    m.vf = d.vf;
+    if (d.vf == dev::kF64) {
+        m.val = upload_array(vals);
+        m.bytes += vals.size() * sizeof(double);
+        return;
+    }
+    m.tab = upload_array(d.tab);
+    m.ntab = static_cast<int>(d.tab.size());
+    if (d.vf == dev::kU8) {
+        m.val = upload_array(d.c8);
+        m.bytes += d.c8.size();
+    } else {
+        m.val = upload_array(d.c16);
+        m.bytes += 2 * d.c16.size();
+    }
+    if (omega > 0.0 && m.fmt == dev::kDia && d.vf == dev::kU8) {
+        // omega * (1 / a_ii) per diagonal code: exactly the host's wd
+        // (jacobi_weight * inv_diag[i], amg.cpp:100-113, 123).
+        std::vector<double> wd(d.tab.size());
+        for (size_t c = 0; c < d.tab.size(); ++c) wd[c] = omega * (1.0 / d.tab[c]);
+        m.wdtab = upload_array(wd);
+    }
+}
+
+// DIA when the pattern is <= 16 diagonals with <= 15% padding; else SELL-32.
+// `omega` > 0 requests the omega/diag dictionary (hierarchy operators).
+dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
     dev::Mat m;
     m.rows = A.rows;
     m.cols = A.cols;
@@ -96,28 +170,48 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia) {
                                                offs.begin());
                 v[static_cast<size_t>(d) * A.rows + i] = A.val[k];
             }
-        double* dv = alloc(v.size());
-        IRK_CUDA_CHECK(cudaMemcpy(dv, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
-        m.fmt = 1;
+        m.fmt = dev::kDia;
         m.nd = nd;
-        for (int d = 0; d < nd; ++d) m.off[d] = offs[d];
-        m.val = dv;
+        for (int d = 0; d < nd; ++d) {
+            m.off[d] = offs[d];
+            if (offs[d] == 0) m.diag0 = d;
+        }
+        upload_values(m, v, omega);
         return m;
     }
-    bufs_.emplace_back(sizeof(int) * (A.rows + 1));
-    int* dp = bufs_.back().as<int>();
-    bufs_.emplace_back(sizeof(int) * std::max(1, A.nnz()));
-    int* di = bufs_.back().as<int>();
-    double* dv = alloc(A.nnz());
-    IRK_CUDA_CHECK(cudaMemcpy(dp, A.ptr.data(), sizeof(int) * (A.rows + 1), cudaMemcpyHostToDevice));
-    if (A.nnz()) {
-        IRK_CUDA_CHECK(cudaMemcpy(di, A.idx.data(), sizeof(int) * A.nnz(), cudaMemcpyHostToDevice));
-        IRK_CUDA_CHECK(cudaMemcpy(dv, A.val.data(), sizeof(double) * A.nnz(), cudaMemcpyHostToDevice));
+    // SELL-32: slice = 32 consecutive rows, padded to the slice's longest row;
+    // padding entries repeat the row's last column with a zero value.
+    const int ns = (A.rows + 31) / 32;
+    std::vector<int> sptr(ns + 1, 0);
+    for (int sl = 0; sl < ns; ++sl) {
+        int len = 0;
+        for (int r = sl * 32; r < std::min(A.rows, sl * 32 + 32); ++r)
+            len = std::max(len, A.ptr[r + 1] - A.ptr[r]);
+        sptr[sl + 1] = sptr[sl] + 32 * len;
     }
-    m.fmt = 0;
-    m.ptr = dp;
-    m.idx = di;
-    m.val = dv;
+    std::vector<int> idx(sptr[ns]);
+    std::vector<double> v(sptr[ns], 0.0);
+    for (int sl = 0; sl < ns; ++sl) {
+        const int len = (sptr[sl + 1] - sptr[sl]) / 32;
+        for (int lane = 0; lane < 32; ++lane) {
+            const int r = sl * 32 + lane;
+            const int lo = r < A.rows ? A.ptr[r] : 0, cnt = r < A.rows ? A.ptr[r + 1] - lo : 0;
+            for (int k = 0; k < len; ++k) {
+                const size_t e = static_cast<size_t>(sptr[sl]) + k * 32 + lane;
+                if (k < cnt) {
+                    idx[e] = A.idx[lo + k];
+                    v[e] = A.val[lo + k];
+                } else {
+                    idx[e] = cnt > 0 ? A.idx[lo + cnt - 1] : 0;
+                }
+            }
+        }
+    }
+    m.fmt = dev::kSell;
+    m.sptr = upload_array(sptr);
+    m.idx = upload_array(idx);
+    m.bytes += sizeof(int) * (sptr.size() + idx.size());
+    upload_values(m, v, omega);
     return m;
 }
 
@@ -126,6 +220,7 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
                            Structure structure, double ht, const AmgParams& amg,
                            std::vector<Hierarchy> hiers, int device)
     : s_(s), device_(device), At_(At), structure_(structure), ht_(ht) {
+    compress_values_ = std::getenv("IRK_NO_VALUE_CODES") == nullptr;
     const auto t0 = std::chrono::steady_clock::now();
     check(s >= 1 && s <= dev::kMaxStages, "device solver: s must be in 1..7");
     check(M.rows == M.cols && K.rows == K.cols && M.rows == K.rows,
@@ -154,10 +249,11 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
     check(hiers.size() == distinct.size(), "device solver: hierarchy count mismatch");
     hier_host_ = std::move(hiers);
 
-    M_ = upload(M, true);
-    K_ = upload(K, true);
-    fused_op_ = M_.fmt == 1 && K_.fmt == 1 && M_.nd == K_.nd &&
-                std::equal(M_.off, M_.off + M_.nd, K_.off);
+    M_ = upload(M, true, 0.0);
+    K_ = upload(K, true, 0.0);
+    fused_op_ = M_.fmt == dev::kDia && K_.fmt == dev::kDia && M_.nd == K_.nd &&
+                std::equal(M_.off, M_.off + M_.nd, K_.off) && M_.vf == K_.vf &&
+                (M_.vf == dev::kF64 || M_.vf == dev::kU8);
     coef_.s = s;
     for (int i = 0; i < s * s; ++i) coef_.c[i] = ht * A[i];
     hb_.resize(s);
@@ -171,14 +267,14 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
             const AmgLevel& lev = h.levels[l];
             DevLevel d;
             d.n = lev.A.rows;
-            d.A = upload(lev.A, true);
+            d.A = upload(lev.A, true, h.params.jacobi_weight);
             std::vector<double> wd(d.n);
             for (int i = 0; i < d.n; ++i) wd[i] = h.params.jacobi_weight * lev.inv_diag[i];
             d.wd = alloc(d.n);
             IRK_CUDA_CHECK(cudaMemcpy(d.wd, wd.data(), sizeof(double) * d.n, cudaMemcpyHostToDevice));
             if (l + 1 < L) {
-                d.P = upload(lev.P, false);
-                d.R = upload(lev.R, false);
+                d.P = upload(lev.P, false, 0.0);
+                d.R = upload(lev.R, false, 0.0);
             }
             d.t = alloc(d.n);
             d.u = alloc(d.n);
@@ -324,7 +420,7 @@ void DeviceSolver::record_precond(VecRef v, VecRef w) {
             }
             if (fresh || later) {
                 double* store = later ? fw_ + prev * n : nullptr;
-                if (K_.fmt == 1) {
+                if (K_.fmt == dev::kDia) {
                     dev::sweep_dia(K_, block(w, prev * n), in, t, store, dev::plain(rhs_), n_, st_);
                 } else {
                     dev::SpmvArgs a;

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <cstdint>
 #include <memory>
 #include <vector>
 
@@ -104,7 +105,9 @@ public:
     int graph_mode() const { return graph_mode_; }
 
 private:
-    dev::Mat upload(const Csr& A, bool allow_dia);
+    dev::Mat upload(const Csr& A, bool allow_dia, double omega);
+    void upload_values(dev::Mat& m, const std::vector<double>& vals, double omega);
+    template <class T> const T* upload_array(const std::vector<T>& h);
     double* alloc(size_t count);
     void record_vcycle(int k, dev::VecRef r, dev::VecRef z);
     void record_precond(dev::VecRef v, dev::VecRef w);
@@ -151,7 +154,7 @@ private:
     double g_rtol_ = -1.0;
     int launches_per_iter_ = 0;
     std::array<int, 4> launch_counts_{};
-    int counting_ = 0;
+    bool compress_values_ = true;
 };
 
 }  // namespace irkb
