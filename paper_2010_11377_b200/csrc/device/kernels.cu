@@ -64,7 +64,11 @@ __device__ __forceinline__ double spmv_epilogue(double s, double wdi, int i, con
 // order, so the row sum is the reference's sequential sum; padding entries
 // are stored zeros and contribute exact zeros.  WDT=1: omega*D^-1 comes from
 // the dictionary of the diagonal's code (no wd array traffic).
-template <int XM, int EPI, int VF, int WDT>
+// ND > 0: diagonal count fixed at compile time (fully unrolled, all loads of
+// a row issued together); ND = 0: runtime count.  Neighbour indices are
+// clamped instead of branched on: out-of-range neighbours belong to padding
+// entries whose stored value is exactly zero.
+template <int XM, int EPI, int VF, int WDT, int ND>
 __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
     __shared__ double s_tab[VF == kU8 ? 256 : 1];
     __shared__ double s_wd[VF == kU8 ? 256 : 1];
@@ -78,20 +82,20 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
     const unsigned char* dcode = nullptr;
     if constexpr (WDT == 1)
         dcode = static_cast<const unsigned char*>(A.val) + static_cast<long long>(A.diag0) * n;
+    const int nd = ND > 0 ? ND : A.nd;
     double s = 0.0;
-#pragma unroll 4
-    for (int d = 0; d < A.nd; ++d) {
-        const int c = i + A.off[d];
-        if (c >= 0 && c < n) {
-            double xv;
-            if constexpr (XM == kXWdR) {
-                const double wdc = WDT == 1 ? s_wd[__ldg(dcode + c)] : wd[c];
-                xv = wdc * r[c];
-            } else {
-                xv = x[c];
-            }
-            s += vfetch<VF>(A.val, static_cast<long long>(d) * n + i, tab) * xv;
+#pragma unroll
+    for (int d = 0; d < (ND > 0 ? ND : kMaxDiags); ++d) {
+        if (ND == 0 && d >= nd) break;
+        const int c = min(max(i + A.off[d], 0), n - 1);
+        double xv;
+        if constexpr (XM == kXWdR) {
+            const double wdc = WDT == 1 ? s_wd[__ldg(dcode + c)] : wd[c];
+            xv = wdc * r[c];
+        } else {
+            xv = x[c];
         }
+        s += vfetch<VF>(A.val, static_cast<long long>(d) * n + i, tab) * xv;
     }
     double wdi = 0.0;
     if (EPI == kESmooth || (EPI == kEProlong && !a.zb))
@@ -130,13 +134,80 @@ __global__ void __launch_bounds__(256) k_spmv_sell(Mat A, SpmvArgs a) {
     a.y.get()[row] = spmv_epilogue<XM, EPI>(s, wdi, row, a, r, x);
 }
 
+// CSR-vector: G lanes per row, each lane loading up to 4 entries of a chunk
+// of 4G (all loads of the chunk in flight at once), then every lane adds the
+// chunk's products in column order, reading them with warp shuffles.  The
+// trip count is warp-uniform (max over the warp's rows).
+template <int XM, int EPI, int VF, int G>
+__global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
+    __shared__ double s_tab[VF == kU8 ? 256 : 1];
+    __shared__ double s_wd[1];
+    const double* tab = load_tab<VF>(A, s_tab, s_wd);
+    constexpr int MM = 4;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int row = t / G;
+    const int lane = threadIdx.x % G;
+    const bool live = row < A.rows;
+    const double* r = a.r.base ? a.r.get() : nullptr;
+    const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
+    const double* __restrict__ wd = a.wd;
+    const int lo = live ? __ldg(A.ptr + row) : 0;
+    const int len = live ? __ldg(A.ptr + row + 1) - lo : 0;
+    int chunks = (len + G * MM - 1) / (G * MM);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) chunks = max(chunks, __shfl_xor_sync(0xffffffffu, chunks, o));
+    double s = 0.0;
+    for (int ch = 0; ch < chunks; ++ch) {
+        double p[MM];
+#pragma unroll
+        for (int m = 0; m < MM; ++m) {
+            const int k = ch * G * MM + m * G + lane;
+            p[m] = 0.0;
+            if (k < len) {
+                const int c = __ldg(A.idx + lo + k);
+                const double xv = XM == kXWdR ? wd[c] * r[c] : x[c];
+                p[m] = vfetch<VF>(A.val, lo + k, tab) * xv;
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < MM; ++m)
+#pragma unroll
+            for (int l = 0; l < G; ++l) {
+                const double v = __shfl_sync(0xffffffffu, p[m], l, G);
+                if (ch * G * MM + m * G + l < len) s += v;
+            }
+    }
+    if (!live || lane != 0) return;
+    double wdi = 0.0;
+    if (EPI == kESmooth || (EPI == kEProlong && !a.zb)) wdi = wd[row];
+    a.y.get()[row] = spmv_epilogue<XM, EPI>(s, wdi, row, a, r, x);
+}
+
 template <int XM, int EPI, int VF>
 void launch_spmv_vf(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
     if (A.fmt == kDia) {
-        if (VF == kU8 && A.wdtab && A.diag0 >= 0)
-            k_spmv_dia<XM, EPI, VF, 1><<<blocks_for(A.rows, 256), 256, 0, st>>>(A, a);
-        else
-            k_spmv_dia<XM, EPI, VF, 0><<<blocks_for(A.rows, 256), 256, 0, st>>>(A, a);
+        const int nb = blocks_for(A.rows, 256);
+        const bool wdt = VF == kU8 && A.wdtab && A.diag0 >= 0;
+        if (A.nd == 7) {
+            if (wdt)
+                k_spmv_dia<XM, EPI, VF, 1, 7><<<nb, 256, 0, st>>>(A, a);
+            else
+                k_spmv_dia<XM, EPI, VF, 0, 7><<<nb, 256, 0, st>>>(A, a);
+        } else {
+            if (wdt)
+                k_spmv_dia<XM, EPI, VF, 1, 0><<<nb, 256, 0, st>>>(A, a);
+            else
+                k_spmv_dia<XM, EPI, VF, 0, 0><<<nb, 256, 0, st>>>(A, a);
+        }
+    } else if (A.fmt == kCsrVec) {
+        const int nb = blocks_for(static_cast<long long>(A.rows) * A.lanes, 256);
+        switch (A.lanes) {
+        case 2: k_spmv_csrv<XM, EPI, VF, 2><<<nb, 256, 0, st>>>(A, a); break;
+        case 4: k_spmv_csrv<XM, EPI, VF, 4><<<nb, 256, 0, st>>>(A, a); break;
+        case 8: k_spmv_csrv<XM, EPI, VF, 8><<<nb, 256, 0, st>>>(A, a); break;
+        case 16: k_spmv_csrv<XM, EPI, VF, 16><<<nb, 256, 0, st>>>(A, a); break;
+        default: k_spmv_csrv<XM, EPI, VF, 32><<<nb, 256, 0, st>>>(A, a); break;
+        }
     } else {
         const int nslices = (A.rows + 31) / 32;
         k_spmv_sell<XM, EPI, VF><<<blocks_for(static_cast<long long>(nslices) * 32, 256), 256, 0, st>>>(A, a);
@@ -154,7 +225,7 @@ void launch_spmv(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ stage op
-template <int S, int VF>
+template <int S, int VF, int ND>
 __global__ void __launch_bounds__(256) k_stage_op_dia(Mat M, Mat K, StageCoef cf, VecRef zr,
                                                       VecRef yr) {
     __shared__ double s_tm[VF == kU8 ? 256 : 1];
@@ -170,18 +241,18 @@ __global__ void __launch_bounds__(256) k_stage_op_dia(Mat M, Mat K, StageCoef cf
     double fm[S], fk[S];
 #pragma unroll
     for (int j = 0; j < S; ++j) fm[j] = fk[j] = 0.0;
-    for (int d = 0; d < M.nd; ++d) {
-        const int c = i + M.off[d];
-        if (c >= 0 && c < n) {
-            const long long e = static_cast<long long>(d) * n + i;
-            const double m = vfetch<VF>(M.val, e, tm);
-            const double k = vfetch<VF>(K.val, e, tk);
 #pragma unroll
-            for (int j = 0; j < S; ++j) {
-                const double x = z[static_cast<long long>(j) * n + c];
-                fm[j] += m * x;
-                fk[j] += k * x;
-            }
+    for (int d = 0; d < (ND > 0 ? ND : kMaxDiags); ++d) {
+        if (ND == 0 && d >= M.nd) break;
+        const int c = min(max(i + M.off[d], 0), n - 1);
+        const long long e = static_cast<long long>(d) * n + i;
+        const double m = vfetch<VF>(M.val, e, tm);
+        const double k = vfetch<VF>(K.val, e, tk);
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            const double x = z[static_cast<long long>(j) * n + c];
+            fm[j] += m * x;
+            fk[j] += k * x;
         }
     }
     // y_i = M v_i, then y_i += (ht a_ij) (F v_j) for j = 0..s-1 (stage.cpp:40-43)
@@ -195,7 +266,7 @@ __global__ void __launch_bounds__(256) k_stage_op_dia(Mat M, Mat K, StageCoef cf
 }
 
 // ------------------------------------------------------------------ sweep
-template <int VF>
+template <int VF, int ND>
 __global__ void __launch_bounds__(256) k_sweep_dia(Mat K, VecRef wr, VecRef vr, SweepTerms t,
                                                    double* __restrict__ store, VecRef outr) {
     __shared__ double s_tk[VF == kU8 ? 256 : 1];
@@ -206,9 +277,11 @@ __global__ void __launch_bounds__(256) k_sweep_dia(Mat K, VecRef wr, VecRef vr, 
     if (i >= n) return;
     const double* __restrict__ w = wr.get();
     double f = 0.0;
-    for (int d = 0; d < K.nd; ++d) {
-        const int c = i + K.off[d];
-        if (c >= 0 && c < n) f += vfetch<VF>(K.val, static_cast<long long>(d) * n + i, tk) * w[c];
+#pragma unroll
+    for (int d = 0; d < (ND > 0 ? ND : kMaxDiags); ++d) {
+        if (ND == 0 && d >= K.nd) break;
+        const int c = min(max(i + K.off[d], 0), n - 1);
+        f += vfetch<VF>(K.val, static_cast<long long>(d) * n + i, tk) * w[c];
     }
     if (store) store[i] = f;
     double acc = vr.get()[i];
@@ -722,10 +795,12 @@ void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecR
     switch (c.s) {
 #define IRK_OP_CASE(S)                                                             \
     case S:                                                                        \
-        if (u8)                                                                    \
-            k_stage_op_dia<S, kU8><<<nb, 256, 0, st>>>(M, K, c, z, y);             \
+        if (u8 && M.nd == 7)                                                       \
+            k_stage_op_dia<S, kU8, 7><<<nb, 256, 0, st>>>(M, K, c, z, y);          \
+        else if (u8)                                                               \
+            k_stage_op_dia<S, kU8, 0><<<nb, 256, 0, st>>>(M, K, c, z, y);          \
         else                                                                       \
-            k_stage_op_dia<S, kF64><<<nb, 256, 0, st>>>(M, K, c, z, y);            \
+            k_stage_op_dia<S, kF64, 0><<<nb, 256, 0, st>>>(M, K, c, z, y);         \
         break;
         IRK_OP_CASE(1) IRK_OP_CASE(2) IRK_OP_CASE(3) IRK_OP_CASE(4) IRK_OP_CASE(5)
         IRK_OP_CASE(6) IRK_OP_CASE(7)
@@ -738,9 +813,14 @@ void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecR
 void sweep_dia(const Mat& K, VecRef w, VecRef v, const SweepTerms& t, double* store, VecRef out,
                int n, cudaStream_t st) {
     switch (K.vf) {
-    case kU8: k_sweep_dia<kU8><<<blocks_for(n, 256), 256, 0, st>>>(K, w, v, t, store, out); break;
-    case kU16: k_sweep_dia<kU16><<<blocks_for(n, 256), 256, 0, st>>>(K, w, v, t, store, out); break;
-    default: k_sweep_dia<kF64><<<blocks_for(n, 256), 256, 0, st>>>(K, w, v, t, store, out); break;
+    case kU8:
+        if (K.nd == 7)
+            k_sweep_dia<kU8, 7><<<blocks_for(n, 256), 256, 0, st>>>(K, w, v, t, store, out);
+        else
+            k_sweep_dia<kU8, 0><<<blocks_for(n, 256), 256, 0, st>>>(K, w, v, t, store, out);
+        break;
+    case kU16: k_sweep_dia<kU16, 0><<<blocks_for(n, 256), 256, 0, st>>>(K, w, v, t, store, out); break;
+    default: k_sweep_dia<kF64, 0><<<blocks_for(n, 256), 256, 0, st>>>(K, w, v, t, store, out); break;
     }
 }
 

@@ -19,11 +19,13 @@ constexpr int kMaxDiags = 16;
 //   SELL -- SELL-32: slices of 32 consecutive rows padded to the slice's
 //           longest row, stored column-major inside the slice, so a warp
 //           streams one slice fully coalesced with one thread per row
-//           (P, R and the Galerkin coarse operators).
+//           (short rows: the prolongators).
+//   CSRV -- plain CSR, G lanes per row (long rows: restrictions and the
+//           Galerkin coarse operators).
 // Values are fp64 or, when the matrix has few distinct values, uint8 /
 // uint16 codes into an exact fp64 dictionary (lossless; e.g. 3 distinct
 // values in the fine-level stencils, 14 in the fine prolongator).
-enum MatFmt { kSell = 0, kDia = 1 };
+enum MatFmt { kSell = 0, kDia = 1, kCsrVec = 2 };
 enum ValFmt { kF64 = 0, kU8 = 1, kU16 = 2 };
 
 struct Mat {
@@ -32,7 +34,11 @@ struct Mat {
     int rows = 0, cols = 0, nnz = 0;
     // SELL-32
     const int* sptr = nullptr;  // slice offsets (entries), rows/32 + 1
-    const int* idx = nullptr;   // column per stored entry
+    const int* idx = nullptr;   // column per stored entry (SELL / CSR)
+    // CSR-vector: G lanes per row load the row at once; the row sum is then
+    // accumulated in column order through warp shuffles
+    const int* ptr = nullptr;   // row offsets, rows + 1
+    int lanes = 1;
     // values (both formats): f64 / u8 / u16 per stored entry
     const void* val = nullptr;
     const double* tab = nullptr;  // code dictionary (vf != kF64)

@@ -179,8 +179,22 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
         upload_values(m, v, omega);
         return m;
     }
-    // SELL-32: slice = 32 consecutive rows, padded to the slice's longest row;
-    // padding entries repeat the row's last column with a zero value.
+    // Long rows: CSR-vector with G lanes per row (G ~ average length / 3).
+    const double avg = A.rows ? static_cast<double>(A.nnz()) / A.rows : 0.0;
+    static const int force = std::getenv("IRK_SPARSE_FMT") ? std::atoi(std::getenv("IRK_SPARSE_FMT")) : -1;
+    if ((force < 0 && avg > 4.5) || force == dev::kCsrVec) {
+        int g = 2;
+        while (g < 32 && 3 * g < avg) g *= 2;
+        m.fmt = dev::kCsrVec;
+        m.lanes = g;
+        m.ptr = upload_array(A.ptr);
+        m.idx = upload_array(A.idx);
+        m.bytes += sizeof(int) * (A.ptr.size() + A.idx.size());
+        upload_values(m, A.val, omega);
+        return m;
+    }
+    // Short rows: SELL-32, slice = 32 consecutive rows padded to the slice's
+    // longest row; padding entries repeat the row's last column with a zero.
     const int ns = (A.rows + 31) / 32;
     std::vector<int> sptr(ns + 1, 0);
     for (int sl = 0; sl < ns; ++sl) {
