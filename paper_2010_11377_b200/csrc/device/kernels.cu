@@ -308,7 +308,27 @@ __global__ void k_axpy(int n, double alpha, const double* __restrict__ x, VecRef
     y[i] = y[i] + alpha * x[i];
 }
 
-__global__ void k_dense_mv(int n, const double* __restrict__ A, VecRef rr, VecRef zr) {
+// Coarsest solve z = Ainv r: the CTA stages Ainv (row-major) and r in shared
+// memory with coalesced loads, then each thread forms one row sequentially.
+__global__ void __launch_bounds__(256) k_dense_mv(int n, const double* __restrict__ A, VecRef rr,
+                                                  VecRef zr) {
+    extern __shared__ double sm[];
+    double* sA = sm;
+    double* sr = sm + static_cast<long long>(n) * n;
+    const double* r = rr.get();
+    for (int q = threadIdx.x; q < n * n; q += blockDim.x) sA[q] = A[q];
+    for (int q = threadIdx.x; q < n; q += blockDim.x) sr[q] = r[q];
+    __syncthreads();
+    double* z = zr.get();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double s = 0.0;
+        for (int j = 0; j < n; ++j) s += sA[i * n + j] * sr[j];
+        z[i] = s;
+    }
+}
+
+// Large coarsest level (n*n does not fit shared memory): one thread per row.
+__global__ void k_dense_mv_big(int n, const double* __restrict__ A, VecRef rr, VecRef zr) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double* r = rr.get();
@@ -833,7 +853,11 @@ void axpy(double alpha, const double* x, VecRef y, int n, cudaStream_t st) {
 }
 
 void dense_mv(int n, const double* Ainv, VecRef r, VecRef z, cudaStream_t st) {
-    k_dense_mv<<<blocks_for(n, 128), 128, 0, st>>>(n, Ainv, r, z);
+    const size_t smem = sizeof(double) * (static_cast<size_t>(n) * n + n);
+    if (smem <= 200 * 1024)
+        k_dense_mv<<<1, 256, smem, st>>>(n, Ainv, r, z);
+    else
+        k_dense_mv_big<<<blocks_for(n, 128), 128, 0, st>>>(n, Ainv, r, z);
 }
 
 void wd_times_r(int n, const double* wd, VecRef r, double* z, cudaStream_t st) {
@@ -895,6 +919,7 @@ void dot(const double* x, const double* y, long long n, double* partials, unsign
 }
 
 void set_smem_limits() {
+    cudaFuncSetAttribute(k_dense_mv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const int nv = kMaxRestart + 2;
     cudaFuncSetAttribute(k_gm_blockdot, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(red_smem(nv)));

@@ -182,7 +182,10 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
     // Long rows: CSR-vector with G lanes per row (G ~ average length / 3).
     const double avg = A.rows ? static_cast<double>(A.nnz()) / A.rows : 0.0;
     static const int force = std::getenv("IRK_SPARSE_FMT") ? std::atoi(std::getenv("IRK_SPARSE_FMT")) : -1;
-    if ((force < 0 && avg > 4.5) || force == dev::kCsrVec) {
+    // (SELL wins when there are enough rows to fill the GPU with one thread
+    // per row; small coarse operators need lanes per row to expose
+    // memory-level parallelism.)
+    if ((force < 0 && avg > 4.5 && (A.rows < 65536 || avg > 24.0)) || force == dev::kCsrVec) {
         int g = 2;
         while (g < 32 && 3 * g < avg) g *= 2;
         m.fmt = dev::kCsrVec;
