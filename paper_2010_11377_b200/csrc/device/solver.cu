@@ -139,13 +139,13 @@ void DeviceSolver::upload_values(dev::Mat& m, const std::vector<double>& vals, d
 
 // DIA when the pattern is <= 16 diagonals with <= 15% padding; else SELL-32.
 // `omega` > 0 requests the omega/diag dictionary (hierarchy operators).
-dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
+dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega, bool force_csr) {
     dev::Mat m;
     m.rows = A.rows;
     m.cols = A.cols;
     m.nnz = A.nnz();
     std::vector<int> offs;
-    bool dia = allow_dia && A.rows == A.cols && A.rows > 0;
+    bool dia = allow_dia && !force_csr && A.rows == A.cols && A.rows > 0;
     if (dia) {
         for (int i = 0; i < A.rows && dia; ++i)
             for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
@@ -185,7 +185,7 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
     // (SELL wins when there are enough rows to fill the GPU with one thread
     // per row; small coarse operators need lanes per row to expose
     // memory-level parallelism.)
-    if ((force < 0 && avg > 4.5 && (A.rows < 65536 || avg > 24.0)) || force == dev::kCsrVec) {
+    if (force_csr || (force < 0 && avg > 4.5 && (A.rows < 65536 || avg > 24.0)) || force == dev::kCsrVec) {
         int g = 2;
         while (g < 32 && 3 * g < avg) g *= 2;
         m.fmt = dev::kCsrVec;
@@ -276,22 +276,34 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
     hb_.resize(s);
     for (int i = 0; i < s; ++i) hb_[i] = ht * b[i];
 
+    static const int tail_rows =
+        std::getenv("IRK_TAIL_ROWS") ? std::atoi(std::getenv("IRK_TAIL_ROWS")) : 32768;
     for (const Hierarchy& h : hier_host_) {
         DevHier dh;
         dh.prm = h.params;
         const int L = h.n_levels();
+        // The cluster tail runs levels >= tail (V(1,1) only; <= 8 levels).
+        if (tail_rows > 0 && h.params.pre_sweeps == 1 && h.params.post_sweeps == 1 &&
+            dev::coarse_tail_cluster_size() > 0) {
+            for (int l = 0; l < L; ++l)
+                if (h.levels[l].A.rows <= tail_rows && L - l <= dev::kMaxTailLevels) {
+                    dh.tail = l;
+                    break;
+                }
+        }
         for (int l = 0; l < L; ++l) {
             const AmgLevel& lev = h.levels[l];
+            const bool in_tail = dh.tail >= 0 && l >= dh.tail;
             DevLevel d;
             d.n = lev.A.rows;
-            d.A = upload(lev.A, true, h.params.jacobi_weight);
+            d.A = upload(lev.A, true, h.params.jacobi_weight, in_tail);
             std::vector<double> wd(d.n);
             for (int i = 0; i < d.n; ++i) wd[i] = h.params.jacobi_weight * lev.inv_diag[i];
             d.wd = alloc(d.n);
             IRK_CUDA_CHECK(cudaMemcpy(d.wd, wd.data(), sizeof(double) * d.n, cudaMemcpyHostToDevice));
             if (l + 1 < L) {
-                d.P = upload(lev.P, false, 0.0);
-                d.R = upload(lev.R, false, 0.0);
+                d.P = upload(lev.P, false, 0.0, in_tail);
+                d.R = upload(lev.R, false, 0.0, in_tail);
             }
             d.t = alloc(d.n);
             d.u = alloc(d.n);
@@ -306,6 +318,35 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
         dh.cinv = alloc(static_cast<size_t>(dh.nc) * dh.nc);
         IRK_CUDA_CHECK(cudaMemcpy(dh.cinv, h.coarse_inverse.data(),
                                   sizeof(double) * dh.nc * dh.nc, cudaMemcpyHostToDevice));
+        if (dh.tail >= 0) {
+            dev::TailArgs& ta = dh.targs;
+            ta.nlev = L - dh.tail;
+            ta.cinv = dh.cinv;
+            ta.nc = dh.nc;
+            auto csr = [](const dev::Mat& m) {
+                dev::TailCsr c;
+                c.ptr = m.ptr;
+                c.idx = m.idx;
+                c.val = m.val;
+                c.tab = m.tab;
+                c.vf = m.vf;
+                return c;
+            };
+            for (int l = dh.tail; l < L; ++l) {
+                const DevLevel& d = dh.lv[l];
+                dev::TailLevel& tl = ta.lv[l - dh.tail];
+                tl.n = d.n;
+                tl.A = csr(d.A);
+                if (l + 1 < L) {
+                    tl.P = csr(d.P);
+                    tl.R = csr(d.R);
+                }
+                tl.wd = d.wd;
+                tl.r = d.r;
+                tl.z = d.z;
+                tl.t = d.t;
+            }
+        }
         hier_.push_back(std::move(dh));
     }
 
@@ -351,7 +392,8 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0) {
     const int pre = H.prm.pre_sweeps, post = H.prm.post_sweeps;
     auto rhs_of = [&](int l) { return l == 0 ? r0 : dev::plain(H.lv[l].r); };
     auto out_of = [&](int l) { return l == 0 ? z0 : dev::plain(H.lv[l].z); };
-    for (int l = 0; l + 1 < L; ++l) {
+    const int down_end = H.tail >= 0 ? H.tail : L - 1;  // levels < down_end smooth+restrict
+    for (int l = 0; l < down_end; ++l) {
         DevLevel& d = H.lv[l];
         dev::SpmvArgs a;
         a.r = rhs_of(l);
@@ -380,8 +422,15 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0) {
         ra.y = dev::plain(H.lv[l + 1].r);
         dev::spmv(d.R, dev::kXPlain, dev::kEPlain, ra, st_);
     }
-    dev::dense_mv(H.nc, H.cinv, rhs_of(L - 1), out_of(L - 1), st_);
-    for (int l = L - 2; l >= 0; --l) {
+    if (H.tail >= 0) {
+        dev::TailArgs ta = H.targs;
+        ta.r0 = rhs_of(H.tail);
+        ta.z0 = out_of(H.tail);
+        dev::coarse_tail(ta, st_);
+    } else {
+        dev::dense_mv(H.nc, H.cinv, rhs_of(L - 1), out_of(L - 1), st_);
+    }
+    for (int l = down_end - 1; l >= 0; --l) {
         DevLevel& d = H.lv[l];
         dev::SpmvArgs pa;
         pa.x = dev::plain(H.lv[l + 1].z);

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../host/setup.hpp"
+#include "coarse_tail.cuh"
 #include "kernels.cuh"
 
 namespace irkb {
@@ -63,6 +64,8 @@ struct DevHier {
     double* cinv = nullptr;
     int nc = 0;
     AmgParams prm;
+    int tail = -1;          // first level handled by the cluster tail kernel
+    dev::TailArgs targs{};  // prebuilt tail arguments (r0/z0 set per call)
 };
 
 class DeviceSolver {
@@ -105,7 +108,7 @@ public:
     int graph_mode() const { return graph_mode_; }
 
 private:
-    dev::Mat upload(const Csr& A, bool allow_dia, double omega);
+    dev::Mat upload(const Csr& A, bool allow_dia, double omega, bool force_csr = false);
     void upload_values(dev::Mat& m, const std::vector<double>& vals, double omega);
     template <class T> const T* upload_array(const std::vector<T>& h);
     double* alloc(size_t count);
