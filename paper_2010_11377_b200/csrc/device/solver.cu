@@ -59,9 +59,23 @@ double seconds_since(std::chrono::steady_clock::time_point t0) {
 
 }  // namespace
 
+// Device allocation; while `to_pool_` is set (coarse AMG levels) requests are
+// carved from the L2-persisting pool when it has room.
+void* DeviceSolver::raw_alloc(size_t bytes) {
+    bytes = std::max<size_t>(bytes, 1);
+    if (to_pool_ && pool_.bytes() > 0) {
+        const size_t at = (pool_used_ + 255) / 256 * 256;
+        if (at + bytes <= pool_.bytes()) {
+            pool_used_ = at + bytes;
+            return pool_.as<char>() + at;
+        }
+    }
+    bufs_.emplace_back(bytes);
+    return bufs_.back().as<void>();
+}
+
 double* DeviceSolver::alloc(size_t count) {
-    bufs_.emplace_back(sizeof(double) * std::max<size_t>(count, 1));
-    return bufs_.back().as<double>();
+    return static_cast<double*>(raw_alloc(sizeof(double) * count));
 }
 
 namespace {
@@ -104,8 +118,7 @@ Dict encode(const std::vector<double>& v) {
 
 template <class T>
 const T* DeviceSolver::upload_array(const std::vector<T>& h) {
-    bufs_.emplace_back(sizeof(T) * std::max<size_t>(h.size(), 1));
-    T* p = bufs_.back().as<T>();
+    T* p = static_cast<T*>(raw_alloc(sizeof(T) * h.size()));
     if (!h.empty()) IRK_CUDA_CHECK(cudaMemcpy(p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice));
     return p;
 }
@@ -277,7 +290,17 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
     for (int i = 0; i < s; ++i) hb_[i] = ht * b[i];
 
     static const int tail_rows =
-        std::getenv("IRK_TAIL_ROWS") ? std::atoi(std::getenv("IRK_TAIL_ROWS")) : 32768;
+        std::getenv("IRK_TAIL_ROWS") ? std::atoi(std::getenv("IRK_TAIL_ROWS")) : 4096;
+    // L2-persisting pool for the coarse levels (>= 1): their kernels are
+    // latency-bound and re-read every V-cycle, while the fine level streams
+    // gigabytes per GMRES iteration through L2 and would evict them.
+    {
+        int max_persist = 0, max_window = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
+        const size_t cap = std::min<size_t>(max_persist, max_window);
+        if (cap > (1u << 20) && std::getenv("IRK_NO_L2_PERSIST") == nullptr) pool_ = DevBuf(cap);
+    }
     for (const Hierarchy& h : hier_host_) {
         DevHier dh;
         dh.prm = h.params;
@@ -291,7 +314,10 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
                     break;
                 }
         }
-        for (int l = 0; l < L; ++l) {
+        dh.lv.resize(L);
+        // coarsest first, so the pool holds the most latency-bound levels
+        for (int l = L - 1; l >= 0; --l) {
+            to_pool_ = l >= 1;
             const AmgLevel& lev = h.levels[l];
             const bool in_tail = dh.tail >= 0 && l >= dh.tail;
             DevLevel d;
@@ -312,10 +338,12 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
                 d.r = alloc(d.n);
                 d.z = alloc(d.n);
             }
-            dh.lv.push_back(d);
+            dh.lv[l] = d;
         }
         dh.nc = h.levels.back().A.rows;
+        to_pool_ = true;
         dh.cinv = alloc(static_cast<size_t>(dh.nc) * dh.nc);
+        to_pool_ = false;
         IRK_CUDA_CHECK(cudaMemcpy(dh.cinv, h.coarse_inverse.data(),
                                   sizeof(double) * dh.nc * dh.nc, cudaMemcpyHostToDevice));
         if (dh.tail >= 0) {
@@ -350,6 +378,22 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
         hier_.push_back(std::move(dh));
     }
 
+    to_pool_ = false;
+    if (pool_used_ > 0) {
+        int max_persist = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
+        const size_t persist = std::min<size_t>(pool_used_, max_persist);
+        IRK_CUDA_CHECK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
+        cudaStreamAttrValue av = {};
+        av.accessPolicyWindow.base_ptr = pool_.as<void>();
+        av.accessPolicyWindow.num_bytes = pool_used_;
+        av.accessPolicyWindow.hitRatio =
+            std::min(1.0f, static_cast<float>(persist) / static_cast<float>(pool_used_));
+        av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        IRK_CUDA_CHECK(cudaStreamSetAttribute(st_, cudaStreamAttributeAccessPolicyWindow, &av));
+        persist_bytes_ = persist;
+    }
     rhs_ = alloc(n_);
     fw_ = alloc(static_cast<size_t>(s) * n_);
     u_ = alloc(n_);

@@ -86,6 +86,7 @@ public:
     double setup_seconds() const { return setup_seconds_; }
     bool fused_stage_op() const { return fused_op_; }
     int matrix_format(int which) const;  // 0 M, 1 K -> 0 CSR, 1 DIA
+    size_t persisting_bytes() const { return persist_bytes_; }
 
     // Device-pointer entry points (enqueue + synchronise).
     void stage_apply(const double* v, double* y);
@@ -112,6 +113,7 @@ private:
     void upload_values(dev::Mat& m, const std::vector<double>& vals, double omega);
     template <class T> const T* upload_array(const std::vector<T>& h);
     double* alloc(size_t count);
+    void* raw_alloc(size_t bytes);
     void record_vcycle(int k, dev::VecRef r, dev::VecRef z);
     void record_precond(dev::VecRef v, dev::VecRef w);
     void record_stage_op(dev::VecRef z, dev::VecRef y);
@@ -125,6 +127,9 @@ private:
     int device_ = 0;
     cudaStream_t st_ = nullptr;
     std::vector<DevBuf> bufs_;
+    DevBuf pool_;                 // L2-persisting pool (coarse levels)
+    size_t pool_used_ = 0, persist_bytes_ = 0;
+    bool to_pool_ = false;
     dev::Mat M_, K_;
     bool fused_op_ = false;
     dev::StageCoef coef_{};
