@@ -1,4 +1,11 @@
-// Coarse tail of the AMG V-cycle in ONE launch.
+// Coarse tail of the AMG V-cycle in ONE launch ("bottom solver").
+//
+// Default: a single CTA of 1024 threads takes the levels with <= 512 rows
+// plus the dense coarsest solve (5 launches per V-cycle at C2 become one).
+// A 16-CTA cluster variant (IRK_TAIL_CLUSTER=1) was measured slower on B200:
+// with tens of thousands of rows the phases are DRAM-latency bound and 70% of
+// the warps' stall cycles were spent at the cluster barriers
+// (profiles/r1/ncu_tail_cluster.txt).
 //
 // Below a few tens of thousands of rows every V-cycle phase (residual,
 // restriction, coarse solve, prolongation, post-smoothing) is pure latency:
@@ -106,8 +113,20 @@ __device__ __forceinline__ void for_rows(int n, F&& f) {
     }
 }
 
+// Phase barrier: a single CTA (the bottom solver) only needs __syncthreads.
+struct PhaseSync {
+    cg::cluster_group cl;
+    bool single;
+    __device__ void operator()() {
+        if (single)
+            __syncthreads();
+        else
+            cl();
+    }
+};
+
 __global__ void __launch_bounds__(1024) k_coarse_tail(const __grid_constant__ TailArgs a) {
-    cg::cluster_group cl = cg::this_cluster();
+    PhaseSync cl{cg::this_cluster(), cg::this_cluster().num_blocks() == 1};
     const int L = a.nlev;
     auto rhs = [&](int l) -> const double* { return l == 0 ? a.r0.get() : a.lv[l].r; };
     // down: residual of the pre-smoothed iterate, restriction
@@ -118,13 +137,13 @@ __global__ void __launch_bounds__(1024) k_coarse_tail(const __grid_constant__ Ta
             const double s = row_sum<4, 1>(v.A, row, live, lane, nullptr, v.wd, r);
             if (live && lane == 0) v.t[row] = r[row] - s;
         });
-        cl.sync();
+        cl();
         double* rc = a.lv[l + 1].r;
         for_rows<8>(a.lv[l + 1].n, [&](int row, bool live, int lane) {
             const double s = row_sum<8, 0>(v.R, row, live, lane, v.t, nullptr, nullptr);
             if (live && lane == 0) rc[row] = s;
         });
-        cl.sync();
+        cl();
     }
     // coarsest direct solve
     {
@@ -134,7 +153,7 @@ __global__ void __launch_bounds__(1024) k_coarse_tail(const __grid_constant__ Ta
             const double s = dense_row<8>(a.cinv, a.nc, row, live, lane, r);
             if (live && lane == 0) z[row] = s;
         });
-        cl.sync();
+        cl();
     }
     // up: prolongation + correction, post-smoothing sweep
     for (int l = L - 2; l >= 0; --l) {
@@ -145,13 +164,13 @@ __global__ void __launch_bounds__(1024) k_coarse_tail(const __grid_constant__ Ta
             const double s = row_sum<4, 0>(v.P, row, live, lane, zc, nullptr, nullptr);
             if (live && lane == 0) v.t[row] = v.wd[row] * r[row] + s;
         });
-        cl.sync();
+        cl();
         double* z = l == 0 ? a.z0.get() : v.z;
         for_rows<4>(v.n, [&](int row, bool live, int lane) {
             const double s = row_sum<4, 0>(v.A, row, live, lane, v.t, nullptr, nullptr);
             if (live && lane == 0) z[row] = v.t[row] + v.wd[row] * (r[row] - s);
         });
-        if (l > 0) cl.sync();
+        if (l > 0) cl();
     }
 }
 
@@ -186,8 +205,8 @@ int coarse_tail_cluster_size() {
     return g_cluster;
 }
 
-void coarse_tail(const TailArgs& a, cudaStream_t st) {
-    const int cs = coarse_tail_cluster_size();
+void coarse_tail(const TailArgs& a, int cluster, cudaStream_t st) {
+    const int cs = cluster > 1 ? coarse_tail_cluster_size() : 1;
     if (cs <= 0) throw CudaError("coarse tail: no cluster launch configuration available");
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs);
@@ -199,7 +218,7 @@ void coarse_tail(const TailArgs& a, cudaStream_t st) {
     at.val.clusterDim.y = 1;
     at.val.clusterDim.z = 1;
     cfg.attrs = &at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = cs > 1 ? 1 : 0;
     IRK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_coarse_tail, a));
 }
 

@@ -37,7 +37,8 @@ struct TailArgs {
 
 // 0 / -1 when cluster launches are unavailable.
 int coarse_tail_cluster_size();
-void coarse_tail(const TailArgs& a, cudaStream_t st);
+// cluster <= 1: one CTA (bottom solver); > 1: one 16-CTA cluster.
+void coarse_tail(const TailArgs& a, int cluster, cudaStream_t st);
 
 }  // namespace dev
 }  // namespace irkb

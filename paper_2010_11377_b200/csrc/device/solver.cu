@@ -290,7 +290,8 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
     for (int i = 0; i < s; ++i) hb_[i] = ht * b[i];
 
     static const int tail_rows =
-        std::getenv("IRK_TAIL_ROWS") ? std::atoi(std::getenv("IRK_TAIL_ROWS")) : 4096;
+        std::getenv("IRK_TAIL_ROWS") ? std::atoi(std::getenv("IRK_TAIL_ROWS")) : 512;
+    tail_cluster_ = std::getenv("IRK_TAIL_CLUSTER") ? 16 : 1;
     // L2-persisting pool for the coarse levels (>= 1): their kernels are
     // latency-bound and re-read every V-cycle, while the fine level streams
     // gigabytes per GMRES iteration through L2 and would evict them.
@@ -299,7 +300,9 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
         cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
         cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
         const size_t cap = std::min<size_t>(max_persist, max_window);
-        if (cap > (1u << 20) && std::getenv("IRK_NO_L2_PERSIST") == nullptr) pool_ = DevBuf(cap);
+        // Opt-in: measured slower on C2 (the carve-out costs the streaming
+        // vectors more than it saves the coarse levels), see profiles/r1/ab1.txt.
+        if (cap > (1u << 20) && std::getenv("IRK_L2_PERSIST") != nullptr) pool_ = DevBuf(cap);
     }
     for (const Hierarchy& h : hier_host_) {
         DevHier dh;
@@ -307,7 +310,7 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
         const int L = h.n_levels();
         // The cluster tail runs levels >= tail (V(1,1) only; <= 8 levels).
         if (tail_rows > 0 && h.params.pre_sweeps == 1 && h.params.post_sweeps == 1 &&
-            dev::coarse_tail_cluster_size() > 0) {
+            (tail_cluster_ == 1 || dev::coarse_tail_cluster_size() > 0)) {
             for (int l = 0; l < L; ++l)
                 if (h.levels[l].A.rows <= tail_rows && L - l <= dev::kMaxTailLevels) {
                     dh.tail = l;
@@ -470,7 +473,7 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0) {
         dev::TailArgs ta = H.targs;
         ta.r0 = rhs_of(H.tail);
         ta.z0 = out_of(H.tail);
-        dev::coarse_tail(ta, st_);
+        dev::coarse_tail(ta, tail_cluster_, st_);
     } else {
         dev::dense_mv(H.nc, H.cinv, rhs_of(L - 1), out_of(L - 1), st_);
     }

@@ -130,6 +130,7 @@ private:
     DevBuf pool_;                 // L2-persisting pool (coarse levels)
     size_t pool_used_ = 0, persist_bytes_ = 0;
     bool to_pool_ = false;
+    int tail_cluster_ = 1;
     dev::Mat M_, K_;
     bool fused_op_ = false;
     dev::StageCoef coef_{};
