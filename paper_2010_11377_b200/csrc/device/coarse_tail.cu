@@ -121,7 +121,7 @@ struct PhaseSync {
         if (single)
             __syncthreads();
         else
-            cl();
+            cl.sync();
     }
 };
 
