@@ -126,6 +126,8 @@ struct PhaseSync {
 };
 
 __global__ void __launch_bounds__(1024) k_coarse_tail(const __grid_constant__ TailArgs a) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     PhaseSync cl{cg::this_cluster(), cg::this_cluster().num_blocks() == 1};
     const int L = a.nlev;
     auto rhs = [&](int l) -> const double* { return l == 0 ? a.r0.get() : a.lv[l].r; };
@@ -217,8 +219,16 @@ void coarse_tail(const TailArgs& a, int cluster, cudaStream_t st) {
     at.val.clusterDim.x = cs;
     at.val.clusterDim.y = 1;
     at.val.clusterDim.z = 1;
-    cfg.attrs = &at;
-    cfg.numAttrs = cs > 1 ? 1 : 0;
+    cudaLaunchAttribute attrs[2];
+    int na = 0;
+    if (cs > 1) attrs[na++] = at;
+    if (pdl_enabled()) {
+        attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attrs[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attrs;
+    cfg.numAttrs = na;
     IRK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_coarse_tail, a));
 }
 

@@ -4,6 +4,8 @@
 // stencil (DIA), fused epilogues instead of separate BLAS-1 passes, and
 // deterministic reductions (see common.cuh for the numerics contract).
 #include <cstdio>
+#include <cstdlib>
+#include <utility>
 #include <string>
 
 #include "../host/sparse.hpp"
@@ -19,6 +21,39 @@ struct Offs {
 };
 
 inline int blocks_for(long long n, int t) { return static_cast<int>((n + t - 1) / t); }
+
+}  // namespace
+
+bool pdl_enabled() {
+    static const bool on = std::getenv("IRK_NO_PDL") == nullptr;
+    return on;
+}
+
+namespace {
+
+// Programmatic dependent launch: every kernel is launched with
+// programmaticStreamSerialization (captured into the graph as programmatic
+// edges), signals launch_dependents first thing and waits on its
+// predecessor's completion (griddepcontrol.wait) only after its own static
+// prologue -- so the next launch's scheduling and prologue overlap the
+// previous kernel's tail.  Without PDL both instructions are no-ops.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+void launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    IRK_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
 
 // ------------------------------------------------------------------ SpMV
 // Value fetch: fp64, or a code into the exact dictionary (u8: shared-memory
@@ -37,6 +72,7 @@ __device__ __forceinline__ double vfetch(const void* v, long long k, const doubl
 // Shared-memory dictionaries for u8 codes (256 entries each).
 template <int VF>
 __device__ __forceinline__ const double* load_tab(const Mat& A, double* s_tab, double* s_wd) {
+    pdl_trigger();
     if constexpr (VF == kU8) {
         for (int i = threadIdx.x; i < A.ntab; i += blockDim.x) {
             s_tab[i] = A.tab[i];
@@ -73,6 +109,7 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
     __shared__ double s_tab[VF == kU8 ? 256 : 1];
     __shared__ double s_wd[VF == kU8 ? 256 : 1];
     const double* tab = load_tab<VF>(A, s_tab, s_wd);
+    pdl_wait();
     const int n = A.rows;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -110,6 +147,7 @@ __global__ void __launch_bounds__(256) k_spmv_sell(Mat A, SpmvArgs a) {
     __shared__ double s_tab[VF == kU8 ? 256 : 1];
     __shared__ double s_wd[1];
     const double* tab = load_tab<VF>(A, s_tab, s_wd);
+    pdl_wait();
     const int slice = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int nslices = (A.rows + 31) >> 5;
@@ -143,6 +181,7 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
     __shared__ double s_tab[VF == kU8 ? 256 : 1];
     __shared__ double s_wd[1];
     const double* tab = load_tab<VF>(A, s_tab, s_wd);
+    pdl_wait();
     constexpr int MM = 4;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int row = t / G;
@@ -190,27 +229,27 @@ void launch_spmv_vf(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
         const bool wdt = VF == kU8 && A.wdtab && A.diag0 >= 0;
         if (A.nd == 7) {
             if (wdt)
-                k_spmv_dia<XM, EPI, VF, 1, 7><<<nb, 256, 0, st>>>(A, a);
+                launch(k_spmv_dia<XM, EPI, VF, 1, 7>, nb, 256, 0, st, A, a);
             else
-                k_spmv_dia<XM, EPI, VF, 0, 7><<<nb, 256, 0, st>>>(A, a);
+                launch(k_spmv_dia<XM, EPI, VF, 0, 7>, nb, 256, 0, st, A, a);
         } else {
             if (wdt)
-                k_spmv_dia<XM, EPI, VF, 1, 0><<<nb, 256, 0, st>>>(A, a);
+                launch(k_spmv_dia<XM, EPI, VF, 1, 0>, nb, 256, 0, st, A, a);
             else
-                k_spmv_dia<XM, EPI, VF, 0, 0><<<nb, 256, 0, st>>>(A, a);
+                launch(k_spmv_dia<XM, EPI, VF, 0, 0>, nb, 256, 0, st, A, a);
         }
     } else if (A.fmt == kCsrVec) {
         const int nb = blocks_for(static_cast<long long>(A.rows) * A.lanes, 256);
         switch (A.lanes) {
-        case 2: k_spmv_csrv<XM, EPI, VF, 2><<<nb, 256, 0, st>>>(A, a); break;
-        case 4: k_spmv_csrv<XM, EPI, VF, 4><<<nb, 256, 0, st>>>(A, a); break;
-        case 8: k_spmv_csrv<XM, EPI, VF, 8><<<nb, 256, 0, st>>>(A, a); break;
-        case 16: k_spmv_csrv<XM, EPI, VF, 16><<<nb, 256, 0, st>>>(A, a); break;
-        default: k_spmv_csrv<XM, EPI, VF, 32><<<nb, 256, 0, st>>>(A, a); break;
+        case 2: launch(k_spmv_csrv<XM, EPI, VF, 2>, nb, 256, 0, st, A, a); break;
+        case 4: launch(k_spmv_csrv<XM, EPI, VF, 4>, nb, 256, 0, st, A, a); break;
+        case 8: launch(k_spmv_csrv<XM, EPI, VF, 8>, nb, 256, 0, st, A, a); break;
+        case 16: launch(k_spmv_csrv<XM, EPI, VF, 16>, nb, 256, 0, st, A, a); break;
+        default: launch(k_spmv_csrv<XM, EPI, VF, 32>, nb, 256, 0, st, A, a); break;
         }
     } else {
         const int nslices = (A.rows + 31) / 32;
-        k_spmv_sell<XM, EPI, VF><<<blocks_for(static_cast<long long>(nslices) * 32, 256), 256, 0, st>>>(A, a);
+        launch(k_spmv_sell<XM, EPI, VF>, blocks_for(static_cast<long long>(nslices) * 32, 256), 256, 0, st, A, a);
     }
 }
 
@@ -233,6 +272,7 @@ __global__ void __launch_bounds__(256) k_stage_op_dia(Mat M, Mat K, StageCoef cf
     __shared__ double s_dummy[1];
     const double* tm = load_tab<VF>(M, s_tm, s_dummy);
     const double* tk = load_tab<VF>(K, s_tk, s_dummy);
+    pdl_wait();
     const int n = M.rows;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -272,6 +312,7 @@ __global__ void __launch_bounds__(256) k_sweep_dia(Mat K, VecRef wr, VecRef vr, 
     __shared__ double s_tk[VF == kU8 ? 256 : 1];
     __shared__ double s_dummy[1];
     const double* tk = load_tab<VF>(K, s_tk, s_dummy);
+    pdl_wait();
     const int n = K.rows;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -292,6 +333,8 @@ __global__ void __launch_bounds__(256) k_sweep_dia(Mat K, VecRef wr, VecRef vr, 
 }
 
 __global__ void k_combine(int n, VecRef vr, SweepTerms t, VecRef outr) {
+    pdl_trigger();
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double acc = vr.get()[i];
@@ -302,6 +345,8 @@ __global__ void k_combine(int n, VecRef vr, SweepTerms t, VecRef outr) {
 }
 
 __global__ void k_axpy(int n, double alpha, const double* __restrict__ x, VecRef yr) {
+    pdl_trigger();
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double* y = yr.get();
@@ -312,6 +357,8 @@ __global__ void k_axpy(int n, double alpha, const double* __restrict__ x, VecRef
 // memory with coalesced loads, then each thread forms one row sequentially.
 __global__ void __launch_bounds__(256) k_dense_mv(int n, const double* __restrict__ A, VecRef rr,
                                                   VecRef zr) {
+    pdl_trigger();
+    pdl_wait();
     extern __shared__ double sm[];
     double* sA = sm;
     double* sr = sm + static_cast<long long>(n) * n;
@@ -329,6 +376,8 @@ __global__ void __launch_bounds__(256) k_dense_mv(int n, const double* __restric
 
 // Large coarsest level (n*n does not fit shared memory): one thread per row.
 __global__ void k_dense_mv_big(int n, const double* __restrict__ A, VecRef rr, VecRef zr) {
+    pdl_trigger();
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double* r = rr.get();
@@ -340,6 +389,8 @@ __global__ void k_dense_mv_big(int n, const double* __restrict__ A, VecRef rr, V
 
 __global__ void k_wd_times_r(int n, const double* __restrict__ wd, VecRef rr,
                              double* __restrict__ z) {
+    pdl_trigger();
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     z[i] = wd[i] * rr.get()[i];
@@ -347,6 +398,8 @@ __global__ void k_wd_times_r(int n, const double* __restrict__ wd, VecRef rr,
 
 __global__ void k_stage_rhs(int n, int s, const double* __restrict__ ku,
                             const double* __restrict__ lift, double* __restrict__ b) {
+    pdl_trigger();
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double f = ku[i];
@@ -362,6 +415,8 @@ struct HB {
 
 __global__ void k_irk_update(int n, int s, const double* __restrict__ u,
                              const double* __restrict__ x, HB hb, double* __restrict__ un) {
+    pdl_trigger();
+    pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double acc = u[i];
@@ -421,6 +476,8 @@ __global__ void __launch_bounds__(kRedThreads) k_dot(const double* __restrict__ 
                                                      const double* __restrict__ y, long long n,
                                                      double* part, unsigned* counter,
                                                      double* out) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double red[kRedThreads / 32 * 1];
     __shared__ double res[1];
     const int c = blockIdx.x;
@@ -542,6 +599,8 @@ __device__ void arnoldi_tail(const GmresBufs& g) {
 
 // Pass 1: h_i = V_i . w (i <= j) and ||w||^2; pass 2 (if reorth): c_i = V_i . w.
 __global__ void __launch_bounds__(kRedThreads) k_gm_blockdot(GmresBufs g, int pass) {
+    pdl_trigger();
+    pdl_wait();
     extern __shared__ double red[];
     GmresCtl* ctl = g.ctl;
     if (pass == 2 && !ctl->reorth) return;
@@ -578,6 +637,8 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_blockdot(GmresBufs g, int pa
 
 // w -= sum_i coef_i V_i (sequential in i), then ||w|| and the scalar tail.
 __global__ void __launch_bounds__(kRedThreads) k_gm_update(GmresBufs g, int pass) {
+    pdl_trigger();
+    pdl_wait();
     extern __shared__ double red[];
     GmresCtl* ctl = g.ctl;
     if (pass == 2 && !ctl->reorth) return;
@@ -630,6 +691,8 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_update(GmresBufs g, int pass
 
 // V_{j+1} *= 1/h_{j+1,j} when the cycle continues; advance j.
 __global__ void __launch_bounds__(kRedThreads) k_gm_normalize(GmresBufs g) {
+    pdl_trigger();
+    pdl_wait();
     GmresCtl* ctl = g.ctl;
     const int stop = ctl->stop;
     const int j = ctl->j;
@@ -654,6 +717,8 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_normalize(GmresBufs g) {
 __global__ void __launch_bounds__(kRedThreads) k_gm_init(GmresBufs g, const double* __restrict__ b,
                                                          double* __restrict__ r, double rel_tol,
                                                          int restart, int max_iter) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double red[kRedThreads / 32 + 1];
     double v[kRedPerThread];
     load_chunk(b, g.sN, blockIdx.x, v);
@@ -702,6 +767,8 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_init(GmresBufs g, const doub
 
 __global__ void __launch_bounds__(kRedThreads) k_gm_cycle_begin(GmresBufs g,
                                                                 const double* __restrict__ r) {
+    pdl_trigger();
+    pdl_wait();
     GmresCtl* ctl = g.ctl;
     const double inv = ctl->inv;
     double v[kRedPerThread];
@@ -721,6 +788,8 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_cycle_begin(GmresBufs g,
 
 // Back substitution for y (gmres.cpp:126-131), one thread.
 __global__ void k_gm_backsub(GmresBufs g) {
+    pdl_trigger();
+    pdl_wait();
     GmresCtl* c = g.ctl;
     const int m = c->m;
     const int ld = c->restart + 1;
@@ -733,6 +802,8 @@ __global__ void k_gm_backsub(GmresBufs g) {
 
 // x += sum_i y_i Z_i (sequential in i).  Z slots are padded like V.
 __global__ void __launch_bounds__(kRedThreads) k_gm_xupdate(GmresBufs g, double* __restrict__ x) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double ys[kMaxRestart];
     const GmresCtl* c = g.ctl;
     const int m = c->m;
@@ -754,6 +825,8 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_xupdate(GmresBufs g, double*
 __global__ void __launch_bounds__(kRedThreads) k_gm_residual(GmresBufs g, const double* __restrict__ b,
                                                              const double* __restrict__ ax,
                                                              double* __restrict__ r) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double red[kRedThreads / 32 + 1];
     double bv[kRedPerThread], av[kRedPerThread];
     load_chunk(b, g.sN, blockIdx.x, bv);
@@ -816,11 +889,11 @@ void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecR
 #define IRK_OP_CASE(S)                                                             \
     case S:                                                                        \
         if (u8 && M.nd == 7)                                                       \
-            k_stage_op_dia<S, kU8, 7><<<nb, 256, 0, st>>>(M, K, c, z, y);          \
+            launch(k_stage_op_dia<S, kU8, 7>, nb, 256, 0, st, M, K, c, z, y);          \
         else if (u8)                                                               \
-            k_stage_op_dia<S, kU8, 0><<<nb, 256, 0, st>>>(M, K, c, z, y);          \
+            launch(k_stage_op_dia<S, kU8, 0>, nb, 256, 0, st, M, K, c, z, y);          \
         else                                                                       \
-            k_stage_op_dia<S, kF64, 0><<<nb, 256, 0, st>>>(M, K, c, z, y);         \
+            launch(k_stage_op_dia<S, kF64, 0>, nb, 256, 0, st, M, K, c, z, y);         \
         break;
         IRK_OP_CASE(1) IRK_OP_CASE(2) IRK_OP_CASE(3) IRK_OP_CASE(4) IRK_OP_CASE(5)
         IRK_OP_CASE(6) IRK_OP_CASE(7)
@@ -835,87 +908,86 @@ void sweep_dia(const Mat& K, VecRef w, VecRef v, const SweepTerms& t, double* st
     switch (K.vf) {
     case kU8:
         if (K.nd == 7)
-            k_sweep_dia<kU8, 7><<<blocks_for(n, 256), 256, 0, st>>>(K, w, v, t, store, out);
+            launch(k_sweep_dia<kU8, 7>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out);
         else
-            k_sweep_dia<kU8, 0><<<blocks_for(n, 256), 256, 0, st>>>(K, w, v, t, store, out);
+            launch(k_sweep_dia<kU8, 0>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out);
         break;
-    case kU16: k_sweep_dia<kU16, 0><<<blocks_for(n, 256), 256, 0, st>>>(K, w, v, t, store, out); break;
-    default: k_sweep_dia<kF64, 0><<<blocks_for(n, 256), 256, 0, st>>>(K, w, v, t, store, out); break;
+    case kU16: launch(k_sweep_dia<kU16, 0>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out); break;
+    default: launch(k_sweep_dia<kF64, 0>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out); break;
     }
 }
 
 void combine(VecRef v, const SweepTerms& t, VecRef out, int n, cudaStream_t st) {
-    k_combine<<<blocks_for(n, 256), 256, 0, st>>>(n, v, t, out);
+    launch(k_combine, blocks_for(n, 256), 256, 0, st, n, v, t, out);
 }
 
 void axpy(double alpha, const double* x, VecRef y, int n, cudaStream_t st) {
-    k_axpy<<<blocks_for(n, 256), 256, 0, st>>>(n, alpha, x, y);
+    launch(k_axpy, blocks_for(n, 256), 256, 0, st, n, alpha, x, y);
 }
 
 void dense_mv(int n, const double* Ainv, VecRef r, VecRef z, cudaStream_t st) {
     const size_t smem = sizeof(double) * (static_cast<size_t>(n) * n + n);
     if (smem <= 200 * 1024)
-        k_dense_mv<<<1, 256, smem, st>>>(n, Ainv, r, z);
+        launch(k_dense_mv, 1, 256, smem, st, n, Ainv, r, z);
     else
-        k_dense_mv_big<<<blocks_for(n, 128), 128, 0, st>>>(n, Ainv, r, z);
+        launch(k_dense_mv_big, blocks_for(n, 128), 128, 0, st, n, Ainv, r, z);
 }
 
 void wd_times_r(int n, const double* wd, VecRef r, double* z, cudaStream_t st) {
-    k_wd_times_r<<<blocks_for(n, 256), 256, 0, st>>>(n, wd, r, z);
+    launch(k_wd_times_r, blocks_for(n, 256), 256, 0, st, n, wd, r, z);
 }
 
 void stage_rhs_finish(const double* ku, const double* lift, double* b, int n, int s,
                       cudaStream_t st) {
-    k_stage_rhs<<<blocks_for(n, 256), 256, 0, st>>>(n, s, ku, lift, b);
+    launch(k_stage_rhs, blocks_for(n, 256), 256, 0, st, n, s, ku, lift, b);
 }
 
 void irk_update(const double* u, const double* x, const double* hb, int n, int s, double* un,
                 cudaStream_t st) {
     HB h;
     for (int q = 0; q < s; ++q) h.v[q] = hb[q];
-    k_irk_update<<<blocks_for(n, 256), 256, 0, st>>>(n, s, u, x, h, un);
+    launch(k_irk_update, blocks_for(n, 256), 256, 0, st, n, s, u, x, h, un);
 }
 
 static size_t red_smem(int nv) { return sizeof(double) * (kRedThreads / 32 * nv + nv + 8); }
 
 void gm_init(const GmresBufs& g, const double* b, double* r, double rel_tol, int restart,
              int max_iter, cudaStream_t st) {
-    k_gm_init<<<g.nchunks, kRedThreads, 0, st>>>(g, b, r, rel_tol, restart, max_iter);
+    launch(k_gm_init, g.nchunks, kRedThreads, 0, st, g, b, r, rel_tol, restart, max_iter);
 }
 
 void gm_cycle_begin(const GmresBufs& g, const double* r, cudaStream_t st) {
-    k_gm_cycle_begin<<<g.nchunks, kRedThreads, 0, st>>>(g, r);
+    launch(k_gm_cycle_begin, g.nchunks, kRedThreads, 0, st, g, r);
 }
 
 void gm_blockdot(const GmresBufs& g, int pass, cudaStream_t st) {
     // capacity for up to restart+1 basis vectors plus ||w||
     const int nv = kMaxRestart + 2;
-    k_gm_blockdot<<<g.nchunks, kRedThreads, red_smem(nv), st>>>(g, pass);
+    launch(k_gm_blockdot, g.nchunks, kRedThreads, red_smem(nv), st, g, pass);
 }
 
 void gm_update(const GmresBufs& g, int pass, cudaStream_t st) {
-    k_gm_update<<<g.nchunks, kRedThreads, sizeof(double) * (kRedThreads / 32 + 1 + kMaxRestart + 8),
-                  st>>>(g, pass);
+    launch(k_gm_update, g.nchunks, kRedThreads, sizeof(double) * (kRedThreads / 32 + 1 + kMaxRestart + 8), st, g, pass);
 }
 
 void gm_normalize(const GmresBufs& g, cudaStream_t st) {
-    k_gm_normalize<<<g.nchunks, kRedThreads, 0, st>>>(g);
+    launch(k_gm_normalize, g.nchunks, kRedThreads, 0, st, g);
 }
 
 void gm_solution(const GmresBufs& g, double* x, cudaStream_t st) {
-    k_gm_backsub<<<1, 1, 0, st>>>(g);
-    k_gm_xupdate<<<g.nchunks, kRedThreads, 0, st>>>(g, x);
+    launch(k_gm_backsub, 1, 1, 0, st, g);
+    launch(k_gm_xupdate, g.nchunks, kRedThreads, 0, st, g, x);
 }
 
 void gm_residual(const GmresBufs& g, const double* b, const double* ax, double* r,
                  cudaStream_t st) {
-    k_gm_residual<<<g.nchunks, kRedThreads, 0, st>>>(g, b, ax, r);
+    launch(k_gm_residual, g.nchunks, kRedThreads, 0, st, g, b, ax, r);
 }
 
 void dot(const double* x, const double* y, long long n, double* partials, unsigned* counter,
          double* out, cudaStream_t st) {
     const int nch = static_cast<int>((n + kChunk - 1) / kChunk);
-    k_dot<<<nch > 0 ? nch : 1, kRedThreads, 0, st>>>(x, y, n, partials, counter, out);
+    launch(k_dot, nch > 0 ? nch : 1, kRedThreads, 0, st, x, y, n, partials, counter, out);
 }
 
 void set_smem_limits() {

@@ -70,6 +70,9 @@ struct SpmvArgs {
     VecRef y{};
 };
 
+// Programmatic dependent launch on (default) unless IRK_NO_PDL is set.
+bool pdl_enabled();
+
 void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st);
 
 // Stage operator y_i = M z_i + sum_j c_ij K z_j (c = ht*A), M/K sharing one

@@ -290,7 +290,7 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
     for (int i = 0; i < s; ++i) hb_[i] = ht * b[i];
 
     static const int tail_rows =
-        std::getenv("IRK_TAIL_ROWS") ? std::atoi(std::getenv("IRK_TAIL_ROWS")) : 512;
+        std::getenv("IRK_TAIL_ROWS") ? std::atoi(std::getenv("IRK_TAIL_ROWS")) : 0;
     tail_cluster_ = std::getenv("IRK_TAIL_CLUSTER") ? 16 : 1;
     // L2-persisting pool for the coarse levels (>= 1): their kernels are
     // latency-bound and re-read every V-cycle, while the fine level streams
