@@ -25,13 +25,14 @@ inline int blocks_for(long long n, int t) { return static_cast<int>((n + t - 1) 
 }  // namespace
 
 bool pdl_enabled() {
-    static const bool on = std::getenv("IRK_NO_PDL") == nullptr;
+    static const bool on = std::getenv("IRK_PDL") != nullptr;
     return on;
 }
 
 namespace {
 
-// Programmatic dependent launch: every kernel is launched with
+// Programmatic dependent launch (opt-in, IRK_PDL=1: measured 2% slower on
+// C2, profiles/r1/ab3_pdl.txt): every kernel is launched with
 // programmaticStreamSerialization (captured into the graph as programmatic
 // edges), signals launch_dependents first thing and waits on its
 // predecessor's completion (griddepcontrol.wait) only after its own static

@@ -70,7 +70,7 @@ struct SpmvArgs {
     VecRef y{};
 };
 
-// Programmatic dependent launch on (default) unless IRK_NO_PDL is set.
+// Programmatic dependent launch, opt-in via IRK_PDL=1.
 bool pdl_enabled();
 
 void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st);

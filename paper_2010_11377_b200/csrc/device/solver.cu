@@ -433,14 +433,15 @@ int DeviceSolver::matrix_format(int which) const { return which == 0 ? M_.fmt : 
 //   r_{l+1} = R t          restriction
 //   t = wd.*r + P z_{l+1}  prolongation fused with the pre-smoothed iterate
 //   z = t + wd.*(r - A t)  post-smoothing sweep
-void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0) {
+void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
     DevHier& H = hier_[k];
     const int L = static_cast<int>(H.lv.size());
     const int pre = H.prm.pre_sweeps, post = H.prm.post_sweeps;
-    auto rhs_of = [&](int l) { return l == 0 ? r0 : dev::plain(H.lv[l].r); };
-    auto out_of = [&](int l) { return l == 0 ? z0 : dev::plain(H.lv[l].z); };
+    // `first` > 0 runs only the part of the cycle below level `first` (timing)
+    auto rhs_of = [&](int l) { return l == first ? r0 : dev::plain(H.lv[l].r); };
+    auto out_of = [&](int l) { return l == first ? z0 : dev::plain(H.lv[l].z); };
     const int down_end = H.tail >= 0 ? H.tail : L - 1;  // levels < down_end smooth+restrict
-    for (int l = 0; l < down_end; ++l) {
+    for (int l = first; l < down_end; ++l) {
         DevLevel& d = H.lv[l];
         dev::SpmvArgs a;
         a.r = rhs_of(l);
@@ -477,7 +478,7 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0) {
     } else {
         dev::dense_mv(H.nc, H.cinv, rhs_of(L - 1), out_of(L - 1), st_);
     }
-    for (int l = down_end - 1; l >= 0; --l) {
+    for (int l = down_end - 1; l >= first; --l) {
         DevLevel& d = H.lv[l];
         dev::SpmvArgs pa;
         pa.x = dev::plain(H.lv[l + 1].z);
@@ -949,7 +950,12 @@ double DeviceSolver::time_kernel(int which, int reps) {
             break;
         }
         case 2: record_precond(dev::plain(a.as<double>()), dev::plain(b.as<double>())); break;
-        default: record_vcycle(0, dev::plain(a.as<double>()), dev::plain(b.as<double>())); break;
+        case 3: record_vcycle(0, dev::plain(a.as<double>()), dev::plain(b.as<double>())); break;
+        default: {  // 4, 5, ...: the V-cycle below level which-3
+            const int first = std::min<int>(which - 3, static_cast<int>(hier_[0].lv.size()) - 1);
+            record_vcycle(0, dev::plain(a.as<double>()), dev::plain(b.as<double>()), first);
+            break;
+        }
         }
     };
     once();

@@ -114,7 +114,7 @@ private:
     template <class T> const T* upload_array(const std::vector<T>& h);
     double* alloc(size_t count);
     void* raw_alloc(size_t bytes);
-    void record_vcycle(int k, dev::VecRef r, dev::VecRef z);
+    void record_vcycle(int k, dev::VecRef r, dev::VecRef z, int first = 0);
     void record_precond(dev::VecRef v, dev::VecRef w);
     void record_stage_op(dev::VecRef z, dev::VecRef y);
     void record_iteration();
