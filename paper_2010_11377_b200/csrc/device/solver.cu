@@ -302,7 +302,10 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
         const size_t cap = std::min<size_t>(max_persist, max_window);
         // Opt-in: measured slower on C2 (the carve-out costs the streaming
         // vectors more than it saves the coarse levels), see profiles/r1/ab1.txt.
-        if (cap > (1u << 20) && std::getenv("IRK_L2_PERSIST") != nullptr) pool_ = DevBuf(cap);
+        if (cap > (1u << 20) && std::getenv("IRK_L2_PERSIST") != nullptr) {
+            pool_ = DevBuf(cap);
+            persist_level_ = std::max(1, std::atoi(std::getenv("IRK_L2_PERSIST")));
+        }
     }
     for (const Hierarchy& h : hier_host_) {
         DevHier dh;
@@ -320,7 +323,7 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
         dh.lv.resize(L);
         // coarsest first, so the pool holds the most latency-bound levels
         for (int l = L - 1; l >= 0; --l) {
-            to_pool_ = l >= 1;
+            to_pool_ = l >= persist_level_;
             const AmgLevel& lev = h.levels[l];
             const bool in_tail = dh.tail >= 0 && l >= dh.tail;
             DevLevel d;

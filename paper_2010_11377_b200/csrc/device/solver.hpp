@@ -131,6 +131,7 @@ private:
     size_t pool_used_ = 0, persist_bytes_ = 0;
     bool to_pool_ = false;
     int tail_cluster_ = 1;
+    int persist_level_ = 1;
     dev::Mat M_, K_;
     bool fused_op_ = false;
     dev::StageCoef coef_{};
