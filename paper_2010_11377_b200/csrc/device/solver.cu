@@ -292,6 +292,8 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
     static const int tail_rows =
         std::getenv("IRK_TAIL_ROWS") ? std::atoi(std::getenv("IRK_TAIL_ROWS")) : 0;
     tail_cluster_ = std::getenv("IRK_TAIL_CLUSTER") ? 16 : 1;
+    static const int fused_rows =
+        std::getenv("IRK_FUSED_ROWS") ? std::atoi(std::getenv("IRK_FUSED_ROWS")) : 32768;
     // L2-persisting pool for the coarse levels (>= 1): their kernels are
     // latency-bound and re-read every V-cycle, while the fine level streams
     // gigabytes per GMRES iteration through L2 and would evict them.
@@ -322,10 +324,17 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
         }
         dh.lv.resize(L);
         // coarsest first, so the pool holds the most latency-bound levels
+        // Fused down/up kernels for the small levels (V(1,1); not with the tail).
+        if (dh.tail < 0 && fused_rows > 0 && h.params.pre_sweeps == 1 && h.params.post_sweeps == 1)
+            for (int l = 0; l + 1 < L; ++l)
+                if (h.levels[l].A.rows <= fused_rows) {
+                    dh.fused = l;
+                    break;
+                }
         for (int l = L - 1; l >= 0; --l) {
             to_pool_ = l >= persist_level_;
             const AmgLevel& lev = h.levels[l];
-            const bool in_tail = dh.tail >= 0 && l >= dh.tail;
+            const bool in_tail = (dh.tail >= 0 && l >= dh.tail) || (dh.fused >= 0 && l >= dh.fused);
             DevLevel d;
             d.n = lev.A.rows;
             d.A = upload(lev.A, true, h.params.jacobi_weight, in_tail);
@@ -352,6 +361,39 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
         to_pool_ = false;
         IRK_CUDA_CHECK(cudaMemcpy(dh.cinv, h.coarse_inverse.data(),
                                   sizeof(double) * dh.nc * dh.nc, cudaMemcpyHostToDevice));
+        if (dh.fused >= 0) {
+            auto csr = [](const dev::Mat& m) {
+                dev::TailCsr c;
+                c.ptr = m.ptr;
+                c.idx = m.idx;
+                c.val = m.val;
+                c.tab = m.tab;
+                c.vf = m.vf;
+                return c;
+            };
+            bufs_.emplace_back(sizeof(unsigned));
+            dh.counter = bufs_.back().as<unsigned>();
+            IRK_CUDA_CHECK(cudaMemset(dh.counter, 0, sizeof(unsigned)));
+            dh.fl.resize(L);
+            for (int l = dh.fused; l + 1 < L; ++l) {
+                dev::FusedLevel& f = dh.fl[l];
+                const DevLevel& d = dh.lv[l];
+                f.n = d.n;
+                f.nrc = dh.lv[l + 1].n;
+                f.A = csr(d.A);
+                f.P = csr(d.P);
+                f.R = csr(d.R);
+                f.wd = d.wd;
+                f.rc = dh.lv[l + 1].r;
+                f.zc = dh.lv[l + 1].z;
+                if (l + 2 == L) {
+                    f.cinv = dh.cinv;
+                    f.nc = dh.nc;
+                    f.zcw = dh.lv[l + 1].z;
+                    f.counter = dh.counter;
+                }
+            }
+        }
         if (dh.tail >= 0) {
             dev::TailArgs& ta = dh.targs;
             ta.nlev = L - dh.tail;
@@ -444,7 +486,14 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
     auto rhs_of = [&](int l) { return l == first ? r0 : dev::plain(H.lv[l].r); };
     auto out_of = [&](int l) { return l == first ? z0 : dev::plain(H.lv[l].z); };
     const int down_end = H.tail >= 0 ? H.tail : L - 1;  // levels < down_end smooth+restrict
+    const bool fused_coarse = H.fused >= 0 && H.fused <= L - 2;
     for (int l = first; l < down_end; ++l) {
+        if (H.fused >= 0 && l >= H.fused) {
+            dev::FusedLevel f = H.fl[l];
+            f.r = rhs_of(l);
+            dev::amg_down_fused(f, st_);
+            continue;
+        }
         DevLevel& d = H.lv[l];
         dev::SpmvArgs a;
         a.r = rhs_of(l);
@@ -478,10 +527,17 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
         ta.r0 = rhs_of(H.tail);
         ta.z0 = out_of(H.tail);
         dev::coarse_tail(ta, tail_cluster_, st_);
-    } else {
+    } else if (!fused_coarse || first > L - 2) {
         dev::dense_mv(H.nc, H.cinv, rhs_of(L - 1), out_of(L - 1), st_);
     }
     for (int l = down_end - 1; l >= first; --l) {
+        if (H.fused >= 0 && l >= H.fused) {
+            dev::FusedLevel f = H.fl[l];
+            f.r = rhs_of(l);
+            f.z = out_of(l);
+            dev::amg_up_fused(f, st_);
+            continue;
+        }
         DevLevel& d = H.lv[l];
         dev::SpmvArgs pa;
         pa.x = dev::plain(H.lv[l + 1].z);

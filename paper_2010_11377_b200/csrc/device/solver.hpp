@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../host/setup.hpp"
+#include "amg_fused.cuh"
 #include "coarse_tail.cuh"
 #include "kernels.cuh"
 
@@ -66,6 +67,9 @@ struct DevHier {
     AmgParams prm;
     int tail = -1;          // first level handled by the cluster tail kernel
     dev::TailArgs targs{};  // prebuilt tail arguments (r0/z0 set per call)
+    int fused = -1;         // first level run by the fused down/up kernels
+    std::vector<dev::FusedLevel> fl;  // per level (r/z set per call)
+    unsigned* counter = nullptr;
 };
 
 class DeviceSolver {
