@@ -523,6 +523,28 @@ __device__ __forceinline__ void load_chunk(const double* __restrict__ v, long lo
     }
 }
 
+// As load_chunk, with default caching (re-reads that should hit L2).
+__device__ __forceinline__ void load_chunk_l2(const double* __restrict__ v, long long n, int c,
+                                              double (&o)[kRedPerThread]) {
+    const long long base = static_cast<long long>(c) * kChunk + 2 * threadIdx.x;
+    if (static_cast<long long>(c + 1) * kChunk <= n) {
+#pragma unroll
+        for (int u = 0; u < kRedPerThread / 2; ++u) {
+            const double2 p = __ldcg(reinterpret_cast<const double2*>(v + base + u * 2 * kRedThreads));
+            o[2 * u] = p.x;
+            o[2 * u + 1] = p.y;
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < kRedPerThread / 2; ++u)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const long long k = base + u * 2 * kRedThreads + e;
+                o[2 * u + e] = k < n ? v[k] : 0.0;
+            }
+    }
+}
+
 __device__ __forceinline__ void store_chunk(double* v, long long n, int c,
                                             const double (&o)[kRedPerThread]) {
     const long long base = static_cast<long long>(c) * kChunk + 2 * threadIdx.x;
@@ -687,6 +709,68 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_update(GmresBufs g, int pass
             arnoldi_tail(g);
         }
         g.counters[2 + pass - 1] = 0u;
+    }
+}
+
+// Pass-1 update fused with the pass-2 block-dot (CGS2): per chunk,
+// w' = w - sum_i h_i V_i, then c_i = V_i . w' and ||w'||^2 with V_i re-read
+// (in reverse order, most recently loaded first) while it is still in L2.  A
+// persistent grid of at most one CTA per SM keeps the re-read working set
+// (CTAs x (j+1) x 32 KB) near L2 capacity.  Per-vector partials use exactly
+// the chunk tree of k_gm_blockdot / k_gm_update, so c and ||w'|| are
+// bit-identical to running those two kernels; when the 0.7071 test says no
+// re-orthogonalisation is needed, c is simply dropped.
+__global__ void __launch_bounds__(kRedThreads) k_gm_update_cgs2(GmresBufs g) {
+    extern __shared__ double red[];
+    pdl_trigger();
+    pdl_wait();
+    GmresCtl* ctl = g.ctl;
+    const int j = ctl->j;
+    const int nb = j + 1;
+    const int nv = nb + 1;  // c_0..c_j, ||w'||^2
+    double* cf = red + (kRedThreads / 32) * nv + nv + 1;
+    for (int i = threadIdx.x; i < nb; i += kRedThreads) cf[i] = ctl->hcol[i];
+    __syncthreads();
+    const long long n = g.sN;
+    const long long stride = (g.sN + 63) / 64 * 64;
+    double* wp = g.V + static_cast<long long>(j + 1) * stride;
+    for (int c = blockIdx.x; c < g.nchunks; c += gridDim.x) {
+        double w[kRedPerThread];
+        load_chunk(wp, n, c, w);
+        for (int i = 0; i < nb; ++i) {
+            double v[kRedPerThread];
+            load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v);
+            const double h = cf[i];
+#pragma unroll
+            for (int q = 0; q < kRedPerThread; ++q) w[q] = w[q] - h * v[q];
+        }
+        store_chunk(wp, n, c, w);
+        warp_tree_store(chunk_dot_local(w, w), red, nv, nb);
+        for (int i = nb - 1; i >= 0; --i) {
+            double v[kRedPerThread];
+            load_chunk_l2(g.V + static_cast<long long>(i) * stride, n, c, v);
+            warp_tree_store(chunk_dot_local(v, w), red, nv, i);
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < nv; q += kRedThreads)
+            g.partials[static_cast<long long>(q) * g.nchunks + c] = warp_sum8(red, nv, q);
+        __syncthreads();
+    }
+    if (!elect_last(g.counters + 8)) return;
+    double* res = red + (kRedThreads / 32) * nv;
+    final_reduce(g.partials, g.nchunks, nv, red, res);
+    if (threadIdx.x == 0) {
+        const double nrm = sqrt(res[nb]);
+        ctl->after = nrm;
+        if (nrm < 0.70710678118654752 * ctl->before) {
+            ctl->reorth = 1;
+            for (int i = 0; i < nb; ++i) ctl->y[i] = res[i];
+        } else {
+            ctl->reorth = 0;
+            ctl->hnext = nrm;
+            arnoldi_tail(g);
+        }
+        g.counters[8] = 0u;
     }
 }
 
@@ -971,6 +1055,19 @@ void gm_update(const GmresBufs& g, int pass, cudaStream_t st) {
     launch(k_gm_update, g.nchunks, kRedThreads, sizeof(double) * (kRedThreads / 32 + 1 + kMaxRestart + 8), st, g, pass);
 }
 
+void gm_update_cgs2(const GmresBufs& g, cudaStream_t st) {
+    static int ctas = [] {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const char* e = std::getenv("IRK_CGS2_CTAS_PER_SM");
+        return sms * (e ? std::max(1, std::atoi(e)) : 1);
+    }();
+    const int grid = std::min(g.nchunks, ctas);
+    const size_t smem = sizeof(double) * ((kRedThreads / 32 + 1) * (kMaxRestart + 2) + kMaxRestart + 16);
+    launch(k_gm_update_cgs2, grid, kRedThreads, smem, st, g);
+}
+
 void gm_normalize(const GmresBufs& g, cudaStream_t st) {
     launch(k_gm_normalize, g.nchunks, kRedThreads, 0, st, g);
 }
@@ -992,6 +1089,9 @@ void dot(const double* x, const double* y, long long n, double* partials, unsign
 }
 
 void set_smem_limits() {
+    cudaFuncSetAttribute(k_gm_update_cgs2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(sizeof(double) * ((kRedThreads / 32 + 1) * (kMaxRestart + 2) +
+                                                            kMaxRestart + 16)));
     cudaFuncSetAttribute(k_dense_mv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const int nv = kMaxRestart + 2;
     cudaFuncSetAttribute(k_gm_blockdot, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -162,6 +162,8 @@ void gm_cycle_begin(const GmresBufs& g, const double* r, cudaStream_t st);
 void gm_blockdot(const GmresBufs& g, int pass, cudaStream_t st);
 // w -= V h (pass 1) / w -= V c, h += c (pass 2), ||w||, scalar tail.
 void gm_update(const GmresBufs& g, int pass, cudaStream_t st);
+// Pass-1 update fused with the pass-2 block-dot (counter slot 8).
+void gm_update_cgs2(const GmresBufs& g, cudaStream_t st);
 // V_{j+1} = w / h_{j+1,j} if continuing; advance j; set loop condition.
 void gm_normalize(const GmresBufs& g, cudaStream_t st);
 // y = H^-1 g (1 thread) then x += Z y.

@@ -251,6 +251,7 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
                            std::vector<Hierarchy> hiers, int device)
     : s_(s), device_(device), At_(At), structure_(structure), ht_(ht) {
     compress_values_ = std::getenv("IRK_NO_VALUE_CODES") == nullptr;
+    fused_cgs2_ = std::getenv("IRK_NO_FUSED_CGS2") == nullptr;
     const auto t0 = std::chrono::steady_clock::now();
     check(s >= 1 && s <= dev::kMaxStages, "device solver: s must be in 1..7");
     check(M.rows == M.cols && K.rows == K.cols && M.rows == K.rows,
@@ -293,7 +294,7 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
         std::getenv("IRK_TAIL_ROWS") ? std::atoi(std::getenv("IRK_TAIL_ROWS")) : 0;
     tail_cluster_ = std::getenv("IRK_TAIL_CLUSTER") ? 16 : 1;
     static const int fused_rows =
-        std::getenv("IRK_FUSED_ROWS") ? std::atoi(std::getenv("IRK_FUSED_ROWS")) : 32768;
+        std::getenv("IRK_FUSED_ROWS") ? std::atoi(std::getenv("IRK_FUSED_ROWS")) : 0;
     // L2-persisting pool for the coarse levels (>= 1): their kernels are
     // latency-bound and re-read every V-cycle, while the fine level streams
     // gigabytes per GMRES iteration through L2 and would evict them.
@@ -645,8 +646,12 @@ void DeviceSolver::record_iteration() {
     record_precond(slot(gb_.V, jp, stride_, 0), slot(gb_.Z, jp, stride_, 0));
     record_stage_op(slot(gb_.Z, jp, stride_, 0), slot(gb_.V, jp, stride_, 1));
     dev::gm_blockdot(gb_, 1, st_);
-    dev::gm_update(gb_, 1, st_);
-    dev::gm_blockdot(gb_, 2, st_);
+    if (fused_cgs2_) {
+        dev::gm_update_cgs2(gb_, st_);
+    } else {
+        dev::gm_update(gb_, 1, st_);
+        dev::gm_blockdot(gb_, 2, st_);
+    }
     dev::gm_update(gb_, 2, st_);
     dev::gm_normalize(gb_, st_);
 }

@@ -169,6 +169,7 @@ private:
     int launches_per_iter_ = 0;
     std::array<int, 4> launch_counts_{};
     bool compress_values_ = true;
+    bool fused_cgs2_ = true;
 };
 
 }  // namespace irkb
