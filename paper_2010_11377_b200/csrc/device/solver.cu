@@ -251,7 +251,7 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
                            std::vector<Hierarchy> hiers, int device)
     : s_(s), device_(device), At_(At), structure_(structure), ht_(ht) {
     compress_values_ = std::getenv("IRK_NO_VALUE_CODES") == nullptr;
-    fused_cgs2_ = std::getenv("IRK_NO_FUSED_CGS2") == nullptr;
+    fused_cgs2_ = std::getenv("IRK_FUSED_CGS2") != nullptr;  // opt-in: A/B break-even
     const auto t0 = std::chrono::steady_clock::now();
     check(s >= 1 && s <= dev::kMaxStages, "device solver: s must be in 1..7");
     check(M.rows == M.cols && K.rows == K.cols && M.rows == K.rows,
