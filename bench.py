@@ -74,7 +74,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -333,15 +333,26 @@ def our_arm(args):
                                            C.byref(d_), C.byref(f_)))
             lv.append((a.value, b_.value, c_.value, d_.value))
         levels.append(lv)
-    kms = C.c_double()
-    _abi.check(L.irkdev_time_kernel(dev._h, 1, 200, C.byref(kms)))
-    nd = 7
-    # algorithmic bytes of one smoother launch: 7 diagonals of values,
-    # x, r, wd read once, y written once
-    k_bytes = 8 * nd * n + 4 * 8 * n
     pk = peaks()
     hbm_peak = pk.get("hbm_gbs", 6650.0)
+    # Dominant kernel (launch list, profiles/r1): the GMRES classical
+    # Gram-Schmidt block-dot.  Algorithmic bytes of one launch at the average
+    # inner index j = 15: (j + 2) basis/work vectors of sN doubles read once.
+    jd = 15
+    kms = C.c_double()
+    _abi.check(L.irkdev_time_kernel(dev._h, 100 + jd, 50, C.byref(kms)))
+    k_bytes = (jd + 2) * 8 * S * n
     k_gbs = k_bytes / (kms.value * 1e-3) / 1e9
+    traffic = None
+    try:  # dram__bytes_read.sum + dram__bytes_write.sum of the same launch (ncu --set full)
+        traffic = json.loads((ROOT / "profiles" / "r1" / "traffic.json").read_text())["k_gm_blockdot_j15"]
+    except Exception:
+        pass
+    # fine-level smoother (DIA, u8 value codes): bytes it must move in its own
+    # format (7 code bytes + x, r, diagonal code, y per row)
+    sms = C.c_double()
+    _abi.check(L.irkdev_time_kernel(dev._h, 1, 200, C.byref(sms)))
+    s_bytes = (7 + 8 + 8 + 1 + 8) * n
     # whole-solve byte model on the actual hierarchies and iterations
     nnz_mk = prob.M.nnz
     model = [solve_bytes(info, levels, (r.iterations, r.n_reorth, r.cycles), n, S, nnz_mk)[0]
@@ -363,11 +374,15 @@ def our_arm(args):
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 4 * 8 + 8 * 501,
                 "wall_seconds": wall_e2e},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "fine-level Jacobi smoother SpMV (DIA, k_spmv_dia)",
+        "roofline": {"bound": "hbm", "kernel": "k_gm_blockdot (CGS block-dot, j=15: 17 x sN doubles)",
                      "achieved": k_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": k_gbs / hbm_peak,
-                     "traffic": None, "bytes_per_launch": k_bytes,
+                     "traffic": traffic, "bytes_per_launch": k_bytes, "ms_per_launch": kms.value,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in pk
                      else "fallback 6650 GB/s (B200_PROFILING.md)"},
+        "smoother_roofline": {"kernel": "fine-level Jacobi smoother k_spmv_dia (DIA, u8 value codes)",
+                              "bytes_per_launch": s_bytes, "ms_per_launch": sms.value,
+                              "achieved_gbs": s_bytes / (sms.value * 1e-3) / 1e9,
+                              "frac": s_bytes / (sms.value * 1e-3) / 1e9 / hbm_peak},
         "solve_roofline": {"model_bytes_per_solve": sum(model) / len(model),
                            "achieved_gbs": solve_gbs, "peak_gbs": hbm_peak,
                            "frac": solve_gbs / hbm_peak,

@@ -145,7 +145,9 @@ int irkdev_dot(irkdev* d, const double* x, const double* y, long long n, double*
 
 /* Roofline hook: mean ms per launch of a hot kernel, CUDA events on the
  * solver stream.  which: 0 stage operator, 1 fine smoother SpMV,
- * 2 preconditioner apply, 3 V-cycle. */
+ * 2 preconditioner apply, 3 V-cycle, 4+l V-cycle below level l+1,
+ * 100+j GMRES block-dot at inner index j, 20 / 21 empty-kernel launch
+ * floor in a graph / on the stream. */
 int irkdev_time_kernel(irkdev* d, int which, int reps, double* ms);
 /* Kernel launches per GMRES iteration in the captured graph body, and the
  * graph mode (1 conditional WHILE nodes, 0 host-driven). */

@@ -997,7 +997,66 @@ double DeviceSolver::dot(const double* x, const double* y, long long n) {
     return out;
 }
 
+namespace {
+__global__ void k_empty() {}
+}  // namespace
+
 double DeviceSolver::time_kernel(int which, int reps) {
+    if (which >= 100 && which < 100 + dev::kMaxRestart) {
+        // GMRES block-dot (pass 1) with j = which - 100 (j+2 vectors of sN)
+        const int j = which - 100;
+        ensure_gmres(std::max(50, j + 2), 500);
+        IRK_CUDA_CHECK(cudaMemsetAsync(gb_.V, 0, sizeof(double) * stride_ * (j + 2), st_));
+        IRK_CUDA_CHECK(cudaMemcpyAsync(&gb_.ctl->j, &j, sizeof(int), cudaMemcpyHostToDevice, st_));
+        const int zero = 0;
+        IRK_CUDA_CHECK(cudaMemcpyAsync(&gb_.ctl->reorth, &zero, sizeof(int), cudaMemcpyHostToDevice, st_));
+        gb_.use_cond = 0;
+        dev::gm_blockdot(gb_, 1, st_);
+        cudaEvent_t e0, e1;
+        IRK_CUDA_CHECK(cudaEventCreate(&e0));
+        IRK_CUDA_CHECK(cudaEventCreate(&e1));
+        IRK_CUDA_CHECK(cudaEventRecord(e0, st_));
+        for (int i = 0; i < reps; ++i) dev::gm_blockdot(gb_, 1, st_);
+        IRK_CUDA_CHECK(cudaEventRecord(e1, st_));
+        IRK_CUDA_CHECK(cudaEventSynchronize(e1));
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        g_restart_ = -1;  // graphs captured the old use_cond; rebuild on the next step
+        return static_cast<double>(ms) / reps;
+    }
+    if (which == 20 || which == 21) {
+        // launch floor: 100 dependent empty kernels, graph (20) or stream (21)
+        cudaEvent_t e0, e1;
+        IRK_CUDA_CHECK(cudaEventCreate(&e0));
+        IRK_CUDA_CHECK(cudaEventCreate(&e1));
+        cudaGraphExec_t ge = nullptr;
+        if (which == 20) {
+            cudaGraph_t g;
+            IRK_CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+            for (int i = 0; i < 100; ++i) k_empty<<<1, 32, 0, st_>>>();
+            IRK_CUDA_CHECK(cudaStreamEndCapture(st_, &g));
+            IRK_CUDA_CHECK(cudaGraphInstantiate(&ge, g, 0));
+            cudaGraphDestroy(g);
+            IRK_CUDA_CHECK(cudaGraphLaunch(ge, st_));
+        }
+        IRK_CUDA_CHECK(cudaEventRecord(e0, st_));
+        for (int r = 0; r < reps; ++r) {
+            if (ge)
+                IRK_CUDA_CHECK(cudaGraphLaunch(ge, st_));
+            else
+                for (int i = 0; i < 100; ++i) k_empty<<<1, 32, 0, st_>>>();
+        }
+        IRK_CUDA_CHECK(cudaEventRecord(e1, st_));
+        IRK_CUDA_CHECK(cudaEventSynchronize(e1));
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ge) cudaGraphExecDestroy(ge);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return static_cast<double>(ms) / (reps * 100.0);
+    }
     DevBuf a(sizeof(double) * stride_), b(sizeof(double) * stride_);
     IRK_CUDA_CHECK(cudaMemsetAsync(a.as<void>(), 0, sizeof(double) * stride_, st_));
     auto once = [&]() {

@@ -106,7 +106,9 @@ public:
     // Timing hooks for the roofline (bench.py): launches `reps` applications
     // of the named hot kernel between CUDA events on the solver's stream and
     // returns the mean milliseconds per launch.  which: 0 stage operator,
-    // 1 fine-level smoother SpMV, 2 preconditioner apply, 3 V-cycle.
+    // 1 fine-level smoother SpMV, 2 preconditioner apply, 3 V-cycle, 4.. V-cycle
+    // below level which-3, 100+j GMRES block-dot at inner index j, 20/21 empty-
+    // kernel launch floor (graph / stream).
     double time_kernel(int which, int reps);
     int launches_per_iteration() const { return launches_per_iter_; }
     const std::array<int, 4>& launch_counts() const { return launch_counts_; }

@@ -16,7 +16,8 @@ Pc = P.BlockPreconditioner(prob.M, prob.F, P.precond_coeff(t, P.CoeffKind.LowerF
 L = _abi.lib()
 names = {0: "stage operator", 1: "fine smoother SpMV", 2: "precond apply (3 V-cycles + 2 sweeps)",
          3: "V-cycle (hierarchy 0)", 4: "V-cycle below level 1", 5: "V-cycle below level 2",
-         6: "V-cycle below level 3"}
+         6: "V-cycle below level 3", 115: "GMRES block-dot j=15 (17 vectors)",
+         20: "empty kernel, graph launch (per kernel)", 21: "empty kernel, stream launch (per kernel)"}
 for w, name in names.items():
     ms = C.c_double()
     _abi.check(L.irkdev_time_kernel(Pc._dev._h, w, 50, C.byref(ms)))
