@@ -125,7 +125,12 @@ const T* DeviceSolver::upload_array(const std::vector<T>& h) {
 
 // Stores the entry values (fp64 or dictionary codes) of an operator.
 void DeviceSolver::upload_values(dev::Mat& m, const std::vector<double>& vals, double omega) {
-    Dict d = compress_values_ ? encode(vals) : Dict{};
+    // Small operators keep fp64 values: their kernels are latency-bound and a
+    // dictionary lookup is one more dependent memory trip.
+    static const long long min_rows =
+        std::getenv("IRK_CODES_MIN_ROWS") ? std::atoll(std::getenv("IRK_CODES_MIN_ROWS")) : 0;
+    const bool small = std::max(m.rows, m.cols) < min_rows;
+    Dict d = compress_values_ && !small ? encode(vals) : Dict{};
     m.vf = d.vf;
     if (d.vf == dev::kF64) {
         m.val = upload_array(vals);
