@@ -24,6 +24,11 @@ inline int blocks_for(long long n, int t) { return static_cast<int>((n + t - 1) 
 
 }  // namespace
 
+bool p1_enabled() {
+    static const bool on = std::getenv("IRK_NO_P1") == nullptr;
+    return on;
+}
+
 bool pdl_enabled() {
     static const bool on = std::getenv("IRK_PDL") != nullptr;
     return on;
@@ -119,7 +124,7 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
     const double* __restrict__ wd = a.wd;
     const unsigned char* dcode = nullptr;
     if constexpr (WDT == 1)
-        dcode = static_cast<const unsigned char*>(A.val) + static_cast<long long>(A.diag0) * n;
+        dcode = static_cast<const unsigned char*>(A.val) + static_cast<long long>(A.diag0) * A.dstride;
     const int nd = ND > 0 ? ND : A.nd;
     double s = 0.0;
 #pragma unroll
@@ -133,12 +138,87 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
         } else {
             xv = x[c];
         }
-        s += vfetch<VF>(A.val, static_cast<long long>(d) * n + i, tab) * xv;
+        s += vfetch<VF>(A.val, static_cast<long long>(d) * A.dstride + i, tab) * xv;
     }
     double wdi = 0.0;
     if (EPI == kESmooth || (EPI == kEProlong && !a.zb))
         wdi = WDT == 1 ? s_wd[__ldg(dcode + i)] : wd[i];
     a.y.get()[i] = spmv_epilogue<XM, EPI>(s, wdi, i, a, r, x);
+}
+
+// P1 SW-NE stencil, u8 codes, omega/diag from the diagonal code: 4
+// consecutive rows per thread.  The 7 offsets {-w-1,-w,-1,0,1,w,w+1} of 4
+// rows need only three windows of x (5 + 6 + 5 values instead of 28
+// gathers) and one 32-bit load of codes per diagonal.  Per-row sums keep the
+// ascending-offset order of k_spmv_dia, so results are bit-identical.
+template <int XM, int EPI>
+__global__ void __launch_bounds__(256) k_spmv_p1(Mat A, SpmvArgs a) {
+    __shared__ double s_tab[256];
+    __shared__ double s_wd[256];
+    const double* tab = load_tab<kU8>(A, s_tab, s_wd);
+    pdl_wait();
+    const int n = A.rows, w = A.p1w;
+    const int i0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i0 >= n) return;
+    const double* r = a.r.base ? a.r.get() : nullptr;
+    const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
+    const unsigned char* code = static_cast<const unsigned char*>(A.val);
+    const unsigned char* dcode = code + static_cast<long long>(A.diag0) * A.dstride;
+    auto cl = [n](int c) { return min(max(c, 0), n - 1); };
+    // windows of the x operand (XM: wd .* r) at columns i0-w-1.., i0-1.., i0+w..
+    double wa[5], wb[6], wc[5];
+    double rb[6] = {};
+    unsigned char db[6] = {};
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        const int c = cl(i0 - 1 + q);
+        if constexpr (XM == kXWdR) {
+            rb[q] = r[c];
+            db[q] = __ldg(dcode + c);
+            wb[q] = s_wd[db[q]] * rb[q];
+        } else {
+            wb[q] = x[c];
+            if (EPI != kEPlain) {
+                rb[q] = r[c];
+                db[q] = __ldg(dcode + c);
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const int ca = cl(i0 - w - 1 + q), cc = cl(i0 + w + q);
+        if constexpr (XM == kXWdR) {
+            wa[q] = s_wd[__ldg(dcode + ca)] * r[ca];
+            wc[q] = s_wd[__ldg(dcode + cc)] * r[cc];
+        } else {
+            wa[q] = x[ca];
+            wc[q] = x[cc];
+        }
+    }
+    unsigned cd[7];
+#pragma unroll
+    for (int d = 0; d < 7; ++d)
+        cd[d] = __ldg(reinterpret_cast<const unsigned*>(code + static_cast<long long>(d) * A.dstride + i0));
+    double* y = a.y.get();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int i = i0 + q;
+        if (i >= n) break;
+        auto av = [&](int d) { return tab[(cd[d] >> (8 * q)) & 0xffu]; };
+        double s = 0.0;
+        s += av(0) * wa[q];
+        s += av(1) * wa[q + 1];
+        s += av(2) * wb[q];
+        s += av(3) * wb[q + 1];
+        s += av(4) * wb[q + 2];
+        s += av(5) * wc[q];
+        s += av(6) * wc[q + 1];
+        double out = s;
+        if (EPI == kEResid) out = rb[q + 1] - s;
+        if (EPI == kESmooth) out = x[i] + s_wd[db[q + 1]] * (rb[q + 1] - s);
+        if (EPI == kEProlong) out = (a.zb ? a.zb[i] : s_wd[db[q + 1]] * rb[q + 1]) + s;
+        y[i] = out;
+    }
 }
 
 // SELL-32: one warp per 32-row slice, entries column-major inside the slice,
@@ -225,7 +305,9 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
 
 template <int XM, int EPI, int VF>
 void launch_spmv_vf(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
-    if (A.fmt == kDia) {
+    if (A.fmt == kDia && VF == kU8 && A.p1w > 0 && A.wdtab && A.diag0 >= 0 && p1_enabled()) {
+        launch(k_spmv_p1<XM, EPI>, blocks_for((A.rows + 3) / 4, 256), 256, 0, st, A, a);
+    } else if (A.fmt == kDia) {
         const int nb = blocks_for(A.rows, 256);
         const bool wdt = VF == kU8 && A.wdtab && A.diag0 >= 0;
         if (A.nd == 7) {
@@ -286,7 +368,7 @@ __global__ void __launch_bounds__(256) k_stage_op_dia(Mat M, Mat K, StageCoef cf
     for (int d = 0; d < (ND > 0 ? ND : kMaxDiags); ++d) {
         if (ND == 0 && d >= M.nd) break;
         const int c = min(max(i + M.off[d], 0), n - 1);
-        const long long e = static_cast<long long>(d) * n + i;
+        const long long e = static_cast<long long>(d) * M.dstride + i;
         const double m = vfetch<VF>(M.val, e, tm);
         const double k = vfetch<VF>(K.val, e, tk);
 #pragma unroll
@@ -323,7 +405,7 @@ __global__ void __launch_bounds__(256) k_sweep_dia(Mat K, VecRef wr, VecRef vr, 
     for (int d = 0; d < (ND > 0 ? ND : kMaxDiags); ++d) {
         if (ND == 0 && d >= K.nd) break;
         const int c = min(max(i + K.off[d], 0), n - 1);
-        f += vfetch<VF>(K.val, static_cast<long long>(d) * n + i, tk) * w[c];
+        f += vfetch<VF>(K.val, static_cast<long long>(d) * K.dstride + i, tk) * w[c];
     }
     if (store) store[i] = f;
     double acc = vr.get()[i];

@@ -47,6 +47,9 @@ struct Mat {
     int nd = 0;
     int off[kMaxDiags] = {};
     int diag0 = -1;                 // slot of offset 0
+    long long dstride = 0;          // entries per stored diagonal (>= rows, multiple of 4)
+    int p1w = 0;                    // > 0: offsets are the P1 SW-NE stencil
+                                    //   {-w-1, -w, -1, 0, 1, w, w+1}
     const double* wdtab = nullptr;  // omega / diagonal value per code (DIA, u8)
     size_t bytes = 0;               // device bytes of the stored operator
 };
@@ -72,6 +75,8 @@ struct SpmvArgs {
 
 // Programmatic dependent launch, opt-in via IRK_PDL=1.
 bool pdl_enabled();
+// The 4-rows-per-thread P1 stencil kernel (default on; IRK_NO_P1 disables).
+bool p1_enabled();
 
 void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st);
 

@@ -128,7 +128,7 @@ void DeviceSolver::upload_values(dev::Mat& m, const std::vector<double>& vals, d
     // Small operators keep fp64 values: their kernels are latency-bound and a
     // dictionary lookup is one more dependent memory trip.
     static const long long min_rows =
-        std::getenv("IRK_CODES_MIN_ROWS") ? std::atoll(std::getenv("IRK_CODES_MIN_ROWS")) : 0;
+        std::getenv("IRK_CODES_MIN_ROWS") ? std::atoll(std::getenv("IRK_CODES_MIN_ROWS")) : 500000;
     const bool small = std::max(m.rows, m.cols) < min_rows;
     Dict d = compress_values_ && !small ? encode(vals) : Dict{};
     m.vf = d.vf;
@@ -181,15 +181,22 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega, bool f
     if (dia) {
         std::sort(offs.begin(), offs.end());
         const int nd = static_cast<int>(offs.size());
-        std::vector<double> v(static_cast<size_t>(nd) * A.rows, 0.0);
+        const long long ds = (static_cast<long long>(A.rows) + 3) / 4 * 4;  // aligned stride
+        std::vector<double> v(static_cast<size_t>(nd) * ds, 0.0);
         for (int i = 0; i < A.rows; ++i)
             for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
                 const int d = static_cast<int>(std::lower_bound(offs.begin(), offs.end(), A.idx[k] - i) -
                                                offs.begin());
-                v[static_cast<size_t>(d) * A.rows + i] = A.val[k];
+                v[static_cast<size_t>(d) * ds + i] = A.val[k];
             }
         m.fmt = dev::kDia;
+        m.dstride = ds;
         m.nd = nd;
+        if (nd == 7) {
+            const int w = offs[5];
+            const int want[7] = {-w - 1, -w, -1, 0, 1, w, w + 1};
+            if (w >= 2 && std::equal(offs.begin(), offs.end(), want)) m.p1w = w;
+        }
         for (int d = 0; d < nd; ++d) {
             m.off[d] = offs[d];
             if (offs[d] == 0) m.diag0 = d;
