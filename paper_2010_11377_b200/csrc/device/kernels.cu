@@ -24,9 +24,12 @@ inline int blocks_for(long long n, int t) { return static_cast<int>((n + t - 1) 
 
 }  // namespace
 
-bool p1_enabled() {
-    static const bool on = std::getenv("IRK_NO_P1") == nullptr;
-    return on;
+// Bit mask of the P1-stencil (multi-row) kernels in use: 1 SpMV, 2 stage
+// operator, 4 sweep (IRK_P1_MASK; default none: A/B measured slower for the
+// SpMV, profiles/r1/ab8_p1.txt).
+int p1_mask() {
+    static const int m = std::getenv("IRK_P1_MASK") ? std::atoi(std::getenv("IRK_P1_MASK")) : 0;
+    return m;
 }
 
 bool pdl_enabled() {
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
 
 template <int XM, int EPI, int VF>
 void launch_spmv_vf(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
-    if (A.fmt == kDia && VF == kU8 && A.p1w > 0 && A.wdtab && A.diag0 >= 0 && p1_enabled()) {
+    if (A.fmt == kDia && VF == kU8 && A.p1w > 0 && A.wdtab && A.diag0 >= 0 && (p1_mask() & 1)) {
         launch(k_spmv_p1<XM, EPI>, blocks_for((A.rows + 3) / 4, 256), 256, 0, st, A, a);
     } else if (A.fmt == kDia) {
         const int nb = blocks_for(A.rows, 256);
@@ -385,6 +388,124 @@ __global__ void __launch_bounds__(256) k_stage_op_dia(Mat M, Mat K, StageCoef cf
 #pragma unroll
         for (int j = 0; j < S; ++j) acc += cf.c[b * S + j] * fk[j];
         y[static_cast<long long>(b) * n + i] = acc;
+    }
+}
+
+// Stage operator on the P1 stencil with u8 codes, RB consecutive rows per
+// thread (windows shared across the 7 offsets, as k_spmv_p1).  Same per-row
+// operation order as k_stage_op_dia.
+template <int S, int RB>
+__global__ void __launch_bounds__(256) k_stage_op_p1(Mat M, Mat K, StageCoef cf, VecRef zr,
+                                                     VecRef yr) {
+    __shared__ double s_tm[256];
+    __shared__ double s_tk[256];
+    __shared__ double s_dummy[1];
+    const double* tm = load_tab<kU8>(M, s_tm, s_dummy);
+    const double* tk = load_tab<kU8>(K, s_tk, s_dummy);
+    pdl_wait();
+    const int n = M.rows, w = M.p1w;
+    const int i0 = RB * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i0 >= n) return;
+    const double* __restrict__ z = zr.get();
+    double* __restrict__ y = yr.get();
+    auto cl = [n](int c) { return min(max(c, 0), n - 1); };
+    const unsigned char* mc = static_cast<const unsigned char*>(M.val);
+    const unsigned char* kc = static_cast<const unsigned char*>(K.val);
+    unsigned cmd[7], ckd[7];
+#pragma unroll
+    for (int d = 0; d < 7; ++d) {
+        const long long e = static_cast<long long>(d) * M.dstride + i0;
+        if constexpr (RB == 4) {
+            cmd[d] = __ldg(reinterpret_cast<const unsigned*>(mc + e));
+            ckd[d] = __ldg(reinterpret_cast<const unsigned*>(kc + e));
+        } else {
+            cmd[d] = __ldg(reinterpret_cast<const unsigned short*>(mc + e));
+            ckd[d] = __ldg(reinterpret_cast<const unsigned short*>(kc + e));
+        }
+    }
+    double fm[RB][S], fk[RB][S];
+#pragma unroll
+    for (int q = 0; q < RB; ++q)
+#pragma unroll
+        for (int j = 0; j < S; ++j) fm[q][j] = fk[q][j] = 0.0;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+        const double* zj = z + static_cast<long long>(j) * n;
+        double wa[RB + 1], wb[RB + 2], wc[RB + 1];
+#pragma unroll
+        for (int q = 0; q < RB + 1; ++q) {
+            wa[q] = zj[cl(i0 - w - 1 + q)];
+            wc[q] = zj[cl(i0 + w + q)];
+        }
+#pragma unroll
+        for (int q = 0; q < RB + 2; ++q) wb[q] = zj[cl(i0 - 1 + q)];
+#pragma unroll
+        for (int q = 0; q < RB; ++q) {
+            const double xs[7] = {wa[q], wa[q + 1], wb[q], wb[q + 1], wb[q + 2], wc[q], wc[q + 1]};
+#pragma unroll
+            for (int d = 0; d < 7; ++d) {
+                const double m = tm[(cmd[d] >> (8 * q)) & 0xffu];
+                const double k = tk[(ckd[d] >> (8 * q)) & 0xffu];
+                fm[q][j] += m * xs[d];
+                fk[q][j] += k * xs[d];
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < RB; ++q) {
+        const int i = i0 + q;
+        if (i >= n) break;
+#pragma unroll
+        for (int b = 0; b < S; ++b) {
+            double acc = fm[q][b];
+#pragma unroll
+            for (int j = 0; j < S; ++j) acc += cf.c[b * S + j] * fk[q][j];
+            y[static_cast<long long>(b) * n + i] = acc;
+        }
+    }
+}
+
+// Block sweep on the P1 stencil (u8): fresh = K w for 4 rows per thread.
+__global__ void __launch_bounds__(256) k_sweep_p1(Mat K, VecRef wr, VecRef vr, SweepTerms t,
+                                                  double* __restrict__ store, VecRef outr) {
+    __shared__ double s_tk[256];
+    __shared__ double s_dummy[1];
+    const double* tk = load_tab<kU8>(K, s_tk, s_dummy);
+    pdl_wait();
+    const int n = K.rows, w = K.p1w;
+    const int i0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i0 >= n) return;
+    const double* __restrict__ wv = wr.get();
+    auto cl = [n](int c) { return min(max(c, 0), n - 1); };
+    const unsigned char* kc = static_cast<const unsigned char*>(K.val);
+    unsigned ckd[7];
+#pragma unroll
+    for (int d = 0; d < 7; ++d)
+        ckd[d] = __ldg(reinterpret_cast<const unsigned*>(kc + static_cast<long long>(d) * K.dstride + i0));
+    double wa[5], wb[6], wc[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        wa[q] = wv[cl(i0 - w - 1 + q)];
+        wc[q] = wv[cl(i0 + w + q)];
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) wb[q] = wv[cl(i0 - 1 + q)];
+    const double* v = vr.get();
+    double* out = outr.get();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int i = i0 + q;
+        if (i >= n) break;
+        const double xs[7] = {wa[q], wa[q + 1], wb[q], wb[q + 1], wb[q + 2], wc[q], wc[q + 1]};
+        double f = 0.0;
+#pragma unroll
+        for (int d = 0; d < 7; ++d) f += tk[(ckd[d] >> (8 * q)) & 0xffu] * xs[d];
+        if (store) store[i] = f;
+        double acc = v[i];
+#pragma unroll
+        for (int k = 0; k < kMaxStages; ++k)
+            if (k < t.nt) acc += t.coef[k] * (t.buf[k] ? t.buf[k][i] : f);
+        out[i] = acc;
     }
 }
 
@@ -1052,6 +1173,18 @@ void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecR
     if (M.vf != K.vf || (M.vf != kF64 && M.vf != kU8))
         throw InvalidArgument("stage_op: M and K must share a value format (f64 or u8)");
     const bool u8 = M.vf == kU8;
+    if (u8 && M.p1w > 0 && M.p1w == K.p1w && M.dstride == K.dstride && (p1_mask() & 2)) {
+        switch (c.s) {
+#define IRK_OP_P1(S, RB)                                                                   \
+    case S:                                                                                \
+        launch(k_stage_op_p1<S, RB>, blocks_for((n + RB - 1) / RB, 256), 256, 0, st, M, K, c, z, y); \
+        return;
+            IRK_OP_P1(1, 4) IRK_OP_P1(2, 4) IRK_OP_P1(3, 4) IRK_OP_P1(4, 4) IRK_OP_P1(5, 2)
+            IRK_OP_P1(6, 2) IRK_OP_P1(7, 2)
+#undef IRK_OP_P1
+        default: break;
+        }
+    }
     switch (c.s) {
 #define IRK_OP_CASE(S)                                                             \
     case S:                                                                        \
@@ -1072,6 +1205,10 @@ void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecR
 
 void sweep_dia(const Mat& K, VecRef w, VecRef v, const SweepTerms& t, double* store, VecRef out,
                int n, cudaStream_t st) {
+    if (K.vf == kU8 && K.p1w > 0 && (p1_mask() & 4)) {
+        launch(k_sweep_p1, blocks_for((n + 3) / 4, 256), 256, 0, st, K, w, v, t, store, out);
+        return;
+    }
     switch (K.vf) {
     case kU8:
         if (K.nd == 7)

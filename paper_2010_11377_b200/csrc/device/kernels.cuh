@@ -75,8 +75,8 @@ struct SpmvArgs {
 
 // Programmatic dependent launch, opt-in via IRK_PDL=1.
 bool pdl_enabled();
-// The 4-rows-per-thread P1 stencil kernel (default on; IRK_NO_P1 disables).
-bool p1_enabled();
+// Multi-row P1-stencil kernels in use (bit mask, IRK_P1_MASK).
+int p1_mask();
 
 void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st);
 
