@@ -239,7 +239,7 @@ def our_arm(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2010_11377_b200 as P
-    from paper_2010_11377_b200 import _abi
+    from paper_2010_11377_b200 import _abi, replicas
     L = _abi.lib()
 
     t_setup = time.time()
@@ -272,8 +272,7 @@ def our_arm(args):
     nxt = torch.empty_like(cur)
     reps = []
     torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
+    replicas.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(st)
@@ -282,22 +281,17 @@ def our_arm(args):
             cur, nxt = nxt, cur
         e1.record(st)
         torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    if dist:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
-        dist.barrier()
+    ms = replicas.max_over_ranks(e0.elapsed_time(e1), device="cuda")
+    replicas.barrier()
     its = [r.iterations for r in reps]
-    value = world * args.steps / (ms / 1e3)
+    value = replicas.whole_job_throughput(args.steps, world, ms)
 
     # e2e: host pointers through the public C ABI (H2D u_n, D2H u_{n+1} + report)
     hu = torch.from_numpy(u0.copy()).pin_memory()
     hun = torch.empty_like(hu).pin_memory()
     hist = np.empty(501)
     torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
+    replicas.barrier()
     t0 = time.perf_counter()
     e2 = torch.cuda.Event(enable_timing=True)
     e3 = torch.cuda.Event(enable_timing=True)
@@ -309,12 +303,8 @@ def our_arm(args):
         hu, hun = hun, hu
     e3.record(st)
     torch.cuda.synchronize()
-    e2e_ms = e2.elapsed_time(e3)
+    e2e_ms = replicas.max_over_ranks(e2.elapsed_time(e3), device="cuda")
     wall_e2e = time.perf_counter() - t0
-    if dist:
-        t = torch.tensor([e2e_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = t.item()
 
     # launches inside the timed region: per-phase kernel counts of the graph
     cnt = (C.c_int * 4)()
@@ -370,7 +360,7 @@ def our_arm(args):
                           "true_rel_residual": [r.true_rel_residual for r in reps],
                           "launches_per_iteration": cnt[2], "setup_seconds": setup_s,
                           "hierarchy_sizes": [[x[0] for x in lv] for lv in levels]}),
-        "e2e": {"value": world * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+        "e2e": {"value": replicas.whole_job_throughput(args.steps, world, e2e_ms), "unit": UNIT,
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 4 * 8 + 8 * 501,
                 "wall_seconds": wall_e2e},
         "gpu_launches": launches,
