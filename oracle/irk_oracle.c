@@ -227,6 +227,12 @@ void or_precond_apply(const or_sys* S, const double* v, double* w) {
 }
 
 /* ------------------------------------------------------------ GMRES(m) */
+/* Orthogonalisation scheme: 1 = delayed classical Gram-Schmidt with
+ * re-orthogonalisation (DCGS2, the device default), 0 = CGS with the
+ * reference's conditional second pass (gmres.cpp:84-90). */
+static int g_ortho = 1;
+void or_set_ortho(int scheme) { g_ortho = scheme; }
+
 static double hyp(double a, double b) {
     a = fabs(a);
     b = fabs(b);
@@ -234,6 +240,147 @@ static double hyp(double a, double b) {
     if (mx == 0.0) return 0.0;
     const double r = mn / mx;
     return mx * sqrt(1.0 + r * r);
+}
+
+/* Rotates column `col` (entries 0..j+1, j = its index) into triangular form
+ * with the stored rotations, adds rotation j and updates g (gmres.cpp:93-112). */
+static void givens_column(double* col, int j, double* cs, double* sn, double* g) {
+    for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * col[i] + sn[i] * col[i + 1];
+        col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
+        col[i] = t;
+    }
+    const double denom = hyp(col[j], col[j + 1]);
+    double c = 1.0, sv = 0.0;
+    if (denom > 0.0) {
+        c = col[j] / denom;
+        sv = col[j + 1] / denom;
+    }
+    cs[j] = c;
+    sn[j] = sv;
+    col[j] = denom;
+    col[j + 1] = 0.0;
+    g[j + 1] = -sv * g[j];
+    g[j] = c * g[j];
+}
+
+/* One restart cycle of GMRES with delayed classical Gram-Schmidt
+ * re-orthogonalisation (DCGS2; Bielich, Langou, Thomas, Swirydowicz,
+ * Yamazaki, Boman 2022).  Slot j of V holds the once-orthogonalised,
+ * unnormalised vector vt_j until iteration j re-orthogonalises it against
+ * v_0..v_{j-1} in the same pass that projects w = A P^-1 vt_j:
+ *   block-dot : s_i = v_i.vt_j, p_i = v_i.w (i < j), sig = vt_j.vt_j, pi = vt_j.w
+ *   scalars   : alpha = sqrt(sig - sum s_i^2); column j-1 += s, h_{j,j-1} = alpha
+ *               (finalised, rotated, residual recorded); h_jj = (pi - s.p)/alpha
+ *   update    : v_j = (vt_j - sum s_i v_i)/alpha;  w' = w - sum p_i v_i - h_jj v_j
+ * so each iteration streams the basis twice instead of four times.  The stop
+ * test after iteration j uses the first-pass column with h_{j+1,j} = ||w'||;
+ * the last column is finalised by one more block-dot at the end of the cycle.
+ * Mirrors paper_2010_11377_b200/csrc/device/kernels.cu (k_dgs_*) bit for bit. */
+static void dcgs2_cycle(const or_sys* S, long N, int R, int budget, double* V, double* Z,
+                        double* H, double* g, double* cs, double* sn, double* s_, double* p_,
+                        const double* r, double bnorm, double* beta_io, double tol_c, int cycles,
+                        int* total, int* m_out, int* stop_out, double* final_rel, double* hist) {
+    double beta = *beta_io;
+    memcpy(V, r, sizeof(double) * N); /* vt_0 = r, unnormalised */
+    int j = 0, stop = 0;
+    double* col = (double*)malloc(sizeof(double) * (R + 2));
+    while (1) {
+        double* vt = V + (long)j * N;
+        double* w = V + (long)(j + 1) * N;
+        or_precond_apply(S, vt, Z + (long)j * N);
+        or_stage_apply(S, Z + (long)j * N, w);
+        for (int i = 0; i < j; ++i) {
+            s_[i] = or_dot(V + (long)i * N, vt, N);
+            p_[i] = or_dot(V + (long)i * N, w, N);
+        }
+        const double sig = or_dot(vt, vt, N);
+        const double pi = or_dot(vt, w, N);
+        double ss = 0.0, sp = 0.0;
+        for (int i = 0; i < j; ++i) ss += s_[i] * s_[i];
+        for (int i = 0; i < j; ++i) sp += s_[i] * p_[i];
+        const double a2 = sig - ss;
+        const double alpha = a2 > 0.0 ? sqrt(a2) : 0.0;
+        if (j == 0) {
+            beta = alpha;
+            g[0] = beta;
+        } else {
+            double* hc = H + (long)(j - 1) * (R + 1);
+            for (int i = 0; i < j; ++i) hc[i] = hc[i] + s_[i];
+            hc[j] = alpha;
+            givens_column(hc, j - 1, cs, sn, g);
+            *total += 1;
+            const double res_rel = fabs(g[j]) / beta;
+            const double hv = cycles == 0 ? res_rel : res_rel * beta / bnorm;
+            if (hist) hist[*total] = hv;
+            *final_rel = hv;
+        }
+        const double hjj = alpha > 0.0 ? (pi - sp) / alpha : 0.0;
+        double* hcj = H + (long)j * (R + 1);
+        for (int i = 0; i < j; ++i) hcj[i] = p_[i];
+        hcj[j] = hjj;
+        const double inv = alpha > 0.0 ? 1.0 / alpha : 0.0;
+        for (long k = 0; k < N; ++k) {
+            double v = vt[k], ww = w[k];
+            for (int i = 0; i < j; ++i) {
+                const double vi = V[(long)i * N + k];
+                v = v - s_[i] * vi;
+                ww = ww - p_[i] * vi;
+            }
+            v = v * inv;
+            ww = ww - hjj * v;
+            vt[k] = v;
+            w[k] = ww;
+        }
+        const double wn = sqrt(or_dot(w, w, N));
+        /* provisional test on the first-pass column */
+        for (int i = 0; i <= j; ++i) col[i] = hcj[i];
+        col[j + 1] = wn;
+        {
+            double gj = g[j], gn;
+            for (int i = 0; i < j; ++i) {
+                const double t = cs[i] * col[i] + sn[i] * col[i + 1];
+                col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
+                col[i] = t;
+            }
+            const double denom = hyp(col[j], col[j + 1]);
+            const double sv = denom > 0.0 ? col[j + 1] / denom : 0.0;
+            gn = -sv * gj;
+            const double res_prov = fabs(gn) / beta;
+            const int bad = !(res_prov == res_prov) || !(wn == wn) || !(alpha == alpha);
+            if (res_prov <= tol_c) stop = 1;
+            else if (wn <= 1e-14 * beta || bad || alpha == 0.0) stop = 2;
+            else if (j + 1 >= budget) stop = 3;
+            else stop = 0;
+        }
+        if (stop) break;
+        j += 1;
+    }
+    /* finalise column j against the fully orthogonal v_0..v_j */
+    {
+        double* w = V + (long)(j + 1) * N;
+        for (int i = 0; i <= j; ++i) s_[i] = or_dot(V + (long)i * N, w, N);
+        const double sig = or_dot(w, w, N);
+        double ss = 0.0;
+        for (int i = 0; i <= j; ++i) ss += s_[i] * s_[i];
+        const double a2 = sig - ss;
+        const double alpha = a2 > 0.0 ? sqrt(a2) : 0.0;
+        double* hc = H + (long)j * (R + 1);
+        for (int i = 0; i <= j; ++i) hc[i] = hc[i] + s_[i];
+        hc[j + 1] = alpha;
+        givens_column(hc, j, cs, sn, g);
+        *total += 1;
+        const double res_rel = fabs(g[j + 1]) / beta;
+        const double hv = cycles == 0 ? res_rel : res_rel * beta / bnorm;
+        if (hist) hist[*total] = hv;
+        *final_rel = hv;
+        if (stop == 1 && !(res_rel <= tol_c)) stop = 3; /* provisional pass, final fail: restart */
+        if (stop == 3 && res_rel <= tol_c) stop = 1;
+    }
+    free(col);
+    *m_out = j + 1;
+    *stop_out = stop;
+    *beta_io = beta;
 }
 
 int or_irk_step(const or_sys* S, const double* u, const double* lift, double rtol, int restart,
@@ -282,10 +429,16 @@ int or_irk_step(const or_sys* S, const double* u, const double* lift, double rto
         int budget = R < max_iter ? R : max_iter;
         double inv = 1.0 / bnorm;
         while (budget > 0) {
-            for (long k = 0; k < N; ++k) V[k] = r[k] * inv;
-            g[0] = beta;
             int j = 0, m = 0;
             stop = 0;
+            if (g_ortho == 1) {
+                dcgs2_cycle(S, N, R, budget, V, Z, H, g, cs, sn, h, cc, r, bnorm, &beta, tol_c,
+                            cycles, &total, &m, &stop, &final_rel, hist);
+                nre += m;
+                goto cycle_end;
+            }
+            for (long k = 0; k < N; ++k) V[k] = r[k] * inv;
+            g[0] = beta;
             while (1) {
                 double* vj = V + (long)j * N;
                 double* zj = Z + (long)j * N;
@@ -347,6 +500,7 @@ int or_irk_step(const or_sys* S, const double* u, const double* lift, double rto
                 for (long k = 0; k < N; ++k) w[k] = w[k] * hinv;
                 j += 1;
             }
+        cycle_end:
             /* y = H^-1 g, x += Z y (gmres.cpp:126-132, flexible form) */
             for (int i = m - 1; i >= 0; --i) {
                 double acc = g[i];
@@ -367,6 +521,7 @@ int or_irk_step(const or_sys* S, const double* u, const double* lift, double rto
                 converged = stop == 1;
                 break;
             }
+            (void)inv;
             beta = rn;
             tol_c = rtol * bnorm / rn;
             const int left = max_iter - total;

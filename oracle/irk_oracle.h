@@ -52,6 +52,10 @@ typedef struct {
     double seconds;
 } or_report;
 
+/* 1 (default): delayed CGS2 (the device's scheme); 0: CGS + conditional
+ * second pass (the device's former scheme, IRK_ORTHO=cgs2). */
+void or_set_ortho(int scheme);
+
 /* One IRK step: rhs, GMRES(restart) (right preconditioning, CGS with the
  * reference's conditional second pass, flexible basis), u_next.  hist gets
  * max_iter+1 entries (may be NULL). */

@@ -977,6 +977,211 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_update_cgs2(GmresBufs g) {
     }
 }
 
+// Rotates column col (entries 0..j+1) with rotations 0..j-1, adds rotation j
+// and updates g (gmres.cpp:93-112); identical to oracle givens_column().
+__device__ void givens_column(GmresCtl* c, double* col, int j) {
+    for (int i = 0; i < j; ++i) {
+        const double t = c->cs[i] * col[i] + c->sn[i] * col[i + 1];
+        col[i + 1] = -c->sn[i] * col[i] + c->cs[i] * col[i + 1];
+        col[i] = t;
+    }
+    const double denom = hyp(col[j], col[j + 1]);
+    double cs = 1.0, sn = 0.0;
+    if (denom > 0.0) {
+        cs = col[j] / denom;
+        sn = col[j + 1] / denom;
+    }
+    c->cs[j] = cs;
+    c->sn[j] = sn;
+    col[j] = denom;
+    col[j + 1] = 0.0;
+    c->g[j + 1] = -sn * c->g[j];
+    c->g[j] = cs * c->g[j];
+}
+
+// Records the residual estimate of a just-finalised column (history, total).
+__device__ void record_column(const GmresBufs& g, int col_index) {
+    GmresCtl* c = g.ctl;
+    c->total += 1;
+    const double res_rel = fabs(c->g[col_index + 1]) / c->beta;
+    const double hv = c->cycles == 0 ? res_rel : res_rel * c->beta / c->bnorm;
+    g.hist[c->total] = hv;
+    c->final_rel = hv;
+}
+
+// DCGS2 block-dot.  Iteration j (finalize = 0): targets A = slot j (vt_j) and
+// B = slot j+1 (w); values [s_0..s_{j-1}, p_0..p_{j-1}, A.A, A.B].
+// Cycle end (finalize = 1, j = last iteration): target B = slot j+1 (w');
+// values [s_0..s_j, B.B].  Per-pair chunk partials follow the reduction
+// contract (thread t's 16 elements in order, warp tree, warps in order).
+__global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot(GmresBufs g, int finalize) {
+    extern __shared__ double red[];
+    pdl_trigger();
+    pdl_wait();
+    GmresCtl* ctl = g.ctl;
+    const int j = ctl->j;
+    const int nvv = finalize ? j + 1 : j;   // basis vectors v_0..v_{nvv-1}
+    const int nv = finalize ? nvv + 1 : 2 * nvv + 2;
+    const int c = blockIdx.x;
+    const long long n = g.sN;
+    const long long stride = (g.sN + 63) / 64 * 64;
+    double b[kRedPerThread];
+    load_chunk(g.V + static_cast<long long>(j + 1) * stride, n, c, b);
+    if (finalize) {
+        warp_tree_store(chunk_dot_local(b, b), red, nv, nvv);
+        for (int i = 0; i < nvv; ++i) {
+            double v[kRedPerThread];
+            load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v);
+            warp_tree_store(chunk_dot_local(v, b), red, nv, i);
+        }
+    } else {
+        double a[kRedPerThread];
+        load_chunk(g.V + static_cast<long long>(j) * stride, n, c, a);
+        warp_tree_store(chunk_dot_local(a, a), red, nv, 2 * nvv);
+        warp_tree_store(chunk_dot_local(a, b), red, nv, 2 * nvv + 1);
+        for (int i = 0; i < nvv; ++i) {
+            double v[kRedPerThread];
+            load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v);
+            warp_tree_store(chunk_dot_local(v, a), red, nv, i);
+            warp_tree_store(chunk_dot_local(v, b), red, nv, nvv + i);
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nv; q += kRedThreads)
+        g.partials[static_cast<long long>(q) * g.nchunks + c] = warp_sum8(red, nv, q);
+    if (!elect_last(g.counters + 9)) return;
+    double* res = red + (kRedThreads / 32) * nv;
+    final_reduce(g.partials, g.nchunks, nv, red, res);
+    if (threadIdx.x != 0) return;
+    g.counters[9] = 0u;
+    const int ld = ctl->restart + 1;
+    double ss = 0.0, sp = 0.0;
+    for (int i = 0; i < nvv; ++i) ss += res[i] * res[i];
+    const double sig = res[finalize ? nvv : 2 * nvv];
+    const double a2 = sig - ss;
+    const double alpha = a2 > 0.0 ? sqrt(a2) : 0.0;
+    if (finalize) {
+        // complete column j against the orthonormal v_0..v_j
+        double* hc = g.H + static_cast<long long>(j) * ld;
+        for (int i = 0; i <= j; ++i) hc[i] = hc[i] + res[i];
+        hc[j + 1] = alpha;
+        givens_column(ctl, hc, j);
+        record_column(g, j);
+        const double res_rel = fabs(ctl->g[j + 1]) / ctl->beta;
+        if (ctl->stop == 1 && !(res_rel <= ctl->tol_c)) ctl->stop = 3;
+        if (ctl->stop == 3 && res_rel <= ctl->tol_c) ctl->stop = 1;
+        ctl->m = j + 1;
+        return;
+    }
+    for (int i = 0; i < nvv; ++i) {
+        ctl->sv[i] = res[i];
+        ctl->pv[i] = res[nvv + i];
+        sp += res[i] * res[nvv + i];
+    }
+    if (j == 0) {
+        ctl->beta = alpha;
+        ctl->g[0] = alpha;
+    } else {
+        double* hc = g.H + static_cast<long long>(j - 1) * ld;
+        for (int i = 0; i < j; ++i) hc[i] = hc[i] + res[i];
+        hc[j] = alpha;
+        givens_column(ctl, hc, j - 1);
+        record_column(g, j - 1);
+    }
+    const double pi = res[2 * nvv + 1];
+    const double hjj = alpha > 0.0 ? (pi - sp) / alpha : 0.0;
+    double* hcj = g.H + static_cast<long long>(j) * ld;
+    for (int i = 0; i < j; ++i) hcj[i] = res[nvv + i];
+    hcj[j] = hjj;
+    ctl->hjj = hjj;
+    ctl->inv_alpha = alpha > 0.0 ? 1.0 / alpha : 0.0;
+    ctl->hnext = alpha;
+    if (!(alpha == alpha)) ctl->bad = 1;
+}
+
+// DCGS2 update: v_j = (vt_j - sum_i s_i v_i) / alpha and
+// w' = w - sum_i p_i v_i - h_jj v_j in one pass (element-wise order as the
+// oracle), ||w'||^2, then the provisional stop test on the first-pass column.
+__global__ void __launch_bounds__(kRedThreads, 2) k_dgs_update(GmresBufs g) {
+    extern __shared__ double red[];
+    pdl_trigger();
+    pdl_wait();
+    GmresCtl* ctl = g.ctl;
+    const int j = ctl->j;
+    double* sc = red + kRedThreads / 32 + 1;  // s coefficients
+    double* pc = sc + j + 1;                  // p coefficients
+    for (int i = threadIdx.x; i < j; i += kRedThreads) {
+        sc[i] = ctl->sv[i];
+        pc[i] = ctl->pv[i];
+    }
+    __syncthreads();
+    const double inv = ctl->inv_alpha, hjj = ctl->hjj;
+    const int c = blockIdx.x;
+    const long long n = g.sN;
+    const long long stride = (g.sN + 63) / 64 * 64;
+    double* ap = g.V + static_cast<long long>(j) * stride;
+    double* bp = g.V + static_cast<long long>(j + 1) * stride;
+    double a[kRedPerThread], b[kRedPerThread];
+    load_chunk(ap, n, c, a);
+    load_chunk(bp, n, c, b);
+    for (int i = 0; i < j; ++i) {
+        double v[kRedPerThread];
+        load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v);
+        const double si = sc[i], pi = pc[i];
+#pragma unroll
+        for (int q = 0; q < kRedPerThread; ++q) {
+            a[q] = a[q] - si * v[q];
+            b[q] = b[q] - pi * v[q];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kRedPerThread; ++q) {
+        a[q] = a[q] * inv;
+        b[q] = b[q] - hjj * a[q];
+    }
+    store_chunk(ap, n, c, a);
+    store_chunk(bp, n, c, b);
+    warp_tree_store(chunk_dot_local(b, b), red, 1, 0);
+    __syncthreads();
+    if (threadIdx.x == 0) g.partials[c] = warp_sum8(red, 1, 0);
+    if (!elect_last(g.counters + 10)) return;
+    double* res = red + kRedThreads / 32;
+    final_reduce(g.partials, g.nchunks, 1, red, res);
+    if (threadIdx.x != 0) return;
+    g.counters[10] = 0u;
+    const double wn = sqrt(res[0]);
+    // provisional test: column j with h_{j+1,j} = ||w'||, rotations not stored
+    const int ld = ctl->restart + 1;
+    const double* hcj = g.H + static_cast<long long>(j) * ld;
+    double* col = ctl->hcol;
+    for (int i = 0; i <= j; ++i) col[i] = hcj[i];
+    col[j + 1] = wn;
+    for (int i = 0; i < j; ++i) {
+        const double t = ctl->cs[i] * col[i] + ctl->sn[i] * col[i + 1];
+        col[i + 1] = -ctl->sn[i] * col[i] + ctl->cs[i] * col[i + 1];
+        col[i] = t;
+    }
+    const double denom = hyp(col[j], col[j + 1]);
+    const double sv = denom > 0.0 ? col[j + 1] / denom : 0.0;
+    const double gn = -sv * ctl->g[j];
+    const double res_prov = fabs(gn) / ctl->beta;
+    const double alpha = ctl->hnext;
+    const int bad = !(res_prov == res_prov) || !(wn == wn) || !(alpha == alpha) || ctl->bad;
+    int stop;
+    if (res_prov <= ctl->tol_c)
+        stop = 1;
+    else if (wn <= 1e-14 * ctl->beta || bad || alpha == 0.0)
+        stop = 2;
+    else if (j + 1 >= ctl->budget)
+        stop = 3;
+    else
+        stop = 0;
+    ctl->stop = stop;
+    ctl->n_reorth += 1;
+    if (stop == 0) ctl->j = j + 1;
+    set_cond(g.h_inner, g.use_cond, stop == 0 ? 1u : 0u);
+}
+
 // V_{j+1} *= 1/h_{j+1,j} when the cycle continues; advance j.
 __global__ void __launch_bounds__(kRedThreads) k_gm_normalize(GmresBufs g) {
     pdl_trigger();
@@ -1004,7 +1209,7 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_normalize(GmresBufs g) {
 
 __global__ void __launch_bounds__(kRedThreads) k_gm_init(GmresBufs g, const double* __restrict__ b,
                                                          double* __restrict__ r, double rel_tol,
-                                                         int restart, int max_iter) {
+                                                         int restart, int max_iter, int ortho) {
     pdl_trigger();
     pdl_wait();
     __shared__ double red[kRedThreads / 32 + 1];
@@ -1027,6 +1232,7 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_init(GmresBufs g, const doub
         c->total = 0;
         c->cycles = 0;
         c->n_reorth = 0;
+        c->ortho = ortho;
         c->reorth = 0;
         c->bad = 0;
         c->j = 0;
@@ -1059,10 +1265,13 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_cycle_begin(GmresBufs g,
     pdl_wait();
     GmresCtl* ctl = g.ctl;
     const double inv = ctl->inv;
+    const bool dgs = ctl->ortho == 1;  // DCGS2: vt_0 = r, normalised by its first block-dot
     double v[kRedPerThread];
     load_chunk(r, g.sN, blockIdx.x, v);
+    if (!dgs) {
 #pragma unroll
-    for (int q = 0; q < kRedPerThread; ++q) v[q] = v[q] * inv;
+        for (int q = 0; q < kRedPerThread; ++q) v[q] = v[q] * inv;
+    }
     store_chunk(g.V, g.sN, blockIdx.x, v);
     if (!elect_last(g.counters + 6)) return;
     if (threadIdx.x == 0) {
@@ -1256,8 +1465,8 @@ void irk_update(const double* u, const double* x, const double* hb, int n, int s
 static size_t red_smem(int nv) { return sizeof(double) * (kRedThreads / 32 * nv + nv + 8); }
 
 void gm_init(const GmresBufs& g, const double* b, double* r, double rel_tol, int restart,
-             int max_iter, cudaStream_t st) {
-    launch(k_gm_init, g.nchunks, kRedThreads, 0, st, g, b, r, rel_tol, restart, max_iter);
+             int max_iter, int ortho, cudaStream_t st) {
+    launch(k_gm_init, g.nchunks, kRedThreads, 0, st, g, b, r, rel_tol, restart, max_iter, ortho);
 }
 
 void gm_cycle_begin(const GmresBufs& g, const double* r, cudaStream_t st) {
@@ -1287,6 +1496,19 @@ void gm_update_cgs2(const GmresBufs& g, cudaStream_t st) {
     launch(k_gm_update_cgs2, grid, kRedThreads, smem, st, g);
 }
 
+static size_t dgs_smem(const GmresBufs& g) {
+    const int nv = 2 * g.cap + 4;
+    return sizeof(double) * ((kRedThreads / 32 + 1) * nv + 16);
+}
+
+void gm_dgs_dot(const GmresBufs& g, int finalize, cudaStream_t st) {
+    launch(k_dgs_dot, g.nchunks, kRedThreads, dgs_smem(g), st, g, finalize);
+}
+
+void gm_dgs_update(const GmresBufs& g, cudaStream_t st) {
+    launch(k_dgs_update, g.nchunks, kRedThreads, dgs_smem(g), st, g);
+}
+
 void gm_normalize(const GmresBufs& g, cudaStream_t st) {
     launch(k_gm_normalize, g.nchunks, kRedThreads, 0, st, g);
 }
@@ -1308,6 +1530,9 @@ void dot(const double* x, const double* y, long long n, double* partials, unsign
 }
 
 void set_smem_limits() {
+    const int big = static_cast<int>(sizeof(double) * ((kRedThreads / 32 + 1) * (2 * kMaxRestart + 4) + 16));
+    cudaFuncSetAttribute(k_dgs_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_dgs_update, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_gm_update_cgs2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(double) * ((kRedThreads / 32 + 1) * (kMaxRestart + 2) +
                                                             kMaxRestart + 16)));

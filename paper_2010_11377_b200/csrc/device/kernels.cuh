@@ -140,6 +140,11 @@ struct GmresCtl {
     double sn[kMaxRestart];
     double hcol[kMaxRestart + 2];
     double y[kMaxRestart];
+    // delayed CGS2 (DCGS2) scalars of the current iteration
+    double sv[kMaxRestart + 1];  // s_i = v_i . vt_j   (re-orthogonalisation of vt_j)
+    double pv[kMaxRestart + 1];  // p_i = v_i . w      (projections of w)
+    double hjj, inv_alpha;
+    int ortho;                   // 1 DCGS2, 0 CGS + conditional second pass
 };
 
 struct GmresBufs {
@@ -155,12 +160,13 @@ struct GmresBufs {
     cudaGraphConditionalHandle h_inner;
     cudaGraphConditionalHandle h_outer;
     int use_cond;       // 1 when running inside conditional graph nodes
+    int cap;            // restart capacity (sizes the DCGS2 reduction buffers)
 };
 
 // b -> r copy and ||b||; initialises the control block (bnorm == 0 ends the
 // solve: x = 0).
 void gm_init(const GmresBufs& g, const double* b, double* r, double rel_tol,
-             int restart, int max_iter, cudaStream_t st);
+             int restart, int max_iter, int ortho, cudaStream_t st);
 // V_0 = r / beta, g_0 = beta, j = 0 (start of a restart cycle).
 void gm_cycle_begin(const GmresBufs& g, const double* r, cudaStream_t st);
 // h = V_{0..j}^T w and ||w||  (pass 1), or c = V^T w (pass 2, if reorth).
@@ -169,6 +175,12 @@ void gm_blockdot(const GmresBufs& g, int pass, cudaStream_t st);
 void gm_update(const GmresBufs& g, int pass, cudaStream_t st);
 // Pass-1 update fused with the pass-2 block-dot (counter slot 8).
 void gm_update_cgs2(const GmresBufs& g, cudaStream_t st);
+// Delayed CGS2 (the default orthogonalisation): one fused block-dot
+// (s = V_{j-1}^T vt_j, p = V_{j-1}^T w, vt_j.vt_j, vt_j.w; finalises column
+// j-1) and one fused update (v_j, w') per iteration; `finalize` runs the
+// cycle-end block-dot that completes the last column.
+void gm_dgs_dot(const GmresBufs& g, int finalize, cudaStream_t st);
+void gm_dgs_update(const GmresBufs& g, cudaStream_t st);
 // V_{j+1} = w / h_{j+1,j} if continuing; advance j; set loop condition.
 void gm_normalize(const GmresBufs& g, cudaStream_t st);
 // y = H^-1 g (1 thread) then x += Z y.

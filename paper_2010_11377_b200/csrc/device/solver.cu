@@ -264,6 +264,10 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
     : s_(s), device_(device), At_(At), structure_(structure), ht_(ht) {
     compress_values_ = std::getenv("IRK_NO_VALUE_CODES") == nullptr;
     fused_cgs2_ = std::getenv("IRK_FUSED_CGS2") != nullptr;  // opt-in: A/B break-even
+    {
+        const char* o = std::getenv("IRK_ORTHO");
+        ortho_ = (o && std::string(o) == "cgs2") ? 0 : 1;
+    }
     const auto t0 = std::chrono::steady_clock::now();
     check(s >= 1 && s <= dev::kMaxStages, "device solver: s must be in 1..7");
     check(M.rows == M.cols && K.rows == K.cols && M.rows == K.rows,
@@ -657,6 +661,11 @@ void DeviceSolver::record_iteration() {
     const int* jp = &gb_.ctl->j;
     record_precond(slot(gb_.V, jp, stride_, 0), slot(gb_.Z, jp, stride_, 0));
     record_stage_op(slot(gb_.Z, jp, stride_, 0), slot(gb_.V, jp, stride_, 1));
+    if (ortho_ == 1) {
+        dev::gm_dgs_dot(gb_, 0, st_);
+        dev::gm_dgs_update(gb_, st_);
+        return;
+    }
     dev::gm_blockdot(gb_, 1, st_);
     if (fused_cgs2_) {
         dev::gm_update_cgs2(gb_, st_);
@@ -703,6 +712,7 @@ void DeviceSolver::ensure_gmres(int restart, int max_iter) {
     gb_.Z = Z_.as<double>();
     gb_.sN = sN_;
     gb_.nchunks = nch;
+    gb_.cap = cap_restart_;
 }
 
 namespace {
@@ -781,10 +791,11 @@ void DeviceSolver::build_graph(bool lift, int restart, int max_iter, double rtol
         dev::spmv(K_, dev::kXPlain, dev::kEPlain, a, st_);
         dev::stage_rhs_finish(ku_, lift ? lift_ : nullptr, b_, n_, s_, st_);
         IRK_CUDA_CHECK(cudaMemsetAsync(x_, 0, sizeof(double) * sN_, st_));
-        dev::gm_init(gb_, b_, r_, rtol, restart, max_iter, st_);
+        dev::gm_init(gb_, b_, r_, rtol, restart, max_iter, ortho_, st_);
     };
     auto cycle_begin = [&]() { dev::gm_cycle_begin(gb_, r_, st_); };
     auto cycle_end = [&]() {
+        if (ortho_ == 1) dev::gm_dgs_dot(gb_, 1, st_);
         dev::gm_solution(gb_, x_, st_);
         record_stage_op(dev::plain(x_), dev::plain(ax_));
         dev::gm_residual(gb_, b_, ax_, r_, st_);

@@ -172,6 +172,7 @@ private:
     std::array<int, 4> launch_counts_{};
     bool compress_values_ = true;
     bool fused_cgs2_ = true;
+    int ortho_ = 1;  // 1 DCGS2 (default), 0 CGS + conditional second pass
 };
 
 }  // namespace irkb

@@ -275,6 +275,7 @@ class Oracle:
             L.or_precond_apply.argtypes = [C.POINTER(or_sys), dptr, dptr]
             L.or_irk_step.argtypes = [C.POINTER(or_sys), dptr, dptr, C.c_double, C.c_int, C.c_int,
                                       dptr, dptr, C.POINTER(or_report), dptr]
+            L.or_set_ortho.argtypes = [C.c_int]
             cls._lib = L
         return cls._lib
 
@@ -349,6 +350,11 @@ class OracleSystem:
                 "n_reorth": rep.n_reorth, "converged": bool(rep.converged),
                 "true_rel": rep.true_rel, "final_rel": rep.final_rel, "seconds": rep.seconds,
                 "history": hist[: rep.iterations + 1].copy()}
+
+
+def oracle_ortho(scheme: str) -> None:
+    """Selects the oracle's orthogonalisation: 'dcgs2' (device default) or 'cgs2'."""
+    Oracle.lib().or_set_ortho(1 if scheme == "dcgs2" else 0)
 
 
 def oracle_dot(x, y):
