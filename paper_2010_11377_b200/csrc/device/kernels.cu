@@ -1009,6 +1009,266 @@ __device__ void record_column(const GmresBufs& g, int col_index) {
     c->final_rel = hv;
 }
 
+// Provisional stop test after the DCGS2 update of iteration j: column j with
+// h_{j+1,j} = ||w'|| (rotations applied to a copy, not stored).
+__device__ void dgs_stop_test(const GmresBufs& g, int j, double wn) {
+    GmresCtl* ctl = g.ctl;
+    const int ld = ctl->restart + 1;
+    const double* hcj = g.H + static_cast<long long>(j) * ld;
+    double* col = ctl->hcol;
+    for (int i = 0; i <= j; ++i) col[i] = hcj[i];
+    col[j + 1] = wn;
+    for (int i = 0; i < j; ++i) {
+        const double t = ctl->cs[i] * col[i] + ctl->sn[i] * col[i + 1];
+        col[i + 1] = -ctl->sn[i] * col[i] + ctl->cs[i] * col[i + 1];
+        col[i] = t;
+    }
+    const double denom = hyp(col[j], col[j + 1]);
+    const double sv = denom > 0.0 ? col[j + 1] / denom : 0.0;
+    const double gn = -sv * ctl->g[j];
+    const double res_prov = fabs(gn) / ctl->beta;
+    const double alpha = ctl->hnext;
+    const int bad = !(res_prov == res_prov) || !(wn == wn) || !(alpha == alpha) || ctl->bad;
+    int stop;
+    if (res_prov <= ctl->tol_c)
+        stop = 1;
+    else if (wn <= 1e-14 * ctl->beta || bad || alpha == 0.0)
+        stop = 2;
+    else if (j + 1 >= ctl->budget)
+        stop = 3;
+    else
+        stop = 0;
+    ctl->stop = stop;
+    ctl->n_reorth += 1;
+    if (stop == 0) ctl->j = j + 1;
+    set_cond(g.h_inner, g.use_cond, stop == 0 ? 1u : 0u);
+}
+
+// Scalar tail of the DCGS2 block-dot (last CTA, one thread): finalises column
+// j-1 (or, at cycle end, column j), stores s, p, h_jj and 1/alpha.
+__device__ void dgs_dot_scalars(const GmresBufs& g, int j, int finalize, int nvv, const double* res) {
+    GmresCtl* ctl = g.ctl;
+    const int ld = ctl->restart + 1;
+    double ss = 0.0, sp = 0.0;
+    for (int i = 0; i < nvv; ++i) ss += res[i] * res[i];
+    const double sig = res[finalize ? nvv : 2 * nvv];
+    const double a2 = sig - ss;
+    const double alpha = a2 > 0.0 ? sqrt(a2) : 0.0;
+    if (finalize) {
+        // complete column j against the orthonormal v_0..v_j
+        double* hc = g.H + static_cast<long long>(j) * ld;
+        for (int i = 0; i <= j; ++i) hc[i] = hc[i] + res[i];
+        hc[j + 1] = alpha;
+        givens_column(ctl, hc, j);
+        record_column(g, j);
+        const double res_rel = fabs(ctl->g[j + 1]) / ctl->beta;
+        if (ctl->stop == 1 && !(res_rel <= ctl->tol_c)) ctl->stop = 3;
+        if (ctl->stop == 3 && res_rel <= ctl->tol_c) ctl->stop = 1;
+        ctl->m = j + 1;
+        return;
+    }
+    for (int i = 0; i < nvv; ++i) {
+        ctl->sv[i] = res[i];
+        ctl->pv[i] = res[nvv + i];
+        sp += res[i] * res[nvv + i];
+    }
+    if (j == 0) {
+        ctl->beta = alpha;
+        ctl->g[0] = alpha;
+    } else {
+        double* hc = g.H + static_cast<long long>(j - 1) * ld;
+        for (int i = 0; i < j; ++i) hc[i] = hc[i] + res[i];
+        hc[j] = alpha;
+        givens_column(ctl, hc, j - 1);
+        record_column(g, j - 1);
+    }
+    const double pi = res[2 * nvv + 1];
+    const double hjj = alpha > 0.0 ? (pi - sp) / alpha : 0.0;
+    double* hcj = g.H + static_cast<long long>(j) * ld;
+    for (int i = 0; i < j; ++i) hcj[i] = res[nvv + i];
+    hcj[j] = hjj;
+    ctl->hjj = hjj;
+    ctl->inv_alpha = alpha > 0.0 ? 1.0 / alpha : 0.0;
+    ctl->hnext = alpha;
+    if (!(alpha == alpha)) ctl->bad = 1;
+}
+
+// Half-chunk load: elements u = 4h..4h+3 of the thread's (u, e) sequence, so
+// processing half 0 then half 1 keeps the contract's per-thread order.
+template <bool kKeepL1 = false>
+__device__ __forceinline__ void load_half(const double* __restrict__ v, long long n, int c, int h,
+                                          double (&o)[kRedPerThread / 2]) {
+    const long long base = static_cast<long long>(c) * kChunk + 2 * threadIdx.x;
+    if (static_cast<long long>(c + 1) * kChunk <= n) {
+#pragma unroll
+        for (int u = 0; u < kRedPerThread / 4; ++u) {
+            const double2* src = reinterpret_cast<const double2*>(v + base + (4 * h + u) * 2 * kRedThreads);
+            const double2 p = kKeepL1 ? __ldca(src) : __ldcs(src);
+            o[2 * u] = p.x;
+            o[2 * u + 1] = p.y;
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < kRedPerThread / 4; ++u)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const long long k = base + (4 * h + u) * 2 * kRedThreads + e;
+                o[2 * u + e] = k < n ? v[k] : 0.0;
+            }
+    }
+}
+
+__device__ __forceinline__ void store_half(double* v, long long n, int c, int h,
+                                           const double (&o)[kRedPerThread / 2]) {
+    const long long base = static_cast<long long>(c) * kChunk + 2 * threadIdx.x;
+    if (static_cast<long long>(c + 1) * kChunk <= n) {
+#pragma unroll
+        for (int u = 0; u < kRedPerThread / 4; ++u)
+            *reinterpret_cast<double2*>(v + base + (4 * h + u) * 2 * kRedThreads) =
+                make_double2(o[2 * u], o[2 * u + 1]);
+    } else {
+#pragma unroll
+        for (int u = 0; u < kRedPerThread / 4; ++u)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const long long k = base + (4 * h + u) * 2 * kRedThreads + e;
+                if (k < n) v[k] = o[2 * u + e];
+            }
+    }
+}
+
+// Low-register DCGS2 update: the chunk in two halves (order-preserving).
+__global__ void __launch_bounds__(kRedThreads, 3) k_dgs_update_h(GmresBufs g) {
+    extern __shared__ double red[];
+    pdl_trigger();
+    pdl_wait();
+    GmresCtl* ctl = g.ctl;
+    const int j = ctl->j;
+    double* sc = red + kRedThreads / 32 + 1;
+    double* pc = sc + j + 1;
+    for (int i = threadIdx.x; i < j; i += kRedThreads) {
+        sc[i] = ctl->sv[i];
+        pc[i] = ctl->pv[i];
+    }
+    __syncthreads();
+    const double inv = ctl->inv_alpha, hjj = ctl->hjj;
+    const int c = blockIdx.x;
+    const long long n = g.sN;
+    const long long stride = (g.sN + 63) / 64 * 64;
+    double* ap = g.V + static_cast<long long>(j) * stride;
+    double* bp = g.V + static_cast<long long>(j + 1) * stride;
+    double acc = 0.0;
+    for (int h = 0; h < 2; ++h) {
+        double a[kRedPerThread / 2], b[kRedPerThread / 2];
+        load_half(ap, n, c, h, a);
+        load_half(bp, n, c, h, b);
+        for (int i = 0; i < j; ++i) {
+            double v[kRedPerThread / 2];
+            load_half(g.V + static_cast<long long>(i) * stride, n, c, h, v);
+            const double si = sc[i], pi = pc[i];
+#pragma unroll
+            for (int q = 0; q < kRedPerThread / 2; ++q) {
+                a[q] = a[q] - si * v[q];
+                b[q] = b[q] - pi * v[q];
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kRedPerThread / 2; ++q) {
+            a[q] = a[q] * inv;
+            b[q] = b[q] - hjj * a[q];
+            acc += b[q] * b[q];
+        }
+        store_half(ap, n, c, h, a);
+        store_half(bp, n, c, h, b);
+    }
+    warp_tree_store(acc, red, 1, 0);
+    __syncthreads();
+    if (threadIdx.x == 0) g.partials[c] = warp_sum8(red, 1, 0);
+    if (!elect_last(g.counters + 10)) return;
+    double* res = red + kRedThreads / 32;
+    final_reduce(g.partials, g.nchunks, 1, red, res);
+    if (threadIdx.x != 0) return;
+    g.counters[10] = 0u;
+    dgs_stop_test(g, j, sqrt(res[0]));
+}
+
+// Low-register DCGS2 block-dot: per basis vector, the two target chunks are
+// re-read (L1-resident) half by half; per-thread order as k_dgs_dot.
+__global__ void __launch_bounds__(kRedThreads, 3) k_dgs_dot_h(GmresBufs g, int finalize) {
+    extern __shared__ double red[];
+    pdl_trigger();
+    pdl_wait();
+    GmresCtl* ctl = g.ctl;
+    const int j = ctl->j;
+    const int nvv = finalize ? j + 1 : j;
+    const int nv = finalize ? nvv + 1 : 2 * nvv + 2;
+    const int c = blockIdx.x;
+    const long long n = g.sN;
+    const long long stride = (g.sN + 63) / 64 * 64;
+    const double* ap = g.V + static_cast<long long>(j) * stride;
+    const double* bp = g.V + static_cast<long long>(j + 1) * stride;
+    if (finalize) {
+        double acc = 0.0;
+        for (int h = 0; h < 2; ++h) {
+            double b[kRedPerThread / 2];
+            load_half<true>(bp, n, c, h, b);
+#pragma unroll
+            for (int q = 0; q < kRedPerThread / 2; ++q) acc += b[q] * b[q];
+        }
+        warp_tree_store(acc, red, nv, nvv);
+        for (int i = 0; i < nvv; ++i) {
+            double ab = 0.0;
+            for (int h = 0; h < 2; ++h) {
+                double b[kRedPerThread / 2], v[kRedPerThread / 2];
+                load_half<true>(bp, n, c, h, b);
+                load_half(g.V + static_cast<long long>(i) * stride, n, c, h, v);
+#pragma unroll
+                for (int q = 0; q < kRedPerThread / 2; ++q) ab += v[q] * b[q];
+            }
+            warp_tree_store(ab, red, nv, i);
+        }
+    } else {
+        double aa = 0.0, ab = 0.0;
+        for (int h = 0; h < 2; ++h) {
+            double a[kRedPerThread / 2], b[kRedPerThread / 2];
+            load_half<true>(ap, n, c, h, a);
+            load_half<true>(bp, n, c, h, b);
+#pragma unroll
+            for (int q = 0; q < kRedPerThread / 2; ++q) {
+                aa += a[q] * a[q];
+                ab += a[q] * b[q];
+            }
+        }
+        warp_tree_store(aa, red, nv, 2 * nvv);
+        warp_tree_store(ab, red, nv, 2 * nvv + 1);
+        for (int i = 0; i < nvv; ++i) {
+            double sa = 0.0, sb = 0.0;
+            for (int h = 0; h < 2; ++h) {
+                double a[kRedPerThread / 2], b[kRedPerThread / 2], v[kRedPerThread / 2];
+                load_half(g.V + static_cast<long long>(i) * stride, n, c, h, v);
+                load_half<true>(ap, n, c, h, a);
+                load_half<true>(bp, n, c, h, b);
+#pragma unroll
+                for (int q = 0; q < kRedPerThread / 2; ++q) {
+                    sa += v[q] * a[q];
+                    sb += v[q] * b[q];
+                }
+            }
+            warp_tree_store(sa, red, nv, i);
+            warp_tree_store(sb, red, nv, nvv + i);
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nv; q += kRedThreads)
+        g.partials[static_cast<long long>(q) * g.nchunks + c] = warp_sum8(red, nv, q);
+    if (!elect_last(g.counters + 9)) return;
+    double* res = red + (kRedThreads / 32) * nv;
+    final_reduce(g.partials, g.nchunks, nv, red, res);
+    if (threadIdx.x != 0) return;
+    g.counters[9] = 0u;
+    dgs_dot_scalars(g, j, finalize, nvv, res);
+}
+
 // DCGS2 block-dot.  Iteration j (finalize = 0): targets A = slot j (vt_j) and
 // B = slot j+1 (w); values [s_0..s_{j-1}, p_0..p_{j-1}, A.A, A.B].
 // Cycle end (finalize = 1, j = last iteration): target B = slot j+1 (w');
@@ -1054,49 +1314,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot(GmresBufs g, int fin
     final_reduce(g.partials, g.nchunks, nv, red, res);
     if (threadIdx.x != 0) return;
     g.counters[9] = 0u;
-    const int ld = ctl->restart + 1;
-    double ss = 0.0, sp = 0.0;
-    for (int i = 0; i < nvv; ++i) ss += res[i] * res[i];
-    const double sig = res[finalize ? nvv : 2 * nvv];
-    const double a2 = sig - ss;
-    const double alpha = a2 > 0.0 ? sqrt(a2) : 0.0;
-    if (finalize) {
-        // complete column j against the orthonormal v_0..v_j
-        double* hc = g.H + static_cast<long long>(j) * ld;
-        for (int i = 0; i <= j; ++i) hc[i] = hc[i] + res[i];
-        hc[j + 1] = alpha;
-        givens_column(ctl, hc, j);
-        record_column(g, j);
-        const double res_rel = fabs(ctl->g[j + 1]) / ctl->beta;
-        if (ctl->stop == 1 && !(res_rel <= ctl->tol_c)) ctl->stop = 3;
-        if (ctl->stop == 3 && res_rel <= ctl->tol_c) ctl->stop = 1;
-        ctl->m = j + 1;
-        return;
-    }
-    for (int i = 0; i < nvv; ++i) {
-        ctl->sv[i] = res[i];
-        ctl->pv[i] = res[nvv + i];
-        sp += res[i] * res[nvv + i];
-    }
-    if (j == 0) {
-        ctl->beta = alpha;
-        ctl->g[0] = alpha;
-    } else {
-        double* hc = g.H + static_cast<long long>(j - 1) * ld;
-        for (int i = 0; i < j; ++i) hc[i] = hc[i] + res[i];
-        hc[j] = alpha;
-        givens_column(ctl, hc, j - 1);
-        record_column(g, j - 1);
-    }
-    const double pi = res[2 * nvv + 1];
-    const double hjj = alpha > 0.0 ? (pi - sp) / alpha : 0.0;
-    double* hcj = g.H + static_cast<long long>(j) * ld;
-    for (int i = 0; i < j; ++i) hcj[i] = res[nvv + i];
-    hcj[j] = hjj;
-    ctl->hjj = hjj;
-    ctl->inv_alpha = alpha > 0.0 ? 1.0 / alpha : 0.0;
-    ctl->hnext = alpha;
-    if (!(alpha == alpha)) ctl->bad = 1;
+    dgs_dot_scalars(g, j, finalize, nvv, res);
 }
 
 // DCGS2 update: v_j = (vt_j - sum_i s_i v_i) / alpha and
@@ -1149,37 +1367,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_update(GmresBufs g) {
     final_reduce(g.partials, g.nchunks, 1, red, res);
     if (threadIdx.x != 0) return;
     g.counters[10] = 0u;
-    const double wn = sqrt(res[0]);
-    // provisional test: column j with h_{j+1,j} = ||w'||, rotations not stored
-    const int ld = ctl->restart + 1;
-    const double* hcj = g.H + static_cast<long long>(j) * ld;
-    double* col = ctl->hcol;
-    for (int i = 0; i <= j; ++i) col[i] = hcj[i];
-    col[j + 1] = wn;
-    for (int i = 0; i < j; ++i) {
-        const double t = ctl->cs[i] * col[i] + ctl->sn[i] * col[i + 1];
-        col[i + 1] = -ctl->sn[i] * col[i] + ctl->cs[i] * col[i + 1];
-        col[i] = t;
-    }
-    const double denom = hyp(col[j], col[j + 1]);
-    const double sv = denom > 0.0 ? col[j + 1] / denom : 0.0;
-    const double gn = -sv * ctl->g[j];
-    const double res_prov = fabs(gn) / ctl->beta;
-    const double alpha = ctl->hnext;
-    const int bad = !(res_prov == res_prov) || !(wn == wn) || !(alpha == alpha) || ctl->bad;
-    int stop;
-    if (res_prov <= ctl->tol_c)
-        stop = 1;
-    else if (wn <= 1e-14 * ctl->beta || bad || alpha == 0.0)
-        stop = 2;
-    else if (j + 1 >= ctl->budget)
-        stop = 3;
-    else
-        stop = 0;
-    ctl->stop = stop;
-    ctl->n_reorth += 1;
-    if (stop == 0) ctl->j = j + 1;
-    set_cond(g.h_inner, g.use_cond, stop == 0 ? 1u : 0u);
+    dgs_stop_test(g, j, sqrt(res[0]));
 }
 
 // V_{j+1} *= 1/h_{j+1,j} when the cycle continues; advance j.
@@ -1502,11 +1690,19 @@ static size_t dgs_smem(const GmresBufs& g) {
 }
 
 void gm_dgs_dot(const GmresBufs& g, int finalize, cudaStream_t st) {
-    launch(k_dgs_dot, g.nchunks, kRedThreads, dgs_smem(g), st, g, finalize);
+    static const bool half = std::getenv("IRK_DGS_FULL") == nullptr;
+    if (half)
+        launch(k_dgs_dot_h, g.nchunks, kRedThreads, dgs_smem(g), st, g, finalize);
+    else
+        launch(k_dgs_dot, g.nchunks, kRedThreads, dgs_smem(g), st, g, finalize);
 }
 
 void gm_dgs_update(const GmresBufs& g, cudaStream_t st) {
-    launch(k_dgs_update, g.nchunks, kRedThreads, dgs_smem(g), st, g);
+    static const bool half = std::getenv("IRK_DGS_FULL") == nullptr;
+    if (half)
+        launch(k_dgs_update_h, g.nchunks, kRedThreads, dgs_smem(g), st, g);
+    else
+        launch(k_dgs_update, g.nchunks, kRedThreads, dgs_smem(g), st, g);
 }
 
 void gm_normalize(const GmresBufs& g, cudaStream_t st) {
@@ -1533,6 +1729,8 @@ void set_smem_limits() {
     const int big = static_cast<int>(sizeof(double) * ((kRedThreads / 32 + 1) * (2 * kMaxRestart + 4) + 16));
     cudaFuncSetAttribute(k_dgs_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_dgs_update, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_dgs_update_h, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_dgs_dot_h, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_gm_update_cgs2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(double) * ((kRedThreads / 32 + 1) * (kMaxRestart + 2) +
                                                             kMaxRestart + 16)));
