@@ -1690,7 +1690,7 @@ static size_t dgs_smem(const GmresBufs& g) {
 }
 
 void gm_dgs_dot(const GmresBufs& g, int finalize, cudaStream_t st) {
-    static const bool half = std::getenv("IRK_DGS_FULL") == nullptr;
+    static const bool half = std::getenv("IRK_DGS_HALF") != nullptr;  // A/B neutral
     if (half)
         launch(k_dgs_dot_h, g.nchunks, kRedThreads, dgs_smem(g), st, g, finalize);
     else
@@ -1698,7 +1698,7 @@ void gm_dgs_dot(const GmresBufs& g, int finalize, cudaStream_t st) {
 }
 
 void gm_dgs_update(const GmresBufs& g, cudaStream_t st) {
-    static const bool half = std::getenv("IRK_DGS_FULL") == nullptr;
+    static const bool half = std::getenv("IRK_DGS_HALF") != nullptr;  // A/B neutral
     if (half)
         launch(k_dgs_update_h, g.nchunks, kRedThreads, dgs_smem(g), st, g);
     else
