@@ -11,6 +11,8 @@
 #include "../host/sparse.hpp"
 #include "kernels.cuh"
 
+#include <cuda_pipeline.h>
+
 namespace irkb {
 namespace dev {
 
@@ -775,8 +777,14 @@ __device__ __forceinline__ double chunk_dot_local(const double (&a)[kRedPerThrea
     return acc;
 }
 
-__device__ void set_cond(cudaGraphConditionalHandle h, int use, unsigned v) {
-    if (use) cudaGraphSetConditional(h, v);
+// COND = false instantiations contain no device-graph API call, so the
+// host-driven profiling mode launches kernels ncu can profile (ncu skips
+// kernels that reference cudaGraphSetConditional).
+template <bool COND>
+__device__ __forceinline__ void set_cond(cudaGraphConditionalHandle h, int use, unsigned v) {
+    if constexpr (COND) {
+        if (use) cudaGraphSetConditional(h, v);
+    }
 }
 
 // Scalar tail of one Arnoldi step (gmres.cpp:93-118), single thread.
@@ -1011,6 +1019,7 @@ __device__ void record_column(const GmresBufs& g, int col_index) {
 
 // Provisional stop test after the DCGS2 update of iteration j: column j with
 // h_{j+1,j} = ||w'|| (rotations applied to a copy, not stored).
+template <bool COND>
 __device__ void dgs_stop_test(const GmresBufs& g, int j, double wn) {
     GmresCtl* ctl = g.ctl;
     const int ld = ctl->restart + 1;
@@ -1041,7 +1050,7 @@ __device__ void dgs_stop_test(const GmresBufs& g, int j, double wn) {
     ctl->stop = stop;
     ctl->n_reorth += 1;
     if (stop == 0) ctl->j = j + 1;
-    set_cond(g.h_inner, g.use_cond, stop == 0 ? 1u : 0u);
+    set_cond<COND>(g.h_inner, g.use_cond, stop == 0 ? 1u : 0u);
 }
 
 // Scalar tail of the DCGS2 block-dot (last CTA, one thread): finalises column
@@ -1138,6 +1147,7 @@ __device__ __forceinline__ void store_half(double* v, long long n, int c, int h,
 }
 
 // Low-register DCGS2 update: the chunk in two halves (order-preserving).
+template <bool COND>
 __global__ void __launch_bounds__(kRedThreads, 3) k_dgs_update_h(GmresBufs g) {
     extern __shared__ double red[];
     pdl_trigger();
@@ -1189,7 +1199,7 @@ __global__ void __launch_bounds__(kRedThreads, 3) k_dgs_update_h(GmresBufs g) {
     final_reduce(g.partials, g.nchunks, 1, red, res);
     if (threadIdx.x != 0) return;
     g.counters[10] = 0u;
-    dgs_stop_test(g, j, sqrt(res[0]));
+    dgs_stop_test<COND>(g, j, sqrt(res[0]));
 }
 
 // Low-register DCGS2 block-dot: per basis vector, the two target chunks are
@@ -1269,6 +1279,166 @@ __global__ void __launch_bounds__(kRedThreads, 3) k_dgs_dot_h(GmresBufs g, int f
     dgs_dot_scalars(g, j, finalize, nvv, res);
 }
 
+// cp.async ring for streaming basis vectors: each thread copies exactly the
+// 16-byte pieces it later consumes (its 16 contract elements of the chunk),
+// so producer and consumer are the same thread and only cp.async
+// wait_group is needed -- no block barriers.  Layout [stage][u][thread]
+// (16 B per (u, thread)) keeps the shared-memory reads conflict-free.
+constexpr int kPipeStages = 3;
+constexpr int kPipeStageBytes = kChunk * 8;  // 32 KB per stage
+
+__device__ __forceinline__ void pipe_issue(double2* ring, int stage, const double* v, int c) {
+    const double* base = v + static_cast<long long>(c) * kChunk + 2 * threadIdx.x;
+    double2* dst = ring + stage * (kChunk / 2) + threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < kRedPerThread / 2; ++u)
+        __pipeline_memcpy_async(dst + u * kRedThreads, base + u * 2 * kRedThreads, 16);
+}
+
+__device__ __forceinline__ void pipe_read(const double2* ring, int stage, double (&o)[kRedPerThread]) {
+    const double2* src = ring + stage * (kChunk / 2) + threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < kRedPerThread / 2; ++u) {
+        const double2 p = src[u * kRedThreads];
+        o[2 * u] = p.x;
+        o[2 * u + 1] = p.y;
+    }
+}
+
+// DCGS2 block-dot with the cp.async ring (full chunks; the partial last
+// chunk takes the direct-load path).  Same values and order as k_dgs_dot.
+__global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot_pipe(GmresBufs g, int finalize) {
+    extern __shared__ double red[];
+    pdl_trigger();
+    pdl_wait();
+    GmresCtl* ctl = g.ctl;
+    const int j = ctl->j;
+    const int nvv = finalize ? j + 1 : j;
+    const int nv = finalize ? nvv + 1 : 2 * nvv + 2;
+    const int c = blockIdx.x;
+    const long long n = g.sN;
+    const long long stride = (g.sN + 63) / 64 * 64;
+    double2* ring = reinterpret_cast<double2*>(red);
+    double* tree = red + kPipeStages * kChunk;  // (8 x nv) warp values, then results
+    const bool full = static_cast<long long>(c + 1) * kChunk <= n;
+    double b[kRedPerThread];
+    load_chunk(g.V + static_cast<long long>(j + 1) * stride, n, c, b);
+    double a[kRedPerThread];
+    if (!finalize) load_chunk(g.V + static_cast<long long>(j) * stride, n, c, a);
+    if (full) {
+#pragma unroll
+        for (int st = 0; st < kPipeStages - 1; ++st) {
+            if (st < nvv) pipe_issue(ring, st, g.V + static_cast<long long>(st) * stride, c);
+            __pipeline_commit();
+        }
+    }
+    if (finalize) {
+        warp_tree_store(chunk_dot_local(b, b), tree, nv, nvv);
+    } else {
+        warp_tree_store(chunk_dot_local(a, a), tree, nv, 2 * nvv);
+        warp_tree_store(chunk_dot_local(a, b), tree, nv, 2 * nvv + 1);
+    }
+    for (int i = 0; i < nvv; ++i) {
+        double v[kRedPerThread];
+        if (full) {
+            const int ahead = i + kPipeStages - 1;
+            if (ahead < nvv)
+                pipe_issue(ring, ahead % kPipeStages, g.V + static_cast<long long>(ahead) * stride, c);
+            __pipeline_commit();
+            __pipeline_wait_prior(kPipeStages - 1);
+            pipe_read(ring, i % kPipeStages, v);
+        } else {
+            load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v);
+        }
+        if (finalize) {
+            warp_tree_store(chunk_dot_local(v, b), tree, nv, i);
+        } else {
+            warp_tree_store(chunk_dot_local(v, a), tree, nv, i);
+            warp_tree_store(chunk_dot_local(v, b), tree, nv, nvv + i);
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nv; q += kRedThreads)
+        g.partials[static_cast<long long>(q) * g.nchunks + c] = warp_sum8(tree, nv, q);
+    if (!elect_last(g.counters + 9)) return;
+    double* res = tree + (kRedThreads / 32) * nv;
+    final_reduce(g.partials, g.nchunks, nv, tree, res);
+    if (threadIdx.x != 0) return;
+    g.counters[9] = 0u;
+    dgs_dot_scalars(g, j, finalize, nvv, res);
+}
+
+// DCGS2 update with the cp.async ring.  Same per-element order as k_dgs_update.
+template <bool COND>
+__global__ void __launch_bounds__(kRedThreads, 2) k_dgs_update_pipe(GmresBufs g) {
+    extern __shared__ double red[];
+    pdl_trigger();
+    pdl_wait();
+    GmresCtl* ctl = g.ctl;
+    const int j = ctl->j;
+    double2* ring = reinterpret_cast<double2*>(red);
+    double* tree = red + kPipeStages * kChunk;
+    double* sc = tree + kRedThreads / 32 + 1;
+    double* pc = sc + j + 1;
+    for (int i = threadIdx.x; i < j; i += kRedThreads) {
+        sc[i] = ctl->sv[i];
+        pc[i] = ctl->pv[i];
+    }
+    __syncthreads();
+    const double inv = ctl->inv_alpha, hjj = ctl->hjj;
+    const int c = blockIdx.x;
+    const long long n = g.sN;
+    const long long stride = (g.sN + 63) / 64 * 64;
+    const bool full = static_cast<long long>(c + 1) * kChunk <= n;
+    double* ap = g.V + static_cast<long long>(j) * stride;
+    double* bp = g.V + static_cast<long long>(j + 1) * stride;
+    if (full) {
+#pragma unroll
+        for (int st = 0; st < kPipeStages - 1; ++st) {
+            if (st < j) pipe_issue(ring, st, g.V + static_cast<long long>(st) * stride, c);
+            __pipeline_commit();
+        }
+    }
+    double a[kRedPerThread], b[kRedPerThread];
+    load_chunk(ap, n, c, a);
+    load_chunk(bp, n, c, b);
+    for (int i = 0; i < j; ++i) {
+        double v[kRedPerThread];
+        if (full) {
+            const int ahead = i + kPipeStages - 1;
+            if (ahead < j)
+                pipe_issue(ring, ahead % kPipeStages, g.V + static_cast<long long>(ahead) * stride, c);
+            __pipeline_commit();
+            __pipeline_wait_prior(kPipeStages - 1);
+            pipe_read(ring, i % kPipeStages, v);
+        } else {
+            load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v);
+        }
+        const double si = sc[i], pi = pc[i];
+#pragma unroll
+        for (int q = 0; q < kRedPerThread; ++q) {
+            a[q] = a[q] - si * v[q];
+            b[q] = b[q] - pi * v[q];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kRedPerThread; ++q) {
+        a[q] = a[q] * inv;
+        b[q] = b[q] - hjj * a[q];
+    }
+    store_chunk(ap, n, c, a);
+    store_chunk(bp, n, c, b);
+    warp_tree_store(chunk_dot_local(b, b), tree, 1, 0);
+    __syncthreads();
+    if (threadIdx.x == 0) g.partials[c] = warp_sum8(tree, 1, 0);
+    if (!elect_last(g.counters + 10)) return;
+    double* res = tree + kRedThreads / 32;
+    final_reduce(g.partials, g.nchunks, 1, tree, res);
+    if (threadIdx.x != 0) return;
+    g.counters[10] = 0u;
+    dgs_stop_test<COND>(g, j, sqrt(res[0]));
+}
+
 // DCGS2 block-dot.  Iteration j (finalize = 0): targets A = slot j (vt_j) and
 // B = slot j+1 (w); values [s_0..s_{j-1}, p_0..p_{j-1}, A.A, A.B].
 // Cycle end (finalize = 1, j = last iteration): target B = slot j+1 (w');
@@ -1320,6 +1490,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot(GmresBufs g, int fin
 // DCGS2 update: v_j = (vt_j - sum_i s_i v_i) / alpha and
 // w' = w - sum_i p_i v_i - h_jj v_j in one pass (element-wise order as the
 // oracle), ||w'||^2, then the provisional stop test on the first-pass column.
+template <bool COND>
 __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_update(GmresBufs g) {
     extern __shared__ double red[];
     pdl_trigger();
@@ -1367,10 +1538,11 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_update(GmresBufs g) {
     final_reduce(g.partials, g.nchunks, 1, red, res);
     if (threadIdx.x != 0) return;
     g.counters[10] = 0u;
-    dgs_stop_test(g, j, sqrt(res[0]));
+    dgs_stop_test<COND>(g, j, sqrt(res[0]));
 }
 
 // V_{j+1} *= 1/h_{j+1,j} when the cycle continues; advance j.
+template <bool COND>
 __global__ void __launch_bounds__(kRedThreads) k_gm_normalize(GmresBufs g) {
     pdl_trigger();
     pdl_wait();
@@ -1390,11 +1562,12 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_normalize(GmresBufs g) {
     if (!elect_last(g.counters + 4)) return;
     if (threadIdx.x == 0) {
         if (stop == 0) ctl->j = j + 1;
-        set_cond(g.h_inner, g.use_cond, stop == 0 ? 1u : 0u);
+        set_cond<COND>(g.h_inner, g.use_cond, stop == 0 ? 1u : 0u);
         g.counters[4] = 0u;
     }
 }
 
+template <bool COND>
 __global__ void __launch_bounds__(kRedThreads) k_gm_init(GmresBufs g, const double* __restrict__ b,
                                                          double* __restrict__ r, double rel_tol,
                                                          int restart, int max_iter, int ortho) {
@@ -1442,11 +1615,12 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_init(GmresBufs g, const doub
             c->inv = 1.0 / bn;
             if (c->budget <= 0) c->done = 1;
         }
-        set_cond(g.h_outer, g.use_cond, c->done ? 0u : 1u);
+        set_cond<COND>(g.h_outer, g.use_cond, c->done ? 0u : 1u);
         g.counters[5] = 0u;
     }
 }
 
+template <bool COND>
 __global__ void __launch_bounds__(kRedThreads) k_gm_cycle_begin(GmresBufs g,
                                                                 const double* __restrict__ r) {
     pdl_trigger();
@@ -1466,7 +1640,7 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_cycle_begin(GmresBufs g,
         ctl->g[0] = ctl->beta;
         ctl->j = 0;
         ctl->stop = 0;
-        set_cond(g.h_inner, g.use_cond, 1u);
+        set_cond<COND>(g.h_inner, g.use_cond, 1u);
         g.counters[6] = 0u;
     }
 }
@@ -1507,6 +1681,7 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_xupdate(GmresBufs g, double*
 }
 
 // r = b - Ax, beta = ||r||, restart decision.
+template <bool COND>
 __global__ void __launch_bounds__(kRedThreads) k_gm_residual(GmresBufs g, const double* __restrict__ b,
                                                              const double* __restrict__ ax,
                                                              double* __restrict__ r) {
@@ -1540,7 +1715,7 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_residual(GmresBufs g, const 
             c->budget = c->restart < left ? c->restart : left;
             c->inv = 1.0 / rn;
         }
-        set_cond(g.h_outer, g.use_cond, finished ? 0u : 1u);
+        set_cond<COND>(g.h_outer, g.use_cond, finished ? 0u : 1u);
         g.counters[7] = 0u;
     }
 }
@@ -1654,11 +1829,11 @@ static size_t red_smem(int nv) { return sizeof(double) * (kRedThreads / 32 * nv 
 
 void gm_init(const GmresBufs& g, const double* b, double* r, double rel_tol, int restart,
              int max_iter, int ortho, cudaStream_t st) {
-    launch(k_gm_init, g.nchunks, kRedThreads, 0, st, g, b, r, rel_tol, restart, max_iter, ortho);
+    launch(g.use_cond ? k_gm_init<true> : k_gm_init<false>, g.nchunks, kRedThreads, 0, st, g, b, r, rel_tol, restart, max_iter, ortho);
 }
 
 void gm_cycle_begin(const GmresBufs& g, const double* r, cudaStream_t st) {
-    launch(k_gm_cycle_begin, g.nchunks, kRedThreads, 0, st, g, r);
+    launch(g.use_cond ? k_gm_cycle_begin<true> : k_gm_cycle_begin<false>, g.nchunks, kRedThreads, 0, st, g, r);
 }
 
 void gm_blockdot(const GmresBufs& g, int pass, cudaStream_t st) {
@@ -1689,8 +1864,22 @@ static size_t dgs_smem(const GmresBufs& g) {
     return sizeof(double) * ((kRedThreads / 32 + 1) * nv + 16);
 }
 
+static size_t dgs_pipe_smem(const GmresBufs& g) {
+    return sizeof(double) * kPipeStages * kChunk + dgs_smem(g);
+}
+
+static int dgs_variant() {
+    // 2 = cp.async ring (default), 1 = half-chunk, 0 = direct loads
+    static const int v = std::getenv("IRK_DGS") ? std::atoi(std::getenv("IRK_DGS")) : 2;
+    return v;
+}
+
 void gm_dgs_dot(const GmresBufs& g, int finalize, cudaStream_t st) {
-    static const bool half = std::getenv("IRK_DGS_HALF") != nullptr;  // A/B neutral
+    if (dgs_variant() == 2) {
+        launch(k_dgs_dot_pipe, g.nchunks, kRedThreads, dgs_pipe_smem(g), st, g, finalize);
+        return;
+    }
+    const bool half = dgs_variant() == 1;
     if (half)
         launch(k_dgs_dot_h, g.nchunks, kRedThreads, dgs_smem(g), st, g, finalize);
     else
@@ -1698,15 +1887,20 @@ void gm_dgs_dot(const GmresBufs& g, int finalize, cudaStream_t st) {
 }
 
 void gm_dgs_update(const GmresBufs& g, cudaStream_t st) {
-    static const bool half = std::getenv("IRK_DGS_HALF") != nullptr;  // A/B neutral
+    if (dgs_variant() == 2) {
+        launch(g.use_cond ? k_dgs_update_pipe<true> : k_dgs_update_pipe<false>, g.nchunks, kRedThreads,
+               dgs_pipe_smem(g), st, g);
+        return;
+    }
+    const bool half = dgs_variant() == 1;
     if (half)
-        launch(k_dgs_update_h, g.nchunks, kRedThreads, dgs_smem(g), st, g);
+        launch(g.use_cond ? k_dgs_update_h<true> : k_dgs_update_h<false>, g.nchunks, kRedThreads, dgs_smem(g), st, g);
     else
-        launch(k_dgs_update, g.nchunks, kRedThreads, dgs_smem(g), st, g);
+        launch(g.use_cond ? k_dgs_update<true> : k_dgs_update<false>, g.nchunks, kRedThreads, dgs_smem(g), st, g);
 }
 
 void gm_normalize(const GmresBufs& g, cudaStream_t st) {
-    launch(k_gm_normalize, g.nchunks, kRedThreads, 0, st, g);
+    launch(g.use_cond ? k_gm_normalize<true> : k_gm_normalize<false>, g.nchunks, kRedThreads, 0, st, g);
 }
 
 void gm_solution(const GmresBufs& g, double* x, cudaStream_t st) {
@@ -1716,7 +1910,7 @@ void gm_solution(const GmresBufs& g, double* x, cudaStream_t st) {
 
 void gm_residual(const GmresBufs& g, const double* b, const double* ax, double* r,
                  cudaStream_t st) {
-    launch(k_gm_residual, g.nchunks, kRedThreads, 0, st, g, b, ax, r);
+    launch(g.use_cond ? k_gm_residual<true> : k_gm_residual<false>, g.nchunks, kRedThreads, 0, st, g, b, ax, r);
 }
 
 void dot(const double* x, const double* y, long long n, double* partials, unsigned* counter,
@@ -1728,9 +1922,15 @@ void dot(const double* x, const double* y, long long n, double* partials, unsign
 void set_smem_limits() {
     const int big = static_cast<int>(sizeof(double) * ((kRedThreads / 32 + 1) * (2 * kMaxRestart + 4) + 16));
     cudaFuncSetAttribute(k_dgs_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_dgs_update, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_dgs_update_h, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_dgs_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_dgs_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_dgs_update_h<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(k_dgs_update_h<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_dgs_dot_h, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    const int pipe = big + static_cast<int>(sizeof(double)) * kPipeStages * kChunk;
+    cudaFuncSetAttribute(k_dgs_dot_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, pipe);
+    cudaFuncSetAttribute(k_dgs_update_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pipe);
+    cudaFuncSetAttribute(k_dgs_update_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pipe);
     cudaFuncSetAttribute(k_gm_update_cgs2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(sizeof(double) * ((kRedThreads / 32 + 1) * (kMaxRestart + 2) +
                                                             kMaxRestart + 16)));
