@@ -1869,8 +1869,8 @@ static size_t dgs_pipe_smem(const GmresBufs& g) {
 }
 
 static int dgs_variant() {
-    // 2 = cp.async ring (default), 1 = half-chunk, 0 = direct loads
-    static const int v = std::getenv("IRK_DGS") ? std::atoi(std::getenv("IRK_DGS")) : 2;
+    // 0 = direct loads (default), 1 = half-chunk, 2 = cp.async ring (A/B: both slower)
+    static const int v = std::getenv("IRK_DGS") ? std::atoi(std::getenv("IRK_DGS")) : 0;
     return v;
 }
 
