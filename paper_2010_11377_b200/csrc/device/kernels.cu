@@ -569,7 +569,21 @@ __global__ void __launch_bounds__(256) k_dense_mv(int n, const double* __restric
     double* sA = sm;
     double* sr = sm + static_cast<long long>(n) * n;
     const double* r = rr.get();
-    for (int q = threadIdx.x; q < n * n; q += blockDim.x) sA[q] = A[q];
+    // batched fill: all of a thread's loads are issued before any store
+    const int nn = n * n;
+    for (int q0 = 0; q0 < nn; q0 += 8 * blockDim.x) {
+        double t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = q0 + u * blockDim.x + threadIdx.x;
+            t[u] = q < nn ? A[q] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = q0 + u * blockDim.x + threadIdx.x;
+            if (q < nn) sA[q] = t[u];
+        }
+    }
     for (int q = threadIdx.x; q < n; q += blockDim.x) sr[q] = r[q];
     __syncthreads();
     double* z = zr.get();

@@ -1049,6 +1049,34 @@ double DeviceSolver::time_kernel(int which, int reps) {
         g_restart_ = -1;  // graphs captured the old use_cond; rebuild on the next step
         return static_cast<double>(ms) / reps;
     }
+    if (which >= 30 && which < 40) {
+        // graph-captured repetitions of the V-cycle below level which-30
+        DevBuf a(sizeof(double) * stride_), b(sizeof(double) * stride_);
+        IRK_CUDA_CHECK(cudaMemsetAsync(a.as<void>(), 0, sizeof(double) * stride_, st_));
+        const int first = std::min<int>(which - 30, static_cast<int>(hier_[0].lv.size()) - 1);
+        cudaGraph_t gr;
+        IRK_CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+        for (int r = 0; r < reps; ++r)
+            record_vcycle(0, dev::plain(a.as<double>()), dev::plain(b.as<double>()), first);
+        IRK_CUDA_CHECK(cudaStreamEndCapture(st_, &gr));
+        cudaGraphExec_t ge;
+        IRK_CUDA_CHECK(cudaGraphInstantiate(&ge, gr, 0));
+        cudaGraphDestroy(gr);
+        IRK_CUDA_CHECK(cudaGraphLaunch(ge, st_));
+        cudaEvent_t e0, e1;
+        IRK_CUDA_CHECK(cudaEventCreate(&e0));
+        IRK_CUDA_CHECK(cudaEventCreate(&e1));
+        IRK_CUDA_CHECK(cudaEventRecord(e0, st_));
+        IRK_CUDA_CHECK(cudaGraphLaunch(ge, st_));
+        IRK_CUDA_CHECK(cudaEventRecord(e1, st_));
+        IRK_CUDA_CHECK(cudaEventSynchronize(e1));
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaGraphExecDestroy(ge);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return static_cast<double>(ms) / reps;
+    }
     if (which == 20 || which == 21) {
         // launch floor: 100 dependent empty kernels, graph (20) or stream (21)
         cudaEvent_t e0, e1;

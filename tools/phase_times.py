@@ -17,7 +17,10 @@ L = _abi.lib()
 names = {0: "stage operator", 1: "fine smoother SpMV", 2: "precond apply (3 V-cycles + 2 sweeps)",
          3: "V-cycle (hierarchy 0)", 4: "V-cycle below level 1", 5: "V-cycle below level 2",
          6: "V-cycle below level 3", 115: "GMRES block-dot j=15 (17 vectors)",
-         20: "empty kernel, graph launch (per kernel)", 21: "empty kernel, stream launch (per kernel)"}
+         20: "empty kernel, graph launch (per kernel)", 21: "empty kernel, stream launch (per kernel)",
+         30: "graph: V-cycle (hot, repeated)", 31: "graph: V-cycle below level 1",
+         32: "graph: V-cycle below level 2", 33: "graph: V-cycle below level 3",
+         34: "graph: V-cycle below level 4", 35: "graph: coarse solve only"}
 for w, name in names.items():
     ms = C.c_double()
     _abi.check(L.irkdev_time_kernel(Pc._dev._h, w, 50, C.byref(ms)))
