@@ -1453,6 +1453,95 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_update_pipe(GmresBufs g)
     dgs_stop_test<COND>(g, j, sqrt(res[0]));
 }
 
+// DCGS2 block-dot, low-register / deep-prefetch variant: the thread's target
+// elements (vt_j and w) live in shared memory ([q][thread], conflict-free),
+// basis vectors are streamed two at a time (32 loads of 16 B in flight per
+// thread).  Same per-thread order and values as k_dgs_dot.
+__global__ void __launch_bounds__(kRedThreads, 3) k_dgs_dot_s(GmresBufs g, int finalize) {
+    extern __shared__ double red[];
+    pdl_trigger();
+    pdl_wait();
+    GmresCtl* ctl = g.ctl;
+    const int j = ctl->j;
+    const int nvv = finalize ? j + 1 : j;
+    const int nv = finalize ? nvv + 1 : 2 * nvv + 2;
+    const int c = blockIdx.x;
+    const long long n = g.sN;
+    const long long stride = (g.sN + 63) / 64 * 64;
+    double* sa = red;                         // [16][256]
+    double* sb = red + kChunk;                // [16][256]
+    double* tree = red + 2 * kChunk;
+    const int t = threadIdx.x;
+    {
+        double b[kRedPerThread];
+        load_chunk(g.V + static_cast<long long>(j + 1) * stride, n, c, b);
+#pragma unroll
+        for (int q = 0; q < kRedPerThread; ++q) sb[q * kRedThreads + t] = b[q];
+        if (finalize) {
+            warp_tree_store(chunk_dot_local(b, b), tree, nv, nvv);
+        } else {
+            double a[kRedPerThread];
+            load_chunk(g.V + static_cast<long long>(j) * stride, n, c, a);
+#pragma unroll
+            for (int q = 0; q < kRedPerThread; ++q) sa[q * kRedThreads + t] = a[q];
+            warp_tree_store(chunk_dot_local(a, a), tree, nv, 2 * nvv);
+            warp_tree_store(chunk_dot_local(a, b), tree, nv, 2 * nvv + 1);
+        }
+    }
+    int i = 0;
+    for (; i + 1 < nvv; i += 2) {
+        double v0[kRedPerThread], v1[kRedPerThread];
+        load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v0);
+        load_chunk(g.V + static_cast<long long>(i + 1) * stride, n, c, v1);
+        double sa0 = 0.0, sb0 = 0.0, sa1 = 0.0, sb1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < kRedPerThread; ++q) {
+            const double bq = sb[q * kRedThreads + t];
+            sb0 += v0[q] * bq;
+            sb1 += v1[q] * bq;
+            if (!finalize) {
+                const double aq = sa[q * kRedThreads + t];
+                sa0 += v0[q] * aq;
+                sa1 += v1[q] * aq;
+            }
+        }
+        if (finalize) {
+            warp_tree_store(sb0, tree, nv, i);
+            warp_tree_store(sb1, tree, nv, i + 1);
+        } else {
+            warp_tree_store(sa0, tree, nv, i);
+            warp_tree_store(sb0, tree, nv, nvv + i);
+            warp_tree_store(sa1, tree, nv, i + 1);
+            warp_tree_store(sb1, tree, nv, nvv + i + 1);
+        }
+    }
+    for (; i < nvv; ++i) {
+        double v0[kRedPerThread];
+        load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v0);
+        double sa0 = 0.0, sb0 = 0.0;
+#pragma unroll
+        for (int q = 0; q < kRedPerThread; ++q) {
+            sb0 += v0[q] * sb[q * kRedThreads + t];
+            if (!finalize) sa0 += v0[q] * sa[q * kRedThreads + t];
+        }
+        if (finalize) {
+            warp_tree_store(sb0, tree, nv, i);
+        } else {
+            warp_tree_store(sa0, tree, nv, i);
+            warp_tree_store(sb0, tree, nv, nvv + i);
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nv; q += kRedThreads)
+        g.partials[static_cast<long long>(q) * g.nchunks + c] = warp_sum8(tree, nv, q);
+    if (!elect_last(g.counters + 9)) return;
+    double* res = tree + (kRedThreads / 32) * nv;
+    final_reduce(g.partials, g.nchunks, nv, tree, res);
+    if (threadIdx.x != 0) return;
+    g.counters[9] = 0u;
+    dgs_dot_scalars(g, j, finalize, nvv, res);
+}
+
 // DCGS2 block-dot.  Iteration j (finalize = 0): targets A = slot j (vt_j) and
 // B = slot j+1 (w); values [s_0..s_{j-1}, p_0..p_{j-1}, A.A, A.B].
 // Cycle end (finalize = 1, j = last iteration): target B = slot j+1 (w');
@@ -1889,6 +1978,11 @@ static int dgs_variant() {
 }
 
 void gm_dgs_dot(const GmresBufs& g, int finalize, cudaStream_t st) {
+    if (dgs_variant() == 3) {
+        launch(k_dgs_dot_s, g.nchunks, kRedThreads, sizeof(double) * 2 * kChunk + dgs_smem(g), st, g,
+               finalize);
+        return;
+    }
     if (dgs_variant() == 2) {
         launch(k_dgs_dot_pipe, g.nchunks, kRedThreads, dgs_pipe_smem(g), st, g, finalize);
         return;
@@ -1943,6 +2037,8 @@ void set_smem_limits() {
     cudaFuncSetAttribute(k_dgs_dot_h, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     const int pipe = big + static_cast<int>(sizeof(double)) * kPipeStages * kChunk;
     cudaFuncSetAttribute(k_dgs_dot_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, pipe);
+    cudaFuncSetAttribute(k_dgs_dot_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         big + static_cast<int>(sizeof(double)) * 2 * kChunk);
     cudaFuncSetAttribute(k_dgs_update_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pipe);
     cudaFuncSetAttribute(k_dgs_update_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pipe);
     cudaFuncSetAttribute(k_gm_update_cgs2, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1025,21 +1025,29 @@ __global__ void k_empty() {}
 }  // namespace
 
 double DeviceSolver::time_kernel(int which, int reps) {
-    if (which >= 100 && which < 100 + dev::kMaxRestart) {
-        // GMRES block-dot (pass 1) with j = which - 100 (j+2 vectors of sN)
-        const int j = which - 100;
+    if (which >= 100 && which < 100 + 2 * dev::kMaxRestart) {
+        // GMRES block-dot with j = which - 100 (CGS pass 1) or which - 600
+        // (DCGS2 block-dot): j+2 vectors of sN streamed
+        const bool dgs = which >= 600;
+        const int j = dgs ? which - 600 : which - 100;
         ensure_gmres(std::max(50, j + 2), 500);
         IRK_CUDA_CHECK(cudaMemsetAsync(gb_.V, 0, sizeof(double) * stride_ * (j + 2), st_));
         IRK_CUDA_CHECK(cudaMemcpyAsync(&gb_.ctl->j, &j, sizeof(int), cudaMemcpyHostToDevice, st_));
         const int zero = 0;
         IRK_CUDA_CHECK(cudaMemcpyAsync(&gb_.ctl->reorth, &zero, sizeof(int), cudaMemcpyHostToDevice, st_));
         gb_.use_cond = 0;
-        dev::gm_blockdot(gb_, 1, st_);
+        auto launch_once = [&]() {
+            if (dgs)
+                dev::gm_dgs_dot(gb_, 0, st_);
+            else
+                dev::gm_blockdot(gb_, 1, st_);
+        };
+        launch_once();
         cudaEvent_t e0, e1;
         IRK_CUDA_CHECK(cudaEventCreate(&e0));
         IRK_CUDA_CHECK(cudaEventCreate(&e1));
         IRK_CUDA_CHECK(cudaEventRecord(e0, st_));
-        for (int i = 0; i < reps; ++i) dev::gm_blockdot(gb_, 1, st_);
+        for (int i = 0; i < reps; ++i) launch_once();
         IRK_CUDA_CHECK(cudaEventRecord(e1, st_));
         IRK_CUDA_CHECK(cudaEventSynchronize(e1));
         float ms = 0.0f;
