@@ -226,6 +226,50 @@ __global__ void __launch_bounds__(256) k_spmv_p1(Mat A, SpmvArgs a) {
     }
 }
 
+template <int ND, int W, int PVF, int WDT>
+__global__ void __launch_bounds__(256) k_prolong_smooth(Mat A, EllP P, const double* __restrict__ zc,
+                                                        VecRef rr, VecRef zr, const double* __restrict__ wd) {
+    __shared__ double s_tab[256];
+    __shared__ double s_wd[256];
+    __shared__ double s_pt[PVF == kU8 ? 256 : 1];
+    const double* tab = load_tab<kU8>(A, s_tab, s_wd);
+    if constexpr (PVF == kU8) {
+        for (int q = threadIdx.x; q < P.ntab; q += blockDim.x) s_pt[q] = P.tab[q];
+        __syncthreads();
+    }
+    pdl_wait();
+    const int n = A.rows;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double* r = rr.get();
+    const unsigned char* dcode = static_cast<const unsigned char*>(A.val) + static_cast<long long>(A.diag0) * A.dstride;
+    const int* __restrict__ pidx = P.idx;
+    const void* pval = P.val;
+    // plain locals only (no lambda captures of kernel parameters: taking their
+    // address would force a stack copy)
+    auto wdk = [=](int k) { return WDT == 1 ? s_wd[__ldg(dcode + k)] : wd[k]; };
+    auto tval = [=](int k) {
+        double s = 0.0;
+#pragma unroll
+        for (int e = 0; e < W; ++e) {
+            const long long q = static_cast<long long>(e) * n + k;
+            const double pv = PVF == kU8 ? s_pt[__ldg(static_cast<const unsigned char*>(pval) + q)]
+                                         : __ldg(static_cast<const double*>(pval) + q);
+            s += pv * zc[__ldg(pidx + q)];
+        }
+        return wdk(k) * r[k] + s;
+    };
+    const int diag0 = A.diag0;
+    double s = 0.0, ti = 0.0;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+        const double t = tval(min(max(i + A.off[d], 0), n - 1));
+        s += vfetch<kU8>(A.val, static_cast<long long>(d) * A.dstride + i, tab) * t;
+        if (d == diag0) ti = t;
+    }
+    zr.get()[i] = ti + wdk(i) * (r[i] - s);
+}
+
 // SELL-32: one warp per 32-row slice, entries column-major inside the slice,
 // sequential per-row sums (same order as CSR; padding adds exact zeros).
 template <int XM, int EPI, int VF>
@@ -1840,6 +1884,25 @@ void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st) 
     IRK_SPMV_CASE(kXWdR, kEPlain)
 #undef IRK_SPMV_CASE
     throw InvalidArgument("spmv: unsupported mode combination");
+}
+
+void prolong_smooth_fused(const Mat& A, const EllP& P, const double* zc, VecRef r, VecRef z,
+                          const double* wd, cudaStream_t st) {
+    const int nb = blocks_for(A.rows, 256);
+    const bool wdt = A.wdtab && A.diag0 >= 0;
+    if (A.nd != 7 || A.vf != kU8) throw InvalidArgument("prolong_smooth_fused: needs a 7-diagonal u8 DIA A");
+#define IRK_PS(W, PVF)                                                                              \
+    if (P.width == W && P.vf == PVF) {                                                              \
+        if (wdt)                                                                                    \
+            launch(k_prolong_smooth<7, W, PVF, 1>, nb, 256, 0, st, A, P, zc, r, z, wd);             \
+        else                                                                                        \
+            launch(k_prolong_smooth<7, W, PVF, 0>, nb, 256, 0, st, A, P, zc, r, z, wd);             \
+        return;                                                                                     \
+    }
+    IRK_PS(3, kU8) IRK_PS(4, kU8) IRK_PS(5, kU8) IRK_PS(6, kU8)
+    IRK_PS(3, kF64) IRK_PS(4, kF64) IRK_PS(5, kF64) IRK_PS(6, kF64)
+#undef IRK_PS
+    throw InvalidArgument("prolong_smooth_fused: unsupported prolongator width / format");
 }
 
 void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecRef y, int n,

@@ -80,6 +80,23 @@ int p1_mask();
 
 void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st);
 
+// Level-0 prolongation fused with the post-smoothing sweep (DIA A, ELL P):
+//   t_k = wd_k r_k + sum_e P(e,k) zc_{idx(e,k)}   (recomputed for each
+//   stencil neighbour k of row i), z_i = t_i + wd_i (r_i - sum_d A(d,i) t_{i+off_d}).
+// Bit-identical to the separate prolongation (kEProlong) and smoothing
+// (kESmooth) kernels: same per-row orders, padding adds exact zeros.
+struct EllP {
+    int width = 0;               // entries per row (padded)
+    const int* idx = nullptr;    // [width][rows]
+    const void* val = nullptr;   // u8 codes or f64, [width][rows]
+    const double* tab = nullptr;
+    int ntab = 0;
+    int vf = kF64;
+    int cols = 0;
+};
+void prolong_smooth_fused(const Mat& A, const EllP& P, const double* zc, VecRef r, VecRef z,
+                          const double* wd, cudaStream_t st);
+
 // Stage operator y_i = M z_i + sum_j c_ij K z_j (c = ht*A), M/K sharing one
 // DIA pattern; one pass over both value arrays for all s stage vectors.
 struct StageCoef {

@@ -155,6 +155,41 @@ void DeviceSolver::upload_values(dev::Mat& m, const std::vector<double>& vals, d
     }
 }
 
+// ELL copy of a short-row operator (the level-0 prolongator) for the fused
+// prolongation + smoothing kernel: [width][rows] indices and values, rows
+// padded with zero values on their last column.  width = 0 if too wide.
+dev::EllP DeviceSolver::upload_ell(const Csr& P, int max_width) {
+    dev::EllP e;
+    int w = 0;
+    for (int i = 0; i < P.rows; ++i) w = std::max(w, P.ptr[i + 1] - P.ptr[i]);
+    if (w < 3) w = 3;
+    if (w > max_width) return e;
+    const size_t n = static_cast<size_t>(P.rows);
+    std::vector<int> idx(w * n, 0);
+    std::vector<double> val(w * n, 0.0);
+    for (int i = 0; i < P.rows; ++i) {
+        const int lo = P.ptr[i], cnt = P.ptr[i + 1] - lo;
+        for (int k = 0; k < w; ++k) {
+            idx[k * n + i] = k < cnt ? P.idx[lo + k] : (cnt > 0 ? P.idx[lo + cnt - 1] : 0);
+            if (k < cnt) val[k * n + i] = P.val[lo + k];
+        }
+    }
+    Dict d = encode(val);
+    e.width = w;
+    e.cols = P.cols;
+    e.idx = upload_array(idx);
+    if (d.vf == dev::kU8) {
+        e.vf = dev::kU8;
+        e.val = upload_array(d.c8);
+        e.tab = upload_array(d.tab);
+        e.ntab = static_cast<int>(d.tab.size());
+    } else {
+        e.vf = dev::kF64;
+        e.val = upload_array(val);
+    }
+    return e;
+}
+
 // DIA when the pattern is <= 16 diagonals with <= 15% padding; else SELL-32.
 // `omega` > 0 requests the omega/diag dictionary (hierarchy operators).
 dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega, bool force_csr) {
@@ -263,6 +298,7 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
                            std::vector<Hierarchy> hiers, int device)
     : s_(s), device_(device), At_(At), structure_(structure), ht_(ht) {
     compress_values_ = std::getenv("IRK_NO_VALUE_CODES") == nullptr;
+    fuse_ps0_ = std::getenv("IRK_NO_PS0") == nullptr;
     fused_cgs2_ = std::getenv("IRK_FUSED_CGS2") != nullptr;  // opt-in: A/B break-even
     {
         const char* o = std::getenv("IRK_ORTHO");
@@ -362,6 +398,9 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
             if (l + 1 < L) {
                 d.P = upload(lev.P, false, 0.0, in_tail);
                 d.R = upload(lev.R, false, 0.0, in_tail);
+                if (l == 0 && fuse_ps0_ && d.A.fmt == dev::kDia && d.A.nd == 7 && d.A.vf == dev::kU8 &&
+                    h.params.pre_sweeps == 1 && h.params.post_sweeps == 1)
+                    d.pe = upload_ell(lev.P, 6);
             }
             d.t = alloc(d.n);
             d.u = alloc(d.n);
@@ -548,6 +587,12 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
         dev::dense_mv(H.nc, H.cinv, rhs_of(L - 1), out_of(L - 1), st_);
     }
     for (int l = down_end - 1; l >= first; --l) {
+        if (H.lv[l].pe.width > 0) {
+            // prolongation + post-smoothing in one kernel (level 0)
+            dev::prolong_smooth_fused(H.lv[l].A, H.lv[l].pe, H.lv[l + 1].z, rhs_of(l), out_of(l),
+                                      H.lv[l].wd, st_);
+            continue;
+        }
         if (H.fused >= 0 && l >= H.fused) {
             dev::FusedLevel f = H.fl[l];
             f.r = rhs_of(l);

@@ -58,6 +58,7 @@ struct DevLevel {
     double* t = nullptr;          // residual / prolongated iterate
     double* u = nullptr;          // post-sweep ping-pong
     double* zp = nullptr;         // pre-smoothed iterate (pre > 1 only)
+    dev::EllP pe;                 // ELL copy of P for the fused prolong+smooth (level 0)
 };
 
 struct DevHier {
@@ -116,6 +117,7 @@ public:
 
 private:
     dev::Mat upload(const Csr& A, bool allow_dia, double omega, bool force_csr = false);
+    dev::EllP upload_ell(const Csr& P, int max_width);
     void upload_values(dev::Mat& m, const std::vector<double>& vals, double omega);
     template <class T> const T* upload_array(const std::vector<T>& h);
     double* alloc(size_t count);
@@ -171,6 +173,7 @@ private:
     int launches_per_iter_ = 0;
     std::array<int, 4> launch_counts_{};
     bool compress_values_ = true;
+    bool fuse_ps0_ = true;
     bool fused_cgs2_ = true;
     int ortho_ = 1;  // 1 DCGS2 (default), 0 CGS + conditional second pass
 };
