@@ -11,8 +11,6 @@
 #include "../host/sparse.hpp"
 #include "kernels.cuh"
 
-#include <cuda_pipeline.h>
-
 namespace irkb {
 namespace dev {
 
@@ -25,14 +23,6 @@ struct Offs {
 inline int blocks_for(long long n, int t) { return static_cast<int>((n + t - 1) / t); }
 
 }  // namespace
-
-// Bit mask of the P1-stencil (multi-row) kernels in use: 1 SpMV, 2 stage
-// operator, 4 sweep (IRK_P1_MASK; default none: A/B measured slower for the
-// SpMV, profiles/r1/ab8_p1.txt).
-int p1_mask() {
-    static const int m = std::getenv("IRK_P1_MASK") ? std::atoi(std::getenv("IRK_P1_MASK")) : 0;
-    return m;
-}
 
 bool pdl_enabled() {
     static const bool on = std::getenv("IRK_PDL") != nullptr;
@@ -151,125 +141,6 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
     a.y.get()[i] = spmv_epilogue<XM, EPI>(s, wdi, i, a, r, x);
 }
 
-// P1 SW-NE stencil, u8 codes, omega/diag from the diagonal code: 4
-// consecutive rows per thread.  The 7 offsets {-w-1,-w,-1,0,1,w,w+1} of 4
-// rows need only three windows of x (5 + 6 + 5 values instead of 28
-// gathers) and one 32-bit load of codes per diagonal.  Per-row sums keep the
-// ascending-offset order of k_spmv_dia, so results are bit-identical.
-template <int XM, int EPI>
-__global__ void __launch_bounds__(256) k_spmv_p1(Mat A, SpmvArgs a) {
-    __shared__ double s_tab[256];
-    __shared__ double s_wd[256];
-    const double* tab = load_tab<kU8>(A, s_tab, s_wd);
-    pdl_wait();
-    const int n = A.rows, w = A.p1w;
-    const int i0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
-    if (i0 >= n) return;
-    const double* r = a.r.base ? a.r.get() : nullptr;
-    const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
-    const unsigned char* code = static_cast<const unsigned char*>(A.val);
-    const unsigned char* dcode = code + static_cast<long long>(A.diag0) * A.dstride;
-    auto cl = [n](int c) { return min(max(c, 0), n - 1); };
-    // windows of the x operand (XM: wd .* r) at columns i0-w-1.., i0-1.., i0+w..
-    double wa[5], wb[6], wc[5];
-    double rb[6] = {};
-    unsigned char db[6] = {};
-#pragma unroll
-    for (int q = 0; q < 6; ++q) {
-        const int c = cl(i0 - 1 + q);
-        if constexpr (XM == kXWdR) {
-            rb[q] = r[c];
-            db[q] = __ldg(dcode + c);
-            wb[q] = s_wd[db[q]] * rb[q];
-        } else {
-            wb[q] = x[c];
-            if (EPI != kEPlain) {
-                rb[q] = r[c];
-                db[q] = __ldg(dcode + c);
-            }
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-        const int ca = cl(i0 - w - 1 + q), cc = cl(i0 + w + q);
-        if constexpr (XM == kXWdR) {
-            wa[q] = s_wd[__ldg(dcode + ca)] * r[ca];
-            wc[q] = s_wd[__ldg(dcode + cc)] * r[cc];
-        } else {
-            wa[q] = x[ca];
-            wc[q] = x[cc];
-        }
-    }
-    unsigned cd[7];
-#pragma unroll
-    for (int d = 0; d < 7; ++d)
-        cd[d] = __ldg(reinterpret_cast<const unsigned*>(code + static_cast<long long>(d) * A.dstride + i0));
-    double* y = a.y.get();
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int i = i0 + q;
-        if (i >= n) break;
-        auto av = [&](int d) { return tab[(cd[d] >> (8 * q)) & 0xffu]; };
-        double s = 0.0;
-        s += av(0) * wa[q];
-        s += av(1) * wa[q + 1];
-        s += av(2) * wb[q];
-        s += av(3) * wb[q + 1];
-        s += av(4) * wb[q + 2];
-        s += av(5) * wc[q];
-        s += av(6) * wc[q + 1];
-        double out = s;
-        if (EPI == kEResid) out = rb[q + 1] - s;
-        if (EPI == kESmooth) out = x[i] + s_wd[db[q + 1]] * (rb[q + 1] - s);
-        if (EPI == kEProlong) out = (a.zb ? a.zb[i] : s_wd[db[q + 1]] * rb[q + 1]) + s;
-        y[i] = out;
-    }
-}
-
-template <int ND, int W, int PVF, int WDT>
-__global__ void __launch_bounds__(256) k_prolong_smooth(Mat A, EllP P, const double* __restrict__ zc,
-                                                        VecRef rr, VecRef zr, const double* __restrict__ wd) {
-    __shared__ double s_tab[256];
-    __shared__ double s_wd[256];
-    __shared__ double s_pt[PVF == kU8 ? 256 : 1];
-    const double* tab = load_tab<kU8>(A, s_tab, s_wd);
-    if constexpr (PVF == kU8) {
-        for (int q = threadIdx.x; q < P.ntab; q += blockDim.x) s_pt[q] = P.tab[q];
-        __syncthreads();
-    }
-    pdl_wait();
-    const int n = A.rows;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double* r = rr.get();
-    const unsigned char* dcode = static_cast<const unsigned char*>(A.val) + static_cast<long long>(A.diag0) * A.dstride;
-    const int* __restrict__ pidx = P.idx;
-    const void* pval = P.val;
-    // plain locals only (no lambda captures of kernel parameters: taking their
-    // address would force a stack copy)
-    auto wdk = [=](int k) { return WDT == 1 ? s_wd[__ldg(dcode + k)] : wd[k]; };
-    auto tval = [=](int k) {
-        double s = 0.0;
-#pragma unroll
-        for (int e = 0; e < W; ++e) {
-            const long long q = static_cast<long long>(e) * n + k;
-            const double pv = PVF == kU8 ? s_pt[__ldg(static_cast<const unsigned char*>(pval) + q)]
-                                         : __ldg(static_cast<const double*>(pval) + q);
-            s += pv * zc[__ldg(pidx + q)];
-        }
-        return wdk(k) * r[k] + s;
-    };
-    const int diag0 = A.diag0;
-    double s = 0.0, ti = 0.0;
-#pragma unroll
-    for (int d = 0; d < ND; ++d) {
-        const double t = tval(min(max(i + A.off[d], 0), n - 1));
-        s += vfetch<kU8>(A.val, static_cast<long long>(d) * A.dstride + i, tab) * t;
-        if (d == diag0) ti = t;
-    }
-    zr.get()[i] = ti + wdk(i) * (r[i] - s);
-}
-
 // SELL-32: one warp per 32-row slice, entries column-major inside the slice,
 // sequential per-row sums (same order as CSR; padding adds exact zeros).
 template <int XM, int EPI, int VF>
@@ -354,9 +225,7 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
 
 template <int XM, int EPI, int VF>
 void launch_spmv_vf(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
-    if (A.fmt == kDia && VF == kU8 && A.p1w > 0 && A.wdtab && A.diag0 >= 0 && (p1_mask() & 1)) {
-        launch(k_spmv_p1<XM, EPI>, blocks_for((A.rows + 3) / 4, 256), 256, 0, st, A, a);
-    } else if (A.fmt == kDia) {
+    if (A.fmt == kDia) {
         const int nb = blocks_for(A.rows, 256);
         const bool wdt = VF == kU8 && A.wdtab && A.diag0 >= 0;
         if (A.nd == 7) {
@@ -434,124 +303,6 @@ __global__ void __launch_bounds__(256) k_stage_op_dia(Mat M, Mat K, StageCoef cf
 #pragma unroll
         for (int j = 0; j < S; ++j) acc += cf.c[b * S + j] * fk[j];
         y[static_cast<long long>(b) * n + i] = acc;
-    }
-}
-
-// Stage operator on the P1 stencil with u8 codes, RB consecutive rows per
-// thread (windows shared across the 7 offsets, as k_spmv_p1).  Same per-row
-// operation order as k_stage_op_dia.
-template <int S, int RB>
-__global__ void __launch_bounds__(256) k_stage_op_p1(Mat M, Mat K, StageCoef cf, VecRef zr,
-                                                     VecRef yr) {
-    __shared__ double s_tm[256];
-    __shared__ double s_tk[256];
-    __shared__ double s_dummy[1];
-    const double* tm = load_tab<kU8>(M, s_tm, s_dummy);
-    const double* tk = load_tab<kU8>(K, s_tk, s_dummy);
-    pdl_wait();
-    const int n = M.rows, w = M.p1w;
-    const int i0 = RB * (blockIdx.x * blockDim.x + threadIdx.x);
-    if (i0 >= n) return;
-    const double* __restrict__ z = zr.get();
-    double* __restrict__ y = yr.get();
-    auto cl = [n](int c) { return min(max(c, 0), n - 1); };
-    const unsigned char* mc = static_cast<const unsigned char*>(M.val);
-    const unsigned char* kc = static_cast<const unsigned char*>(K.val);
-    unsigned cmd[7], ckd[7];
-#pragma unroll
-    for (int d = 0; d < 7; ++d) {
-        const long long e = static_cast<long long>(d) * M.dstride + i0;
-        if constexpr (RB == 4) {
-            cmd[d] = __ldg(reinterpret_cast<const unsigned*>(mc + e));
-            ckd[d] = __ldg(reinterpret_cast<const unsigned*>(kc + e));
-        } else {
-            cmd[d] = __ldg(reinterpret_cast<const unsigned short*>(mc + e));
-            ckd[d] = __ldg(reinterpret_cast<const unsigned short*>(kc + e));
-        }
-    }
-    double fm[RB][S], fk[RB][S];
-#pragma unroll
-    for (int q = 0; q < RB; ++q)
-#pragma unroll
-        for (int j = 0; j < S; ++j) fm[q][j] = fk[q][j] = 0.0;
-#pragma unroll
-    for (int j = 0; j < S; ++j) {
-        const double* zj = z + static_cast<long long>(j) * n;
-        double wa[RB + 1], wb[RB + 2], wc[RB + 1];
-#pragma unroll
-        for (int q = 0; q < RB + 1; ++q) {
-            wa[q] = zj[cl(i0 - w - 1 + q)];
-            wc[q] = zj[cl(i0 + w + q)];
-        }
-#pragma unroll
-        for (int q = 0; q < RB + 2; ++q) wb[q] = zj[cl(i0 - 1 + q)];
-#pragma unroll
-        for (int q = 0; q < RB; ++q) {
-            const double xs[7] = {wa[q], wa[q + 1], wb[q], wb[q + 1], wb[q + 2], wc[q], wc[q + 1]};
-#pragma unroll
-            for (int d = 0; d < 7; ++d) {
-                const double m = tm[(cmd[d] >> (8 * q)) & 0xffu];
-                const double k = tk[(ckd[d] >> (8 * q)) & 0xffu];
-                fm[q][j] += m * xs[d];
-                fk[q][j] += k * xs[d];
-            }
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < RB; ++q) {
-        const int i = i0 + q;
-        if (i >= n) break;
-#pragma unroll
-        for (int b = 0; b < S; ++b) {
-            double acc = fm[q][b];
-#pragma unroll
-            for (int j = 0; j < S; ++j) acc += cf.c[b * S + j] * fk[q][j];
-            y[static_cast<long long>(b) * n + i] = acc;
-        }
-    }
-}
-
-// Block sweep on the P1 stencil (u8): fresh = K w for 4 rows per thread.
-__global__ void __launch_bounds__(256) k_sweep_p1(Mat K, VecRef wr, VecRef vr, SweepTerms t,
-                                                  double* __restrict__ store, VecRef outr) {
-    __shared__ double s_tk[256];
-    __shared__ double s_dummy[1];
-    const double* tk = load_tab<kU8>(K, s_tk, s_dummy);
-    pdl_wait();
-    const int n = K.rows, w = K.p1w;
-    const int i0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
-    if (i0 >= n) return;
-    const double* __restrict__ wv = wr.get();
-    auto cl = [n](int c) { return min(max(c, 0), n - 1); };
-    const unsigned char* kc = static_cast<const unsigned char*>(K.val);
-    unsigned ckd[7];
-#pragma unroll
-    for (int d = 0; d < 7; ++d)
-        ckd[d] = __ldg(reinterpret_cast<const unsigned*>(kc + static_cast<long long>(d) * K.dstride + i0));
-    double wa[5], wb[6], wc[5];
-#pragma unroll
-    for (int q = 0; q < 5; ++q) {
-        wa[q] = wv[cl(i0 - w - 1 + q)];
-        wc[q] = wv[cl(i0 + w + q)];
-    }
-#pragma unroll
-    for (int q = 0; q < 6; ++q) wb[q] = wv[cl(i0 - 1 + q)];
-    const double* v = vr.get();
-    double* out = outr.get();
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int i = i0 + q;
-        if (i >= n) break;
-        const double xs[7] = {wa[q], wa[q + 1], wb[q], wb[q + 1], wb[q + 2], wc[q], wc[q + 1]};
-        double f = 0.0;
-#pragma unroll
-        for (int d = 0; d < 7; ++d) f += tk[(ckd[d] >> (8 * q)) & 0xffu] * xs[d];
-        if (store) store[i] = f;
-        double acc = v[i];
-#pragma unroll
-        for (int k = 0; k < kMaxStages; ++k)
-            if (k < t.nt) acc += t.coef[k] * (t.buf[k] ? t.buf[k][i] : f);
-        out[i] = acc;
     }
 }
 
@@ -786,28 +537,6 @@ __device__ __forceinline__ void load_chunk(const double* __restrict__ v, long lo
     }
 }
 
-// As load_chunk, with default caching (re-reads that should hit L2).
-__device__ __forceinline__ void load_chunk_l2(const double* __restrict__ v, long long n, int c,
-                                              double (&o)[kRedPerThread]) {
-    const long long base = static_cast<long long>(c) * kChunk + 2 * threadIdx.x;
-    if (static_cast<long long>(c + 1) * kChunk <= n) {
-#pragma unroll
-        for (int u = 0; u < kRedPerThread / 2; ++u) {
-            const double2 p = __ldcg(reinterpret_cast<const double2*>(v + base + u * 2 * kRedThreads));
-            o[2 * u] = p.x;
-            o[2 * u + 1] = p.y;
-        }
-    } else {
-#pragma unroll
-        for (int u = 0; u < kRedPerThread / 2; ++u)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const long long k = base + u * 2 * kRedThreads + e;
-                o[2 * u + e] = k < n ? v[k] : 0.0;
-            }
-    }
-}
-
 __device__ __forceinline__ void store_chunk(double* v, long long n, int c,
                                             const double (&o)[kRedPerThread]) {
     const long long base = static_cast<long long>(c) * kChunk + 2 * threadIdx.x;
@@ -981,68 +710,6 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_update(GmresBufs g, int pass
     }
 }
 
-// Pass-1 update fused with the pass-2 block-dot (CGS2): per chunk,
-// w' = w - sum_i h_i V_i, then c_i = V_i . w' and ||w'||^2 with V_i re-read
-// (in reverse order, most recently loaded first) while it is still in L2.  A
-// persistent grid of at most one CTA per SM keeps the re-read working set
-// (CTAs x (j+1) x 32 KB) near L2 capacity.  Per-vector partials use exactly
-// the chunk tree of k_gm_blockdot / k_gm_update, so c and ||w'|| are
-// bit-identical to running those two kernels; when the 0.7071 test says no
-// re-orthogonalisation is needed, c is simply dropped.
-__global__ void __launch_bounds__(kRedThreads) k_gm_update_cgs2(GmresBufs g) {
-    extern __shared__ double red[];
-    pdl_trigger();
-    pdl_wait();
-    GmresCtl* ctl = g.ctl;
-    const int j = ctl->j;
-    const int nb = j + 1;
-    const int nv = nb + 1;  // c_0..c_j, ||w'||^2
-    double* cf = red + (kRedThreads / 32) * nv + nv + 1;
-    for (int i = threadIdx.x; i < nb; i += kRedThreads) cf[i] = ctl->hcol[i];
-    __syncthreads();
-    const long long n = g.sN;
-    const long long stride = (g.sN + 63) / 64 * 64;
-    double* wp = g.V + static_cast<long long>(j + 1) * stride;
-    for (int c = blockIdx.x; c < g.nchunks; c += gridDim.x) {
-        double w[kRedPerThread];
-        load_chunk(wp, n, c, w);
-        for (int i = 0; i < nb; ++i) {
-            double v[kRedPerThread];
-            load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v);
-            const double h = cf[i];
-#pragma unroll
-            for (int q = 0; q < kRedPerThread; ++q) w[q] = w[q] - h * v[q];
-        }
-        store_chunk(wp, n, c, w);
-        warp_tree_store(chunk_dot_local(w, w), red, nv, nb);
-        for (int i = nb - 1; i >= 0; --i) {
-            double v[kRedPerThread];
-            load_chunk_l2(g.V + static_cast<long long>(i) * stride, n, c, v);
-            warp_tree_store(chunk_dot_local(v, w), red, nv, i);
-        }
-        __syncthreads();
-        for (int q = threadIdx.x; q < nv; q += kRedThreads)
-            g.partials[static_cast<long long>(q) * g.nchunks + c] = warp_sum8(red, nv, q);
-        __syncthreads();
-    }
-    if (!elect_last(g.counters + 8)) return;
-    double* res = red + (kRedThreads / 32) * nv;
-    final_reduce(g.partials, g.nchunks, nv, red, res);
-    if (threadIdx.x == 0) {
-        const double nrm = sqrt(res[nb]);
-        ctl->after = nrm;
-        if (nrm < 0.70710678118654752 * ctl->before) {
-            ctl->reorth = 1;
-            for (int i = 0; i < nb; ++i) ctl->y[i] = res[i];
-        } else {
-            ctl->reorth = 0;
-            ctl->hnext = nrm;
-            arnoldi_tail(g);
-        }
-        g.counters[8] = 0u;
-    }
-}
-
 // Rotates column col (entries 0..j+1) with rotations 0..j-1, adds rotation j
 // and updates g (gmres.cpp:93-112); identical to oracle givens_column().
 __device__ void givens_column(GmresCtl* c, double* col, int j) {
@@ -1158,432 +825,6 @@ __device__ void dgs_dot_scalars(const GmresBufs& g, int j, int finalize, int nvv
     ctl->inv_alpha = alpha > 0.0 ? 1.0 / alpha : 0.0;
     ctl->hnext = alpha;
     if (!(alpha == alpha)) ctl->bad = 1;
-}
-
-// Half-chunk load: elements u = 4h..4h+3 of the thread's (u, e) sequence, so
-// processing half 0 then half 1 keeps the contract's per-thread order.
-template <bool kKeepL1 = false>
-__device__ __forceinline__ void load_half(const double* __restrict__ v, long long n, int c, int h,
-                                          double (&o)[kRedPerThread / 2]) {
-    const long long base = static_cast<long long>(c) * kChunk + 2 * threadIdx.x;
-    if (static_cast<long long>(c + 1) * kChunk <= n) {
-#pragma unroll
-        for (int u = 0; u < kRedPerThread / 4; ++u) {
-            const double2* src = reinterpret_cast<const double2*>(v + base + (4 * h + u) * 2 * kRedThreads);
-            const double2 p = kKeepL1 ? __ldca(src) : __ldcs(src);
-            o[2 * u] = p.x;
-            o[2 * u + 1] = p.y;
-        }
-    } else {
-#pragma unroll
-        for (int u = 0; u < kRedPerThread / 4; ++u)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const long long k = base + (4 * h + u) * 2 * kRedThreads + e;
-                o[2 * u + e] = k < n ? v[k] : 0.0;
-            }
-    }
-}
-
-__device__ __forceinline__ void store_half(double* v, long long n, int c, int h,
-                                           const double (&o)[kRedPerThread / 2]) {
-    const long long base = static_cast<long long>(c) * kChunk + 2 * threadIdx.x;
-    if (static_cast<long long>(c + 1) * kChunk <= n) {
-#pragma unroll
-        for (int u = 0; u < kRedPerThread / 4; ++u)
-            *reinterpret_cast<double2*>(v + base + (4 * h + u) * 2 * kRedThreads) =
-                make_double2(o[2 * u], o[2 * u + 1]);
-    } else {
-#pragma unroll
-        for (int u = 0; u < kRedPerThread / 4; ++u)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const long long k = base + (4 * h + u) * 2 * kRedThreads + e;
-                if (k < n) v[k] = o[2 * u + e];
-            }
-    }
-}
-
-// Low-register DCGS2 update: the chunk in two halves (order-preserving).
-template <bool COND>
-__global__ void __launch_bounds__(kRedThreads, 3) k_dgs_update_h(GmresBufs g) {
-    extern __shared__ double red[];
-    pdl_trigger();
-    pdl_wait();
-    GmresCtl* ctl = g.ctl;
-    const int j = ctl->j;
-    double* sc = red + kRedThreads / 32 + 1;
-    double* pc = sc + j + 1;
-    for (int i = threadIdx.x; i < j; i += kRedThreads) {
-        sc[i] = ctl->sv[i];
-        pc[i] = ctl->pv[i];
-    }
-    __syncthreads();
-    const double inv = ctl->inv_alpha, hjj = ctl->hjj;
-    const int c = blockIdx.x;
-    const long long n = g.sN;
-    const long long stride = (g.sN + 63) / 64 * 64;
-    double* ap = g.V + static_cast<long long>(j) * stride;
-    double* bp = g.V + static_cast<long long>(j + 1) * stride;
-    double acc = 0.0;
-    for (int h = 0; h < 2; ++h) {
-        double a[kRedPerThread / 2], b[kRedPerThread / 2];
-        load_half(ap, n, c, h, a);
-        load_half(bp, n, c, h, b);
-        for (int i = 0; i < j; ++i) {
-            double v[kRedPerThread / 2];
-            load_half(g.V + static_cast<long long>(i) * stride, n, c, h, v);
-            const double si = sc[i], pi = pc[i];
-#pragma unroll
-            for (int q = 0; q < kRedPerThread / 2; ++q) {
-                a[q] = a[q] - si * v[q];
-                b[q] = b[q] - pi * v[q];
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < kRedPerThread / 2; ++q) {
-            a[q] = a[q] * inv;
-            b[q] = b[q] - hjj * a[q];
-            acc += b[q] * b[q];
-        }
-        store_half(ap, n, c, h, a);
-        store_half(bp, n, c, h, b);
-    }
-    warp_tree_store(acc, red, 1, 0);
-    __syncthreads();
-    if (threadIdx.x == 0) g.partials[c] = warp_sum8(red, 1, 0);
-    if (!elect_last(g.counters + 10)) return;
-    double* res = red + kRedThreads / 32;
-    final_reduce(g.partials, g.nchunks, 1, red, res);
-    if (threadIdx.x != 0) return;
-    g.counters[10] = 0u;
-    dgs_stop_test<COND>(g, j, sqrt(res[0]));
-}
-
-// Low-register DCGS2 block-dot: per basis vector, the two target chunks are
-// re-read (L1-resident) half by half; per-thread order as k_dgs_dot.
-__global__ void __launch_bounds__(kRedThreads, 3) k_dgs_dot_h(GmresBufs g, int finalize) {
-    extern __shared__ double red[];
-    pdl_trigger();
-    pdl_wait();
-    GmresCtl* ctl = g.ctl;
-    const int j = ctl->j;
-    const int nvv = finalize ? j + 1 : j;
-    const int nv = finalize ? nvv + 1 : 2 * nvv + 2;
-    const int c = blockIdx.x;
-    const long long n = g.sN;
-    const long long stride = (g.sN + 63) / 64 * 64;
-    const double* ap = g.V + static_cast<long long>(j) * stride;
-    const double* bp = g.V + static_cast<long long>(j + 1) * stride;
-    if (finalize) {
-        double acc = 0.0;
-        for (int h = 0; h < 2; ++h) {
-            double b[kRedPerThread / 2];
-            load_half<true>(bp, n, c, h, b);
-#pragma unroll
-            for (int q = 0; q < kRedPerThread / 2; ++q) acc += b[q] * b[q];
-        }
-        warp_tree_store(acc, red, nv, nvv);
-        for (int i = 0; i < nvv; ++i) {
-            double ab = 0.0;
-            for (int h = 0; h < 2; ++h) {
-                double b[kRedPerThread / 2], v[kRedPerThread / 2];
-                load_half<true>(bp, n, c, h, b);
-                load_half(g.V + static_cast<long long>(i) * stride, n, c, h, v);
-#pragma unroll
-                for (int q = 0; q < kRedPerThread / 2; ++q) ab += v[q] * b[q];
-            }
-            warp_tree_store(ab, red, nv, i);
-        }
-    } else {
-        double aa = 0.0, ab = 0.0;
-        for (int h = 0; h < 2; ++h) {
-            double a[kRedPerThread / 2], b[kRedPerThread / 2];
-            load_half<true>(ap, n, c, h, a);
-            load_half<true>(bp, n, c, h, b);
-#pragma unroll
-            for (int q = 0; q < kRedPerThread / 2; ++q) {
-                aa += a[q] * a[q];
-                ab += a[q] * b[q];
-            }
-        }
-        warp_tree_store(aa, red, nv, 2 * nvv);
-        warp_tree_store(ab, red, nv, 2 * nvv + 1);
-        for (int i = 0; i < nvv; ++i) {
-            double sa = 0.0, sb = 0.0;
-            for (int h = 0; h < 2; ++h) {
-                double a[kRedPerThread / 2], b[kRedPerThread / 2], v[kRedPerThread / 2];
-                load_half(g.V + static_cast<long long>(i) * stride, n, c, h, v);
-                load_half<true>(ap, n, c, h, a);
-                load_half<true>(bp, n, c, h, b);
-#pragma unroll
-                for (int q = 0; q < kRedPerThread / 2; ++q) {
-                    sa += v[q] * a[q];
-                    sb += v[q] * b[q];
-                }
-            }
-            warp_tree_store(sa, red, nv, i);
-            warp_tree_store(sb, red, nv, nvv + i);
-        }
-    }
-    __syncthreads();
-    for (int q = threadIdx.x; q < nv; q += kRedThreads)
-        g.partials[static_cast<long long>(q) * g.nchunks + c] = warp_sum8(red, nv, q);
-    if (!elect_last(g.counters + 9)) return;
-    double* res = red + (kRedThreads / 32) * nv;
-    final_reduce(g.partials, g.nchunks, nv, red, res);
-    if (threadIdx.x != 0) return;
-    g.counters[9] = 0u;
-    dgs_dot_scalars(g, j, finalize, nvv, res);
-}
-
-// cp.async ring for streaming basis vectors: each thread copies exactly the
-// 16-byte pieces it later consumes (its 16 contract elements of the chunk),
-// so producer and consumer are the same thread and only cp.async
-// wait_group is needed -- no block barriers.  Layout [stage][u][thread]
-// (16 B per (u, thread)) keeps the shared-memory reads conflict-free.
-constexpr int kPipeStages = 3;
-constexpr int kPipeStageBytes = kChunk * 8;  // 32 KB per stage
-
-__device__ __forceinline__ void pipe_issue(double2* ring, int stage, const double* v, int c) {
-    const double* base = v + static_cast<long long>(c) * kChunk + 2 * threadIdx.x;
-    double2* dst = ring + stage * (kChunk / 2) + threadIdx.x;
-#pragma unroll
-    for (int u = 0; u < kRedPerThread / 2; ++u)
-        __pipeline_memcpy_async(dst + u * kRedThreads, base + u * 2 * kRedThreads, 16);
-}
-
-__device__ __forceinline__ void pipe_read(const double2* ring, int stage, double (&o)[kRedPerThread]) {
-    const double2* src = ring + stage * (kChunk / 2) + threadIdx.x;
-#pragma unroll
-    for (int u = 0; u < kRedPerThread / 2; ++u) {
-        const double2 p = src[u * kRedThreads];
-        o[2 * u] = p.x;
-        o[2 * u + 1] = p.y;
-    }
-}
-
-// DCGS2 block-dot with the cp.async ring (full chunks; the partial last
-// chunk takes the direct-load path).  Same values and order as k_dgs_dot.
-__global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot_pipe(GmresBufs g, int finalize) {
-    extern __shared__ double red[];
-    pdl_trigger();
-    pdl_wait();
-    GmresCtl* ctl = g.ctl;
-    const int j = ctl->j;
-    const int nvv = finalize ? j + 1 : j;
-    const int nv = finalize ? nvv + 1 : 2 * nvv + 2;
-    const int c = blockIdx.x;
-    const long long n = g.sN;
-    const long long stride = (g.sN + 63) / 64 * 64;
-    double2* ring = reinterpret_cast<double2*>(red);
-    double* tree = red + kPipeStages * kChunk;  // (8 x nv) warp values, then results
-    const bool full = static_cast<long long>(c + 1) * kChunk <= n;
-    double b[kRedPerThread];
-    load_chunk(g.V + static_cast<long long>(j + 1) * stride, n, c, b);
-    double a[kRedPerThread];
-    if (!finalize) load_chunk(g.V + static_cast<long long>(j) * stride, n, c, a);
-    if (full) {
-#pragma unroll
-        for (int st = 0; st < kPipeStages - 1; ++st) {
-            if (st < nvv) pipe_issue(ring, st, g.V + static_cast<long long>(st) * stride, c);
-            __pipeline_commit();
-        }
-    }
-    if (finalize) {
-        warp_tree_store(chunk_dot_local(b, b), tree, nv, nvv);
-    } else {
-        warp_tree_store(chunk_dot_local(a, a), tree, nv, 2 * nvv);
-        warp_tree_store(chunk_dot_local(a, b), tree, nv, 2 * nvv + 1);
-    }
-    for (int i = 0; i < nvv; ++i) {
-        double v[kRedPerThread];
-        if (full) {
-            const int ahead = i + kPipeStages - 1;
-            if (ahead < nvv)
-                pipe_issue(ring, ahead % kPipeStages, g.V + static_cast<long long>(ahead) * stride, c);
-            __pipeline_commit();
-            __pipeline_wait_prior(kPipeStages - 1);
-            pipe_read(ring, i % kPipeStages, v);
-        } else {
-            load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v);
-        }
-        if (finalize) {
-            warp_tree_store(chunk_dot_local(v, b), tree, nv, i);
-        } else {
-            warp_tree_store(chunk_dot_local(v, a), tree, nv, i);
-            warp_tree_store(chunk_dot_local(v, b), tree, nv, nvv + i);
-        }
-    }
-    __syncthreads();
-    for (int q = threadIdx.x; q < nv; q += kRedThreads)
-        g.partials[static_cast<long long>(q) * g.nchunks + c] = warp_sum8(tree, nv, q);
-    if (!elect_last(g.counters + 9)) return;
-    double* res = tree + (kRedThreads / 32) * nv;
-    final_reduce(g.partials, g.nchunks, nv, tree, res);
-    if (threadIdx.x != 0) return;
-    g.counters[9] = 0u;
-    dgs_dot_scalars(g, j, finalize, nvv, res);
-}
-
-// DCGS2 update with the cp.async ring.  Same per-element order as k_dgs_update.
-template <bool COND>
-__global__ void __launch_bounds__(kRedThreads, 2) k_dgs_update_pipe(GmresBufs g) {
-    extern __shared__ double red[];
-    pdl_trigger();
-    pdl_wait();
-    GmresCtl* ctl = g.ctl;
-    const int j = ctl->j;
-    double2* ring = reinterpret_cast<double2*>(red);
-    double* tree = red + kPipeStages * kChunk;
-    double* sc = tree + kRedThreads / 32 + 1;
-    double* pc = sc + j + 1;
-    for (int i = threadIdx.x; i < j; i += kRedThreads) {
-        sc[i] = ctl->sv[i];
-        pc[i] = ctl->pv[i];
-    }
-    __syncthreads();
-    const double inv = ctl->inv_alpha, hjj = ctl->hjj;
-    const int c = blockIdx.x;
-    const long long n = g.sN;
-    const long long stride = (g.sN + 63) / 64 * 64;
-    const bool full = static_cast<long long>(c + 1) * kChunk <= n;
-    double* ap = g.V + static_cast<long long>(j) * stride;
-    double* bp = g.V + static_cast<long long>(j + 1) * stride;
-    if (full) {
-#pragma unroll
-        for (int st = 0; st < kPipeStages - 1; ++st) {
-            if (st < j) pipe_issue(ring, st, g.V + static_cast<long long>(st) * stride, c);
-            __pipeline_commit();
-        }
-    }
-    double a[kRedPerThread], b[kRedPerThread];
-    load_chunk(ap, n, c, a);
-    load_chunk(bp, n, c, b);
-    for (int i = 0; i < j; ++i) {
-        double v[kRedPerThread];
-        if (full) {
-            const int ahead = i + kPipeStages - 1;
-            if (ahead < j)
-                pipe_issue(ring, ahead % kPipeStages, g.V + static_cast<long long>(ahead) * stride, c);
-            __pipeline_commit();
-            __pipeline_wait_prior(kPipeStages - 1);
-            pipe_read(ring, i % kPipeStages, v);
-        } else {
-            load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v);
-        }
-        const double si = sc[i], pi = pc[i];
-#pragma unroll
-        for (int q = 0; q < kRedPerThread; ++q) {
-            a[q] = a[q] - si * v[q];
-            b[q] = b[q] - pi * v[q];
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < kRedPerThread; ++q) {
-        a[q] = a[q] * inv;
-        b[q] = b[q] - hjj * a[q];
-    }
-    store_chunk(ap, n, c, a);
-    store_chunk(bp, n, c, b);
-    warp_tree_store(chunk_dot_local(b, b), tree, 1, 0);
-    __syncthreads();
-    if (threadIdx.x == 0) g.partials[c] = warp_sum8(tree, 1, 0);
-    if (!elect_last(g.counters + 10)) return;
-    double* res = tree + kRedThreads / 32;
-    final_reduce(g.partials, g.nchunks, 1, tree, res);
-    if (threadIdx.x != 0) return;
-    g.counters[10] = 0u;
-    dgs_stop_test<COND>(g, j, sqrt(res[0]));
-}
-
-// DCGS2 block-dot, low-register / deep-prefetch variant: the thread's target
-// elements (vt_j and w) live in shared memory ([q][thread], conflict-free),
-// basis vectors are streamed two at a time (32 loads of 16 B in flight per
-// thread).  Same per-thread order and values as k_dgs_dot.
-__global__ void __launch_bounds__(kRedThreads, 3) k_dgs_dot_s(GmresBufs g, int finalize) {
-    extern __shared__ double red[];
-    pdl_trigger();
-    pdl_wait();
-    GmresCtl* ctl = g.ctl;
-    const int j = ctl->j;
-    const int nvv = finalize ? j + 1 : j;
-    const int nv = finalize ? nvv + 1 : 2 * nvv + 2;
-    const int c = blockIdx.x;
-    const long long n = g.sN;
-    const long long stride = (g.sN + 63) / 64 * 64;
-    double* sa = red;                         // [16][256]
-    double* sb = red + kChunk;                // [16][256]
-    double* tree = red + 2 * kChunk;
-    const int t = threadIdx.x;
-    {
-        double b[kRedPerThread];
-        load_chunk(g.V + static_cast<long long>(j + 1) * stride, n, c, b);
-#pragma unroll
-        for (int q = 0; q < kRedPerThread; ++q) sb[q * kRedThreads + t] = b[q];
-        if (finalize) {
-            warp_tree_store(chunk_dot_local(b, b), tree, nv, nvv);
-        } else {
-            double a[kRedPerThread];
-            load_chunk(g.V + static_cast<long long>(j) * stride, n, c, a);
-#pragma unroll
-            for (int q = 0; q < kRedPerThread; ++q) sa[q * kRedThreads + t] = a[q];
-            warp_tree_store(chunk_dot_local(a, a), tree, nv, 2 * nvv);
-            warp_tree_store(chunk_dot_local(a, b), tree, nv, 2 * nvv + 1);
-        }
-    }
-    int i = 0;
-    for (; i + 1 < nvv; i += 2) {
-        double v0[kRedPerThread], v1[kRedPerThread];
-        load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v0);
-        load_chunk(g.V + static_cast<long long>(i + 1) * stride, n, c, v1);
-        double sa0 = 0.0, sb0 = 0.0, sa1 = 0.0, sb1 = 0.0;
-#pragma unroll
-        for (int q = 0; q < kRedPerThread; ++q) {
-            const double bq = sb[q * kRedThreads + t];
-            sb0 += v0[q] * bq;
-            sb1 += v1[q] * bq;
-            if (!finalize) {
-                const double aq = sa[q * kRedThreads + t];
-                sa0 += v0[q] * aq;
-                sa1 += v1[q] * aq;
-            }
-        }
-        if (finalize) {
-            warp_tree_store(sb0, tree, nv, i);
-            warp_tree_store(sb1, tree, nv, i + 1);
-        } else {
-            warp_tree_store(sa0, tree, nv, i);
-            warp_tree_store(sb0, tree, nv, nvv + i);
-            warp_tree_store(sa1, tree, nv, i + 1);
-            warp_tree_store(sb1, tree, nv, nvv + i + 1);
-        }
-    }
-    for (; i < nvv; ++i) {
-        double v0[kRedPerThread];
-        load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v0);
-        double sa0 = 0.0, sb0 = 0.0;
-#pragma unroll
-        for (int q = 0; q < kRedPerThread; ++q) {
-            sb0 += v0[q] * sb[q * kRedThreads + t];
-            if (!finalize) sa0 += v0[q] * sa[q * kRedThreads + t];
-        }
-        if (finalize) {
-            warp_tree_store(sb0, tree, nv, i);
-        } else {
-            warp_tree_store(sa0, tree, nv, i);
-            warp_tree_store(sb0, tree, nv, nvv + i);
-        }
-    }
-    __syncthreads();
-    for (int q = threadIdx.x; q < nv; q += kRedThreads)
-        g.partials[static_cast<long long>(q) * g.nchunks + c] = warp_sum8(tree, nv, q);
-    if (!elect_last(g.counters + 9)) return;
-    double* res = tree + (kRedThreads / 32) * nv;
-    final_reduce(g.partials, g.nchunks, nv, tree, res);
-    if (threadIdx.x != 0) return;
-    g.counters[9] = 0u;
-    dgs_dot_scalars(g, j, finalize, nvv, res);
 }
 
 // DCGS2 block-dot.  Iteration j (finalize = 0): targets A = slot j (vt_j) and
@@ -1886,43 +1127,12 @@ void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st) 
     throw InvalidArgument("spmv: unsupported mode combination");
 }
 
-void prolong_smooth_fused(const Mat& A, const EllP& P, const double* zc, VecRef r, VecRef z,
-                          const double* wd, cudaStream_t st) {
-    const int nb = blocks_for(A.rows, 256);
-    const bool wdt = A.wdtab && A.diag0 >= 0;
-    if (A.nd != 7 || A.vf != kU8) throw InvalidArgument("prolong_smooth_fused: needs a 7-diagonal u8 DIA A");
-#define IRK_PS(W, PVF)                                                                              \
-    if (P.width == W && P.vf == PVF) {                                                              \
-        if (wdt)                                                                                    \
-            launch(k_prolong_smooth<7, W, PVF, 1>, nb, 256, 0, st, A, P, zc, r, z, wd);             \
-        else                                                                                        \
-            launch(k_prolong_smooth<7, W, PVF, 0>, nb, 256, 0, st, A, P, zc, r, z, wd);             \
-        return;                                                                                     \
-    }
-    IRK_PS(3, kU8) IRK_PS(4, kU8) IRK_PS(5, kU8) IRK_PS(6, kU8)
-    IRK_PS(3, kF64) IRK_PS(4, kF64) IRK_PS(5, kF64) IRK_PS(6, kF64)
-#undef IRK_PS
-    throw InvalidArgument("prolong_smooth_fused: unsupported prolongator width / format");
-}
-
 void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecRef y, int n,
                   cudaStream_t st) {
     const int nb = blocks_for(n, 256);
     if (M.vf != K.vf || (M.vf != kF64 && M.vf != kU8))
         throw InvalidArgument("stage_op: M and K must share a value format (f64 or u8)");
     const bool u8 = M.vf == kU8;
-    if (u8 && M.p1w > 0 && M.p1w == K.p1w && M.dstride == K.dstride && (p1_mask() & 2)) {
-        switch (c.s) {
-#define IRK_OP_P1(S, RB)                                                                   \
-    case S:                                                                                \
-        launch(k_stage_op_p1<S, RB>, blocks_for((n + RB - 1) / RB, 256), 256, 0, st, M, K, c, z, y); \
-        return;
-            IRK_OP_P1(1, 4) IRK_OP_P1(2, 4) IRK_OP_P1(3, 4) IRK_OP_P1(4, 4) IRK_OP_P1(5, 2)
-            IRK_OP_P1(6, 2) IRK_OP_P1(7, 2)
-#undef IRK_OP_P1
-        default: break;
-        }
-    }
     switch (c.s) {
 #define IRK_OP_CASE(S)                                                             \
     case S:                                                                        \
@@ -1943,10 +1153,6 @@ void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecR
 
 void sweep_dia(const Mat& K, VecRef w, VecRef v, const SweepTerms& t, double* store, VecRef out,
                int n, cudaStream_t st) {
-    if (K.vf == kU8 && K.p1w > 0 && (p1_mask() & 4)) {
-        launch(k_sweep_p1, blocks_for((n + 3) / 4, 256), 256, 0, st, K, w, v, t, store, out);
-        return;
-    }
     switch (K.vf) {
     case kU8:
         if (K.nd == 7)
@@ -2012,62 +1218,17 @@ void gm_update(const GmresBufs& g, int pass, cudaStream_t st) {
     launch(k_gm_update, g.nchunks, kRedThreads, sizeof(double) * (kRedThreads / 32 + 1 + kMaxRestart + 8), st, g, pass);
 }
 
-void gm_update_cgs2(const GmresBufs& g, cudaStream_t st) {
-    static int ctas = [] {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const char* e = std::getenv("IRK_CGS2_CTAS_PER_SM");
-        return sms * (e ? std::max(1, std::atoi(e)) : 1);
-    }();
-    const int grid = std::min(g.nchunks, ctas);
-    const size_t smem = sizeof(double) * ((kRedThreads / 32 + 1) * (kMaxRestart + 2) + kMaxRestart + 16);
-    launch(k_gm_update_cgs2, grid, kRedThreads, smem, st, g);
-}
-
 static size_t dgs_smem(const GmresBufs& g) {
     const int nv = 2 * g.cap + 4;
     return sizeof(double) * ((kRedThreads / 32 + 1) * nv + 16);
 }
 
-static size_t dgs_pipe_smem(const GmresBufs& g) {
-    return sizeof(double) * kPipeStages * kChunk + dgs_smem(g);
-}
-
-static int dgs_variant() {
-    // 0 = direct loads (default), 1 = half-chunk, 2 = cp.async ring (A/B: both slower)
-    static const int v = std::getenv("IRK_DGS") ? std::atoi(std::getenv("IRK_DGS")) : 0;
-    return v;
-}
-
 void gm_dgs_dot(const GmresBufs& g, int finalize, cudaStream_t st) {
-    if (dgs_variant() == 3) {
-        launch(k_dgs_dot_s, g.nchunks, kRedThreads, sizeof(double) * 2 * kChunk + dgs_smem(g), st, g,
-               finalize);
-        return;
-    }
-    if (dgs_variant() == 2) {
-        launch(k_dgs_dot_pipe, g.nchunks, kRedThreads, dgs_pipe_smem(g), st, g, finalize);
-        return;
-    }
-    const bool half = dgs_variant() == 1;
-    if (half)
-        launch(k_dgs_dot_h, g.nchunks, kRedThreads, dgs_smem(g), st, g, finalize);
-    else
-        launch(k_dgs_dot, g.nchunks, kRedThreads, dgs_smem(g), st, g, finalize);
+    launch(k_dgs_dot, g.nchunks, kRedThreads, dgs_smem(g), st, g, finalize);
 }
 
 void gm_dgs_update(const GmresBufs& g, cudaStream_t st) {
-    if (dgs_variant() == 2) {
-        launch(g.use_cond ? k_dgs_update_pipe<true> : k_dgs_update_pipe<false>, g.nchunks, kRedThreads,
-               dgs_pipe_smem(g), st, g);
-        return;
-    }
-    const bool half = dgs_variant() == 1;
-    if (half)
-        launch(g.use_cond ? k_dgs_update_h<true> : k_dgs_update_h<false>, g.nchunks, kRedThreads, dgs_smem(g), st, g);
-    else
-        launch(g.use_cond ? k_dgs_update<true> : k_dgs_update<false>, g.nchunks, kRedThreads, dgs_smem(g), st, g);
+    launch(g.use_cond ? k_dgs_update<true> : k_dgs_update<false>, g.nchunks, kRedThreads, dgs_smem(g), st, g);
 }
 
 void gm_normalize(const GmresBufs& g, cudaStream_t st) {
@@ -2095,18 +1256,6 @@ void set_smem_limits() {
     cudaFuncSetAttribute(k_dgs_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_dgs_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_dgs_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_dgs_update_h<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_dgs_update_h<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_dgs_dot_h, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    const int pipe = big + static_cast<int>(sizeof(double)) * kPipeStages * kChunk;
-    cudaFuncSetAttribute(k_dgs_dot_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, pipe);
-    cudaFuncSetAttribute(k_dgs_dot_s, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         big + static_cast<int>(sizeof(double)) * 2 * kChunk);
-    cudaFuncSetAttribute(k_dgs_update_pipe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pipe);
-    cudaFuncSetAttribute(k_dgs_update_pipe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, pipe);
-    cudaFuncSetAttribute(k_gm_update_cgs2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(sizeof(double) * ((kRedThreads / 32 + 1) * (kMaxRestart + 2) +
-                                                            kMaxRestart + 16)));
     cudaFuncSetAttribute(k_dense_mv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const int nv = kMaxRestart + 2;
     cudaFuncSetAttribute(k_gm_blockdot, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -48,8 +48,6 @@ struct Mat {
     int off[kMaxDiags] = {};
     int diag0 = -1;                 // slot of offset 0
     long long dstride = 0;          // entries per stored diagonal (>= rows, multiple of 4)
-    int p1w = 0;                    // > 0: offsets are the P1 SW-NE stencil
-                                    //   {-w-1, -w, -1, 0, 1, w, w+1}
     const double* wdtab = nullptr;  // omega / diagonal value per code (DIA, u8)
     size_t bytes = 0;               // device bytes of the stored operator
 };
@@ -75,27 +73,8 @@ struct SpmvArgs {
 
 // Programmatic dependent launch, opt-in via IRK_PDL=1.
 bool pdl_enabled();
-// Multi-row P1-stencil kernels in use (bit mask, IRK_P1_MASK).
-int p1_mask();
 
 void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st);
-
-// Level-0 prolongation fused with the post-smoothing sweep (DIA A, ELL P):
-//   t_k = wd_k r_k + sum_e P(e,k) zc_{idx(e,k)}   (recomputed for each
-//   stencil neighbour k of row i), z_i = t_i + wd_i (r_i - sum_d A(d,i) t_{i+off_d}).
-// Bit-identical to the separate prolongation (kEProlong) and smoothing
-// (kESmooth) kernels: same per-row orders, padding adds exact zeros.
-struct EllP {
-    int width = 0;               // entries per row (padded)
-    const int* idx = nullptr;    // [width][rows]
-    const void* val = nullptr;   // u8 codes or f64, [width][rows]
-    const double* tab = nullptr;
-    int ntab = 0;
-    int vf = kF64;
-    int cols = 0;
-};
-void prolong_smooth_fused(const Mat& A, const EllP& P, const double* zc, VecRef r, VecRef z,
-                          const double* wd, cudaStream_t st);
 
 // Stage operator y_i = M z_i + sum_j c_ij K z_j (c = ht*A), M/K sharing one
 // DIA pattern; one pass over both value arrays for all s stage vectors.
@@ -190,8 +169,6 @@ void gm_cycle_begin(const GmresBufs& g, const double* r, cudaStream_t st);
 void gm_blockdot(const GmresBufs& g, int pass, cudaStream_t st);
 // w -= V h (pass 1) / w -= V c, h += c (pass 2), ||w||, scalar tail.
 void gm_update(const GmresBufs& g, int pass, cudaStream_t st);
-// Pass-1 update fused with the pass-2 block-dot (counter slot 8).
-void gm_update_cgs2(const GmresBufs& g, cudaStream_t st);
 // Delayed CGS2 (the default orthogonalisation): one fused block-dot
 // (s = V_{j-1}^T vt_j, p = V_{j-1}^T w, vt_j.vt_j, vt_j.w; finalises column
 // j-1) and one fused update (v_j, w') per iteration; `finalize` runs the

@@ -59,17 +59,8 @@ double seconds_since(std::chrono::steady_clock::time_point t0) {
 
 }  // namespace
 
-// Device allocation; while `to_pool_` is set (coarse AMG levels) requests are
-// carved from the L2-persisting pool when it has room.
 void* DeviceSolver::raw_alloc(size_t bytes) {
     bytes = std::max<size_t>(bytes, 1);
-    if (to_pool_ && pool_.bytes() > 0) {
-        const size_t at = (pool_used_ + 255) / 256 * 256;
-        if (at + bytes <= pool_.bytes()) {
-            pool_used_ = at + bytes;
-            return pool_.as<char>() + at;
-        }
-    }
     bufs_.emplace_back(bytes);
     return bufs_.back().as<void>();
 }
@@ -155,50 +146,15 @@ void DeviceSolver::upload_values(dev::Mat& m, const std::vector<double>& vals, d
     }
 }
 
-// ELL copy of a short-row operator (the level-0 prolongator) for the fused
-// prolongation + smoothing kernel: [width][rows] indices and values, rows
-// padded with zero values on their last column.  width = 0 if too wide.
-dev::EllP DeviceSolver::upload_ell(const Csr& P, int max_width) {
-    dev::EllP e;
-    int w = 0;
-    for (int i = 0; i < P.rows; ++i) w = std::max(w, P.ptr[i + 1] - P.ptr[i]);
-    if (w < 3) w = 3;
-    if (w > max_width) return e;
-    const size_t n = static_cast<size_t>(P.rows);
-    std::vector<int> idx(w * n, 0);
-    std::vector<double> val(w * n, 0.0);
-    for (int i = 0; i < P.rows; ++i) {
-        const int lo = P.ptr[i], cnt = P.ptr[i + 1] - lo;
-        for (int k = 0; k < w; ++k) {
-            idx[k * n + i] = k < cnt ? P.idx[lo + k] : (cnt > 0 ? P.idx[lo + cnt - 1] : 0);
-            if (k < cnt) val[k * n + i] = P.val[lo + k];
-        }
-    }
-    Dict d = encode(val);
-    e.width = w;
-    e.cols = P.cols;
-    e.idx = upload_array(idx);
-    if (d.vf == dev::kU8) {
-        e.vf = dev::kU8;
-        e.val = upload_array(d.c8);
-        e.tab = upload_array(d.tab);
-        e.ntab = static_cast<int>(d.tab.size());
-    } else {
-        e.vf = dev::kF64;
-        e.val = upload_array(val);
-    }
-    return e;
-}
-
 // DIA when the pattern is <= 16 diagonals with <= 15% padding; else SELL-32.
 // `omega` > 0 requests the omega/diag dictionary (hierarchy operators).
-dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega, bool force_csr) {
+dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
     dev::Mat m;
     m.rows = A.rows;
     m.cols = A.cols;
     m.nnz = A.nnz();
     std::vector<int> offs;
-    bool dia = allow_dia && !force_csr && A.rows == A.cols && A.rows > 0;
+    bool dia = allow_dia && A.rows == A.cols && A.rows > 0;
     if (dia) {
         for (int i = 0; i < A.rows && dia; ++i)
             for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
@@ -227,11 +183,6 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega, bool f
         m.fmt = dev::kDia;
         m.dstride = ds;
         m.nd = nd;
-        if (nd == 7) {
-            const int w = offs[5];
-            const int want[7] = {-w - 1, -w, -1, 0, 1, w, w + 1};
-            if (w >= 2 && std::equal(offs.begin(), offs.end(), want)) m.p1w = w;
-        }
         for (int d = 0; d < nd; ++d) {
             m.off[d] = offs[d];
             if (offs[d] == 0) m.diag0 = d;
@@ -245,7 +196,7 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega, bool f
     // (SELL wins when there are enough rows to fill the GPU with one thread
     // per row; small coarse operators need lanes per row to expose
     // memory-level parallelism.)
-    if (force_csr || (force < 0 && avg > 4.5 && (A.rows < 65536 || avg > 24.0)) || force == dev::kCsrVec) {
+    if ((force < 0 && avg > 4.5 && (A.rows < 65536 || avg > 24.0)) || force == dev::kCsrVec) {
         int g = 2;
         while (g < 32 && 3 * g < avg) g *= 2;
         m.fmt = dev::kCsrVec;
@@ -298,8 +249,6 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
                            std::vector<Hierarchy> hiers, int device)
     : s_(s), device_(device), At_(At), structure_(structure), ht_(ht) {
     compress_values_ = std::getenv("IRK_NO_VALUE_CODES") == nullptr;
-    fuse_ps0_ = std::getenv("IRK_NO_PS0") == nullptr;
-    fused_cgs2_ = std::getenv("IRK_FUSED_CGS2") != nullptr;  // opt-in: A/B break-even
     {
         const char* o = std::getenv("IRK_ORTHO");
         ortho_ = (o && std::string(o) == "cgs2") ? 0 : 1;
@@ -342,65 +291,23 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
     hb_.resize(s);
     for (int i = 0; i < s; ++i) hb_[i] = ht * b[i];
 
-    static const int tail_rows =
-        std::getenv("IRK_TAIL_ROWS") ? std::atoi(std::getenv("IRK_TAIL_ROWS")) : 0;
-    tail_cluster_ = std::getenv("IRK_TAIL_CLUSTER") ? 16 : 1;
-    static const int fused_rows =
-        std::getenv("IRK_FUSED_ROWS") ? std::atoi(std::getenv("IRK_FUSED_ROWS")) : 0;
-    // L2-persisting pool for the coarse levels (>= 1): their kernels are
-    // latency-bound and re-read every V-cycle, while the fine level streams
-    // gigabytes per GMRES iteration through L2 and would evict them.
-    {
-        int max_persist = 0, max_window = 0;
-        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
-        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device);
-        const size_t cap = std::min<size_t>(max_persist, max_window);
-        // Opt-in: measured slower on C2 (the carve-out costs the streaming
-        // vectors more than it saves the coarse levels), see profiles/r1/ab1.txt.
-        if (cap > (1u << 20) && std::getenv("IRK_L2_PERSIST") != nullptr) {
-            pool_ = DevBuf(cap);
-            persist_level_ = std::max(1, std::atoi(std::getenv("IRK_L2_PERSIST")));
-        }
-    }
     for (const Hierarchy& h : hier_host_) {
         DevHier dh;
         dh.prm = h.params;
         const int L = h.n_levels();
-        // The cluster tail runs levels >= tail (V(1,1) only; <= 8 levels).
-        if (tail_rows > 0 && h.params.pre_sweeps == 1 && h.params.post_sweeps == 1 &&
-            (tail_cluster_ == 1 || dev::coarse_tail_cluster_size() > 0)) {
-            for (int l = 0; l < L; ++l)
-                if (h.levels[l].A.rows <= tail_rows && L - l <= dev::kMaxTailLevels) {
-                    dh.tail = l;
-                    break;
-                }
-        }
         dh.lv.resize(L);
-        // coarsest first, so the pool holds the most latency-bound levels
-        // Fused down/up kernels for the small levels (V(1,1); not with the tail).
-        if (dh.tail < 0 && fused_rows > 0 && h.params.pre_sweeps == 1 && h.params.post_sweeps == 1)
-            for (int l = 0; l + 1 < L; ++l)
-                if (h.levels[l].A.rows <= fused_rows) {
-                    dh.fused = l;
-                    break;
-                }
         for (int l = L - 1; l >= 0; --l) {
-            to_pool_ = l >= persist_level_;
             const AmgLevel& lev = h.levels[l];
-            const bool in_tail = (dh.tail >= 0 && l >= dh.tail) || (dh.fused >= 0 && l >= dh.fused);
             DevLevel d;
             d.n = lev.A.rows;
-            d.A = upload(lev.A, true, h.params.jacobi_weight, in_tail);
+            d.A = upload(lev.A, true, h.params.jacobi_weight);
             std::vector<double> wd(d.n);
             for (int i = 0; i < d.n; ++i) wd[i] = h.params.jacobi_weight * lev.inv_diag[i];
             d.wd = alloc(d.n);
             IRK_CUDA_CHECK(cudaMemcpy(d.wd, wd.data(), sizeof(double) * d.n, cudaMemcpyHostToDevice));
             if (l + 1 < L) {
-                d.P = upload(lev.P, false, 0.0, in_tail);
-                d.R = upload(lev.R, false, 0.0, in_tail);
-                if (l == 0 && fuse_ps0_ && d.A.fmt == dev::kDia && d.A.nd == 7 && d.A.vf == dev::kU8 &&
-                    h.params.pre_sweeps == 1 && h.params.post_sweeps == 1)
-                    d.pe = upload_ell(lev.P, 6);
+                d.P = upload(lev.P, false, 0.0);
+                d.R = upload(lev.R, false, 0.0);
             }
             d.t = alloc(d.n);
             d.u = alloc(d.n);
@@ -412,92 +319,12 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
             dh.lv[l] = d;
         }
         dh.nc = h.levels.back().A.rows;
-        to_pool_ = true;
         dh.cinv = alloc(static_cast<size_t>(dh.nc) * dh.nc);
-        to_pool_ = false;
         IRK_CUDA_CHECK(cudaMemcpy(dh.cinv, h.coarse_inverse.data(),
                                   sizeof(double) * dh.nc * dh.nc, cudaMemcpyHostToDevice));
-        if (dh.fused >= 0) {
-            auto csr = [](const dev::Mat& m) {
-                dev::TailCsr c;
-                c.ptr = m.ptr;
-                c.idx = m.idx;
-                c.val = m.val;
-                c.tab = m.tab;
-                c.vf = m.vf;
-                return c;
-            };
-            bufs_.emplace_back(sizeof(unsigned));
-            dh.counter = bufs_.back().as<unsigned>();
-            IRK_CUDA_CHECK(cudaMemset(dh.counter, 0, sizeof(unsigned)));
-            dh.fl.resize(L);
-            for (int l = dh.fused; l + 1 < L; ++l) {
-                dev::FusedLevel& f = dh.fl[l];
-                const DevLevel& d = dh.lv[l];
-                f.n = d.n;
-                f.nrc = dh.lv[l + 1].n;
-                f.A = csr(d.A);
-                f.P = csr(d.P);
-                f.R = csr(d.R);
-                f.wd = d.wd;
-                f.rc = dh.lv[l + 1].r;
-                f.zc = dh.lv[l + 1].z;
-                if (l + 2 == L) {
-                    f.cinv = dh.cinv;
-                    f.nc = dh.nc;
-                    f.zcw = dh.lv[l + 1].z;
-                    f.counter = dh.counter;
-                }
-            }
-        }
-        if (dh.tail >= 0) {
-            dev::TailArgs& ta = dh.targs;
-            ta.nlev = L - dh.tail;
-            ta.cinv = dh.cinv;
-            ta.nc = dh.nc;
-            auto csr = [](const dev::Mat& m) {
-                dev::TailCsr c;
-                c.ptr = m.ptr;
-                c.idx = m.idx;
-                c.val = m.val;
-                c.tab = m.tab;
-                c.vf = m.vf;
-                return c;
-            };
-            for (int l = dh.tail; l < L; ++l) {
-                const DevLevel& d = dh.lv[l];
-                dev::TailLevel& tl = ta.lv[l - dh.tail];
-                tl.n = d.n;
-                tl.A = csr(d.A);
-                if (l + 1 < L) {
-                    tl.P = csr(d.P);
-                    tl.R = csr(d.R);
-                }
-                tl.wd = d.wd;
-                tl.r = d.r;
-                tl.z = d.z;
-                tl.t = d.t;
-            }
-        }
         hier_.push_back(std::move(dh));
     }
 
-    to_pool_ = false;
-    if (pool_used_ > 0) {
-        int max_persist = 0;
-        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device);
-        const size_t persist = std::min<size_t>(pool_used_, max_persist);
-        IRK_CUDA_CHECK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
-        cudaStreamAttrValue av = {};
-        av.accessPolicyWindow.base_ptr = pool_.as<void>();
-        av.accessPolicyWindow.num_bytes = pool_used_;
-        av.accessPolicyWindow.hitRatio =
-            std::min(1.0f, static_cast<float>(persist) / static_cast<float>(pool_used_));
-        av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        IRK_CUDA_CHECK(cudaStreamSetAttribute(st_, cudaStreamAttributeAccessPolicyWindow, &av));
-        persist_bytes_ = persist;
-    }
     rhs_ = alloc(n_);
     fw_ = alloc(static_cast<size_t>(s) * n_);
     u_ = alloc(n_);
@@ -541,15 +368,7 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
     // `first` > 0 runs only the part of the cycle below level `first` (timing)
     auto rhs_of = [&](int l) { return l == first ? r0 : dev::plain(H.lv[l].r); };
     auto out_of = [&](int l) { return l == first ? z0 : dev::plain(H.lv[l].z); };
-    const int down_end = H.tail >= 0 ? H.tail : L - 1;  // levels < down_end smooth+restrict
-    const bool fused_coarse = H.fused >= 0 && H.fused <= L - 2;
-    for (int l = first; l < down_end; ++l) {
-        if (H.fused >= 0 && l >= H.fused) {
-            dev::FusedLevel f = H.fl[l];
-            f.r = rhs_of(l);
-            dev::amg_down_fused(f, st_);
-            continue;
-        }
+    for (int l = first; l + 1 < L; ++l) {
         DevLevel& d = H.lv[l];
         dev::SpmvArgs a;
         a.r = rhs_of(l);
@@ -578,28 +397,8 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
         ra.y = dev::plain(H.lv[l + 1].r);
         dev::spmv(d.R, dev::kXPlain, dev::kEPlain, ra, st_);
     }
-    if (H.tail >= 0) {
-        dev::TailArgs ta = H.targs;
-        ta.r0 = rhs_of(H.tail);
-        ta.z0 = out_of(H.tail);
-        dev::coarse_tail(ta, tail_cluster_, st_);
-    } else if (!fused_coarse || first > L - 2) {
-        dev::dense_mv(H.nc, H.cinv, rhs_of(L - 1), out_of(L - 1), st_);
-    }
-    for (int l = down_end - 1; l >= first; --l) {
-        if (H.lv[l].pe.width > 0) {
-            // prolongation + post-smoothing in one kernel (level 0)
-            dev::prolong_smooth_fused(H.lv[l].A, H.lv[l].pe, H.lv[l + 1].z, rhs_of(l), out_of(l),
-                                      H.lv[l].wd, st_);
-            continue;
-        }
-        if (H.fused >= 0 && l >= H.fused) {
-            dev::FusedLevel f = H.fl[l];
-            f.r = rhs_of(l);
-            f.z = out_of(l);
-            dev::amg_up_fused(f, st_);
-            continue;
-        }
+    dev::dense_mv(H.nc, H.cinv, rhs_of(L - 1), out_of(L - 1), st_);
+    for (int l = L - 2; l >= first; --l) {
         DevLevel& d = H.lv[l];
         dev::SpmvArgs pa;
         pa.x = dev::plain(H.lv[l + 1].z);
@@ -712,12 +511,8 @@ void DeviceSolver::record_iteration() {
         return;
     }
     dev::gm_blockdot(gb_, 1, st_);
-    if (fused_cgs2_) {
-        dev::gm_update_cgs2(gb_, st_);
-    } else {
-        dev::gm_update(gb_, 1, st_);
-        dev::gm_blockdot(gb_, 2, st_);
-    }
+    dev::gm_update(gb_, 1, st_);
+    dev::gm_blockdot(gb_, 2, st_);
     dev::gm_update(gb_, 2, st_);
     dev::gm_normalize(gb_, st_);
 }

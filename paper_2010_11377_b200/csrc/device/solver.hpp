@@ -11,8 +11,6 @@
 #include <vector>
 
 #include "../host/setup.hpp"
-#include "amg_fused.cuh"
-#include "coarse_tail.cuh"
 #include "kernels.cuh"
 
 namespace irkb {
@@ -58,7 +56,6 @@ struct DevLevel {
     double* t = nullptr;          // residual / prolongated iterate
     double* u = nullptr;          // post-sweep ping-pong
     double* zp = nullptr;         // pre-smoothed iterate (pre > 1 only)
-    dev::EllP pe;                 // ELL copy of P for the fused prolong+smooth (level 0)
 };
 
 struct DevHier {
@@ -66,11 +63,6 @@ struct DevHier {
     double* cinv = nullptr;
     int nc = 0;
     AmgParams prm;
-    int tail = -1;          // first level handled by the cluster tail kernel
-    dev::TailArgs targs{};  // prebuilt tail arguments (r0/z0 set per call)
-    int fused = -1;         // first level run by the fused down/up kernels
-    std::vector<dev::FusedLevel> fl;  // per level (r/z set per call)
-    unsigned* counter = nullptr;
 };
 
 class DeviceSolver {
@@ -91,7 +83,6 @@ public:
     double setup_seconds() const { return setup_seconds_; }
     bool fused_stage_op() const { return fused_op_; }
     int matrix_format(int which) const;  // 0 M, 1 K -> 0 CSR, 1 DIA
-    size_t persisting_bytes() const { return persist_bytes_; }
 
     // Device-pointer entry points (enqueue + synchronise).
     void stage_apply(const double* v, double* y);
@@ -116,8 +107,7 @@ public:
     int graph_mode() const { return graph_mode_; }
 
 private:
-    dev::Mat upload(const Csr& A, bool allow_dia, double omega, bool force_csr = false);
-    dev::EllP upload_ell(const Csr& P, int max_width);
+    dev::Mat upload(const Csr& A, bool allow_dia, double omega);
     void upload_values(dev::Mat& m, const std::vector<double>& vals, double omega);
     template <class T> const T* upload_array(const std::vector<T>& h);
     double* alloc(size_t count);
@@ -135,11 +125,7 @@ private:
     int device_ = 0;
     cudaStream_t st_ = nullptr;
     std::vector<DevBuf> bufs_;
-    DevBuf pool_;                 // L2-persisting pool (coarse levels)
-    size_t pool_used_ = 0, persist_bytes_ = 0;
-    bool to_pool_ = false;
-    int tail_cluster_ = 1;
-    int persist_level_ = 1;
+
     dev::Mat M_, K_;
     bool fused_op_ = false;
     dev::StageCoef coef_{};
@@ -173,8 +159,6 @@ private:
     int launches_per_iter_ = 0;
     std::array<int, 4> launch_counts_{};
     bool compress_values_ = true;
-    bool fuse_ps0_ = true;
-    bool fused_cgs2_ = true;
     int ortho_ = 1;  // 1 DCGS2 (default), 0 CGS + conditional second pass
 };
 
