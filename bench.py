@@ -325,17 +325,18 @@ def our_arm(args):
         levels.append(lv)
     pk = peaks()
     hbm_peak = pk.get("hbm_gbs", 6650.0)
-    # Dominant kernel (launch list, profiles/r1): the GMRES classical
-    # Gram-Schmidt block-dot.  Algorithmic bytes of one launch at the average
-    # inner index j = 15: (j + 2) basis/work vectors of sN doubles read once.
+    # Dominant kernel (launch list, profiles/r1): the delayed-CGS2 fused
+    # block-dot k_dgs_dot.  Algorithmic bytes of one launch at the average
+    # inner index j = 15: v_0..v_{j-1}, v_j (unnormalised) and w = (j + 2)
+    # vectors of sN doubles, each read once.
     jd = 15
     kms = C.c_double()
-    _abi.check(L.irkdev_time_kernel(dev._h, 100 + jd, 50, C.byref(kms)))
+    _abi.check(L.irkdev_time_kernel(dev._h, 600 + jd, 50, C.byref(kms)))
     k_bytes = (jd + 2) * 8 * S * n
     k_gbs = k_bytes / (kms.value * 1e-3) / 1e9
     traffic = None
     try:  # dram__bytes_read.sum + dram__bytes_write.sum of the same launch (ncu --set full)
-        traffic = json.loads((ROOT / "profiles" / "r1" / "traffic.json").read_text())["k_gm_blockdot_j15"]
+        traffic = json.loads((ROOT / "profiles" / "r1" / "traffic.json").read_text())["k_dgs_dot_j15"]
     except Exception:
         pass
     # fine-level smoother (DIA, u8 value codes): bytes it must move in its own
@@ -364,7 +365,7 @@ def our_arm(args):
                 "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 4 * 8 + 8 * 501,
                 "wall_seconds": wall_e2e},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "k_gm_blockdot (CGS block-dot, j=15: 17 x sN doubles)",
+        "roofline": {"bound": "hbm", "kernel": "k_dgs_dot (DCGS2 fused block-dot, j=15: 17 x sN doubles)",
                      "achieved": k_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": k_gbs / hbm_peak,
                      "traffic": traffic, "bytes_per_launch": k_bytes, "ms_per_launch": kms.value,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in pk

@@ -134,6 +134,41 @@ int irkdev_step_device(irkdev* d, const double* d_u_n, const double* d_f_lift,
                        const irk_gmres_cfg* cfg, double* d_u_next, double* d_k_out,
                        irk_report* rep);
 
+/* Forcing (irk.hpp:19, std::function<Vec(double)>): write the forcing at time
+ * t into out[0..n); return 0 on success (nonzero -> IRK_EINVAL). */
+typedef int (*irk_forcing_fn)(double t, double* out, int n, void* user);
+
+/* irk_step at time t_n with forcing (stage_rhs, irk.cpp:9-33): block i of the
+ * right-hand side gets forcing(t_n + c_i ht), evaluated on the host.  c: the
+ * tableau's s stage nodes.  forcing may be NULL (then c may be NULL). */
+int irkdev_step_forced(irkdev* d, const double* u_n, const double* f_lift, double t_n,
+                       const double* c, irk_forcing_fn forcing, void* forcing_user,
+                       const irk_gmres_cfg* cfg, double* u_next, double* k_out, irk_report* rep,
+                       double* history);
+
+/* PrecondFactory (irk.hpp:51-52): a solver for step size ht.  Handles it
+ * returns stay owned by the caller (destroy them after integrate returns). */
+typedef irkdev* (*irkdev_factory_fn)(double ht, void* user);
+
+/* Number of steps integrate takes for (t_final, ht): the reference loop
+ * (irk.cpp:85-99) including a truncated last step. */
+int irk_integrate_steps(double t_final, double ht, int* steps);
+
+/* integrate (irk.hpp:55-59, irk.cpp:70-102), device-resident: u stays in HBM
+ * across steps, the host evaluates only the forcing (overlapped with the
+ * previous step) and reads the reports once.  d is the solver for ht (the
+ * reference's first make_precond(ht)); make is consulted when the step size
+ * changes (the truncated last step) and may be NULL when no step changes
+ * size.  u0, f_lift, u_final: host pointers (f_lift may be NULL).  reports:
+ * cap entries, histories: NULL or cap * (max_iter + 1) doubles (per-step
+ * residual histories).  Outputs: *steps, *t_out (the accumulated time) and
+ * *all_converged. */
+int irkdev_integrate(irkdev* d, irkdev_factory_fn make, void* make_user, const double* u0,
+                     const double* f_lift, const double* c, irk_forcing_fn forcing,
+                     void* forcing_user, double t_final, double ht, const irk_gmres_cfg* cfg,
+                     double* u_final, irk_report* reports, int cap, double* histories,
+                     int* steps, double* t_out, int* all_converged);
+
 /* Kernel-level entry points, host pointers (parity tests):
  * StageOperator::apply (stage.cpp:28-44), BlockPreconditioner::apply
  * (stage.cpp:138-182), amg_vcycle for hierarchy k (amg.cpp:229-237). */

@@ -14,11 +14,12 @@
  *   or_stage_apply    stage.cpp:28-44       s F-products, s M-products, s^2 axpys
  *   or_vcycle         amg.cpp:115-168, 229-237  V(pre,post) damped Jacobi
  *   or_precond_apply  stage.cpp:138-182     diagonal / forward / backward sweeps
- *   or_irk_step       irk.cpp:9-68, gmres.cpp:14-142 with the documented
- *                     deviations of the B200 path: GMRES(m) restarts, classical
- *                     Gram-Schmidt with the reference's 0.7071 second-pass
- *                     rule (gmres.cpp:84), a flexible basis (x = Z y, which
- *                     equals P^-1 V y by linearity), dense coarse inverse.
+ *   or_irk_step(_f)   irk.cpp:9-68, gmres.cpp:14-142 with the documented
+ *                     deviations of the B200 path: GMRES(m) restarts,
+ *                     delayed CGS2 (default) or classical Gram-Schmidt with
+ *                     the reference's 0.7071 second-pass rule (gmres.cpp:84),
+ *                     a flexible basis (x = Z y, which equals P^-1 V y by
+ *                     linearity), dense coarse inverse.
  *
  * Floating-point order mirrors the device kernels exactly (compiled with
  * -ffp-contract=off; device with --fmad=false), including the fixed
@@ -385,6 +386,12 @@ static void dcgs2_cycle(const or_sys* S, long N, int R, int budget, double* V, d
 
 int or_irk_step(const or_sys* S, const double* u, const double* lift, double rtol, int restart,
                 int max_iter, double* u_next, double* K, or_report* rep, double* hist) {
+    return or_irk_step_f(S, u, lift, NULL, rtol, restart, max_iter, u_next, K, rep, hist);
+}
+
+int or_irk_step_f(const or_sys* S, const double* u, const double* lift, const double* forcing,
+                  double rtol, int restart, int max_iter, double* u_next, double* K,
+                  or_report* rep, double* hist) {
     struct timespec ts0, ts1;
     clock_gettime(CLOCK_MONOTONIC, &ts0);
     const int n = S->n, s = S->s;
@@ -405,14 +412,18 @@ int or_irk_step(const or_sys* S, const double* u, const double* lift, double rto
     double* cc = (double*)calloc(R + 2, sizeof(double));
     double* y = (double*)calloc(R + 1, sizeof(double));
 
-    /* stage right-hand side (irk.cpp:9-33, no forcing) */
+    /* stage right-hand side (irk.cpp:9-33): blk = -(F u + lift), then
+     * blk += 1.0 * forcing(t_n + c_q ht) (forcing: s*n stage-major, or NULL) */
     {
         double* ku = (double*)malloc(sizeof(double) * n);
         or_spmv(&S->K, u, ku);
         for (int i = 0; i < n; ++i) {
             double f = ku[i];
             if (lift) f = f + lift[i];
-            for (int q = 0; q < s; ++q) b[(long)q * n + i] = -f;
+            for (int q = 0; q < s; ++q) {
+                const long k = (long)q * n + i;
+                b[k] = forcing ? -f + forcing[k] : -f;
+            }
         }
         free(ku);
     }

@@ -56,12 +56,17 @@ typedef struct {
  * second pass (the device's former scheme, IRK_ORTHO=cgs2). */
 void or_set_ortho(int scheme);
 
-/* One IRK step: rhs, GMRES(restart) (right preconditioning, CGS with the
- * reference's conditional second pass, flexible basis), u_next.  hist gets
+/* One IRK step: rhs, GMRES(restart) (right preconditioning, the scheme of
+ * or_set_ortho, flexible basis), u_next.  hist gets
  * max_iter+1 entries (may be NULL). */
 int or_irk_step(const or_sys* S, const double* u, const double* lift, double rtol,
                 int restart, int max_iter, double* u_next, double* K, or_report* rep,
                 double* hist);
+/* Same with a forcing term: forcing = s*n stage-major values of
+ * forcing(t_n + c_q ht) (irk.cpp:24-30), or NULL. */
+int or_irk_step_f(const or_sys* S, const double* u, const double* lift, const double* forcing,
+                  double rtol, int restart, int max_iter, double* u_next, double* K,
+                  or_report* rep, double* hist);
 
 #ifdef __cplusplus
 }

@@ -13,10 +13,13 @@
 //     (gmres.cpp:14-142) -- the reference itself never restarts
 //     (gmres.hpp:20), SURVEY §8c3 item 2;
 //   * a K-returning IRK step (irk.cpp:35-68 keeps K internal; the wrapper
-//     replicates it the way run_error_study does, study.cpp:628-634).
+//     replicates it the way run_error_study does, study.cpp:628-634), with
+//     an optional time-dependent forcing cos(t) * q;
+//   * the reference's own integrate (irk.cpp:70-102) behind a C entry point.
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -83,6 +86,18 @@ struct RefSolver {
     std::unique_ptr<BlockPreconditioner> P;
     std::unique_ptr<StageOperator> op;
 };
+
+// forcing(t) = cos(t) * q: a deterministic time-dependent forcing the tests
+// evaluate identically on both sides (libm cos, one IEEE multiply).
+std::function<Vec(double)> cos_forcing(const double* q, int n) {
+    Vec qv(q, q + n);
+    return [qv](double t) {
+        Vec f(qv.size());
+        const double c = std::cos(t);
+        for (std::size_t k = 0; k < qv.size(); ++k) f[k] = c * qv[k];
+        return f;
+    };
+}
 
 ButcherTable make_table(int scheme, int s) {
     return scheme == 1 ? make_lobatto_iiic(s) : make_radau_iia(s);
@@ -288,10 +303,11 @@ int ref_precond_apply(void* h, const double* v, double* w) {
 // u_next, K (may be null), total iterations, the number of restart cycles,
 // true relative residual, converged flag, solve seconds (wall, excludes
 // nothing but setup) and the per-iteration residual history (<= hist_cap).
-int ref_irk_step(void* h, const double* u_n, const double* f_lift, double rtol,
-                 int restart, int max_iter, double* u_next, double* K_out,
-                 int* iters, int* cycles, double* true_rel, int* converged,
-                 double* seconds, double* hist, int hist_cap, int* hist_len) {
+int ref_irk_step_forced(void* h, const double* u_n, const double* f_lift, double t_n,
+                        const double* fq, double rtol, int restart, int max_iter,
+                        double* u_next, double* K_out, int* iters, int* cycles,
+                        double* true_rel, int* converged, double* seconds, double* hist,
+                        int hist_cap, int* hist_len) {
     return guard([&] {
         auto* S = static_cast<RefSolver*>(h);
         const int n = S->M->n_rows;
@@ -301,9 +317,10 @@ int ref_irk_step(void* h, const double* u_n, const double* f_lift, double rtol,
         sys.M = S->M;
         sys.F = S->F;
         if (f_lift) sys.f_lift.assign(f_lift, f_lift + n);
+        if (fq) sys.forcing = cos_forcing(fq, n);
 
         const auto t0 = std::chrono::steady_clock::now();
-        const Vec rhs = stage_rhs(sys, S->table, S->ht, 0.0,
+        const Vec rhs = stage_rhs(sys, S->table, S->ht, t_n,
                                   std::span<const double>(u_n, n));
         ApplyFn apply = [S](std::span<const double> v, std::span<double> y) {
             S->op->apply(v, y);
@@ -371,6 +388,50 @@ int ref_irk_step(void* h, const double* u_n, const double* f_lift, double rtol,
         const int len = std::min<int>(hist_cap, static_cast<int>(history.size()));
         for (int k = 0; k < len; ++k) hist[k] = history[k];
         *hist_len = static_cast<int>(history.size());
+    });
+}
+
+int ref_irk_step(void* h, const double* u_n, const double* f_lift, double rtol,
+                 int restart, int max_iter, double* u_next, double* K_out,
+                 int* iters, int* cycles, double* true_rel, int* converged,
+                 double* seconds, double* hist, int hist_cap, int* hist_len) {
+    return ref_irk_step_forced(h, u_n, f_lift, 0.0, nullptr, rtol, restart, max_iter, u_next,
+                               K_out, iters, cycles, true_rel, converged, seconds, hist,
+                               hist_cap, hist_len);
+}
+
+// The reference's own time loop, integrate (irk.cpp:70-102), with full
+// GMRES (the reference's gmres, no restart).  The PrecondFactory hands out
+// the preconditioner of `main` for its ht and of `trunc` (may be null) for
+// any other step size; forcing(t) = cos(t) * fq (fq may be null).
+// iters: per-step iteration counts (cap entries).
+int ref_integrate(void* main, void* trunc, const double* u0, const double* f_lift,
+                  const double* fq, double t_final, double rtol, int max_iter,
+                  double* u_final, int* steps, double* t_out, int* iters, int cap,
+                  int* all_converged) {
+    return guard([&] {
+        auto* S = static_cast<RefSolver*>(main);
+        auto* T = static_cast<RefSolver*>(trunc);
+        const int n = S->M->n_rows;
+        LinearParabolicSystem sys;
+        sys.M = S->M;
+        sys.F = S->F;
+        if (f_lift) sys.f_lift.assign(f_lift, f_lift + n);
+        if (fq) sys.forcing = cos_forcing(fq, n);
+        PrecondFactory make = [S, T](double ht) -> std::shared_ptr<const BlockPreconditioner> {
+            if (ht == S->ht) return {std::shared_ptr<const BlockPreconditioner>(), S->P.get()};
+            if (T && ht == T->ht) return {std::shared_ptr<const BlockPreconditioner>(), T->P.get()};
+            throw std::invalid_argument("ref_integrate: no preconditioner for this step size");
+        };
+        GmresConfig cfg{PrecondSide::Right, rtol, max_iter};
+        const TrajectorySummary tr = integrate(sys, S->table, std::span<const double>(u0, n),
+                                               t_final, S->ht, make, cfg);
+        if (tr.steps > cap) throw std::invalid_argument("ref_integrate: cap too small");
+        std::memcpy(u_final, tr.u_final.data(), sizeof(double) * n);
+        *steps = tr.steps;
+        *t_out = tr.t_final;
+        for (int k = 0; k < tr.steps; ++k) iters[k] = tr.reports[k].iterations;
+        *all_converged = tr.all_converged ? 1 : 0;
     });
 }
 

@@ -218,10 +218,15 @@ def amg_setup(A: CsrMatrix, params: AmgParams | None = None) -> AmgHierarchy:
 
 @dataclass
 class LinearParabolicSystem:
-    """M du/dt = -F u - f_lift over the free dofs (irk.hpp:15-22); no forcing."""
+    """M du/dt = -F u - f_lift + forcing(t) over the free dofs (irk.hpp:15-22).
+
+    ``forcing`` (may be None) maps t to an n-vector, like the reference's
+    ``std::function<Vec(double)>``; it is evaluated on the host at the stage
+    times t_n + c_i h_t and uploaded."""
     M: CsrMatrix
     F: CsrMatrix
     f_lift: np.ndarray | None = None
+    forcing: object = None
 
     def n(self) -> int:
         return self.M.n_rows
@@ -410,30 +415,69 @@ class StageOperator:
         return self._dev._apply(_abi.lib().irkdev_stage_apply, v)
 
 
-def irk_step(sys: LinearParabolicSystem, table: ButcherTable, ht: float, t_n: float,
-             u_n: np.ndarray, P: BlockPreconditioner, cfg: GmresConfig | None = None,
-             want_K: bool = False) -> IrkStepResult:
-    """One IRK step (irk.cpp:35-68): stage rhs, GMRES(m) with P, u_{n+1}."""
-    if ht <= 0.0:
-        raise ValueError("irk_step: ht must be positive")
+class _Forcing:
+    """irk_forcing_fn around a Python callable; re-raises its exception."""
+
+    def __init__(self, fn):
+        self.fn, self.error = fn, None
+        self.c = _abi.FORCING_FN(self._call) if fn is not None else _abi.FORCING_FN()
+
+    def _call(self, t, out, n, user):
+        try:
+            f = np.ascontiguousarray(self.fn(t), dtype=np.float64)
+            if f.shape != (n,):
+                raise ValueError("stage_rhs: forcing size mismatch")
+            C.memmove(out, f.ctypes.data, 8 * n)
+            return 0
+        except Exception as e:  # surfaced after the C call returns
+            self.error = self.error or e
+            return 1
+
+    def reraise(self):
+        if self.error is not None:
+            raise self.error
+
+
+def _check_precond(P, ht: float, table: ButcherTable, n: int) -> None:
     if P is None:
         raise Unsupported("the device path needs a BlockPreconditioner")
     if P.ht != ht:
         raise ValueError("irk_step: preconditioner built for a different ht")
     P.bind_table(table)
+    if P._dev.n != n:
+        raise ValueError("stage_rhs: dimension mismatch")
+
+
+def irk_step(sys: LinearParabolicSystem, table: ButcherTable, ht: float, t_n: float,
+             u_n: np.ndarray, P: BlockPreconditioner, cfg: GmresConfig | None = None,
+             want_K: bool = False) -> IrkStepResult:
+    """One IRK step (irk.cpp:35-68): stage rhs (with forcing at t_n + c_i h_t),
+    GMRES(m) with P, u_{n+1}."""
+    if ht <= 0.0:
+        raise ValueError("irk_step: ht must be positive")
+    u = np.ascontiguousarray(u_n, dtype=np.float64)
+    _check_precond(P, ht, table, u.shape[0])
     cfg = cfg or GmresConfig()
     dev = P._dev
-    u = np.ascontiguousarray(u_n, dtype=np.float64)
-    if u.shape[0] != dev.n:
-        raise ValueError("stage_rhs: dimension mismatch")
     un = np.empty_like(u)
     K = np.empty(dev.n * dev.s) if want_K else None
     hist = np.empty(cfg.max_iter + 1)
     rep = _abi.irk_report()
     lift = None if sys.f_lift is None else np.ascontiguousarray(sys.f_lift, dtype=np.float64)
-    check(_abi.lib().irkdev_step(dev._h, _abi.as_d(u), None if lift is None else _abi.as_d(lift),
-                                 C.byref(cfg.c()), _abi.as_d(un),
-                                 None if K is None else _abi.as_d(K), C.byref(rep), _abi.as_d(hist)))
+    L = _abi.lib()
+    if sys.forcing is None:
+        check(L.irkdev_step(dev._h, _abi.as_d(u), None if lift is None else _abi.as_d(lift),
+                            C.byref(cfg.c()), _abi.as_d(un), None if K is None else _abi.as_d(K),
+                            C.byref(rep), _abi.as_d(hist)))
+    else:
+        fc = _Forcing(sys.forcing)
+        c = np.ascontiguousarray(table.c, dtype=np.float64)
+        rc = L.irkdev_step_forced(dev._h, _abi.as_d(u), None if lift is None else _abi.as_d(lift),
+                                  float(t_n), _abi.as_d(c), fc.c, None, C.byref(cfg.c()),
+                                  _abi.as_d(un), None if K is None else _abi.as_d(K),
+                                  C.byref(rep), _abi.as_d(hist))
+        fc.reraise()
+        check(rc)
     return IrkStepResult(un, _report(rep, hist), K)
 
 
@@ -448,24 +492,52 @@ class TrajectorySummary:
 
 def integrate(sys: LinearParabolicSystem, table: ButcherTable, u0: np.ndarray, t_final: float,
               ht: float, make_precond, cfg: GmresConfig | None = None) -> TrajectorySummary:
-    """Time loop of irk.cpp:70-102 (truncated last step, factory on ht change)."""
+    """Time loop of irk.cpp:70-102 (truncated last step, factory consulted on a
+    step-size change), device-resident: u stays in HBM between steps
+    (irkdev_integrate); only the forcing is evaluated on the host."""
     if ht <= 0.0:
         raise ValueError("integrate: ht must be positive")
     if t_final < 0.0:
         raise ValueError("integrate: t_final must be nonnegative")
-    out = TrajectorySummary(np.array(u0, dtype=np.float64))
-    t, cur = 0.0, ht
-    P = make_precond(cur)
-    while t < t_final - 1e-14 * t_final:
-        step = ht if t + ht <= t_final else t_final - t
-        if step != cur:
-            cur = step
-            P = make_precond(cur)
-        r = irk_step(sys, table, step, t, out.u_final, P, cfg)
-        out.u_final = r.u_next
-        out.all_converged = out.all_converged and r.report.converged
-        out.reports.append(r.report)
-        t += step
-        out.steps += 1
-    out.t_final = t
-    return out
+    cfg = cfg or GmresConfig()
+    u = np.ascontiguousarray(u0, dtype=np.float64)
+    L = _abi.lib()
+    nsteps = C.c_int()
+    check(L.irk_integrate_steps(float(t_final), float(ht), C.byref(nsteps)))
+    if nsteps.value == 0:
+        return TrajectorySummary(u.copy(), 0.0, 0, [], True)
+    P = make_precond(ht)
+    _check_precond(P, ht, table, u.shape[0])
+    keep, errors = [P], []
+
+    def factory(h, user):
+        try:
+            Q = make_precond(h)
+            _check_precond(Q, h, table, u.shape[0])
+            keep.append(Q)
+            return Q._dev._h.value
+        except Exception as e:
+            errors.append(e)
+            return None
+
+    fac = _abi.FACTORY_FN(factory)
+    fc = _Forcing(sys.forcing)
+    c = np.ascontiguousarray(table.c, dtype=np.float64)
+    lift = None if sys.f_lift is None else np.ascontiguousarray(sys.f_lift, dtype=np.float64)
+    cap = nsteps.value
+    reps = (_abi.irk_report * cap)()
+    hl = cfg.max_iter + 1
+    hist = np.empty(cap * hl)
+    uf = np.empty_like(u)
+    steps, t_out, conv = C.c_int(), C.c_double(), C.c_int()
+    rc = L.irkdev_integrate(P._dev._h, fac, None, _abi.as_d(u),
+                            None if lift is None else _abi.as_d(lift), _abi.as_d(c), fc.c, None,
+                            float(t_final), float(ht), C.byref(cfg.c()), _abi.as_d(uf), reps, cap,
+                            _abi.as_d(hist), C.byref(steps), C.byref(t_out), C.byref(conv))
+    if errors:
+        raise errors[0]
+    fc.reraise()
+    check(rc)
+    return TrajectorySummary(uf, t_out.value, steps.value,
+                             [_report(reps[k], hist[k * hl:(k + 1) * hl]) for k in range(steps.value)],
+                             bool(conv.value))

@@ -46,6 +46,9 @@ class irk_report(C.Structure):
 
 
 V = C.c_void_p
+# irk_forcing_fn / irkdev_factory_fn (irkdev.h)
+FORCING_FN = C.CFUNCTYPE(C.c_int, C.c_double, dptr, C.c_int, C.c_void_p)
+FACTORY_FN = C.CFUNCTYPE(C.c_void_p, C.c_double, C.c_void_p)
 _SIGS = {
     "irk_last_error": (C.c_char_p, []),
     "irk_amg_params_default": (None, [C.POINTER(irk_amg_params)]),
@@ -78,6 +81,13 @@ _SIGS = {
                               C.POINTER(irk_report), dptr]),
     "irkdev_step_device": (C.c_int, [V, C.c_void_p, C.c_void_p, C.POINTER(irk_gmres_cfg),
                                      C.c_void_p, C.c_void_p, C.POINTER(irk_report)]),
+    "irkdev_step_forced": (C.c_int, [V, dptr, dptr, C.c_double, dptr, FORCING_FN, V,
+                                     C.POINTER(irk_gmres_cfg), dptr, dptr, C.POINTER(irk_report),
+                                     dptr]),
+    "irk_integrate_steps": (C.c_int, [C.c_double, C.c_double, iptr]),
+    "irkdev_integrate": (C.c_int, [V, FACTORY_FN, V, dptr, dptr, dptr, FORCING_FN, V, C.c_double,
+                                   C.c_double, C.POINTER(irk_gmres_cfg), dptr,
+                                   C.POINTER(irk_report), C.c_int, dptr, iptr, dptr, iptr]),
     "irkdev_stage_apply": (C.c_int, [V, dptr, dptr]),
     "irkdev_precond_apply": (C.c_int, [V, dptr, dptr]),
     "irkdev_vcycle": (C.c_int, [V, C.c_int, dptr, dptr]),

@@ -107,6 +107,20 @@ void fill_report(const irkb::SolveReport& r, double setup, irk_report* rep, doub
     if (history) std::memcpy(history, r.history.data(), sizeof(double) * r.history.size());
 }
 
+// The reference time loop's step sizes (irk.cpp:85-99): ht repeated, the
+// last one truncated to land on t_final.
+std::vector<double> integrate_plan(double t_final, double ht) {
+    std::vector<double> plan;
+    double t = 0.0;
+    while (t < t_final - 1e-14 * t_final) {
+        double step = ht;
+        if (t + step > t_final) step = t_final - t;
+        plan.push_back(step);
+        t += step;
+    }
+    return plan;
+}
+
 irkb::GmresConfig to_cfg(const irk_gmres_cfg* c) {
     irkb::GmresConfig g;
     if (c) {
@@ -316,6 +330,82 @@ int irkdev_step_device(irkdev* d, const double* u_n, const double* f_lift,
     return guard([&] {
         const irkb::SolveReport r = d->s->step(u_n, f_lift, to_cfg(cfg), u_next, k_out);
         fill_report(r, d->s->setup_seconds(), rep, nullptr);
+    });
+}
+
+int irkdev_step_forced(irkdev* d, const double* u_n, const double* f_lift, double t_n,
+                       const double* c, irk_forcing_fn forcing, void* forcing_user,
+                       const irk_gmres_cfg* cfg, double* u_next, double* k_out, irk_report* rep,
+                       double* history) {
+    return guard([&] {
+        std::vector<double> fv;
+        if (forcing) {
+            irkb::check(c != nullptr, "stage_rhs: forcing needs the stage nodes c");
+            const int n = d->s->n(), s = d->s->s();
+            fv.resize(static_cast<size_t>(s) * n);
+            for (int i = 0; i < s; ++i)
+                irkb::check(forcing(t_n + c[i] * d->s->ht(), fv.data() + static_cast<size_t>(i) * n, n,
+                                    forcing_user) == 0,
+                            "stage_rhs: forcing callback failed");
+        }
+        const irkb::SolveReport r = d->s->step_host(u_n, f_lift, to_cfg(cfg), u_next, k_out,
+                                                    forcing ? fv.data() : nullptr);
+        fill_report(r, d->s->setup_seconds(), rep, history);
+    });
+}
+
+int irk_integrate_steps(double t_final, double ht, int* steps) {
+    return guard([&] {
+        irkb::check(ht > 0.0, "integrate: ht must be positive");
+        irkb::check(t_final >= 0.0, "integrate: t_final must be nonnegative");
+        *steps = static_cast<int>(integrate_plan(t_final, ht).size());
+    });
+}
+
+int irkdev_integrate(irkdev* d, irkdev_factory_fn make, void* make_user, const double* u0,
+                     const double* f_lift, const double* c, irk_forcing_fn forcing,
+                     void* forcing_user, double t_final, double ht, const irk_gmres_cfg* cfg,
+                     double* u_final, irk_report* reports, int cap, double* histories,
+                     int* steps, double* t_out, int* all_converged) {
+    return guard([&] {
+        irkb::check(ht > 0.0, "integrate: ht must be positive");
+        irkb::check(t_final >= 0.0, "integrate: t_final must be nonnegative");
+        irkb::check(d->s->ht() == ht, "integrate: the solver was built for a different ht");
+        const std::vector<double> plan = integrate_plan(t_final, ht);
+        irkb::check(static_cast<long long>(plan.size()) <= cap, "integrate: reports capacity too small");
+        const irkb::GmresConfig g = to_cfg(cfg);
+        const size_t hl = static_cast<size_t>(g.max_iter) + 1;
+        irkdev* cur = d;
+        double t = 0.0;
+        bool conv = true;
+        cur->s->load_u(u0);
+        size_t k = 0;
+        while (k < plan.size()) {
+            if (plan[k] != cur->s->ht()) {  // step size changed: make_precond(step), irk.cpp:89-92
+                irkb::check(make != nullptr, "integrate: step size changed and no factory was given");
+                irkdev* nd = make(plan[k], make_user);
+                irkb::check(nd != nullptr && nd->s, "integrate: factory returned no solver");
+                irkb::check(nd->s->ht() == plan[k], "integrate: factory solver has the wrong ht");
+                irkb::check(nd->s->n() == cur->s->n() && nd->s->s() == cur->s->s(),
+                            "integrate: factory solver has the wrong size");
+                nd->s->load_u(cur->s->state());
+                cur = nd;
+            }
+            size_t run = 0;
+            while (k + run < plan.size() && plan[k + run] == cur->s->ht()) ++run;
+            const std::vector<irkb::SolveReport> reps = cur->s->run_segment(
+                static_cast<int>(run), &t, f_lift, forcing, forcing_user, c, g, histories != nullptr);
+            for (size_t q = 0; q < run; ++q) {
+                fill_report(reps[q], cur->s->setup_seconds(), reports + k + q,
+                            histories ? histories + hl * (k + q) : nullptr);
+                conv = conv && reps[q].converged;
+            }
+            k += run;
+        }
+        cur->s->store_u(u_final);
+        if (steps) *steps = static_cast<int>(plan.size());
+        if (t_out) *t_out = t;
+        if (all_converged) *all_converged = conv ? 1 : 0;
     });
 }
 

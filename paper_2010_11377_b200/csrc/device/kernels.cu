@@ -412,16 +412,21 @@ __global__ void k_wd_times_r(int n, const double* __restrict__ wd, VecRef rr,
 }
 
 __global__ void k_stage_rhs(int n, int s, const double* __restrict__ ku,
-                            const double* __restrict__ lift, double* __restrict__ b) {
+                            const double* __restrict__ lift, const double* __restrict__ forcing,
+                            double* __restrict__ b) {
     pdl_trigger();
     pdl_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double f = ku[i];
-    if (lift) f = f + lift[i];
+    if (lift) f = f + lift[i];  // axpy(1, f_lift, fu), irk.cpp:18
 #pragma unroll
     for (int q = 0; q < kMaxStages; ++q)
-        if (q < s) b[static_cast<long long>(q) * n + i] = -f;
+        if (q < s) {
+            const long long k = static_cast<long long>(q) * n + i;
+            // blk = -fu; axpy(1, forcing(t_n + c_q ht), blk), irk.cpp:24-29
+            b[k] = forcing ? -f + forcing[k] : -f;
+        }
 }
 
 struct HB {
@@ -1185,9 +1190,10 @@ void wd_times_r(int n, const double* wd, VecRef r, double* z, cudaStream_t st) {
     launch(k_wd_times_r, blocks_for(n, 256), 256, 0, st, n, wd, r, z);
 }
 
-void stage_rhs_finish(const double* ku, const double* lift, double* b, int n, int s,
+void stage_rhs_finish(const double* ku, const double* lift, const double* forcing, double* b,
+                      int n, int s,
                       cudaStream_t st) {
-    launch(k_stage_rhs, blocks_for(n, 256), 256, 0, st, n, s, ku, lift, b);
+    launch(k_stage_rhs, blocks_for(n, 256), 256, 0, st, n, s, ku, lift, forcing, b);
 }
 
 void irk_update(const double* u, const double* x, const double* hb, int n, int s, double* un,

@@ -106,9 +106,10 @@ void dense_mv(int n, const double* Ainv, VecRef r, VecRef z, cudaStream_t st);
 // z = wd .* r (first Jacobi sweep from a zero iterate, amg.cpp:119-124).
 void wd_times_r(int n, const double* wd, VecRef r, double* z, cudaStream_t st);
 
-// rhs block i = -(K u + lift) for i < s (irk.cpp:9-33 without forcing).
-void stage_rhs_finish(const double* ku, const double* lift, double* b, int n, int s,
-                      cudaStream_t st);
+// b_q = -(K u + lift) + forcing_q for every stage q (irk.cpp:9-33); lift and
+// forcing (s*n, stage-major) may be null.
+void stage_rhs_finish(const double* ku, const double* lift, const double* forcing, double* b,
+                      int n, int s, cudaStream_t st);
 // u_next = u + sum_i hb_i x_i (irk.cpp:59-65).
 void irk_update(const double* u, const double* x, const double* hb, int n, int s,
                 double* u_next, cudaStream_t st);

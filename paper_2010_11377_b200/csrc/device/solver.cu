@@ -617,7 +617,8 @@ int count_launches(cudaStream_t st, F&& fn) {
 
 }  // namespace
 
-void DeviceSolver::build_graph(bool lift, int restart, int max_iter, double rtol, bool use_cond) {
+void DeviceSolver::build_graph(bool lift, bool forcing, int restart, int max_iter, double rtol,
+                               bool use_cond) {
     for (cudaGraphExec_t* e : {&exec_, &exec_iter_, &exec_pre_, &exec_cb_, &exec_ce_, &exec_post_})
         if (*e) {
             cudaGraphExecDestroy(*e);
@@ -629,7 +630,8 @@ void DeviceSolver::build_graph(bool lift, int restart, int max_iter, double rtol
         a.x = dev::plain(u_);
         a.y = dev::plain(ku_);
         dev::spmv(K_, dev::kXPlain, dev::kEPlain, a, st_);
-        dev::stage_rhs_finish(ku_, lift ? lift_ : nullptr, b_, n_, s_, st_);
+        dev::stage_rhs_finish(ku_, lift ? lift_ : nullptr, forcing ? forcing_ : nullptr, b_, n_, s_,
+                              st_);
         IRK_CUDA_CHECK(cudaMemsetAsync(x_, 0, sizeof(double) * sN_, st_));
         dev::gm_init(gb_, b_, r_, rtol, restart, max_iter, ortho_, st_);
     };
@@ -746,41 +748,43 @@ void DeviceSolver::build_graph(bool lift, int restart, int max_iter, double rtol
     }
     graph_mode_ = use_cond ? 1 : 0;
     g_lift_ = lift;
+    g_forcing_ = forcing;
     g_restart_ = restart;
     g_iter_ = max_iter;
     g_rtol_ = rtol;
 }
 
-SolveReport DeviceSolver::read_report(int max_iter) {
+SolveReport DeviceSolver::report_from(const dev::GmresCtl& c, const double* hist, int max_iter) {
     SolveReport rep;
-    const dev::GmresCtl& c = *ctl_host_;
     rep.iterations = c.total;
     rep.cycles = c.cycles;
     rep.n_reorth = c.n_reorth;
     rep.converged = c.converged;
     rep.final_rel = c.final_rel;
     rep.true_rel = c.true_rel;
-    const int len = std::min(c.total, max_iter) + 1;
-    rep.history.assign(hist_host_, hist_host_ + len);
+    if (hist) {
+        const int len = std::min(c.total, max_iter) + 1;
+        rep.history.assign(hist, hist + len);
+    }
     return rep;
 }
 
-SolveReport DeviceSolver::step(const double* u, const double* lift, const GmresConfig& cfg,
-                               double* u_next, double* k_out) {
+int DeviceSolver::prepare(const GmresConfig& cfg, bool lift, bool forcing) {
     check(cfg.rel_tol > 0.0, "gmres: rel_tol must be positive");
     check(cfg.side == 1, "device gmres: only right preconditioning runs on the device");
     const int max_iter = cfg.max_iter;
     int restart = cfg.restart <= 0 || cfg.restart > max_iter ? max_iter : cfg.restart;
     if (restart < 1) restart = 1;
     ensure_gmres(restart, std::max(max_iter, 1));
+    if (forcing && !forcing_) forcing_ = alloc(static_cast<size_t>(s_) * n_);
     static const bool no_cond = std::getenv("IRK_NO_COND_GRAPH") != nullptr;
     const bool want_cond = !no_cond;
     if (g_restart_ != restart || g_iter_ != max_iter || g_rtol_ != cfg.rel_tol ||
-        g_lift_ != (lift != nullptr) || (graph_mode_ == 1) != want_cond) {
+        g_lift_ != lift || g_forcing_ != forcing || (graph_mode_ == 1) != want_cond) {
         bool ok = false;
         if (want_cond) {
             try {
-                build_graph(lift != nullptr, restart, max_iter, cfg.rel_tol, true);
+                build_graph(lift, forcing, restart, max_iter, cfg.rel_tol, true);
                 ok = true;
             } catch (const CudaError&) {
                 cudaGetLastError();
@@ -791,47 +795,146 @@ SolveReport DeviceSolver::step(const double* u, const double* lift, const GmresC
                 }
             }
         }
-        if (!ok) build_graph(lift != nullptr, restart, max_iter, cfg.rel_tol, false);
+        if (!ok) build_graph(lift, forcing, restart, max_iter, cfg.rel_tol, false);
     }
+    return max_iter;
+}
+
+void DeviceSolver::launch_solve() {
+    if (graph_mode_ == 1) {
+        IRK_CUDA_CHECK(cudaGraphLaunch(exec_, st_));
+        return;
+    }
+    IRK_CUDA_CHECK(cudaGraphLaunch(exec_pre_, st_));
+    IRK_CUDA_CHECK(cudaMemcpyAsync(ctl_host_, gb_.ctl, sizeof(dev::GmresCtl), cudaMemcpyDeviceToHost, st_));
+    IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
+    while (!ctl_host_->done) {
+        IRK_CUDA_CHECK(cudaGraphLaunch(exec_cb_, st_));
+        while (true) {
+            IRK_CUDA_CHECK(cudaGraphLaunch(exec_iter_, st_));
+            IRK_CUDA_CHECK(cudaMemcpyAsync(&ctl_host_->stop, &gb_.ctl->stop, sizeof(int),
+                                           cudaMemcpyDeviceToHost, st_));
+            IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
+            if (ctl_host_->stop != 0) break;
+        }
+        IRK_CUDA_CHECK(cudaGraphLaunch(exec_ce_, st_));
+        IRK_CUDA_CHECK(cudaMemcpyAsync(ctl_host_, gb_.ctl, sizeof(dev::GmresCtl), cudaMemcpyDeviceToHost, st_));
+        IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
+    }
+    IRK_CUDA_CHECK(cudaGraphLaunch(exec_post_, st_));
+}
+
+SolveReport DeviceSolver::step(const double* u, const double* lift, const GmresConfig& cfg,
+                               double* u_next, double* k_out, const double* forcing) {
+    const int max_iter = prepare(cfg, lift != nullptr, forcing != nullptr);
     const auto t0 = std::chrono::steady_clock::now();
     IRK_CUDA_CHECK(cudaMemcpyAsync(u_, u, sizeof(double) * n_, cudaMemcpyDefault, st_));
     if (lift) IRK_CUDA_CHECK(cudaMemcpyAsync(lift_, lift, sizeof(double) * n_, cudaMemcpyDefault, st_));
-    if (graph_mode_ == 1) {
-        IRK_CUDA_CHECK(cudaGraphLaunch(exec_, st_));
-    } else {
-        IRK_CUDA_CHECK(cudaGraphLaunch(exec_pre_, st_));
-        IRK_CUDA_CHECK(cudaMemcpyAsync(ctl_host_, gb_.ctl, sizeof(dev::GmresCtl), cudaMemcpyDeviceToHost, st_));
-        IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
-        while (!ctl_host_->done) {
-            IRK_CUDA_CHECK(cudaGraphLaunch(exec_cb_, st_));
-            while (true) {
-                IRK_CUDA_CHECK(cudaGraphLaunch(exec_iter_, st_));
-                IRK_CUDA_CHECK(cudaMemcpyAsync(&ctl_host_->stop, &gb_.ctl->stop, sizeof(int),
-                                               cudaMemcpyDeviceToHost, st_));
-                IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
-                if (ctl_host_->stop != 0) break;
-            }
-            IRK_CUDA_CHECK(cudaGraphLaunch(exec_ce_, st_));
-            IRK_CUDA_CHECK(cudaMemcpyAsync(ctl_host_, gb_.ctl, sizeof(dev::GmresCtl), cudaMemcpyDeviceToHost, st_));
-            IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
-        }
-        IRK_CUDA_CHECK(cudaGraphLaunch(exec_post_, st_));
-    }
+    if (forcing)
+        IRK_CUDA_CHECK(cudaMemcpyAsync(forcing_, forcing, sizeof(double) * sN_, cudaMemcpyDefault, st_));
+    launch_solve();
     if (u_next) IRK_CUDA_CHECK(cudaMemcpyAsync(u_next, unext_, sizeof(double) * n_, cudaMemcpyDefault, st_));
     if (k_out) IRK_CUDA_CHECK(cudaMemcpyAsync(k_out, x_, sizeof(double) * sN_, cudaMemcpyDefault, st_));
     IRK_CUDA_CHECK(cudaMemcpyAsync(ctl_host_, gb_.ctl, sizeof(dev::GmresCtl), cudaMemcpyDeviceToHost, st_));
     IRK_CUDA_CHECK(cudaMemcpyAsync(hist_host_, gb_.hist, sizeof(double) * (max_iter + 1),
                                    cudaMemcpyDeviceToHost, st_));
     IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
-    SolveReport rep = read_report(max_iter);
+    SolveReport rep = report_from(*ctl_host_, hist_host_, max_iter);
     rep.solve_seconds = seconds_since(t0);
     return rep;
 }
 
 SolveReport DeviceSolver::step_host(const double* u, const double* lift, const GmresConfig& cfg,
-                                    double* u_next, double* k_out) {
+                                    double* u_next, double* k_out, const double* forcing) {
     // cudaMemcpyDefault handles pageable or pinned host pointers.
-    return step(u, lift, cfg, u_next, k_out);
+    return step(u, lift, cfg, u_next, k_out, forcing);
+}
+
+// ------------------------------------------------------- device-resident loop
+namespace {
+
+// Pinned host block, freed on scope exit.
+struct Pinned {
+    void* p = nullptr;
+    explicit Pinned(size_t bytes) { IRK_CUDA_CHECK(cudaMallocHost(&p, bytes ? bytes : 1)); }
+    ~Pinned() { cudaFreeHost(p); }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct Events {
+    std::vector<cudaEvent_t> ev;
+    explicit Events(size_t k) : ev(k, nullptr) {
+        for (auto& e : ev) IRK_CUDA_CHECK(cudaEventCreate(&e));
+    }
+    ~Events() {
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+}  // namespace
+
+void DeviceSolver::load_u(const double* u0) {
+    IRK_CUDA_CHECK(cudaMemcpyAsync(u_, u0, sizeof(double) * n_, cudaMemcpyDefault, st_));
+    IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
+}
+
+void DeviceSolver::store_u(double* dst) {
+    IRK_CUDA_CHECK(cudaMemcpyAsync(dst, u_, sizeof(double) * n_, cudaMemcpyDefault, st_));
+    IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
+}
+
+std::vector<SolveReport> DeviceSolver::run_segment(int nsteps, double* t, const double* lift,
+                                                   ForcingFn forcing, void* user, const double* c,
+                                                   const GmresConfig& cfg, bool want_history) {
+    check(nsteps >= 0, "integrate: negative step count");
+    check(!forcing || c, "integrate: forcing needs the stage nodes c");
+    const int max_iter = prepare(cfg, lift != nullptr, forcing != nullptr);
+    if (lift) IRK_CUDA_CHECK(cudaMemcpyAsync(lift_, lift, sizeof(double) * n_, cudaMemcpyDefault, st_));
+    const size_t hl = static_cast<size_t>(max_iter) + 1;
+    Pinned ctl(sizeof(dev::GmresCtl) * nsteps);
+    Pinned hist(want_history ? sizeof(double) * hl * nsteps : 0);
+    Pinned stage(forcing ? sizeof(double) * 2 * sN_ : 0);
+    Events ev(2 * static_cast<size_t>(nsteps) + 2);
+    cudaEvent_t* staged = ev.ev.data() + 2 * nsteps;  // H2D of staging buffer k%2 done
+    bool staged_used[2] = {false, false};
+    for (int k = 0; k < nsteps; ++k) {
+        if (forcing) {
+            double* buf = stage.as<double>() + (k % 2) * sN_;
+            if (staged_used[k % 2]) IRK_CUDA_CHECK(cudaEventSynchronize(staged[k % 2]));
+            for (int i = 0; i < s_; ++i) {
+                // sys.forcing(t_n + c_i ht), irk.cpp:26
+                const int rc = forcing(*t + c[i] * ht_, buf + static_cast<long long>(i) * n_, n_, user);
+                check(rc == 0, "stage_rhs: forcing callback failed");
+            }
+            IRK_CUDA_CHECK(cudaMemcpyAsync(forcing_, buf, sizeof(double) * sN_, cudaMemcpyHostToDevice, st_));
+            IRK_CUDA_CHECK(cudaEventRecord(staged[k % 2], st_));
+            staged_used[k % 2] = true;
+        }
+        IRK_CUDA_CHECK(cudaEventRecord(ev.ev[2 * k], st_));
+        launch_solve();
+        IRK_CUDA_CHECK(cudaEventRecord(ev.ev[2 * k + 1], st_));
+        // u_n <- u_{n+1} stays on the device (irk.cpp:95)
+        IRK_CUDA_CHECK(cudaMemcpyAsync(u_, unext_, sizeof(double) * n_, cudaMemcpyDeviceToDevice, st_));
+        IRK_CUDA_CHECK(cudaMemcpyAsync(ctl.as<dev::GmresCtl>() + k, gb_.ctl, sizeof(dev::GmresCtl),
+                                       cudaMemcpyDeviceToHost, st_));
+        if (want_history)
+            IRK_CUDA_CHECK(cudaMemcpyAsync(hist.as<double>() + hl * k, gb_.hist, sizeof(double) * hl,
+                                           cudaMemcpyDeviceToHost, st_));
+        *t += ht_;  // t += step (irk.cpp:97)
+    }
+    IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
+    std::vector<SolveReport> out;
+    out.reserve(nsteps);
+    for (int k = 0; k < nsteps; ++k) {
+        SolveReport r = report_from(ctl.as<dev::GmresCtl>()[k],
+                                    want_history ? hist.as<double>() + hl * k : nullptr, max_iter);
+        float ms = 0.f;
+        IRK_CUDA_CHECK(cudaEventElapsedTime(&ms, ev.ev[2 * k], ev.ev[2 * k + 1]));
+        r.solve_seconds = ms * 1e-3;
+        out.push_back(std::move(r));
+    }
+    return out;
 }
 
 void DeviceSolver::stage_apply(const double* v, double* y) {

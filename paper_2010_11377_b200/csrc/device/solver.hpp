@@ -89,11 +89,29 @@ public:
     void precond_apply(const double* v, double* w);
     void vcycle(int k, const double* r, double* z);
     double dot(const double* x, const double* y, long long n);
+    // forcing (may be null): s*n stage-major values forcing(t_n + c_i ht)
+    // (irk.cpp:24-30), host or device pointer.
     SolveReport step(const double* u, const double* lift, const GmresConfig& cfg, double* u_next,
-                     double* k_out);
+                     double* k_out, const double* forcing = nullptr);
     // Host-pointer step: H2D of u (and lift), D2H of u_next (and K).
     SolveReport step_host(const double* u, const double* lift, const GmresConfig& cfg,
-                          double* u_next, double* k_out);
+                          double* u_next, double* k_out, const double* forcing = nullptr);
+
+    // Device-resident trajectory segment (irk.cpp:85-99 for a run of steps of
+    // this solver's ht): u stays in HBM between steps; the host only
+    // evaluates the forcing (double-buffered pinned staging, overlapped with
+    // the previous step) and collects the reports once at the end.
+    // load_u copies u0 (host or device) into the solver's state vector.
+    using ForcingFn = int (*)(double t, double* out, int n, void* user);
+    void load_u(const double* u0);
+    const double* state() const { return u_; }
+    // Runs nsteps steps from time *t (advanced in place as t += ht, the
+    // reference's accumulation); c: the tableau's stage nodes (s values).
+    std::vector<SolveReport> run_segment(int nsteps, double* t, const double* lift,
+                                         ForcingFn forcing, void* user, const double* c,
+                                         const GmresConfig& cfg, bool want_history);
+    void store_u(double* dst);  // u -> dst (host or device), synchronises
+    double ht() const { return ht_; }
 
     // Timing hooks for the roofline (bench.py): launches `reps` applications
     // of the named hot kernel between CUDA events on the solver's stream and
@@ -117,8 +135,11 @@ private:
     void record_stage_op(dev::VecRef z, dev::VecRef y);
     void record_iteration();
     void ensure_gmres(int restart, int max_iter);
-    void build_graph(bool lift, int restart, int max_iter, double rtol, bool use_cond);
-    SolveReport read_report(int max_iter);
+    void build_graph(bool lift, bool forcing, int restart, int max_iter, double rtol,
+                     bool use_cond);
+    int prepare(const GmresConfig& cfg, bool lift, bool forcing);  // -> max_iter
+    void launch_solve();  // enqueue one step (graph mode) / run it (host-driven)
+    static SolveReport report_from(const dev::GmresCtl& c, const double* hist, int max_iter);
 
     int n_ = 0, s_ = 0;
     long long sN_ = 0, stride_ = 0;
@@ -139,6 +160,7 @@ private:
     // work vectors
     double *rhs_ = nullptr, *fw_ = nullptr;  // fw_: s * n
     double *u_ = nullptr, *lift_ = nullptr, *unext_ = nullptr, *ku_ = nullptr;
+    double* forcing_ = nullptr;  // s * n, allocated on first forced step
     double *b_ = nullptr, *x_ = nullptr, *r_ = nullptr, *ax_ = nullptr;
     double *red_part_ = nullptr, *red_out_ = nullptr;
     unsigned* red_cnt_ = nullptr;
@@ -153,7 +175,7 @@ private:
     cudaGraphExec_t exec_iter_ = nullptr, exec_pre_ = nullptr, exec_cb_ = nullptr,
                     exec_ce_ = nullptr, exec_post_ = nullptr;
     int graph_mode_ = -1;  // 1 conditional nodes, 0 host-driven loop
-    bool g_lift_ = false;
+    bool g_lift_ = false, g_forcing_ = false;
     int g_restart_ = -1, g_iter_ = -1;
     double g_rtol_ = -1.0;
     int launches_per_iter_ = 0;

@@ -57,6 +57,12 @@ class Ref:
             L.ref_irk_step.argtypes = [C.c_void_p, dptr, dptr, C.c_double, C.c_int, C.c_int,
                                        dptr, dptr, iptr, iptr, dptr, iptr, dptr, dptr, C.c_int,
                                        iptr]
+            L.ref_irk_step_forced.argtypes = [C.c_void_p, dptr, dptr, C.c_double, dptr,
+                                              C.c_double, C.c_int, C.c_int, dptr, dptr, iptr,
+                                              iptr, dptr, iptr, dptr, dptr, C.c_int, iptr]
+            L.ref_integrate.argtypes = [C.c_void_p, C.c_void_p, dptr, dptr, dptr, C.c_double,
+                                        C.c_double, C.c_int, dptr, iptr, dptr, iptr, C.c_int,
+                                        iptr]
             for name in ("ref_problem_free", "ref_amg_free", "ref_solver_free"):
                 getattr(L, name).argtypes = [C.c_void_p]
             L.ref_problem_csr.argtypes = [C.c_void_p, C.c_int, iptr, iptr, C.POINTER(iptr),
@@ -215,7 +221,24 @@ class RefSolver:
     def distinct(self):
         return Ref.lib().ref_solver_distinct(self.h)
 
-    def step(self, u, lift=None, rtol=1e-8, restart=50, max_iter=500):
+    def integrate(self, u0, t_final, trunc=None, lift=None, fq=None, rtol=1e-8, max_iter=500,
+                  cap=64):
+        """The reference's integrate (irk.cpp:70-102), full GMRES; `trunc` is
+        the RefSolver for the truncated last step size."""
+        u0 = np.ascontiguousarray(u0, np.float64)
+        uf = np.zeros_like(u0)
+        its = (C.c_int * cap)()
+        steps, cv = C.c_int(), C.c_int()
+        t_out = C.c_double()
+        fq = None if fq is None else np.ascontiguousarray(fq, np.float64)
+        Ref.check(Ref.lib().ref_integrate(self.h, None if trunc is None else trunc.h, _d(u0),
+                                          _d(lift), _d(fq), t_final, rtol, max_iter, _d(uf),
+                                          C.byref(steps), C.byref(t_out), its, cap, C.byref(cv)))
+        return {"u_final": uf, "steps": steps.value, "t_final": t_out.value,
+                "iterations": list(its[: steps.value]), "all_converged": bool(cv.value)}
+
+    def step(self, u, lift=None, rtol=1e-8, restart=50, max_iter=500, t_n=0.0, fq=None):
+        """fq: forcing(t) = cos(t) * fq (ref_harness.cpp cos_forcing), or None."""
         n, s = self.n, self.s
         u = np.ascontiguousarray(u, np.float64)
         un = np.zeros(n)
@@ -223,9 +246,11 @@ class RefSolver:
         hist = np.zeros(max_iter + 2)
         it, cyc, cv, hl = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         tr, sec = C.c_double(), C.c_double()
-        Ref.check(Ref.lib().ref_irk_step(self.h, _d(u), _d(lift), rtol, restart, max_iter, _d(un),
-                                         _d(K), C.byref(it), C.byref(cyc), C.byref(tr), C.byref(cv),
-                                         C.byref(sec), _d(hist), len(hist), C.byref(hl)))
+        fq = None if fq is None else np.ascontiguousarray(fq, np.float64)
+        Ref.check(Ref.lib().ref_irk_step_forced(self.h, _d(u), _d(lift), t_n, _d(fq), rtol, restart,
+                                                max_iter, _d(un), _d(K), C.byref(it), C.byref(cyc),
+                                                C.byref(tr), C.byref(cv), C.byref(sec), _d(hist),
+                                                len(hist), C.byref(hl)))
         return {"u_next": un, "K": K, "iterations": it.value, "cycles": cyc.value,
                 "true_rel": tr.value, "converged": bool(cv.value), "seconds": sec.value,
                 "history": hist[: min(hl.value, len(hist))].copy()}
@@ -275,6 +300,8 @@ class Oracle:
             L.or_precond_apply.argtypes = [C.POINTER(or_sys), dptr, dptr]
             L.or_irk_step.argtypes = [C.POINTER(or_sys), dptr, dptr, C.c_double, C.c_int, C.c_int,
                                       dptr, dptr, C.POINTER(or_report), dptr]
+            L.or_irk_step_f.argtypes = [C.POINTER(or_sys), dptr, dptr, dptr, C.c_double, C.c_int,
+                                        C.c_int, dptr, dptr, C.POINTER(or_report), dptr]
             L.or_set_ortho.argtypes = [C.c_int]
             cls._lib = L
         return cls._lib
@@ -336,7 +363,8 @@ class OracleSystem:
         Oracle.lib().or_vcycle(C.byref(self.sys.h[k]), _d(r), _d(z))
         return z
 
-    def step(self, u, lift=None, rtol=1e-8, restart=50, max_iter=500):
+    def step(self, u, lift=None, rtol=1e-8, restart=50, max_iter=500, forcing=None):
+        """forcing: s*n stage-major forcing values at t_n + c_i ht, or None."""
         n, s = self.n, self.s
         u = np.ascontiguousarray(u, np.float64)
         un = np.zeros(n)
@@ -344,8 +372,9 @@ class OracleSystem:
         hist = np.zeros(max_iter + 1)
         rep = or_report()
         lift_arr = None if lift is None else np.ascontiguousarray(lift, np.float64)
-        Oracle.lib().or_irk_step(C.byref(self.sys), _d(u), _d(lift_arr), rtol, restart, max_iter,
-                                 _d(un), _d(K), C.byref(rep), _d(hist))
+        f_arr = None if forcing is None else np.ascontiguousarray(forcing, np.float64)
+        Oracle.lib().or_irk_step_f(C.byref(self.sys), _d(u), _d(lift_arr), _d(f_arr), rtol, restart,
+                                   max_iter, _d(un), _d(K), C.byref(rep), _d(hist))
         return {"u_next": un, "K": K, "iterations": rep.iterations, "cycles": rep.cycles,
                 "n_reorth": rep.n_reorth, "converged": bool(rep.converged),
                 "true_rel": rep.true_rel, "final_rel": rep.final_rel, "seconds": rep.seconds,
