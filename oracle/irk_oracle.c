@@ -7,7 +7,7 @@
  *      oracle/Makefile from /root/reference/proj/src): stage apply, V-cycle,
  *      preconditioner apply and whole IRK steps, tests/test_oracle_vs_ref.py;
  *   2. against the reference's own known-answer tests restated in
- *      tests/test_oracle_kat.py (test_blocksolve.cpp, test_amg.cpp KATs).
+ *      tests/test_kat.py (test_blocksolve.cpp, test_amg.cpp KATs).
  *
  * Restated algorithms (reference file:line):
  *   or_spmv           csr.cpp:102-114       sequential row sums

@@ -459,6 +459,39 @@ __device__ __forceinline__ void warp_tree_store(double v, double* red, int strid
     if ((threadIdx.x & 31) == 0) red[(threadIdx.x >> 5) * stride + slot] = v;
 }
 
+// K warp trees at once (K a power of two <= 32) with the association of
+// warp_tree_store for every value: each level adds the partials of positions
+// p and p + off.  The first log2(K) levels trade halves of the value set
+// between lanes l and l ^ off, so a level costs K/2 shuffles instead of K
+// (K - 1 + 5 - log2 K shuffles in total instead of 5K).  Afterwards lane
+// d * (32 / K) holds the sum of v[d].  (IEEE addition is commutative, so the
+// upper lane's received + own equals the tree's own + received bit for bit.)
+template <int K>
+__device__ __forceinline__ double warp_tree_multi(double (&v)[K]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = K, off = 16; k > 1; k >>= 1, off >>= 1) {
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int q = 0; q < k / 2; ++q) {
+            const double keep = up ? v[q + k / 2] : v[q];
+            const double send = up ? v[q] : v[q + k / 2];
+            v[q] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    double x = v[0];
+#pragma unroll
+    for (int off = 16 / K; off > 0; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+    return x;
+}
+
+// Stores the K results of warp_tree_multi: value d goes to red[warp * stride + slot(d)].
+template <int K, class Slot>
+__device__ __forceinline__ void warp_multi_store(double x, double* red, int stride, Slot slot) {
+    const int lane = threadIdx.x & 31;
+    if ((lane & (32 / K - 1)) == 0) red[(threadIdx.x >> 5) * stride + slot(lane / (32 / K))] = x;
+}
+
 // After a __syncthreads: the 8 warp values of `slot` added in warp order.
 __device__ __forceinline__ double warp_sum8(const double* red, int stride, int slot) {
     double r = red[slot];
@@ -481,11 +514,19 @@ __device__ __forceinline__ bool elect_last(unsigned* counter) {
 // Thread t sums partials t, t+256, ... sequentially; then the warp tree and
 // the 8 warp results in order.  Called by the whole last CTA.
 __device__ void final_reduce(const double* part, int nch, int nv, double* red, double* out) {
-    for (int q = 0; q < nv; ++q) {
-        double acc = 0.0;
-        for (int p = threadIdx.x; p < nch; p += kRedThreads)
-            acc += __ldcg(part + static_cast<long long>(q) * nch + p);
-        warp_tree_store(acc, red, nv, q);
+    // eight values per multi-value warp tree (same association per value)
+    for (int q0 = 0; q0 < nv; q0 += 8) {
+        double acc[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            acc[r] = 0.0;
+            if (q0 + r < nv)
+                for (int p = threadIdx.x; p < nch; p += kRedThreads)
+                    acc[r] += __ldcg(part + static_cast<long long>(q0 + r) * nch + p);
+        }
+        const double x = warp_tree_multi<8>(acc);
+        const int q = q0 + (threadIdx.x & 31) / 4;
+        if ((threadIdx.x & 3) == 0 && q < nv) red[(threadIdx.x >> 5) * nv + q] = x;
     }
     __syncthreads();
     for (int q = threadIdx.x; q < nv; q += kRedThreads) out[q] = warp_sum8(red, nv, q);
@@ -837,6 +878,40 @@ __device__ void dgs_dot_scalars(const GmresBufs& g, int j, int finalize, int nvv
 // Cycle end (finalize = 1, j = last iteration): target B = slot j+1 (w');
 // values [s_0..s_j, B.B].  Per-pair chunk partials follow the reduction
 // contract (thread t's 16 elements in order, warp tree, warps in order).
+#ifndef IRK_DGS_BATCH
+#define IRK_DGS_BATCH 1
+#endif
+constexpr int kDgsBatch = IRK_DGS_BATCH;  // basis vectors per DCGS2 block-dot batch
+
+// Batch of B basis vectors v_{i0..i0+B-1} against the targets: 2B dots
+// (v.a -> slot i, v.b -> slot nvv + i) or, without A, B dots (v.b -> slot i),
+// reduced by one multi-value warp tree.
+template <int B, bool A>
+__device__ __forceinline__ void dgs_batch(const double* V, long long stride, long long n, int c,
+                                          int i0, const double (&a)[kRedPerThread],
+                                          const double (&b)[kRedPerThread], double* red, int nv,
+                                          int nvv) {
+    double v[B][kRedPerThread];
+#pragma unroll
+    for (int r = 0; r < B; ++r) load_chunk(V + static_cast<long long>(i0 + r) * stride, n, c, v[r]);
+    if constexpr (A) {
+        double d[2 * B];
+#pragma unroll
+        for (int r = 0; r < B; ++r) {
+            d[2 * r] = chunk_dot_local(v[r], a);
+            d[2 * r + 1] = chunk_dot_local(v[r], b);
+        }
+        const double x = warp_tree_multi<2 * B>(d);
+        warp_multi_store<2 * B>(x, red, nv, [&](int q) { return (q & 1) ? nvv + i0 + (q >> 1) : i0 + (q >> 1); });
+    } else {
+        double d[B];
+#pragma unroll
+        for (int r = 0; r < B; ++r) d[r] = chunk_dot_local(v[r], b);
+        const double x = warp_tree_multi<B>(d);
+        warp_multi_store<B>(x, red, nv, [&](int q) { return i0 + q; });
+    }
+}
+
 __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot(GmresBufs g, int finalize) {
     extern __shared__ double red[];
     pdl_trigger();
@@ -850,24 +925,26 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot(GmresBufs g, int fin
     const long long stride = (g.sN + 63) / 64 * 64;
     double b[kRedPerThread];
     load_chunk(g.V + static_cast<long long>(j + 1) * stride, n, c, b);
+    int i = 0;
     if (finalize) {
-        warp_tree_store(chunk_dot_local(b, b), red, nv, nvv);
-        for (int i = 0; i < nvv; ++i) {
-            double v[kRedPerThread];
-            load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v);
-            warp_tree_store(chunk_dot_local(v, b), red, nv, i);
+        {
+            double d[1] = {chunk_dot_local(b, b)};
+            const double x = warp_tree_multi<1>(d);
+            warp_multi_store<1>(x, red, nv, [&](int) { return nvv; });
         }
+        for (; i + 2 <= nvv; i += 2) dgs_batch<2, false>(g.V, stride, n, c, i, b, b, red, nv, nvv);
+        if (i < nvv) dgs_batch<1, false>(g.V, stride, n, c, i, b, b, red, nv, nvv);
     } else {
         double a[kRedPerThread];
         load_chunk(g.V + static_cast<long long>(j) * stride, n, c, a);
-        warp_tree_store(chunk_dot_local(a, a), red, nv, 2 * nvv);
-        warp_tree_store(chunk_dot_local(a, b), red, nv, 2 * nvv + 1);
-        for (int i = 0; i < nvv; ++i) {
-            double v[kRedPerThread];
-            load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v);
-            warp_tree_store(chunk_dot_local(v, a), red, nv, i);
-            warp_tree_store(chunk_dot_local(v, b), red, nv, nvv + i);
+        {
+            double d[2] = {chunk_dot_local(a, a), chunk_dot_local(a, b)};
+            const double x = warp_tree_multi<2>(d);
+            warp_multi_store<2>(x, red, nv, [&](int q) { return 2 * nvv + q; });
         }
+        for (; i + kDgsBatch <= nvv; i += kDgsBatch)
+            dgs_batch<kDgsBatch, true>(g.V, stride, n, c, i, a, b, red, nv, nvv);
+        for (; i < nvv; ++i) dgs_batch<1, true>(g.V, stride, n, c, i, a, b, red, nv, nvv);
     }
     __syncthreads();
     for (int q = threadIdx.x; q < nv; q += kRedThreads)

@@ -1,0 +1,342 @@
+"""The reference's own known-answer tests for the solve path, restated.
+
+SURVEY §8(c4) lists them: stage apply vs the dense Kronecker operator
+(test_blocksolve.cpp:52-66, acceptance.cpp:171-241), exact block
+preconditioners vs the dense Kronecker solve and forward-substitution
+causality (test_blocksolve.cpp:141-199), the GMRES Krylov-dimension bound and
+reported-vs-true residual (test_blocksolve.cpp:251-305), complex Dahlquist
+pairs through a 2x2 rotation block (test_blocksolve.cpp:339-358), the V-cycle
+properties (test_amg.cpp:40-127: single exact level, zero -> zero, Galerkin
+identity, V(1,1) contraction <= 0.5 on Poisson, linearity, bitwise
+repeatability, symmetric Jacobi cycles) and constant trajectories of
+integrate (test_blocksolve.cpp:360-376).
+
+Each KAT runs on the C oracle (CPU, `-m "not gpu"`) and on the device through
+the C ABI (`-m gpu`).  The reference's ExactLU subsolver is analysis-only and
+out of scope; where its KAT needs an exact block solve, blocks of at most
+max_coarse = 64 rows are used, for which the AMG hierarchy is a single exact
+level (amg.cpp:172-227) -- the same substitution the reference's own
+test_amg.cpp:40-50 relies on.
+"""
+import math
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import paper_2010_11377_b200 as P
+from conftest import has_gpu
+from refs import Oracle
+from systems import Case, heat_case
+
+oracle_only = pytest.mark.skipif(not Oracle.available(), reason="oracle not built")
+gpu = pytest.mark.gpu
+needs_gpu = pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+
+
+# ----------------------------------------------------------------- helpers
+def csr(a) -> P.CsrMatrix:
+    a = sp.csr_matrix(a)
+    a.sort_indices()
+    return P.CsrMatrix(a.indptr.astype(np.int32), a.indices.astype(np.int32),
+                       a.data.astype(np.float64), a.shape[1])
+
+
+def dense(m: P.CsrMatrix) -> np.ndarray:
+    return sp.csr_matrix((m.vals, m.col_idx, m.row_ptr), shape=(m.n_rows, m.n_cols)).toarray()
+
+
+def random_pair(n, density, seed):
+    """M, F on one shared random pattern (diagonal included), diagonally
+    dominant so that the block hierarchies exist; explicit zeros kept."""
+    rng = np.random.default_rng(seed)
+    mask = rng.random((n, n)) < density
+    np.fill_diagonal(mask, True)
+    rows, cols = np.nonzero(mask)
+    out = []
+    for _ in range(2):
+        v = rng.uniform(-1.0, 1.0, rows.size)
+        v[rows == cols] = np.abs(v[rows == cols]) + n * density + 1.0
+        out.append(csr(sp.coo_matrix((v, (rows, cols)), shape=(n, n))))
+    return out
+
+
+def kron_stage(M, F, A, ht):
+    s = A.shape[0]
+    return np.kron(np.eye(s), dense(M)) + ht * np.kron(A, dense(F))
+
+
+def scalar(x) -> P.CsrMatrix:
+    return P.CsrMatrix(np.array([0, 1], np.int32), np.array([0], np.int32), np.array([float(x)]), 1)
+
+
+def rotation(z: complex) -> P.CsrMatrix:
+    """Multiplication by z on R^2 (test_blocksolve.cpp rotation_matrix), full
+    2x2 pattern (explicit zeros kept so M and F share it)."""
+    return P.CsrMatrix(np.array([0, 2, 4], np.int32), np.array([0, 1, 0, 1], np.int32),
+                       np.array([z.real, -z.imag, z.imag, z.real]), 2)
+
+
+def stability(table: P.ButcherTable, z: complex) -> complex:
+    s = table.s
+    A = table.A.astype(complex)
+    return 1.0 + z * table.b @ np.linalg.solve(np.eye(s) - z * A, np.ones(s))
+
+
+def rng_vec(n, seed):
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+
+
+SIDES = [pytest.param("oracle", marks=oracle_only),
+         pytest.param("device", marks=[gpu, needs_gpu])]
+
+
+def stage_apply(c: Case, side, v):
+    return c.oracle.stage_apply(v) if side == "oracle" else P.StageOperator(c.device()).apply(v)
+
+
+def precond_apply(c: Case, side, v):
+    return c.oracle.precond_apply(v) if side == "oracle" else c.device().apply(v)
+
+
+def vcycle(c: Case, side, r, k=0):
+    return c.oracle.vcycle(k, r) if side == "oracle" else c.device().vcycle(k, r)
+
+
+def poisson_case(cells):
+    """Single block B = K (the P1 Laplacian on the free dofs): s = 1, Ã = [1],
+    F = 0 on K's pattern, so M + ht*1*F reproduces K bit for bit."""
+    prob = P.make_heat_setup(cells)
+    K = prob.F
+    Z = P.CsrMatrix(K.row_ptr.copy(), K.col_idx.copy(), np.zeros_like(K.vals), K.n_cols)
+    table = P.make_radau_iia(1)
+    return Case(K, Z, table, P.custom_coeff(np.ones((1, 1))), 0.5)
+
+
+# ----------------------------------------------------------- stage operator
+@pytest.mark.parametrize("side", SIDES)
+@pytest.mark.parametrize("s,n", [(3, 20), (2, 40), (3, 150), (5, 60), (7, 71)])
+def test_stage_apply_equals_dense_kronecker(side, s, n):
+    M, F = random_pair(n, 0.3, 111 + n)
+    table = P.make_radau_iia(s)
+    ht = 0.37
+    c = Case(M, F, table, P.precond_coeff(table, P.CoeffKind.LowerFactor), ht)
+    v = rng_vec(s * n, 115)
+    got = stage_apply(c, side, v)
+    want = kron_stage(M, F, table.A, ht) @ v
+    assert np.max(np.abs(got - want)) <= 1e-12 * max(np.max(np.abs(want)), 1.0)
+    assert not np.any(stage_apply(c, side, np.zeros(s * n)))
+
+
+# ------------------------------------------------------------ preconditioner
+KINDS = [P.CoeffKind.Jacobi, P.CoeffKind.GaussSeidelLower, P.CoeffKind.UpperFactor,
+         P.CoeffKind.LowerFactor]
+
+
+@pytest.mark.parametrize("side", SIDES)
+@pytest.mark.parametrize("s", [2, 3, 5])
+def test_exact_block_preconditioner_equals_dense_solve(side, s):
+    """Blocks of 12 rows: single exact AMG level, so P^-1 is the exact block
+    (triangular / diagonal) solve of I (x) M + ht Ã (x) F."""
+    n, ht = 12, 0.4
+    M, F = random_pair(n, 0.3, 200 + s)
+    table = P.make_radau_iia(s)
+    for kind in KINDS:
+        coeff = P.precond_coeff(table, kind)
+        c = Case(M, F, table, coeff, ht)
+        assert all(h.n_levels() == 1 for h in c.hiers)
+        v = rng_vec(s * n, 400 + s)
+        got = precond_apply(c, side, v)
+        want = np.linalg.solve(kron_stage(M, F, coeff.Atilde, ht), v)
+        assert np.max(np.abs(got - want)) <= 1e-9 * max(np.max(np.abs(want)), 1.0), kind
+
+
+@pytest.mark.parametrize("side", SIDES)
+def test_scalar_block_preconditioner(side):
+    lam, ht = 1.7, 0.31
+    for s in (2, 4):
+        table = P.make_radau_iia(s)
+        for kind in KINDS:
+            coeff = P.precond_coeff(table, kind)
+            c = Case(scalar(1.0), scalar(lam), table, coeff, ht)
+            v = rng_vec(s, 33 + s)
+            got = precond_apply(c, side, v)
+            want = np.linalg.solve(np.eye(s) + ht * lam * coeff.Atilde, v)
+            np.testing.assert_allclose(got, want, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("side", SIDES)
+def test_sweep_causality(side):
+    """Forward (LD) sweeps never read later blocks; backward (DU) sweeps never
+    read earlier ones."""
+    n, s = 6, 3
+    M, F = random_pair(n, 0.4, 41)
+    table = P.make_radau_iia(s)
+    for kind, moved, fixed in ((P.CoeffKind.LowerFactor, slice(2 * n, 3 * n), slice(0, n)),
+                               (P.CoeffKind.UpperFactor, slice(0, n), slice(2 * n, 3 * n))):
+        c = Case(M, F, table, P.precond_coeff(table, kind), 0.2)
+        v = rng_vec(s * n, 45)
+        w1 = precond_apply(c, side, v)
+        v2 = v.copy()
+        v2[moved] += 10.0
+        w2 = precond_apply(c, side, v2)
+        assert np.array_equal(w1[fixed], w2[fixed])
+        assert not np.array_equal(w1[moved], w2[moved])
+
+
+# --------------------------------------------------------------------- GMRES
+def run_step(c: Case, side, u, rtol=1e-8, restart=50, max_iter=500):
+    if side == "oracle":
+        o = c.oracle.step(u, c.f_lift, rtol=rtol, restart=restart, max_iter=max_iter)
+        return o["u_next"], o["iterations"], o["converged"], o["final_rel"], o["true_rel"]
+    sys = P.LinearParabolicSystem(c.M, c.K, c.f_lift)
+    r = P.irk_step(sys, c.table, c.ht, 0.0, u, c.device(),
+                   P.GmresConfig(rel_tol=rtol, restart=restart, max_iter=max_iter))
+    rep = r.report
+    return r.u_next, rep.iterations, rep.converged, rep.final_rel_residual, rep.true_rel_residual
+
+
+@pytest.mark.parametrize("side", SIDES)
+def test_krylov_dimension_bound_scalar_stage_problem(side):
+    lam, ht = 2.3, 0.7
+    for s in (1, 2, 4, 7):
+        table = P.make_radau_iia(s)
+        kind = P.CoeffKind.Jacobi if s == 1 else P.CoeffKind.LowerFactor
+        c = Case(scalar(1.0), scalar(lam), table, P.precond_coeff(table, kind), ht)
+        _, its, conv, _, _ = run_step(c, side, np.array([0.9 + 0.1 * s]), rtol=1e-12)
+        assert conv and its <= s
+        if s == 1:
+            assert its == 1  # exact preconditioner
+
+
+@pytest.mark.parametrize("side", SIDES)
+def test_right_preconditioned_residual_is_true(side):
+    c = heat_case(8, s=3, ht=0.2)
+    _, its, conv, final, true = run_step(c, side, c.problem.initial(0.01, 9))
+    assert conv and its > 0
+    assert abs(final - true) <= 1e-6 * true
+    assert true <= 1e-8
+
+
+@pytest.mark.parametrize("side", SIDES)
+def test_complex_dahlquist_rotation_pairs(side):
+    rng = np.random.default_rng(2024)
+    for table in (P.make_radau_iia(3), P.make_lobatto_iiic(4)):
+        for _ in range(5):
+            z = complex(rng.uniform(-4.0, -0.05), rng.uniform(-4.0, 4.0))
+            # z = -ht*lambda with ht = 1: M = I, F = multiplication by -z
+            c = Case(rotation(1.0), rotation(-z), table,
+                     P.precond_coeff(table, P.CoeffKind.LowerFactor), 1.0)
+            un, _, conv, _, _ = run_step(c, side, np.array([1.0, 0.0]), rtol=1e-13)
+            R = stability(table, z)
+            assert conv
+            np.testing.assert_allclose(un, [R.real, R.imag], rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("side", SIDES)
+def test_real_dahlquist(side):
+    lam, ht, u0 = 3.7, 0.29, 1.13
+    for s in (1, 2, 3, 5, 7):
+        table = P.make_radau_iia(s)
+        kind = P.CoeffKind.Jacobi if s == 1 else P.CoeffKind.LowerFactor
+        c = Case(scalar(1.0), scalar(lam), table, P.precond_coeff(table, kind), ht)
+        un, _, conv, _, _ = run_step(c, side, np.array([u0]), rtol=1e-13)
+        assert conv
+        np.testing.assert_allclose(un[0], stability(table, -ht * lam).real * u0, rtol=1e-9)
+
+
+# ------------------------------------------------------------------- V-cycle
+@pytest.mark.parametrize("side", SIDES)
+def test_single_level_is_exact(side):
+    n = 40
+    lap = csr(sp.diags([-np.ones(n - 1), 2.0 * np.ones(n), -np.ones(n - 1)], [-1, 0, 1]))
+    Z = P.CsrMatrix(lap.row_ptr.copy(), lap.col_idx.copy(), np.zeros(lap.nnz), n)
+    c = Case(lap, Z, P.make_radau_iia(1), P.custom_coeff(np.ones((1, 1))), 0.5)
+    assert c.hiers[0].n_levels() == 1
+    b = rng_vec(n, 5)
+    z = vcycle(c, side, b)
+    assert np.linalg.norm(dense(lap) @ z - b) <= 1e-12 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("side", SIDES)
+def test_vcycle_zero_linear_repeatable(side):
+    c = poisson_case(16)
+    n = c.n
+    assert not np.any(vcycle(c, side, np.zeros(n)))
+    r1, r2 = rng_vec(n, 11), rng_vec(n, 13)
+    al, be = 0.83, -2.31
+    lhs = vcycle(c, side, al * r1 + be * r2)
+    rhs = al * vcycle(c, side, r1) + be * vcycle(c, side, r2)
+    assert np.max(np.abs(lhs - rhs)) <= 1e-12 * max(np.linalg.norm(lhs), np.linalg.norm(rhs))
+    assert np.array_equal(vcycle(c, side, r1), vcycle(c, side, r1))
+
+
+@pytest.mark.parametrize("side", SIDES)
+def test_vcycle_contracts_poisson(side):
+    """x_{k+1} = x_k + V(-A x_k): 10 cycles, geometric-mean factor <= 0.5."""
+    c = poisson_case(32)
+    A = dense(c.M)
+    x = rng_vec(c.n, 321)
+    e0 = np.linalg.norm(x)
+    for _ in range(10):
+        x = x + vcycle(c, side, -(A @ x))
+    rho = (np.linalg.norm(x) / e0) ** 0.1
+    assert rho <= 0.5, rho
+
+
+@pytest.mark.parametrize("side", SIDES)
+def test_jacobi_vcycle_is_symmetric_positive(side):
+    c = poisson_case(16)
+    for seed in (21, 22, 23):
+        x, y = rng_vec(c.n, seed), rng_vec(c.n, seed + 100)
+        bx, by = vcycle(c, side, x), vcycle(c, side, y)
+        assert abs(bx @ y - x @ by) <= 1e-10 * np.linalg.norm(x) * np.linalg.norm(y)
+        assert bx @ x > 0.0
+
+
+def test_galerkin_identity_and_shape():
+    """Host setup: A_{l+1} = R_l A_l P_l (values <= 1e-12, symbolic pattern)."""
+    K = P.make_heat_setup(32).F
+    h = P.amg_setup(K)
+    L = h.n_levels()
+    assert 2 <= L <= 5
+    sizes = h.sizes()
+    assert all(sizes[l] < sizes[l - 1] for l in range(1, L))
+    def one(X):  # structural pattern: products of ones never cancel
+        return sp.csr_matrix((np.ones_like(X.data), X.indices, X.indptr), shape=X.shape)
+
+    for l in range(L - 1):
+        A, Pm, R = (sp.csr_matrix((m.vals, m.col_idx, m.row_ptr), shape=(m.n_rows, m.n_cols))
+                    for m in (h.level(l, "A"), h.level(l, "P"), h.level(l, "R")))
+        got = h.level(l + 1, "A")
+        # pattern = the symbolic product R A P (csr_matmul keeps cancellations)
+        pat = (one(R) @ (one(A) @ one(Pm))).tocsr()
+        pat.sort_indices()
+        assert np.array_equal(pat.indptr, got.row_ptr) and np.array_equal(pat.indices, got.col_idx)
+        want = (R @ (A @ Pm)).toarray()
+        assert np.max(np.abs(want - dense(got))) <= 1e-12
+
+
+# ------------------------------------------------------------------ integrate
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_integrate_constant_trajectory_and_step_count():
+    I3 = csr(np.eye(3))
+    Z = P.CsrMatrix(I3.row_ptr.copy(), I3.col_idx.copy(), np.zeros(3), 3)
+    table = P.make_radau_iia(2)
+    coeff = P.precond_coeff(table, P.CoeffKind.LowerFactor)
+    cases = {}
+
+    def make(h):
+        if h not in cases:
+            cases[h] = Case(I3, Z, table, coeff, h)
+        return cases[h].device()
+
+    sys = P.LinearParabolicSystem(I3, Z)
+    u0 = np.array([1.0, -2.0, 3.0])
+    assert P.integrate(sys, table, u0, 0.1, 0.1, make).steps == 1
+    tr = P.integrate(sys, table, u0, 1.0, 0.3, make)
+    assert tr.steps == 4  # 0.3 + 0.3 + 0.3 + 0.1
+    assert math.isclose(tr.t_final, 1.0, rel_tol=1e-12)
+    np.testing.assert_allclose(tr.u_final, u0, rtol=1e-12)
+    assert len(cases) == 2
