@@ -278,10 +278,15 @@ static void givens_column(double* col, int j, double* cs, double* sn, double* g)
  * test after iteration j uses the first-pass column with h_{j+1,j} = ||w'||;
  * the last column is finalised by one more block-dot at the end of the cycle.
  * Mirrors paper_2010_11377_b200/csrc/device/kernels.cu (k_dgs_*) bit for bit. */
+/* side 1 (right): w = A P^-1 vt_j, Z_j = P^-1 vt_j.  side 0 (left,
+ * gmres.cpp:69-71): w = P^-1 (A vt_j), Z_j = vt_j (scratch: N doubles); the
+ * base r is then P^-1 r_k and its norm (alpha at j = 0) fixes the cycle's
+ * tolerance rtol ||P^-1 b|| / ||P^-1 r_k|| (*hnorm = ||P^-1 b|| in cycle 0). */
 static void dcgs2_cycle(const or_sys* S, long N, int R, int budget, double* V, double* Z,
                         double* H, double* g, double* cs, double* sn, double* s_, double* p_,
-                        const double* r, double bnorm, double* beta_io, double tol_c, int cycles,
-                        int* total, int* m_out, int* stop_out, double* final_rel, double* hist) {
+                        const double* r, double* hnorm, double* beta_io, double tol_c, int cycles,
+                        int* total, int* m_out, int* stop_out, double* final_rel, double* hist,
+                        int side, double rtol, double* scratch) {
     double beta = *beta_io;
     memcpy(V, r, sizeof(double) * N); /* vt_0 = r, unnormalised */
     int j = 0, stop = 0;
@@ -289,8 +294,14 @@ static void dcgs2_cycle(const or_sys* S, long N, int R, int budget, double* V, d
     while (1) {
         double* vt = V + (long)j * N;
         double* w = V + (long)(j + 1) * N;
-        or_precond_apply(S, vt, Z + (long)j * N);
-        or_stage_apply(S, Z + (long)j * N, w);
+        if (side == 0) {
+            memcpy(Z + (long)j * N, vt, sizeof(double) * N);
+            or_stage_apply(S, vt, scratch);
+            or_precond_apply(S, scratch, w);
+        } else {
+            or_precond_apply(S, vt, Z + (long)j * N);
+            or_stage_apply(S, Z + (long)j * N, w);
+        }
         for (int i = 0; i < j; ++i) {
             s_[i] = or_dot(V + (long)i * N, vt, N);
             p_[i] = or_dot(V + (long)i * N, w, N);
@@ -305,6 +316,14 @@ static void dcgs2_cycle(const or_sys* S, long N, int R, int budget, double* V, d
         if (j == 0) {
             beta = alpha;
             g[0] = beta;
+            if (side == 0) {
+                if (cycles == 0) {
+                    *hnorm = alpha;
+                    tol_c = rtol;
+                } else {
+                    tol_c = rtol * *hnorm / alpha;
+                }
+            }
         } else {
             double* hc = H + (long)(j - 1) * (R + 1);
             for (int i = 0; i < j; ++i) hc[i] = hc[i] + s_[i];
@@ -312,7 +331,7 @@ static void dcgs2_cycle(const or_sys* S, long N, int R, int budget, double* V, d
             givens_column(hc, j - 1, cs, sn, g);
             *total += 1;
             const double res_rel = fabs(g[j]) / beta;
-            const double hv = cycles == 0 ? res_rel : res_rel * beta / bnorm;
+            const double hv = cycles == 0 ? res_rel : res_rel * beta / *hnorm;
             if (hist) hist[*total] = hv;
             *final_rel = hv;
         }
@@ -372,7 +391,7 @@ static void dcgs2_cycle(const or_sys* S, long N, int R, int budget, double* V, d
         givens_column(hc, j, cs, sn, g);
         *total += 1;
         const double res_rel = fabs(g[j + 1]) / beta;
-        const double hv = cycles == 0 ? res_rel : res_rel * beta / bnorm;
+        const double hv = cycles == 0 ? res_rel : res_rel * beta / *hnorm;
         if (hist) hist[*total] = hv;
         *final_rel = hv;
         if (stop == 1 && !(res_rel <= tol_c)) stop = 3; /* provisional pass, final fail: restart */
@@ -386,12 +405,13 @@ static void dcgs2_cycle(const or_sys* S, long N, int R, int budget, double* V, d
 
 int or_irk_step(const or_sys* S, const double* u, const double* lift, double rtol, int restart,
                 int max_iter, double* u_next, double* K, or_report* rep, double* hist) {
-    return or_irk_step_f(S, u, lift, NULL, rtol, restart, max_iter, u_next, K, rep, hist);
+    return or_irk_step_f(S, u, lift, NULL, 1, rtol, restart, max_iter, u_next, K, rep, hist);
 }
 
 int or_irk_step_f(const or_sys* S, const double* u, const double* lift, const double* forcing,
-                  double rtol, int restart, int max_iter, double* u_next, double* K,
+                  int side, double rtol, int restart, int max_iter, double* u_next, double* K,
                   or_report* rep, double* hist) {
+    if (side == 0 && g_ortho != 1) return -1; /* left runs with delayed CGS2 only */
     struct timespec ts0, ts1;
     clock_gettime(CLOCK_MONOTONIC, &ts0);
     const int n = S->n, s = S->s;
@@ -429,6 +449,8 @@ int or_irk_step_f(const or_sys* S, const double* u, const double* lift, const do
     }
     memcpy(r, b, sizeof(double) * N);
     const double bnorm = sqrt(or_dot(b, b, N));
+    double hnorm = bnorm; /* history / tolerance base (left: ||P^-1 b||, set in cycle 0) */
+    double* base = side == 0 ? (double*)malloc(sizeof(double) * N) : NULL;
     int total = 0, cycles = 0, nre = 0, converged = 0, stop = 0;
     double beta = bnorm, tol_c = rtol, final_rel = 1.0, true_rel = 0.0;
     if (hist) hist[0] = 1.0;
@@ -443,8 +465,10 @@ int or_irk_step_f(const or_sys* S, const double* u, const double* lift, const do
             int j = 0, m = 0;
             stop = 0;
             if (g_ortho == 1) {
-                dcgs2_cycle(S, N, R, budget, V, Z, H, g, cs, sn, h, cc, r, bnorm, &beta, tol_c,
-                            cycles, &total, &m, &stop, &final_rel, hist);
+                if (side == 0) or_precond_apply(S, r, base); /* left: base P^-1 r_k */
+                dcgs2_cycle(S, N, R, budget, V, Z, H, g, cs, sn, h, cc, side == 0 ? base : r,
+                            &hnorm, &beta, tol_c, cycles, &total, &m, &stop, &final_rel, hist,
+                            side, rtol, ax);
                 nre += m;
                 goto cycle_end;
             }
@@ -498,7 +522,7 @@ int or_irk_step_f(const or_sys* S, const double* u, const double* lift, const do
                 total += 1;
                 m = j + 1;
                 const double res_rel = fabs(g[j + 1]) / beta;
-                const double hv = cycles == 0 ? res_rel : res_rel * beta / bnorm;
+                const double hv = cycles == 0 ? res_rel : res_rel * beta / hnorm;
                 if (hist) hist[total] = hv;
                 final_rel = hv;
                 const int bad = !(res_rel == res_rel) || !(hnext == hnext);
@@ -559,7 +583,7 @@ int or_irk_step_f(const or_sys* S, const double* u, const double* lift, const do
         rep->final_rel = final_rel;
         rep->seconds = (ts1.tv_sec - ts0.tv_sec) + 1e-9 * (ts1.tv_nsec - ts0.tv_nsec);
     }
-    free(b); free(x); free(r); free(ax); free(V); free(Z); free(H);
+    free(b); free(x); free(r); free(ax); free(V); free(Z); free(H); free(base);
     free(g); free(cs); free(sn); free(h); free(cc); free(y);
     return 0;
 }

@@ -62,10 +62,11 @@ void or_set_ortho(int scheme);
 int or_irk_step(const or_sys* S, const double* u, const double* lift, double rtol,
                 int restart, int max_iter, double* u_next, double* K, or_report* rep,
                 double* hist);
-/* Same with a forcing term: forcing = s*n stage-major values of
- * forcing(t_n + c_q ht) (irk.cpp:24-30), or NULL. */
+/* Same with a forcing term (forcing = s*n stage-major values of
+ * forcing(t_n + c_q ht), irk.cpp:24-30, or NULL) and the preconditioning
+ * side (1 right, 0 left: delayed CGS2 only, returns -1 otherwise). */
 int or_irk_step_f(const or_sys* S, const double* u, const double* lift, const double* forcing,
-                  double rtol, int restart, int max_iter, double* u_next, double* K,
+                  int side, double rtol, int restart, int max_iter, double* u_next, double* K,
                   or_report* rep, double* hist);
 
 #ifdef __cplusplus

@@ -298,13 +298,15 @@ int ref_precond_apply(void* h, const double* v, double* w) {
     });
 }
 
-// One IRK step with GMRES(restart) built on the reference's full `gmres`.
+// One IRK step with GMRES(restart) built on the reference's full `gmres`
+// (side 1 right, 0 left; the restart tolerance is rescaled in the side's
+// metric: ||r_k|| for right, ||P^-1 r_k|| for left).
 // restart <= 0 calls the reference gmres once (its own semantics).  Returns
 // u_next, K (may be null), total iterations, the number of restart cycles,
 // true relative residual, converged flag, solve seconds (wall, excludes
 // nothing but setup) and the per-iteration residual history (<= hist_cap).
 int ref_irk_step_forced(void* h, const double* u_n, const double* f_lift, double t_n,
-                        const double* fq, double rtol, int restart, int max_iter,
+                        const double* fq, int side, double rtol, int restart, int max_iter,
                         double* u_next, double* K_out, int* iters, int* cycles,
                         double* true_rel, int* converged, double* seconds, double* hist,
                         int hist_cap, int* hist_len) {
@@ -334,8 +336,16 @@ int ref_irk_step_forced(void* h, const double* u_n, const double* f_lift, double
         double trel = 0.0;
         std::vector<double> history{1.0};
         const double bnorm = nrm2(rhs);
+        const PrecondSide ps = side == 0 ? PrecondSide::Left : PrecondSide::Right;
+        // the metric base of the restart rescaling: ||b|| (right), ||P^-1 b|| (left)
+        auto metric = [&](const Vec& v) {
+            if (ps == PrecondSide::Right) return nrm2(v);
+            Vec pv(v.size());
+            papply(v, pv);
+            return nrm2(pv);
+        };
         if (restart <= 0) {
-            GmresConfig cfg{PrecondSide::Right, rtol, max_iter};
+            GmresConfig cfg{ps, rtol, max_iter};
             auto [sol, rep] = gmres(apply, static_cast<int>(N), rhs, &papply, cfg);
             x = std::move(sol);
             total = rep.iterations;
@@ -348,6 +358,7 @@ int ref_irk_step_forced(void* h, const double* u_n, const double* f_lift, double
             // tolerance rescaled so that the cycle stops at ||r|| <= tol ||b||.
             Vec r = rhs;
             double rnorm = bnorm;
+            const double mb = bnorm > 0.0 ? metric(rhs) : 0.0;
             while (true) {
                 if (bnorm == 0.0) {
                     conv = true;
@@ -355,10 +366,11 @@ int ref_irk_step_forced(void* h, const double* u_n, const double* f_lift, double
                 }
                 const int budget = std::min(restart, max_iter - total);
                 if (budget <= 0) break;
-                GmresConfig cfg{PrecondSide::Right, rtol * bnorm / rnorm, budget};
+                const double mr = total == 0 ? mb : metric(r);
+                GmresConfig cfg{ps, rtol * mb / mr, budget};
                 auto [dx, rep] = gmres(apply, static_cast<int>(N), r, &papply, cfg);
                 for (std::size_t k = 1; k < rep.history.size(); ++k)
-                    history.push_back(rep.history[k] * rnorm / bnorm);
+                    history.push_back(rep.history[k] * mr / mb);
                 axpy(1.0, dx, x);
                 total += rep.iterations;
                 ncyc += 1;
@@ -395,7 +407,7 @@ int ref_irk_step(void* h, const double* u_n, const double* f_lift, double rtol,
                  int restart, int max_iter, double* u_next, double* K_out,
                  int* iters, int* cycles, double* true_rel, int* converged,
                  double* seconds, double* hist, int hist_cap, int* hist_len) {
-    return ref_irk_step_forced(h, u_n, f_lift, 0.0, nullptr, rtol, restart, max_iter, u_next,
+    return ref_irk_step_forced(h, u_n, f_lift, 0.0, nullptr, 1, rtol, restart, max_iter, u_next,
                                K_out, iters, cycles, true_rel, converged, seconds, hist,
                                hist_cap, hist_len);
 }

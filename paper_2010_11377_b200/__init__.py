@@ -283,9 +283,10 @@ class GmresConfig:
     restart: int = 50
 
     def c(self) -> _abi.irk_gmres_cfg:
-        if self.side != "right":
-            raise Unsupported("device GMRES runs right preconditioning (the reference default)")
-        return _abi.irk_gmres_cfg(1, self.rel_tol, self.max_iter, self.restart)
+        if self.side not in ("right", "left"):
+            raise ValueError("gmres: side must be 'right' or 'left'")
+        return _abi.irk_gmres_cfg(1 if self.side == "right" else 0, self.rel_tol, self.max_iter,
+                                  self.restart)
 
 
 @dataclass

@@ -648,7 +648,7 @@ __device__ void arnoldi_tail(const GmresBufs& g) {
     c->total += 1;
     c->m = j + 1;
     const double res_rel = fabs(c->g[j + 1]) / c->beta;
-    const double hist = c->cycles == 0 ? res_rel : res_rel * c->beta / c->bnorm;
+    const double hist = c->cycles == 0 ? res_rel : res_rel * c->beta / c->hnorm;
     g.hist[c->total] = hist;
     c->final_rel = hist;
     if (!(res_rel == res_rel) || !(c->hnext == c->hnext)) c->bad = 1;
@@ -783,7 +783,7 @@ __device__ void record_column(const GmresBufs& g, int col_index) {
     GmresCtl* c = g.ctl;
     c->total += 1;
     const double res_rel = fabs(c->g[col_index + 1]) / c->beta;
-    const double hv = c->cycles == 0 ? res_rel : res_rel * c->beta / c->bnorm;
+    const double hv = c->cycles == 0 ? res_rel : res_rel * c->beta / c->hnorm;
     g.hist[c->total] = hv;
     c->final_rel = hv;
 }
@@ -855,6 +855,16 @@ __device__ void dgs_dot_scalars(const GmresBufs& g, int j, int finalize, int nvv
     if (j == 0) {
         ctl->beta = alpha;
         ctl->g[0] = alpha;
+        if (ctl->side == 0) {
+            // left: the cycle's base is P^-1 r; its norm sets the metric
+            // (gmres.cpp:41-46) and the restart tolerance rel_tol ||P^-1 b|| / ||P^-1 r||
+            if (ctl->cycles == 0) {
+                ctl->hnorm = alpha;
+                ctl->tol_c = ctl->rel_tol;
+            } else {
+                ctl->tol_c = ctl->rel_tol * ctl->hnorm / alpha;
+            }
+        }
     } else {
         double* hc = g.H + static_cast<long long>(j - 1) * ld;
         for (int i = 0; i < j; ++i) hc[i] = hc[i] + res[i];
@@ -1037,10 +1047,27 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_normalize(GmresBufs g) {
     }
 }
 
+// y = x on resolved basis slots (left preconditioning keeps the operator
+// inputs vt_j as the solution basis Z).
+__global__ void k_copy_ref(VecRef x, VecRef y, long long n) {
+    pdl_trigger();
+    pdl_wait();
+    const double* xp = x.get();
+    double* yp = y.get();
+    const long long i = 4 * (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x);
+    if (i + 3 < n) {
+        *reinterpret_cast<double2*>(yp + i) = *reinterpret_cast<const double2*>(xp + i);
+        *reinterpret_cast<double2*>(yp + i + 2) = *reinterpret_cast<const double2*>(xp + i + 2);
+    } else {
+        for (long long k = i; k < n; ++k) yp[k] = xp[k];
+    }
+}
+
 template <bool COND>
 __global__ void __launch_bounds__(kRedThreads) k_gm_init(GmresBufs g, const double* __restrict__ b,
                                                          double* __restrict__ r, double rel_tol,
-                                                         int restart, int max_iter, int ortho) {
+                                                         int restart, int max_iter, int ortho,
+                                                         int side) {
     pdl_trigger();
     pdl_wait();
     __shared__ double red[kRedThreads / 32 + 1];
@@ -1059,6 +1086,8 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_init(GmresBufs g, const doub
         c->restart = restart;
         c->max_iter = max_iter;
         c->bnorm = bn;
+        c->hnorm = bn;
+        c->side = side;
         c->beta = bn;
         c->total = 0;
         c->cycles = 0;
@@ -1179,6 +1208,7 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_residual(GmresBufs g, const 
             c->done = 1;
             c->converged = c->stop == 1 ? 1 : 0;
         } else {
+            // right: next cycle's base is r (left: P^-1 r, normed in k_dgs_dot)
             c->beta = rn;
             c->tol_c = c->rel_tol * c->bnorm / rn;
             const int left = c->max_iter - c->total;
@@ -1283,8 +1313,12 @@ void irk_update(const double* u, const double* x, const double* hb, int n, int s
 static size_t red_smem(int nv) { return sizeof(double) * (kRedThreads / 32 * nv + nv + 8); }
 
 void gm_init(const GmresBufs& g, const double* b, double* r, double rel_tol, int restart,
-             int max_iter, int ortho, cudaStream_t st) {
-    launch(g.use_cond ? k_gm_init<true> : k_gm_init<false>, g.nchunks, kRedThreads, 0, st, g, b, r, rel_tol, restart, max_iter, ortho);
+             int max_iter, int ortho, int side, cudaStream_t st) {
+    launch(g.use_cond ? k_gm_init<true> : k_gm_init<false>, g.nchunks, kRedThreads, 0, st, g, b, r, rel_tol, restart, max_iter, ortho, side);
+}
+
+void copy_ref(VecRef x, VecRef y, long long n, cudaStream_t st) {
+    launch(k_copy_ref, static_cast<int>((n + 4 * 256 - 1) / (4 * 256)), 256, 0, st, x, y, n);
 }
 
 void gm_cycle_begin(const GmresBufs& g, const double* r, cudaStream_t st) {

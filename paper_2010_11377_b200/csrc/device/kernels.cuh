@@ -142,6 +142,8 @@ struct GmresCtl {
     double pv[kMaxRestart + 1];  // p_i = v_i . w      (projections of w)
     double hjj, inv_alpha;
     int ortho;                   // 1 DCGS2, 0 CGS + conditional second pass
+    int side;                    // 1 right (flexible Z basis), 0 left (gmres.cpp:41-46, 69-71)
+    double hnorm;                // history / tolerance base: ||b|| (right), ||P^-1 b|| (left)
 };
 
 struct GmresBufs {
@@ -163,7 +165,9 @@ struct GmresBufs {
 // b -> r copy and ||b||; initialises the control block (bnorm == 0 ends the
 // solve: x = 0).
 void gm_init(const GmresBufs& g, const double* b, double* r, double rel_tol,
-             int restart, int max_iter, int ortho, cudaStream_t st);
+             int restart, int max_iter, int ortho, int side, cudaStream_t st);
+// y = x for the basis slot x resolves to (sN values).
+void copy_ref(VecRef x, VecRef y, long long n, cudaStream_t st);
 // V_0 = r / beta, g_0 = beta, j = 0 (start of a restart cycle).
 void gm_cycle_begin(const GmresBufs& g, const double* r, cudaStream_t st);
 // h = V_{0..j}^T w and ||w||  (pass 1), or c = V^T w (pass 2, if reorth).

@@ -348,6 +348,10 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
 DeviceSolver::~DeviceSolver() {
     for (cudaGraphExec_t* e : {&exec_, &exec_iter_, &exec_pre_, &exec_cb_, &exec_ce_, &exec_post_})
         if (*e) cudaGraphExecDestroy(*e);
+    for (cudaStream_t b : branch_)
+        if (b) cudaStreamDestroy(b);
+    for (cudaEvent_t e : branch_ev_)
+        if (e) cudaEventDestroy(e);
     if (ctl_host_) cudaFreeHost(ctl_host_);
     if (hist_host_) cudaFreeHost(hist_host_);
     if (st_) cudaStreamDestroy(st_);
@@ -429,6 +433,33 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
 void DeviceSolver::record_precond(VecRef v, VecRef w) {
     const int s = s_;
     const long long n = n_;
+    const int nh = static_cast<int>(hier_.size());
+    static const bool serial = std::getenv("IRK_SERIAL_JACOBI") != nullptr;
+    if (structure_ == Structure::Diagonal && nh > 1 && !serial) {
+        // Block Jacobi (stage.cpp:151-153): the subsolves are independent, so
+        // each distinct hierarchy gets its own stream branch (a fork/join in
+        // the captured graph); blocks sharing a hierarchy share its level
+        // buffers and run in stage order on that branch.
+        if (branch_.empty()) {
+            branch_.resize(nh);
+            branch_ev_.resize(nh + 1);
+            for (int k = 1; k < nh; ++k)
+                IRK_CUDA_CHECK(cudaStreamCreateWithFlags(&branch_[k], cudaStreamNonBlocking));
+            for (auto& e : branch_ev_) IRK_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        cudaStream_t main = st_;
+        IRK_CUDA_CHECK(cudaEventRecord(branch_ev_[0], main));
+        for (int k = 0; k < nh; ++k) {
+            st_ = k == 0 ? main : branch_[k];
+            if (k > 0) IRK_CUDA_CHECK(cudaStreamWaitEvent(st_, branch_ev_[0], 0));
+            for (int j = 0; j < s; ++j)
+                if (sob_[j] == k) record_vcycle(k, block(v, j * n), block(w, j * n));
+            if (k > 0) IRK_CUDA_CHECK(cudaEventRecord(branch_ev_[k], st_));
+        }
+        st_ = main;
+        for (int k = 1; k < nh; ++k) IRK_CUDA_CHECK(cudaStreamWaitEvent(main, branch_ev_[k], 0));
+        return;
+    }
     auto e = [&](int j, int k) { return -ht_ * At_[j * s + k]; };
     for (int q = 0; q < s; ++q) {
         const int j = structure_ == Structure::Upper ? s - 1 - q : q;
@@ -503,8 +534,16 @@ void DeviceSolver::record_stage_op(VecRef z, VecRef y) {
 // second pass), Givens, normalisation.
 void DeviceSolver::record_iteration() {
     const int* jp = &gb_.ctl->j;
-    record_precond(slot(gb_.V, jp, stride_, 0), slot(gb_.Z, jp, stride_, 0));
-    record_stage_op(slot(gb_.Z, jp, stride_, 0), slot(gb_.V, jp, stride_, 1));
+    if (side_ == 0) {
+        // left (gmres.cpp:69-71): w = P^-1 (A vt_j); Z_j keeps the operator
+        // input vt_j so that x += Z y in both sides' flexible form
+        dev::copy_ref(slot(gb_.V, jp, stride_, 0), slot(gb_.Z, jp, stride_, 0), sN_, st_);
+        record_stage_op(slot(gb_.V, jp, stride_, 0), dev::plain(ax_));
+        record_precond(dev::plain(ax_), slot(gb_.V, jp, stride_, 1));
+    } else {
+        record_precond(slot(gb_.V, jp, stride_, 0), slot(gb_.Z, jp, stride_, 0));
+        record_stage_op(slot(gb_.Z, jp, stride_, 0), slot(gb_.V, jp, stride_, 1));
+    }
     if (ortho_ == 1) {
         dev::gm_dgs_dot(gb_, 0, st_);
         dev::gm_dgs_update(gb_, st_);
@@ -633,9 +672,16 @@ void DeviceSolver::build_graph(bool lift, bool forcing, int restart, int max_ite
         dev::stage_rhs_finish(ku_, lift ? lift_ : nullptr, forcing ? forcing_ : nullptr, b_, n_, s_,
                               st_);
         IRK_CUDA_CHECK(cudaMemsetAsync(x_, 0, sizeof(double) * sN_, st_));
-        dev::gm_init(gb_, b_, r_, rtol, restart, max_iter, ortho_, st_);
+        dev::gm_init(gb_, b_, r_, rtol, restart, max_iter, ortho_, side_, st_);
     };
-    auto cycle_begin = [&]() { dev::gm_cycle_begin(gb_, r_, st_); };
+    auto cycle_begin = [&]() {
+        if (side_ == 0) {  // left: the cycle's base vector is P^-1 r (gmres.cpp:41-46)
+            record_precond(dev::plain(r_), dev::plain(ax_));
+            dev::gm_cycle_begin(gb_, ax_, st_);
+        } else {
+            dev::gm_cycle_begin(gb_, r_, st_);
+        }
+    };
     auto cycle_end = [&]() {
         if (ortho_ == 1) dev::gm_dgs_dot(gb_, 1, st_);
         dev::gm_solution(gb_, x_, st_);
@@ -749,6 +795,7 @@ void DeviceSolver::build_graph(bool lift, bool forcing, int restart, int max_ite
     graph_mode_ = use_cond ? 1 : 0;
     g_lift_ = lift;
     g_forcing_ = forcing;
+    g_side_ = side_;
     g_restart_ = restart;
     g_iter_ = max_iter;
     g_rtol_ = rtol;
@@ -771,7 +818,10 @@ SolveReport DeviceSolver::report_from(const dev::GmresCtl& c, const double* hist
 
 int DeviceSolver::prepare(const GmresConfig& cfg, bool lift, bool forcing) {
     check(cfg.rel_tol > 0.0, "gmres: rel_tol must be positive");
-    check(cfg.side == 1, "device gmres: only right preconditioning runs on the device");
+    check(cfg.side == 0 || cfg.side == 1, "gmres: side must be 0 (left) or 1 (right)");
+    if (cfg.side == 0 && ortho_ != 1)
+        throw Unsupported("device gmres: left preconditioning runs with the delayed CGS2 scheme only");
+    side_ = cfg.side;
     const int max_iter = cfg.max_iter;
     int restart = cfg.restart <= 0 || cfg.restart > max_iter ? max_iter : cfg.restart;
     if (restart < 1) restart = 1;
@@ -780,7 +830,8 @@ int DeviceSolver::prepare(const GmresConfig& cfg, bool lift, bool forcing) {
     static const bool no_cond = std::getenv("IRK_NO_COND_GRAPH") != nullptr;
     const bool want_cond = !no_cond;
     if (g_restart_ != restart || g_iter_ != max_iter || g_rtol_ != cfg.rel_tol ||
-        g_lift_ != lift || g_forcing_ != forcing || (graph_mode_ == 1) != want_cond) {
+        g_lift_ != lift || g_forcing_ != forcing || g_side_ != side_ ||
+        (graph_mode_ == 1) != want_cond) {
         bool ok = false;
         if (want_cond) {
             try {

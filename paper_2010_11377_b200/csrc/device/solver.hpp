@@ -34,7 +34,7 @@ private:
 };
 
 struct GmresConfig {
-    int side = 1;        // 1 right (the only device mode), 0 left
+    int side = 1;        // 1 right, 0 left (delayed CGS2 only)
     double rel_tol = 1e-8;
     int max_iter = 500;
     int restart = 50;    // 0 = full GMRES (restart = max_iter)
@@ -145,6 +145,8 @@ private:
     long long sN_ = 0, stride_ = 0;
     int device_ = 0;
     cudaStream_t st_ = nullptr;
+    std::vector<cudaStream_t> branch_;   // block-Jacobi V-cycle branches (index 0 unused)
+    std::vector<cudaEvent_t> branch_ev_; // [0] fork, [k] join of branch k
     std::vector<DevBuf> bufs_;
 
     dev::Mat M_, K_;
@@ -182,6 +184,7 @@ private:
     std::array<int, 4> launch_counts_{};
     bool compress_values_ = true;
     int ortho_ = 1;  // 1 DCGS2 (default), 0 CGS + conditional second pass
+    int side_ = 1, g_side_ = -1;  // GMRES preconditioning side (1 right, 0 left)
 };
 
 }  // namespace irkb

@@ -57,7 +57,7 @@ class Ref:
             L.ref_irk_step.argtypes = [C.c_void_p, dptr, dptr, C.c_double, C.c_int, C.c_int,
                                        dptr, dptr, iptr, iptr, dptr, iptr, dptr, dptr, C.c_int,
                                        iptr]
-            L.ref_irk_step_forced.argtypes = [C.c_void_p, dptr, dptr, C.c_double, dptr,
+            L.ref_irk_step_forced.argtypes = [C.c_void_p, dptr, dptr, C.c_double, dptr, C.c_int,
                                               C.c_double, C.c_int, C.c_int, dptr, dptr, iptr,
                                               iptr, dptr, iptr, dptr, dptr, C.c_int, iptr]
             L.ref_integrate.argtypes = [C.c_void_p, C.c_void_p, dptr, dptr, dptr, C.c_double,
@@ -237,7 +237,8 @@ class RefSolver:
         return {"u_final": uf, "steps": steps.value, "t_final": t_out.value,
                 "iterations": list(its[: steps.value]), "all_converged": bool(cv.value)}
 
-    def step(self, u, lift=None, rtol=1e-8, restart=50, max_iter=500, t_n=0.0, fq=None):
+    def step(self, u, lift=None, rtol=1e-8, restart=50, max_iter=500, t_n=0.0, fq=None,
+             side="right"):
         """fq: forcing(t) = cos(t) * fq (ref_harness.cpp cos_forcing), or None."""
         n, s = self.n, self.s
         u = np.ascontiguousarray(u, np.float64)
@@ -247,7 +248,8 @@ class RefSolver:
         it, cyc, cv, hl = C.c_int(), C.c_int(), C.c_int(), C.c_int()
         tr, sec = C.c_double(), C.c_double()
         fq = None if fq is None else np.ascontiguousarray(fq, np.float64)
-        Ref.check(Ref.lib().ref_irk_step_forced(self.h, _d(u), _d(lift), t_n, _d(fq), rtol, restart,
+        Ref.check(Ref.lib().ref_irk_step_forced(self.h, _d(u), _d(lift), t_n, _d(fq),
+                                                0 if side == "left" else 1, rtol, restart,
                                                 max_iter, _d(un), _d(K), C.byref(it), C.byref(cyc),
                                                 C.byref(tr), C.byref(cv), C.byref(sec), _d(hist),
                                                 len(hist), C.byref(hl)))
@@ -300,8 +302,8 @@ class Oracle:
             L.or_precond_apply.argtypes = [C.POINTER(or_sys), dptr, dptr]
             L.or_irk_step.argtypes = [C.POINTER(or_sys), dptr, dptr, C.c_double, C.c_int, C.c_int,
                                       dptr, dptr, C.POINTER(or_report), dptr]
-            L.or_irk_step_f.argtypes = [C.POINTER(or_sys), dptr, dptr, dptr, C.c_double, C.c_int,
-                                        C.c_int, dptr, dptr, C.POINTER(or_report), dptr]
+            L.or_irk_step_f.argtypes = [C.POINTER(or_sys), dptr, dptr, dptr, C.c_int, C.c_double,
+                                        C.c_int, C.c_int, dptr, dptr, C.POINTER(or_report), dptr]
             L.or_set_ortho.argtypes = [C.c_int]
             cls._lib = L
         return cls._lib
@@ -363,7 +365,8 @@ class OracleSystem:
         Oracle.lib().or_vcycle(C.byref(self.sys.h[k]), _d(r), _d(z))
         return z
 
-    def step(self, u, lift=None, rtol=1e-8, restart=50, max_iter=500, forcing=None):
+    def step(self, u, lift=None, rtol=1e-8, restart=50, max_iter=500, forcing=None,
+             side="right"):
         """forcing: s*n stage-major forcing values at t_n + c_i ht, or None."""
         n, s = self.n, self.s
         u = np.ascontiguousarray(u, np.float64)
@@ -373,8 +376,10 @@ class OracleSystem:
         rep = or_report()
         lift_arr = None if lift is None else np.ascontiguousarray(lift, np.float64)
         f_arr = None if forcing is None else np.ascontiguousarray(forcing, np.float64)
-        Oracle.lib().or_irk_step_f(C.byref(self.sys), _d(u), _d(lift_arr), _d(f_arr), rtol, restart,
-                                   max_iter, _d(un), _d(K), C.byref(rep), _d(hist))
+        rc = Oracle.lib().or_irk_step_f(C.byref(self.sys), _d(u), _d(lift_arr), _d(f_arr),
+                                        0 if side == "left" else 1, rtol, restart, max_iter,
+                                        _d(un), _d(K), C.byref(rep), _d(hist))
+        assert rc == 0, "oracle: left preconditioning needs the delayed CGS2 scheme"
         return {"u_next": un, "K": K, "iterations": rep.iterations, "cycles": rep.cycles,
                 "n_reorth": rep.n_reorth, "converged": bool(rep.converged),
                 "true_rel": rep.true_rel, "final_rel": rep.final_rel, "seconds": rep.seconds,

@@ -6,7 +6,9 @@ The switches are read once per process, so each mode runs in a subprocess:
                            (oracle scheme 0) instead of delayed CGS2;
   * IRK_NO_VALUE_CODES=1, IRK_SPARSE_FMT=0/2 -- fp64 values, all-SELL /
                            all-CSR-vector sparse formats;
-  * IRK_PDL=1           -- programmatic dependent launch.
+  * IRK_PDL=1           -- programmatic dependent launch;
+  * IRK_SERIAL_JACOBI=1 -- block-Jacobi V-cycles in stage order on one stream
+                           instead of one graph branch per hierarchy.
 """
 import os
 import subprocess
@@ -27,8 +29,8 @@ import paper_2010_11377_b200 as P
 from systems import heat_case
 from refs import oracle_ortho
 oracle_ortho({ortho!r})
-for s, restart in ((2, 50), (3, 5)):
-    c = heat_case(48, s=s, ht=0.01)
+for s, restart, kind in ((2, 50, 3), (3, 5, 3), (3, 50, 0), (5, 8, 0)):
+    c = heat_case(48, s=s, ht=0.01, kind=P.CoeffKind(kind))
     u = c.problem.initial(0.01, 7)
     r = P.irk_step(P.LinearParabolicSystem(c.M, c.K, c.f_lift), c.table, c.ht, 0.0, u, c.device(),
                    P.GmresConfig(restart=restart), want_K=True)
@@ -47,6 +49,7 @@ print("MODE-OK")
     ({"IRK_SPARSE_FMT": "0"}, "dcgs2"),
     ({"IRK_SPARSE_FMT": "2"}, "dcgs2"),
     ({"IRK_PDL": "1"}, "dcgs2"),
+    ({"IRK_SERIAL_JACOBI": "1"}, "dcgs2"),
 ])
 def test_mode_bitwise(env, ortho):
     code = SCRIPT.format(root=str(ROOT), tests=str(ROOT / "tests"), ortho=ortho)

@@ -16,9 +16,10 @@ from paper_2010_11377_b200 import _abi
 
 cells = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 s = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+kind = P.CoeffKind(int(sys.argv[3])) if len(sys.argv) > 3 else P.CoeffKind.LowerFactor
 prob = P.make_heat_setup(cells)
 table = P.make_radau_iia(s)
-Pc = P.BlockPreconditioner(prob.M, prob.F, P.precond_coeff(table, P.CoeffKind.LowerFactor), 1e-3,
+Pc = P.BlockPreconditioner(prob.M, prob.F, P.precond_coeff(table, kind), 1e-3,
                            table=table)
 u0 = prob.initial(0.01, 1)
 cfg = P.GmresConfig(restart=50).c()
