@@ -105,6 +105,24 @@ const double* irk_hierarchy_inv_diag(const irk_hierarchy* h, int level);
 const double* irk_hierarchy_coarse_inverse(const irk_hierarchy* h, int* n);
 void irk_hierarchy_free(irk_hierarchy* h);
 
+/* ------------------------------------------------------ on-disk formats */
+/* MatrixMarket coordinate files (csr.cpp:240-290): write_matrix_market
+ * ("general", 1-based, %.17g) and read_matrix_market (general or symmetric,
+ * duplicates summed); the read matrix is owned by the handle. */
+typedef struct irk_matrix irk_matrix;
+int irk_mm_write(const irk_csr* A, const char* path);
+int irk_mm_read(const char* path, irk_matrix** out);
+int irk_matrix_view(const irk_matrix* m, irk_csr* out);
+void irk_matrix_free(irk_matrix* m);
+/* Study CSV (study.cpp:334-360): header and one row, NUL-terminated into
+ * buf (cap bytes).  scheme 0 radau_iia / 1 lobatto_iiic / 2 custom; kind as
+ * irk_precond_coeff (4 custom); side 1 right / 0 left; subsolver 0 amg / 1 lu;
+ * failed != 0 writes the reference's "failed" row. */
+int irk_csv_header(char* buf, int cap);
+int irk_csv_row(int scheme, int s, int hx_inv, double ht, int n_free, int kind, int side,
+                int subsolver, double iterations, double true_residual, double rel_error,
+                double seconds, int failed, char* buf, int cap);
+
 /* ------------------------------------------------------ device solver - */
 typedef struct irkdev irkdev;
 

@@ -447,6 +447,26 @@ int ref_integrate(void* main, void* trunc, const double* u0, const double* f_lif
     });
 }
 
+// The reference's MatrixMarket writer / reader (csr.cpp:240-290).
+int ref_mm_write(int n_rows, int n_cols, const int* rp, const int* ci, const double* v,
+                 const char* path) {
+    return guard([&] { write_matrix_market(from_arrays(n_rows, n_cols, rp, ci, v), path); });
+}
+
+// Reads into caller arrays sized by a first call with null outputs.
+int ref_mm_read(const char* path, int* n_rows, int* n_cols, int* nnz, int* rp, int* ci,
+                double* v) {
+    return guard([&] {
+        const CsrMatrix A = read_matrix_market(path);
+        *n_rows = A.n_rows;
+        *n_cols = A.n_cols;
+        *nnz = A.nnz();
+        if (rp) std::memcpy(rp, A.row_ptr.data(), sizeof(int) * (A.n_rows + 1));
+        if (ci) std::memcpy(ci, A.col_idx.data(), sizeof(int) * A.nnz());
+        if (v) std::memcpy(v, A.vals.data(), sizeof(double) * A.nnz());
+    });
+}
+
 // Plain CSR y = A x through the reference spmv (csr.cpp:102-114).
 int ref_spmv(int n_rows, int n_cols, const int* rp, const int* ci,
              const double* v, const double* x, double* y) {

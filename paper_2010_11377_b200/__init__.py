@@ -216,6 +216,45 @@ def amg_setup(A: CsrMatrix, params: AmgParams | None = None) -> AmgHierarchy:
     return AmgHierarchy(h)
 
 
+# ---------------------------------------------------------- on-disk formats
+def write_matrix_market(A: CsrMatrix, path) -> None:
+    """write_matrix_market (csr.cpp:240-251): coordinate real general, %.17g."""
+    check(_abi.lib().irk_mm_write(C.byref(A.view()), str(path).encode()))
+
+
+def read_matrix_market(path) -> CsrMatrix:
+    """read_matrix_market (csr.cpp:253-290): general or symmetric coordinate real."""
+    L = _abi.lib()
+    h = C.c_void_p()
+    check(L.irk_mm_read(str(path).encode(), C.byref(h)))
+    try:
+        v = _abi.irk_csr()
+        check(L.irk_matrix_view(h, C.byref(v)))
+        rp, ci, vals, nc = _abi.csr_arrays(v)
+        return CsrMatrix(rp.copy(), ci.copy(), vals.copy(), nc)
+    finally:
+        L.irk_matrix_free(h)
+
+
+def csv_header() -> str:
+    """study.cpp:334-337."""
+    buf = C.create_string_buffer(256)
+    check(_abi.lib().irk_csv_header(buf, len(buf)))
+    return buf.value.decode()
+
+
+def csv_row(table: ButcherTable, hx_inv: int, ht: float, n_free: int, coeff_kind: CoeffKind,
+            cfg: GmresConfig, iterations: float, true_residual: float, rel_error: float,
+            seconds: float, failed: bool = False) -> str:
+    """study.cpp:339-360 (AMG subsolver: the only one on the device)."""
+    buf = C.create_string_buffer(512)
+    check(_abi.lib().irk_csv_row(int(table.scheme), table.s, hx_inv, ht, n_free, int(coeff_kind),
+                                 0 if cfg.side == "left" else 1, 0, float(iterations),
+                                 float(true_residual), float(rel_error), float(seconds),
+                                 1 if failed else 0, buf, len(buf)))
+    return buf.value.decode()
+
+
 @dataclass
 class LinearParabolicSystem:
     """M du/dt = -F u - f_lift + forcing(t) over the free dofs (irk.hpp:15-22).

@@ -70,6 +70,14 @@ _SIGS = {
     "irk_hierarchy_inv_diag": (dptr, [V, C.c_int]),
     "irk_hierarchy_coarse_inverse": (dptr, [V, iptr]),
     "irk_hierarchy_free": (None, [V]),
+    "irk_mm_write": (C.c_int, [C.POINTER(irk_csr), C.c_char_p]),
+    "irk_mm_read": (C.c_int, [C.c_char_p, C.POINTER(V)]),
+    "irk_matrix_view": (C.c_int, [V, C.POINTER(irk_csr)]),
+    "irk_matrix_free": (None, [V]),
+    "irk_csv_header": (C.c_int, [C.c_char_p, C.c_int]),
+    "irk_csv_row": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
+                              C.c_int, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int,
+                              C.c_char_p, C.c_int]),
     "irkdev_create": (C.c_int, [C.POINTER(irk_csr), C.POINTER(irk_csr), C.c_int, dptr, dptr, dptr,
                                 C.c_int, C.c_double, C.POINTER(irk_amg_params), C.c_int,
                                 C.POINTER(V), C.c_int, C.POINTER(V)]),

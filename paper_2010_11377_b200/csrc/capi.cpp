@@ -7,6 +7,7 @@
 
 #include "../../include/irkdev.h"
 #include "device/solver.hpp"
+#include "host/mmio.hpp"
 #include "host/setup.hpp"
 
 struct irk_problem {
@@ -17,6 +18,9 @@ struct irk_hierarchy {
 };
 struct irkdev {
     std::unique_ptr<irkb::DeviceSolver> s;
+};
+struct irk_matrix {
+    irkb::Csr a;
 };
 
 namespace {
@@ -258,6 +262,60 @@ const double* irk_hierarchy_coarse_inverse(const irk_hierarchy* h, int* n) {
 }
 
 void irk_hierarchy_free(irk_hierarchy* h) { delete h; }
+
+int irk_mm_write(const irk_csr* A, const char* path) {
+    return guard([&] {
+        irkb::check(path != nullptr, "matrix market: null path");
+        irkb::write_matrix_market(to_csr(A), path);
+    });
+}
+
+int irk_mm_read(const char* path, irk_matrix** out) {
+    return guard([&] {
+        irkb::check(path != nullptr, "matrix market: null path");
+        *out = new irk_matrix{irkb::read_matrix_market(path)};
+    });
+}
+
+int irk_matrix_view(const irk_matrix* m, irk_csr* out) {
+    return guard([&] { view(m->a, out); });
+}
+
+void irk_matrix_free(irk_matrix* m) { delete m; }
+
+namespace {
+int put_text(const std::string& t, char* buf, int cap) {
+    irkb::check(buf != nullptr && cap > static_cast<int>(t.size()), "csv: buffer too small");
+    std::memcpy(buf, t.c_str(), t.size() + 1);
+    return static_cast<int>(t.size());
+}
+}  // namespace
+
+int irk_csv_header(char* buf, int cap) {
+    return guard([&] { put_text(irkb::csv_header(), buf, cap); });
+}
+
+int irk_csv_row(int scheme, int s, int hx_inv, double ht, int n_free, int kind, int side,
+                int subsolver, double iterations, double true_residual, double rel_error,
+                double seconds, int failed, char* buf, int cap) {
+    return guard([&] {
+        irkb::CsvCell c;
+        c.scheme = scheme;
+        c.s = s;
+        c.hx_inv = hx_inv;
+        c.ht = ht;
+        c.n_free = n_free;
+        c.kind = kind;
+        c.side = side;
+        c.subsolver = subsolver;
+        c.iterations = iterations;
+        c.true_residual = true_residual;
+        c.rel_error = rel_error;
+        c.seconds = seconds;
+        c.failed = failed != 0;
+        put_text(irkb::csv_row(c), buf, cap);
+    });
+}
 
 int irkdev_create(const irk_csr* M, const irk_csr* K, int s, const double* A, const double* b,
                   const double* Atilde, int structure, double ht, const irk_amg_params* amg,

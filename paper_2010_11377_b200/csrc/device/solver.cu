@@ -348,10 +348,12 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
 DeviceSolver::~DeviceSolver() {
     for (cudaGraphExec_t* e : {&exec_, &exec_iter_, &exec_pre_, &exec_cb_, &exec_ce_, &exec_post_})
         if (*e) cudaGraphExecDestroy(*e);
-    for (cudaStream_t b : branch_)
-        if (b) cudaStreamDestroy(b);
-    for (cudaEvent_t e : branch_ev_)
-        if (e) cudaEventDestroy(e);
+    for (Branches& b : branch_sets_) {
+        for (cudaStream_t x : b.st)
+            if (x) cudaStreamDestroy(x);
+        for (cudaEvent_t e : b.ev)
+            if (e) cudaEventDestroy(e);
+    }
     if (ctl_host_) cudaFreeHost(ctl_host_);
     if (hist_host_) cudaFreeHost(hist_host_);
     if (st_) cudaStreamDestroy(st_);
@@ -440,13 +442,33 @@ void DeviceSolver::record_precond(VecRef v, VecRef w) {
         // each distinct hierarchy gets its own stream branch (a fork/join in
         // the captured graph); blocks sharing a hierarchy share its level
         // buffers and run in stage order on that branch.
-        if (branch_.empty()) {
-            branch_.resize(nh);
-            branch_ev_.resize(nh + 1);
-            for (int k = 1; k < nh; ++k)
-                IRK_CUDA_CHECK(cudaStreamCreateWithFlags(&branch_[k], cudaStreamNonBlocking));
-            for (auto& e : branch_ev_) IRK_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        // A stream that joined one capture stays in it until that capture
+        // ends, so nested captures (outer and inner WHILE bodies) each take
+        // a set of branch streams no capture is using.
+        Branches* set = nullptr;
+        for (Branches& b : branch_sets_) {
+            bool busy = false;
+            for (int k = 1; k < nh; ++k) {
+                cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+                IRK_CUDA_CHECK(cudaStreamIsCapturing(b.st[k], &cs));
+                busy = busy || cs != cudaStreamCaptureStatusNone;
+            }
+            if (!busy) {
+                set = &b;
+                break;
+            }
         }
+        if (!set) {
+            branch_sets_.emplace_back();
+            set = &branch_sets_.back();
+            set->st.assign(nh, nullptr);
+            set->ev.assign(nh + 1, nullptr);
+            for (int k = 1; k < nh; ++k)
+                IRK_CUDA_CHECK(cudaStreamCreateWithFlags(&set->st[k], cudaStreamNonBlocking));
+            for (auto& e : set->ev) IRK_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        const std::vector<cudaStream_t>& branch_ = set->st;
+        const std::vector<cudaEvent_t>& branch_ev_ = set->ev;
         cudaStream_t main = st_;
         IRK_CUDA_CHECK(cudaEventRecord(branch_ev_[0], main));
         for (int k = 0; k < nh; ++k) {
@@ -700,77 +722,94 @@ void DeviceSolver::build_graph(bool lift, bool forcing, int restart, int max_ite
         IRK_CUDA_CHECK(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
         cudaStream_t main = st_;
         cudaGraph_t top = nullptr;
-        IRK_CUDA_CHECK(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
-        // The outer handle must exist before the init kernel is recorded.
-        cudaGraphConditionalHandle ho;
-        {
-            cudaStreamCaptureStatus status;
-            cudaGraph_t cg = nullptr;
-            IRK_CUDA_CHECK(cudaStreamGetCaptureInfo(main, &status, nullptr, &cg, nullptr, nullptr));
-            IRK_CUDA_CHECK(cudaGraphConditionalHandleCreate(&ho, cg, 0, 0));
+        try {
+            IRK_CUDA_CHECK(cudaStreamBeginCapture(main, cudaStreamCaptureModeThreadLocal));
+            // The outer handle must exist before the init kernel is recorded.
+            cudaGraphConditionalHandle ho;
+            {
+                cudaStreamCaptureStatus status;
+                cudaGraph_t cg = nullptr;
+                IRK_CUDA_CHECK(cudaStreamGetCaptureInfo(main, &status, nullptr, &cg, nullptr, nullptr));
+                IRK_CUDA_CHECK(cudaGraphConditionalHandleCreate(&ho, cg, 0, 0));
+            }
+            gb_.h_outer = ho;
+            pre();
+            // outer WHILE node (handle created above, on the top graph)
+            cudaGraph_t outer_body;
+            {
+                cudaStreamCaptureStatus status;
+                cudaGraph_t cg = nullptr;
+                const cudaGraphNode_t* deps = nullptr;
+                size_t ndeps = 0;
+                IRK_CUDA_CHECK(cudaStreamGetCaptureInfo(main, &status, nullptr, &cg, &deps, &ndeps));
+                cudaGraphNodeParams p = {};
+                p.type = cudaGraphNodeTypeConditional;
+                p.conditional.handle = ho;
+                p.conditional.type = cudaGraphCondTypeWhile;
+                p.conditional.size = 1;
+                cudaGraphNode_t node;
+                IRK_CUDA_CHECK(cudaGraphAddNode(&node, cg, deps, ndeps, &p));
+                IRK_CUDA_CHECK(cudaStreamUpdateCaptureDependencies(main, &node, 1, cudaStreamSetCaptureDependencies));
+                outer_body = p.conditional.phGraph_out[0];
+            }
+            // outer body: cycle begin -> inner WHILE -> cycle end
+            st_ = s2;
+            IRK_CUDA_CHECK(cudaStreamBeginCaptureToGraph(s2, outer_body, nullptr, nullptr, 0,
+                                                         cudaStreamCaptureModeThreadLocal));
+            cudaGraphConditionalHandle hi;
+            {
+                cudaStreamCaptureStatus status;
+                cudaGraph_t cg = nullptr;
+                IRK_CUDA_CHECK(cudaStreamGetCaptureInfo(s2, &status, nullptr, &cg, nullptr, nullptr));
+                IRK_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hi, cg, 0, 0));
+            }
+            gb_.h_inner = hi;
+            cycle_begin();
+            cudaGraph_t inner_body;
+            {
+                cudaStreamCaptureStatus status;
+                cudaGraph_t cg = nullptr;
+                const cudaGraphNode_t* deps = nullptr;
+                size_t ndeps = 0;
+                IRK_CUDA_CHECK(cudaStreamGetCaptureInfo(s2, &status, nullptr, &cg, &deps, &ndeps));
+                cudaGraphNodeParams p = {};
+                p.type = cudaGraphNodeTypeConditional;
+                p.conditional.handle = hi;
+                p.conditional.type = cudaGraphCondTypeWhile;
+                p.conditional.size = 1;
+                cudaGraphNode_t node;
+                IRK_CUDA_CHECK(cudaGraphAddNode(&node, cg, deps, ndeps, &p));
+                IRK_CUDA_CHECK(cudaStreamUpdateCaptureDependencies(s2, &node, 1, cudaStreamSetCaptureDependencies));
+                inner_body = p.conditional.phGraph_out[0];
+            }
+            st_ = s3;
+            IRK_CUDA_CHECK(cudaStreamBeginCaptureToGraph(s3, inner_body, nullptr, nullptr, 0,
+                                                         cudaStreamCaptureModeThreadLocal));
+            record_iteration();
+            IRK_CUDA_CHECK(cudaStreamEndCapture(s3, &inner_body));
+            launches_per_iter_ = count_nodes(inner_body);
+            st_ = s2;
+            cycle_end();
+            IRK_CUDA_CHECK(cudaStreamEndCapture(s2, &outer_body));
+            st_ = main;
+            post();
+            IRK_CUDA_CHECK(cudaStreamEndCapture(main, &top));
+        } catch (...) {
+            // leave no stream in capture mode and the solver on its own stream
+            st_ = main;
+            for (cudaStream_t x : {s3, s2, main}) {
+                cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+                if (cudaStreamIsCapturing(x, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+                    cudaGraph_t junk = nullptr;
+                    cudaStreamEndCapture(x, &junk);
+                    if (junk) cudaGraphDestroy(junk);
+                }
+            }
+            cudaGetLastError();
+            cudaStreamDestroy(s2);
+            cudaStreamDestroy(s3);
+            throw;
         }
-        gb_.h_outer = ho;
-        pre();
-        // outer WHILE node (handle created above, on the top graph)
-        cudaGraph_t outer_body;
-        {
-            cudaStreamCaptureStatus status;
-            cudaGraph_t cg = nullptr;
-            const cudaGraphNode_t* deps = nullptr;
-            size_t ndeps = 0;
-            IRK_CUDA_CHECK(cudaStreamGetCaptureInfo(main, &status, nullptr, &cg, &deps, &ndeps));
-            cudaGraphNodeParams p = {};
-            p.type = cudaGraphNodeTypeConditional;
-            p.conditional.handle = ho;
-            p.conditional.type = cudaGraphCondTypeWhile;
-            p.conditional.size = 1;
-            cudaGraphNode_t node;
-            IRK_CUDA_CHECK(cudaGraphAddNode(&node, cg, deps, ndeps, &p));
-            IRK_CUDA_CHECK(cudaStreamUpdateCaptureDependencies(main, &node, 1, cudaStreamSetCaptureDependencies));
-            outer_body = p.conditional.phGraph_out[0];
-        }
-        // outer body: cycle begin -> inner WHILE -> cycle end
-        st_ = s2;
-        IRK_CUDA_CHECK(cudaStreamBeginCaptureToGraph(s2, outer_body, nullptr, nullptr, 0,
-                                                     cudaStreamCaptureModeThreadLocal));
-        cudaGraphConditionalHandle hi;
-        {
-            cudaStreamCaptureStatus status;
-            cudaGraph_t cg = nullptr;
-            IRK_CUDA_CHECK(cudaStreamGetCaptureInfo(s2, &status, nullptr, &cg, nullptr, nullptr));
-            IRK_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hi, cg, 0, 0));
-        }
-        gb_.h_inner = hi;
-        cycle_begin();
-        cudaGraph_t inner_body;
-        {
-            cudaStreamCaptureStatus status;
-            cudaGraph_t cg = nullptr;
-            const cudaGraphNode_t* deps = nullptr;
-            size_t ndeps = 0;
-            IRK_CUDA_CHECK(cudaStreamGetCaptureInfo(s2, &status, nullptr, &cg, &deps, &ndeps));
-            cudaGraphNodeParams p = {};
-            p.type = cudaGraphNodeTypeConditional;
-            p.conditional.handle = hi;
-            p.conditional.type = cudaGraphCondTypeWhile;
-            p.conditional.size = 1;
-            cudaGraphNode_t node;
-            IRK_CUDA_CHECK(cudaGraphAddNode(&node, cg, deps, ndeps, &p));
-            IRK_CUDA_CHECK(cudaStreamUpdateCaptureDependencies(s2, &node, 1, cudaStreamSetCaptureDependencies));
-            inner_body = p.conditional.phGraph_out[0];
-        }
-        st_ = s3;
-        IRK_CUDA_CHECK(cudaStreamBeginCaptureToGraph(s3, inner_body, nullptr, nullptr, 0,
-                                                     cudaStreamCaptureModeThreadLocal));
-        record_iteration();
-        IRK_CUDA_CHECK(cudaStreamEndCapture(s3, &inner_body));
-        launches_per_iter_ = count_nodes(inner_body);
-        st_ = s2;
-        cycle_end();
-        IRK_CUDA_CHECK(cudaStreamEndCapture(s2, &outer_body));
-        st_ = main;
-        post();
-        IRK_CUDA_CHECK(cudaStreamEndCapture(main, &top));
         exec_ = instantiate(top);
         cudaGraphDestroy(top);
         cudaStreamDestroy(s2);

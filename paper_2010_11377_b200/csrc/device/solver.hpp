@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <deque>
 #include <cstdint>
 #include <memory>
 #include <vector>
@@ -145,8 +146,11 @@ private:
     long long sN_ = 0, stride_ = 0;
     int device_ = 0;
     cudaStream_t st_ = nullptr;
-    std::vector<cudaStream_t> branch_;   // block-Jacobi V-cycle branches (index 0 unused)
-    std::vector<cudaEvent_t> branch_ev_; // [0] fork, [k] join of branch k
+    struct Branches {                    // block-Jacobi V-cycle branches
+        std::vector<cudaStream_t> st;    // index 0 unused (the recording stream)
+        std::vector<cudaEvent_t> ev;     // [0] fork, [k] join of branch k
+    };
+    std::deque<Branches> branch_sets_;   // one set per concurrently open capture
     std::vector<DevBuf> bufs_;
 
     dev::Mat M_, K_;

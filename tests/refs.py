@@ -82,6 +82,8 @@ class Ref:
             L.ref_ldu.argtypes = [C.c_int, dptr, dptr, dptr, dptr]
             L.ref_spmv.argtypes = [C.c_int, C.c_int, iptr, iptr, dptr, dptr, dptr]
             L.ref_dot.argtypes = [C.c_int, dptr, dptr]
+            L.ref_mm_write.argtypes = [C.c_int, C.c_int, iptr, iptr, dptr, C.c_char_p]
+            L.ref_mm_read.argtypes = [C.c_char_p, iptr, iptr, iptr, iptr, iptr, dptr]
             cls._lib = L
         return cls._lib
 

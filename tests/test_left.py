@@ -66,6 +66,11 @@ def test_device_left_bitwise(prob, s, kind, restart):
     assert np.array_equal(np.array(g.report.history), o["history"])
     assert np.array_equal(g.K, o["K"]) and np.array_equal(g.u_next, o["u_next"])
     assert g.report.true_rel_residual == o["true_rel"]
+    # the whole solve stays one conditional graph (no host-driven fallback)
+    import ctypes as C
+    lp, mode = C.c_int(), C.c_int()
+    P._abi.check(P._abi.lib().irkdev_graph_info(c.device()._dev._h, C.byref(lp), C.byref(mode)))
+    assert mode.value == 1
     # switching sides on one handle rebuilds the graph and stays exact
     g2 = P.irk_step(sys, c.table, c.ht, 0.0, u, c.device(), P.GmresConfig(restart=restart),
                     want_K=True)
