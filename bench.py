@@ -36,8 +36,47 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "IRK timestep solves/s (2D heat, Radau IIA); solve-phase HBM GB/s vs peak"
 UNIT = "solves/s"
-CELLS, S, HT, NOISE, SEED = 1024, 3, 1e-3, 0.01, 1
-WORKLOAD = "C2: heat 1024^2 P1, Radau IIA s=3, h_t=1e-3, P_LD + AMG V(1,1) Jacobi, GMRES(50) rtol 1e-8"
+# BASELINE.json configs.  C2 is the headline workload; the
+# others are selectable with --workload for the record (profiles/).
+WORKLOADS = {
+    "C1": dict(problem="heat", cells=64, scheme=0, s=2, ht=1e-2, noise=0.0, seed=0, steps=1,
+               desc="C1: heat 64^2 P1, Radau IIA s=2, h_t=1e-2, P_LD + AMG V(1,1) Jacobi, GMRES(50) rtol 1e-8"),
+    "C2": dict(problem="heat", cells=1024, scheme=0, s=3, ht=1e-3, noise=0.01, seed=1, steps=10,
+               desc="C2: heat 1024^2 P1, Radau IIA s=3, h_t=1e-3, P_LD + AMG V(1,1) Jacobi, GMRES(50) rtol 1e-8"),
+    "C3": dict(problem="heat", cells=2048, scheme=1, s=5, ht=1e-3, noise=0.01, seed=1, steps=5,
+               desc="C3: heat 2048^2 P1, Lobatto IIIC s=5, h_t=1e-3, P_LD + AMG V(1,1) Jacobi, GMRES(50) rtol 1e-8"),
+    "C4": dict(problem="dg", cells=1024, scheme=0, s=4, ht=1e-2, noise=None, seed=0, steps=10,
+               desc="C4: double glazing 1024^2 P1 SUPG (eps 0.005), Radau IIA s=4, h_t=1e-2, u0=0, "
+                    "P_LD + AMG V(1,1) Jacobi, GMRES(50) rtol 1e-8"),
+}
+WL = WORKLOADS["C2"]
+CELLS, S, HT = WL["cells"], WL["s"], WL["ht"]
+WORKLOAD = WL["desc"]
+
+
+def set_workload(name: str, cells: int | None = None):
+    global WL, CELLS, S, HT, WORKLOAD
+    WL = dict(WORKLOADS[name])
+    if cells:
+        WL["cells"] = cells
+    CELLS, S, HT, WORKLOAD = WL["cells"], WL["s"], WL["ht"], WL["desc"]
+
+
+def make_problem(P):
+    """(ProblemSetup, Butcher table, u0, f_lift or None) of the workload."""
+    if WL["problem"] == "heat":
+        prob = P.make_heat_setup(CELLS)
+        u0 = prob.initial(WL["noise"], WL["seed"])
+        lift = None
+    else:
+        prob = P.make_double_glazing_setup(CELLS, 0.005)
+        u0 = np.zeros(prob.M.n_rows)
+        lift = np.ascontiguousarray(prob.f_lift)
+    table = P.make_table(P.Scheme(WL["scheme"]), S)
+    return prob, table, u0, lift
+
+
+DATA = "synthetic (seeded u0 noise / zero u0 for C4, BASELINE configs; no dataset involved)"
 
 
 def peaks():
@@ -48,8 +87,9 @@ def peaks():
 
 
 def config(extra=None):
-    c = {"workload": WORKLOAD, "grid": f"{CELLS}x{CELLS}", "dofs_per_stage": (CELLS - 1) ** 2,
-         "stages": S, "unknowns": S * (CELLS - 1) ** 2, "ht": HT, "preconditioner": "LD",
+    n = (CELLS - 1) ** 2 if WL["problem"] == "heat" else None
+    c = {"workload": WORKLOAD, "grid": f"{CELLS}x{CELLS}", "dofs_per_stage": n,
+         "stages": S, "unknowns": S * n if n else None, "ht": HT, "preconditioner": "LD",
          "gmres_restart": 50, "rel_tol": 1e-8,
          "l2_policy": "inputs larger than L2 (>=2.8 GB streamed per GMRES iteration vs 126 MB L2)"}
     if extra:
@@ -162,10 +202,9 @@ def run_reference_steps(steps, warmup, rank0=True):
     if not Ref.available():
         raise RuntimeError("oracle/_ref/libirkref.so not built")
     import paper_2010_11377_b200 as P
-    prob = P.make_heat_setup(CELLS)
-    u0 = prob.initial(NOISE, SEED)
-    ref_prob = Ref.problem("heat", CELLS)
-    rs = RefSolver(ref_prob["M"], ref_prob["K"], 0, S, 3, HT)
+    _, _, u0, _ = make_problem(P)
+    ref_prob = Ref.problem(WL["problem"], CELLS)
+    rs = RefSolver(ref_prob["M"], ref_prob["K"], WL["scheme"], S, 3, HT)
     u = u0.copy()
     for _ in range(warmup):
         rs.step(u, ref_prob["f_lift"])
@@ -198,10 +237,10 @@ def reference_arm(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": 1e3 * total / steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded u0 noise, BASELINE configs[1])",
+        "data": DATA,
         "config": config({"reference_iterations": its}),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "reference",
-                         "sample": f"{steps} C2 timesteps of the reference irk_step (irkprec compiled "
+                         "sample": f"{steps} {WORKLOAD[:2]} timesteps of the reference irk_step (irkprec compiled "
                                    "from /root/reference sources, OpenMP, GMRES(50) wrapper), "
                                    "setup excluded"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -218,16 +257,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cells", type=int, default=CELLS)
+    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--cells", type=int, default=None, help="override the workload's grid")
     args = ap.parse_args()
+    set_workload(args.workload, args.cells)
     if args.impl == "reference":
         return reference_arm(args)
     return our_arm(args)
 
 
 def our_arm(args):
-    global CELLS
-    CELLS = args.cells
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -243,14 +282,14 @@ def our_arm(args):
     L = _abi.lib()
 
     t_setup = time.time()
-    prob = P.make_heat_setup(CELLS)
-    table = P.make_radau_iia(S)
+    prob, table, u0, lift = make_problem(P)
     coeff = P.precond_coeff(table, P.CoeffKind.LowerFactor)
     Pc = P.BlockPreconditioner(prob.M, prob.F, coeff, HT, P.AmgParams(), table=table, device=local)
     dev = Pc._dev
     setup_s = time.time() - t_setup
-    u0 = prob.initial(NOISE, SEED)
     n = prob.M.n_rows
+    d_lift = torch.from_numpy(lift).cuda() if lift is not None else None
+    lift_ptr = C.c_void_p(d_lift.data_ptr()) if d_lift is not None else None
     cfg = P.GmresConfig(restart=50).c()
 
     d_u = torch.from_numpy(u0).cuda()
@@ -261,7 +300,7 @@ def our_arm(args):
 
     def dstep(u_t, un_t):
         rep = _abi.irk_report()
-        _abi.check(L.irkdev_step_device(dev._h, C.c_void_p(u_t.data_ptr()), None, C.byref(cfg),
+        _abi.check(L.irkdev_step_device(dev._h, C.c_void_p(u_t.data_ptr()), lift_ptr, C.byref(cfg),
                                         C.c_void_p(un_t.data_ptr()), None, C.byref(rep)))
         return rep
 
@@ -288,6 +327,7 @@ def our_arm(args):
 
     # e2e: host pointers through the public C ABI (H2D u_n, D2H u_{n+1} + report)
     hu = torch.from_numpy(u0.copy()).pin_memory()
+    h_lift = None if lift is None else _abi.as_d(torch.from_numpy(lift).pin_memory().numpy())
     hun = torch.empty_like(hu).pin_memory()
     hist = np.empty(501)
     torch.cuda.synchronize()
@@ -298,7 +338,7 @@ def our_arm(args):
     e2.record(st)
     for _ in range(args.steps):
         rep = _abi.irk_report()
-        _abi.check(L.irkdev_step(dev._h, _abi.as_d(hu.numpy()), None, C.byref(cfg),
+        _abi.check(L.irkdev_step(dev._h, _abi.as_d(hu.numpy()), h_lift, C.byref(cfg),
                                  _abi.as_d(hun.numpy()), None, C.byref(rep), _abi.as_d(hist)))
         hu, hun = hun, hu
     e3.record(st)
@@ -354,7 +394,7 @@ def our_arm(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded u0 noise, BASELINE configs[1])",
+        "data": DATA,
         "config": config({"parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                           "gmres_iterations": its, "reorth_passes": [r.n_reorth for r in reps],
                           "restart_cycles": [r.cycles for r in reps],
@@ -362,7 +402,8 @@ def our_arm(args):
                           "launches_per_iteration": cnt[2], "setup_seconds": setup_s,
                           "hierarchy_sizes": [[x[0] for x in lv] for lv in levels]}),
         "e2e": {"value": replicas.whole_job_throughput(args.steps, world, e2e_ms), "unit": UNIT,
-                "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n + 4 * 8 + 8 * 501,
+                "h2d_bytes_per_step": 8 * n * (1 if lift is None else 2),
+                "d2h_bytes_per_step": 8 * n + 4 * 8 + 8 * 501,
                 "wall_seconds": wall_e2e},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "k_dgs_dot (DCGS2 fused block-dot, j=15: 17 x sN doubles)",
@@ -383,10 +424,11 @@ def our_arm(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            total, rits = run_reference_steps(2, 0)
+            nref = 1 if CELLS > 1024 else 2
+            total, rits = run_reference_steps(nref, 0)
             line["cpu_baseline"] = {
-                "value": 2 / total, "unit": UNIT, "cores": cpu_threads(), "kind": "reference",
-                "sample": "2 C2 timesteps of the reference irk_step (irkprec compiled from its "
+                "value": nref / total, "unit": UNIT, "cores": cpu_threads(), "kind": "reference",
+                "sample": f"{nref} {WORKLOAD[:2]} timesteps of the reference irk_step (irkprec compiled from its "
                           "own sources, OpenMP on all host threads, GMRES(50) wrapper), setup "
                           f"excluded; reference iterations {rits}"}
         except Exception as e:  # reported, not fatal

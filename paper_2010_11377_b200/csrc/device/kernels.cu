@@ -70,11 +70,14 @@ __device__ __forceinline__ double vfetch(const void* v, long long k, const doubl
     }
 }
 
-// Shared-memory dictionaries for u8 codes (256 entries each).
+// Dictionaries for u8 codes (256 entries each): a shared-memory copy per CTA
+// (A.tab_smem), or read in place from global memory through L1 (no per-CTA
+// prologue and barrier before the first row load).
 template <int VF>
 __device__ __forceinline__ const double* load_tab(const Mat& A, double* s_tab, double* s_wd) {
     pdl_trigger();
     if constexpr (VF == kU8) {
+        if (!A.tab_smem) return A.tab;
         for (int i = threadIdx.x; i < A.ntab; i += blockDim.x) {
             s_tab[i] = A.tab[i];
             if (A.wdtab) s_wd[i] = A.wdtab[i];
@@ -121,6 +124,7 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
     if constexpr (WDT == 1)
         dcode = static_cast<const unsigned char*>(A.val) + static_cast<long long>(A.diag0) * A.dstride;
     const int nd = ND > 0 ? ND : A.nd;
+    const double* wdt = A.tab_smem ? s_wd : A.wdtab;
     double s = 0.0;
 #pragma unroll
     for (int d = 0; d < (ND > 0 ? ND : kMaxDiags); ++d) {
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
         const int c = min(max(i + A.off[d], 0), n - 1);
         double xv;
         if constexpr (XM == kXWdR) {
-            const double wdc = WDT == 1 ? s_wd[__ldg(dcode + c)] : wd[c];
+            const double wdc = WDT == 1 ? wdt[__ldg(dcode + c)] : wd[c];
             xv = wdc * r[c];
         } else {
             xv = x[c];
@@ -137,7 +141,7 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
     }
     double wdi = 0.0;
     if (EPI == kESmooth || (EPI == kEProlong && !a.zb))
-        wdi = WDT == 1 ? s_wd[__ldg(dcode + i)] : wd[i];
+        wdi = WDT == 1 ? wdt[__ldg(dcode + i)] : wd[i];
     a.y.get()[i] = spmv_epilogue<XM, EPI>(s, wdi, i, a, r, x);
 }
 
@@ -158,11 +162,10 @@ __global__ void __launch_bounds__(256) k_spmv_sell(Mat A, SpmvArgs a) {
     const double* __restrict__ wd = a.wd;
     const int base = __ldg(A.sptr + slice);
     const int len = (__ldg(A.sptr + slice + 1) - base) >> 5;
-    const int* __restrict__ idx = A.idx + base + lane;
     double s = 0.0;
 #pragma unroll 4
     for (int k = 0; k < len; ++k) {
-        const int c = __ldg(idx + k * 32);
+        const int c = __ldg(A.idx + base + k * 32 + lane);
         const double xv = XM == kXWdR ? wd[c] * r[c] : x[c];
         s += vfetch<VF>(A.val, base + k * 32 + lane, tab) * xv;
     }

@@ -43,6 +43,7 @@ struct Mat {
     const void* val = nullptr;
     const double* tab = nullptr;  // code dictionary (vf != kF64)
     int ntab = 0;
+    int tab_smem = 0;             // u8: stage the dictionaries in shared memory per CTA
     // DIA
     int nd = 0;
     int off[kMaxDiags] = {};

@@ -130,6 +130,10 @@ void DeviceSolver::upload_values(dev::Mat& m, const std::vector<double>& vals, d
     }
     m.tab = upload_array(d.tab);
     m.ntab = static_cast<int>(d.tab.size());
+    // u8 dictionaries are read in place through L1 (a per-CTA shared-memory
+    // copy costs a dependent prologue and a barrier; IRK_U8_TAB_SMEM=1 keeps it)
+    static const bool tab_smem = std::getenv("IRK_U8_TAB_SMEM") != nullptr;
+    m.tab_smem = tab_smem ? 1 : 0;
     if (d.vf == dev::kU8) {
         m.val = upload_array(d.c8);
         m.bytes += d.c8.size();

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <array>
+#include <cstdlib>
 #include <deque>
 #include <cstdint>
 #include <memory>

@@ -8,7 +8,11 @@ The switches are read once per process, so each mode runs in a subprocess:
                            all-CSR-vector sparse formats;
   * IRK_PDL=1           -- programmatic dependent launch;
   * IRK_SERIAL_JACOBI=1 -- block-Jacobi V-cycles in stage order on one stream
-                           instead of one graph branch per hierarchy.
+                           instead of one graph branch per hierarchy;
+  * IRK_CODES_MIN_ROWS=0 -- value dictionaries on every operator (the
+                           full-size defaults use them at level 0 only), read
+                           through L1 (default) or staged in shared memory
+                           (IRK_U8_TAB_SMEM=1).
 """
 import os
 import subprocess
@@ -50,6 +54,8 @@ print("MODE-OK")
     ({"IRK_SPARSE_FMT": "2"}, "dcgs2"),
     ({"IRK_PDL": "1"}, "dcgs2"),
     ({"IRK_SERIAL_JACOBI": "1"}, "dcgs2"),
+    ({"IRK_CODES_MIN_ROWS": "0"}, "dcgs2"),
+    ({"IRK_CODES_MIN_ROWS": "0", "IRK_U8_TAB_SMEM": "1"}, "dcgs2"),
 ])
 def test_mode_bitwise(env, ortho):
     code = SCRIPT.format(root=str(ROOT), tests=str(ROOT / "tests"), ortho=ortho)
