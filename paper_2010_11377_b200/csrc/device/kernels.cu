@@ -24,10 +24,16 @@ inline int blocks_for(long long n, int t) { return static_cast<int>((n + t - 1) 
 
 }  // namespace
 
+namespace {
+thread_local bool g_pdl_scope = false;
+}
+
 bool pdl_enabled() {
     static const bool on = std::getenv("IRK_PDL") != nullptr;
-    return on;
+    return on || g_pdl_scope;
 }
+
+void set_pdl_scope(bool on) { g_pdl_scope = on; }
 
 namespace {
 

@@ -74,6 +74,9 @@ struct SpmvArgs {
 
 // Programmatic dependent launch, opt-in via IRK_PDL=1.
 bool pdl_enabled();
+// Programmatic launch for the kernels recorded while the scope is on (the
+// latency-bound coarse AMG levels, IRK_PDL_COARSE).
+void set_pdl_scope(bool on);
 
 void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st);
 

@@ -377,9 +377,13 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
     const int pre = H.prm.pre_sweeps, post = H.prm.post_sweeps;
     // `first` > 0 runs only the part of the cycle below level `first` (timing)
     auto rhs_of = [&](int l) { return l == first ? r0 : dev::plain(H.lv[l].r); };
+    // programmatic launches for the latency-bound levels >= 2 (IRK_PDL_COARSE=0 off)
+    static const int pdl_from = std::getenv("IRK_PDL_COARSE") ? std::atoi(std::getenv("IRK_PDL_COARSE")) : 2;
+    auto scope = [&](int l) { dev::set_pdl_scope(pdl_from > 0 && l >= pdl_from); };
     auto out_of = [&](int l) { return l == first ? z0 : dev::plain(H.lv[l].z); };
     for (int l = first; l + 1 < L; ++l) {
         DevLevel& d = H.lv[l];
+        scope(l);
         dev::SpmvArgs a;
         a.r = rhs_of(l);
         a.wd = d.wd;
@@ -407,9 +411,11 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
         ra.y = dev::plain(H.lv[l + 1].r);
         dev::spmv(d.R, dev::kXPlain, dev::kEPlain, ra, st_);
     }
+    scope(L - 1);
     dev::dense_mv(H.nc, H.cinv, rhs_of(L - 1), out_of(L - 1), st_);
     for (int l = L - 2; l >= first; --l) {
         DevLevel& d = H.lv[l];
+        scope(l);
         dev::SpmvArgs pa;
         pa.x = dev::plain(H.lv[l + 1].z);
         pa.r = rhs_of(l);
@@ -430,6 +436,7 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
             cur = nxt;
         }
     }
+    dev::set_pdl_scope(false);
 }
 
 // Block preconditioner apply (stage.cpp:138-182): diagonal, forward (LD,

@@ -6,7 +6,8 @@ The switches are read once per process, so each mode runs in a subprocess:
                            (oracle scheme 0) instead of delayed CGS2;
   * IRK_NO_VALUE_CODES=1, IRK_SPARSE_FMT=0/2 -- fp64 values, all-SELL /
                            all-CSR-vector sparse formats;
-  * IRK_PDL=1           -- programmatic dependent launch;
+  * IRK_PDL=1           -- programmatic dependent launch for every kernel;
+  * IRK_PDL_COARSE=0    -- no programmatic launch on AMG levels >= 2 (default on);
   * IRK_SERIAL_JACOBI=1 -- block-Jacobi V-cycles in stage order on one stream
                            instead of one graph branch per hierarchy;
   * IRK_CODES_MIN_ROWS=0 -- value dictionaries on every operator (the
@@ -53,6 +54,7 @@ print("MODE-OK")
     ({"IRK_SPARSE_FMT": "0"}, "dcgs2"),
     ({"IRK_SPARSE_FMT": "2"}, "dcgs2"),
     ({"IRK_PDL": "1"}, "dcgs2"),
+    ({"IRK_PDL_COARSE": "0"}, "dcgs2"),
     ({"IRK_SERIAL_JACOBI": "1"}, "dcgs2"),
     ({"IRK_CODES_MIN_ROWS": "0"}, "dcgs2"),
     ({"IRK_CODES_MIN_ROWS": "0", "IRK_U8_TAB_SMEM": "1"}, "dcgs2"),
