@@ -59,6 +59,18 @@ def main():
         ("heat48_radau3_jacobi", "heat", 48, 0, 3, 0, 0.005, 0.01, 3, 50),
         ("dg64_radau2_ld", "dg", 64, 0, 2, 3, 0.01, 0.0, 1, 50),
     ]
+    # extras: side (GMRES preconditioning side) and a time-dependent forcing
+    # cos(t) * fq at t_n (ref_harness.cpp cos_forcing)
+    extras = {
+        "heat48_radau3_ld_left": dict(side="left"),
+        "heat48_radau3_ld_left_restart5": dict(side="left"),
+        "heat32_radau3_ld_forced": dict(t_n=0.37, fq_seed=11),
+    }
+    cases += [
+        ("heat48_radau3_ld_left", "heat", 48, 0, 3, 3, 0.01, 0.01, 5, 50),
+        ("heat48_radau3_ld_left_restart5", "heat", 48, 0, 3, 3, 0.01, 0.01, 5, 5),
+        ("heat32_radau3_ld_forced", "heat", 32, 0, 3, 3, 0.01, 0.01, 2, 50),
+    ]
     for name, kind, cells, scheme, s, ck, ht, noise, seed, restart in cases:
         prob = Ref.problem(kind, cells, 0.005)
         g = {"cells": np.array(cells), "scheme": np.array(scheme), "s": np.array(s),
@@ -88,14 +100,45 @@ def main():
             g[f"hier{k}_sha"] = np.array(shas)
         u0 = np.zeros(len(prob["M"][0]) - 1) if kind == "dg" else heat_u0(cells, noise, seed)
         rs = RefSolver(prob["M"], prob["K"], scheme, s, ck, ht)
-        r = rs.step(u0, prob["f_lift"], restart=restart)
+        ex = extras.get(name, {})
+        side = ex.get("side", "right")
+        t_n = ex.get("t_n", 0.0)
+        fq = (np.random.default_rng(ex["fq_seed"]).uniform(-1.0, 1.0, len(u0))
+              if "fq_seed" in ex else None)
+        r = rs.step(u0, prob["f_lift"], restart=restart, side=side, t_n=t_n, fq=fq)
         g.update(u0=u0, u_next=r["u_next"], K=r["K"], iterations=np.array(r["iterations"]),
                  cycles=np.array(r["cycles"]), true_rel=np.array(r["true_rel"]),
-                 history=r["history"])
+                 history=r["history"], side=np.array(side), t_n=np.array(t_n))
+        if fq is not None:
+            g["fq"] = fq
         np.savez_compressed(HERE / f"{name}.npz", **g)
         print(name, "iterations", r["iterations"], "cycles", r["cycles"], "levels",
               [g[f"hier{k}_sizes"].tolist() for k in range(len(distinct))])
 
 
+def trajectory():
+    """The reference's own integrate (irk.cpp:70-102) with a truncated last
+    step and the cos(t) * fq forcing: heat 24^2, Radau IIA s=2, P_LD,
+    h_t = 0.01, t_final = 0.035 (steps 0.01, 0.01, 0.01, ~0.005)."""
+    cells, s, ht, t_final = 24, 2, 0.01, 0.035
+    prob = Ref.problem("heat", cells)
+    u0 = heat_u0(cells, 0.01, 4)
+    fq = np.random.default_rng(5).uniform(-1.0, 1.0, len(u0))
+    t, steps = 0.0, []
+    while t < t_final - 1e-14 * t_final:
+        st = ht if t + ht <= t_final else t_final - t
+        steps.append(st)
+        t += st
+    main_s = RefSolver(prob["M"], prob["K"], 0, s, 3, ht)
+    trunc = RefSolver(prob["M"], prob["K"], 0, s, 3, steps[-1])
+    r = main_s.integrate(u0, t_final, trunc=trunc, lift=prob["f_lift"], fq=fq)
+    np.savez_compressed(HERE / "traj_heat24_radau2_ld_forced.npz", cells=np.array(cells),
+                        s=np.array(s), ht=np.array(ht), t_final=np.array(t_final), u0=u0, fq=fq,
+                        u_final=r["u_final"], steps=np.array(r["steps"]),
+                        t_end=np.array(r["t_final"]), iterations=np.array(r["iterations"]))
+    print("trajectory steps", r["steps"], "iterations", r["iterations"])
+
+
 if __name__ == "__main__":
     main()
+    trajectory()
