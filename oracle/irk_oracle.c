@@ -286,7 +286,7 @@ static void dcgs2_cycle(const or_sys* S, long N, int R, int budget, double* V, d
                         double* H, double* g, double* cs, double* sn, double* s_, double* p_,
                         const double* r, double* hnorm, double* beta_io, double tol_c, int cycles,
                         int* total, int* m_out, int* stop_out, double* final_rel, double* hist,
-                        int side, double rtol, double* scratch) {
+                        int side, double rtol, double* scratch, double* zs) {
     double beta = *beta_io;
     memcpy(V, r, sizeof(double) * N); /* vt_0 = r, unnormalised */
     int j = 0, stop = 0;
@@ -336,10 +336,13 @@ static void dcgs2_cycle(const or_sys* S, long N, int R, int budget, double* V, d
             *final_rel = hv;
         }
         const double hjj = alpha > 0.0 ? (pi - sp) / alpha : 0.0;
-        double* hcj = H + (long)j * (R + 1);
-        for (int i = 0; i < j; ++i) hcj[i] = p_[i];
-        hcj[j] = hjj;
         const double inv = alpha > 0.0 ? 1.0 / alpha : 0.0;
+        /* column j (input Z_j = P^-1 vt_j) stored for the unit input: / alpha;
+         * the next direction is stored / alpha as well, x uses y_j / alpha_j */
+        double* hcj = H + (long)j * (R + 1);
+        for (int i = 0; i < j; ++i) hcj[i] = p_[i] * inv;
+        hcj[j] = hjj * inv;
+        zs[j] = inv;
         for (long k = 0; k < N; ++k) {
             double v = vt[k], ww = w[k];
             for (int i = 0; i < j; ++i) {
@@ -348,7 +351,7 @@ static void dcgs2_cycle(const or_sys* S, long N, int R, int budget, double* V, d
                 ww = ww - p_[i] * vi;
             }
             v = v * inv;
-            ww = ww - hjj * v;
+            ww = (ww - hjj * v) * inv;
             vt[k] = v;
             w[k] = ww;
         }
@@ -431,6 +434,8 @@ int or_irk_step_f(const or_sys* S, const double* u, const double* lift, const do
     double* h = (double*)calloc(R + 2, sizeof(double));
     double* cc = (double*)calloc(R + 2, sizeof(double));
     double* y = (double*)calloc(R + 1, sizeof(double));
+    double* zs = (double*)calloc(R + 1, sizeof(double)); /* DCGS2 column scales */
+    double* ys = (double*)calloc(R + 1, sizeof(double));
 
     /* stage right-hand side (irk.cpp:9-33): blk = -(F u + lift), then
      * blk += 1.0 * forcing(t_n + c_q ht) (forcing: s*n stage-major, or NULL) */
@@ -468,7 +473,7 @@ int or_irk_step_f(const or_sys* S, const double* u, const double* lift, const do
                 if (side == 0) or_precond_apply(S, r, base); /* left: base P^-1 r_k */
                 dcgs2_cycle(S, N, R, budget, V, Z, H, g, cs, sn, h, cc, side == 0 ? base : r,
                             &hnorm, &beta, tol_c, cycles, &total, &m, &stop, &final_rel, hist,
-                            side, rtol, ax);
+                            side, rtol, ax, zs);
                 nre += m;
                 goto cycle_end;
             }
@@ -542,9 +547,10 @@ int or_irk_step_f(const or_sys* S, const double* u, const double* lift, const do
                 for (int k = i + 1; k < m; ++k) acc -= H[(long)k * (R + 1) + i] * y[k];
                 y[i] = acc / H[(long)i * (R + 1) + i];
             }
+            for (int i = 0; i < m; ++i) ys[i] = g_ortho == 1 ? y[i] * zs[i] : y[i];
             for (long k = 0; k < N; ++k) {
                 double t = x[k];
-                for (int i = 0; i < m; ++i) t = t + y[i] * Z[(long)i * N + k];
+                for (int i = 0; i < m; ++i) t = t + ys[i] * Z[(long)i * N + k];
                 x[k] = t;
             }
             or_stage_apply(S, x, ax);
@@ -584,6 +590,6 @@ int or_irk_step_f(const or_sys* S, const double* u, const double* lift, const do
         rep->seconds = (ts1.tv_sec - ts0.tv_sec) + 1e-9 * (ts1.tv_nsec - ts0.tv_nsec);
     }
     free(b); free(x); free(r); free(ax); free(V); free(Z); free(H); free(base);
-    free(g); free(cs); free(sn); free(h); free(cc); free(y);
+    free(g); free(cs); free(sn); free(h); free(cc); free(y); free(zs); free(ys);
     return 0;
 }

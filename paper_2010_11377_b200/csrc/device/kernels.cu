@@ -523,8 +523,10 @@ __device__ __forceinline__ bool elect_last(unsigned* counter) {
 // Thread t sums partials t, t+256, ... sequentially; then the warp tree and
 // the 8 warp results in order.  Called by the whole last CTA.
 __device__ void final_reduce(const double* part, int nch, int nv, double* red, double* out) {
-    // eight values per multi-value warp tree (same association per value)
-    for (int q0 = 0; q0 < nv; q0 += 8) {
+    // eight values per multi-value warp tree (same association per value);
+    // threads beyond the first kRedThreads (512-thread CTAs) only join barriers
+    const bool active = threadIdx.x < kRedThreads;
+    for (int q0 = 0; q0 < nv && active; q0 += 8) {
         double acc[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
@@ -538,7 +540,8 @@ __device__ void final_reduce(const double* part, int nch, int nv, double* red, d
         if ((threadIdx.x & 3) == 0 && q < nv) red[(threadIdx.x >> 5) * nv + q] = x;
     }
     __syncthreads();
-    for (int q = threadIdx.x; q < nv; q += kRedThreads) out[q] = warp_sum8(red, nv, q);
+    if (active)
+        for (int q = threadIdx.x; q < nv; q += kRedThreads) out[q] = warp_sum8(red, nv, q);
     __syncthreads();
 }
 
@@ -883,11 +886,18 @@ __device__ void dgs_dot_scalars(const GmresBufs& g, int j, int finalize, int nvv
     }
     const double pi = res[2 * nvv + 1];
     const double hjj = alpha > 0.0 ? (pi - sp) / alpha : 0.0;
+    const double inv = alpha > 0.0 ? 1.0 / alpha : 0.0;
+    // Column j describes w = A Z_j with Z_j = P^-1 vt_j, |vt_j| ~ alpha: it is
+    // stored divided by alpha (the column of the unit input), the next
+    // direction is stored divided by alpha too (k_dgs_update), and x += Z y
+    // uses y_j / alpha_j (zscale) -- so magnitudes stay O(1) and the
+    // breakdown test compares the same quantity as gmres.cpp:118.
     double* hcj = g.H + static_cast<long long>(j) * ld;
-    for (int i = 0; i < j; ++i) hcj[i] = res[nvv + i];
-    hcj[j] = hjj;
+    for (int i = 0; i < j; ++i) hcj[i] = res[nvv + i] * inv;
+    hcj[j] = hjj * inv;
+    ctl->zscale[j] = inv;
     ctl->hjj = hjj;
-    ctl->inv_alpha = alpha > 0.0 ? 1.0 / alpha : 0.0;
+    ctl->inv_alpha = inv;
     ctl->hnext = alpha;
     if (!(alpha == alpha)) ctl->bad = 1;
 }
@@ -1015,7 +1025,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_update(GmresBufs g) {
 #pragma unroll
     for (int q = 0; q < kRedPerThread; ++q) {
         a[q] = a[q] * inv;
-        b[q] = b[q] - hjj * a[q];
+        b[q] = (b[q] - hjj * a[q]) * inv;  // next direction in unit-input scale
     }
     store_chunk(ap, n, c, a);
     store_chunk(bp, n, c, b);
@@ -1174,7 +1184,8 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_xupdate(GmresBufs g, double*
     __shared__ double ys[kMaxRestart];
     const GmresCtl* c = g.ctl;
     const int m = c->m;
-    for (int i = threadIdx.x; i < m; i += kRedThreads) ys[i] = c->y[i];
+    for (int i = threadIdx.x; i < m; i += kRedThreads)
+        ys[i] = c->ortho == 1 ? c->y[i] * c->zscale[i] : c->y[i];
     __syncthreads();
     const long long stride = (g.sN + 63) / 64 * 64;
     double xv[kRedPerThread];

@@ -145,6 +145,7 @@ struct GmresCtl {
     double sv[kMaxRestart + 1];  // s_i = v_i . vt_j   (re-orthogonalisation of vt_j)
     double pv[kMaxRestart + 1];  // p_i = v_i . w      (projections of w)
     double hjj, inv_alpha;
+    double zscale[kMaxRestart];  // DCGS2: x += sum_j y_j zscale_j Z_j (1 for CGS2)
     int ortho;                   // 1 DCGS2, 0 CGS + conditional second pass
     int side;                    // 1 right (flexible Z basis), 0 left (gmres.cpp:41-46, 69-71)
     double hnorm;                // history / tolerance base: ||b|| (right), ||P^-1 b|| (left)

@@ -1,5 +1,5 @@
-"""Isolated timing of the DCGS2 block-dot at j=15 (17 vectors of sN) for the
-IRK_DGS_TMA variant in the environment; prints achieved GB/s."""
+"""Isolated timing of the DCGS2 block-dot at j=15 (17 vectors of sN) and of
+the CGS block-dot for comparison; prints achieved GB/s."""
 import ctypes as C
 import os
 import sys
@@ -18,4 +18,4 @@ for which, name in ((115, "CGS block-dot j=15"), (615, "DCGS2 block-dot j=15")):
     ms = C.c_double()
     _abi.check(L.irkdev_time_kernel(Pc._dev._h, which, 50, C.byref(ms)))
     b = 17 * 8 * 3 * n
-    print(f"IRK_DGS_TMA={os.environ.get('IRK_DGS_TMA', '0')} {name}: {1e3 * ms.value:.1f} us, {b / ms.value / 1e6:.0f} GB/s")
+    print(f"{name}: {1e3 * ms.value:.1f} us, {b / ms.value / 1e6:.0f} GB/s")
