@@ -158,16 +158,20 @@ __global__ void __launch_bounds__(256) k_spmv_sell(Mat A, SpmvArgs a) {
     __shared__ double s_tab[VF == kU8 ? 256 : 1];
     __shared__ double s_wd[1];
     const double* tab = load_tab<VF>(A, s_tab, s_wd);
-    pdl_wait();
     const int slice = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int nslices = (A.rows + 31) >> 5;
-    if (slice >= nslices) return;
+    if (slice >= nslices) {
+        pdl_wait();
+        return;
+    }
+    // the slice structure is static: read it before waiting on the predecessor
+    const int base = __ldg(A.sptr + slice);
+    const int len = (__ldg(A.sptr + slice + 1) - base) >> 5;
+    pdl_wait();
     const double* r = a.r.base ? a.r.get() : nullptr;
     const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
     const double* __restrict__ wd = a.wd;
-    const int base = __ldg(A.sptr + slice);
-    const int len = (__ldg(A.sptr + slice + 1) - base) >> 5;
     double s = 0.0;
 #pragma unroll 4
     for (int k = 0; k < len; ++k) {
@@ -191,20 +195,21 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
     __shared__ double s_tab[VF == kU8 ? 256 : 1];
     __shared__ double s_wd[1];
     const double* tab = load_tab<VF>(A, s_tab, s_wd);
-    pdl_wait();
     constexpr int MM = 4;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int row = t / G;
     const int lane = threadIdx.x % G;
     const bool live = row < A.rows;
-    const double* r = a.r.base ? a.r.get() : nullptr;
-    const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
-    const double* __restrict__ wd = a.wd;
+    // the row structure is static: read it before waiting on the predecessor
     const int lo = live ? __ldg(A.ptr + row) : 0;
     const int len = live ? __ldg(A.ptr + row + 1) - lo : 0;
     int chunks = (len + G * MM - 1) / (G * MM);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) chunks = max(chunks, __shfl_xor_sync(0xffffffffu, chunks, o));
+    pdl_wait();
+    const double* r = a.r.base ? a.r.get() : nullptr;
+    const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
+    const double* __restrict__ wd = a.wd;
     double s = 0.0;
     for (int ch = 0; ch < chunks; ++ch) {
         double p[MM];
@@ -368,11 +373,9 @@ __global__ void k_axpy(int n, double alpha, const double* __restrict__ x, VecRef
 __global__ void __launch_bounds__(256) k_dense_mv(int n, const double* __restrict__ A, VecRef rr,
                                                   VecRef zr) {
     pdl_trigger();
-    pdl_wait();
     extern __shared__ double sm[];
     double* sA = sm;
     double* sr = sm + static_cast<long long>(n) * n;
-    const double* r = rr.get();
     // batched fill: all of a thread's loads are issued before any store
     const int nn = n * n;
     for (int q0 = 0; q0 < nn; q0 += 8 * blockDim.x) {
@@ -388,6 +391,8 @@ __global__ void __launch_bounds__(256) k_dense_mv(int n, const double* __restric
             if (q < nn) sA[q] = t[u];
         }
     }
+    pdl_wait();  // the inverse is static: its fill overlaps the predecessor's tail
+    const double* r = rr.get();
     for (int q = threadIdx.x; q < n; q += blockDim.x) sr[q] = r[q];
     __syncthreads();
     double* z = zr.get();

@@ -96,8 +96,13 @@ constexpr double kRefGrad[3][2] = {{-1.0, -1.0}, {1.0, 0.0}, {0.0, 1.0}};
 // Visits every triangle in mesh order with its three vertex ids and coords.
 template <class F>
 void for_each_triangle(const Lattice& L, F&& f) {
+    // element e = 2 (j n + i) + t in the reference's (row, cell, triangle)
+    // order; cells are independent, so rows of cells run in parallel and each
+    // element writes only its own triplet slots (9 e .. 9 e + 8)
+#pragma omp parallel for schedule(static)
     for (int j = 0; j < L.n; ++j)
         for (int i = 0; i < L.n; ++i) {
+            const long long e0 = 2LL * (static_cast<long long>(j) * L.n + i);
             const int v00 = L.vid(i, j), v10 = L.vid(i + 1, j);
             const int v11 = L.vid(i + 1, j + 1), v01 = L.vid(i, j + 1);
             const double p00[2] = {L.x(i), L.x(j)}, p10[2] = {L.x(i + 1), L.x(j)};
@@ -105,12 +110,12 @@ void for_each_triangle(const Lattice& L, F&& f) {
             {
                 const int v[3] = {v00, v10, v11};
                 const double* p[3] = {p00, p10, p11};
-                f(v, p);
+                f(e0, v, p);
             }
             {
                 const int v[3] = {v00, v11, v01};
                 const double* p[3] = {p00, p11, p01};
-                f(v, p);
+                f(e0 + 1, v, p);
             }
         }
 }
@@ -176,9 +181,9 @@ Problem make_heat_problem(int cells) {
     const int nv = (cells + 1) * (cells + 1);
     const TriRule& q = duffy25();
     Triplets tm(nv, nv), tk(nv, nv);
-    tm.reserve(static_cast<std::size_t>(18) * cells * cells);
-    tk.reserve(static_cast<std::size_t>(18) * cells * cells);
-    for_each_triangle(L, [&](const int* v, const double* const* p) {
+    tm.resize(static_cast<std::size_t>(18) * cells * cells);
+    tk.resize(static_cast<std::size_t>(18) * cells * cells);
+    for_each_triangle(L, [&](long long e, const int* v, const double* const* p) {
         const Geometry g = geometry(p[0], p[1], p[2]);
         double gx[3], gy[3];
         for (int a = 0; a < 3; ++a) {
@@ -197,8 +202,8 @@ Problem make_heat_problem(int cells) {
         }
         for (int a = 0; a < 3; ++a)
             for (int b = 0; b < 3; ++b) {
-                tm.add(v[a], v[b], me[a][b]);
-                tk.add(v[a], v[b], ke[a][b]);
+                tm.set(9 * e + 3 * a + b, v[a], v[b], me[a][b]);
+                tk.set(9 * e + 3 * a + b, v[a], v[b], ke[a][b]);
             }
     });
     const Csr M = tm.compress(), K = tk.compress();
@@ -223,9 +228,9 @@ Problem make_double_glazing_problem(int cells, double eps) {
         w[1] = -2.0 * x * (1.0 - y * y);
     };
     Triplets tf(nv, nv), tm(nv, nv);
-    tf.reserve(static_cast<std::size_t>(18) * cells * cells);
-    tm.reserve(static_cast<std::size_t>(18) * cells * cells);
-    for_each_triangle(L, [&](const int* v, const double* const* p) {
+    tf.resize(static_cast<std::size_t>(18) * cells * cells);
+    tm.resize(static_cast<std::size_t>(18) * cells * cells);
+    for_each_triangle(L, [&](long long e, const int* v, const double* const* p) {
         const Geometry g = geometry(p[0], p[1], p[2]);
         auto edge = [](const double* a, const double* b) {
             return std::hypot(b[0] - a[0], b[1] - a[1]);
@@ -264,8 +269,8 @@ Problem make_double_glazing_problem(int cells, double eps) {
         }
         for (int a = 0; a < 3; ++a)
             for (int b = 0; b < 3; ++b) {
-                tf.add(v[a], v[b], fe[a][b]);
-                tm.add(v[a], v[b], me[a][b]);
+                tf.set(9 * e + 3 * a + b, v[a], v[b], fe[a][b]);
+                tm.set(9 * e + 3 * a + b, v[a], v[b], me[a][b]);
             }
     });
     const Csr F = tf.compress(), M = tm.compress();

@@ -1,6 +1,7 @@
 #include "sparse.hpp"
 
 #include <algorithm>
+#include <cstdint>
 #include <cmath>
 #include <numeric>
 
@@ -23,30 +24,40 @@ void Csr::validate() const {
 
 Csr Triplets::compress() const {
     const std::size_t nt = v_.size();
-    std::vector<std::size_t> perm(nt);
-    std::iota(perm.begin(), perm.end(), std::size_t{0});
-    std::sort(perm.begin(), perm.end(), [this](std::size_t a, std::size_t b) {
-        return r_[a] != r_[b] ? r_[a] < r_[b] : c_[a] < c_[b];
-    });
+    // The reference sorts an index permutation by (row, col) with std::sort
+    // (csr.cpp:55-62) and sums duplicates in the resulting order.  Sorting
+    // (key, value) pairs by key alone performs the same comparisons and
+    // moves, hence leaves the values in the same order -- with contiguous
+    // keys and a linear summation pass instead of indirect loads.
+    struct KV {
+        std::uint64_t key;
+        double v;
+    };
+    std::vector<KV> kv(nt);
+    for (std::size_t t = 0; t < nt; ++t) {
+        check(r_[t] >= 0 && r_[t] < rows_ && c_[t] >= 0 && c_[t] < cols_, "triplets: index out of range");
+        kv[t] = {(static_cast<std::uint64_t>(static_cast<std::uint32_t>(r_[t])) << 32) |
+                     static_cast<std::uint32_t>(c_[t]),
+                 v_[t]};
+    }
+    std::sort(kv.begin(), kv.end(), [](const KV& a, const KV& b) { return a.key < b.key; });
     Csr A;
     A.rows = rows_;
     A.cols = cols_;
     A.ptr.assign(rows_ + 1, 0);
     A.idx.reserve(nt);
     A.val.reserve(nt);
-    long last_r = -1, last_c = -1;
-    for (std::size_t t : perm) {
-        const int r = r_[t], c = c_[t];
-        check(r >= 0 && r < rows_ && c >= 0 && c < cols_, "triplets: index out of range");
-        if (r == last_r && c == last_c) {
-            A.val.back() += v_[t];
+    std::uint64_t last = ~std::uint64_t{0};
+    for (const KV& e : kv) {
+        if (e.key == last) {
+            A.val.back() += e.v;
             continue;
         }
+        const int r = static_cast<int>(e.key >> 32), c = static_cast<int>(e.key & 0xffffffffu);
         A.idx.push_back(c);
-        A.val.push_back(v_[t]);
+        A.val.push_back(e.v);
         ++A.ptr[r + 1];
-        last_r = r;
-        last_c = c;
+        last = e.key;
     }
     std::partial_sum(A.ptr.begin(), A.ptr.end(), A.ptr.begin());
     return A;

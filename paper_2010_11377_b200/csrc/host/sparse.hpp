@@ -62,6 +62,9 @@ public:
     Triplets(int rows, int cols) : rows_(rows), cols_(cols) {}
     void reserve(std::size_t n) { r_.reserve(n); c_.reserve(n); v_.reserve(n); }
     void add(int r, int c, double v) { r_.push_back(r); c_.push_back(c); v_.push_back(v); }
+    // fixed-slot filling (parallel assembly): the slot order is the add order
+    void resize(std::size_t n) { r_.resize(n); c_.resize(n); v_.resize(n); }
+    void set(std::size_t k, int r, int c, double v) { r_[k] = r; c_[k] = c; v_[k] = v; }
     Csr compress() const;
 
 private:

@@ -156,3 +156,21 @@ def test_c2_one_step_full_size():
         assert abs(g.report.iterations - r["iterations"]) <= 1
         assert rel_l2(g.K, r["K"]) <= 1e-9
         assert rel_l2(g.u_next, r["u_next"]) <= 1e-9
+
+
+@pytest.mark.parametrize("cells", [256, 512])
+def test_fused_coarse_levels_bitwise(cells):
+    """Deep hierarchies (5-6 levels, every coarse-level kernel shape and the
+    programmatic launches from level 2): V-cycles and a whole step stay
+    bit-identical."""
+    c = heat_case(cells, s=3, ht=1e-3)
+    assert all(h.n_levels() >= 5 for h in c.hiers)
+    rng = np.random.default_rng(cells)
+    for k in range(len(c.hiers)):
+        r = rng.standard_normal(c.n)
+        assert np.array_equal(c.device().vcycle(k, r), c.oracle.vcycle(k, r))
+    u = c.problem.initial(0.01, 2)
+    g = _step(c, u)
+    o = c.oracle.step(u, c.f_lift)
+    assert g.report.iterations == o["iterations"]
+    assert np.array_equal(g.K, o["K"])
