@@ -119,18 +119,33 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
     __shared__ double s_tab[VF == kU8 ? 256 : 1];
     __shared__ double s_wd[VF == kU8 ? 256 : 1];
     const double* tab = load_tab<VF>(A, s_tab, s_wd);
-    pdl_wait();
     const int n = A.rows;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double* r = a.r.base ? a.r.get() : nullptr;
-    const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
+    if (i >= n) {
+        pdl_wait();
+        return;
+    }
     const double* __restrict__ wd = a.wd;
     const unsigned char* dcode = nullptr;
     if constexpr (WDT == 1)
         dcode = static_cast<const unsigned char*>(A.val) + static_cast<long long>(A.diag0) * A.dstride;
     const int nd = ND > 0 ? ND : A.nd;
     const double* wdt = A.tab_smem ? s_wd : A.wdtab;
+    // fixed diagonal count, u8 values: the row's codes are static, so they are
+    // loaded before waiting on the predecessor (decoded after it, together
+    // with the dependent x loads -- one memory round trip after the wait)
+    constexpr bool kPre = ND > 0 && VF == kU8;
+    unsigned cd[kPre ? ND : 1], cw[kPre ? ND : 1];
+    if constexpr (kPre) {
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+            cd[d] = __ldg(static_cast<const unsigned char*>(A.val) + static_cast<long long>(d) * A.dstride + i);
+            if constexpr (XM == kXWdR && WDT == 1) cw[d] = __ldg(dcode + min(max(i + A.off[d], 0), n - 1));
+        }
+    }
+    pdl_wait();
+    const double* r = a.r.base ? a.r.get() : nullptr;
+    const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
     double s = 0.0;
 #pragma unroll
     for (int d = 0; d < (ND > 0 ? ND : kMaxDiags); ++d) {
@@ -138,12 +153,21 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
         const int c = min(max(i + A.off[d], 0), n - 1);
         double xv;
         if constexpr (XM == kXWdR) {
-            const double wdc = WDT == 1 ? wdt[__ldg(dcode + c)] : wd[c];
+            double wdc;
+            if constexpr (kPre && WDT == 1)
+                wdc = wdt[cw[d]];
+            else
+                wdc = WDT == 1 ? wdt[__ldg(dcode + c)] : wd[c];
             xv = wdc * r[c];
         } else {
             xv = x[c];
         }
-        s += vfetch<VF>(A.val, static_cast<long long>(d) * A.dstride + i, tab) * xv;
+        double v;
+        if constexpr (kPre)
+            v = tab[cd[d]];
+        else
+            v = vfetch<VF>(A.val, static_cast<long long>(d) * A.dstride + i, tab);
+        s += v * xv;
     }
     double wdi = 0.0;
     if (EPI == kESmooth || (EPI == kEProlong && !a.zb))

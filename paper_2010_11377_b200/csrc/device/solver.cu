@@ -377,9 +377,10 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
     const int pre = H.prm.pre_sweeps, post = H.prm.post_sweeps;
     // `first` > 0 runs only the part of the cycle below level `first` (timing)
     auto rhs_of = [&](int l) { return l == first ? r0 : dev::plain(H.lv[l].r); };
-    // programmatic launches for the latency-bound levels >= 2 (IRK_PDL_COARSE=0 off)
+    // programmatic launches for the latency-bound levels >= 2
+    // (IRK_PDL_COARSE=<level> moves the threshold, -1 turns it off)
     static const int pdl_from = std::getenv("IRK_PDL_COARSE") ? std::atoi(std::getenv("IRK_PDL_COARSE")) : 2;
-    auto scope = [&](int l) { dev::set_pdl_scope(pdl_from > 0 && l >= pdl_from); };
+    auto scope = [&](int l) { dev::set_pdl_scope(pdl_from >= 0 && l >= pdl_from); };
     auto out_of = [&](int l) { return l == first ? z0 : dev::plain(H.lv[l].z); };
     for (int l = first; l + 1 < L; ++l) {
         DevLevel& d = H.lv[l];

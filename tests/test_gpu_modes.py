@@ -7,7 +7,8 @@ The switches are read once per process, so each mode runs in a subprocess:
   * IRK_NO_VALUE_CODES=1, IRK_SPARSE_FMT=0/2 -- fp64 values, all-SELL /
                            all-CSR-vector sparse formats;
   * IRK_PDL=1           -- programmatic dependent launch for every kernel;
-  * IRK_PDL_COARSE=0    -- no programmatic launch on AMG levels >= 2 (default on);
+  * IRK_PDL_COARSE=-1/0 -- programmatic launches on no / every AMG level
+                           (default: levels >= 2);
   * IRK_SERIAL_JACOBI=1 -- block-Jacobi V-cycles in stage order on one stream
                            instead of one graph branch per hierarchy;
   * IRK_CODES_MIN_ROWS=0 -- value dictionaries on every operator (the
@@ -54,6 +55,7 @@ print("MODE-OK")
     ({"IRK_SPARSE_FMT": "0"}, "dcgs2"),
     ({"IRK_SPARSE_FMT": "2"}, "dcgs2"),
     ({"IRK_PDL": "1"}, "dcgs2"),
+    ({"IRK_PDL_COARSE": "-1"}, "dcgs2"),
     ({"IRK_PDL_COARSE": "0"}, "dcgs2"),
     ({"IRK_SERIAL_JACOBI": "1"}, "dcgs2"),
     ({"IRK_CODES_MIN_ROWS": "0"}, "dcgs2"),
