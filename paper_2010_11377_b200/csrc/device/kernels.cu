@@ -993,16 +993,22 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot(GmresBufs g, int fin
         for (; i + 2 <= nvv; i += 2) dgs_batch<2, false>(g.V, stride, n, c, i, b, b, red, nv, nvv);
         if (i < nvv) dgs_batch<1, false>(g.V, stride, n, c, i, b, b, red, nv, nvv);
     } else {
-        double a[kRedPerThread];
+        // v_{i+1} is loaded as soon as v_i's local sums are formed, so its
+        // latency overlaps v_i's warp trees (same trees and values as before)
+        double a[kRedPerThread], v[kRedPerThread];
         load_chunk(g.V + static_cast<long long>(j) * stride, n, c, a);
+        if (nvv > 0) load_chunk(g.V, n, c, v);
         {
             double d[2] = {chunk_dot_local(a, a), chunk_dot_local(a, b)};
             const double x = warp_tree_multi<2>(d);
             warp_multi_store<2>(x, red, nv, [&](int q) { return 2 * nvv + q; });
         }
-        for (; i + kDgsBatch <= nvv; i += kDgsBatch)
-            dgs_batch<kDgsBatch, true>(g.V, stride, n, c, i, a, b, red, nv, nvv);
-        for (; i < nvv; ++i) dgs_batch<1, true>(g.V, stride, n, c, i, a, b, red, nv, nvv);
+        for (i = 0; i < nvv; ++i) {
+            double d[2] = {chunk_dot_local(v, a), chunk_dot_local(v, b)};
+            if (i + 1 < nvv) load_chunk(g.V + static_cast<long long>(i + 1) * stride, n, c, v);
+            const double x = warp_tree_multi<2>(d);
+            warp_multi_store<2>(x, red, nv, [&](int q) { return q ? nvv + i : i; });
+        }
     }
     __syncthreads();
     for (int q = threadIdx.x; q < nv; q += kRedThreads)
