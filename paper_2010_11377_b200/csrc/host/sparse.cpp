@@ -5,6 +5,8 @@
 #include <cmath>
 #include <numeric>
 
+#include <omp.h>
+
 namespace irkb {
 
 void Csr::validate() const {
@@ -63,6 +65,9 @@ Csr Triplets::compress() const {
     return A;
 }
 
+// Threads take contiguous row blocks; per-thread column counts give every
+// (column, thread) pair its slot range, so entries land in row order inside
+// each column exactly as in the sequential counting sort.
 Csr transpose(const Csr& A) {
     Csr T;
     T.rows = A.cols;
@@ -70,79 +75,140 @@ Csr transpose(const Csr& A) {
     T.ptr.assign(T.rows + 1, 0);
     T.idx.resize(A.idx.size());
     T.val.resize(A.val.size());
-    for (int c : A.idx) ++T.ptr[c + 1];
-    std::partial_sum(T.ptr.begin(), T.ptr.end(), T.ptr.begin());
-    std::vector<int> fill(T.ptr.begin(), T.ptr.end() - 1);
-    for (int i = 0; i < A.rows; ++i)
-        for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
-            const int at = fill[A.idx[k]]++;
-            T.idx[at] = i;
-            T.val[at] = A.val[k];
+    const int nt = A.idx.size() >= (1u << 16) ? omp_get_max_threads() : 1;
+    std::vector<std::vector<int>> cnt(nt);
+#pragma omp parallel num_threads(nt)
+    {
+        const int t = omp_get_thread_num();
+        const int lo = static_cast<int>(static_cast<long long>(A.rows) * t / nt);
+        const int hi = static_cast<int>(static_cast<long long>(A.rows) * (t + 1) / nt);
+        std::vector<int>& c = cnt[t];
+        c.assign(A.cols, 0);
+        for (int k = A.ptr[lo]; k < A.ptr[hi]; ++k) ++c[A.idx[k]];
+#pragma omp barrier
+#pragma omp single
+        {
+            int run = 0;
+            for (int col = 0; col < A.cols; ++col) {
+                T.ptr[col] = run;
+                for (int u = 0; u < nt; ++u) {
+                    const int m = cnt[u][col];
+                    cnt[u][col] = run;  // this thread's first slot in the column
+                    run += m;
+                }
+            }
+            T.ptr[A.cols] = run;
         }
+        for (int i = lo; i < hi; ++i)
+            for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+                const int at = c[A.idx[k]]++;
+                T.idx[at] = i;
+                T.val[at] = A.val[k];
+            }
+    }
     return T;
 }
 
+// alpha*A + beta*B over the union pattern: row counts, prefix sum, then every
+// row merged independently (same expressions as the sequential merge).
 Csr add(double alpha, const Csr& A, double beta, const Csr& B) {
     check(A.rows == B.rows && A.cols == B.cols, "csr add: shape mismatch");
     Csr C;
     C.rows = A.rows;
     C.cols = A.cols;
-    C.ptr.resize(A.rows + 1);
-    C.ptr[0] = 0;
-    C.idx.reserve(std::max(A.idx.size(), B.idx.size()));
-    C.val.reserve(C.idx.capacity());
-    for (int i = 0; i < A.rows; ++i) {
-        int a = A.ptr[i], b = B.ptr[i];
+    C.ptr.assign(A.rows + 1, 0);
+    auto merge = [&](int i, int* oi, double* ov) {
+        int a = A.ptr[i], b = B.ptr[i], m = 0;
         const int ae = A.ptr[i + 1], be = B.ptr[i + 1];
         while (a < ae || b < be) {
             const int ca = a < ae ? A.idx[a] : INT32_MAX;
             const int cb = b < be ? B.idx[b] : INT32_MAX;
             if (ca == cb) {
-                C.idx.push_back(ca);
-                C.val.push_back(alpha * A.val[a++] + beta * B.val[b++]);
+                if (oi) {
+                    oi[m] = ca;
+                    ov[m] = alpha * A.val[a] + beta * B.val[b];
+                }
+                ++a;
+                ++b;
             } else if (ca < cb) {
-                C.idx.push_back(ca);
-                C.val.push_back(alpha * A.val[a++]);
+                if (oi) {
+                    oi[m] = ca;
+                    ov[m] = alpha * A.val[a];
+                }
+                ++a;
             } else {
-                C.idx.push_back(cb);
-                C.val.push_back(beta * B.val[b++]);
+                if (oi) {
+                    oi[m] = cb;
+                    ov[m] = beta * B.val[b];
+                }
+                ++b;
             }
+            ++m;
         }
-        C.ptr[i + 1] = static_cast<int>(C.idx.size());
-    }
+        return m;
+    };
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < A.rows; ++i) C.ptr[i + 1] = merge(i, nullptr, nullptr);
+    std::partial_sum(C.ptr.begin(), C.ptr.end(), C.ptr.begin());
+    C.idx.resize(C.ptr.back());
+    C.val.resize(C.ptr.back());
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < A.rows; ++i) merge(i, C.idx.data() + C.ptr[i], C.val.data() + C.ptr[i]);
     return C;
 }
 
+// Row-wise Gustavson product.  Rows are independent, so contiguous row blocks
+// run on OpenMP threads with private accumulators and are concatenated in row
+// order: every entry is accumulated exactly as in the sequential loop (k
+// ascending), so the result is bit-identical for any thread count.
 Csr matmul(const Csr& A, const Csr& B) {
     check(A.cols == B.rows, "csr matmul: shape mismatch");
     Csr C;
     C.rows = A.rows;
     C.cols = B.cols;
     C.ptr.assign(A.rows + 1, 0);
-    std::vector<double> acc(B.cols, 0.0);
-    std::vector<int> seen(B.cols, -1);
-    std::vector<int> touched;
-    for (int i = 0; i < A.rows; ++i) {
-        touched.clear();
-        for (int ka = A.ptr[i]; ka < A.ptr[i + 1]; ++ka) {
-            const int j = A.idx[ka];
-            const double a = A.val[ka];
-            for (int kb = B.ptr[j]; kb < B.ptr[j + 1]; ++kb) {
-                const int c = B.idx[kb];
-                if (seen[c] != i) {
-                    seen[c] = i;
-                    acc[c] = 0.0;
-                    touched.push_back(c);
+    const int nt = A.rows >= 4096 ? omp_get_max_threads() : 1;
+    std::vector<std::vector<int>> bidx(nt);
+    std::vector<std::vector<double>> bval(nt);
+#pragma omp parallel num_threads(nt)
+    {
+        const int t = omp_get_thread_num();
+        const int lo = static_cast<int>(static_cast<long long>(A.rows) * t / nt);
+        const int hi = static_cast<int>(static_cast<long long>(A.rows) * (t + 1) / nt);
+        std::vector<double> acc(B.cols, 0.0);
+        std::vector<int> seen(B.cols, -1);
+        std::vector<int> touched;
+        std::vector<int>& oi = bidx[t];
+        std::vector<double>& ov = bval[t];
+        for (int i = lo; i < hi; ++i) {
+            touched.clear();
+            for (int ka = A.ptr[i]; ka < A.ptr[i + 1]; ++ka) {
+                const int j = A.idx[ka];
+                const double a = A.val[ka];
+                for (int kb = B.ptr[j]; kb < B.ptr[j + 1]; ++kb) {
+                    const int c = B.idx[kb];
+                    if (seen[c] != i) {
+                        seen[c] = i;
+                        acc[c] = 0.0;
+                        touched.push_back(c);
+                    }
+                    acc[c] += a * B.val[kb];
                 }
-                acc[c] += a * B.val[kb];
             }
+            std::sort(touched.begin(), touched.end());
+            for (int c : touched) {
+                oi.push_back(c);
+                ov.push_back(acc[c]);
+            }
+            C.ptr[i + 1] = static_cast<int>(touched.size());
         }
-        std::sort(touched.begin(), touched.end());
-        for (int c : touched) {
-            C.idx.push_back(c);
-            C.val.push_back(acc[c]);
-        }
-        C.ptr[i + 1] = static_cast<int>(C.idx.size());
+    }
+    std::partial_sum(C.ptr.begin(), C.ptr.end(), C.ptr.begin());
+    C.idx.reserve(C.ptr.back());
+    C.val.reserve(C.ptr.back());
+    for (int t = 0; t < nt; ++t) {
+        C.idx.insert(C.idx.end(), bidx[t].begin(), bidx[t].end());
+        C.val.insert(C.val.end(), bval[t].begin(), bval[t].end());
     }
     return C;
 }
