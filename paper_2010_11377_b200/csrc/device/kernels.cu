@@ -227,9 +227,10 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
     // the row structure is static: read it before waiting on the predecessor
     const int lo = live ? __ldg(A.ptr + row) : 0;
     const int len = live ? __ldg(A.ptr + row + 1) - lo : 0;
-    int chunks = (len + G * MM - 1) / (G * MM);
+    int maxlen = len;  // longest row of the warp: bounds the shuffles
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) chunks = max(chunks, __shfl_xor_sync(0xffffffffu, chunks, o));
+    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    const int chunks = (maxlen + G * MM - 1) / (G * MM);
     pdl_wait();
     const double* r = a.r.base ? a.r.get() : nullptr;
     const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
@@ -248,12 +249,14 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
             }
         }
 #pragma unroll
-        for (int m = 0; m < MM; ++m)
+        for (int m = 0; m < MM; ++m) {
+            if (ch * G * MM + m * G >= maxlen) break;  // warp-uniform
 #pragma unroll
             for (int l = 0; l < G; ++l) {
                 const double v = __shfl_sync(0xffffffffu, p[m], l, G);
                 if (ch * G * MM + m * G + l < len) s += v;
             }
+        }
     }
     if (!live || lane != 0) return;
     double wdi = 0.0;

@@ -201,8 +201,10 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
     // per row; small coarse operators need lanes per row to expose
     // memory-level parallelism.)
     if ((force < 0 && avg > 4.5 && (A.rows < 65536 || avg > 24.0)) || force == dev::kCsrVec) {
+        static const double per_lane =
+            std::getenv("IRK_CSRV_PER_LANE") ? std::atof(std::getenv("IRK_CSRV_PER_LANE")) : 3.0;
         int g = 2;
-        while (g < 32 && 3 * g < avg) g *= 2;
+        while (g < 32 && per_lane * g < avg) g *= 2;
         m.fmt = dev::kCsrVec;
         m.lanes = g;
         m.ptr = upload_array(A.ptr);
