@@ -12,7 +12,9 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libirkdev.so"
+# IRK_LIB selects another build of the same ABI (A/B timing of two builds on
+# one box, tools/ab.sh); the product default is the in-tree library.
+LIB_PATH = Path(os.environ.get("IRK_LIB") or Path(__file__).resolve().parent / "lib" / "libirkdev.so")
 HEADER = Path(__file__).resolve().parent.parent / "include" / "irkdev.h"
 
 IRK_OK, IRK_EINVAL, IRK_ESINGULAR, IRK_ENUMERICAL, IRK_ECUDA, IRK_EUNSUPPORTED = 0, 1, 2, 3, 4, 5

@@ -119,7 +119,7 @@ void DeviceSolver::upload_values(dev::Mat& m, const std::vector<double>& vals, d
     // Small operators keep fp64 values: their kernels are latency-bound and a
     // dictionary lookup is one more dependent memory trip.
     static const long long min_rows =
-        std::getenv("IRK_CODES_MIN_ROWS") ? std::atoll(std::getenv("IRK_CODES_MIN_ROWS")) : 500000;
+        std::getenv("IRK_CODES_MIN_ROWS") ? std::atoll(std::getenv("IRK_CODES_MIN_ROWS")) : 100000;
     const bool small = std::max(m.rows, m.cols) < min_rows;
     Dict d = compress_values_ && !small ? encode(vals) : Dict{};
     m.vf = d.vf;
