@@ -98,6 +98,11 @@ int irk_custom_coeff(int s, const double* Atilde, int* structure);
 typedef struct irk_hierarchy irk_hierarchy;
 /* amg_setup (amg.hpp:52): the reference's smoothed-aggregation coarsening. */
 int irk_amg_setup(const irk_csr* A, const irk_amg_params* p, irk_hierarchy** out);
+/* amg_setup on the GPU `device` (amg.cpp:172-227): strength
+ * graph, rho estimate, prolongator smoothing, R = P^T and the Galerkin
+ * products run on the device, the greedy aggregation passes on the host.
+ * Bit-identical to irk_amg_setup; IRK_ECUDA without a GPU (no fallback). */
+int irk_amg_setup_device(const irk_csr* A, const irk_amg_params* p, int device, irk_hierarchy** out);
 int irk_hierarchy_levels(const irk_hierarchy* h);
 /* which: 0 A, 1 P, 2 R (amg.hpp:35-40). */
 int irk_hierarchy_level(const irk_hierarchy* h, int level, int which, irk_csr* out);

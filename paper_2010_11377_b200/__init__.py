@@ -42,7 +42,7 @@ __all__ = [
     "AmgParams", "AmgHierarchy", "GmresConfig", "SolveReport", "IrkStepResult",
     "LinearParabolicSystem", "ProblemSetup", "BlockPreconditioner", "StageOperator",
     "make_radau_iia", "make_lobatto_iiic", "make_table", "ldu_factorize", "precond_coeff",
-    "custom_coeff", "amg_setup", "make_heat_setup", "make_double_glazing_setup", "irk_step",
+    "custom_coeff", "amg_setup", "amg_setup_device", "make_heat_setup", "make_double_glazing_setup", "irk_step",
     "integrate", "SingularError", "NumericalError", "CudaError", "Unsupported",
 ]
 
@@ -213,6 +213,16 @@ def amg_setup(A: CsrMatrix, params: AmgParams | None = None) -> AmgHierarchy:
     h = C.c_void_p()
     v = A.view()
     check(_abi.lib().irk_amg_setup(C.byref(v), C.byref((params or AmgParams()).c()), C.byref(h)))
+    return AmgHierarchy(h)
+
+
+def amg_setup_device(A: CsrMatrix, params: AmgParams | None = None, device: int = 0) -> AmgHierarchy:
+    """amg_setup (amg.cpp:172-227) with the sparse algebra on GPU `device`
+    (SURVEY §8 f2); bit-identical to ``amg_setup``.  Raises without a GPU."""
+    h = C.c_void_p()
+    v = A.view()
+    check(_abi.lib().irk_amg_setup_device(C.byref(v), C.byref((params or AmgParams()).c()), int(device),
+                                          C.byref(h)))
     return AmgHierarchy(h)
 
 

@@ -67,6 +67,7 @@ _SIGS = {
     "irk_precond_coeff": (C.c_int, [C.c_int, C.c_int, C.c_int, dptr, iptr]),
     "irk_custom_coeff": (C.c_int, [C.c_int, dptr, iptr]),
     "irk_amg_setup": (C.c_int, [C.POINTER(irk_csr), C.POINTER(irk_amg_params), C.POINTER(V)]),
+    "irk_amg_setup_device": (C.c_int, [C.POINTER(irk_csr), C.POINTER(irk_amg_params), C.c_int, C.POINTER(V)]),
     "irk_hierarchy_levels": (C.c_int, [V]),
     "irk_hierarchy_level": (C.c_int, [V, C.c_int, C.c_int, C.POINTER(irk_csr)]),
     "irk_hierarchy_inv_diag": (dptr, [V, C.c_int]),

@@ -6,6 +6,7 @@
 #include <string>
 
 #include "../../include/irkdev.h"
+#include "device/amg_device.hpp"
 #include "device/solver.hpp"
 #include "host/mmio.hpp"
 #include "host/setup.hpp"
@@ -240,6 +241,10 @@ int irk_custom_coeff(int s, const double* Atilde, int* structure) {
 
 int irk_amg_setup(const irk_csr* A, const irk_amg_params* p, irk_hierarchy** out) {
     return guard([&] { *out = new irk_hierarchy{irkb::amg_setup(to_csr(A), to_params(p))}; });
+}
+
+int irk_amg_setup_device(const irk_csr* A, const irk_amg_params* p, int device, irk_hierarchy** out) {
+    return guard([&] { *out = new irk_hierarchy{irkb::amg_setup_device(to_csr(A), to_params(p), device)}; });
 }
 
 int irk_hierarchy_levels(const irk_hierarchy* h) { return h->h.n_levels(); }

@@ -5,13 +5,17 @@
 // read the iteration index from the device control block, which keeps the
 // captured iteration body iteration-invariant.
 #include <algorithm>
+#include <atomic>
+#include <unordered_set>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
 
+#include "amg_device.hpp"
 #include "solver.hpp"
 
 namespace irkb {
@@ -82,9 +86,29 @@ struct Dict {
 
 Dict encode(const std::vector<double>& v) {
     Dict d;
+    const long long n = static_cast<long long>(v.size());
     std::vector<uint64_t> bits(v.size());
     std::memcpy(bits.data(), v.data(), v.size() * sizeof(double));
-    std::vector<uint64_t> u = bits;
+    // distinct bit patterns (thread-local sets, giving up past 65,536)
+    std::vector<uint64_t> u;
+    std::atomic<bool> too_many{false};
+#pragma omp parallel
+    {
+        std::unordered_set<uint64_t> loc;
+        uint64_t last = 0;
+        bool have = false;
+#pragma omp for schedule(static)
+        for (long long i = 0; i < n; ++i) {
+            if ((have && bits[i] == last) || too_many.load(std::memory_order_relaxed)) continue;
+            loc.insert(bits[i]);
+            last = bits[i];
+            have = true;
+            if (loc.size() > 65536) too_many.store(true, std::memory_order_relaxed);
+        }
+#pragma omp critical
+        u.insert(u.end(), loc.begin(), loc.end());
+    }
+    if (too_many.load()) return d;
     std::sort(u.begin(), u.end());
     u.erase(std::unique(u.begin(), u.end()), u.end());
     if (u.size() > 65536) return d;
@@ -96,11 +120,13 @@ Dict encode(const std::vector<double>& v) {
     if (u.size() <= 256) {
         d.vf = dev::kU8;
         d.c8.resize(v.size());
-        for (size_t i = 0; i < v.size(); ++i) d.c8[i] = static_cast<unsigned char>(code(bits[i]));
+#pragma omp parallel for schedule(static)
+        for (long long i = 0; i < n; ++i) d.c8[i] = static_cast<unsigned char>(code(bits[i]));
     } else {
         d.vf = dev::kU16;
         d.c16.resize(v.size());
-        for (size_t i = 0; i < v.size(); ++i) d.c16[i] = static_cast<unsigned short>(code(bits[i]));
+#pragma omp parallel for schedule(static)
+        for (long long i = 0; i < n; ++i) d.c16[i] = static_cast<unsigned short>(code(bits[i]));
     }
     return d;
 }
@@ -282,13 +308,23 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
     std::vector<double> distinct;
     distinct_diagonals(s, At, sob_, distinct);
     if (hiers.empty()) {
-        for (double d : distinct) hiers.push_back(amg_setup(add(1.0, M, ht * d, K), amg));
+        // device setup (bit-identical; IRK_HOST_AMG_SETUP=1 selects the host one)
+        static const bool host_setup = std::getenv("IRK_HOST_AMG_SETUP") != nullptr;
+        for (double d : distinct)
+            hiers.push_back(host_setup ? amg_setup(add(1.0, M, ht * d, K), amg)
+                                       : amg_setup_device(add(1.0, M, ht * d, K), amg, device));
     }
     check(hiers.size() == distinct.size(), "device solver: hierarchy count mismatch");
+    static const bool timing = std::getenv("IRK_SETUP_TIMING") != nullptr;
+    auto lap = [&](const char* what) {
+        if (timing) std::fprintf(stderr, "solver setup %-14s %8.1f ms\n", what, 1e3 * seconds_since(t0));
+    };
+    lap("hierarchies");
     hier_host_ = std::move(hiers);
 
     M_ = upload(M, true, 0.0);
     K_ = upload(K, true, 0.0);
+    lap("M, K");
     fused_op_ = M_.fmt == dev::kDia && K_.fmt == dev::kDia && M_.nd == K_.nd &&
                 std::equal(M_.off, M_.off + M_.nd, K_.off) && M_.vf == K_.vf &&
                 (M_.vf == dev::kF64 || M_.vf == dev::kU8);
@@ -329,6 +365,7 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
         IRK_CUDA_CHECK(cudaMemcpy(dh.cinv, h.coarse_inverse.data(),
                                   sizeof(double) * dh.nc * dh.nc, cudaMemcpyHostToDevice));
         hier_.push_back(std::move(dh));
+        lap("hierarchy up");
     }
 
     rhs_ = alloc(n_);

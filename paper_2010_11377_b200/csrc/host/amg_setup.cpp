@@ -101,7 +101,9 @@ double spectral_radius(const Csr& A, const std::vector<double>& dinv) {
     return std::max(rho, 1e-12);
 }
 
-std::vector<double> dense_inverse(const Csr& A) {
+}  // namespace
+
+std::vector<double> dense_inverse_host(const Csr& A) {
     const int n = A.rows;
     std::vector<double> M(static_cast<std::size_t>(n) * n, 0.0), X(M.size(), 0.0);
     for (int i = 0; i < n; ++i) {
@@ -137,8 +139,6 @@ std::vector<double> dense_inverse(const Csr& A) {
     }
     return X;
 }
-
-}  // namespace
 
 Hierarchy amg_setup(const Csr& A, const AmgParams& p) {
     check(A.rows == A.cols, "amg_setup: matrix must be square");
@@ -181,7 +181,7 @@ Hierarchy amg_setup(const Csr& A, const AmgParams& p) {
         std::vector<double> dinv = inverse_diagonal(Ac);
         h.levels.push_back({std::move(Ac), std::move(dinv), {}, {}});
     }
-    h.coarse_inverse = dense_inverse(h.levels.back().A);
+    h.coarse_inverse = dense_inverse_host(h.levels.back().A);
     return h;
 }
 

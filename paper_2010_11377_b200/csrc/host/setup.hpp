@@ -90,6 +90,8 @@ struct Hierarchy {
 };
 
 Hierarchy amg_setup(const Csr& A, const AmgParams& p);
+// Dense inverse of the coarsest operator (Gauss-Jordan, partial pivoting).
+std::vector<double> dense_inverse_host(const Csr& A);
 
 // Distinct diagonal coefficients by exact equality (stage.cpp:85-97):
 // block j uses hierarchy solver_of_block[j], built for distinct[k].
