@@ -556,16 +556,29 @@ __device__ __forceinline__ bool elect_last(unsigned* counter) {
 // the 8 warp results in order.  Called by the whole last CTA.
 __device__ void final_reduce(const double* part, int nch, int nv, double* red, double* out) {
     // eight values per multi-value warp tree (same association per value);
-    // threads beyond the first kRedThreads (512-thread CTAs) only join barriers
+    // threads beyond the first kRedThreads (512-thread CTAs) only join barriers.
+    // Each thread issues the loads of 4 partials of all 8 values before adding
+    // any of them (same sequential order per value, 32 loads in flight).
     const bool active = threadIdx.x < kRedThreads;
+    constexpr int kU = 4;
     for (int q0 = 0; q0 < nv && active; q0 += 8) {
         double acc[8];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            acc[r] = 0.0;
-            if (q0 + r < nv)
-                for (int p = threadIdx.x; p < nch; p += kRedThreads)
-                    acc[r] += __ldcg(part + static_cast<long long>(q0 + r) * nch + p);
+        for (int r = 0; r < 8; ++r) acc[r] = 0.0;
+        for (int p0 = threadIdx.x; p0 < nch; p0 += kU * kRedThreads) {
+            double x[8][kU];
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const int p = p0 + u * kRedThreads;
+                    x[r][u] = (q0 + r < nv && p < nch) ? __ldcg(part + static_cast<long long>(q0 + r) * nch + p) : 0.0;
+                }
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+#pragma unroll
+                for (int u = 0; u < kU; ++u)
+                    if (p0 + u * kRedThreads < nch) acc[r] += x[r][u];
         }
         const double x = warp_tree_multi<8>(acc);
         const int q = q0 + (threadIdx.x & 31) / 4;
@@ -822,6 +835,29 @@ __device__ void givens_column(GmresCtl* c, double* col, int j) {
     c->g[j] = cs * c->g[j];
 }
 
+// givens_column on staged copies: cs, sn (rotations 0..j-1, shared memory),
+// col (shared memory); new rotation -> cs[j], sn[j]; g0 = g[j] in, (g[j], g[j+1]) out.
+__device__ __forceinline__ void givens_column_s(double* cs, double* sn, double* col, int j, double& gj,
+                                                double& gj1) {
+    for (int i = 0; i < j; ++i) {
+        const double t = cs[i] * col[i] + sn[i] * col[i + 1];
+        col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
+        col[i] = t;
+    }
+    const double denom = hyp(col[j], col[j + 1]);
+    double c = 1.0, s = 0.0;
+    if (denom > 0.0) {
+        c = col[j] / denom;
+        s = col[j + 1] / denom;
+    }
+    cs[j] = c;
+    sn[j] = s;
+    col[j] = denom;
+    col[j + 1] = 0.0;
+    gj1 = -s * gj;
+    gj = c * gj;
+}
+
 // Records the residual estimate of a just-finalised column (history, total).
 __device__ void record_column(const GmresBufs& g, int col_index) {
     GmresCtl* c = g.ctl;
@@ -833,32 +869,45 @@ __device__ void record_column(const GmresBufs& g, int col_index) {
 }
 
 // Provisional stop test after the DCGS2 update of iteration j: column j with
-// h_{j+1,j} = ||w'|| (rotations applied to a copy, not stored).
+// h_{j+1,j} = ||w'|| (rotations applied to a copy, not stored).  Called by the
+// whole last CTA: the column and the rotations are staged in shared memory
+// `sm` (3 (j + 2) doubles), thread 0 does the arithmetic.
 template <bool COND>
-__device__ void dgs_stop_test(const GmresBufs& g, int j, double wn) {
+__device__ void dgs_stop_test(const GmresBufs& g, int j, double wn, double* sm) {
     GmresCtl* ctl = g.ctl;
     const int ld = ctl->restart + 1;
     const double* hcj = g.H + static_cast<long long>(j) * ld;
-    double* col = ctl->hcol;
-    for (int i = 0; i <= j; ++i) col[i] = hcj[i];
+    double* col = sm;
+    double* cs = col + (j + 2);
+    double* sn = cs + (j + 1);
+    for (int i = threadIdx.x; i <= j; i += blockDim.x) {
+        col[i] = __ldcg(hcj + i);
+        if (i < j) {
+            cs[i] = ctl->cs[i];
+            sn[i] = ctl->sn[i];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const double beta = ctl->beta, tol_c = ctl->tol_c, alpha = ctl->hnext, gjv = ctl->g[j];
+    const int bad0 = ctl->bad, budget = ctl->budget;
     col[j + 1] = wn;
     for (int i = 0; i < j; ++i) {
-        const double t = ctl->cs[i] * col[i] + ctl->sn[i] * col[i + 1];
-        col[i + 1] = -ctl->sn[i] * col[i] + ctl->cs[i] * col[i + 1];
+        const double t = cs[i] * col[i] + sn[i] * col[i + 1];
+        col[i + 1] = -sn[i] * col[i] + cs[i] * col[i + 1];
         col[i] = t;
     }
     const double denom = hyp(col[j], col[j + 1]);
     const double sv = denom > 0.0 ? col[j + 1] / denom : 0.0;
-    const double gn = -sv * ctl->g[j];
-    const double res_prov = fabs(gn) / ctl->beta;
-    const double alpha = ctl->hnext;
-    const int bad = !(res_prov == res_prov) || !(wn == wn) || !(alpha == alpha) || ctl->bad;
+    const double gn = -sv * gjv;
+    const double res_prov = fabs(gn) / beta;
+    const int bad = !(res_prov == res_prov) || !(wn == wn) || !(alpha == alpha) || bad0;
     int stop;
-    if (res_prov <= ctl->tol_c)
+    if (res_prov <= tol_c)
         stop = 1;
-    else if (wn <= 1e-14 * ctl->beta || bad || alpha == 0.0)
+    else if (wn <= 1e-14 * beta || bad || alpha == 0.0)
         stop = 2;
-    else if (j + 1 >= ctl->budget)
+    else if (j + 1 >= budget)
         stop = 3;
     else
         stop = 0;
@@ -868,70 +917,106 @@ __device__ void dgs_stop_test(const GmresBufs& g, int j, double wn) {
     set_cond<COND>(g.h_inner, g.use_cond, stop == 0 ? 1u : 0u);
 }
 
-// Scalar tail of the DCGS2 block-dot (last CTA, one thread): finalises column
-// j-1 (or, at cycle end, column j), stores s, p, h_jj and 1/alpha.
-__device__ void dgs_dot_scalars(const GmresBufs& g, int j, int finalize, int nvv, const double* res) {
+// Scalar tail of the DCGS2 block-dot (whole last CTA; arithmetic by thread 0
+// on shared-memory copies): finalises column j-1 (or, at cycle end, column j),
+// stores s, p, h_jj and 1/alpha.  `sm` holds 3 (j + 3) doubles.
+__device__ void dgs_dot_scalars(const GmresBufs& g, int j, int finalize, int nvv, const double* res,
+                                double* sm) {
     GmresCtl* ctl = g.ctl;
     const int ld = ctl->restart + 1;
-    double ss = 0.0, sp = 0.0;
-    for (int i = 0; i < nvv; ++i) ss += res[i] * res[i];
-    const double sig = res[finalize ? nvv : 2 * nvv];
-    const double a2 = sig - ss;
-    const double alpha = a2 > 0.0 ? sqrt(a2) : 0.0;
-    if (finalize) {
-        // complete column j against the orthonormal v_0..v_j
-        double* hc = g.H + static_cast<long long>(j) * ld;
-        for (int i = 0; i <= j; ++i) hc[i] = hc[i] + res[i];
-        hc[j + 1] = alpha;
-        givens_column(ctl, hc, j);
-        record_column(g, j);
-        const double res_rel = fabs(ctl->g[j + 1]) / ctl->beta;
-        if (ctl->stop == 1 && !(res_rel <= ctl->tol_c)) ctl->stop = 3;
-        if (ctl->stop == 3 && res_rel <= ctl->tol_c) ctl->stop = 1;
-        ctl->m = j + 1;
-        return;
+    // column being completed: j (cycle end) or j - 1 (none at j = 0)
+    const int ci = finalize ? j : j - 1;
+    double* hc = ci >= 0 ? g.H + static_cast<long long>(ci) * ld : nullptr;
+    double* col = sm;
+    double* cs = col + (j + 3);
+    double* sn = cs + (j + 2);
+    for (int i = threadIdx.x; i <= ci; i += blockDim.x) {
+        col[i] = __ldcg(hc + i);
+        if (i < ci) {
+            cs[i] = ctl->cs[i];
+            sn[i] = ctl->sn[i];
+        }
     }
-    for (int i = 0; i < nvv; ++i) {
-        ctl->sv[i] = res[i];
-        ctl->pv[i] = res[nvv + i];
-        sp += res[i] * res[nvv + i];
-    }
-    if (j == 0) {
-        ctl->beta = alpha;
-        ctl->g[0] = alpha;
-        if (ctl->side == 0) {
-            // left: the cycle's base is P^-1 r; its norm sets the metric
-            // (gmres.cpp:41-46) and the restart tolerance rel_tol ||P^-1 b|| / ||P^-1 r||
-            if (ctl->cycles == 0) {
-                ctl->hnorm = alpha;
-                ctl->tol_c = ctl->rel_tol;
-            } else {
-                ctl->tol_c = ctl->rel_tol * ctl->hnorm / alpha;
+    // s, p coefficients for the update kernel (plain copies of res)
+    if (!finalize)
+        for (int i = threadIdx.x; i < nvv; i += blockDim.x) {
+            ctl->sv[i] = res[i];
+            ctl->pv[i] = res[nvv + i];
+        }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double beta0 = ctl->beta, hnorm0 = ctl->hnorm, tol0 = ctl->tol_c, rel_tol = ctl->rel_tol;
+        const int cycles = ctl->cycles, side = ctl->side, stop0 = ctl->stop, total0 = ctl->total;
+        const double gci = ci >= 0 ? ctl->g[ci] : 0.0;
+        double ss = 0.0, sp = 0.0;
+        for (int i = 0; i < nvv; ++i) ss += res[i] * res[i];
+        const double sig = res[finalize ? nvv : 2 * nvv];
+        const double a2 = sig - ss;
+        const double alpha = a2 > 0.0 ? sqrt(a2) : 0.0;
+        double beta = beta0;
+        if (!finalize) {
+            for (int i = 0; i < nvv; ++i) sp += res[i] * res[nvv + i];
+            if (j == 0) {
+                beta = alpha;
+                ctl->beta = alpha;
+                ctl->g[0] = alpha;
+                if (side == 0) {
+                    // left: the cycle's base is P^-1 r; its norm sets the metric
+                    // (gmres.cpp:41-46) and the restart tolerance rel_tol ||P^-1 b|| / ||P^-1 r||
+                    if (cycles == 0) {
+                        ctl->hnorm = alpha;
+                        ctl->tol_c = rel_tol;
+                    } else {
+                        ctl->tol_c = rel_tol * hnorm0 / alpha;
+                    }
+                }
             }
         }
-    } else {
-        double* hc = g.H + static_cast<long long>(j - 1) * ld;
-        for (int i = 0; i < j; ++i) hc[i] = hc[i] + res[i];
-        hc[j] = alpha;
-        givens_column(ctl, hc, j - 1);
-        record_column(g, j - 1);
+        if (ci >= 0) {
+            // complete column ci against the orthonormal v_0..v_j
+            for (int i = 0; i <= (finalize ? j : j - 1); ++i) col[i] = col[i] + res[i];
+            col[ci + 1] = alpha;
+            double gj = gci, gj1 = 0.0;
+            givens_column_s(cs, sn, col, ci, gj, gj1);
+            ctl->cs[ci] = cs[ci];
+            ctl->sn[ci] = sn[ci];
+            ctl->g[ci] = gj;
+            ctl->g[ci + 1] = gj1;
+            // record_column: history of the finalised column
+            ctl->total = total0 + 1;
+            const double res_rel = fabs(gj1) / beta;
+            const double hv = cycles == 0 ? res_rel : res_rel * beta / hnorm0;
+            g.hist[total0 + 1] = hv;
+            ctl->final_rel = hv;
+            if (finalize) {
+                if (stop0 == 1 && !(res_rel <= tol0)) ctl->stop = 3;
+                if (stop0 == 3 && res_rel <= tol0) ctl->stop = 1;
+                ctl->m = j + 1;
+            }
+        }
+        if (!finalize) {
+            const double pi = res[2 * nvv + 1];
+            const double hjj = alpha > 0.0 ? (pi - sp) / alpha : 0.0;
+            const double inv = alpha > 0.0 ? 1.0 / alpha : 0.0;
+            // Column j describes w = A Z_j with Z_j = P^-1 vt_j, |vt_j| ~ alpha: it is
+            // stored divided by alpha (the column of the unit input), the next
+            // direction is stored divided by alpha too (k_dgs_update), and x += Z y
+            // uses y_j / alpha_j (zscale) -- so magnitudes stay O(1) and the
+            // breakdown test compares the same quantity as gmres.cpp:118.
+            double* hcj = g.H + static_cast<long long>(j) * ld;
+            for (int i = 0; i < j; ++i) hcj[i] = res[nvv + i] * inv;
+            hcj[j] = hjj * inv;
+            ctl->zscale[j] = inv;
+            ctl->hjj = hjj;
+            ctl->inv_alpha = inv;
+            ctl->hnext = alpha;
+            if (!(alpha == alpha)) ctl->bad = 1;
+        }
     }
-    const double pi = res[2 * nvv + 1];
-    const double hjj = alpha > 0.0 ? (pi - sp) / alpha : 0.0;
-    const double inv = alpha > 0.0 ? 1.0 / alpha : 0.0;
-    // Column j describes w = A Z_j with Z_j = P^-1 vt_j, |vt_j| ~ alpha: it is
-    // stored divided by alpha (the column of the unit input), the next
-    // direction is stored divided by alpha too (k_dgs_update), and x += Z y
-    // uses y_j / alpha_j (zscale) -- so magnitudes stay O(1) and the
-    // breakdown test compares the same quantity as gmres.cpp:118.
-    double* hcj = g.H + static_cast<long long>(j) * ld;
-    for (int i = 0; i < j; ++i) hcj[i] = res[nvv + i] * inv;
-    hcj[j] = hjj * inv;
-    ctl->zscale[j] = inv;
-    ctl->hjj = hjj;
-    ctl->inv_alpha = inv;
-    ctl->hnext = alpha;
-    if (!(alpha == alpha)) ctl->bad = 1;
+    __syncthreads();
+    // the completed column back to H
+    if (ci >= 0)
+        for (int i = threadIdx.x; i <= ci + 1; i += blockDim.x) hc[i] = col[i];
 }
 
 // DCGS2 block-dot.  Iteration j (finalize = 0): targets A = slot j (vt_j) and
@@ -1016,12 +1101,14 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot(GmresBufs g, int fin
     __syncthreads();
     for (int q = threadIdx.x; q < nv; q += kRedThreads)
         g.partials[static_cast<long long>(q) * g.nchunks + c] = warp_sum8(red, nv, q);
+#ifdef IRK_DGS_SKIPFINAL
+    return;  // timing diagnostic only: the scalar tail is skipped
+#endif
     if (!elect_last(g.counters + 9)) return;
     double* res = red + (kRedThreads / 32) * nv;
     final_reduce(g.partials, g.nchunks, nv, red, res);
-    if (threadIdx.x != 0) return;
-    g.counters[9] = 0u;
-    dgs_dot_scalars(g, j, finalize, nvv, res);
+    if (threadIdx.x == 0) g.counters[9] = 0u;
+    dgs_dot_scalars(g, j, finalize, nvv, res, res + nv);
 }
 
 // DCGS2 update: v_j = (vt_j - sum_i s_i v_i) / alpha and
@@ -1073,9 +1160,8 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_update(GmresBufs g) {
     if (!elect_last(g.counters + 10)) return;
     double* res = red + kRedThreads / 32;
     final_reduce(g.partials, g.nchunks, 1, red, res);
-    if (threadIdx.x != 0) return;
-    g.counters[10] = 0u;
-    dgs_stop_test<COND>(g, j, sqrt(res[0]));
+    if (threadIdx.x == 0) g.counters[10] = 0u;
+    dgs_stop_test<COND>(g, j, sqrt(res[0]), pc + j + 1);
 }
 
 // V_{j+1} *= 1/h_{j+1,j} when the cycle continues; advance j.
@@ -1395,7 +1481,8 @@ void gm_update(const GmresBufs& g, int pass, cudaStream_t st) {
 
 static size_t dgs_smem(const GmresBufs& g) {
     const int nv = 2 * g.cap + 4;
-    return sizeof(double) * ((kRedThreads / 32 + 1) * nv + 16);
+    // reduction slots + the staged Hessenberg column and rotations of the tail
+    return sizeof(double) * ((kRedThreads / 32 + 1) * nv + 16 + 3 * (g.cap + 4));
 }
 
 void gm_dgs_dot(const GmresBufs& g, int finalize, cudaStream_t st) {
@@ -1427,7 +1514,8 @@ void dot(const double* x, const double* y, long long n, double* partials, unsign
 }
 
 void set_smem_limits() {
-    const int big = static_cast<int>(sizeof(double) * ((kRedThreads / 32 + 1) * (2 * kMaxRestart + 4) + 16));
+    const int big = static_cast<int>(sizeof(double) * ((kRedThreads / 32 + 1) * (2 * kMaxRestart + 4) + 16 +
+                                                       3 * (kMaxRestart + 4)));
     cudaFuncSetAttribute(k_dgs_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_dgs_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_dgs_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
