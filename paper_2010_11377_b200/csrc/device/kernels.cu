@@ -134,9 +134,17 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
     // fixed diagonal count, u8 values: the row's codes are static, so they are
     // loaded before waiting on the predecessor (decoded after it, together
     // with the dependent x loads -- one memory round trip after the wait)
-    constexpr bool kPre = ND > 0 && VF == kU8;
+    constexpr bool kPre = ND > 0 && (VF == kU8 || VF == kCls);
     unsigned cd[kPre ? ND : 1], cw[kPre ? ND : 1];
-    if constexpr (kPre) {
+    if constexpr (VF == kCls) {
+        // row class (static) and, for wd .* r, the neighbours' classes
+        const unsigned char* cls = static_cast<const unsigned char*>(A.val);
+        cd[0] = __ldg(cls + i);
+        if constexpr (XM == kXWdR && WDT == 1) {
+#pragma unroll
+            for (int d = 0; d < ND; ++d) cw[d] = __ldg(cls + min(max(i + A.off[d], 0), n - 1));
+        }
+    } else if constexpr (kPre) {
 #pragma unroll
         for (int d = 0; d < ND; ++d) {
             cd[d] = __ldg(static_cast<const unsigned char*>(A.val) + static_cast<long long>(d) * A.dstride + i);
@@ -154,7 +162,9 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
         double xv;
         if constexpr (XM == kXWdR) {
             double wdc;
-            if constexpr (kPre && WDT == 1)
+            if constexpr (VF == kCls)
+                wdc = __ldg(A.wdtab + cw[d]);
+            else if constexpr (kPre && WDT == 1)
                 wdc = wdt[cw[d]];
             else
                 wdc = WDT == 1 ? wdt[__ldg(dcode + c)] : wd[c];
@@ -163,15 +173,21 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
             xv = x[c];
         }
         double v;
-        if constexpr (kPre)
+        if constexpr (VF == kCls)
+            v = __ldg(A.tab + cd[0] * ND + d);
+        else if constexpr (kPre)
             v = tab[cd[d]];
         else
             v = vfetch<VF>(A.val, static_cast<long long>(d) * A.dstride + i, tab);
         s += v * xv;
     }
     double wdi = 0.0;
-    if (EPI == kESmooth || (EPI == kEProlong && !a.zb))
-        wdi = WDT == 1 ? wdt[__ldg(dcode + i)] : wd[i];
+    if (EPI == kESmooth || (EPI == kEProlong && !a.zb)) {
+        if constexpr (VF == kCls)
+            wdi = WDT == 1 ? __ldg(A.wdtab + cd[0]) : wd[i];
+        else
+            wdi = WDT == 1 ? wdt[__ldg(dcode + i)] : wd[i];
+    }
     a.y.get()[i] = spmv_epilogue<XM, EPI>(s, wdi, i, a, r, x);
 }
 
@@ -301,6 +317,14 @@ void launch_spmv(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
     switch (A.vf) {
     case kU8: launch_spmv_vf<XM, EPI, kU8>(A, a, st); break;
     case kU16: launch_spmv_vf<XM, EPI, kU16>(A, a, st); break;
+    case kCls:
+        // DIA row classes (7 diagonals)
+        if (A.fmt != kDia || A.nd != 7) throw InvalidArgument("row classes need a 7-diagonal DIA operator");
+        if (A.wdtab)
+            launch(k_spmv_dia<XM, EPI, kCls, 1, 7>, blocks_for(A.rows, 256), 256, 0, st, A, a);
+        else
+            launch(k_spmv_dia<XM, EPI, kCls, 0, 7>, blocks_for(A.rows, 256), 256, 0, st, A, a);
+        break;
     default: launch_spmv_vf<XM, EPI, kF64>(A, a, st); break;
     }
 }
@@ -314,9 +338,11 @@ __global__ void __launch_bounds__(256) k_stage_op_dia(Mat M, Mat K, StageCoef cf
     __shared__ double s_dummy[1];
     const double* tm = load_tab<VF>(M, s_tm, s_dummy);
     const double* tk = load_tab<VF>(K, s_tk, s_dummy);
-    pdl_wait();
     const int n = M.rows;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned ci = 0;  // joint (M, K) row class
+    if constexpr (VF == kCls) ci = i < n ? __ldg(static_cast<const unsigned char*>(M.val) + i) : 0u;
+    pdl_wait();
     if (i >= n) return;
     const double* __restrict__ z = zr.get();
     double* __restrict__ y = yr.get();
@@ -327,9 +353,15 @@ __global__ void __launch_bounds__(256) k_stage_op_dia(Mat M, Mat K, StageCoef cf
     for (int d = 0; d < (ND > 0 ? ND : kMaxDiags); ++d) {
         if (ND == 0 && d >= M.nd) break;
         const int c = min(max(i + M.off[d], 0), n - 1);
-        const long long e = static_cast<long long>(d) * M.dstride + i;
-        const double m = vfetch<VF>(M.val, e, tm);
-        const double k = vfetch<VF>(K.val, e, tk);
+        double m, k;
+        if constexpr (VF == kCls) {
+            m = __ldg(M.tab + ci * ND + d);
+            k = __ldg(K.tab + ci * ND + d);
+        } else {
+            const long long e = static_cast<long long>(d) * M.dstride + i;
+            m = vfetch<VF>(M.val, e, tm);
+            k = vfetch<VF>(K.val, e, tk);
+        }
 #pragma unroll
         for (int j = 0; j < S; ++j) {
             const double x = z[static_cast<long long>(j) * n + c];
@@ -354,9 +386,11 @@ __global__ void __launch_bounds__(256) k_sweep_dia(Mat K, VecRef wr, VecRef vr, 
     __shared__ double s_tk[VF == kU8 ? 256 : 1];
     __shared__ double s_dummy[1];
     const double* tk = load_tab<VF>(K, s_tk, s_dummy);
-    pdl_wait();
     const int n = K.rows;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned ci = 0;
+    if constexpr (VF == kCls) ci = i < n ? __ldg(static_cast<const unsigned char*>(K.val) + i) : 0u;
+    pdl_wait();
     if (i >= n) return;
     const double* __restrict__ w = wr.get();
     double f = 0.0;
@@ -364,7 +398,12 @@ __global__ void __launch_bounds__(256) k_sweep_dia(Mat K, VecRef wr, VecRef vr, 
     for (int d = 0; d < (ND > 0 ? ND : kMaxDiags); ++d) {
         if (ND == 0 && d >= K.nd) break;
         const int c = min(max(i + K.off[d], 0), n - 1);
-        f += vfetch<VF>(K.val, static_cast<long long>(d) * K.dstride + i, tk) * w[c];
+        double k;
+        if constexpr (VF == kCls)
+            k = __ldg(K.tab + ci * ND + d);
+        else
+            k = vfetch<VF>(K.val, static_cast<long long>(d) * K.dstride + i, tk);
+        f += k * w[c];
     }
     if (store) store[i] = f;
     double acc = vr.get()[i];
@@ -1386,13 +1425,18 @@ void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st) 
 void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecRef y, int n,
                   cudaStream_t st) {
     const int nb = blocks_for(n, 256);
-    if (M.vf != K.vf || (M.vf != kF64 && M.vf != kU8))
-        throw InvalidArgument("stage_op: M and K must share a value format (f64 or u8)");
+    if (M.vf != K.vf || (M.vf != kF64 && M.vf != kU8 && M.vf != kCls))
+        throw InvalidArgument("stage_op: M and K must share a value format (f64, u8 or row classes)");
+    if (M.vf == kCls && (M.nd != 7 || M.val != K.val))
+        throw InvalidArgument("stage_op: row classes need 7 diagonals and one joint class array");
     const bool u8 = M.vf == kU8;
+    const bool cls = M.vf == kCls;
     switch (c.s) {
 #define IRK_OP_CASE(S)                                                             \
     case S:                                                                        \
-        if (u8 && M.nd == 7)                                                       \
+        if (cls)                                                                   \
+            launch(k_stage_op_dia<S, kCls, 7>, nb, 256, 0, st, M, K, c, z, y);         \
+        else if (u8 && M.nd == 7)                                                  \
             launch(k_stage_op_dia<S, kU8, 7>, nb, 256, 0, st, M, K, c, z, y);          \
         else if (u8)                                                               \
             launch(k_stage_op_dia<S, kU8, 0>, nb, 256, 0, st, M, K, c, z, y);          \
@@ -1410,6 +1454,10 @@ void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecR
 void sweep_dia(const Mat& K, VecRef w, VecRef v, const SweepTerms& t, double* store, VecRef out,
                int n, cudaStream_t st) {
     switch (K.vf) {
+    case kCls:
+        if (K.nd != 7) throw InvalidArgument("row classes need 7 diagonals");
+        launch(k_sweep_dia<kCls, 7>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out);
+        break;
     case kU8:
         if (K.nd == 7)
             launch(k_sweep_dia<kU8, 7>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out);

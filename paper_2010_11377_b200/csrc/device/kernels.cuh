@@ -26,7 +26,12 @@ constexpr int kMaxDiags = 16;
 // uint16 codes into an exact fp64 dictionary (lossless; e.g. 3 distinct
 // values in the fine-level stencils, 14 in the fine prolongator).
 enum MatFmt { kSell = 0, kDia = 1, kCsrVec = 2 };
-enum ValFmt { kF64 = 0, kU8 = 1, kU16 = 2 };
+// kCls (DIA with 7 diagonals only): one u8 row class per row; rows of one
+// class have the identical stencil, stored once in tab[class * nd + d]
+// (lossless: a class is a distinct tuple of fp64 bit patterns).  On the
+// uniform P1 grid nearly every row is interior, so a row costs one byte and
+// one coalesced load instead of nd codes.
+enum ValFmt { kF64 = 0, kU8 = 1, kU16 = 2, kCls = 3 };
 
 struct Mat {
     int fmt = kSell;

@@ -6,6 +6,7 @@
 // captured iteration body iteration-invariant.
 #include <algorithm>
 #include <atomic>
+#include <unordered_map>
 #include <unordered_set>
 #include <chrono>
 #include <cmath>
@@ -176,6 +177,130 @@ void DeviceSolver::upload_values(dev::Mat& m, const std::vector<double>& vals, d
     }
 }
 
+namespace {
+
+// DIA layout of a square operator: sorted offsets, aligned stride and the
+// diagonal-major values (padding = 0.0); empty when the pattern has more
+// than kMaxDiags diagonals or more than 15% padding.
+struct DiaLayout {
+    std::vector<int> offs;
+    long long ds = 0;
+    std::vector<double> v;
+};
+
+DiaLayout dia_layout(const Csr& A) {
+    DiaLayout L;
+    if (A.rows != A.cols || A.rows == 0) return L;
+    std::vector<int>& offs = L.offs;
+    for (int i = 0; i < A.rows; ++i)
+        for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+            const int o = A.idx[k] - i;
+            if (std::find(offs.begin(), offs.end(), o) == offs.end()) {
+                offs.push_back(o);
+                if (static_cast<int>(offs.size()) > dev::kMaxDiags) {
+                    offs.clear();
+                    return L;
+                }
+            }
+        }
+    if (static_cast<double>(offs.size()) * A.rows > 1.15 * A.nnz() + 64) {
+        offs.clear();
+        return L;
+    }
+    std::sort(offs.begin(), offs.end());
+    L.ds = (static_cast<long long>(A.rows) + 3) / 4 * 4;  // aligned stride
+    L.v.assign(offs.size() * L.ds, 0.0);
+    for (int i = 0; i < A.rows; ++i)
+        for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+            const int d = static_cast<int>(std::lower_bound(offs.begin(), offs.end(), A.idx[k] - i) - offs.begin());
+            L.v[static_cast<size_t>(d) * L.ds + i] = A.val[k];
+        }
+    return L;
+}
+
+// Row classes: rows whose stencil values (over all `vals` operators) are the
+// same fp64 bit patterns share a class; at most 256 classes (else false).
+bool row_classes(const std::vector<const std::vector<double>*>& vals, int nd, int rows, long long ds,
+                 std::vector<unsigned char>& cls, std::vector<std::vector<double>>& tabs) {
+    const int nm = static_cast<int>(vals.size());
+    const int w = nm * nd;
+    std::vector<uint64_t> reps;  // class tuples, w words each
+    std::unordered_map<uint64_t, std::vector<int>> by_hash;
+    std::vector<uint64_t> t(w);
+    cls.resize(rows);
+    int prev = -1;
+    for (int i = 0; i < rows; ++i) {
+        uint64_t h = 1469598103934665603ULL;
+        for (int m = 0; m < nm; ++m)
+            for (int d = 0; d < nd; ++d) {
+                uint64_t b;
+                std::memcpy(&b, &(*vals[m])[static_cast<size_t>(d) * ds + i], sizeof(b));
+                t[m * nd + d] = b;
+                h = (h ^ b) * 1099511628211ULL;
+            }
+        auto same = [&](int c) { return std::equal(t.begin(), t.end(), reps.begin() + static_cast<size_t>(c) * w); };
+        int c = -1;
+        if (prev >= 0 && same(prev)) {
+            c = prev;
+        } else {
+            std::vector<int>& cand = by_hash[h];
+            for (int q : cand)
+                if (same(q)) c = q;
+            if (c < 0) {
+                c = static_cast<int>(reps.size() / w);
+                if (c >= 256) return false;
+                reps.insert(reps.end(), t.begin(), t.end());
+                cand.push_back(c);
+            }
+        }
+        cls[i] = static_cast<unsigned char>(c);
+        prev = c;
+    }
+    const int nc = static_cast<int>(reps.size() / w);
+    tabs.assign(nm, std::vector<double>(static_cast<size_t>(nc) * nd));
+    for (int c = 0; c < nc; ++c)
+        for (int m = 0; m < nm; ++m)
+            std::memcpy(&tabs[m][static_cast<size_t>(c) * nd], &reps[static_cast<size_t>(c) * w + m * nd],
+                        sizeof(double) * nd);
+    return true;
+}
+
+bool row_classes_enabled() {
+    static const bool on = !(std::getenv("IRK_ROW_CLASSES") && std::string(std::getenv("IRK_ROW_CLASSES")) == "0");
+    return on;
+}
+
+}  // namespace
+
+// Re-stores DIA operators (7 diagonals, shared layout) as row classes: one
+// class array (shared by all `mats`) and one value table per operator;
+// `omega` > 0 adds the omega / diagonal table per class (hierarchy operators).
+bool DeviceSolver::to_row_classes(std::vector<dev::Mat*> mats, const std::vector<const std::vector<double>*>& vals,
+                                  double omega) {
+    dev::Mat& m0 = *mats[0];
+    if (!row_classes_enabled() || m0.fmt != dev::kDia || m0.nd != 7) return false;
+    std::vector<unsigned char> cls;
+    std::vector<std::vector<double>> tabs;
+    if (!row_classes(vals, m0.nd, m0.rows, m0.dstride, cls, tabs)) return false;
+    const unsigned char* dcls = upload_array(cls);
+    for (size_t q = 0; q < mats.size(); ++q) {
+        dev::Mat& m = *mats[q];
+        m.vf = dev::kCls;
+        m.val = dcls;
+        m.tab = upload_array(tabs[q]);
+        m.ntab = static_cast<int>(tabs[q].size() / m.nd);
+        m.tab_smem = 0;
+        m.bytes = (q == 0 ? cls.size() : 0) + sizeof(double) * tabs[q].size();
+        m.wdtab = nullptr;
+        if (omega > 0.0 && m.diag0 >= 0) {
+            std::vector<double> wd(m.ntab);
+            for (int c = 0; c < m.ntab; ++c) wd[c] = omega * (1.0 / tabs[q][static_cast<size_t>(c) * m.nd + m.diag0]);
+            m.wdtab = upload_array(wd);
+        }
+    }
+    return true;
+}
+
 // DIA when the pattern is <= 16 diagonals with <= 15% padding; else SELL-32.
 // `omega` > 0 requests the omega/diag dictionary (hierarchy operators).
 dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
@@ -183,41 +308,20 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
     m.rows = A.rows;
     m.cols = A.cols;
     m.nnz = A.nnz();
-    std::vector<int> offs;
-    bool dia = allow_dia && A.rows == A.cols && A.rows > 0;
-    if (dia) {
-        for (int i = 0; i < A.rows && dia; ++i)
-            for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
-                const int o = A.idx[k] - i;
-                if (std::find(offs.begin(), offs.end(), o) == offs.end()) {
-                    offs.push_back(o);
-                    if (static_cast<int>(offs.size()) > dev::kMaxDiags) {
-                        dia = false;
-                        break;
-                    }
-                }
-            }
-        if (dia && static_cast<double>(offs.size()) * A.rows > 1.15 * A.nnz() + 64) dia = false;
-    }
-    if (dia) {
-        std::sort(offs.begin(), offs.end());
-        const int nd = static_cast<int>(offs.size());
-        const long long ds = (static_cast<long long>(A.rows) + 3) / 4 * 4;  // aligned stride
-        std::vector<double> v(static_cast<size_t>(nd) * ds, 0.0);
-        for (int i = 0; i < A.rows; ++i)
-            for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
-                const int d = static_cast<int>(std::lower_bound(offs.begin(), offs.end(), A.idx[k] - i) -
-                                               offs.begin());
-                v[static_cast<size_t>(d) * ds + i] = A.val[k];
-            }
+    DiaLayout L;
+    if (allow_dia) L = dia_layout(A);
+    if (!L.offs.empty()) {
+        const int nd = static_cast<int>(L.offs.size());
         m.fmt = dev::kDia;
-        m.dstride = ds;
+        m.dstride = L.ds;
         m.nd = nd;
         for (int d = 0; d < nd; ++d) {
-            m.off[d] = offs[d];
-            if (offs[d] == 0) m.diag0 = d;
+            m.off[d] = L.offs[d];
+            if (L.offs[d] == 0) m.diag0 = d;
         }
-        upload_values(m, v, omega);
+        // hierarchy operators: row classes when the stencil repeats
+        if (omega > 0.0 && to_row_classes({&m}, {&L.v}, omega)) return m;
+        upload_values(m, L.v, omega);
         return m;
     }
     // Long rows: CSR-vector with G lanes per row (G ~ average length / 3).
@@ -226,7 +330,10 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
     // (SELL wins when there are enough rows to fill the GPU with one thread
     // per row; small coarse operators need lanes per row to expose
     // memory-level parallelism.)
-    if ((force < 0 && avg > 4.5 && (A.rows < 65536 || avg > 24.0)) || force == dev::kCsrVec) {
+    // (big operators switch to CSR-vector above IRK_CSRV_BIG_AVG entries per row)
+    static const double big_avg =
+        std::getenv("IRK_CSRV_BIG_AVG") ? std::atof(std::getenv("IRK_CSRV_BIG_AVG")) : 24.0;
+    if ((force < 0 && avg > 4.5 && (A.rows < 65536 || avg > big_avg)) || force == dev::kCsrVec) {
         static const double per_lane =
             std::getenv("IRK_CSRV_PER_LANE") ? std::atof(std::getenv("IRK_CSRV_PER_LANE")) : 3.0;
         int g = 2;
@@ -328,6 +435,11 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
     fused_op_ = M_.fmt == dev::kDia && K_.fmt == dev::kDia && M_.nd == K_.nd &&
                 std::equal(M_.off, M_.off + M_.nd, K_.off) && M_.vf == K_.vf &&
                 (M_.vf == dev::kF64 || M_.vf == dev::kU8);
+    if (fused_op_ && M_.nd == 7) {
+        // one joint row class per row for the stage operator and the sweeps
+        const DiaLayout lm = dia_layout(M), lk = dia_layout(K);
+        if (lm.ds == M_.dstride && lk.ds == K_.dstride) to_row_classes({&M_, &K_}, {&lm.v, &lk.v}, 0.0);
+    }
     coef_.s = s;
     for (int i = 0; i < s * s; ++i) coef_.c[i] = ht * A[i];
     hb_.resize(s);

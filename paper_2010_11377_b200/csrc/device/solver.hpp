@@ -128,6 +128,9 @@ public:
 
 private:
     dev::Mat upload(const Csr& A, bool allow_dia, double omega);
+    // DIA row classes (dev::kCls) for one operator or a pair sharing a pattern
+    bool to_row_classes(std::vector<dev::Mat*> mats, const std::vector<const std::vector<double>*>& vals,
+                        double omega);
     void upload_values(dev::Mat& m, const std::vector<double>& vals, double omega);
     template <class T> const T* upload_array(const std::vector<T>& h);
     double* alloc(size_t count);
