@@ -188,7 +188,9 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
         else
             wdi = WDT == 1 ? wdt[__ldg(dcode + i)] : wd[i];
     }
-    a.y.get()[i] = spmv_epilogue<XM, EPI>(s, wdi, i, a, r, x);
+    const double out = spmv_epilogue<XM, EPI>(s, wdi, i, a, r, x);
+    a.y.get()[i] = out;
+    if (a.y2) a.y2[i] = a.wd2[i] * out;
 }
 
 // SELL-32: one warp per 32-row slice, entries column-major inside the slice,
@@ -223,7 +225,9 @@ __global__ void __launch_bounds__(256) k_spmv_sell(Mat A, SpmvArgs a) {
     if (row >= A.rows) return;
     double wdi = 0.0;
     if (EPI == kESmooth || (EPI == kEProlong && !a.zb)) wdi = wd[row];
-    a.y.get()[row] = spmv_epilogue<XM, EPI>(s, wdi, row, a, r, x);
+    const double out = spmv_epilogue<XM, EPI>(s, wdi, row, a, r, x);
+    a.y.get()[row] = out;
+    if (a.y2) a.y2[row] = a.wd2[row] * out;
 }
 
 // CSR-vector: G lanes per row, each lane loading up to 4 entries of a chunk
@@ -277,7 +281,9 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
     if (!live || lane != 0) return;
     double wdi = 0.0;
     if (EPI == kESmooth || (EPI == kEProlong && !a.zb)) wdi = wd[row];
-    a.y.get()[row] = spmv_epilogue<XM, EPI>(s, wdi, row, a, r, x);
+    const double out = spmv_epilogue<XM, EPI>(s, wdi, row, a, r, x);
+    a.y.get()[row] = out;
+    if (a.y2) a.y2[row] = a.wd2[row] * out;
 }
 
 template <int XM, int EPI, int VF>

@@ -75,6 +75,11 @@ struct SpmvArgs {
     const double* wd = nullptr;  // omega * D^-1
     const double* zb = nullptr;  // prolong base (nullptr -> wd .* r)
     VecRef y{};
+    // optional second output y2 = wd2 .* y (a restriction also writes the
+    // next level's pre-smoothed iterate wd .* r, so that level's residual
+    // gathers one vector instead of two)
+    double* y2 = nullptr;
+    const double* wd2 = nullptr;
 };
 
 // Programmatic dependent launch, opt-in via IRK_PDL=1.

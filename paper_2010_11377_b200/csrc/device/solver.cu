@@ -469,6 +469,7 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
             if (l > 0) {
                 d.r = alloc(d.n);
                 d.z = alloc(d.n);
+                d.zr = alloc(d.n);
             }
             dh.lv[l] = d;
         }
@@ -522,6 +523,15 @@ int DeviceSolver::matrix_format(int which) const { return which == 0 ? M_.fmt : 
 //   r_{l+1} = R t          restriction
 //   t = wd.*r + P z_{l+1}  prolongation fused with the pre-smoothed iterate
 //   z = t + wd.*(r - A t)  post-smoothing sweep
+namespace {
+// IRK_ZR=0: levels >= 1 recompute wd .* r on the fly instead of reading the
+// copy the restriction wrote (A/B switch)
+bool zr_on() {
+    static const bool on = !(std::getenv("IRK_ZR") && std::string(std::getenv("IRK_ZR")) == "0");
+    return on;
+}
+}  // namespace
+
 void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
     DevHier& H = hier_[k];
     const int L = static_cast<int>(H.lv.size());
@@ -540,7 +550,12 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
         a.r = rhs_of(l);
         a.wd = d.wd;
         a.y = dev::plain(d.t);
-        if (pre == 1) {
+        // below the entry level the restriction already wrote wd .* r
+        const bool zr = zr_on() && pre == 1 && l > first && d.zr;
+        if (zr) {
+            a.x = dev::plain(d.zr);
+            dev::spmv(d.A, dev::kXPlain, dev::kEResid, a, st_);
+        } else if (pre == 1) {
             dev::spmv(d.A, dev::kXWdR, dev::kEResid, a, st_);
         } else {
             dev::wd_times_r(d.n, d.wd, a.r, d.zp, st_);
@@ -561,6 +576,10 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
         dev::SpmvArgs ra;
         ra.x = dev::plain(d.t);
         ra.y = dev::plain(H.lv[l + 1].r);
+        if (zr_on() && pre == 1 && l + 2 < L) {
+            ra.y2 = H.lv[l + 1].zr;
+            ra.wd2 = H.lv[l + 1].wd;
+        }
         dev::spmv(d.R, dev::kXPlain, dev::kEPlain, ra, st_);
     }
     scope(L - 1);
@@ -572,7 +591,7 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
         pa.x = dev::plain(H.lv[l + 1].z);
         pa.r = rhs_of(l);
         pa.wd = d.wd;
-        pa.zb = pre == 1 ? nullptr : d.zp;
+        pa.zb = pre == 1 ? (zr_on() && l > first && d.zr ? d.zr : nullptr) : d.zp;
         pa.y = dev::plain(d.t);
         dev::spmv(d.P, dev::kXPlain, dev::kEProlong, pa, st_);
         double* cur = d.t;

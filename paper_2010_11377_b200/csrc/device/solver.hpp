@@ -58,6 +58,7 @@ struct DevLevel {
     double* t = nullptr;          // residual / prolongated iterate
     double* u = nullptr;          // post-sweep ping-pong
     double* zp = nullptr;         // pre-smoothed iterate (pre > 1 only)
+    double* zr = nullptr;         // wd .* r, written by the restriction (levels >= 1)
 };
 
 struct DevHier {

@@ -40,4 +40,13 @@ torch.cuda.profiler.start()
 step()
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
-print("iterations", rep.iterations, "reorth", rep.n_reorth, "ms", rep.solve_seconds * 1e3)
+first = rep.solve_seconds * 1e3
+# IRK_AB_REPS=k: k more timed steps (same input) -> min / median for A/B runs
+reps = int(__import__("os").environ.get("IRK_AB_REPS", "0"))
+ts = [first]
+for _ in range(reps):
+    step()
+    ts.append(rep.solve_seconds * 1e3)
+ts.sort()
+extra = f" min {ts[0]:.3f} med {ts[len(ts) // 2]:.3f}" if reps else ""
+print("iterations", rep.iterations, "reorth", rep.n_reorth, "ms", first, extra)
