@@ -379,11 +379,15 @@ def our_arm(args):
         traffic = json.loads((ROOT / "profiles" / "r1" / "traffic.json").read_text())["k_dgs_dot_j15"]
     except Exception:
         pass
-    # fine-level smoother (DIA, u8 value codes): bytes it must move in its own
-    # format (7 code bytes + x, r, diagonal code, y per row)
+    # fine-level smoother: bytes it must move in its own format -- row classes
+    # (1 class byte + x, r, y per row; the stencil and omega/diagonal come from
+    # the per-class table) or u8 codes (7 code bytes + x, r, diagonal code, y)
     sms = C.c_double()
     _abi.check(L.irkdev_time_kernel(dev._h, 1, 200, C.byref(sms)))
-    s_bytes = (7 + 8 + 8 + 1 + 8) * n
+    vf0 = C.c_int()
+    _abi.check(L.irkdev_level_value_format(dev._h, 0, 0, C.byref(vf0)))
+    s_fmt = "row classes" if vf0.value == 3 else "u8 value codes"
+    s_bytes = (1 + 8 + 8 + 8) * n if vf0.value == 3 else (7 + 8 + 8 + 1 + 8) * n
     # whole-solve byte model on the actual hierarchies and iterations
     nnz_mk = prob.M.nnz
     model = [solve_bytes(info, levels, (r.iterations, r.n_reorth, r.cycles), n, S, nnz_mk)[0]
@@ -411,7 +415,7 @@ def our_arm(args):
                      "traffic": traffic, "bytes_per_launch": k_bytes, "ms_per_launch": kms.value,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in pk
                      else "fallback 6650 GB/s (B200_PROFILING.md)"},
-        "smoother_roofline": {"kernel": "fine-level Jacobi smoother k_spmv_dia (DIA, u8 value codes)",
+        "smoother_roofline": {"kernel": f"fine-level Jacobi smoother k_spmv_dia (DIA, {s_fmt})",
                               "bytes_per_launch": s_bytes, "ms_per_launch": sms.value,
                               "achieved_gbs": s_bytes / (sms.value * 1e-3) / 1e9,
                               "frac": s_bytes / (sms.value * 1e-3) / 1e9 / hbm_peak},

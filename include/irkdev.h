@@ -147,6 +147,9 @@ int irkdev_info(const irkdev* d, int* n, int* s, int* n_hier, int* solver_of_blo
 int irkdev_level_info(const irkdev* d, int k, int l, int* n, int* nnz_A, int* nnz_P,
                       int* nnz_R, int* fmt_A);
 int irkdev_num_levels(const irkdev* d, int k);
+/* Stored value format of hierarchy k's level-l operator on the device:
+ * 0 fp64, 1 u8 codes, 2 u16 codes, 3 DIA row classes (roofline byte counts). */
+int irkdev_level_value_format(const irkdev* d, int k, int l, int* vf);
 
 /* irk_step (irk.hpp:36-39): host pointers.  f_lift may be NULL (zero),
  * k_out may be NULL; history (max_iter+1 doubles) may be NULL. */

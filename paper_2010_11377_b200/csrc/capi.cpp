@@ -380,6 +380,10 @@ int irkdev_level_info(const irkdev* d, int k, int l, int* n, int* nnz_A, int* nn
     });
 }
 
+int irkdev_level_value_format(const irkdev* d, int k, int l, int* vf) {
+    return guard([&] { *vf = d->s->level_value_format(k, l); });
+}
+
 int irkdev_step(irkdev* d, const double* u_n, const double* f_lift, const irk_gmres_cfg* cfg,
                 double* u_next, double* k_out, irk_report* rep, double* history) {
     return guard([&] {

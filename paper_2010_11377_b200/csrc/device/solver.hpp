@@ -85,7 +85,12 @@ public:
     const std::vector<int>& solver_of_block() const { return sob_; }
     double setup_seconds() const { return setup_seconds_; }
     bool fused_stage_op() const { return fused_op_; }
-    int matrix_format(int which) const;  // 0 M, 1 K -> 0 CSR, 1 DIA
+    int matrix_format(int which) const;
+    int level_value_format(int k, int l) const {
+        check(k >= 0 && k < static_cast<int>(hier_.size()), "level_value_format: hierarchy out of range");
+        check(l >= 0 && l < static_cast<int>(hier_[k].lv.size()), "level_value_format: level out of range");
+        return hier_[k].lv[l].A.vf;
+    }  // 0 M, 1 K -> 0 CSR, 1 DIA
 
     // Device-pointer entry points (enqueue + synchronise).
     void stage_apply(const double* v, double* y);
