@@ -150,6 +150,9 @@ int irkdev_num_levels(const irkdev* d, int k);
 /* Stored value format of hierarchy k's level-l operator on the device:
  * 0 fp64, 1 u8 codes, 2 u16 codes, 3 DIA row classes (roofline byte counts). */
 int irkdev_level_value_format(const irkdev* d, int k, int l, int* vf);
+/* Tuning switch override (same names as the IRK_* environment variables);
+ * solvers re-record their graphs on the next step.  For same-process A/B runs. */
+int irk_set_option(const char* name, long long value);
 
 /* irk_step (irk.hpp:36-39): host pointers.  f_lift may be NULL (zero),
  * k_out may be NULL; history (max_iter+1 doubles) may be NULL. */

@@ -89,6 +89,7 @@ _SIGS = {
     "irkdev_level_info": (C.c_int, [V, C.c_int, C.c_int, iptr, iptr, iptr, iptr, iptr]),
     "irkdev_num_levels": (C.c_int, [V, C.c_int]),
     "irkdev_level_value_format": (C.c_int, [V, C.c_int, C.c_int, iptr]),
+    "irk_set_option": (C.c_int, [C.c_char_p, C.c_longlong]),
     "irkdev_step": (C.c_int, [V, dptr, dptr, C.POINTER(irk_gmres_cfg), dptr, dptr,
                               C.POINTER(irk_report), dptr]),
     "irkdev_step_device": (C.c_int, [V, C.c_void_p, C.c_void_p, C.POINTER(irk_gmres_cfg),

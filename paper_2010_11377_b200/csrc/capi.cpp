@@ -380,6 +380,13 @@ int irkdev_level_info(const irkdev* d, int k, int l, int* n, int* nnz_A, int* nn
     });
 }
 
+int irk_set_option(const char* name, long long value) {
+    return guard([&] {
+        irkb::check(name != nullptr, "set_option: name is null");
+        irkb::dev::set_option(name, value);
+    });
+}
+
 int irkdev_level_value_format(const irkdev* d, int k, int l, int* vf) {
     return guard([&] { *vf = d->s->level_value_format(k, l); });
 }

@@ -5,6 +5,9 @@
 // deterministic reductions (see common.cuh for the numerics contract).
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
+#include <map>
+#include <mutex>
 #include <utility>
 #include <string>
 
@@ -27,6 +30,30 @@ inline int blocks_for(long long n, int t) { return static_cast<int>((n + t - 1) 
 namespace {
 thread_local bool g_pdl_scope = false;
 }
+
+namespace {
+std::mutex g_opt_mu;
+std::map<std::string, long long> g_opt;
+std::atomic<unsigned> g_opt_gen{0};
+}  // namespace
+
+long long option(const char* name, long long dflt) {
+    {
+        std::lock_guard<std::mutex> lock(g_opt_mu);
+        auto it = g_opt.find(name);
+        if (it != g_opt.end()) return it->second;
+    }
+    const char* e = std::getenv(name);
+    return e ? std::atoll(e) : dflt;
+}
+
+void set_option(const char* name, long long value) {
+    std::lock_guard<std::mutex> lock(g_opt_mu);
+    g_opt[name] = value;
+    g_opt_gen.fetch_add(1);
+}
+
+unsigned option_generation() { return g_opt_gen.load(); }
 
 bool pdl_enabled() {
     static const bool on = std::getenv("IRK_PDL") != nullptr;
@@ -1105,15 +1132,30 @@ __device__ __forceinline__ void dgs_batch(const double* V, long long stride, lon
 
 __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot(GmresBufs g, int finalize) {
     extern __shared__ double red[];
-    pdl_trigger();
-    pdl_wait();
+    // Iteration mode: j, vt_j and v_0 were final before the operator ran, so
+    // under a programmatic launch they are loaded during its tail; only w
+    // (slot j+1, the operator's output) waits.  Cycle end: everything waits.
+    // The trigger follows the wait: the update (launched programmatically
+    // after this kernel) loads w before its own wait, so it may only start
+    // once every CTA here has seen the operator complete.
+    if (finalize) {
+        pdl_wait();
+        pdl_trigger();
+    }
     GmresCtl* ctl = g.ctl;
-    const int j = ctl->j;
+    const int j = *reinterpret_cast<volatile const int*>(&ctl->j);
     const int nvv = finalize ? j + 1 : j;   // basis vectors v_0..v_{nvv-1}
     const int nv = finalize ? nvv + 1 : 2 * nvv + 2;
     const int c = blockIdx.x;
     const long long n = g.sN;
     const long long stride = (g.sN + 63) / 64 * 64;
+    double a[kRedPerThread], v[kRedPerThread];
+    if (!finalize) {
+        load_chunk(g.V + static_cast<long long>(j) * stride, n, c, a);
+        if (nvv > 0) load_chunk(g.V, n, c, v);
+        pdl_wait();
+        pdl_trigger();
+    }
     double b[kRedPerThread];
     load_chunk(g.V + static_cast<long long>(j + 1) * stride, n, c, b);
     int i = 0;
@@ -1128,9 +1170,6 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot(GmresBufs g, int fin
     } else {
         // v_{i+1} is loaded as soon as v_i's local sums are formed, so its
         // latency overlaps v_i's warp trees (same trees and values as before)
-        double a[kRedPerThread], v[kRedPerThread];
-        load_chunk(g.V + static_cast<long long>(j) * stride, n, c, a);
-        if (nvv > 0) load_chunk(g.V, n, c, v);
         {
             double d[2] = {chunk_dot_local(a, a), chunk_dot_local(a, b)};
             const double x = warp_tree_multi<2>(d);
@@ -1163,9 +1202,21 @@ template <bool COND>
 __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_update(GmresBufs g) {
     extern __shared__ double red[];
     pdl_trigger();
-    pdl_wait();
+    // vt_j, w and v_0 are final before the block-dot runs: under a
+    // programmatic launch they are loaded during its scalar tail; the
+    // coefficients wait for it
     GmresCtl* ctl = g.ctl;
-    const int j = ctl->j;
+    const int j = *reinterpret_cast<volatile const int*>(&ctl->j);
+    const int c = blockIdx.x;
+    const long long n = g.sN;
+    const long long stride = (g.sN + 63) / 64 * 64;
+    double* ap = g.V + static_cast<long long>(j) * stride;
+    double* bp = g.V + static_cast<long long>(j + 1) * stride;
+    double a[kRedPerThread], b[kRedPerThread], v[kRedPerThread];
+    load_chunk(ap, n, c, a);
+    load_chunk(bp, n, c, b);
+    if (j > 0) load_chunk(g.V, n, c, v);
+    pdl_wait();
     double* sc = red + kRedThreads / 32 + 1;  // s coefficients
     double* pc = sc + j + 1;                  // p coefficients
     for (int i = threadIdx.x; i < j; i += kRedThreads) {
@@ -1174,23 +1225,14 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_update(GmresBufs g) {
     }
     __syncthreads();
     const double inv = ctl->inv_alpha, hjj = ctl->hjj;
-    const int c = blockIdx.x;
-    const long long n = g.sN;
-    const long long stride = (g.sN + 63) / 64 * 64;
-    double* ap = g.V + static_cast<long long>(j) * stride;
-    double* bp = g.V + static_cast<long long>(j + 1) * stride;
-    double a[kRedPerThread], b[kRedPerThread];
-    load_chunk(ap, n, c, a);
-    load_chunk(bp, n, c, b);
     for (int i = 0; i < j; ++i) {
-        double v[kRedPerThread];
-        load_chunk(g.V + static_cast<long long>(i) * stride, n, c, v);
         const double si = sc[i], pi = pc[i];
 #pragma unroll
         for (int q = 0; q < kRedPerThread; ++q) {
             a[q] = a[q] - si * v[q];
             b[q] = b[q] - pi * v[q];
         }
+        if (i + 1 < j) load_chunk(g.V + static_cast<long long>(i + 1) * stride, n, c, v);
     }
 #pragma unroll
     for (int q = 0; q < kRedPerThread; ++q) {

@@ -90,6 +90,13 @@ void set_pdl_scope(bool on);
 
 void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st);
 
+// Tuning switches: a runtime override (irk_set_option) or the environment
+// variable of the same name, else `dflt`.  Read when a graph is recorded;
+// every override bumps option_generation() so solvers re-record.
+long long option(const char* name, long long dflt);
+void set_option(const char* name, long long value);
+unsigned option_generation();
+
 // Stage operator y_i = M z_i + sum_j c_ij K z_j (c = ht*A), M/K sharing one
 // DIA pattern; one pass over both value arrays for all s stage vectors.
 struct StageCoef {

@@ -526,10 +526,7 @@ int DeviceSolver::matrix_format(int which) const { return which == 0 ? M_.fmt : 
 namespace {
 // IRK_ZR=0: levels >= 1 recompute wd .* r on the fly instead of reading the
 // copy the restriction wrote (A/B switch)
-bool zr_on() {
-    static const bool on = !(std::getenv("IRK_ZR") && std::string(std::getenv("IRK_ZR")) == "0");
-    return on;
-}
+bool zr_on() { return dev::option("IRK_ZR", 1) != 0; }
 }  // namespace
 
 void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
@@ -749,8 +746,13 @@ void DeviceSolver::record_iteration() {
         record_stage_op(slot(gb_.Z, jp, stride_, 0), slot(gb_.V, jp, stride_, 1));
     }
     if (ortho_ == 1) {
+        // programmatic launches: the block-dot's static loads overlap the
+        // operator's tail, the update's the block-dot's scalar tail
+        // (IRK_PDL_DGS=0 turns this off)
+        dev::set_pdl_scope(dev::option("IRK_PDL_DGS", 1) != 0);
         dev::gm_dgs_dot(gb_, 0, st_);
         dev::gm_dgs_update(gb_, st_);
+        dev::set_pdl_scope(false);
         return;
     }
     dev::gm_blockdot(gb_, 1, st_);
@@ -1052,7 +1054,8 @@ int DeviceSolver::prepare(const GmresConfig& cfg, bool lift, bool forcing) {
     const bool want_cond = !no_cond;
     if (g_restart_ != restart || g_iter_ != max_iter || g_rtol_ != cfg.rel_tol ||
         g_lift_ != lift || g_forcing_ != forcing || g_side_ != side_ ||
-        (graph_mode_ == 1) != want_cond) {
+        (graph_mode_ == 1) != want_cond || g_opt_gen_ != dev::option_generation()) {
+        g_opt_gen_ = dev::option_generation();
         bool ok = false;
         if (want_cond) {
             try {

@@ -193,6 +193,7 @@ private:
     int graph_mode_ = -1;  // 1 conditional nodes, 0 host-driven loop
     bool g_lift_ = false, g_forcing_ = false;
     int g_restart_ = -1, g_iter_ = -1;
+    unsigned g_opt_gen_ = ~0u;  // dev::option_generation() the graphs were recorded with
     double g_rtol_ = -1.0;
     int launches_per_iter_ = 0;
     std::array<int, 4> launch_counts_{};
