@@ -145,10 +145,12 @@ const T* DeviceSolver::upload_array(const std::vector<T>& h) {
 void DeviceSolver::upload_values(dev::Mat& m, const std::vector<double>& vals, double omega) {
     // Small operators keep fp64 values: their kernels are latency-bound and a
     // dictionary lookup is one more dependent memory trip.
-    static const long long min_rows =
-        std::getenv("IRK_CODES_MIN_ROWS") ? std::atoll(std::getenv("IRK_CODES_MIN_ROWS")) : 100000;
+    const long long min_rows = dev::option("IRK_CODES_MIN_ROWS", 100000);
     const bool small = std::max(m.rows, m.cols) < min_rows;
     Dict d = compress_values_ && !small ? encode(vals) : Dict{};
+    // u16 dictionaries (up to 512 KB) are L2 gathers: only worth it where the
+    // operator is big enough for its value bytes to dominate
+    if (d.vf == dev::kU16 && std::max(m.rows, m.cols) < dev::option("IRK_U16_MIN_ROWS", 0)) d = Dict{};
     m.vf = d.vf;
     if (d.vf == dev::kF64) {
         m.val = upload_array(vals);
@@ -338,6 +340,17 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
             std::getenv("IRK_CSRV_PER_LANE") ? std::atof(std::getenv("IRK_CSRV_PER_LANE")) : 3.0;
         int g = 2;
         while (g < 32 && per_lane * g < avg) g *= 2;
+        // fewer lanes when the grid would spill just past one wave of
+        // resident threads (a second, nearly empty wave costs a full row trip)
+        if (dev::option("IRK_CSRV_WAVE_CAP", 1) != 0) {
+            int dev_id = 0, sms = 148, tpm = 2048;
+            cudaGetDevice(&dev_id);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev_id);
+            cudaDeviceGetAttribute(&tpm, cudaDevAttrMaxThreadsPerMultiProcessor, dev_id);
+            const long long wave = static_cast<long long>(sms) * tpm;
+            const long long thr = static_cast<long long>(A.rows) * g;
+            if (thr > wave && thr < 2 * wave && g > 2) g /= 2;
+        }
         m.fmt = dev::kCsrVec;
         m.lanes = g;
         m.ptr = upload_array(A.ptr);

@@ -21,7 +21,9 @@ import paper_2010_11377_b200 as P  # noqa: E402
 from paper_2010_11377_b200 import _abi  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("switches", nargs="+")
+ap.add_argument("switches", nargs="*")
+ap.add_argument("--construct", default=None,
+                help="NAME=a,b: one solver per value (set before construction), alternated")
 ap.add_argument("--rounds", type=int, default=6)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--cells", type=int, default=1024)
@@ -32,12 +34,27 @@ for sw in args.switches:
     k, v = sw.split("=")
     names.append(k)
     values.append([int(x) for x in v.split(",")])
-variants = list(itertools.product(*values))
-
+L = _abi.lib()
 prob = P.make_heat_setup(args.cells)
 table = P.make_radau_iia(args.s)
-Pc = P.BlockPreconditioner(prob.M, prob.F, P.precond_coeff(table, P.CoeffKind.LowerFactor), 1e-3, table=table)
-L = _abi.lib()
+solvers = {}
+cname, cvals = None, [None]
+if args.construct:
+    cname, cv = args.construct.split("=")
+    cvals = [int(x) for x in cv.split(",")]
+for cvv in cvals:
+    if cname:
+        _abi.check(L.irk_set_option(cname.encode(), cvv))
+    solvers[cvv] = P.BlockPreconditioner(prob.M, prob.F, P.precond_coeff(table, P.CoeffKind.LowerFactor),
+                                         1e-3, table=table)
+    solvers[cvv]._dev  # construct now
+if cname:
+    names.insert(0, cname)
+    values.insert(0, cvals)
+else:
+    names.insert(0, "_")
+    values.insert(0, [None])
+variants = list(itertools.product(*values))
 u0 = prob.initial(0.01, 1)
 d_u = torch.from_numpy(u0).cuda()
 d_un = torch.empty_like(d_u)
@@ -45,7 +62,7 @@ cfg = P.GmresConfig(restart=50).c()
 rep = _abi.irk_report()
 
 
-def step():
+def step(Pc):
     _abi.check(L.irkdev_step_device(Pc._dev._h, C.c_void_p(d_u.data_ptr()), None, C.byref(cfg),
                                     C.c_void_p(d_un.data_ptr()), None, C.byref(rep)))
     return rep.solve_seconds * 1e3, rep.iterations
@@ -55,14 +72,15 @@ times = {v: [] for v in variants}
 its = {}
 for r in range(args.rounds):
     for v in variants:
-        for k, x in zip(names, v):
+        for k, x in zip(names[1:], v[1:]):
             _abi.check(L.irk_set_option(k.encode(), x))
-        step()
+        Pc = solvers[v[0]]
+        step(Pc)
         for _ in range(args.reps):
-            t, it = step()
+            t, it = step(Pc)
             times[v].append(t)
             its[v] = it
 for v in variants:
-    label = " ".join(f"{k}={x}" for k, x in zip(names, v))
+    label = " ".join(f"{k}={x}" for k, x in zip(names, v) if k != "_")
     ts = times[v]
     print(f"{label:40s} iterations {its[v]}  min {min(ts):.3f}  med {statistics.median(ts):.3f} ms")
