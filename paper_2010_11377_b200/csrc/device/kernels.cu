@@ -502,6 +502,111 @@ __global__ void __launch_bounds__(256) k_dense_mv(int n, const double* __restric
     }
 }
 
+// Bottom V-cycle (see BotDesc).  Every row sum is sequential in CSR order
+// from 0.0 with the epilogues of the level kernels it replaces (kEResid with
+// x = wd .* r, kEPlain, k_dense_mv, kEProlong, kESmooth): bit-identical.
+constexpr int kBotThreads = 1024;
+__global__ void __launch_bounds__(kBotThreads) k_bottom(BotDesc d, const double* __restrict__ r_in,
+                                                         double* __restrict__ z_out) {
+    pdl_trigger();
+    extern __shared__ __align__(16) char bsm[];
+    // static operators first: this copy overlaps the predecessor's tail
+    {
+        const int4* src = reinterpret_cast<const int4*>(d.blob);
+        int4* dst = reinterpret_cast<int4*>(bsm);
+        const int nq = d.bytes / 16;
+        for (int q = threadIdx.x; q < nq; q += kBotThreads) dst[q] = __ldg(src + q);
+    }
+    auto I = [&](int off) { return reinterpret_cast<const int*>(bsm + off); };
+    auto U = [&](int off) { return reinterpret_cast<const unsigned short*>(bsm + off); };
+    auto D = [&](int off) { return reinterpret_cast<const double*>(bsm + off); };
+    // level vectors r_l, t_l, z_l (l = 0..nl; the coarsest has r and z)
+    double* vr[kMaxBot + 1];
+    double* vt[kMaxBot + 1];
+    double* vz[kMaxBot + 1];
+    {
+        double* p = reinterpret_cast<double*>(bsm + d.vec);
+        for (int l = 0; l <= d.nl; ++l) {
+            const int n = l < d.nl ? d.lv[l].n : d.nc;
+            vr[l] = p;
+            vt[l] = p + n;
+            vz[l] = p + 2 * n;
+            p += 3 * n;
+        }
+    }
+    pdl_wait();
+    for (int i = threadIdx.x; i < d.lv[0].n; i += kBotThreads) vr[0][i] = r_in[i];
+    __syncthreads();
+    for (int l = 0; l < d.nl; ++l) {
+        const BotLevel& L = d.lv[l];
+        const int* ap = I(L.a_ptr);
+        const unsigned short* ai = U(L.a_idx);
+        const double* av = D(L.a_val);
+        const double* wd = D(L.wd);
+        const double* r = vr[l];
+        double* t = vt[l];
+        // t = r - A (wd .* r)
+        for (int i = threadIdx.x; i < L.n; i += kBotThreads) {
+            double sum = 0.0;
+            for (int k = ap[i]; k < ap[i + 1]; ++k) {
+                const int c = ai[k];
+                sum += av[k] * (wd[c] * r[c]);
+            }
+            t[i] = r[i] - sum;
+        }
+        __syncthreads();
+        // r_{l+1} = R t
+        const int nn = l + 1 < d.nl ? d.lv[l + 1].n : d.nc;
+        const int* rp = I(L.r_ptr);
+        const unsigned short* ri = U(L.r_idx);
+        const double* rv = D(L.r_val);
+        for (int i = threadIdx.x; i < nn; i += kBotThreads) {
+            double sum = 0.0;
+            for (int k = rp[i]; k < rp[i + 1]; ++k) sum += rv[k] * t[ri[k]];
+            vr[l + 1][i] = sum;
+        }
+        __syncthreads();
+    }
+    {
+        const double* A = D(d.cinv);
+        const int n = d.nc;
+        for (int i = threadIdx.x; i < n; i += kBotThreads) {
+            double sum = 0.0;
+            for (int j = 0; j < n; ++j) sum += A[i * n + j] * vr[d.nl][j];
+            vz[d.nl][i] = sum;
+        }
+        __syncthreads();
+    }
+    for (int l = d.nl - 1; l >= 0; --l) {
+        const BotLevel& L = d.lv[l];
+        const double* wd = D(L.wd);
+        const double* r = vr[l];
+        double* t = vt[l];
+        const int* pp = I(L.p_ptr);
+        const unsigned short* pi = U(L.p_idx);
+        const double* pv = D(L.p_val);
+        const double* zc = vz[l + 1];
+        // t = wd .* r + P z_{l+1}
+        for (int i = threadIdx.x; i < L.n; i += kBotThreads) {
+            double sum = 0.0;
+            for (int k = pp[i]; k < pp[i + 1]; ++k) sum += pv[k] * zc[pi[k]];
+            t[i] = wd[i] * r[i] + sum;
+        }
+        __syncthreads();
+        // z = t + wd .* (r - A t)
+        const int* ap = I(L.a_ptr);
+        const unsigned short* ai = U(L.a_idx);
+        const double* av = D(L.a_val);
+        double* z = l == 0 ? z_out : vz[l];
+        for (int i = threadIdx.x; i < L.n; i += kBotThreads) {
+            double sum = 0.0;
+            for (int k = ap[i]; k < ap[i + 1]; ++k) sum += av[k] * t[ai[k]];
+            z[i] = t[i] + wd[i] * (r[i] - sum);
+        }
+        __syncthreads();
+    }
+}
+
 // Large coarsest level (n*n does not fit shared memory): one thread per row.
 __global__ void k_dense_mv_big(int n, const double* __restrict__ A, VecRef rr, VecRef zr) {
     pdl_trigger();
@@ -1515,6 +1620,15 @@ void sweep_dia(const Mat& K, VecRef w, VecRef v, const SweepTerms& t, double* st
     case kU16: launch(k_sweep_dia<kU16, 0>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out); break;
     default: launch(k_sweep_dia<kF64, 0>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out); break;
     }
+}
+
+void bottom_cycle(const BotDesc& d, const double* r_in, double* z_out, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        IRK_CUDA_CHECK(cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    launch(k_bottom, 1, kBotThreads, d.smem, st, d, r_in, z_out);
 }
 
 void combine(VecRef v, const SweepTerms& t, VecRef out, int n, cudaStream_t st) {

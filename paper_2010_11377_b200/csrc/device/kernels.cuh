@@ -124,6 +124,31 @@ void axpy(double alpha, const double* x, VecRef y, int n, cudaStream_t st);
 
 // Coarsest-level solve z = Ainv r (dense row-major inverse).
 void dense_mv(int n, const double* Ainv, VecRef r, VecRef z, cudaStream_t st);
+
+// Bottom of a V-cycle in one CTA (levels b..L-1 of a hierarchy whose
+// operators fit in shared memory): residual, restriction, dense coarse solve,
+// prolongation and smoothing with barriers between phases.  The operators are
+// packed once into a blob (CSR, u16 column indices, fp64 values, 16-byte
+// aligned arrays; offsets below are byte offsets into it) that the CTA copies
+// to shared memory before waiting on its predecessor.
+constexpr int kMaxBot = 4;
+struct BotLevel {
+    int n;
+    int a_ptr, a_idx, a_val;  // A_l
+    int p_ptr, p_idx, p_val;  // P_l (n x n_{l+1})
+    int r_ptr, r_idx, r_val;  // R_l (n_{l+1} x n)
+    int wd;                   // omega / a_ii
+};
+struct BotDesc {
+    const char* blob = nullptr;
+    int bytes = 0;            // blob bytes (multiple of 16)
+    int nl = 0;               // smoothed levels in the kernel (the dense one excluded)
+    BotLevel lv[kMaxBot];
+    int nc = 0, cinv = 0;     // coarsest size, dense inverse offset
+    int vec = 0;              // smem offset of the level vectors
+    int smem = 0;             // dynamic smem bytes
+};
+void bottom_cycle(const BotDesc& d, const double* r_in, double* z_out, cudaStream_t st);
 // z = wd .* r (first Jacobi sweep from a zero iterate, amg.cpp:119-124).
 void wd_times_r(int n, const double* wd, VecRef r, double* z, cudaStream_t st);
 

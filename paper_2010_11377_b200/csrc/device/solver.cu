@@ -487,6 +487,7 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
             dh.lv[l] = d;
         }
         dh.nc = h.levels.back().A.rows;
+        build_bottom(dh, h);
         dh.cinv = alloc(static_cast<size_t>(dh.nc) * dh.nc);
         IRK_CUDA_CHECK(cudaMemcpy(dh.cinv, h.coarse_inverse.data(),
                                   sizeof(double) * dh.nc * dh.nc, cudaMemcpyHostToDevice));
@@ -536,6 +537,61 @@ int DeviceSolver::matrix_format(int which) const { return which == 0 ? M_.fmt : 
 //   r_{l+1} = R t          restriction
 //   t = wd.*r + P z_{l+1}  prolongation fused with the pre-smoothed iterate
 //   z = t + wd.*(r - A t)  post-smoothing sweep
+// Packs the deepest levels whose operators fit one CTA's shared memory into
+// the bottom kernel's blob (smallest first level b >= 1 that fits).
+void DeviceSolver::build_bottom(DevHier& dh, const Hierarchy& h) {
+    const int L = h.n_levels();
+    if (dev::option("IRK_BOTTOM", 1) == 0 || L < 3) return;
+    if (h.params.pre_sweeps != 1 || h.params.post_sweeps != 1) return;
+    const int budget = 225 * 1024;
+    for (int b = 1; b <= L - 2; ++b) {
+        if (L - 1 - b > dev::kMaxBot) continue;
+        std::vector<char> blob;
+        auto put = [&](const void* p, size_t bytes) {
+            const int off = static_cast<int>(blob.size());
+            blob.resize((blob.size() + bytes + 15) / 16 * 16, 0);
+            if (bytes) std::memcpy(blob.data() + off, p, bytes);
+            return off;
+        };
+        bool ok = true;
+        auto put_csr = [&](const Csr& A, int& po, int& io, int& vo) {
+            if (A.cols > 65535) ok = false;
+            std::vector<unsigned short> ix(A.idx.begin(), A.idx.end());
+            po = put(A.ptr.data(), sizeof(int) * A.ptr.size());
+            io = put(ix.data(), sizeof(unsigned short) * ix.size());
+            vo = put(A.val.data(), sizeof(double) * A.val.size());
+        };
+        dev::BotDesc d;
+        d.nl = L - 1 - b;
+        long long vec = 0;
+        for (int q = 0; q < d.nl; ++q) {
+            const AmgLevel& lev = h.levels[b + q];
+            dev::BotLevel& bl = d.lv[q];
+            bl.n = lev.A.rows;
+            put_csr(lev.A, bl.a_ptr, bl.a_idx, bl.a_val);
+            put_csr(lev.P, bl.p_ptr, bl.p_idx, bl.p_val);
+            put_csr(lev.R, bl.r_ptr, bl.r_idx, bl.r_val);
+            std::vector<double> wd(bl.n);
+            for (int i = 0; i < bl.n; ++i) wd[i] = h.params.jacobi_weight * lev.inv_diag[i];
+            bl.wd = put(wd.data(), sizeof(double) * wd.size());
+            vec += 3LL * bl.n;
+        }
+        d.nc = h.levels.back().A.rows;
+        d.cinv = put(h.coarse_inverse.data(), sizeof(double) * h.coarse_inverse.size());
+        vec += 3LL * d.nc;
+        d.bytes = static_cast<int>(blob.size());
+        d.vec = d.bytes;
+        const long long total = d.bytes + 8 * vec;
+        if (!ok || total > budget) continue;
+        d.smem = static_cast<int>(total);
+        std::vector<char> padded = blob;
+        d.blob = upload_array(padded);
+        dh.bot = d;
+        dh.bot_from = b;
+        return;
+    }
+}
+
 namespace {
 // IRK_ZR=0: levels >= 1 recompute wd .* r on the fly instead of reading the
 // copy the restriction wrote (A/B switch)
@@ -553,7 +609,11 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
     static const int pdl_from = std::getenv("IRK_PDL_COARSE") ? std::atoi(std::getenv("IRK_PDL_COARSE")) : 2;
     auto scope = [&](int l) { dev::set_pdl_scope(pdl_from >= 0 && l >= pdl_from); };
     auto out_of = [&](int l) { return l == first ? z0 : dev::plain(H.lv[l].z); };
-    for (int l = first; l + 1 < L; ++l) {
+    // levels >= bot run in the single-CTA bottom kernel
+    const int bot = dev::option("IRK_BOTTOM", 1) != 0 && H.bot_from > first && pre == 1 && post == 1
+                        ? H.bot_from : -1;
+    const int down_end = bot > 0 ? bot : L - 1;
+    for (int l = first; l < down_end; ++l) {
         DevLevel& d = H.lv[l];
         scope(l);
         dev::SpmvArgs a;
@@ -586,15 +646,20 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
         dev::SpmvArgs ra;
         ra.x = dev::plain(d.t);
         ra.y = dev::plain(H.lv[l + 1].r);
-        if (zr_on() && pre == 1 && l + 2 < L) {
+        if (zr_on() && pre == 1 && l + 2 < L && l + 1 != bot) {
             ra.y2 = H.lv[l + 1].zr;
             ra.wd2 = H.lv[l + 1].wd;
         }
         dev::spmv(d.R, dev::kXPlain, dev::kEPlain, ra, st_);
     }
-    scope(L - 1);
-    dev::dense_mv(H.nc, H.cinv, rhs_of(L - 1), out_of(L - 1), st_);
-    for (int l = L - 2; l >= first; --l) {
+    if (bot > 0) {
+        scope(bot);
+        dev::bottom_cycle(H.bot, H.lv[bot].r, H.lv[bot].z, st_);
+    } else {
+        scope(L - 1);
+        dev::dense_mv(H.nc, H.cinv, rhs_of(L - 1), out_of(L - 1), st_);
+    }
+    for (int l = (bot > 0 ? bot - 1 : L - 2); l >= first; --l) {
         DevLevel& d = H.lv[l];
         scope(l);
         dev::SpmvArgs pa;

@@ -66,6 +66,8 @@ struct DevHier {
     double* cinv = nullptr;
     int nc = 0;
     AmgParams prm;
+    int bot_from = -1;    // first level handled by the single-CTA bottom kernel
+    dev::BotDesc bot;
 };
 
 class DeviceSolver {
@@ -134,6 +136,7 @@ public:
 
 private:
     dev::Mat upload(const Csr& A, bool allow_dia, double omega);
+    void build_bottom(DevHier& dh, const Hierarchy& h);
     // DIA row classes (dev::kCls) for one operator or a pair sharing a pattern
     bool to_row_classes(std::vector<dev::Mat*> mats, const std::vector<const std::vector<double>*>& vals,
                         double omega);
