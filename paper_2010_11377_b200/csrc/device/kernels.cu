@@ -506,104 +506,141 @@ __global__ void __launch_bounds__(256) k_dense_mv(int n, const double* __restric
 // from 0.0 with the epilogues of the level kernels it replaces (kEResid with
 // x = wd .* r, kEPlain, k_dense_mv, kEProlong, kESmooth): bit-identical.
 constexpr int kBotThreads = 1024;
+
+// sum_{k in [b, e)} f(k), added sequentially in k order from 0.0; the
+// products of 8 consecutive entries are formed before any of them is added
+// (independent shared-memory loads in flight), so the association is the
+// plain sequential one.
+template <class F>
+__device__ __forceinline__ double ordered_sum(int b, int e, F f) {
+    double sum = 0.0;
+    int k = b;
+    for (; k + 8 <= e; k += 8) {
+        double p[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) p[q] = f(k + q);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) sum += p[q];
+    }
+    for (; k < e; ++k) sum += f(k);
+    return sum;
+}
+// (A x)_i of a bottom level, sequential in column order: SELL-32 (row i is
+// lane i % 32 of slice i / 32, entries 32 apart: conflict-free shared loads)
+// or CSR.
+__device__ __forceinline__ double bot_row_a(const BotLevel& L, const int* ap, const unsigned short* ai,
+                                            const double* av, int i, const double* x, const char* bsm) {
+    if (L.a_sell) {
+        const int base = ap[i >> 5] + (i & 31);
+        const int len = reinterpret_cast<const unsigned short*>(bsm + L.a_len)[i];
+        return ordered_sum(0, len, [&](int q) { return av[base + 32 * q] * x[ai[base + 32 * q]]; });
+    }
+    return ordered_sum(ap[i], ap[i + 1], [&](int k) { return av[k] * x[ai[k]]; });
+}
+
 __global__ void __launch_bounds__(kBotThreads) k_bottom(BotDesc d, const double* __restrict__ r_in,
                                                          double* __restrict__ z_out) {
     pdl_trigger();
     extern __shared__ __align__(16) char bsm[];
-    // static operators first: this copy overlaps the predecessor's tail
+    int stamp = 0;
+    auto mark = [&]() {
+        if (d.prof && threadIdx.x == 0 && stamp < 16) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            d.prof[stamp] = static_cast<long long>(t);
+        }
+        ++stamp;
+    };
+    mark();
+    // static operators first (all 16-byte async copies in flight at once):
+    // this copy overlaps the predecessor's tail
     {
-        const int4* src = reinterpret_cast<const int4*>(d.blob);
-        int4* dst = reinterpret_cast<int4*>(bsm);
         const int nq = d.bytes / 16;
-        for (int q = threadIdx.x; q < nq; q += kBotThreads) dst[q] = __ldg(src + q);
+        for (int q = threadIdx.x; q < nq; q += kBotThreads) {
+            const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(bsm + 16 * q));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(d.blob + 16 * q) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
     auto I = [&](int off) { return reinterpret_cast<const int*>(bsm + off); };
     auto U = [&](int off) { return reinterpret_cast<const unsigned short*>(bsm + off); };
     auto D = [&](int off) { return reinterpret_cast<const double*>(bsm + off); };
-    // level vectors r_l, t_l, z_l (l = 0..nl; the coarsest has r and z)
-    double* vr[kMaxBot + 1];
-    double* vt[kMaxBot + 1];
-    double* vz[kMaxBot + 1];
-    {
-        double* p = reinterpret_cast<double*>(bsm + d.vec);
-        for (int l = 0; l <= d.nl; ++l) {
-            const int n = l < d.nl ? d.lv[l].n : d.nc;
-            vr[l] = p;
-            vt[l] = p + n;
-            vz[l] = p + 2 * n;
-            p += 3 * n;
-        }
-    }
+    // level vectors r_l, t_l, z_l at byte offsets d.vr / d.vt / d.vz (kept as
+    // offsets from the shared base so every access compiles to LDS / STS)
+    auto V = [&](int off) { return reinterpret_cast<double*>(bsm + off); };
+    mark();
     pdl_wait();
-    for (int i = threadIdx.x; i < d.lv[0].n; i += kBotThreads) vr[0][i] = r_in[i];
+    for (int i = threadIdx.x; i < d.lv[0].n; i += kBotThreads) V(d.vr[0])[i] = r_in[i];
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+    mark();
     for (int l = 0; l < d.nl; ++l) {
         const BotLevel& L = d.lv[l];
         const int* ap = I(L.a_ptr);
         const unsigned short* ai = U(L.a_idx);
         const double* av = D(L.a_val);
         const double* wd = D(L.wd);
-        const double* r = vr[l];
-        double* t = vt[l];
+        const double* r = V(d.vr[l]);
+        double* t = V(d.vt[l]);
+        // wd .* r once per row (z_l is free during the down-sweep)
+        double* zz = V(d.vz[l]);
+        for (int i = threadIdx.x; i < L.n; i += kBotThreads) zz[i] = wd[i] * r[i];
+        __syncthreads();
         // t = r - A (wd .* r)
         for (int i = threadIdx.x; i < L.n; i += kBotThreads) {
-            double sum = 0.0;
-            for (int k = ap[i]; k < ap[i + 1]; ++k) {
-                const int c = ai[k];
-                sum += av[k] * (wd[c] * r[c]);
-            }
+            const double sum = bot_row_a(L, ap, ai, av, i, zz, bsm);
             t[i] = r[i] - sum;
         }
         __syncthreads();
+        mark();
         // r_{l+1} = R t
         const int nn = l + 1 < d.nl ? d.lv[l + 1].n : d.nc;
         const int* rp = I(L.r_ptr);
         const unsigned short* ri = U(L.r_idx);
         const double* rv = D(L.r_val);
-        for (int i = threadIdx.x; i < nn; i += kBotThreads) {
-            double sum = 0.0;
-            for (int k = rp[i]; k < rp[i + 1]; ++k) sum += rv[k] * t[ri[k]];
-            vr[l + 1][i] = sum;
-        }
+        double* rn = V(d.vr[l + 1]);
+        for (int i = threadIdx.x; i < nn; i += kBotThreads)
+            rn[i] = ordered_sum(rp[i], rp[i + 1], [&](int k) { return rv[k] * t[ri[k]]; });
         __syncthreads();
+        mark();
     }
     {
-        const double* A = D(d.cinv);
+        // inverse stored column-major in the blob (conflict-free reads)
+        const double* At = D(d.cinv);
         const int n = d.nc;
-        for (int i = threadIdx.x; i < n; i += kBotThreads) {
-            double sum = 0.0;
-            for (int j = 0; j < n; ++j) sum += A[i * n + j] * vr[d.nl][j];
-            vz[d.nl][i] = sum;
-        }
+        const double* rc = V(d.vr[d.nl]);
+        for (int i = threadIdx.x; i < n; i += kBotThreads)
+            V(d.vz[d.nl])[i] = ordered_sum(0, n, [&](int j) { return At[j * n + i] * rc[j]; });
         __syncthreads();
+        mark();
     }
     for (int l = d.nl - 1; l >= 0; --l) {
         const BotLevel& L = d.lv[l];
         const double* wd = D(L.wd);
-        const double* r = vr[l];
-        double* t = vt[l];
+        const double* r = V(d.vr[l]);
+        double* t = V(d.vt[l]);
         const int* pp = I(L.p_ptr);
         const unsigned short* pi = U(L.p_idx);
         const double* pv = D(L.p_val);
-        const double* zc = vz[l + 1];
+        const double* zc = V(d.vz[l + 1]);
         // t = wd .* r + P z_{l+1}
         for (int i = threadIdx.x; i < L.n; i += kBotThreads) {
-            double sum = 0.0;
-            for (int k = pp[i]; k < pp[i + 1]; ++k) sum += pv[k] * zc[pi[k]];
+            const double sum = ordered_sum(pp[i], pp[i + 1], [&](int k) { return pv[k] * zc[pi[k]]; });
             t[i] = wd[i] * r[i] + sum;
         }
         __syncthreads();
+        mark();
         // z = t + wd .* (r - A t)
         const int* ap = I(L.a_ptr);
         const unsigned short* ai = U(L.a_idx);
         const double* av = D(L.a_val);
-        double* z = l == 0 ? z_out : vz[l];
+        double* z = l == 0 ? z_out : V(d.vz[l]);
         for (int i = threadIdx.x; i < L.n; i += kBotThreads) {
-            double sum = 0.0;
-            for (int k = ap[i]; k < ap[i + 1]; ++k) sum += av[k] * t[ai[k]];
+            const double sum = bot_row_a(L, ap, ai, av, i, t, bsm);
             z[i] = t[i] + wd[i] * (r[i] - sum);
         }
         __syncthreads();
+        mark();
     }
 }
 

@@ -134,6 +134,8 @@ void dense_mv(int n, const double* Ainv, VecRef r, VecRef z, cudaStream_t st);
 constexpr int kMaxBot = 4;
 struct BotLevel {
     int n;
+    int a_sell;               // A_l stored as SELL-32 (a_ptr = slice offsets, a_len = row lengths)
+    int a_len;
     int a_ptr, a_idx, a_val;  // A_l
     int p_ptr, p_idx, p_val;  // P_l (n x n_{l+1})
     int r_ptr, r_idx, r_val;  // R_l (n_{l+1} x n)
@@ -146,7 +148,9 @@ struct BotDesc {
     BotLevel lv[kMaxBot];
     int nc = 0, cinv = 0;     // coarsest size, dense inverse offset
     int vec = 0;              // smem offset of the level vectors
+    int vr[kMaxBot + 1], vt[kMaxBot + 1], vz[kMaxBot + 1];  // per-level vector offsets
     int smem = 0;             // dynamic smem bytes
+    long long* prof = nullptr; // optional phase timestamps (globaltimer ns, 16 slots)
 };
 void bottom_cycle(const BotDesc& d, const double* r_in, double* z_out, cudaStream_t st);
 // z = wd .* r (first Jacobi sweep from a zero iterate, amg.cpp:119-124).

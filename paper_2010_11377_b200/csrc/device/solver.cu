@@ -544,6 +544,7 @@ void DeviceSolver::build_bottom(DevHier& dh, const Hierarchy& h) {
     if (dev::option("IRK_BOTTOM", 1) == 0 || L < 3) return;
     if (h.params.pre_sweeps != 1 || h.params.post_sweeps != 1) return;
     const int budget = 225 * 1024;
+    bool force_csr = false;
     for (int b = 1; b <= L - 2; ++b) {
         if (L - 1 - b > dev::kMaxBot) continue;
         std::vector<char> blob;
@@ -561,6 +562,36 @@ void DeviceSolver::build_bottom(DevHier& dh, const Hierarchy& h) {
             io = put(ix.data(), sizeof(unsigned short) * ix.size());
             vo = put(A.val.data(), sizeof(double) * A.val.size());
         };
+        // A_l as SELL-32 (conflict-free shared loads) unless the padding
+        // would not fit, then CSR
+        auto put_sell = [&](const Csr& A, dev::BotLevel& bl) {
+            if (A.cols > 65535) ok = false;
+            const int ns = (A.rows + 31) / 32;
+            std::vector<int> sp(ns + 1, 0);
+            std::vector<unsigned short> len(A.rows);
+            for (int sl = 0; sl < ns; ++sl) {
+                int mx = 0;
+                for (int r = sl * 32; r < std::min(A.rows, sl * 32 + 32); ++r) {
+                    len[r] = static_cast<unsigned short>(A.ptr[r + 1] - A.ptr[r]);
+                    mx = std::max(mx, A.ptr[r + 1] - A.ptr[r]);
+                }
+                sp[sl + 1] = sp[sl] + 32 * mx;
+            }
+            std::vector<unsigned short> ix(sp[ns], 0);
+            std::vector<double> vv(sp[ns], 0.0);
+            for (int r = 0; r < A.rows; ++r)
+                for (int q = 0; q < A.ptr[r + 1] - A.ptr[r]; ++q) {
+                    const size_t e = static_cast<size_t>(sp[r / 32]) + 32 * q + (r % 32);
+                    ix[e] = static_cast<unsigned short>(A.idx[A.ptr[r] + q]);
+                    vv[e] = A.val[A.ptr[r] + q];
+                }
+            bl.a_sell = 1;
+            bl.a_ptr = put(sp.data(), sizeof(int) * sp.size());
+            bl.a_len = put(len.data(), sizeof(unsigned short) * len.size());
+            bl.a_idx = put(ix.data(), sizeof(unsigned short) * ix.size());
+            bl.a_val = put(vv.data(), sizeof(double) * vv.size());
+        };
+        const bool sell = dev::option("IRK_BOTTOM_SELL", 1) != 0 && !force_csr;
         dev::BotDesc d;
         d.nl = L - 1 - b;
         long long vec = 0;
@@ -568,7 +599,13 @@ void DeviceSolver::build_bottom(DevHier& dh, const Hierarchy& h) {
             const AmgLevel& lev = h.levels[b + q];
             dev::BotLevel& bl = d.lv[q];
             bl.n = lev.A.rows;
-            put_csr(lev.A, bl.a_ptr, bl.a_idx, bl.a_val);
+            if (sell) {
+                put_sell(lev.A, bl);
+            } else {
+                bl.a_sell = 0;
+                bl.a_len = 0;
+                put_csr(lev.A, bl.a_ptr, bl.a_idx, bl.a_val);
+            }
             put_csr(lev.P, bl.p_ptr, bl.p_idx, bl.p_val);
             put_csr(lev.R, bl.r_ptr, bl.r_idx, bl.r_val);
             std::vector<double> wd(bl.n);
@@ -577,13 +614,39 @@ void DeviceSolver::build_bottom(DevHier& dh, const Hierarchy& h) {
             vec += 3LL * bl.n;
         }
         d.nc = h.levels.back().A.rows;
-        d.cinv = put(h.coarse_inverse.data(), sizeof(double) * h.coarse_inverse.size());
+        {
+            // column-major copy of the dense inverse
+            const int nc = h.levels.back().A.rows;
+            std::vector<double> ct(h.coarse_inverse.size());
+            for (int i = 0; i < nc; ++i)
+                for (int j = 0; j < nc; ++j) ct[static_cast<size_t>(j) * nc + i] = h.coarse_inverse[static_cast<size_t>(i) * nc + j];
+            d.cinv = put(ct.data(), sizeof(double) * ct.size());
+        }
         vec += 3LL * d.nc;
         d.bytes = static_cast<int>(blob.size());
         d.vec = d.bytes;
+        {
+            int off = d.vec;
+            for (int q = 0; q <= d.nl; ++q) {
+                const int nq = q < d.nl ? d.lv[q].n : d.nc;
+                d.vr[q] = off;
+                d.vt[q] = off + 8 * nq;
+                d.vz[q] = off + 16 * nq;
+                off += 24 * nq;
+            }
+        }
         const long long total = d.bytes + 8 * vec;
+        if (ok && total > budget && !force_csr) {
+            force_csr = true;  // retry this b with CSR operators
+            --b;
+            continue;
+        }
+        force_csr = false;
         if (!ok || total > budget) continue;
         d.smem = static_cast<int>(total);
+        if (std::getenv("IRK_SETUP_TIMING"))
+            std::fprintf(stderr, "bottom kernel: levels %d..%d, A %s, blob %d B, smem %d B\n", b, L - 1,
+                         d.lv[0].a_sell ? "SELL-32" : "CSR", d.bytes, d.smem);
         std::vector<char> padded = blob;
         d.blob = upload_array(padded);
         dh.bot = d;
@@ -1351,6 +1414,58 @@ double DeviceSolver::time_kernel(int which, int reps) {
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         g_restart_ = -1;  // graphs captured the old use_cond; rebuild on the next step
+        return static_cast<double>(ms) / reps;
+    }
+    if (which == 50 || which == 51) {
+        // bottom kernel of hierarchy 0 back to back (50), or alternating with
+        // the level-1 smoother SpMV (51: forces the shared-memory carveout to
+        // switch between launches)
+        DevHier& H = hier_[0];
+        check(H.bot_from > 0, "time_kernel: hierarchy 0 has no bottom kernel");
+        DevBuf prof(16 * sizeof(long long));
+        const bool want_prof = std::getenv("IRK_BOT_PROF") != nullptr;
+        if (want_prof) {
+            IRK_CUDA_CHECK(cudaMemset(prof.as<void>(), 0, 16 * sizeof(long long)));
+            H.bot.prof = prof.as<long long>();
+        }
+        cudaGraph_t gr;
+        IRK_CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+        for (int r = 0; r < reps; ++r) {
+            dev::bottom_cycle(H.bot, H.lv[H.bot_from].r, H.lv[H.bot_from].z, st_);
+            if (which == 51) {
+                dev::SpmvArgs a;
+                a.x = dev::plain(H.lv[1].t);
+                a.r = dev::plain(H.lv[1].r);
+                a.wd = H.lv[1].wd;
+                a.y = dev::plain(H.lv[1].u);
+                dev::spmv(H.lv[1].A, dev::kXPlain, dev::kESmooth, a, st_);
+            }
+        }
+        IRK_CUDA_CHECK(cudaStreamEndCapture(st_, &gr));
+        cudaGraphExec_t ge;
+        IRK_CUDA_CHECK(cudaGraphInstantiate(&ge, gr, 0));
+        cudaGraphDestroy(gr);
+        IRK_CUDA_CHECK(cudaGraphLaunch(ge, st_));
+        cudaEvent_t e0, e1;
+        IRK_CUDA_CHECK(cudaEventCreate(&e0));
+        IRK_CUDA_CHECK(cudaEventCreate(&e1));
+        IRK_CUDA_CHECK(cudaEventRecord(e0, st_));
+        IRK_CUDA_CHECK(cudaGraphLaunch(ge, st_));
+        IRK_CUDA_CHECK(cudaEventRecord(e1, st_));
+        IRK_CUDA_CHECK(cudaEventSynchronize(e1));
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaGraphExecDestroy(ge);
+        if (want_prof) {
+            long long t[16];
+            IRK_CUDA_CHECK(cudaMemcpy(t, prof.as<void>(), sizeof(t), cudaMemcpyDeviceToHost));
+            std::fprintf(stderr, "bottom phases (ns from start):");
+            for (int q = 1; q < 16 && t[q]; ++q) std::fprintf(stderr, " %lld", t[q] - t[0]);
+            std::fprintf(stderr, "\n");
+            H.bot.prof = nullptr;
+        }
         return static_cast<double>(ms) / reps;
     }
     if (which >= 30 && which < 40) {
