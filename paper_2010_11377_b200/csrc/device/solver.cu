@@ -636,6 +636,9 @@ void DeviceSolver::build_bottom(DevHier& dh, const Hierarchy& h) {
             }
         }
         const long long total = d.bytes + 8 * vec;
+        if (std::getenv("IRK_SETUP_TIMING"))
+            std::fprintf(stderr, "bottom candidate: levels %d..%d, A %s: %lld B%s\n", b, L - 1,
+                         force_csr ? "CSR" : "SELL-32", total, total > budget ? " (too big)" : "");
         if (ok && total > budget && !force_csr) {
             force_csr = true;  // retry this b with CSR operators
             --b;
