@@ -363,8 +363,14 @@ void launch_spmv(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ stage op
+// Resident CTAs per SM the stage operator is compiled for: unbounded, the
+// fully unrolled 7-point stencil keeps 7 S loads in flight and needs 88-150
+// registers (2 CTAs / SM); these bounds trade part of that for occupancy
+// (same-box A/B, profiles/r1/ab33_stage_op_occupancy.txt).
+constexpr int stage_op_min_blocks(int S) { return S <= 2 ? 8 : S <= 4 ? 6 : 4; }
+
 template <int S, int VF, int ND>
-__global__ void __launch_bounds__(256) k_stage_op_dia(Mat M, Mat K, StageCoef cf, VecRef zr,
+__global__ void __launch_bounds__(256, stage_op_min_blocks(S)) k_stage_op_dia(Mat M, Mat K, StageCoef cf, VecRef zr,
                                                       VecRef yr) {
     __shared__ double s_tm[VF == kU8 ? 256 : 1];
     __shared__ double s_tk[VF == kU8 ? 256 : 1];
