@@ -237,13 +237,33 @@ __global__ void __launch_bounds__(256) k_spmv_sell(Mat A, SpmvArgs a) {
     // the slice structure is static: read it before waiting on the predecessor
     const int base = __ldg(A.sptr + slice);
     const int len = (__ldg(A.sptr + slice + 1) - base) >> 5;
+    // the first entries' columns and values are static too
+    constexpr int kPre = 4;
+    int c0[kPre];
+    double v0[kPre];
+#pragma unroll
+    for (int k = 0; k < kPre; ++k) {
+        c0[k] = 0;
+        v0[k] = 0.0;
+        if (k < len) {
+            c0[k] = __ldg(A.idx + base + k * 32 + lane);
+            v0[k] = vfetch<VF>(A.val, base + k * 32 + lane, tab);
+        }
+    }
     pdl_wait();
     const double* r = a.r.base ? a.r.get() : nullptr;
     const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
     const double* __restrict__ wd = a.wd;
     double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kPre; ++k)
+        if (k < len) {
+            const int c = c0[k];
+            const double xv = XM == kXWdR ? wd[c] * r[c] : x[c];
+            s += v0[k] * xv;
+        }
 #pragma unroll 4
-    for (int k = 0; k < len; ++k) {
+    for (int k = kPre; k < len; ++k) {
         const int c = __ldg(A.idx + base + k * 32 + lane);
         const double xv = XM == kXWdR ? wd[c] * r[c] : x[c];
         s += vfetch<VF>(A.val, base + k * 32 + lane, tab) * xv;
@@ -278,6 +298,19 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
     const int chunks = (maxlen + G * MM - 1) / (G * MM);
+    // the first chunk's columns and values are static too
+    int c0[MM];
+    double v0[MM];
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+        const int k = m * G + lane;
+        c0[m] = 0;
+        v0[m] = 0.0;
+        if (k < len) {
+            c0[m] = __ldg(A.idx + lo + k);
+            v0[m] = vfetch<VF>(A.val, lo + k, tab);
+        }
+    }
     pdl_wait();
     const double* r = a.r.base ? a.r.get() : nullptr;
     const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
@@ -290,9 +323,9 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
             const int k = ch * G * MM + m * G + lane;
             p[m] = 0.0;
             if (k < len) {
-                const int c = __ldg(A.idx + lo + k);
+                const int c = ch == 0 ? c0[m] : __ldg(A.idx + lo + k);
                 const double xv = XM == kXWdR ? wd[c] * r[c] : x[c];
-                p[m] = vfetch<VF>(A.val, lo + k, tab) * xv;
+                p[m] = (ch == 0 ? v0[m] : vfetch<VF>(A.val, lo + k, tab)) * xv;
             }
         }
 #pragma unroll
