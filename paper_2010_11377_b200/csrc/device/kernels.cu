@@ -238,7 +238,10 @@ __global__ void __launch_bounds__(256) k_spmv_sell(Mat A, SpmvArgs a) {
     const int base = __ldg(A.sptr + slice);
     const int len = (__ldg(A.sptr + slice + 1) - base) >> 5;
     // the first entries' columns and values are static too
-    constexpr int kPre = 4;
+#ifndef IRK_SELL_PRE
+#define IRK_SELL_PRE 6
+#endif
+    constexpr int kPre = IRK_SELL_PRE;
     int c0[kPre];
     double v0[kPre];
 #pragma unroll
