@@ -289,7 +289,10 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
     __shared__ double s_tab[VF == kU8 ? 256 : 1];
     __shared__ double s_wd[1];
     const double* tab = load_tab<VF>(A, s_tab, s_wd);
-    constexpr int MM = 4;
+#ifndef IRK_CSRV_MM
+#define IRK_CSRV_MM 4
+#endif
+    constexpr int MM = IRK_CSRV_MM;  // entries per lane per chunk
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int row = t / G;
     const int lane = threadIdx.x % G;
