@@ -400,7 +400,7 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
                            Structure structure, double ht, const AmgParams& amg,
                            std::vector<Hierarchy> hiers, int device)
     : s_(s), device_(device), At_(At), structure_(structure), ht_(ht) {
-    compress_values_ = std::getenv("IRK_NO_VALUE_CODES") == nullptr;
+    compress_values_ = dev::option("IRK_NO_VALUE_CODES", 0) == 0;
     {
         const char* o = std::getenv("IRK_ORTHO");
         ortho_ = (o && std::string(o) == "cgs2") ? 0 : 1;
@@ -444,6 +444,17 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
 
     M_ = upload(M, true, 0.0);
     K_ = upload(K, true, 0.0);
+    if (M_.fmt == dev::kDia && K_.fmt == dev::kDia && M_.nd == K_.nd &&
+        std::equal(M_.off, M_.off + M_.nd, K_.off) &&
+        !(M_.vf == K_.vf && (M_.vf == dev::kF64 || M_.vf == dev::kU8))) {
+        // the fused stage operator needs M and K in one value format (fp64 or
+        // u8 codes): e.g. SUPG K with > 256 distinct values -> both fp64
+        const bool keep = compress_values_;
+        compress_values_ = false;
+        M_ = upload(M, true, 0.0);
+        K_ = upload(K, true, 0.0);
+        compress_values_ = keep;
+    }
     lap("M, K");
     fused_op_ = M_.fmt == dev::kDia && K_.fmt == dev::kDia && M_.nd == K_.nd &&
                 std::equal(M_.off, M_.off + M_.nd, K_.off) && M_.vf == K_.vf &&

@@ -28,6 +28,7 @@ ap.add_argument("--rounds", type=int, default=6)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--cells", type=int, default=1024)
 ap.add_argument("--s", type=int, default=3)
+ap.add_argument("--dg", action="store_true", help="C4-style double glazing (u0 = 0, lift, h_t = 1e-2)")
 args = ap.parse_args()
 names, values = [], []
 for sw in args.switches:
@@ -35,8 +36,9 @@ for sw in args.switches:
     names.append(k)
     values.append([int(x) for x in v.split(",")])
 L = _abi.lib()
-prob = P.make_heat_setup(args.cells)
+prob = P.make_double_glazing_setup(args.cells, 0.005) if args.dg else P.make_heat_setup(args.cells)
 table = P.make_radau_iia(args.s)
+HT = 1e-2 if args.dg else 1e-3
 solvers = {}
 cname, cvals = None, [None]
 if args.construct:
@@ -46,7 +48,7 @@ for cvv in cvals:
     if cname:
         _abi.check(L.irk_set_option(cname.encode(), cvv))
     solvers[cvv] = P.BlockPreconditioner(prob.M, prob.F, P.precond_coeff(table, P.CoeffKind.LowerFactor),
-                                         1e-3, table=table)
+                                         HT, table=table)
     solvers[cvv]._dev  # construct now
 if cname:
     names.insert(0, cname)
@@ -55,15 +57,18 @@ else:
     names.insert(0, "_")
     values.insert(0, [None])
 variants = list(itertools.product(*values))
-u0 = prob.initial(0.01, 1)
+import numpy as np  # noqa: E402
+u0 = np.zeros(prob.M.n_rows) if args.dg else prob.initial(0.01, 1)
 d_u = torch.from_numpy(u0).cuda()
+d_lift = torch.from_numpy(np.ascontiguousarray(prob.f_lift)).cuda() if args.dg else None
 d_un = torch.empty_like(d_u)
 cfg = P.GmresConfig(restart=50).c()
 rep = _abi.irk_report()
 
 
 def step(Pc):
-    _abi.check(L.irkdev_step_device(Pc._dev._h, C.c_void_p(d_u.data_ptr()), None, C.byref(cfg),
+    lift = C.c_void_p(d_lift.data_ptr()) if d_lift is not None else None
+    _abi.check(L.irkdev_step_device(Pc._dev._h, C.c_void_p(d_u.data_ptr()), lift, C.byref(cfg),
                                     C.c_void_p(d_un.data_ptr()), None, C.byref(rep)))
     return rep.solve_seconds * 1e3, rep.iterations
 
