@@ -56,6 +56,24 @@ def test_device_fails_loudly_without_gpu():
                               table=t)
 
 
+@pytest.mark.skipif(has_gpu(), reason="checks the no-GPU failure path")
+def test_device_amg_setup_fails_loudly_without_gpu():
+    """amg_setup_device has no CPU fallback."""
+    pr = P.make_heat_setup(8)
+    with pytest.raises(P.CudaError):
+        P.amg_setup_device(pr.F)
+    with pytest.raises(ValueError):  # argument checks come first, as in amg_setup
+        P.amg_setup_device(pr.F, P.AmgParams(theta=1.5))
+
+
+def test_tuning_switches_are_settable_without_gpu():
+    """irk_set_option only records the override (read when graphs are recorded)."""
+    from paper_2010_11377_b200 import _abi
+    _abi.check(_abi.lib().irk_set_option(b"IRK_ZR", 1))
+    with pytest.raises(ValueError):
+        _abi.check(_abi.lib().irk_set_option(None, 1))
+
+
 def test_gauss_seidel_smoother_is_rejected_not_emulated():
     pr = P.make_heat_setup(8)
     t = P.make_radau_iia(2)
