@@ -1705,11 +1705,10 @@ void sweep_dia(const Mat& K, VecRef w, VecRef v, const SweepTerms& t, double* st
 }
 
 void bottom_cycle(const BotDesc& d, const double* r_in, double* z_out, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static std::once_flag attr;
+    std::call_once(attr, [] {
         IRK_CUDA_CHECK(cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
-    }
+    });
     launch(k_bottom, 1, kBotThreads, d.smem, st, d, r_in, z_out);
 }
 
