@@ -1179,8 +1179,28 @@ __device__ void dgs_stop_test(const GmresBufs& g, int j, double wn, double* sm) 
 // Scalar tail of the DCGS2 block-dot (whole last CTA; arithmetic by thread 0
 // on shared-memory copies): finalises column j-1 (or, at cycle end, column j),
 // stores s, p, h_jj and 1/alpha.  `sm` holds 3 (j + 3) doubles.
+// Control scalars the block-dot tail reads (thread 0 loads them before the
+// final reduction so their latency overlaps it).
+struct DgsScal {
+    double beta0, hnorm0, tol0, rel_tol, gci;
+    int cycles, side, stop0, total0;
+};
+__device__ __forceinline__ DgsScal dgs_scal_load(const GmresCtl* ctl, int ci) {
+    DgsScal p;
+    p.beta0 = ctl->beta;
+    p.hnorm0 = ctl->hnorm;
+    p.tol0 = ctl->tol_c;
+    p.rel_tol = ctl->rel_tol;
+    p.gci = ci >= 0 ? ctl->g[ci] : 0.0;
+    p.cycles = ctl->cycles;
+    p.side = ctl->side;
+    p.stop0 = ctl->stop;
+    p.total0 = ctl->total;
+    return p;
+}
+
 __device__ void dgs_dot_scalars(const GmresBufs& g, int j, int finalize, int nvv, const double* res,
-                                double* sm) {
+                                double* sm, const DgsScal& pre) {
     GmresCtl* ctl = g.ctl;
     const int ld = ctl->restart + 1;
     // column being completed: j (cycle end) or j - 1 (none at j = 0)
@@ -1204,9 +1224,9 @@ __device__ void dgs_dot_scalars(const GmresBufs& g, int j, int finalize, int nvv
         }
     __syncthreads();
     if (threadIdx.x == 0) {
-        const double beta0 = ctl->beta, hnorm0 = ctl->hnorm, tol0 = ctl->tol_c, rel_tol = ctl->rel_tol;
-        const int cycles = ctl->cycles, side = ctl->side, stop0 = ctl->stop, total0 = ctl->total;
-        const double gci = ci >= 0 ? ctl->g[ci] : 0.0;
+        const double beta0 = pre.beta0, hnorm0 = pre.hnorm0, tol0 = pre.tol0, rel_tol = pre.rel_tol;
+        const int cycles = pre.cycles, side = pre.side, stop0 = pre.stop0, total0 = pre.total0;
+        const double gci = pre.gci;
         double ss = 0.0, sp = 0.0;
         for (int i = 0; i < nvv; ++i) ss += res[i] * res[i];
         const double sig = res[finalize ? nvv : 2 * nvv];
@@ -1317,6 +1337,9 @@ __device__ __forceinline__ void dgs_batch(const double* V, long long stride, lon
     }
 }
 
+#ifdef IRK_DGS_PROF
+__device__ long long g_dgs_prof[8];
+#endif
 __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot(GmresBufs g, int finalize) {
     extern __shared__ double red[];
     // Iteration mode: j, vt_j and v_0 were final before the operator ran, so
@@ -1329,6 +1352,13 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot(GmresBufs g, int fin
         pdl_wait();
         pdl_trigger();
     }
+#ifdef IRK_DGS_PROF
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        g_dgs_prof[4] = static_cast<long long>(t0);
+    }
+#endif
     GmresCtl* ctl = g.ctl;
     const int j = *reinterpret_cast<volatile const int*>(&ctl->j);
     const int nvv = finalize ? j + 1 : j;   // basis vectors v_0..v_{nvv-1}
@@ -1375,11 +1405,33 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot(GmresBufs g, int fin
 #ifdef IRK_DGS_SKIPFINAL
     return;  // timing diagnostic only: the scalar tail is skipped
 #endif
+#ifdef IRK_DGS_PROF
+    auto stamp = [&](int k) {
+        if (threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            g_dgs_prof[k] = static_cast<long long>(t);
+        }
+    };
+    stamp(0);
+#endif
     if (!elect_last(g.counters + 9)) return;
+#ifdef IRK_DGS_PROF
+    stamp(1);
+#endif
     double* res = red + (kRedThreads / 32) * nv;
+    DgsScal pre{};
+    if (threadIdx.x == 0) pre = dgs_scal_load(ctl, finalize ? j : j - 1);
     final_reduce(g.partials, g.nchunks, nv, red, res);
+#ifdef IRK_DGS_PROF
+    stamp(2);
+#endif
     if (threadIdx.x == 0) g.counters[9] = 0u;
-    dgs_dot_scalars(g, j, finalize, nvv, res, res + nv);
+    dgs_dot_scalars(g, j, finalize, nvv, res, res + nv, pre);
+#ifdef IRK_DGS_PROF
+    __syncthreads();
+    stamp(3);
+#endif
 }
 
 // DCGS2 update: v_j = (vt_j - sum_i s_i v_i) / alpha and
@@ -1774,6 +1826,14 @@ static size_t dgs_smem(const GmresBufs& g) {
     const int nv = 2 * g.cap + 4;
     // reduction slots + the staged Hessenberg column and rotations of the tail
     return sizeof(double) * ((kRedThreads / 32 + 1) * nv + 16 + 3 * (g.cap + 4));
+}
+
+void dgs_prof_read(long long* out) {
+#ifdef IRK_DGS_PROF
+    cudaMemcpyFromSymbol(out, g_dgs_prof, sizeof(long long) * 8);
+#else
+    for (int k = 0; k < 8; ++k) out[k] = 0;
+#endif
 }
 
 void gm_dgs_dot(const GmresBufs& g, int finalize, cudaStream_t st) {

@@ -94,6 +94,8 @@ void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st);
 // variable of the same name, else `dflt`.  Read when a graph is recorded;
 // every override bumps option_generation() so solvers re-record.
 long long option(const char* name, long long dflt);
+// diagnostic: last DCGS2 block-dot tail timestamps (builds with -DIRK_DGS_PROF)
+void dgs_prof_read(long long* out);
 void set_option(const char* name, long long value);
 unsigned option_generation();
 

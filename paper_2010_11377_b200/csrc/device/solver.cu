@@ -1428,6 +1428,12 @@ double DeviceSolver::time_kernel(int which, int reps) {
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
         g_restart_ = -1;  // graphs captured the old use_cond; rebuild on the next step
+        if (std::getenv("IRK_DGS_PROF_PRINT")) {
+            long long t[8];
+            dev::dgs_prof_read(t);
+            std::fprintf(stderr, "dgs dot (last launch, ns from CTA 0 start): last CTA arrives %lld, elected %lld, "
+                         "reduced %lld, scalars done %lld\n", t[0] - t[4], t[1] - t[4], t[2] - t[4], t[3] - t[4]);
+        }
         return static_cast<double>(ms) / reps;
     }
     if (which == 50 || which == 51) {
