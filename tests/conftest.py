@@ -32,6 +32,7 @@ def built_libraries():
         _make(["-C", "oracle", "oracle"])
         if Path("/root/reference/proj/src").exists():
             _make(["-C", "oracle", "ref"])
+            _make(["-C", "integration"])
     except (subprocess.CalledProcessError, FileNotFoundError):
         pass  # the prebuilt artefacts (if any) are used as they are
     yield
