@@ -19,6 +19,9 @@ namespace irkprec {
 IrkStepResult irk_step_b200(const LinearParabolicSystem& sys, const ButcherTable& table, double ht,
                             double t_n, std::span<const double> u_n, const BlockPreconditioner* P,
                             const GmresConfig& cfg);
+TrajectorySummary integrate_b200(const LinearParabolicSystem& sys, const ButcherTable& table,
+                                 std::span<const double> u0, double t_final, double ht,
+                                 const PrecondFactory& make_precond, const GmresConfig& cfg);
 }
 
 int main(int argc, char** argv) {
@@ -50,7 +53,31 @@ int main(int argc, char** argv) {
     std::printf("heat %d^2 Radau IIA s=%d: device %d iterations (%.3f ms), reference %d iterations (%.3f s), "
                 "u_next rel L2 %.3e\n", cells, s, dev.report.iterations, 1e3 * dev.report.solve_seconds,
                 ref.report.iterations, ref.report.solve_seconds, rel);
-    const bool ok = std::abs(dev.report.iterations - ref.report.iterations) <= 1 && rel <= 1e-9 &&
-                    dev.report.converged;
+    bool ok = std::abs(dev.report.iterations - ref.report.iterations) <= 1 && rel <= 1e-9 &&
+              dev.report.converged;
+    // integrate: 3.5 steps of ht (a truncated last step, so the factory is
+    // consulted twice), device-resident vs the reference's loop
+    const PrecondFactory factory = [&](double h) {
+        return std::make_shared<const BlockPreconditioner>(sys.M, sys.F, precond_coeff(table, CoeffKind::LowerFactor),
+                                                           h, SubsolverKind::AmgVcycle);
+    };
+    const double t_final = 3.5 * ht;
+    const TrajectorySummary td = integrate_b200(sys, table, u, t_final, ht, factory, cfg);
+    const TrajectorySummary tr = integrate(sys, table, u, t_final, ht, factory, cfg);
+    num = den = 0.0;
+    for (int i = 0; i < n; ++i) {
+        num += (td.u_final[i] - tr.u_final[i]) * (td.u_final[i] - tr.u_final[i]);
+        den += tr.u_final[i] * tr.u_final[i];
+    }
+    const double trel = std::sqrt(num / den);
+    std::printf("integrate to %.4g: device %d steps (t %.6g), reference %d steps (t %.6g); iterations", t_final,
+                td.steps, td.t_final, tr.steps, tr.t_final);
+    bool its_ok = td.steps == tr.steps;
+    for (int k = 0; k < td.steps && k < tr.steps; ++k) {
+        std::printf(" %d/%d", td.reports[k].iterations, tr.reports[k].iterations);
+        its_ok = its_ok && std::abs(td.reports[k].iterations - tr.reports[k].iterations) <= 1;
+    }
+    std::printf("; u_final rel L2 %.3e\n", trel);
+    ok = ok && its_ok && trel <= 1e-9 && td.t_final == tr.t_final && td.all_converged;
     return ok ? 0 : 1;
 }

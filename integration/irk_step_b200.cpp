@@ -6,6 +6,7 @@
 // demo can run it beside the reference's irk_step in one binary.
 #include <functional>
 #include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -79,6 +80,85 @@ IrkStepResult irk_step_b200(const LinearParabolicSystem& sys, const ButcherTable
     out.report.true_rel_residual = rep.true_rel_residual;
     out.report.converged = rep.converged != 0;
     out.report.solve_seconds = rep.solve_seconds;
+    return out;
+}
+
+namespace {
+
+// What the PrecondFactory callback needs: the system, the table, the
+// reference's factory, and ownership of what it produced.
+struct IntegrateCtx {
+    const LinearParabolicSystem* sys;
+    const ButcherTable* table;
+    const PrecondFactory* make;
+    std::vector<std::shared_ptr<const BlockPreconditioner>> keep;
+    std::vector<irkdev*> made;
+    std::string err;
+};
+
+// One device solver for step size h from the reference's factory.
+irkdev* make_device(double h, void* user) {
+    IntegrateCtx& c = *static_cast<IntegrateCtx*>(user);
+    auto P = (*c.make)(h);
+    const irk_csr M = view(*c.sys->M), K = view(*c.sys->F);
+    irk_amg_params amg;
+    irk_amg_params_default(&amg);
+    const PrecondCoeff& pc = P->coeff();
+    irkdev* d = nullptr;
+    if (irkdev_create(&M, &K, c.table->s, c.table->A.values.data(), c.table->b.data(),
+                      pc.Atilde.values.data(), static_cast<int>(pc.structure), h, &amg, 0, nullptr, 0,
+                      &d) != IRK_OK) {
+        c.err = irk_last_error();
+        return nullptr;
+    }
+    c.keep.push_back(std::move(P));
+    c.made.push_back(d);
+    return d;
+}
+
+}  // namespace
+
+// integrate (irk.hpp:54-58) on the device: u stays in HBM across the steps;
+// the PrecondFactory is consulted exactly when the reference consults it (the
+// first step size and a truncated last step), each preconditioner it returns
+// becoming one device solver.
+TrajectorySummary integrate_b200(const LinearParabolicSystem& sys, const ButcherTable& table,
+                                 std::span<const double> u0, double t_final, double ht,
+                                 const PrecondFactory& make_precond, const GmresConfig& cfg) {
+    require(static_cast<int>(u0.size()) == sys.n(), "integrate: u0 size mismatch");
+    IntegrateCtx ctx{&sys, &table, &make_precond, {}, {}, {}};
+    irkdev* first = make_device(ht, &ctx);
+    if (!first) throw std::runtime_error(ctx.err);
+    int nsteps = 0;
+    if (int st = irk_integrate_steps(t_final, ht, &nsteps)) rethrow(st);
+    irk_gmres_cfg g{cfg.side == PrecondSide::Left ? 0 : 1, cfg.rel_tol, cfg.max_iter, /*restart=*/50};
+    TrajectorySummary out;
+    out.u_final.resize(u0.size());
+    std::vector<irk_report> reps(nsteps);
+    std::vector<double> hist(static_cast<size_t>(nsteps) * (cfg.max_iter + 1));
+    int steps = 0, all = 0;
+    double t_out = 0.0;
+    const double* lift = sys.f_lift.empty() ? nullptr : sys.f_lift.data();
+    const int st = irkdev_integrate(first, make_device, &ctx, u0.data(), lift, table.c.data(),
+                                    sys.forcing ? forward_forcing : nullptr,
+                                    const_cast<std::function<Vec(double)>*>(&sys.forcing), t_final, ht, &g,
+                                    out.u_final.data(), reps.data(), nsteps, hist.data(), &steps, &t_out, &all);
+    for (irkdev* d : ctx.made) irkdev_destroy(d);
+    if (st) rethrow(st);
+    out.t_final = t_out;
+    out.steps = steps;
+    out.all_converged = all != 0;
+    for (int k = 0; k < steps; ++k) {
+        SolveReport r;
+        r.iterations = reps[k].iterations;
+        const double* h0 = hist.data() + static_cast<size_t>(k) * (cfg.max_iter + 1);
+        r.history.assign(h0, h0 + reps[k].history_len);
+        r.final_rel_residual = reps[k].final_rel_residual;
+        r.true_rel_residual = reps[k].true_rel_residual;
+        r.converged = reps[k].converged != 0;
+        r.solve_seconds = reps[k].solve_seconds;
+        out.reports.push_back(std::move(r));
+    }
     return out;
 }
 
