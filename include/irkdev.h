@@ -47,6 +47,8 @@ typedef struct {
     double jacobi_weight, prolongation_weight;
     int prolongation_steps, max_coarse, max_levels;
 } irk_amg_params;
+/* library-default AmgParams{} (amg.hpp:14-29): theta 0.25, V(1,1) damped
+ * Jacobi with omega 2/3, prolongation weight 4/3 x 1 step, max_coarse 64. */
 void irk_amg_params_default(irk_amg_params* p);
 
 /* GmresConfig (gmres.hpp:17-21) plus the restart length of GMRES(m);
@@ -57,7 +59,9 @@ typedef struct {
     int max_iter;
     int restart;
 } irk_gmres_cfg;
-void irk_gmres_cfg_default(irk_gmres_cfg* c); /* right, 1e-8, 500, 50 */
+/* GmresConfig{} (gmres.hpp:17-21) plus the restart length: right, 1e-8, 500,
+ * GMRES(50) (restart = 0 selects the reference's full GMRES). */
+void irk_gmres_cfg_default(irk_gmres_cfg* c);
 
 /* SolveReport (gmres.hpp:23-38) without the history vector, which is
  * copied into a caller buffer. */
