@@ -2,11 +2,15 @@
 // with the reference's own API, solved by the reference's irk_step (CPU) and
 // by the adapter irk_step_b200 (B200 through the C ABI), on the same inputs.
 // Exit code 0 iff the iteration counts agree within 1 and u_{n+1} agrees to
-// 1e-9 relative L2 (the BASELINE bar).   usage: irk_b200_demo [cells] [s]
+// 1e-9 relative L2 (the BASELINE bar).
+//   usage: irk_b200_demo [cells] [s] [heat|dg]
+// dg: the double-glazing problem (P1 SUPG, eps 0.005, East wall = 1, so the
+// Dirichlet lift f_lift is non-zero; study.cpp:215-249 without forcing).
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "irkprec/butcher.hpp"
@@ -28,16 +32,30 @@ int main(int argc, char** argv) {
     using namespace irkprec;
     const int cells = argc > 1 ? std::atoi(argv[1]) : 256;
     const int s = argc > 2 ? std::atoi(argv[2]) : 3;
-    const double ht = 1e-3;
-    const Mesh2D mesh = build_structured_mesh(Domain::UnitSquare, cells);
-    const FemSpace space = make_space(mesh, 1);
-    EliminatedSystem e = eliminate_dirichlet(assemble_mass(space), assemble_diffusion(space, 1.0), space, {});
+    const bool dg = argc > 3 && std::string(argv[3]) == "dg";
+    const double ht = dg ? 1e-2 : 1e-3;
     LinearParabolicSystem sys;
-    sys.M = std::make_shared<const CsrMatrix>(std::move(e.M_ff));
-    sys.F = std::make_shared<const CsrMatrix>(std::move(e.F_ff));
+    if (dg) {
+        const Mesh2D mesh = build_structured_mesh(Domain::BiUnitSquare, cells);
+        const FemSpace space = make_space(mesh, 1);
+        SupgMatrices supg = assemble_advection_supg(space, make_double_glazing_wind(), 0.005);
+        WallValues walls;
+        walls.east = 1.0;
+        EliminatedSystem e = eliminate_dirichlet(supg.M, supg.F, space, walls);
+        sys.M = std::make_shared<const CsrMatrix>(std::move(e.M_ff));
+        sys.F = std::make_shared<const CsrMatrix>(std::move(e.F_ff));
+        sys.f_lift = std::move(e.f_lift);
+    } else {
+        const Mesh2D mesh = build_structured_mesh(Domain::UnitSquare, cells);
+        const FemSpace space = make_space(mesh, 1);
+        EliminatedSystem e = eliminate_dirichlet(assemble_mass(space), assemble_diffusion(space, 1.0), space, {});
+        sys.M = std::make_shared<const CsrMatrix>(std::move(e.M_ff));
+        sys.F = std::make_shared<const CsrMatrix>(std::move(e.F_ff));
+    }
     const int n = sys.n();
-    std::vector<double> u(n);
-    for (int i = 0; i < n; ++i) u[i] = std::sin(0.37 * i) * 0.5 + 0.5;  // any u_n
+    std::vector<double> u(n, 0.0);
+    if (!dg)
+        for (int i = 0; i < n; ++i) u[i] = std::sin(0.37 * i) * 0.5 + 0.5;  // any u_n (dg: u0 = 0)
     const ButcherTable table = make_radau_iia(s);
     BlockPreconditioner P(sys.M, sys.F, precond_coeff(table, CoeffKind::LowerFactor), ht,
                           SubsolverKind::AmgVcycle);
@@ -50,8 +68,8 @@ int main(int argc, char** argv) {
         den += ref.u_next[i] * ref.u_next[i];
     }
     const double rel = std::sqrt(num / den);
-    std::printf("heat %d^2 Radau IIA s=%d: device %d iterations (%.3f ms), reference %d iterations (%.3f s), "
-                "u_next rel L2 %.3e\n", cells, s, dev.report.iterations, 1e3 * dev.report.solve_seconds,
+    std::printf("%s %d^2 Radau IIA s=%d: device %d iterations (%.3f ms), reference %d iterations (%.3f s), "
+                "u_next rel L2 %.3e\n", dg ? "double glazing" : "heat", cells, s, dev.report.iterations, 1e3 * dev.report.solve_seconds,
                 ref.report.iterations, ref.report.solve_seconds, rel);
     bool ok = std::abs(dev.report.iterations - ref.report.iterations) <= 1 && rel <= 1e-9 &&
               dev.report.converged;

@@ -30,8 +30,8 @@ def test_adapter_fails_loudly_without_gpu():
 @pytest.mark.gpu
 @pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
 @pytest.mark.skipif(not DEMO.exists(), reason="integration demo not built (needs /root/reference at build time)")
-@pytest.mark.parametrize("cells,s", [(128, 2), (256, 3)])
-def test_adapter_matches_reference_irk_step(cells, s):
-    r = subprocess.run([str(DEMO), str(cells), str(s)], capture_output=True, text=True, timeout=600)
+@pytest.mark.parametrize("cells,s,problem", [(128, 2, "heat"), (256, 3, "heat"), (64, 2, "dg"), (128, 4, "dg")])
+def test_adapter_matches_reference_irk_step(cells, s, problem):
+    r = subprocess.run([str(DEMO), str(cells), str(s), problem], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "device" in r.stdout and "reference" in r.stdout
