@@ -50,3 +50,27 @@ def test_double_glazing_256_lift():
 def test_lobatto_512_s5():
     c = heat_case(512, scheme=P.Scheme.LobattoIIIC, s=5, ht=1e-3)
     bitwise_step(c, c.problem.initial(0.01, 1))
+
+
+def test_left_preconditioning_512():
+    c = heat_case(512, s=3, ht=1e-3)
+    u = c.problem.initial(0.01, 1)
+    sys_ = P.LinearParabolicSystem(c.M, c.K, None)
+    g = P.irk_step(sys_, c.table, c.ht, 0.0, u, c.device(), P.GmresConfig(side="left", restart=50), want_K=True)
+    o = c.oracle.step(u, None, restart=50, side="left")
+    assert g.report.iterations == o["iterations"]
+    assert np.array_equal(g.K, o["K"]) and np.array_equal(g.u_next, o["u_next"])
+
+
+def test_restart_cycles_512():
+    """Block Jacobi with Lobatto IIIC s=5 needs > 100 iterations: several
+    GMRES(50) cycles, each ending with x += Z y and a true residual."""
+    c = heat_case(512, scheme=P.Scheme.LobattoIIIC, s=5, kind=P.CoeffKind.Jacobi, ht=1e-3)
+    u = c.problem.initial(0.01, 1)
+    sys_ = P.LinearParabolicSystem(c.M, c.K, None)
+    g = P.irk_step(sys_, c.table, c.ht, 0.0, u, c.device(), P.GmresConfig(restart=50), want_K=True)
+    o = c.oracle.step(u, None, restart=50)
+    assert g.report.cycles >= 3, g.report.cycles
+    assert g.report.iterations == o["iterations"]
+    assert np.array_equal(np.array(g.report.history), o["history"])
+    assert np.array_equal(g.K, o["K"]) and np.array_equal(g.u_next, o["u_next"])
