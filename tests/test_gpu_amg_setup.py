@@ -122,3 +122,19 @@ def test_solver_builds_device_hierarchies():
                    P.GmresConfig(), want_K=True)
     assert a.report.iterations == b.report.iterations
     assert np.array_equal(a.K, b.K) and np.array_equal(a.u_next, b.u_next)
+
+
+def test_device_setup_c3_size():
+    """The C3 block (2048^2: 4,190,209 rows, seven levels; Lobatto IIIC s=5
+    diagonal coefficient scale), device vs host bit for bit."""
+    B = block(P.make_heat_setup(2048), 1e-3, 0.25)
+    dev = P.amg_setup_device(B)
+    host = P.amg_setup(B)
+    assert dev.n_levels() >= 6
+    same_hierarchy(dev, host)
+
+
+def test_device_setup_double_glazing_256():
+    pr = P.make_double_glazing_setup(256, 0.005)
+    B = block(pr, 0.01, 0.2)
+    same_hierarchy(P.amg_setup_device(B), P.amg_setup(B))
