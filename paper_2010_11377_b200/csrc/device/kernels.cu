@@ -168,8 +168,10 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
         const unsigned char* cls = static_cast<const unsigned char*>(A.val);
         cd[0] = __ldg(cls + i);
         if constexpr (XM == kXWdR && WDT == 1) {
+            if (!A.nbwd) {
 #pragma unroll
-            for (int d = 0; d < ND; ++d) cw[d] = __ldg(cls + min(max(i + A.off[d], 0), n - 1));
+                for (int d = 0; d < ND; ++d) cw[d] = __ldg(cls + min(max(i + A.off[d], 0), n - 1));
+            }
         }
     } else if constexpr (kPre) {
 #pragma unroll
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
         if constexpr (XM == kXWdR) {
             double wdc;
             if constexpr (VF == kCls)
-                wdc = __ldg(A.wdtab + cw[d]);
+                wdc = A.nbwd ? __ldg(A.nbwd + cd[0] * ND + d) : __ldg(A.wdtab + cw[d]);
             else if constexpr (kPre && WDT == 1)
                 wdc = wdt[cw[d]];
             else

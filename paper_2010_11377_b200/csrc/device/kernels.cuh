@@ -55,6 +55,10 @@ struct Mat {
     int diag0 = -1;                 // slot of offset 0
     long long dstride = 0;          // entries per stored diagonal (>= rows, multiple of 4)
     const double* wdtab = nullptr;  // omega / diagonal value per code (DIA, u8)
+    // kCls hierarchy operators: per class, omega / a_cc of each diagonal's
+    // partner row (0 where the coefficient is 0), so wd .* r needs no
+    // neighbour class lookups
+    const double* nbwd = nullptr;
     size_t bytes = 0;               // device bytes of the stored operator
 };
 

@@ -285,7 +285,12 @@ bool DeviceSolver::to_row_classes(std::vector<dev::Mat*> mats, const std::vector
     std::vector<std::vector<double>> tabs;
     if (!row_classes(vals, m0.nd, m0.rows, m0.dstride, cls, tabs)) return false;
     const unsigned char* dcls = upload_array(cls);
+    // a null entry in `mats`: its table is the neighbour omega / a_cc table
+    // of mats[0] (same class array)
+    for (size_t q = 0; q < mats.size(); ++q)
+        if (!mats[q]) mats[0]->nbwd = upload_array(tabs[q]);
     for (size_t q = 0; q < mats.size(); ++q) {
+        if (!mats[q]) continue;
         dev::Mat& m = *mats[q];
         m.vf = dev::kCls;
         m.val = dcls;
@@ -321,7 +326,19 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
             m.off[d] = L.offs[d];
             if (L.offs[d] == 0) m.diag0 = d;
         }
-        // hierarchy operators: row classes when the stencil repeats
+        // hierarchy operators: row classes when the stencil repeats; the
+        // class also fixes omega / a_cc of every partner row (nbwd)
+        if (omega > 0.0 && m.diag0 >= 0 && dev::option("IRK_NBWD", 1) != 0) {
+            const long long ds = L.ds;
+            std::vector<double> nbw(static_cast<size_t>(nd) * ds, 0.0);
+            for (int i = 0; i < A.rows; ++i)
+                for (int d = 0; d < nd; ++d) {
+                    if (L.v[static_cast<size_t>(d) * ds + i] == 0.0) continue;
+                    const int c = std::min(std::max(i + L.offs[d], 0), A.rows - 1);
+                    nbw[static_cast<size_t>(d) * ds + i] = omega * (1.0 / L.v[static_cast<size_t>(m.diag0) * ds + c]);
+                }
+            if (to_row_classes({&m, nullptr}, {&L.v, &nbw}, omega)) return m;
+        }
         if (omega > 0.0 && to_row_classes({&m}, {&L.v}, omega)) return m;
         upload_values(m, L.v, omega);
         return m;
