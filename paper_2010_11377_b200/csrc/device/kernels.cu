@@ -267,7 +267,11 @@ __global__ void __launch_bounds__(256) k_spmv_sell(Mat A, SpmvArgs a) {
             const double xv = XM == kXWdR ? wd[c] * r[c] : x[c];
             s += v0[k] * xv;
         }
-#pragma unroll 4
+#ifndef IRK_SELL_UNROLL
+#define IRK_SELL_UNROLL 6
+#endif
+    constexpr int kUnroll = IRK_SELL_UNROLL;
+#pragma unroll kUnroll
     for (int k = kPre; k < len; ++k) {
         const int c = __ldg(A.idx + base + k * 32 + lane);
         const double xv = XM == kXWdR ? wd[c] * r[c] : x[c];
