@@ -353,8 +353,8 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
     static const double big_avg =
         std::getenv("IRK_CSRV_BIG_AVG") ? std::atof(std::getenv("IRK_CSRV_BIG_AVG")) : 24.0;
     if ((force < 0 && avg > 4.5 && (A.rows < 65536 || avg > big_avg)) || force == dev::kCsrVec) {
-        static const double per_lane =
-            std::getenv("IRK_CSRV_PER_LANE") ? std::atof(std::getenv("IRK_CSRV_PER_LANE")) : 3.0;
+        // entries per lane (tenths; IRK_CSRV_PER_LANE10, default 30 = 3.0)
+        const double per_lane = 0.1 * static_cast<double>(dev::option("IRK_CSRV_PER_LANE10", 30));
         int g = 2;
         while (g < 32 && per_lane * g < avg) g *= 2;
         // fewer lanes when the grid would spill just past one wave of
