@@ -352,7 +352,8 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
     // (big operators switch to CSR-vector above IRK_CSRV_BIG_AVG entries per row)
     static const double big_avg =
         std::getenv("IRK_CSRV_BIG_AVG") ? std::atof(std::getenv("IRK_CSRV_BIG_AVG")) : 24.0;
-    if ((force < 0 && avg > 4.5 && (A.rows < 65536 || avg > big_avg)) || force == dev::kCsrVec) {
+    const long long sell_min_rows = dev::option("IRK_SELL_MIN_ROWS", 65536);
+    if ((force < 0 && avg > 4.5 && (A.rows < sell_min_rows || avg > big_avg)) || force == dev::kCsrVec) {
         // entries per lane (tenths; IRK_CSRV_PER_LANE10, default 30 = 3.0)
         const double per_lane = 0.1 * static_cast<double>(dev::option("IRK_CSRV_PER_LANE10", 30));
         int g = 2;
