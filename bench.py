@@ -261,6 +261,10 @@ def main():
     ap.add_argument("--cells", type=int, default=None, help="override the workload's grid")
     args = ap.parse_args()
     set_workload(args.workload, args.cells)
+    # torchrun exports OMP_NUM_THREADS=1 per process; the reference's CPU path
+    # (and the host setup) should use every host thread this process may run
+    # on.  Set before the first OpenMP library (libirkdev / libirkref) loads.
+    os.environ["OMP_NUM_THREADS"] = str(cpu_threads())
     if args.impl == "reference":
         return reference_arm(args)
     return our_arm(args)
