@@ -194,28 +194,49 @@ def solve_bytes(dev_info, levels, its_reorth, n, s, nnz_mk):
 
 
 # ------------------------------------------------------------------ reference arm
-def run_reference_steps(steps, warmup, rank0=True):
+def run_reference_steps(steps, warmup, budget_s=None):
     """The reference's own CPU implementation (oracle/_ref: irkprec compiled from
-    its sources) on the same workload: setup excluded, steps timed."""
+    its sources) on the same workload: setup excluded, steps timed.
+
+    Nothing here imports the product package: M, K, f_lift come from the
+    reference's own assembly and u0 from ref_problem_initial (the project's
+    seeded u0 recipe restated on the reference mesh, pinned bit for bit to
+    irk_problem_initial by tests/test_bench_ref.py).  With `budget_s`, the step
+    count is cut so that the timed steps fit the budget (measured on the first
+    warm-up step).  Returns (seconds, iterations, steps, warmup)."""
     sys.path.insert(0, str(ROOT / "tests"))
     from refs import Ref, RefSolver  # noqa: E402
     if not Ref.available():
         raise RuntimeError("oracle/_ref/libirkref.so not built")
-    import paper_2010_11377_b200 as P
-    _, _, u0, _ = make_problem(P)
-    ref_prob = Ref.problem(WL["problem"], CELLS)
+    noise = WL["noise"] if WL["noise"] is not None else 0.0
+    ref_prob = Ref.problem(WL["problem"], CELLS, initial=(noise, WL["seed"]))
+    u0 = ref_prob["u0"] if WL["noise"] is not None else np.zeros(len(ref_prob["f_lift"]))
+    lift = ref_prob["f_lift"] if WL["problem"] != "heat" else None
     rs = RefSolver(ref_prob["M"], ref_prob["K"], WL["scheme"], S, 3, HT)
     u = u0.copy()
-    for _ in range(warmup):
-        rs.step(u, ref_prob["f_lift"])
+    for w in range(warmup):
+        r = rs.step(u, lift)
+        u = r["u_next"]
+        if w == 0 and budget_s:
+            steps = max(1, min(steps, int(budget_s / max(r["seconds"], 1e-9))))
     u = u0.copy()
     secs, its = [], []
     for _ in range(steps):
-        r = rs.step(u, ref_prob["f_lift"])
+        r = rs.step(u, lift)
         secs.append(r["seconds"])
         its.append(r["iterations"])
         u = r["u_next"]
-    return sum(secs), its
+    return sum(secs), its, steps, warmup
+
+
+def cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 def cpu_threads():
@@ -229,9 +250,9 @@ def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    steps = max(1, min(args.steps, 3))
-    warm = 0 if args.warmup <= 0 else 1
-    total, its = run_reference_steps(steps, warm)
+    # Same warm-up and step count as our arm, cut only if the reference would
+    # need more than ~4 minutes for the timed steps (C3: ~50 s per step).
+    total, its, steps, warm = run_reference_steps(args.steps, max(1, args.warmup), budget_s=240.0)
     value = steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
@@ -239,10 +260,11 @@ def reference_arm(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": DATA,
         "config": config({"reference_iterations": its}),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "reference",
-                         "sample": f"{steps} {WORKLOAD[:2]} timesteps of the reference irk_step (irkprec compiled "
-                                   "from /root/reference sources, OpenMP, GMRES(50) wrapper), "
-                                   "setup excluded"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "cpu_model": cpu_model(),
+                         "kind": "reference",
+                         "sample": f"{steps} {WORKLOAD[:2]} timesteps (after {warm} warm-up) of the reference "
+                                   "irk_step (irkprec compiled from /root/reference sources by oracle/Makefile, "
+                                   f"OpenMP on {cpu_threads()} threads, GMRES(50) wrapper), setup excluded"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -432,10 +454,10 @@ def our_arm(args):
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            nref = 1 if CELLS > 1024 else 2
-            total, rits = run_reference_steps(nref, 0)
+            total, rits, nref, _ = run_reference_steps(1 if CELLS > 1024 else 2, 0)
             line["cpu_baseline"] = {
-                "value": nref / total, "unit": UNIT, "cores": cpu_threads(), "kind": "reference",
+                "value": nref / total, "unit": UNIT, "cores": cpu_threads(), "cpu_model": cpu_model(),
+                "kind": "reference",
                 "sample": f"{nref} {WORKLOAD[:2]} timesteps of the reference irk_step (irkprec compiled from its "
                           "own sources, OpenMP on all host threads, GMRES(50) wrapper), setup "
                           f"excluded; reference iterations {rits}"}

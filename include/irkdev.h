@@ -60,7 +60,8 @@ typedef struct {
     int restart;
 } irk_gmres_cfg;
 /* GmresConfig{} (gmres.hpp:17-21) plus the restart length: right, 1e-8, 500,
- * GMRES(50) (restart = 0 selects the reference's full GMRES). */
+ * restart = 0 -- full GMRES, the reference's behaviour (BASELINE's GMRES(50)
+ * sets restart = 50). */
 void irk_gmres_cfg_default(irk_gmres_cfg* c);
 
 /* SolveReport (gmres.hpp:23-38) without the history vector, which is

@@ -398,7 +398,8 @@ static void dcgs2_cycle(const or_sys* S, long N, int R, int budget, double* V, d
         if (hist) hist[*total] = hv;
         *final_rel = hv;
         if (stop == 1 && !(res_rel <= tol_c)) stop = 3; /* provisional pass, final fail: restart */
-        if (stop == 3 && res_rel <= tol_c) stop = 1;
+        /* converged = final residual <= tol (gmres.cpp:139), also after a breakdown */
+        if ((stop == 3 || stop == 2) && res_rel <= tol_c) stop = 1;
     }
     free(col);
     *m_out = j + 1;

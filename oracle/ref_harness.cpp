@@ -18,6 +18,7 @@
 //   * the reference's own integrate (irk.cpp:70-102) behind a C entry point.
 #include <chrono>
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -76,7 +77,13 @@ CsrMatrix from_arrays(int n_rows, int n_cols, const int* rp, const int* ci,
 struct RefProblem {
     std::shared_ptr<const CsrMatrix> M, F;
     Vec f_lift;
+    std::vector<std::array<double, 2>> free_coords;  // space.dof_coords at free_dofs
 };
+
+void keep_free_coords(RefProblem* p, const FemSpace& space) {
+    p->free_coords.reserve(space.free_dofs.size());
+    for (const int id : space.free_dofs) p->free_coords.push_back(space.dof_coords[id]);
+}
 
 struct RefSolver {
     std::shared_ptr<const CsrMatrix> M, F;
@@ -126,6 +133,7 @@ int ref_problem_create(int kind, int cells, double eps, void** out) {
             p->M = std::make_shared<const CsrMatrix>(std::move(e.M_ff));
             p->F = std::make_shared<const CsrMatrix>(std::move(e.F_ff));
             p->f_lift = std::move(e.f_lift);
+            keep_free_coords(p, space);
         } else {
             const Mesh2D mesh = build_structured_mesh(Domain::BiUnitSquare, cells);
             const FemSpace space = make_space(mesh, 1);
@@ -137,6 +145,7 @@ int ref_problem_create(int kind, int cells, double eps, void** out) {
             p->M = std::make_shared<const CsrMatrix>(std::move(e.M_ff));
             p->F = std::make_shared<const CsrMatrix>(std::move(e.F_ff));
             p->f_lift = std::move(e.f_lift);
+            keep_free_coords(p, space);
         }
         *out = p;
     });
@@ -159,6 +168,32 @@ int ref_problem_csr(void* h, int which, int* n, int* nnz, const int** rp,
 
 const double* ref_problem_flift(void* h) {
     return static_cast<RefProblem*>(h)->f_lift.data();
+}
+
+// The benchmark's initial state u0 = sin(pi x) sin(pi y) + noise * U[-1, 1]
+// at the free dofs, computed from the reference mesh's own coordinates.  The
+// reference defines no noise generator, so the project
+// fixes one -- splitmix64, top 53 bits -- and this restates it so that the
+// reference arm of bench.py never needs the product library (its output is
+// checked bit for bit against irk_problem_initial in tests/test_bench_ref.py).
+int ref_problem_initial(void* h, double noise, unsigned long long seed, double* u0) {
+    return guard([&] {
+        const auto* p = static_cast<RefProblem*>(h);
+        constexpr double pi = 3.14159265358979323846;
+        std::uint64_t st = seed;
+        for (std::size_t k = 0; k < p->free_coords.size(); ++k) {
+            double u = std::sin(pi * p->free_coords[k][0]) * std::sin(pi * p->free_coords[k][1]);
+            if (noise != 0.0) {
+                std::uint64_t z = (st += 0x9e3779b97f4a7c15ULL);
+                z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+                z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+                z ^= z >> 31;
+                const double r = static_cast<double>(z >> 11) * 0x1.0p-53;
+                u += noise * (2.0 * r - 1.0);
+            }
+            u0[k] = u;
+        }
+    });
 }
 
 // ---------------------------------------------------------------- butcher

@@ -329,7 +329,7 @@ class GmresConfig:
     side: str = "right"
     rel_tol: float = 1e-8
     max_iter: int = 500
-    restart: int = 50
+    restart: int = 0  # full GMRES, as the reference (gmres.hpp:20); BASELINE runs GMRES(50)
 
     def c(self) -> _abi.irk_gmres_cfg:
         if self.side not in ("right", "left"):

@@ -140,11 +140,11 @@ irkb::GmresConfig to_cfg(const irk_gmres_cfg* c) {
 template <class F>
 void with_device_vectors(irkdev* d, const double* in, long long nin, double* out, long long nout,
                          F&& f) {
+    irkb::DeviceScope on(d->s->device());
     irkb::DevBuf a(sizeof(double) * nin), b(sizeof(double) * nout);
     IRK_CUDA_CHECK(cudaMemcpy(a.as<double>(), in, sizeof(double) * nin, cudaMemcpyHostToDevice));
     f(a.as<double>(), b.as<double>());
     IRK_CUDA_CHECK(cudaMemcpy(out, b.as<double>(), sizeof(double) * nout, cudaMemcpyDeviceToHost));
-    (void)d;
 }
 
 }  // namespace
@@ -170,7 +170,7 @@ void irk_gmres_cfg_default(irk_gmres_cfg* c) {
     c->side = 1;
     c->rel_tol = 1e-8;
     c->max_iter = 500;
-    c->restart = 50;
+    c->restart = 0;  // full GMRES, the reference (gmres.hpp:20)
 }
 
 int irk_problem_heat(int cells, irk_problem** out) {
@@ -507,6 +507,7 @@ int irkdev_vcycle(irkdev* d, int k, const double* r, double* z) {
 
 int irkdev_dot(irkdev* d, const double* x, const double* y, long long n, double* out) {
     return guard([&] {
+        irkb::DeviceScope on(d->s->device());
         irkb::DevBuf a(sizeof(double) * n), b(sizeof(double) * n);
         IRK_CUDA_CHECK(cudaMemcpy(a.as<double>(), x, sizeof(double) * n, cudaMemcpyHostToDevice));
         IRK_CUDA_CHECK(cudaMemcpy(b.as<double>(), y, sizeof(double) * n, cudaMemcpyHostToDevice));

@@ -677,7 +677,7 @@ Hierarchy amg_setup_device(const Csr& A, const AmgParams& p, int device) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         throw CudaError("no CUDA device: amg_setup_device has no CPU fallback");
-    IRK_CUDA_CHECK(cudaSetDevice(device));
+    DeviceScope on(device);
     cudaStream_t st = nullptr;
     IRK_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     struct StreamGuard {

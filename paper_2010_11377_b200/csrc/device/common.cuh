@@ -64,3 +64,30 @@ __device__ __forceinline__ double hyp(double a, double b) {
         if (e__ != cudaSuccess)                                                  \
             throw ::irkb::CudaError(std::string(#expr) + ": " + cudaGetErrorString(e__)); \
     } while (0)
+
+namespace irkb {
+
+// Makes `device` current for the scope and restores the caller's device on
+// exit, so that a solver on one GPU never changes (or depends on) the device
+// the calling thread has selected (torch.cuda.set_device, another solver).
+class DeviceScope {
+public:
+    explicit DeviceScope(int device) {
+        if (cudaGetDevice(&prev_) != cudaSuccess) prev_ = -1;
+        if (prev_ != device) {
+            IRK_CUDA_CHECK(cudaSetDevice(device));
+            set_ = true;
+        }
+    }
+    ~DeviceScope() {
+        if (set_ && prev_ >= 0) cudaSetDevice(prev_);
+    }
+    DeviceScope(const DeviceScope&) = delete;
+    DeviceScope& operator=(const DeviceScope&) = delete;
+
+private:
+    int prev_ = -1;
+    bool set_ = false;
+};
+
+}  // namespace irkb

@@ -1275,7 +1275,8 @@ __device__ void dgs_dot_scalars(const GmresBufs& g, int j, int finalize, int nvv
             ctl->final_rel = hv;
             if (finalize) {
                 if (stop0 == 1 && !(res_rel <= tol0)) ctl->stop = 3;
-                if (stop0 == 3 && res_rel <= tol0) ctl->stop = 1;
+                // converged = final residual <= tol (gmres.cpp:139), also after a breakdown
+                if ((stop0 == 3 || stop0 == 2) && res_rel <= tol0) ctl->stop = 1;
                 ctl->m = j + 1;
             }
         }

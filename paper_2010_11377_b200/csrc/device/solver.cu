@@ -438,7 +438,8 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         throw CudaError("no CUDA device: the B200 solve phase has no CPU fallback");
-    IRK_CUDA_CHECK(cudaSetDevice(device));
+    device_ = device;
+    DeviceScope on(device_);
     IRK_CUDA_CHECK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     dev::set_smem_limits();
 
@@ -545,6 +546,7 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
 }
 
 DeviceSolver::~DeviceSolver() {
+    DeviceScope on(device_);
     for (cudaGraphExec_t* e : {&exec_, &exec_iter_, &exec_pre_, &exec_cb_, &exec_ce_, &exec_post_})
         if (*e) cudaGraphExecDestroy(*e);
     for (Branches& b : branch_sets_) {
@@ -952,7 +954,9 @@ void DeviceSolver::ensure_gmres(int restart, int max_iter) {
     H_ = DevBuf(sizeof(double) * (cap_restart_ + 1) * (cap_restart_ + 1));
     hist_ = DevBuf(sizeof(double) * (cap_iter_ + 1));
     const int nch = static_cast<int>((sN_ + dev::kChunk - 1) / dev::kChunk);
-    part_ = DevBuf(sizeof(double) * static_cast<size_t>(dev::kMaxRestart + 2) * nch);
+    // k_dgs_dot writes nv = 2j + 2 per-chunk partials at inner index j < cap
+    // (and the cycle-end finalize 2j + 4); size for the largest, like dgs_smem.
+    part_ = DevBuf(sizeof(double) * static_cast<size_t>(2 * cap_restart_ + 4) * nch);
     ctl_ = DevBuf(sizeof(dev::GmresCtl));
     cnt_ = DevBuf(sizeof(unsigned) * 16);
     IRK_CUDA_CHECK(cudaMemset(cnt_.as<void>(), 0, sizeof(unsigned) * 16));
@@ -1274,6 +1278,7 @@ void DeviceSolver::launch_solve() {
 
 SolveReport DeviceSolver::step(const double* u, const double* lift, const GmresConfig& cfg,
                                double* u_next, double* k_out, const double* forcing) {
+    DeviceScope on(device_);
     const int max_iter = prepare(cfg, lift != nullptr, forcing != nullptr);
     const auto t0 = std::chrono::steady_clock::now();
     IRK_CUDA_CHECK(cudaMemcpyAsync(u_, u, sizeof(double) * n_, cudaMemcpyDefault, st_));
@@ -1323,11 +1328,13 @@ struct Events {
 }  // namespace
 
 void DeviceSolver::load_u(const double* u0) {
+    DeviceScope on(device_);
     IRK_CUDA_CHECK(cudaMemcpyAsync(u_, u0, sizeof(double) * n_, cudaMemcpyDefault, st_));
     IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
 }
 
 void DeviceSolver::store_u(double* dst) {
+    DeviceScope on(device_);
     IRK_CUDA_CHECK(cudaMemcpyAsync(dst, u_, sizeof(double) * n_, cudaMemcpyDefault, st_));
     IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
 }
@@ -1335,6 +1342,7 @@ void DeviceSolver::store_u(double* dst) {
 std::vector<SolveReport> DeviceSolver::run_segment(int nsteps, double* t, const double* lift,
                                                    ForcingFn forcing, void* user, const double* c,
                                                    const GmresConfig& cfg, bool want_history) {
+    DeviceScope on(device_);
     check(nsteps >= 0, "integrate: negative step count");
     check(!forcing || c, "integrate: forcing needs the stage nodes c");
     const int max_iter = prepare(cfg, lift != nullptr, forcing != nullptr);
@@ -1386,22 +1394,26 @@ std::vector<SolveReport> DeviceSolver::run_segment(int nsteps, double* t, const 
 }
 
 void DeviceSolver::stage_apply(const double* v, double* y) {
+    DeviceScope on(device_);
     record_stage_op(dev::plain(v), dev::plain(y));
     IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
 }
 
 void DeviceSolver::precond_apply(const double* v, double* w) {
+    DeviceScope on(device_);
     record_precond(dev::plain(v), dev::plain(w));
     IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
 }
 
 void DeviceSolver::vcycle(int k, const double* r, double* z) {
+    DeviceScope on(device_);
     check(k >= 0 && k < static_cast<int>(hier_.size()), "vcycle: hierarchy index out of range");
     record_vcycle(k, dev::plain(r), dev::plain(z));
     IRK_CUDA_CHECK(cudaStreamSynchronize(st_));
 }
 
 double DeviceSolver::dot(const double* x, const double* y, long long n) {
+    DeviceScope on(device_);
     const long long nch = (n + dev::kChunk - 1) / dev::kChunk;
     DevBuf part(sizeof(double) * std::max<long long>(nch, 1));
     dev::dot(x, y, n, part.as<double>(), red_cnt_, red_out_, st_);
@@ -1416,6 +1428,7 @@ __global__ void k_empty() {}
 }  // namespace
 
 double DeviceSolver::time_kernel(int which, int reps) {
+    DeviceScope on(device_);
     if (which >= 100 && which < 100 + 2 * dev::kMaxRestart) {
         // GMRES block-dot with j = which - 100 (CGS pass 1) or which - 600
         // (DCGS2 block-dot): j+2 vectors of sN streamed

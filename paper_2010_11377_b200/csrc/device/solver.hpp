@@ -17,6 +17,7 @@
 
 namespace irkb {
 
+
 // Owns one device allocation.
 class DevBuf {
 public:
@@ -80,6 +81,7 @@ public:
     ~DeviceSolver();
 
     int n() const { return n_; }
+    int device() const { return device_; }
     int s() const { return s_; }
     long long sN() const { return sN_; }
     cudaStream_t stream() const { return st_; }

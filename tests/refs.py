@@ -68,6 +68,7 @@ class Ref:
             L.ref_problem_csr.argtypes = [C.c_void_p, C.c_int, iptr, iptr, C.POINTER(iptr),
                                           C.POINTER(iptr), C.POINTER(dptr)]
             L.ref_problem_flift.argtypes = [C.c_void_p]
+            L.ref_problem_initial.argtypes = [C.c_void_p, C.c_double, C.c_ulonglong, dptr]
             L.ref_amg_nlevels.argtypes = [C.c_void_p]
             L.ref_amg_level.argtypes = [C.c_void_p, C.c_int, C.c_int, iptr, iptr, iptr,
                                         C.POINTER(iptr), C.POINTER(iptr), C.POINTER(dptr)]
@@ -94,7 +95,9 @@ class Ref:
 
     # -- problems
     @classmethod
-    def problem(cls, kind: str, cells: int, eps: float = 0.005):
+    def problem(cls, kind: str, cells: int, eps: float = 0.005, initial=None):
+        """M, K, f_lift of the reference assembly; with initial=(noise, seed) also
+        the benchmark u0 computed from the reference mesh (ref_problem_initial)."""
         L = cls.lib()
         h = C.c_void_p()
         cls.check(L.ref_problem_create(0 if kind == "heat" else 1, cells, eps, C.byref(h)))
@@ -108,6 +111,10 @@ class Ref:
                          np.ctypeslib.as_array(ci, (NZ,)).copy(),
                          np.ctypeslib.as_array(v, (NZ,)).copy())
         out["f_lift"] = np.ctypeslib.as_array(L.ref_problem_flift(h), (len(out["M"][0]) - 1,)).copy()
+        if initial is not None:
+            u0 = np.empty(len(out["f_lift"]))
+            cls.check(L.ref_problem_initial(h, float(initial[0]), int(initial[1]), _d(u0)))
+            out["u0"] = u0
         L.ref_problem_free(h)
         return out
 

@@ -32,7 +32,7 @@ def test_defaults_match_reference():
     assert (p.prolongation_steps, p.max_coarse, p.max_levels) == (1, 64, 10)
     g = _abi.irk_gmres_cfg()
     _abi.lib().irk_gmres_cfg_default(C.byref(g))
-    assert (g.side, g.rel_tol, g.max_iter, g.restart) == (1, 1e-8, 500, 50)
+    assert (g.side, g.rel_tol, g.max_iter, g.restart) == (1, 1e-8, 500, 0)  # full GMRES, gmres.hpp:20
 
 
 def test_errors_map_to_reference_exceptions():

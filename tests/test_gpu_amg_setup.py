@@ -110,7 +110,7 @@ def test_solver_builds_device_hierarchies():
     u = pr.initial(noise=0.01, seed=3)
     sys_ = P.LinearParabolicSystem(pr.M, pr.F, pr.f_lift)
     a = P.irk_step(sys_, t, 1e-3, 0.0, u, P.BlockPreconditioner(pr.M, pr.F, pc, 1e-3, table=t),
-                   P.GmresConfig(), want_K=True)
+                   P.GmresConfig(restart=50), want_K=True)
     blocks = []
     for j in range(3):
         d = pc.Atilde[j, j]
@@ -119,7 +119,7 @@ def test_solver_builds_device_hierarchies():
     hiers = [P.amg_setup(block(pr, 1e-3, d)) for d in blocks]
     b = P.irk_step(sys_, t, 1e-3, 0.0, u, P.BlockPreconditioner(pr.M, pr.F, pc, 1e-3, table=t,
                                                                   hierarchies=hiers),
-                   P.GmresConfig(), want_K=True)
+                   P.GmresConfig(restart=50), want_K=True)
     assert a.report.iterations == b.report.iterations
     assert np.array_equal(a.K, b.K) and np.array_equal(a.u_next, b.u_next)
 

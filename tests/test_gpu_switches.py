@@ -45,7 +45,7 @@ def case():
 def step(case):
     pr, t, dev, u = case
     sys_ = P.LinearParabolicSystem(pr.M, pr.F, pr.f_lift)
-    return P.irk_step(sys_, t, 1e-3, 0.0, u, dev, P.GmresConfig(), want_K=True)
+    return P.irk_step(sys_, t, 1e-3, 0.0, u, dev, P.GmresConfig(restart=50), want_K=True)
 
 
 @pytest.mark.parametrize("name,off", [("IRK_BOTTOM", 0), ("IRK_ZR", 0), ("IRK_PDL_DGS", 0),

@@ -49,3 +49,21 @@ def test_device_long_cycle_bitwise(cells, scheme, s, rtol, restart):
     o = c.oracle.step(u, c.f_lift, rtol=rtol, restart=restart)
     assert g.report.converged and g.report.iterations == o["iterations"]
     assert np.array_equal(g.K, o["K"])
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_device_cycle_longer_than_256_bitwise():
+    """One Arnoldi cycle of 259 iterations (full GMRES, block Jacobi, s = 7):
+    k_dgs_dot writes 2j + 2 partials per chunk, past the old (512 + 2)-slot
+    partials buffer once j > 256."""
+    c = heat_case(128, s=7, kind=P.CoeffKind.Jacobi, ht=1e-3)
+    u = c.problem.initial(0.01, 1)
+    sys_ = P.LinearParabolicSystem(c.M, c.K, c.f_lift)
+    g = P.irk_step(sys_, c.table, c.ht, 0.0, u, c.device(),
+                   P.GmresConfig(rel_tol=1e-20, restart=0, max_iter=300), want_K=True)
+    o = c.oracle.step(u, c.f_lift, rtol=1e-20, restart=0, max_iter=300)
+    assert o["iterations"] > 256 and o["cycles"] == 1
+    assert g.report.iterations == o["iterations"] and g.report.cycles == 1
+    assert g.report.converged == o["converged"]
+    assert np.array_equal(g.K, o["K"])
