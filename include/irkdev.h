@@ -151,6 +151,10 @@ int irkdev_info(const irkdev* d, int* n, int* s, int* n_hier, int* solver_of_blo
 /* hierarchy k, level l: sizes for the roofline byte model. */
 int irkdev_level_info(const irkdev* d, int k, int l, int* n, int* nnz_A, int* nnz_P,
                       int* nnz_R, int* fmt_A);
+/* A copy of hierarchy k as the solver built and uploaded it (its distinct
+ * diagonal block's amg_setup, stage.cpp:85-106); free with irk_hierarchy_free.
+ * Lets a caller pin the device setup against the reference's amg_setup. */
+int irkdev_hierarchy(const irkdev* d, int k, irk_hierarchy** out);
 int irkdev_num_levels(const irkdev* d, int k);
 /* Stored value format of hierarchy k's level-l operator on the device:
  * 0 fp64, 1 u8 codes, 2 u16 codes, 3 DIA row classes (roofline byte counts). */

@@ -437,6 +437,12 @@ class BlockPreconditioner:
     def distinct_subsolvers(self) -> int:
         return self._dev.info()["n_hier"]
 
+    def hierarchy(self, k: int) -> AmgHierarchy:
+        """The k-th distinct subsolver's hierarchy as built and uploaded."""
+        h = C.c_void_p()
+        check(_abi.lib().irkdev_hierarchy(self._dev._h, int(k), C.byref(h)))
+        return AmgHierarchy(h)
+
     def setup_seconds(self) -> float:
         return self._dev.info()["setup_seconds"]
 

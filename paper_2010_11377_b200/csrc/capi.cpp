@@ -362,6 +362,14 @@ int irkdev_info(const irkdev* d, int* n, int* s, int* n_hier, int* sob, double* 
     });
 }
 
+int irkdev_hierarchy(const irkdev* d, int k, irk_hierarchy** out) {
+    return guard([&] {
+        const auto& hs = d->s->hierarchies();
+        irkb::check(k >= 0 && k < static_cast<int>(hs.size()), "hierarchy: index out of range");
+        *out = new irk_hierarchy{hs[k]};
+    });
+}
+
 int irkdev_num_levels(const irkdev* d, int k) {
     return d->s->hierarchies().at(k).n_levels();
 }

@@ -13,7 +13,7 @@ ref_problem_create) gives M, K, f_lift, and the reference's amg_setup
 per array: the digest of the integer structure (row_ptr, col_idx) apart from
 the digest of the values, so a failure says which one broke.  The aggregates
 are pinned through P's pattern (P = (I - w D^-1 A) T, T's columns are the
-aggregate ids).  Output: tests/golden/fullsize_digests.json (a few KB).
+aggregate ids).  Output: tests/golden/fullsize_digests.json (~60 KB of digests).
 """
 import hashlib
 import json
