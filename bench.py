@@ -149,12 +149,24 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ byte model
-def solve_bytes(dev_info, levels, its_reorth, n, s, nnz_mk):
-    """Algorithmic HBM bytes of one IRK solve per SURVEY.md §8(d).
+def cycle_lengths(iters, restart=50):
+    """Columns m_k of each GMRES(restart) cycle of a solve with `iters` iterations."""
+    out = []
+    while iters > 0:
+        out.append(min(restart, iters))
+        iters -= out[-1]
+    return out or [0]
 
-    levels[k] = [(n_l, nnz_A, nnz_P, nnz_R), ...]; its_reorth = (iters, reorths,
-    cycles) of the solve.  Each kernel reads its operands once and writes its
-    result once; no cross-kernel cache credit.
+
+def survey_model_bytes(dev_info, levels, iters, n, s, nnz_mk, restart=50):
+    """Algorithmic HBM bytes of one IRK solve per SURVEY.md §8(d)'s formula:
+    CSR operators (4 B index + 8 B value per nonzero), every array read once
+    and written once per kernel, no cross-kernel cache credit.
+
+    levels[k] = [(n_l, nnz_A, nnz_P, nnz_R), ...].  ORTH(j) is the delayed-CGS2
+    cost the device runs, 8 sN (2j + 6): block-dot (j + 2 vectors) + update
+    (j + 4); DCGS2 folds the second Gram-Schmidt pass into the next block-dot,
+    so no separate re-orthogonalisation pass is charged.
     """
     N = n
     sN = s * N
@@ -173,24 +185,23 @@ def solve_bytes(dev_info, levels, its_reorth, n, s, nnz_mk):
     sob = dev_info["solver_of_block"]
     PREC = sum(VC(levels[sob[i]]) for i in range(s))
     PREC += (s - 1) * (4 * (N + 1) + 12 * nnz_mk + 16 * N) + sum(8 * N * (i + 2) for i in range(1, s))
-    iters, reorths, cycles = its_reorth
-    total = 0
-    # per-iteration ORTH with j = index within the cycle (restart 50)
-    j_list = []
-    left = iters
-    while left > 0:
-        m = min(50, left)
-        j_list.extend(range(m))
-        left -= m
-    for k, j in enumerate(j_list):
-        total += OP + PREC + 8 * sN * (2 * j + 7)
-    # re-orthogonalisation passes: assume they fire on the first `reorths` iterations' j
-    for j in j_list[:reorths]:
-        total += 8 * sN * (2 * j + 5)
+    ms = cycle_lengths(iters, restart)
+    total = sum(OP + PREC + 8 * sN * (2 * j + 6) for m in ms for j in range(m))
     total += 8 * sN * (iters + 1) + PREC + OP + 16 * sN + 8 * N * (s + 2) + (4 * (N + 1) + 12 * nnz_mk)
-    total += max(cycles - 1, 0) * (PREC + OP + 8 * sN * 51 + 24 * sN)
-    per_iter = (OP + PREC + sum(8 * sN * (2 * j + 7) for j in j_list) / max(len(j_list), 1))
-    return total, per_iter
+    total += (len(ms) - 1) * (PREC + OP + 8 * sN * (restart + 1) + 24 * sN)
+    return total
+
+
+def format_model_bytes(mb, iters, restart=50):
+    """Bytes of one solve from the device's own per-kernel tally
+    (irkdev_model_bytes: each kernel's operands once, in their STORED formats
+    -- row classes, u8/u16 codes, SELL/CSR indices)."""
+    pre, cyc, cyc_m, it, it_j, post = mb[:6]
+    ms = cycle_lengths(iters, restart)
+    total = pre + post
+    for m in ms:
+        total += cyc + m * cyc_m + sum(it + j * it_j for j in range(m))
+    return total
 
 
 # ------------------------------------------------------------------ reference arm
@@ -414,11 +425,29 @@ def our_arm(args):
     _abi.check(L.irkdev_level_value_format(dev._h, 0, 0, C.byref(vf0)))
     s_fmt = "row classes" if vf0.value == 3 else "u8 value codes"
     s_bytes = (1 + 8 + 8 + 8) * n if vf0.value == 3 else (7 + 8 + 8 + 1 + 8) * n
-    # whole-solve byte model on the actual hierarchies and iterations
+    # whole-solve byte models on the actual hierarchies and iterations
     nnz_mk = prob.M.nnz
-    model = [solve_bytes(info, levels, (r.iterations, r.n_reorth, r.cycles), n, S, nnz_mk)[0]
-             for r in reps]
-    solve_gbs = sum(model) / (ms / 1e3) / 1e9 / 1.0
+    mb = (C.c_double * 8)()
+    _abi.check(L.irkdev_model_bytes(dev._h, mb))
+    fmt_model = [format_model_bytes(list(mb), r.iterations) for r in reps]
+    survey = [survey_model_bytes(info, levels, r.iterations, n, S, nnz_mk) for r in reps]
+    secs = ms / 1e3
+    fmt_gbs = sum(fmt_model) / secs / 1e9
+    survey_gbs = sum(survey) / secs / 1e9
+    # measured DRAM traffic of one whole step (ncu, every launch, caches not
+    # flushed: tools/step_traffic.sh -> profiles/r2/traffic_<W>.json), scaled by
+    # each step's iteration count
+    meas = None
+    try:
+        tr = json.loads((ROOT / "profiles" / "r2" / f"traffic_{WORKLOAD[:2]}.json").read_text())
+        mbytes = sum(tr["dram_bytes_per_iteration"] * r.iterations for r in reps)
+        meas = {"dram_bytes_per_iteration": tr["dram_bytes_per_iteration"],
+                "achieved_gbs": mbytes / secs / 1e9, "frac": mbytes / secs / 1e9 / hbm_peak,
+                "source": f"profiles/r2/traffic_{WORKLOAD[:2]}.json (ncu dram__bytes_read.sum + "
+                          f"dram__bytes_write.sum over all {tr['launches']} launches of one "
+                          f"{tr['iterations']}-iteration step)"}
+    except Exception:
+        pass
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -426,7 +455,7 @@ def our_arm(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": DATA,
         "config": config({"parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                          "gmres_iterations": its, "reorth_passes": [r.n_reorth for r in reps],
+                          "gmres_iterations": its,
                           "restart_cycles": [r.cycles for r in reps],
                           "true_rel_residual": [r.true_rel_residual for r in reps],
                           "launches_per_iteration": cnt[2], "setup_seconds": setup_s,
@@ -445,11 +474,18 @@ def our_arm(args):
                               "bytes_per_launch": s_bytes, "ms_per_launch": sms.value,
                               "achieved_gbs": s_bytes / (sms.value * 1e-3) / 1e9,
                               "frac": s_bytes / (sms.value * 1e-3) / 1e9 / hbm_peak},
-        "solve_roofline": {"model_bytes_per_solve": sum(model) / len(model),
-                           "achieved_gbs": solve_gbs, "peak_gbs": hbm_peak,
-                           "frac": solve_gbs / hbm_peak,
-                           "definition": "SURVEY.md §8(d) per-kernel byte model on the actual "
-                                         "hierarchies and iteration counts / measured solve time"},
+        "solve_roofline": {
+            "frac": (meas or {}).get("frac", fmt_gbs / hbm_peak),
+            "basis": "measured DRAM traffic" if meas else "format model",
+            "measured": meas,
+            "format_model": {"bytes_per_solve": sum(fmt_model) / len(fmt_model), "achieved_gbs": fmt_gbs,
+                             "frac": fmt_gbs / hbm_peak,
+                             "definition": "each kernel's operands read once and results written once in "
+                                           "their stored formats (irkdev_model_bytes), per solve"},
+            "survey_model": {"bytes_per_solve": sum(survey) / len(survey), "achieved_gbs": survey_gbs,
+                             "frac": survey_gbs / hbm_peak,
+                             "definition": "SURVEY.md §8(d) formula (CSR operators, DCGS2 ORTH 8sN(2j+6))"},
+            "peak_gbs": hbm_peak},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

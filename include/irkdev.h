@@ -229,6 +229,13 @@ int irkdev_graph_info(const irkdev* d, int* launches_per_iteration, int* graph_m
  * before the GMRES loop, [1] per restart cycle, [2] per Arnoldi iteration,
  * [3] once per step after the loop. */
 int irkdev_launch_counts(const irkdev* d, int* counts4);
+/* Algorithmic HBM bytes of the captured step graph (the roofline numerator:
+ * every kernel's operands read once and results written once, in their stored
+ * formats): out8 = {pre, cycle, cycle_per_m, iteration, iteration_per_j,
+ * post, 0, 0}; a step of cycles c_k (m_k columns) and iterations j moves
+ * pre + post + sum_k (cycle + m_k cycle_per_m) + sum_j (iteration + j
+ * iteration_per_j) bytes. */
+int irkdev_model_bytes(const irkdev* d, double* out8);
 /* The solver's CUDA stream (cudaStream_t) for event timing by the caller. */
 int irkdev_stream(const irkdev* d, void** stream);
 

@@ -109,6 +109,7 @@ _SIGS = {
     "irkdev_time_kernel": (C.c_int, [V, C.c_int, C.c_int, dptr]),
     "irkdev_graph_info": (C.c_int, [V, iptr, iptr]),
     "irkdev_launch_counts": (C.c_int, [V, iptr]),
+    "irkdev_model_bytes": (C.c_int, [V, dptr]),
     "irkdev_stream": (C.c_int, [V, C.POINTER(C.c_void_p)]),
 }
 

@@ -534,6 +534,14 @@ int irkdev_launch_counts(const irkdev* d, int* c) {
     });
 }
 
+int irkdev_model_bytes(const irkdev* d, double* out) {
+    return guard([&] {
+        const auto& t = d->s->model_bytes();
+        const double v[8] = {t[0].fixed, t[1].fixed, t[1].per_j, t[2].fixed, t[2].per_j, t[3].fixed, 0.0, 0.0};
+        for (int i = 0; i < 8; ++i) out[i] = v[i];
+    });
+}
+
 int irkdev_stream(const irkdev* d, void** stream) {
     return guard([&] { *stream = static_cast<void*>(d->s->stream()); });
 }

@@ -63,6 +63,47 @@ bool pdl_enabled() {
 void set_pdl_scope(bool on) { g_pdl_scope = on; }
 
 namespace {
+thread_local Tally* g_tally = nullptr;
+void tally(double fixed, double per_j = 0.0) {
+    if (g_tally) {
+        g_tally->fixed += fixed;
+        g_tally->per_j += per_j;
+    }
+}
+}  // namespace
+
+void tally_open(Tally* t) { g_tally = t; }
+void tally_close() { g_tally = nullptr; }
+
+double mat_bytes(const Mat& A) {
+    const double vb = A.vf == kF64 ? 8.0 : A.vf == kU16 ? 2.0 : 1.0;
+    if (A.fmt == kDia) return A.vf == kCls ? static_cast<double>(A.rows) : static_cast<double>(A.nd) * A.rows * vb;
+    const double rowstruct = A.fmt == kCsrVec ? 4.0 * (A.rows + 1) : 4.0 * ((A.rows + 31) / 32 + 1);
+    return static_cast<double>(A.nnz) * (4.0 + vb) + rowstruct;
+}
+
+namespace {
+// One SpMV in its stored format: the operator once, the x operand once per
+// column, and the epilogue's row vectors (omega/a_ii from a per-code or
+// per-class table moves no wd array).
+double spmv_bytes(const Mat& A, int xm, int epi, const SpmvArgs& a) {
+    const double n = A.rows, nc = A.cols;
+    const bool wd_table = A.fmt == kDia && (A.vf == kCls ? A.wdtab != nullptr
+                                                         : A.vf == kU8 && A.wdtab && A.diag0 >= 0);
+    double b = mat_bytes(A);
+    b += 8.0 * nc;                                   // x, or r for x = wd .* r
+    if (xm == kXWdR && !wd_table) b += 8.0 * nc;     // wd of x = wd .* r
+    b += 8.0 * n;                                    // y
+    const bool r_is_x = xm == kXWdR && A.rows == A.cols;
+    if (epi == kEResid && !r_is_x) b += 8.0 * n;
+    if (epi == kESmooth) b += 8.0 * n + (wd_table ? 0.0 : 8.0 * n);
+    if (epi == kEProlong) b += a.zb ? 8.0 * n : 8.0 * n + (wd_table ? 0.0 : 8.0 * n);
+    if (a.y2) b += 16.0 * n;                         // y2 = wd2 .* y
+    return b;
+}
+}  // namespace
+
+namespace {
 
 // Programmatic dependent launch (opt-in, IRK_PDL=1: measured 2% slower on
 // C2, profiles/r1/ab3_pdl.txt): every kernel is launched with
@@ -1701,6 +1742,7 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_residual(GmresBufs g, const 
 
 // ------------------------------------------------------------------ launchers
 void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st) {
+    if (A.rows > 0) tally(spmv_bytes(A, xmode, epi, a));
 #define IRK_SPMV_CASE(X, E)                         \
     if (xmode == X && epi == E) {                   \
         launch_spmv<X, E>(A, a, st);                \
@@ -1725,6 +1767,7 @@ void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecR
         throw InvalidArgument("stage_op: row classes need 7 diagonals and one joint class array");
     const bool u8 = M.vf == kU8;
     const bool cls = M.vf == kCls;
+    tally((cls ? static_cast<double>(n) : mat_bytes(M) + mat_bytes(K)) + 16.0 * c.s * n);
     switch (c.s) {
 #define IRK_OP_CASE(S)                                                             \
     case S:                                                                        \
@@ -1747,6 +1790,11 @@ void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecR
 
 void sweep_dia(const Mat& K, VecRef w, VecRef v, const SweepTerms& t, double* store, VecRef out,
                int n, cudaStream_t st) {
+    {
+        int terms = 0;
+        for (int q = 0; q < t.nt; ++q) terms += t.buf[q] != nullptr;
+        tally(mat_bytes(K) + 8.0 * n * (3 + terms) + (store ? 8.0 * n : 0.0));
+    }
     switch (K.vf) {
     case kCls:
         if (K.nd != 7) throw InvalidArgument("row classes need 7 diagonals");
@@ -1768,19 +1816,23 @@ void bottom_cycle(const BotDesc& d, const double* r_in, double* z_out, cudaStrea
     std::call_once(attr, [] {
         IRK_CUDA_CHECK(cudaFuncSetAttribute(k_bottom, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     });
+    tally(static_cast<double>(d.bytes) + 16.0 * d.lv[0].n);
     launch(k_bottom, 1, kBotThreads, d.smem, st, d, r_in, z_out);
 }
 
 void combine(VecRef v, const SweepTerms& t, VecRef out, int n, cudaStream_t st) {
+    tally(8.0 * n * (t.nt + 2));
     launch(k_combine, blocks_for(n, 256), 256, 0, st, n, v, t, out);
 }
 
 void axpy(double alpha, const double* x, VecRef y, int n, cudaStream_t st) {
+    tally(24.0 * n);
     launch(k_axpy, blocks_for(n, 256), 256, 0, st, n, alpha, x, y);
 }
 
 void dense_mv(int n, const double* Ainv, VecRef r, VecRef z, cudaStream_t st) {
     const size_t smem = sizeof(double) * (static_cast<size_t>(n) * n + n);
+    tally(8.0 * n * n + 16.0 * n);
     if (smem <= 200 * 1024)
         launch(k_dense_mv, 1, 256, smem, st, n, Ainv, r, z);
     else
@@ -1788,12 +1840,14 @@ void dense_mv(int n, const double* Ainv, VecRef r, VecRef z, cudaStream_t st) {
 }
 
 void wd_times_r(int n, const double* wd, VecRef r, double* z, cudaStream_t st) {
+    tally(24.0 * n);
     launch(k_wd_times_r, blocks_for(n, 256), 256, 0, st, n, wd, r, z);
 }
 
 void stage_rhs_finish(const double* ku, const double* lift, const double* forcing, double* b,
                       int n, int s,
                       cudaStream_t st) {
+    tally(8.0 * n * (1 + (lift ? 1 : 0)) + 8.0 * n * s * (1 + (forcing ? 1 : 0)));
     launch(k_stage_rhs, blocks_for(n, 256), 256, 0, st, n, s, ku, lift, forcing, b);
 }
 
@@ -1801,6 +1855,7 @@ void irk_update(const double* u, const double* x, const double* hb, int n, int s
                 cudaStream_t st) {
     HB h;
     for (int q = 0; q < s; ++q) h.v[q] = hb[q];
+    tally(8.0 * n * (s + 2));
     launch(k_irk_update, blocks_for(n, 256), 256, 0, st, n, s, u, x, h, un);
 }
 
@@ -1808,24 +1863,29 @@ static size_t red_smem(int nv) { return sizeof(double) * (kRedThreads / 32 * nv 
 
 void gm_init(const GmresBufs& g, const double* b, double* r, double rel_tol, int restart,
              int max_iter, int ortho, int side, cudaStream_t st) {
+    tally(16.0 * g.sN);
     launch(g.use_cond ? k_gm_init<true> : k_gm_init<false>, g.nchunks, kRedThreads, 0, st, g, b, r, rel_tol, restart, max_iter, ortho, side);
 }
 
 void copy_ref(VecRef x, VecRef y, long long n, cudaStream_t st) {
+    tally(16.0 * n);
     launch(k_copy_ref, static_cast<int>((n + 4 * 256 - 1) / (4 * 256)), 256, 0, st, x, y, n);
 }
 
 void gm_cycle_begin(const GmresBufs& g, const double* r, cudaStream_t st) {
+    tally(16.0 * g.sN);
     launch(g.use_cond ? k_gm_cycle_begin<true> : k_gm_cycle_begin<false>, g.nchunks, kRedThreads, 0, st, g, r);
 }
 
 void gm_blockdot(const GmresBufs& g, int pass, cudaStream_t st) {
     // capacity for up to restart+1 basis vectors plus ||w||
     const int nv = kMaxRestart + 2;
+    tally(16.0 * g.sN, 8.0 * g.sN);  // v_0..v_j and w: (j + 2) vectors
     launch(k_gm_blockdot, g.nchunks, kRedThreads, red_smem(nv), st, g, pass);
 }
 
 void gm_update(const GmresBufs& g, int pass, cudaStream_t st) {
+    tally(24.0 * g.sN, 8.0 * g.sN);  // reads v_0..v_j, w; writes w: (j + 3)
     launch(k_gm_update, g.nchunks, kRedThreads, sizeof(double) * (kRedThreads / 32 + 1 + kMaxRestart + 8), st, g, pass);
 }
 
@@ -1844,24 +1904,34 @@ void dgs_prof_read(long long* out) {
 }
 
 void gm_dgs_dot(const GmresBufs& g, int finalize, cudaStream_t st) {
+    // iteration j: v_0..v_{j-1}, vt_j, w = (j + 2) vectors; cycle end (m
+    // columns): v_0..v_{m-1}, w' = (m + 1) vectors
+    if (finalize)
+        tally(8.0 * g.sN, 8.0 * g.sN);
+    else
+        tally(16.0 * g.sN, 8.0 * g.sN);
     launch(k_dgs_dot, g.nchunks, kRedThreads, dgs_smem(g), st, g, finalize);
 }
 
 void gm_dgs_update(const GmresBufs& g, cudaStream_t st) {
+    tally(32.0 * g.sN, 8.0 * g.sN);  // reads v_0..v_{j-1}, vt_j, w; writes v_j, w': (j + 4)
     launch(g.use_cond ? k_dgs_update<true> : k_dgs_update<false>, g.nchunks, kRedThreads, dgs_smem(g), st, g);
 }
 
 void gm_normalize(const GmresBufs& g, cudaStream_t st) {
+    tally(16.0 * g.sN);
     launch(g.use_cond ? k_gm_normalize<true> : k_gm_normalize<false>, g.nchunks, kRedThreads, 0, st, g);
 }
 
 void gm_solution(const GmresBufs& g, double* x, cudaStream_t st) {
     launch(k_gm_backsub, 1, 1, 0, st, g);
+    tally(16.0 * g.sN, 8.0 * g.sN);  // x += Z y: x in and out, m basis vectors
     launch(k_gm_xupdate, g.nchunks, kRedThreads, 0, st, g, x);
 }
 
 void gm_residual(const GmresBufs& g, const double* b, const double* ax, double* r,
                  cudaStream_t st) {
+    tally(24.0 * g.sN);
     launch(g.use_cond ? k_gm_residual<true> : k_gm_residual<false>, g.nchunks, kRedThreads, 0, st, g, b, ax, r);
 }
 

@@ -86,6 +86,19 @@ struct SpmvArgs {
     const double* wd2 = nullptr;
 };
 
+// Algorithmic-bytes tally (the roofline's numerator): while a
+// tally is open on this thread, every launcher adds the bytes its kernel must
+// move -- each array it reads or writes once, in its STORED format (row
+// classes, u8/u16 codes, SELL/CSR indices) -- as fixed + per_j * j, where j is
+// the Arnoldi index (iteration kernels) or the cycle length m (cycle end).
+struct Tally {
+    double fixed = 0.0, per_j = 0.0;
+};
+void tally_open(Tally* t);
+void tally_close();
+// Bytes of one pass over the stored operator (values, indices, row structure).
+double mat_bytes(const Mat& A);
+
 // Programmatic dependent launch, opt-in via IRK_PDL=1.
 bool pdl_enabled();
 // Programmatic launch for the kernels recorded while the scope is on (the

@@ -1026,11 +1026,21 @@ int count_nodes(cudaGraph_t g) {
 }
 
 // Kernel launches recorded by fn, counted from a throw-away capture.
+// With `t`, also tallies the recorded kernels' algorithmic bytes.
 template <class F>
-int count_launches(cudaStream_t st, F&& fn) {
+int count_launches(cudaStream_t st, F&& fn, dev::Tally* t = nullptr) {
     cudaGraph_t g = nullptr;
     IRK_CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    fn();
+    dev::tally_open(t);
+    try {
+        fn();
+    } catch (...) {
+        dev::tally_close();
+        cudaStreamEndCapture(st, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    dev::tally_close();
     IRK_CUDA_CHECK(cudaStreamEndCapture(st, &g));
     const int k = count_nodes(g);
     cudaGraphDestroy(g);
@@ -1073,10 +1083,11 @@ void DeviceSolver::build_graph(bool lift, bool forcing, int restart, int max_ite
     };
     auto post = [&]() { dev::irk_update(u_, x_, hb_.data(), n_, s_, unext_, st_); };
 
-    launch_counts_[0] = count_launches(st_, pre);
-    launch_counts_[1] = count_launches(st_, [&] { cycle_begin(); cycle_end(); });
-    launch_counts_[2] = count_launches(st_, [&] { record_iteration(); });
-    launch_counts_[3] = count_launches(st_, post);
+    tally_ = {};
+    launch_counts_[0] = count_launches(st_, pre, &tally_[0]);
+    launch_counts_[1] = count_launches(st_, [&] { cycle_begin(); cycle_end(); }, &tally_[1]);
+    launch_counts_[2] = count_launches(st_, [&] { record_iteration(); }, &tally_[2]);
+    launch_counts_[3] = count_launches(st_, post, &tally_[3]);
     if (use_cond) {
         cudaStream_t s2 = nullptr, s3 = nullptr;
         IRK_CUDA_CHECK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));

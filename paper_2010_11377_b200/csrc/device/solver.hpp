@@ -134,6 +134,9 @@ public:
     double time_kernel(int which, int reps);
     int launches_per_iteration() const { return launches_per_iter_; }
     const std::array<int, 4>& launch_counts() const { return launch_counts_; }
+    // Algorithmic bytes per phase (pre, cycle, iteration, post) of the last
+    // recorded step graph, each as fixed + per_j * j (dev::Tally).
+    const std::array<dev::Tally, 4>& model_bytes() const { return tally_; }
     int graph_mode() const { return graph_mode_; }
 
 private:
@@ -201,6 +204,7 @@ private:
     unsigned g_opt_gen_ = ~0u;  // dev::option_generation() the graphs were recorded with
     double g_rtol_ = -1.0;
     int launches_per_iter_ = 0;
+    std::array<dev::Tally, 4> tally_{};
     std::array<int, 4> launch_counts_{};
     bool compress_values_ = true;
     int ortho_ = 1;  // 1 DCGS2 (default), 0 CGS + conditional second pass
