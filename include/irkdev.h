@@ -113,6 +113,10 @@ int irk_hierarchy_levels(const irk_hierarchy* h);
 int irk_hierarchy_level(const irk_hierarchy* h, int level, int which, irk_csr* out);
 const double* irk_hierarchy_inv_diag(const irk_hierarchy* h, int level);
 const double* irk_hierarchy_coarse_inverse(const irk_hierarchy* h, int* n);
+/* The dense V-cycle tail operator attached by the setup (NULL if none):
+ * *from = first level it replaces, B row-major n x *ld with n = rows of that
+ * level (see csrc/host/tail.cpp). */
+const double* irk_hierarchy_tail(const irk_hierarchy* h, int* from, int* n, int* ld);
 void irk_hierarchy_free(irk_hierarchy* h);
 
 /* ------------------------------------------------------ on-disk formats */

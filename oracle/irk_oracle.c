@@ -121,9 +121,45 @@ static void spmv_epi(const or_csr* A, const double* x, const double* r, const do
 }
 
 /* ------------------------------------------------------------ V-cycle */
+/* z = B r in k_tail_mv's order (kernels.cu, kTailWarps = 4): per row, 128
+ * thread partials -- thread t adds the pairs p = t, t+128, ... (B[2p] r[2p],
+ * then B[2p+1] r[2p+1] when 2p+1 < n) from 0.0 -- each warp of 32 folded by
+ * the xor butterfly 16, 8, 4, 2, 1, and the 4 warp sums added in order. */
+static void tail_mv(int n, int ld, const double* B, const double* r, double* z) {
+    enum { W = 4, S = 32 * W };
+    const int np = (n + 1) / 2;
+    for (int i = 0; i < n; ++i) {
+        const double* b = B + (long)i * ld;
+        double ws[W];
+        for (int w = 0; w < W; ++w) {
+            double lane[32], nxt[32];
+            for (int l = 0; l < 32; ++l) {
+                double acc = 0.0;
+                for (int p = 32 * w + l; p < np; p += S) {
+                    acc = acc + b[2 * p] * r[2 * p];
+                    if (2 * p + 1 < n) acc = acc + b[2 * p + 1] * r[2 * p + 1];
+                }
+                lane[l] = acc;
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                for (int l = 0; l < 32; ++l) nxt[l] = lane[l] + lane[l ^ o];
+                memcpy(lane, nxt, sizeof lane);
+            }
+            ws[w] = lane[0];
+        }
+        double sum = ws[0];
+        for (int w = 1; w < W; ++w) sum = sum + ws[w];
+        z[i] = sum;
+    }
+}
+
 static void vcycle_level(const or_hier* h, double** wd, int l, const double* r, double* z) {
     const or_csr* A = &h->A[l];
     const int n = A->rows;
+    if (h->tail && l == h->tail_from) {
+        tail_mv(n, h->tail_ld, h->tail, r, z);
+        return;
+    }
     if (l == h->nlev - 1) {
         for (int i = 0; i < n; ++i) {
             double s = 0.0;

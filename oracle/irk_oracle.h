@@ -25,6 +25,10 @@ typedef struct {
     int nc;
     double omega;
     int pre, post;
+    /* dense V-cycle tail operator (the product's setup, csrc/host/tail.cpp):
+     * levels >= tail_from are z = B r, B row-major n x tail_ld; -1 = none */
+    int tail_from, tail_ld;
+    const double* tail;
 } or_hier;
 
 typedef struct {

@@ -208,6 +208,15 @@ class AmgHierarchy:
     def sizes(self) -> list[int]:
         return [self.level(l).n_rows for l in range(self.n_levels())]
 
+    def tail(self):
+        """(level, B): the dense operator of the V-cycle below `level`
+        (csrc/host/tail.cpp), B of shape (n, ld); (-1, None) if none."""
+        f, n, ld = C.c_int(), C.c_int(), C.c_int()
+        p = _abi.lib().irk_hierarchy_tail(self._h, C.byref(f), C.byref(n), C.byref(ld))
+        if not p:
+            return -1, None
+        return f.value, np.ctypeslib.as_array(p, (n.value * ld.value,)).copy().reshape(n.value, ld.value)
+
 
 def amg_setup(A: CsrMatrix, params: AmgParams | None = None) -> AmgHierarchy:
     h = C.c_void_p()

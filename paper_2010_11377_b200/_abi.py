@@ -73,6 +73,7 @@ _SIGS = {
     "irk_hierarchy_inv_diag": (dptr, [V, C.c_int]),
     "irk_hierarchy_coarse_inverse": (dptr, [V, iptr]),
     "irk_hierarchy_free": (None, [V]),
+    "irk_hierarchy_tail": (dptr, [V, iptr, iptr, iptr]),
     "irkdev_hierarchy": (C.c_int, [V, C.c_int, C.POINTER(V)]),
     "irk_mm_write": (C.c_int, [C.POINTER(irk_csr), C.c_char_p]),
     "irk_mm_read": (C.c_int, [C.c_char_p, C.POINTER(V)]),

@@ -266,6 +266,14 @@ const double* irk_hierarchy_coarse_inverse(const irk_hierarchy* h, int* n) {
     return h->h.coarse_inverse.data();
 }
 
+const double* irk_hierarchy_tail(const irk_hierarchy* h, int* from, int* n, int* ld) {
+    const irkb::Hierarchy& H = h->h;
+    *from = H.tail_from;
+    *n = H.tail_from > 0 ? H.levels[H.tail_from].A.rows : 0;
+    *ld = H.tail_ld;
+    return H.tail_from > 0 ? H.tail.data() : nullptr;
+}
+
 void irk_hierarchy_free(irk_hierarchy* h) { delete h; }
 
 int irk_mm_write(const irk_csr* A, const char* path) {

@@ -12,6 +12,8 @@
 #include <string>
 
 #include "../host/sparse.hpp"
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace irkb {
@@ -561,6 +563,65 @@ __global__ void k_axpy(int n, double alpha, const double* __restrict__ x, VecRef
 
 // Coarsest solve z = Ainv r: the CTA stages Ainv (row-major) and r in shared
 // memory with coalesced loads, then each thread forms one row sequentially.
+// z = B r for the dense V-cycle tail operator B (n x ld, row-major; tail.cpp).
+// kTailWarps warps per row, two rows per 256-thread CTA.  Thread t of a row
+// (t = 32 w + lane) adds the pairs p = t, t + 32 kTailWarps, ... (B[2p] r[2p],
+// then B[2p+1] r[2p+1] when 2p+1 < n) in order to a partial started at 0.0;
+// each warp folds its 32 partials with an xor butterfly (16, 8, 4, 2, 1) and
+// the warp sums are added in warp order -- the order oracle/irk_oracle.c
+// tail_mv restates.  B is static: before waiting on its predecessor every warp
+// prefetches its share of the row into L2, so the matrix stream overlaps the
+// latency-bound restriction that produces r.
+constexpr int kTailWarps = 4;
+__global__ void __launch_bounds__(256) k_tail_mv(int n, int ld, const double* __restrict__ B,
+                                                 const double* __restrict__ r, double* __restrict__ z) {
+    pdl_trigger();
+    __shared__ double s_w[256 / 32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rg = warp / kTailWarps;                 // row slot in the CTA
+    const int t = (warp % kTailWarps) * 32 + lane;    // thread index within the row
+    const int row = blockIdx.x * (256 / (32 * kTailWarps)) + rg;
+    const int np = (n + 1) >> 1;
+    const double2* b2 = reinterpret_cast<const double2*>(B + static_cast<long long>(row < n ? row : 0) * ld);
+    if (row < n)
+        for (int p = t * 8; p < np; p += 32 * kTailWarps * 8)  // one 128-byte line per thread step
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(b2 + p));
+    pdl_wait();
+    double acc = 0.0;
+    if (row < n) {
+        const double2* r2 = reinterpret_cast<const double2*>(r);
+        const int nfull = n >> 1;  // pairs with both entries inside the row
+        constexpr int S = 32 * kTailWarps;
+        int p = t;
+        for (; p + 3 * S < nfull; p += 4 * S) {
+            double2 b[4], x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) b[u] = __ldg(b2 + p + S * u);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = __ldg(r2 + p + S * u);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                acc = acc + b[u].x * x[u].x;
+                acc = acc + b[u].y * x[u].y;
+            }
+        }
+        for (; p < np; p += S) {
+            const double2 b = __ldg(b2 + p);
+            acc = acc + b.x * __ldg(r + 2 * p);
+            if (2 * p + 1 < n) acc = acc + b.y * __ldg(r + 2 * p + 1);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = acc + __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) s_w[warp] = acc;
+    __syncthreads();
+    if (row < n && t == 0) {
+        double sum = s_w[rg * kTailWarps];
+        for (int w = 1; w < kTailWarps; ++w) sum = sum + s_w[rg * kTailWarps + w];
+        z[row] = sum;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_dense_mv(int n, const double* __restrict__ A, VecRef rr,
                                                   VecRef zr) {
     pdl_trigger();
@@ -1837,6 +1898,12 @@ void dense_mv(int n, const double* Ainv, VecRef r, VecRef z, cudaStream_t st) {
         launch(k_dense_mv, 1, 256, smem, st, n, Ainv, r, z);
     else
         launch(k_dense_mv_big, blocks_for(n, 128), 128, 0, st, n, Ainv, r, z);
+}
+
+void tail_mv(int n, int ld, const double* B, const double* r, double* z, cudaStream_t st) {
+    tally(8.0 * n * ld + 16.0 * n);
+    constexpr int rows_per_cta = 256 / (32 * kTailWarps);
+    launch(k_tail_mv, (n + rows_per_cta - 1) / rows_per_cta, 256, 0, st, n, ld, B, r, z);
 }
 
 void wd_times_r(int n, const double* wd, VecRef r, double* z, cudaStream_t st) {

@@ -141,6 +141,9 @@ void combine(VecRef v, const SweepTerms& t, VecRef out, int n, cudaStream_t st);
 // y += alpha * x, element-wise (rounded multiply then add).
 void axpy(double alpha, const double* x, VecRef y, int n, cudaStream_t st);
 
+// z = B r with the dense V-cycle tail operator (n x ld row-major, ld even;
+// tail.cpp): one launch in place of the cycle below the tail level.
+void tail_mv(int n, int ld, const double* B, const double* r, double* z, cudaStream_t st);
 // Coarsest-level solve z = Ainv r (dense row-major inverse).
 void dense_mv(int n, const double* Ainv, VecRef r, VecRef z, cudaStream_t st);
 

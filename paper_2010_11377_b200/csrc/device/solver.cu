@@ -517,6 +517,13 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
             dh.lv[l] = d;
         }
         dh.nc = h.levels.back().A.rows;
+        if (h.tail_from > 0) {
+            dh.tail_from = h.tail_from;
+            dh.tail_ld = h.tail_ld;
+            dh.tail = alloc(h.tail.size());
+            IRK_CUDA_CHECK(cudaMemcpy(dh.tail, h.tail.data(), sizeof(double) * h.tail.size(),
+                                      cudaMemcpyHostToDevice));
+        }
         build_bottom(dh, h);
         dh.cinv = alloc(static_cast<size_t>(dh.nc) * dh.nc);
         IRK_CUDA_CHECK(cudaMemcpy(dh.cinv, h.coarse_inverse.data(),
@@ -707,9 +714,12 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
     auto scope = [&](int l) { dev::set_pdl_scope(pdl_from >= 0 && l >= pdl_from); };
     auto out_of = [&](int l) { return l == first ? z0 : dev::plain(H.lv[l].z); };
     // levels >= bot run in the single-CTA bottom kernel
-    const int bot = dev::option("IRK_BOTTOM", 1) != 0 && H.bot_from > first && pre == 1 && post == 1
+    // levels >= tail are one dense matvec (IRK_TAIL=0: the recursive cycle)
+    const int tail = dev::option("IRK_TAIL", 1) != 0 && H.tail_from > first ? H.tail_from : -1;
+    const int bot = tail < 0 && dev::option("IRK_BOTTOM", 1) != 0 && H.bot_from > first && pre == 1 &&
+                            post == 1
                         ? H.bot_from : -1;
-    const int down_end = bot > 0 ? bot : L - 1;
+    const int down_end = tail > 0 ? tail : bot > 0 ? bot : L - 1;
     for (int l = first; l < down_end; ++l) {
         DevLevel& d = H.lv[l];
         scope(l);
@@ -743,20 +753,23 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
         dev::SpmvArgs ra;
         ra.x = dev::plain(d.t);
         ra.y = dev::plain(H.lv[l + 1].r);
-        if (zr_on() && pre == 1 && l + 2 < L && l + 1 != bot) {
+        if (zr_on() && pre == 1 && l + 2 < L && l + 1 != bot && l + 1 != tail) {
             ra.y2 = H.lv[l + 1].zr;
             ra.wd2 = H.lv[l + 1].wd;
         }
         dev::spmv(d.R, dev::kXPlain, dev::kEPlain, ra, st_);
     }
-    if (bot > 0) {
+    if (tail > 0) {
+        scope(tail);
+        dev::tail_mv(H.lv[tail].n, H.tail_ld, H.tail, H.lv[tail].r, H.lv[tail].z, st_);
+    } else if (bot > 0) {
         scope(bot);
         dev::bottom_cycle(H.bot, H.lv[bot].r, H.lv[bot].z, st_);
     } else {
         scope(L - 1);
         dev::dense_mv(H.nc, H.cinv, rhs_of(L - 1), out_of(L - 1), st_);
     }
-    for (int l = (bot > 0 ? bot - 1 : L - 2); l >= first; --l) {
+    for (int l = (tail > 0 ? tail - 1 : bot > 0 ? bot - 1 : L - 2); l >= first; --l) {
         DevLevel& d = H.lv[l];
         scope(l);
         dev::SpmvArgs pa;
@@ -1539,6 +1552,39 @@ double DeviceSolver::time_kernel(int which, int reps) {
         IRK_CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
         for (int r = 0; r < reps; ++r)
             record_vcycle(0, dev::plain(a.as<double>()), dev::plain(b.as<double>()), first);
+        IRK_CUDA_CHECK(cudaStreamEndCapture(st_, &gr));
+        cudaGraphExec_t ge;
+        IRK_CUDA_CHECK(cudaGraphInstantiate(&ge, gr, 0));
+        cudaGraphDestroy(gr);
+        IRK_CUDA_CHECK(cudaGraphLaunch(ge, st_));
+        cudaEvent_t e0, e1;
+        IRK_CUDA_CHECK(cudaEventCreate(&e0));
+        IRK_CUDA_CHECK(cudaEventCreate(&e1));
+        IRK_CUDA_CHECK(cudaEventRecord(e0, st_));
+        IRK_CUDA_CHECK(cudaGraphLaunch(ge, st_));
+        IRK_CUDA_CHECK(cudaEventRecord(e1, st_));
+        IRK_CUDA_CHECK(cudaEventSynchronize(e1));
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaGraphExecDestroy(ge);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return static_cast<double>(ms) / reps;
+    }
+    if (which == 40) {
+        // graph-captured dense tail matvecs, cycling through the hierarchies
+        DevBuf a(sizeof(double) * stride_), b(sizeof(double) * stride_);
+        IRK_CUDA_CHECK(cudaMemsetAsync(a.as<void>(), 0, sizeof(double) * stride_, st_));
+        std::vector<int> ks;
+        for (int k = 0; k < static_cast<int>(hier_.size()); ++k)
+            if (hier_[k].tail) ks.push_back(k);
+        if (ks.empty()) return 0.0;
+        cudaGraph_t gr;
+        IRK_CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+        for (int r = 0; r < reps; ++r) {
+            const DevHier& H = hier_[ks[r % ks.size()]];
+            dev::tail_mv(H.lv[H.tail_from].n, H.tail_ld, H.tail, a.as<double>(), b.as<double>(), st_);
+        }
         IRK_CUDA_CHECK(cudaStreamEndCapture(st_, &gr));
         cudaGraphExec_t ge;
         IRK_CUDA_CHECK(cudaGraphInstantiate(&ge, gr, 0));

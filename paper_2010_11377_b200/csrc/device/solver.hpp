@@ -69,6 +69,9 @@ struct DevHier {
     AmgParams prm;
     int bot_from = -1;    // first level handled by the single-CTA bottom kernel
     dev::BotDesc bot;
+    int tail_from = -1;   // first level replaced by the dense tail operator
+    int tail_ld = 0;
+    double* tail = nullptr;
 };
 
 class DeviceSolver {

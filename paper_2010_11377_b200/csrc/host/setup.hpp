@@ -86,10 +86,21 @@ struct Hierarchy {
     std::vector<AmgLevel> levels;
     std::vector<double> coarse_inverse;  // dense row-major n_L x n_L
     AmgParams params;
+    // Dense operator of the V-cycle below level tail_from (tail.cpp): row-major
+    // n x tail_ld (n = levels[tail_from].A.rows, tail_ld = n rounded up to
+    // even); tail_from = -1 when no level is small enough.
+    int tail_from = -1, tail_ld = 0;
+    std::vector<double> tail;
     int n_levels() const { return static_cast<int>(levels.size()); }
 };
 
 Hierarchy amg_setup(const Csr& A, const AmgParams& p);
+// Attaches the dense tail operator B_l for the first level l >= 1 (above the
+// coarsest) with at most max_n rows (tail.cpp); amg_setup and
+// amg_setup_device call it with tail_max_rows() (IRK_TAIL_MAX, default 3300;
+// 0 disables).
+void attach_tail(Hierarchy& h, int max_n);
+int tail_max_rows();
 // Dense inverse of the coarsest operator (Gauss-Jordan, partial pivoting).
 std::vector<double> dense_inverse_host(const Csr& A);
 

@@ -275,7 +275,8 @@ class or_csr(C.Structure):
 class or_hier(C.Structure):
     _fields_ = [("nlev", C.c_int), ("A", C.POINTER(or_csr)), ("P", C.POINTER(or_csr)),
                 ("R", C.POINTER(or_csr)), ("inv_diag", C.POINTER(dptr)), ("cinv", dptr),
-                ("nc", C.c_int), ("omega", C.c_double), ("pre", C.c_int), ("post", C.c_int)]
+                ("nc", C.c_int), ("omega", C.c_double), ("pre", C.c_int), ("post", C.c_int),
+                ("tail_from", C.c_int), ("tail_ld", C.c_int), ("tail", dptr)]
 
 
 class or_sys(C.Structure):
@@ -347,8 +348,12 @@ class OracleSystem:
             self._keep.extend([Aarr, Parr, Rarr, ids, cinv])
             idp = (dptr * L)(*[_d(d) for d in ids])
             self._keep.append(idp)
+            tail_from, tail = h.get("tail", (-1, None))
+            tl = None if tail is None else np.ascontiguousarray(tail, np.float64)
+            self._keep.append(tl)
             hs.append(or_hier(L, Aarr, Parr, Rarr, idp, _d(cinv), int(round(np.sqrt(cinv.size))),
-                              h["omega"], h["pre"], h["post"]))
+                              h["omega"], h["pre"], h["post"], tail_from,
+                              0 if tl is None else tl.shape[1], None if tl is None else _d(tl)))
         harr = (or_hier * len(hs))(*hs)
         arrs = [np.ascontiguousarray(x, np.float64).ravel() for x in (A, b, At)]
         sobv = np.ascontiguousarray(sob, np.int32)
@@ -419,4 +424,5 @@ def hierarchy_dict(h, omega=2.0 / 3.0, pre=1, post=1):
             d["P"].append((p.row_ptr, p.col_idx, p.vals, p.n_cols))
             d["R"].append((r.row_ptr, r.col_idx, r.vals, r.n_cols))
     d["cinv"] = h.coarse_inverse()
+    d["tail"] = h.tail()
     return d

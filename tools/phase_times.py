@@ -20,7 +20,8 @@ names = {0: "stage operator", 1: "fine smoother SpMV", 2: "precond apply (3 V-cy
          20: "empty kernel, graph launch (per kernel)", 21: "empty kernel, stream launch (per kernel)",
          30: "graph: V-cycle (hot, repeated)", 31: "graph: V-cycle below level 1",
          32: "graph: V-cycle below level 2", 33: "graph: V-cycle below level 3",
-         34: "graph: V-cycle below level 4", 35: "graph: coarse solve only"}
+         34: "graph: V-cycle below level 4", 35: "graph: coarse solve only",
+         40: "graph: dense tail matvec (cycling hierarchies)"}
 for w, name in names.items():
     ms = C.c_double()
     _abi.check(L.irkdev_time_kernel(Pc._dev._h, w, 50, C.byref(ms)))
