@@ -26,6 +26,8 @@ typedef enum {
     IRK_ENUMERICAL = 3,   /* NumericalError (common.hpp:28-37)            */
     IRK_ECUDA = 4,        /* CUDA runtime failure / no device             */
     IRK_EUNSUPPORTED = 5, /* valid reference option not run on the device */
+    IRK_EIO = 6,          /* std::runtime_error of file I/O / parsing
+                             (butcher.cpp:300-313, csr.cpp:240-290)      */
     IRK_EINTERNAL = 9
 } irk_status;
 
@@ -99,6 +101,15 @@ int irk_ldu(int s, const double* A, double* L, double* D, double* U);
 int irk_precond_coeff(int scheme, int s, int kind, double* Atilde, int* structure);
 /* custom_coeff (butcher.hpp:71-73): validates and infers the structure. */
 int irk_custom_coeff(int s, const double* Atilde, int* structure);
+/* read_coeff_file (butcher.cpp:300-313): the stage count then s*s row-major
+ * values; *s is set, Atilde (cap >= s*s doubles, or NULL to query s) gets
+ * the matrix.  IRK_EIO: cannot open / bad stage count / truncated data. */
+int irk_read_coeff_file(const char* path, int cap, int* s, double* Atilde);
+/* make_coeff (study.cpp:269-282): kinds 0-3 as irk_precond_coeff; kind 4
+ * (custom) reads custom_path (IRK_EINVAL when NULL/empty or when its size is
+ * not s), then custom_coeff validates it and infers the structure. */
+int irk_make_coeff(int scheme, int s, int kind, const char* custom_path, double* Atilde,
+                   int* structure);
 
 typedef struct irk_hierarchy irk_hierarchy;
 /* amg_setup (amg.hpp:52): the reference's smoothed-aggregation coarsening. */

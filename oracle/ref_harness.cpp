@@ -56,6 +56,9 @@ int guard(F&& f) {
     } catch (const NumericalError& e) {
         g_err = e.what();
         return 3;
+    } catch (const std::runtime_error& e) {  // read_coeff_file, matrix market
+        g_err = e.what();
+        return 6;
     } catch (const std::exception& e) {
         g_err = e.what();
         return 9;
@@ -304,6 +307,77 @@ int ref_solver_create(int n, const int* m_rp, const int* m_ci, const double* m_v
             S->M, S->F, S->coeff, ht, SubsolverKind::AmgVcycle, prm);
         S->op = std::make_unique<StageOperator>(S->M, S->F, S->table.A, ht);
         *out = S;
+    });
+}
+
+// Same with every AmgParams field (amg.hpp:14-29) and an optional custom
+// coefficient matrix (kind 4: custom_coeff(At), butcher.cpp:290-297).
+// amgd = {theta, jacobi_weight, prolongation_weight},
+// amgi = {pre, post, smoother, prolongation_steps, max_coarse, max_levels}.
+int ref_solver_create_ex(int n, const int* m_rp, const int* m_ci, const double* m_v,
+                         const int* k_rp, const int* k_ci, const double* k_v, int scheme,
+                         int s, int kind, const double* custom_At, double ht,
+                         const double* amgd, const int* amgi, void** out) {
+    return guard([&] {
+        auto S = std::make_unique<RefSolver>();
+        S->M = std::make_shared<const CsrMatrix>(from_arrays(n, n, m_rp, m_ci, m_v));
+        S->F = std::make_shared<const CsrMatrix>(from_arrays(n, n, k_rp, k_ci, k_v));
+        S->table = make_table(scheme, s);
+        if (kind == 4) {
+            DenseMatrix At(s, s);
+            for (int i = 0; i < s * s; ++i) At.values[i] = custom_At[i];
+            S->coeff = custom_coeff(std::move(At));
+        } else {
+            S->coeff = precond_coeff(S->table, static_cast<CoeffKind>(kind));
+        }
+        S->ht = ht;
+        AmgParams prm;
+        prm.theta = amgd[0];
+        prm.jacobi_weight = amgd[1];
+        prm.prolongation_weight = amgd[2];
+        prm.pre_sweeps = amgi[0];
+        prm.post_sweeps = amgi[1];
+        prm.smoother = amgi[2] ? AmgSmoother::GaussSeidel : AmgSmoother::DampedJacobi;
+        prm.prolongation_steps = amgi[3];
+        prm.max_coarse = amgi[4];
+        prm.max_levels = amgi[5];
+        S->P = std::make_unique<BlockPreconditioner>(
+            S->M, S->F, S->coeff, ht, SubsolverKind::AmgVcycle, prm);
+        S->op = std::make_unique<StageOperator>(S->M, S->F, S->table.A, ht);
+        *out = S.release();
+    });
+}
+
+// custom_coeff(read_coeff_file(path)) (butcher.cpp:290-313), the way the
+// reference's acceptance criterion 3 builds its custom kind
+// (acceptance.cpp:195-215); cap >= s*s or At == NULL to query s.
+int ref_coeff_file(const char* path, int cap, int* s, double* At, int* structure) {
+    return guard([&] {
+        const DenseMatrix M = read_coeff_file(path);
+        *s = M.n_rows;
+        if (!At) return;
+        if (cap < M.n_rows * M.n_cols) throw std::invalid_argument("ref_coeff_file: buffer too small");
+        for (int i = 0; i < M.n_rows * M.n_cols; ++i) At[i] = M.values[i];
+        const PrecondCoeff pc = custom_coeff(M);
+        *structure = static_cast<int>(pc.structure);
+    });
+}
+
+// A V-cycle of the hierarchy with every AmgParams field (see ref_solver_create_ex).
+int ref_amg_setup_ex(int n, const int* rp, const int* ci, const double* v, const double* amgd,
+                     const int* amgi, void** out) {
+    return guard([&] {
+        AmgParams prm;
+        prm.theta = amgd[0];
+        prm.jacobi_weight = amgd[1];
+        prm.prolongation_weight = amgd[2];
+        prm.pre_sweeps = amgi[0];
+        prm.post_sweeps = amgi[1];
+        prm.smoother = amgi[2] ? AmgSmoother::GaussSeidel : AmgSmoother::DampedJacobi;
+        prm.prolongation_steps = amgi[3];
+        prm.max_coarse = amgi[4];
+        prm.max_levels = amgi[5];
+        *out = new AmgHierarchy(amg_setup(from_arrays(n, n, rp, ci, v), prm));
     });
 }
 

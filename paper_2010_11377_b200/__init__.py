@@ -35,15 +35,16 @@ from enum import IntEnum
 import numpy as np
 
 from . import _abi
-from ._abi import CudaError, NumericalError, SingularError, Unsupported, check
+from ._abi import CudaError, IoError, NumericalError, SingularError, Unsupported, check
 
 __all__ = [
     "CsrMatrix", "Scheme", "CoeffKind", "CoeffStructure", "ButcherTable", "PrecondCoeff",
     "AmgParams", "AmgHierarchy", "GmresConfig", "SolveReport", "IrkStepResult",
     "LinearParabolicSystem", "ProblemSetup", "BlockPreconditioner", "StageOperator",
     "make_radau_iia", "make_lobatto_iiic", "make_table", "ldu_factorize", "precond_coeff",
-    "custom_coeff", "amg_setup", "amg_setup_device", "make_heat_setup", "make_double_glazing_setup", "irk_step",
+    "custom_coeff", "read_coeff_file", "make_coeff", "amg_setup", "amg_setup_device", "make_heat_setup", "make_double_glazing_setup", "irk_step",
     "integrate", "SingularError", "NumericalError", "CudaError", "Unsupported",
+    "IoError",
 ]
 
 
@@ -156,6 +157,32 @@ def custom_coeff(Atilde: np.ndarray) -> PrecondCoeff:
     st = C.c_int()
     check(_abi.lib().irk_custom_coeff(At.shape[0], _abi.as_d(At.ravel()), C.byref(st)))
     return PrecondCoeff(CoeffKind.Custom, At.copy(), CoeffStructure(st.value))
+
+
+def read_coeff_file(path) -> np.ndarray:
+    """read_coeff_file (butcher.cpp:300-313): the s x s matrix of a
+    coefficient file ("s" then s*s row-major values).  IoError on a missing
+    file, a bad stage count or truncated data."""
+    L = _abi.lib()
+    s = C.c_int()
+    bp = str(path).encode()
+    check(L.irk_read_coeff_file(bp, 0, C.byref(s), None))
+    At = np.zeros(s.value * s.value)
+    check(L.irk_read_coeff_file(bp, At.size, C.byref(s), _abi.as_d(At)))
+    return At.reshape(s.value, s.value)
+
+
+def make_coeff(table: ButcherTable, kind: CoeffKind, custom_coeff_path=None) -> PrecondCoeff:
+    """make_coeff (study.cpp:269-282): precond_coeff for the built-in kinds; for
+    Custom the matrix of `custom_coeff_path` (ValueError without a path or when
+    its size is not table.s), validated by custom_coeff."""
+    s = table.s
+    At = np.zeros(s * s)
+    st = C.c_int()
+    path = None if custom_coeff_path is None else str(custom_coeff_path).encode()
+    check(_abi.lib().irk_make_coeff(int(table.scheme), s, int(kind), path, _abi.as_d(At),
+                                    C.byref(st)))
+    return PrecondCoeff(CoeffKind(kind), At.reshape(s, s), CoeffStructure(st.value))
 
 
 @dataclass

@@ -17,7 +17,7 @@ import numpy as np
 LIB_PATH = Path(os.environ.get("IRK_LIB") or Path(__file__).resolve().parent / "lib" / "libirkdev.so")
 HEADER = Path(__file__).resolve().parent.parent / "include" / "irkdev.h"
 
-IRK_OK, IRK_EINVAL, IRK_ESINGULAR, IRK_ENUMERICAL, IRK_ECUDA, IRK_EUNSUPPORTED = 0, 1, 2, 3, 4, 5
+IRK_OK, IRK_EINVAL, IRK_ESINGULAR, IRK_ENUMERICAL, IRK_ECUDA, IRK_EUNSUPPORTED, IRK_EIO = 0, 1, 2, 3, 4, 5, 6
 
 dptr = C.POINTER(C.c_double)
 iptr = C.POINTER(C.c_int)
@@ -66,6 +66,8 @@ _SIGS = {
     "irk_ldu": (C.c_int, [C.c_int, dptr, dptr, dptr, dptr]),
     "irk_precond_coeff": (C.c_int, [C.c_int, C.c_int, C.c_int, dptr, iptr]),
     "irk_custom_coeff": (C.c_int, [C.c_int, dptr, iptr]),
+    "irk_read_coeff_file": (C.c_int, [C.c_char_p, C.c_int, iptr, dptr]),
+    "irk_make_coeff": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_char_p, dptr, iptr]),
     "irk_amg_setup": (C.c_int, [C.POINTER(irk_csr), C.POINTER(irk_amg_params), C.POINTER(V)]),
     "irk_amg_setup_device": (C.c_int, [C.POINTER(irk_csr), C.POINTER(irk_amg_params), C.c_int, C.POINTER(V)]),
     "irk_hierarchy_levels": (C.c_int, [V]),
@@ -158,6 +160,11 @@ class Unsupported(RuntimeError):
     """A valid reference option the device path does not implement."""
 
 
+class IoError(RuntimeError):
+    """File I/O or parse failure (the reference's plain std::runtime_error,
+    butcher.cpp:300-313, csr.cpp:240-290)."""
+
+
 def check(status: int) -> None:
     if status == IRK_OK:
         return
@@ -172,6 +179,8 @@ def check(status: int) -> None:
         raise CudaError(msg)
     if status == IRK_EUNSUPPORTED:
         raise Unsupported(msg)
+    if status == IRK_EIO:
+        raise IoError(msg)
     raise RuntimeError(f"irkdev internal error ({status}): {msg}")
 
 

@@ -51,6 +51,9 @@ int guard(F&& f) {
     } catch (const irkb::Unsupported& e) {
         g_err = e.what();
         return IRK_EUNSUPPORTED;
+    } catch (const irkb::IoError& e) {
+        g_err = e.what();
+        return IRK_EIO;
     } catch (const std::bad_alloc&) {
         g_err = "out of host memory";
         return IRK_EINTERNAL;
@@ -235,6 +238,29 @@ int irk_precond_coeff(int scheme, int s, int kind, double* Atilde, int* structur
 int irk_custom_coeff(int s, const double* Atilde, int* structure) {
     return guard([&] {
         const irkb::Coeff c = irkb::custom_coeff(s, std::vector<double>(Atilde, Atilde + s * s));
+        *structure = static_cast<int>(c.structure);
+    });
+}
+
+int irk_read_coeff_file(const char* path, int cap, int* s, double* Atilde) {
+    return guard([&] {
+        irkb::check(path != nullptr, "read_coeff_file: null path");
+        int ns = 0;
+        const std::vector<double> At = irkb::read_coeff_file(path, ns);
+        *s = ns;
+        irkb::check(Atilde == nullptr || cap >= ns * ns, "read_coeff_file: output buffer too small");
+        if (Atilde) std::memcpy(Atilde, At.data(), sizeof(double) * At.size());
+    });
+}
+
+int irk_make_coeff(int scheme, int s, int kind, const char* custom_path, double* Atilde,
+                   int* structure) {
+    return guard([&] {
+        irkb::check(kind >= 0 && kind <= 4, "make_coeff: unknown kind");
+        const irkb::Tableau t = irkb::make_tableau(static_cast<irkb::Scheme>(scheme), s);
+        const irkb::Coeff c = irkb::make_coeff(t, static_cast<irkb::CoeffKind>(kind),
+                                               custom_path ? custom_path : "");
+        std::memcpy(Atilde, c.At.data(), sizeof(double) * s * s);
         *structure = static_cast<int>(c.structure);
     });
 }

@@ -6,6 +6,7 @@
 // kinds J / GSL / DU / LD follow butcher.cpp:190-288.  All of this is s x s
 // host arithmetic uploaded as constants.
 #include <cmath>
+#include <fstream>
 
 #include "orthopoly.hpp"
 #include "setup.hpp"
@@ -232,6 +233,29 @@ Coeff custom_coeff(int s, const std::vector<double>& At) {
     require_nonzero_diagonal(s, At);
     pc.At = At;
     return pc;
+}
+
+std::vector<double> read_coeff_file(const std::string& path, int& s) {
+    std::ifstream in(path);
+    if (!in) throw IoError("cannot open coefficient file: " + path);
+    s = 0;
+    if (!(in >> s) || s < 1) throw IoError("coefficient file: bad stage count");
+    std::vector<double> At(static_cast<size_t>(s) * s);
+    for (double& a : At)
+        if (!(in >> a)) throw IoError("coefficient file: truncated matrix data");
+    return At;
+}
+
+Coeff make_coeff(const Tableau& t, CoeffKind kind, const std::string& custom_path) {
+    if (kind != CoeffKind::Custom) return precond_coeff(t, kind);
+    if (custom_path.empty())
+        throw InvalidArgument("custom preconditioner requested without --custom-coeff");
+    int s = 0;
+    std::vector<double> At = read_coeff_file(custom_path, s);
+    if (s != t.s)
+        throw InvalidArgument("custom coefficient matrix is " + std::to_string(s) + "x" +
+                              std::to_string(s) + ", expected s = " + std::to_string(t.s));
+    return custom_coeff(s, At);
 }
 
 void distinct_diagonals(int s, const std::vector<double>& At,

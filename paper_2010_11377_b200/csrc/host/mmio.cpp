@@ -13,7 +13,7 @@ namespace irkb {
 
 void write_matrix_market(const Csr& A, const std::string& path) {
     std::FILE* f = std::fopen(path.c_str(), "w");
-    if (!f) throw std::runtime_error("cannot open for write: " + path);
+    if (!f) throw IoError("cannot open for write: " + path);
     std::fprintf(f, "%%%%MatrixMarket matrix coordinate real general\n");
     std::fprintf(f, "%d %d %d\n", A.rows, A.cols, A.nnz());
     for (int i = 0; i < A.rows; ++i)
@@ -21,14 +21,14 @@ void write_matrix_market(const Csr& A, const std::string& path) {
             std::fprintf(f, "%d %d %.17g\n", i + 1, A.idx[k] + 1, A.val[k]);
     const bool ok = std::ferror(f) == 0;
     std::fclose(f);
-    if (!ok) throw std::runtime_error("write failed: " + path);
+    if (!ok) throw IoError("write failed: " + path);
 }
 
 // C stdio parsing (strtod is correctly rounded, like the reference's
 // istream extraction, so %.17g files round-trip exactly).
 Csr read_matrix_market(const std::string& path) {
     std::FILE* f = std::fopen(path.c_str(), "r");
-    if (!f) throw std::runtime_error("cannot open for read: " + path);
+    if (!f) throw IoError("cannot open for read: " + path);
     struct Closer {
         std::FILE* f;
         ~Closer() { std::fclose(f); }
@@ -66,10 +66,10 @@ Csr read_matrix_market(const std::string& path) {
         long i, j;
         char vbuf[128];
         if (std::fscanf(f, "%ld %ld %127s", &i, &j, vbuf) != 3)
-            throw std::runtime_error("matrix market: truncated entry list");
+            throw IoError("matrix market: truncated entry list");
         char* end = nullptr;
         const double v = std::strtod(vbuf, &end);
-        if (end == vbuf) throw std::runtime_error("matrix market: truncated entry list");
+        if (end == vbuf) throw IoError("matrix market: truncated entry list");
         t.add(static_cast<int>(i - 1), static_cast<int>(j - 1), v);
         if (symmetric && i != j) t.add(static_cast<int>(j - 1), static_cast<int>(i - 1), v);
     }

@@ -14,6 +14,7 @@
 #pragma once
 
 #include <array>
+#include <string>
 #include <vector>
 
 #include "sparse.hpp"
@@ -63,6 +64,14 @@ struct Coeff {
 };
 Coeff precond_coeff(const Tableau& t, CoeffKind kind);
 Coeff custom_coeff(int s, const std::vector<double>& At);
+// read_coeff_file (butcher.cpp:300-313): "s" then s*s row-major values,
+// whitespace separated, parsed with the same stream extraction; IoError on a
+// missing file, a bad stage count or truncated data.  Returns At, sets s.
+std::vector<double> read_coeff_file(const std::string& path, int& s);
+// make_coeff (study.cpp:269-282): precond_coeff for the built-in kinds; for
+// Custom, read_coeff_file(custom_path), its size checked against t.s, then
+// custom_coeff.
+Coeff make_coeff(const Tableau& t, CoeffKind kind, const std::string& custom_path);
 
 // ------------------------------------------------------------------ AMG
 struct AmgParams {

@@ -34,6 +34,11 @@ struct Unsupported : std::runtime_error {
 struct CudaError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+// File I/O and parse failures: the reference throws plain std::runtime_error
+// (butcher.cpp:300-313, csr.cpp:240-290).
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
 
 inline void check(bool ok, const char* msg) {
     if (!ok) throw InvalidArgument(msg);

@@ -52,6 +52,12 @@ class Ref:
             L.ref_solver_create.argtypes = [C.c_int, iptr, iptr, dptr, iptr, iptr, dptr, C.c_int,
                                             C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
                                             C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+            L.ref_solver_create_ex.argtypes = [C.c_int, iptr, iptr, dptr, iptr, iptr, dptr,
+                                               C.c_int, C.c_int, C.c_int, dptr, C.c_double,
+                                               dptr, iptr, C.POINTER(C.c_void_p)]
+            L.ref_amg_setup_ex.argtypes = [C.c_int, iptr, iptr, dptr, dptr, iptr,
+                                           C.POINTER(C.c_void_p)]
+            L.ref_coeff_file.argtypes = [C.c_char_p, C.c_int, iptr, dptr, iptr]
             L.ref_amg_setup.argtypes = [C.c_int, iptr, iptr, dptr, C.c_double, C.c_int, C.c_int,
                                         C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
             L.ref_irk_step.argtypes = [C.c_void_p, dptr, dptr, C.c_double, C.c_int, C.c_int,
@@ -151,6 +157,35 @@ class Ref:
         return RefHierarchy(h)
 
     @classmethod
+    def amg_ex(cls, csr, amg):
+        """amg_setup with every AmgParams field (amg: an AmgParams-like object)."""
+        rp, ci, v = csr
+        h = C.c_void_p()
+        keep = [np.ascontiguousarray(rp, np.int32), np.ascontiguousarray(ci, np.int32),
+                np.ascontiguousarray(v, np.float64)]
+        d, i = _amg_arrays(amg)
+        cls.check(cls.lib().ref_amg_setup_ex(len(rp) - 1, _i(keep[0]), _i(keep[1]), _d(keep[2]),
+                                             _d(d), _i(i), C.byref(h)))
+        return RefHierarchy(h)
+
+    @classmethod
+    def coeff_file(cls, path):
+        """custom_coeff(read_coeff_file(path)) -> (At, structure); raises
+        RuntimeError with the reference's status (6 = std::runtime_error)."""
+        L = cls.lib()
+        s = C.c_int()
+        st = C.c_int()
+        bp = str(path).encode()
+        rc = L.ref_coeff_file(bp, 0, C.byref(s), None, C.byref(st))
+        if rc != 0:
+            raise RefError(rc, L.ref_last_error().decode())
+        At = np.zeros(s.value * s.value)
+        rc = L.ref_coeff_file(bp, At.size, C.byref(s), _d(At), C.byref(st))
+        if rc != 0:
+            raise RefError(rc, L.ref_last_error().decode())
+        return At.reshape(s.value, s.value), st.value
+
+    @classmethod
     def spmv(cls, csr, x, n_cols=None):
         rp, ci, v = csr
         n = len(rp) - 1
@@ -158,6 +193,19 @@ class Ref:
         x = np.ascontiguousarray(x, np.float64)
         cls.check(cls.lib().ref_spmv(n, n_cols or len(x), _i(rp), _i(ci), _d(v), _d(x), _d(y)))
         return y
+
+
+class RefError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"reference error {status}: {msg}")
+        self.status = status
+
+
+def _amg_arrays(amg):
+    d = np.array([amg.theta, amg.jacobi_weight, amg.prolongation_weight], np.float64)
+    i = np.array([amg.pre_sweeps, amg.post_sweeps, amg.smoother, amg.prolongation_steps,
+                  amg.max_coarse, amg.max_levels], np.int32)
+    return d, i
 
 
 class RefHierarchy:
@@ -199,15 +247,30 @@ class RefHierarchy:
 class RefSolver:
     """BlockPreconditioner(AMG) + StageOperator of the reference on given M, K."""
 
-    def __init__(self, M, K, scheme, s, kind, ht, theta=0.25, pre=1, post=1, max_coarse=64):
+    def __init__(self, M, K, scheme, s, kind, ht, theta=0.25, pre=1, post=1, max_coarse=64,
+                 amg=None, custom_At=None):
+        """amg (an AmgParams-like object) overrides theta/pre/post/max_coarse
+        and sets every AmgParams field; kind 4 with custom_At = custom_coeff."""
         self._keep = [np.ascontiguousarray(a) for a in (*M, *K)]
         m_rp, m_ci, m_v, k_rp, k_ci, k_v = self._keep
         self.n = len(m_rp) - 1
         self.s = s
         h = C.c_void_p()
-        Ref.check(Ref.lib().ref_solver_create(self.n, _i(m_rp), _i(m_ci), _d(m_v), _i(k_rp), _i(k_ci),
-                                              _d(k_v), scheme, s, kind, ht, theta, pre, post,
-                                              max_coarse, C.byref(h)))
+        if amg is None and custom_At is None:
+            Ref.check(Ref.lib().ref_solver_create(self.n, _i(m_rp), _i(m_ci), _d(m_v), _i(k_rp),
+                                                  _i(k_ci), _d(k_v), scheme, s, kind, ht, theta,
+                                                  pre, post, max_coarse, C.byref(h)))
+        else:
+            if amg is None:
+                import paper_2010_11377_b200 as P
+                amg = P.AmgParams(theta=theta, pre_sweeps=pre, post_sweeps=post,
+                                  max_coarse=max_coarse)
+            d, i = _amg_arrays(amg)
+            At = None if custom_At is None else np.ascontiguousarray(custom_At, np.float64).ravel()
+            self._keep.extend([d, i, At])
+            Ref.check(Ref.lib().ref_solver_create_ex(self.n, _i(m_rp), _i(m_ci), _d(m_v), _i(k_rp),
+                                                     _i(k_ci), _d(k_v), scheme, s, kind, _d(At), ht,
+                                                     _d(d), _i(i), C.byref(h)))
         self.h = h
 
     def __del__(self):

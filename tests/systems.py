@@ -76,3 +76,42 @@ def rel_l2(a, b):
     a, b = np.asarray(a), np.asarray(b)
     den = np.linalg.norm(b)
     return np.linalg.norm(a - b) / (den if den > 0 else 1.0)
+
+
+def custom_case(cells, s, upper=False, seed=None, scheme=P.Scheme.RadauIIA, ht=0.01, path=None):
+    """Heat with a Custom preconditioner read from a coefficient file written
+    like the reference's acceptance criterion 3 (acceptance.cpp:195-215)."""
+    import os
+    import tempfile
+    At = seeded_triangular(s, 777 + s if seed is None else seed, upper=upper)
+    prob = P.make_heat_setup(cells)
+    table = P.make_table(scheme, s)
+    with tempfile.TemporaryDirectory() as d:
+        f = path or os.path.join(d, "coeff.txt")
+        write_coeff(f, At)
+        coeff = P.make_coeff(table, P.CoeffKind.Custom, f)
+    c = Case(prob.M, prob.F, table, coeff, ht, None, prob.f_lift)
+    c.problem = prob
+    return c
+
+
+def write_coeff(path, At, fmt="%.17g "):
+    """A coefficient file as acceptance.cpp:195-215 writes it."""
+    s = At.shape[0]
+    with open(path, "w") as f:
+        f.write(f"{s}\n")
+        for i in range(s):
+            f.write("".join(fmt % At[i, j] for j in range(s)) + "\n")
+
+
+def seeded_triangular(s, seed, upper=False):
+    """acceptance.cpp:201-211: diagonal U(0.3, 1.2), off-diagonal 0.4 U(0.3, 1.2)."""
+    rng = np.random.default_rng(seed)
+    At = np.zeros((s, s))
+    for i in range(s):
+        for j in range(s):
+            if (j > i and not upper) or (j < i and upper):
+                continue
+            u = rng.uniform(0.3, 1.2)
+            At[i, j] = u if i == j else 0.4 * u
+    return At

@@ -116,3 +116,23 @@ def test_zero_state_stays_zero():
     o = c.oracle.step(np.zeros(c.n), None)
     assert o["iterations"] == 0 and o["converged"]
     assert not np.any(o["u_next"])
+
+
+@pytest.mark.parametrize("s,upper", [(2, False), (3, True), (5, False), (7, False), (7, True)])
+def test_custom_coeff_step_matches_reference(s, upper):
+    """The Custom kind through a coefficient file (acceptance.cpp:171-241):
+    the reference's BlockPreconditioner with custom_coeff(read_coeff_file)."""
+    from systems import custom_case
+    c = custom_case(32, s, upper)
+    u = c.problem.initial()
+    o = c.oracle.step(u, c.f_lift)
+    M, K = c.M, c.K
+    r = RefSolver((M.row_ptr, M.col_idx, M.vals), (K.row_ptr, K.col_idx, K.vals), 0, s, 4, c.ht,
+                  custom_At=c.coeff.Atilde)
+    v = np.random.default_rng(s).uniform(-1, 1, c.n * s)
+    assert rel_l2(c.oracle.precond_apply(v), r.precond_apply(v)) <= 1e-12
+    rr = r.step(u, c.f_lift)
+    assert o["converged"] and rr["converged"]
+    assert abs(o["iterations"] - rr["iterations"]) <= 1
+    assert rel_l2(o["K"], rr["K"]) <= 1e-9
+    assert rel_l2(o["u_next"], rr["u_next"]) <= 1e-9
