@@ -12,7 +12,8 @@
  * Restated algorithms (reference file:line):
  *   or_spmv           csr.cpp:102-114       sequential row sums
  *   or_stage_apply    stage.cpp:28-44       s F-products, s M-products, s^2 axpys
- *   or_vcycle         amg.cpp:115-168, 229-237  V(pre,post) damped Jacobi
+ *   or_vcycle         amg.cpp:115-168, 229-237  V(pre,post) damped Jacobi or
+ *                     Gauss-Seidel (forward pre-sweeps, backward post-sweeps)
  *   or_precond_apply  stage.cpp:138-182     diagonal / forward / backward sweeps
  *   or_irk_step(_f)   irk.cpp:9-68, gmres.cpp:14-142 with the documented
  *                     deviations of the B200 path: GMRES(m) restarts,
@@ -153,6 +154,43 @@ static void tail_mv(int n, int ld, const double* B, const double* r, double* z) 
     }
 }
 
+/* Gauss-Seidel sweep in place, CSR column order, the diagonal skipped
+ * (amg.cpp:125-140). */
+static void gs_sweep(const or_csr* A, const double* dinv, const double* r, double* z,
+                     int backward) {
+    const int n = A->rows;
+    for (int t = 0; t < n; ++t) {
+        const int i = backward ? n - 1 - t : t;
+        double s = r[i];
+        for (int k = A->ptr[i]; k < A->ptr[i + 1]; ++k)
+            if (A->idx[k] != i) s -= A->val[k] * z[A->idx[k]];
+        z[i] = s * dinv[i];
+    }
+}
+
+static void vcycle_level(const or_hier* h, double** wd, int l, const double* r, double* z);
+
+/* amg.cpp:144-168 with the Gauss-Seidel smoother: the reference's order. */
+static void vcycle_level_gs(const or_hier* h, double** wd, int l, const double* r, double* z) {
+    const or_csr* A = &h->A[l];
+    const int n = A->rows;
+    const int nc = h->A[l + 1].rows;
+    double* t = (double*)malloc(sizeof(double) * n);
+    double* rc = (double*)malloc(sizeof(double) * nc);
+    double* zc = (double*)malloc(sizeof(double) * nc);
+    for (int i = 0; i < n; ++i) z[i] = 0.0;
+    for (int sw = 0; sw < h->pre; ++sw) gs_sweep(A, h->inv_diag[l], r, z, 0);
+    spmv_epi(A, z, r, NULL, NULL, 0, EPI_RESID, t);
+    or_spmv(&h->R[l], t, rc);
+    vcycle_level(h, wd, l + 1, rc, zc);
+    spmv_epi(&h->P[l], zc, r, NULL, z, 0, EPI_PROLONG, t);
+    memcpy(z, t, sizeof(double) * n);
+    for (int sw = 0; sw < h->post; ++sw) gs_sweep(A, h->inv_diag[l], r, z, 1);
+    free(t);
+    free(rc);
+    free(zc);
+}
+
 static void vcycle_level(const or_hier* h, double** wd, int l, const double* r, double* z) {
     const or_csr* A = &h->A[l];
     const int n = A->rows;
@@ -166,6 +204,10 @@ static void vcycle_level(const or_hier* h, double** wd, int l, const double* r, 
             for (int j = 0; j < n; ++j) s += h->cinv[(long)i * n + j] * r[j];
             z[i] = s;
         }
+        return;
+    }
+    if (h->smoother) {
+        vcycle_level_gs(h, wd, l, r, z);
         return;
     }
     const int nc = h->A[l + 1].rows;

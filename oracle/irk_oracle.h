@@ -29,6 +29,7 @@ typedef struct {
      * levels >= tail_from are z = B r, B row-major n x tail_ld; -1 = none */
     int tail_from, tail_ld;
     const double* tail;
+    int smoother;      /* 0 damped Jacobi, 1 Gauss-Seidel (amg.cpp:125-140) */
 } or_hier;
 
 typedef struct {

@@ -368,8 +368,6 @@ int irkdev_create(const irk_csr* M, const irk_csr* K, int s, const double* A, co
         std::vector<irkb::Hierarchy> hv;
         for (int k = 0; k < n_hier; ++k) hv.push_back(hiers[k]->h);
         const irkb::AmgParams prm = to_params(amg);
-        if (prm.smoother != 0)
-            throw irkb::Unsupported("device solver: only the damped-Jacobi smoother is implemented");
         auto* d = new irkdev;
         try {
             d->s = std::make_unique<irkb::DeviceSolver>(Mc, Kc, s, Av, bv, Atv,

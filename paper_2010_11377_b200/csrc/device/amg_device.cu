@@ -673,7 +673,7 @@ Hierarchy amg_setup_device(const Csr& A, const AmgParams& p, int device) {
     check(A.rows > 0, "amg_setup: empty matrix");
     check(p.theta > 0.0 && p.theta < 1.0, "amg_setup: theta must be in (0,1)");
     check(p.pre_sweeps >= 1 && p.post_sweeps >= 1, "amg_setup: sweeps must be >= 1");
-    if (p.smoother != 0) throw Unsupported("amg: only the damped-Jacobi smoother runs on the device");
+    check(p.smoother == 0 || p.smoother == 1, "amg_setup: unknown smoother");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
         throw CudaError("no CUDA device: amg_setup_device has no CPU fallback");

@@ -2008,6 +2008,79 @@ void dot(const double* x, const double* y, long long n, double* partials, unsign
     launch(k_dot, nch > 0 ? nch : 1, kRedThreads, 0, st, x, y, n, partials, counter, out);
 }
 
+// ------------------------------------------------------------------ Gauss-Seidel
+// One sweep in ONE CTA: the depth levels of the schedule run one after the
+// other separated by a barrier, one thread per row.  A sweep is a chain of
+// nlev dependent steps (C2: ~2000 at level 0, ~3100 at level 1 with two
+// prolongator smoothing steps) and is latency-bound by construction -- the
+// reference's own sweep is sequential (amg.cpp:125-140) -- so the kernel
+// keeps the per-step path short: the next level's headers are loaded while
+// the current level computes, a row's entries and operands are issued 8 at a
+// time, and the updated values are plain coherent loads of zout (the
+// barrier orders them within the CTA).
+namespace {
+constexpr int kGsThreads = 512;
+
+template <bool kBack>
+__device__ __forceinline__ void gs_row(const GsSweep& S, int4 h, int q, const double* __restrict__ r,
+                                       const double* __restrict__ zin, double* zout) {
+    const int i = h.x, st = h.y, len = h.z;
+    double s = __ldg(r + i);
+    for (int k = 0; k < len; k += 8) {
+        int c[8];
+        double a[8], zv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const bool ok = k + u < len;
+            c[u] = ok ? __ldg(S.ci + st + k + u) : i;
+            a[u] = ok ? __ldg(S.val + st + k + u) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const bool upd = kBack ? c[u] > i : c[u] < i;
+            zv[u] = upd ? zout[c[u]] : (zin ? __ldg(zin + c[u]) : 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (k + u < len) s = s - a[u] * zv[u];
+    }
+    zout[i] = s * __ldg(S.dinv + q);
+}
+
+template <bool kBack>
+__global__ void __launch_bounds__(kGsThreads) k_gs_sweep(GsSweep S, VecRef rr, const double* zin,
+                                                         VecRef zr) {
+    pdl_trigger();
+    const int tid = threadIdx.x;
+    int q = S.lptr[0] + tid, le = S.lptr[1];
+    int4 h = q < le ? __ldg(S.hdr + q) : make_int4(-1, 0, 0, 0);
+    pdl_wait();
+    const double* r = rr.get();
+    double* zout = zr.get();
+    for (int L = 0; L < S.nlev; ++L) {
+        const int qn = S.lptr[L + 1] + tid, ne = S.lptr[L + 2];
+        const int4 hn = qn < ne ? __ldg(S.hdr + qn) : make_int4(-1, 0, 0, 0);
+        if (h.x >= 0) gs_row<kBack>(S, h, q, r, zin, zout);
+        for (int q2 = q + kGsThreads; q2 < le; q2 += kGsThreads)
+            gs_row<kBack>(S, __ldg(S.hdr + q2), q2, r, zin, zout);
+        __syncthreads();
+        h = hn;
+        q = qn;
+        le = ne;
+    }
+}
+}  // namespace
+
+void gs_sweep(const GsSweep& S, bool backward, VecRef r, const double* zin, VecRef zout,
+              cudaStream_t st) {
+    // headers, entries, dinv, r, zout written, and one operand per entry
+    tally(16.0 * S.n + 12.0 * S.nnz + 8.0 * S.n + 8.0 * S.n + 8.0 * S.n + 8.0 * S.nnz);
+    if (backward)
+        launch(k_gs_sweep<true>, 1, kGsThreads, 0, st, S, r, zin, zout);
+    else
+        launch(k_gs_sweep<false>, 1, kGsThreads, 0, st, S, r, zin, zout);
+}
+
 void set_smem_limits() {
     const int big = static_cast<int>(sizeof(double) * ((kRedThreads / 32 + 1) * (2 * kMaxRestart + 4) + 16 +
                                                        3 * (kMaxRestart + 4)));

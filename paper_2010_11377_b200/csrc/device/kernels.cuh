@@ -175,6 +175,28 @@ struct BotDesc {
     long long* prof = nullptr; // optional phase timestamps (globaltimer ns, 16 slots)
 };
 void bottom_cycle(const BotDesc& d, const double* r_in, double* z_out, cudaStream_t st);
+// Gauss-Seidel sweep (amg.cpp:125-140) of one level, level-scheduled: the
+// rows are grouped by dependency depth (row i after every row j it reads
+// updated, j < i forward / j > i backward) and stored in that order --
+// per position q a header {i, start, len} into the off-diagonal entries
+// (column order, the diagonal dropped: the reference skips it) and
+// dinv[q] = 1 / a_ii.  Rows of one depth are independent.
+struct GsSweep {
+    const int4* hdr = nullptr;   // n headers in schedule order
+    const int* ci = nullptr;     // off-diagonal columns, schedule order
+    const double* val = nullptr; // off-diagonal values
+    const double* dinv = nullptr;
+    const int* lptr = nullptr;   // nlev + 2 (last repeated)
+    int nlev = 0, n = 0;
+    long long nnz = 0;           // off-diagonal entries
+};
+// zout_i = (r_i - sum_{j != i} a_ij z_j) / a_ii in CSR column order, with z_j
+// the updated value (zout) for j before i in sweep order and zin_j otherwise
+// (zin == nullptr: the zero iterate of a cycle's first sweep).  zin and zout
+// are different vectors (ping-pong), which gives exactly the in-place
+// reference sweep.
+void gs_sweep(const GsSweep& S, bool backward, VecRef r, const double* zin, VecRef zout,
+              cudaStream_t st);
 // z = wd .* r (first Jacobi sweep from a zero iterate, amg.cpp:119-124).
 void wd_times_r(int n, const double* wd, VecRef r, double* z, cudaStream_t st);
 

@@ -508,7 +508,11 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
             }
             d.t = alloc(d.n);
             d.u = alloc(d.n);
-            if (h.params.pre_sweeps > 1) d.zp = alloc(d.n);
+            if (h.params.pre_sweeps > 1 || h.params.smoother != 0) d.zp = alloc(d.n);
+            if (h.params.smoother != 0 && l + 1 < L) {
+                d.gsf = upload_gs(lev.A, lev.inv_diag, false);
+                d.gsb = upload_gs(lev.A, lev.inv_diag, true);
+            }
             if (l > 0) {
                 d.r = alloc(d.n);
                 d.z = alloc(d.n);
@@ -580,7 +584,7 @@ int DeviceSolver::matrix_format(int which) const { return which == 0 ? M_.fmt : 
 void DeviceSolver::build_bottom(DevHier& dh, const Hierarchy& h) {
     const int L = h.n_levels();
     if (dev::option("IRK_BOTTOM", 1) == 0 || L < 3) return;
-    if (h.params.pre_sweeps != 1 || h.params.post_sweeps != 1) return;
+    if (h.params.pre_sweeps != 1 || h.params.post_sweeps != 1 || h.params.smoother != 0) return;
     const int budget = 225 * 1024;
     bool force_csr = false;
     for (int b = 1; b <= L - 2; ++b) {
@@ -702,8 +706,122 @@ namespace {
 bool zr_on() { return dev::option("IRK_ZR", 1) != 0; }
 }  // namespace
 
+// Gauss-Seidel schedule of one level (amg.cpp:125-140): depth(i) = 1 + max
+// depth(j) over the entries a_ij the sweep reads updated (j < i forward, j > i
+// backward); positions sorted by depth (stable in i), entries in column order
+// without the diagonal.
+dev::GsSweep DeviceSolver::upload_gs(const Csr& A, const std::vector<double>& inv_diag,
+                                     bool backward) {
+    const int n = A.rows;
+    std::vector<int> depth(n, 0);
+    int nlev = 0;
+    for (int t = 0; t < n; ++t) {
+        const int i = backward ? n - 1 - t : t;
+        int d = 0;
+        for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+            const int c = A.idx[k];
+            if (backward ? c > i : c < i) d = std::max(d, depth[c] + 1);
+        }
+        depth[i] = d;
+        nlev = std::max(nlev, d + 1);
+    }
+    std::vector<int> lptr(nlev + 2, 0);
+    for (int i = 0; i < n; ++i) ++lptr[depth[i] + 1];
+    for (int l = 0; l < nlev; ++l) lptr[l + 1] += lptr[l];
+    lptr[nlev + 1] = lptr[nlev];
+    std::vector<int> pos(lptr.begin(), lptr.end() - 1), order(n);
+    for (int i = 0; i < n; ++i) order[pos[depth[i]]++] = i;
+    std::vector<int4> hdr(n);
+    std::vector<int> ci;
+    std::vector<double> val, dinv(n);
+    ci.reserve(A.idx.size());
+    val.reserve(A.val.size());
+    for (int q = 0; q < n; ++q) {
+        const int i = order[q];
+        const int start = static_cast<int>(ci.size());
+        for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k)
+            if (A.idx[k] != i) {
+                ci.push_back(A.idx[k]);
+                val.push_back(A.val[k]);
+            }
+        hdr[q] = make_int4(i, start, static_cast<int>(ci.size()) - start, 0);
+        dinv[q] = inv_diag[i];
+    }
+    if (ci.empty()) {  // a diagonal level: keep the entry arrays non-null
+        ci.push_back(0);
+        val.push_back(0.0);
+    }
+    dev::GsSweep g;
+    g.hdr = upload_array(hdr);
+    g.ci = upload_array(ci);
+    g.val = upload_array(val);
+    g.dinv = upload_array(dinv);
+    g.lptr = upload_array(lptr);
+    g.nlev = nlev;
+    g.n = n;
+    g.nnz = static_cast<long long>(ci.size());
+    return g;
+}
+
+// V(pre, post) cycle with the Gauss-Seidel smoother, the reference's own
+// order (amg.cpp:144-168): pre forward sweeps from z = 0, t = r - A z,
+// r_c = R t, the coarse cycle, z + P z_c, post backward sweeps.  Sweeps
+// ping-pong between two level vectors (see gs_sweep); the tail operator and
+// the dense coarsest inverse are shared with the Jacobi cycle.
+void DeviceSolver::record_vcycle_gs(int k, VecRef r0, VecRef z0, int first) {
+    DevHier& H = hier_[k];
+    const int L = static_cast<int>(H.lv.size());
+    const int pre = H.prm.pre_sweeps, post = H.prm.post_sweeps;
+    auto rhs_of = [&](int l) { return l == first ? r0 : dev::plain(H.lv[l].r); };
+    auto out_of = [&](int l) { return l == first ? z0 : dev::plain(H.lv[l].z); };
+    const int tail = dev::option("IRK_TAIL", 1) != 0 && H.tail_from > first ? H.tail_from : -1;
+    const int down_end = tail > 0 ? tail : L - 1;
+    for (int l = first; l < down_end; ++l) {
+        DevLevel& d = H.lv[l];
+        // pre sweeps, the last one into zp
+        const double* in = nullptr;
+        for (int sw = 0; sw < pre; ++sw) {
+            double* out = (pre - 1 - sw) % 2 == 0 ? d.zp : d.u;
+            dev::gs_sweep(d.gsf, false, rhs_of(l), in, dev::plain(out), st_);
+            in = out;
+        }
+        dev::SpmvArgs a;
+        a.x = dev::plain(d.zp);
+        a.r = rhs_of(l);
+        a.y = dev::plain(d.t);
+        dev::spmv(d.A, dev::kXPlain, dev::kEResid, a, st_);
+        dev::SpmvArgs ra;
+        ra.x = dev::plain(d.t);
+        ra.y = dev::plain(H.lv[l + 1].r);
+        dev::spmv(d.R, dev::kXPlain, dev::kEPlain, ra, st_);
+    }
+    if (tail > 0)
+        dev::tail_mv(H.lv[tail].n, H.tail_ld, H.tail, H.lv[tail].r, H.lv[tail].z, st_);
+    else
+        dev::dense_mv(H.nc, H.cinv, rhs_of(L - 1), out_of(L - 1), st_);
+    for (int l = down_end - 1; l >= first; --l) {
+        DevLevel& d = H.lv[l];
+        dev::SpmvArgs pa;
+        pa.x = dev::plain(H.lv[l + 1].z);
+        pa.zb = d.zp;
+        pa.y = dev::plain(d.t);
+        dev::spmv(d.P, dev::kXPlain, dev::kEProlong, pa, st_);
+        double* cur = d.t;
+        for (int sw = 0; sw < post; ++sw) {
+            double* nxt = cur == d.t ? d.u : d.t;
+            const VecRef out = sw == post - 1 ? out_of(l) : dev::plain(nxt);
+            dev::gs_sweep(d.gsb, true, rhs_of(l), cur, out, st_);
+            cur = nxt;
+        }
+    }
+}
+
 void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
     DevHier& H = hier_[k];
+    if (H.prm.smoother != 0) {
+        record_vcycle_gs(k, r0, z0, first);
+        return;
+    }
     const int L = static_cast<int>(H.lv.size());
     const int pre = H.prm.pre_sweeps, post = H.prm.post_sweeps;
     // `first` > 0 runs only the part of the cycle below level `first` (timing)

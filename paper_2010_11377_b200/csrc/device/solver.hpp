@@ -60,6 +60,7 @@ struct DevLevel {
     double* u = nullptr;          // post-sweep ping-pong
     double* zp = nullptr;         // pre-smoothed iterate (pre > 1 only)
     double* zr = nullptr;         // wd .* r, written by the restriction (levels >= 1)
+    dev::GsSweep gsf, gsb;        // Gauss-Seidel schedules (forward / backward sweeps)
 };
 
 struct DevHier {
@@ -153,6 +154,8 @@ private:
     double* alloc(size_t count);
     void* raw_alloc(size_t bytes);
     void record_vcycle(int k, dev::VecRef r, dev::VecRef z, int first = 0);
+    void record_vcycle_gs(int k, dev::VecRef r, dev::VecRef z, int first);
+    dev::GsSweep upload_gs(const Csr& A, const std::vector<double>& inv_diag, bool backward);
     void record_precond(dev::VecRef v, dev::VecRef w);
     void record_stage_op(dev::VecRef z, dev::VecRef y);
     void record_iteration();

@@ -339,7 +339,8 @@ class or_hier(C.Structure):
     _fields_ = [("nlev", C.c_int), ("A", C.POINTER(or_csr)), ("P", C.POINTER(or_csr)),
                 ("R", C.POINTER(or_csr)), ("inv_diag", C.POINTER(dptr)), ("cinv", dptr),
                 ("nc", C.c_int), ("omega", C.c_double), ("pre", C.c_int), ("post", C.c_int),
-                ("tail_from", C.c_int), ("tail_ld", C.c_int), ("tail", dptr)]
+                ("tail_from", C.c_int), ("tail_ld", C.c_int), ("tail", dptr),
+                ("smoother", C.c_int)]
 
 
 class or_sys(C.Structure):
@@ -416,7 +417,8 @@ class OracleSystem:
             self._keep.append(tl)
             hs.append(or_hier(L, Aarr, Parr, Rarr, idp, _d(cinv), int(round(np.sqrt(cinv.size))),
                               h["omega"], h["pre"], h["post"], tail_from,
-                              0 if tl is None else tl.shape[1], None if tl is None else _d(tl)))
+                              0 if tl is None else tl.shape[1], None if tl is None else _d(tl),
+                              int(h.get("smoother", 0))))
         harr = (or_hier * len(hs))(*hs)
         arrs = [np.ascontiguousarray(x, np.float64).ravel() for x in (A, b, At)]
         sobv = np.ascontiguousarray(sob, np.int32)
@@ -474,10 +476,11 @@ def oracle_dot(x, y):
     return Oracle.lib().or_dot(_d(x), _d(y), len(x))
 
 
-def hierarchy_dict(h, omega=2.0 / 3.0, pre=1, post=1):
+def hierarchy_dict(h, omega=2.0 / 3.0, pre=1, post=1, smoother=0):
     """Product AmgHierarchy -> oracle hierarchy dict."""
     L = h.n_levels()
-    d = {"A": [], "P": [], "R": [], "inv_diag": [], "omega": omega, "pre": pre, "post": post}
+    d = {"A": [], "P": [], "R": [], "inv_diag": [], "omega": omega, "pre": pre, "post": post,
+         "smoother": smoother}
     for l in range(L):
         a = h.level(l, "A")
         d["A"].append((a.row_ptr, a.col_idx, a.vals, a.n_cols))

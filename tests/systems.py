@@ -36,7 +36,8 @@ class Case:
         self.oracle = OracleSystem(
             (M.row_ptr, M.col_idx, M.vals), (K.row_ptr, K.col_idx, K.vals), table.A, table.b, ht,
             coeff.Atilde, int(coeff.structure),
-            [hierarchy_dict(h, self.amg.jacobi_weight, self.amg.pre_sweeps, self.amg.post_sweeps)
+            [hierarchy_dict(h, self.amg.jacobi_weight, self.amg.pre_sweeps, self.amg.post_sweeps,
+                            self.amg.smoother)
              for h in self.hiers], self.sob)
         self._P = None
 
@@ -64,10 +65,10 @@ def heat_case(cells=64, scheme=P.Scheme.RadauIIA, s=2, kind=P.CoeffKind.LowerFac
     return c
 
 
-def dg_case(cells=64, eps=0.005, s=2, kind=P.CoeffKind.LowerFactor, ht=0.01):
+def dg_case(cells=64, eps=0.005, s=2, kind=P.CoeffKind.LowerFactor, ht=0.01, amg=None):
     prob = P.make_double_glazing_setup(cells, eps)
     table = P.make_radau_iia(s)
-    c = Case(prob.M, prob.F, table, P.precond_coeff(table, kind), ht, None, prob.f_lift)
+    c = Case(prob.M, prob.F, table, P.precond_coeff(table, kind), ht, amg, prob.f_lift)
     c.problem = prob
     return c
 
@@ -115,3 +116,9 @@ def seeded_triangular(s, seed, upper=False):
             u = rng.uniform(0.3, 1.2)
             At[i, j] = u if i == j else 0.4 * u
     return At
+
+
+def study_amg():
+    """The reference study driver's subsolve cycle (study.hpp:44-47):
+    Gauss-Seidel V(4,4) with two prolongator smoothing steps."""
+    return P.AmgParams(pre_sweeps=4, post_sweeps=4, smoother=1, prolongation_steps=2)

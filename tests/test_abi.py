@@ -74,9 +74,19 @@ def test_tuning_switches_are_settable_without_gpu():
         _abi.check(_abi.lib().irk_set_option(None, 1))
 
 
-def test_gauss_seidel_smoother_is_rejected_not_emulated():
+def test_gauss_seidel_setup_and_no_cpu_fallback():
+    """The Gauss-Seidel smoother (amg.cpp:125-140) runs on the device only:
+    host setup accepts it, an unknown smoother is an invalid argument, and
+    without a GPU the device solver fails loudly (no CPU emulation)."""
+    from conftest import has_gpu
     pr = P.make_heat_setup(8)
     t = P.make_radau_iia(2)
-    with pytest.raises((P.Unsupported, P.CudaError)):
-        P.BlockPreconditioner(pr.M, pr.F, P.precond_coeff(t, P.CoeffKind.LowerFactor), 0.01,
-                              P.AmgParams(smoother=1), table=t)
+    B = P.CsrMatrix(pr.M.row_ptr, pr.M.col_idx, pr.M.vals + 0.01 * pr.F.vals, pr.M.n_cols)
+    h = P.amg_setup(B, P.AmgParams(smoother=1, pre_sweeps=4, post_sweeps=4, prolongation_steps=2))
+    assert h.n_levels() >= 1
+    with pytest.raises(ValueError):
+        P.amg_setup(B, P.AmgParams(smoother=2))
+    if not has_gpu():
+        with pytest.raises(P.CudaError):
+            P.BlockPreconditioner(pr.M, pr.F, P.precond_coeff(t, P.CoeffKind.LowerFactor), 0.01,
+                                  P.AmgParams(smoother=1), table=t)

@@ -136,3 +136,39 @@ def test_custom_coeff_step_matches_reference(s, upper):
     assert abs(o["iterations"] - rr["iterations"]) <= 1
     assert rel_l2(o["K"], rr["K"]) <= 1e-9
     assert rel_l2(o["u_next"], rr["u_next"]) <= 1e-9
+
+
+@pytest.mark.parametrize("problem", ["heat", "dg"])
+def test_gauss_seidel_study_cycle_matches_reference(problem):
+    """The reference study driver's subsolve (study.hpp:44-47: Gauss-Seidel
+    V(4,4), two prolongator smoothing steps) -- V-cycle, preconditioner and
+    IRK step against the reference's own smooth_sweep (amg.cpp:125-140)."""
+    from systems import study_amg
+    amg = study_amg()
+    c = (heat_case(64, s=2, ht=0.01, amg=amg) if problem == "heat" else dg_case(64, s=2, amg=amg))
+    M, K = c.M, c.K
+    B = (M.row_ptr, M.col_idx, 1.0 * M.vals + (c.ht * c.coeff.Atilde[0, 0]) * K.vals)
+    ref = Ref.amg_ex(B, amg)
+    r = np.random.default_rng(1).uniform(-1, 1, c.n)
+    assert rel_l2(c.oracle.vcycle(0, r), ref.vcycle(r)) <= 1e-12
+    rs = RefSolver((M.row_ptr, M.col_idx, M.vals), (K.row_ptr, K.col_idx, K.vals), 0, 2, 3, c.ht,
+                   amg=amg)
+    v = np.random.default_rng(2).uniform(-1, 1, 2 * c.n)
+    assert rel_l2(c.oracle.precond_apply(v), rs.precond_apply(v)) <= 1e-12
+    u = c.problem.initial() if problem == "heat" else np.zeros(c.n)
+    o, rr = c.oracle.step(u, c.f_lift), rs.step(u, c.f_lift)
+    assert abs(o["iterations"] - rr["iterations"]) <= 1
+    assert rel_l2(o["K"], rr["K"]) <= 1e-9 and rel_l2(o["u_next"], rr["u_next"]) <= 1e-9
+
+
+def test_gauss_seidel_without_tail_matches_reference(monkeypatch):
+    """The whole cycle recursive (no dense tail): every level's sweeps."""
+    from systems import study_amg
+    monkeypatch.setenv("IRK_TAIL_MAX", "0")
+    amg = P.AmgParams(pre_sweeps=2, post_sweeps=3, smoother=1)
+    c = heat_case(128, s=2, ht=0.01, amg=amg)
+    assert c.hiers[0].tail()[1] is None and c.hiers[0].n_levels() >= 3
+    M, K = c.M, c.K
+    B = (M.row_ptr, M.col_idx, 1.0 * M.vals + (c.ht * c.coeff.Atilde[0, 0]) * K.vals)
+    r = np.random.default_rng(4).uniform(-1, 1, c.n)
+    assert rel_l2(c.oracle.vcycle(0, r), Ref.amg_ex(B, amg).vcycle(r)) <= 1e-12
