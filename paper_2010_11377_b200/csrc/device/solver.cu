@@ -1369,8 +1369,9 @@ int DeviceSolver::prepare(const GmresConfig& cfg, bool lift, bool forcing) {
     if (restart < 1) restart = 1;
     ensure_gmres(restart, std::max(max_iter, 1));
     if (forcing && !forcing_) forcing_ = alloc(static_cast<size_t>(s_) * n_);
-    static const bool no_cond = std::getenv("IRK_NO_COND_GRAPH") != nullptr;
-    const bool want_cond = !no_cond;
+    // IRK_NO_COND_GRAPH=1 (environment or irk_set_option): host-driven loop
+    // over plain graphs, whose kernels profilers can see
+    const bool want_cond = dev::option("IRK_NO_COND_GRAPH", 0) == 0;
     if (g_restart_ != restart || g_iter_ != max_iter || g_rtol_ != cfg.rel_tol ||
         g_lift_ != lift || g_forcing_ != forcing || g_side_ != side_ ||
         (graph_mode_ == 1) != want_cond || g_opt_gen_ != dev::option_generation()) {
