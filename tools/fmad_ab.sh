@@ -19,3 +19,4 @@ for tag in ("false", "true"):
     ms = [float(np.load(f"gpurun_out/fmad_{tag}_{r}.npz")[f"ms{k}"]) for r in (1, 2, 3) for k in range(4)]
     print(f"fmad={tag}: median ms/step {np.median(ms):.3f} over {len(ms)} steps")
 PY
+rm -f gpurun_out/fmad_*.npz  # keep gpurun_out small enough to travel back
