@@ -2009,76 +2009,224 @@ void dot(const double* x, const double* y, long long n, double* partials, unsign
 }
 
 // ------------------------------------------------------------------ Gauss-Seidel
-// One sweep in ONE CTA: the depth levels of the schedule run one after the
-// other separated by a barrier, one thread per row.  A sweep is a chain of
-// nlev dependent steps (C2: ~2000 at level 0, ~3100 at level 1 with two
-// prolongator smoothing steps) and is latency-bound by construction -- the
-// reference's own sweep is sequential (amg.cpp:125-140) -- so the kernel
-// keeps the per-step path short: the next level's headers are loaded while
-// the current level computes, a row's entries and operands are issued 8 at a
-// time, and the updated values are plain coherent loads of zout (the
-// barrier orders them within the CTA).
+// One sweep = a parallel gather + ONE CTA stepping through the schedule's
+// chunks, separated by a barrier, one thread per row.  A sweep is a chain of
+// dependent steps (C2 with the study cycle: ~2000 at level 0, ~3100 at level
+// 1) and latency-bound by construction -- the reference's own sweep is
+// sequential (amg.cpp:125-140) -- so a step is kept to shared-memory reads:
+// the gather kernel has already written r and every not-yet-updated operand
+// product in schedule order, so staging chunk C+1 is a set of contiguous,
+// independent loads issued before chunk C computes and stored to the other
+// buffer after it (chunk C+4 is bulk-prefetched into L2); updated operands
+// come from a ring of the last kGsRing computed values.  What bounds a step
+// now is the one SM's load/store issue rate (profiles/r2/gs_sweep.txt).
 namespace {
-constexpr int kGsThreads = 512;
+constexpr int kGsThreads = 1024;
+struct GsBuf {
+    int2 hdr[kGsRows];
+    double dinv[kGsRows];
+    double r[kGsRows];
+    double e[kGsEnt];
+    int ref[kGsEnt];
+};
+constexpr size_t kGsSmem = sizeof(double) * (kGsRing + 2) + 2 * sizeof(GsBuf);
 
-template <bool kBack>
-__device__ __forceinline__ void gs_row(const GsSweep& S, int4 h, int q, const double* __restrict__ r,
-                                       const double* __restrict__ zin, double* zout) {
-    const int i = h.x, st = h.y, len = h.z;
-    double s = __ldg(r + i);
-    for (int k = 0; k < len; k += 8) {
-        int c[8];
-        double a[8], zv[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const bool ok = k + u < len;
-            c[u] = ok ? __ldg(S.ci + st + k + u) : i;
-            a[u] = ok ? __ldg(S.val + st + k + u) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const bool upd = kBack ? c[u] > i : c[u] < i;
-            zv[u] = upd ? zout[c[u]] : (zin ? __ldg(zin + c[u]) : 0.0);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-            if (k + u < len) s = s - a[u] * zv[u];
+__global__ void __launch_bounds__(256) k_gs_gather(GsSweep S, VecRef rr, const double* zin) {
+    pdl_trigger();
+    pdl_wait();
+    const double* __restrict__ r = rr.get();
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    const long long t0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (long long q = t0; q < S.n; q += stride) S.rs[q] = __ldg(r + __ldg(&S.hdr[q].x));
+    for (long long e = t0; e < S.nnz; e += stride) {
+        const int rf = __ldg(S.ref + e);
+        const double v = __ldg(S.val + e);
+        S.ps[e] = rf < 0 ? v * (zin ? __ldg(zin + (-rf - 1) / 2) : 0.0) : v;
     }
-    zout[i] = s * __ldg(S.dinv + q);
 }
 
-template <bool kBack>
-__global__ void __launch_bounds__(kGsThreads) k_gs_sweep(GsSweep S, VecRef rr, const double* zin,
-                                                         VecRef zr) {
+// Chunk bounds {first position, first entry}: read from global memory one
+// iteration before use (the shared-memory carveout leaves little L1, so
+// every load is an L2 round trip that must not sit on the chunk chain).
+struct GsBounds {
+    int q, e;
+};
+__device__ __forceinline__ GsBounds gs_bounds(const GsSweep& S, int C) {
+    const int c = min(C, S.nch);
+    return {__ldg(S.cptr + c), __ldg(S.ceptr + c)};
+}
+
+// chunk [b0, b1): contiguous loads into registers (issued before the
+// current chunk computes), written to the staging buffer after it
+constexpr int kGsRowPer = kGsRows / kGsThreads;
+constexpr int kGsEntPer = kGsEnt / kGsThreads;
+struct GsRegs {
+    int2 h[kGsRowPer];
+    double dinv[kGsRowPer], r[kGsRowPer];
+    double e[kGsEntPer];
+    int ref[kGsEntPer];
+};
+__device__ __forceinline__ void gs_load(const GsSweep& S, GsBounds b0, GsBounds b1, GsRegs& g) {
+    const int nr = b1.q - b0.q, ne = b1.e - b0.e;
+#pragma unroll
+    for (int u = 0; u < kGsRowPer; ++u) {
+        const int q = threadIdx.x + u * kGsThreads;
+        if (q < nr) {
+            g.h[u] = __ldg(S.hdr + b0.q + q);
+            g.dinv[u] = __ldg(S.dinv + b0.q + q);
+            g.r[u] = __ldcg(S.rs + b0.q + q);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kGsEntPer; ++u) {
+        const int e = threadIdx.x + u * kGsThreads;
+        if (e < ne) {
+            g.e[u] = __ldcg(S.ps + b0.e + e);
+            g.ref[u] = __ldg(S.sref + b0.e + e);
+        }
+    }
+}
+__device__ __forceinline__ void gs_store(GsBounds b0, GsBounds b1, const GsRegs& g, GsBuf& b) {
+    const int nr = b1.q - b0.q, ne = b1.e - b0.e;
+#pragma unroll
+    for (int u = 0; u < kGsRowPer; ++u) {
+        const int q = threadIdx.x + u * kGsThreads;
+        if (q < nr) {
+            b.hdr[q] = g.h[u];
+            b.dinv[q] = g.dinv[u];
+            b.r[q] = g.r[u];
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kGsEntPer; ++u) {
+        const int e = threadIdx.x + u * kGsThreads;
+        if (e < ne) {
+            b.e[e] = g.e[u];
+            b.ref[e] = g.ref[u];
+        }
+    }
+}
+
+// a later chunk [p0, p1) into L2: one asynchronous bulk prefetch per array
+// (cp.async.bulk.prefetch.L2, no completion to wait for -- the per-line
+// prefetch.global.L2 of a thread stalls it for an L2 round trip each)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* lo, const void* hi) {
+    const unsigned long long a = reinterpret_cast<unsigned long long>(lo) & ~15ull;
+    const unsigned long long b = reinterpret_cast<unsigned long long>(hi) & ~15ull;
+    if (b > a)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(static_cast<unsigned>(b - a))
+                     : "memory");
+}
+__device__ __forceinline__ void gs_prefetch(const GsSweep& S, GsBounds p0, GsBounds p1) {
+    switch (threadIdx.x) {
+    case 0: bulk_prefetch_l2(S.sref + p0.e, S.sref + p1.e); break;
+    case 32: bulk_prefetch_l2(S.ps + p0.e, S.ps + p1.e); break;
+    case 64: bulk_prefetch_l2(S.hdr + p0.q, S.hdr + p1.q); break;
+    case 96: bulk_prefetch_l2(S.dinv + p0.q, S.dinv + p1.q); break;
+    case 128: bulk_prefetch_l2(S.rs + p0.q, S.rs + p1.q); break;
+    default: break;
+    }
+}
+
+// kFar: some updated operands are older than the ring (read from zout);
+// otherwise every entry is x * ring[ref] -- a not-yet-updated operand's
+// gathered product times the ring's constant 1.0 slot (exact) -- and a row's
+// 8-entry blocks load, multiply and then subtract in column order.
+constexpr int kGsPf = 4;  // L2 prefetch distance (chunks)
+template <bool kFar>
+__global__ void __launch_bounds__(kGsThreads, 1) k_gs_sweep(GsSweep S, VecRef zr) {
     pdl_trigger();
-    const int tid = threadIdx.x;
-    int q = S.lptr[0] + tid, le = S.lptr[1];
-    int4 h = q < le ? __ldg(S.hdr + q) : make_int4(-1, 0, 0, 0);
+    extern __shared__ __align__(16) unsigned char gs_smem[];
+    double* ring = reinterpret_cast<double*>(gs_smem);
+    GsBuf* buf = reinterpret_cast<GsBuf*>(gs_smem + sizeof(double) * (kGsRing + 2));
+    // chunk bounds travel through shared memory: thread 0 loads the bounds
+    // of chunk C + kGsPf + 2 while chunk C computes and publishes them with
+    // the barrier (a uniform-register copy of a loaded value would stall
+    // every warp on the load right where it is issued)
+    __shared__ GsBounds sbd[8];
+    if (threadIdx.x == 0) {
+        ring[kGsRing] = 1.0;
+        for (int k = 0; k < kGsPf + 2; ++k) sbd[k] = gs_bounds(S, k);
+    }
     pdl_wait();
-    const double* r = rr.get();
+    __syncthreads();
     double* zout = zr.get();
-    for (int L = 0; L < S.nlev; ++L) {
-        const int qn = S.lptr[L + 1] + tid, ne = S.lptr[L + 2];
-        const int4 hn = qn < ne ? __ldg(S.hdr + qn) : make_int4(-1, 0, 0, 0);
-        if (h.x >= 0) gs_row<kBack>(S, h, q, r, zin, zout);
-        for (int q2 = q + kGsThreads; q2 < le; q2 += kGsThreads)
-            gs_row<kBack>(S, __ldg(S.hdr + q2), q2, r, zin, zout);
+    {
+        GsRegs g;
+        gs_load(S, sbd[0], sbd[1], g);
+        gs_store(sbd[0], sbd[1], g, buf[0]);
+    }
+    __syncthreads();
+    long long* prof = S.prof && threadIdx.x == 0 ? S.prof : nullptr;
+    const int pstride = S.nch / 64 > 1 ? S.nch / 64 : 1;
+    for (int C = 0; C < S.nch; ++C) {
+        long long t0 = 0;
+        const bool pr = prof && C % pstride == 0 && C / pstride < 64;
+        long long* pp = pr ? prof + 5 * (C / pstride) : nullptr;
+        if (pr) t0 = clock64();
+        GsBounds bd[kGsPf + 2];
+#pragma unroll
+        for (int k = 0; k < kGsPf + 2; ++k) bd[k] = sbd[(C + k) & 7];
+        GsBounds nxt{0, 0};
+        if (threadIdx.x == 0) nxt = gs_bounds(S, C + kGsPf + 2);
+        GsRegs g;
+        if (C + 1 < S.nch) gs_load(S, bd[1], bd[2], g);
+        if (C + kGsPf < S.nch) gs_prefetch(S, bd[kGsPf], bd[kGsPf + 1]);
+        if (pr) pp[0] = clock64() - t0;
+        const GsBuf& b = buf[C & 1];
+        const int rb = bd[0].q, nr = bd[1].q - bd[0].q, eb = bd[0].e, ne = bd[1].e - bd[0].e;
+        for (int q = threadIdx.x; q < nr; q += kGsThreads) {
+            const int2 h = b.hdr[q];
+            const int e0 = h.y - eb;
+            const int e1 = q + 1 < nr ? b.hdr[q + 1].y - eb : ne;
+            double s = b.r[q];
+            for (int e = e0; e < e1; e += 8) {
+                double p[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int k = min(e + u, e1 - 1);
+                    const int rf = b.ref[k];
+                    const double x = b.e[k];
+                    if (kFar)
+                        p[u] = rf >= 0 ? x * ring[rf] : x * zout[-rf - 2];
+                    else
+                        p[u] = x * ring[rf];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (e + u < e1) s = s - p[u];
+            }
+            const double z = s * b.dinv[q];
+            ring[(rb + q) & (kGsRing - 1)] = z;
+            zout[h.x] = z;
+        }
+        if (pr) pp[1] = clock64() - t0;
+        if (C + 1 < S.nch) gs_store(bd[1], bd[2], g, buf[(C + 1) & 1]);
+        if (threadIdx.x == 0) sbd[(C + kGsPf + 2) & 7] = nxt;
+        if (pr) pp[2] = clock64() - t0;
         __syncthreads();
-        h = hn;
-        q = qn;
-        le = ne;
+        if (pr) {
+            pp[3] = clock64() - t0;
+            pp[4] = bd[1].q - bd[0].q;
+        }
     }
 }
 }  // namespace
 
 void gs_sweep(const GsSweep& S, bool backward, VecRef r, const double* zin, VecRef zout,
               cudaStream_t st) {
-    // headers, entries, dinv, r, zout written, and one operand per entry
-    tally(16.0 * S.n + 12.0 * S.nnz + 8.0 * S.n + 8.0 * S.n + 8.0 * S.n + 8.0 * S.nnz);
-    if (backward)
-        launch(k_gs_sweep<true>, 1, kGsThreads, 0, st, S, r, zin, zout);
+    (void)backward;  // the direction is in the schedule
+    // gather: hdr, r (gathered), rs written; per entry code, value, operand
+    // (old entries) and ps written.  sweep: hdr, dinv, rs, ps, sref once; zout.
+    tally(8.0 * S.n + 8.0 * S.n + 8.0 * S.n + 28.0 * S.nnz);
+    tally(24.0 * S.n + 12.0 * S.nnz + 8.0 * S.n);
+    const long long work = std::max<long long>(S.nnz, S.n);
+    const int blocks = static_cast<int>(std::min<long long>((work + 255) / 256, 148LL * 8));
+    launch(k_gs_gather, std::max(blocks, 1), 256, 0, st, S, r, zin);
+    if (S.far)
+        launch(k_gs_sweep<true>, 1, kGsThreads, kGsSmem, st, S, zout);
     else
-        launch(k_gs_sweep<false>, 1, kGsThreads, 0, st, S, r, zin, zout);
+        launch(k_gs_sweep<false>, 1, kGsThreads, kGsSmem, st, S, zout);
 }
 
 void set_smem_limits() {
@@ -2088,6 +2236,8 @@ void set_smem_limits() {
     cudaFuncSetAttribute(k_dgs_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_dgs_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_dense_mv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_gs_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGsSmem));
+    cudaFuncSetAttribute(k_gs_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGsSmem));
     const int nv = kMaxRestart + 2;
     cudaFuncSetAttribute(k_gm_blockdot, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(red_smem(nv)));

@@ -177,24 +177,41 @@ struct BotDesc {
 void bottom_cycle(const BotDesc& d, const double* r_in, double* z_out, cudaStream_t st);
 // Gauss-Seidel sweep (amg.cpp:125-140) of one level, level-scheduled: the
 // rows are grouped by dependency depth (row i after every row j it reads
-// updated, j < i forward / j > i backward) and stored in that order --
-// per position q a header {i, start, len} into the off-diagonal entries
-// (column order, the diagonal dropped: the reference skips it) and
-// dinv[q] = 1 / a_ii.  Rows of one depth are independent.
+// updated: j < i forward, j > i backward) and stored in that order, the
+// depths cut into chunks of <= kGsRows rows and <= kGsEnt off-diagonal
+// entries (rows of one chunk are independent).  Per schedule position q:
+// hdr[q] = {i, first entry}, dinv[q] = 1 / a_ii; per entry (column order,
+// the diagonal dropped as the reference skips it) its value and two static
+// codes:
+//   ref  (the gather)  -(2c+1): the not-yet-updated value of column c, else 0
+//   sref (the sweep)   0 .. kGsRing-1: an updated value still in the
+//                      kernel's ring of the last kGsRing computed rows (slot
+//                      = position mod kGsRing); kGsRing: the gathered product
+//                      (the ring's constant 1.0 slot); -(c+2): an updated
+//                      value too old for the ring (zout[c]; `far` sweeps).
+constexpr int kGsRows = 1024, kGsEnt = 6144, kGsRing = 4096;
 struct GsSweep {
-    const int4* hdr = nullptr;   // n headers in schedule order
-    const int* ci = nullptr;     // off-diagonal columns, schedule order
-    const double* val = nullptr; // off-diagonal values
+    const int2* hdr = nullptr;   // n, schedule order
+    const int* ref = nullptr;    // nnz gather codes
+    const int* sref = nullptr;   // nnz sweep codes
+    const double* val = nullptr; // nnz values
     const double* dinv = nullptr;
-    const int* lptr = nullptr;   // nlev + 2 (last repeated)
-    int nlev = 0, n = 0;
-    long long nnz = 0;           // off-diagonal entries
+    const int* cptr = nullptr;   // nch + 1 chunk position offsets
+    const int* ceptr = nullptr;  // nch + 1 chunk entry offsets
+    double* rs = nullptr;        // n: r in schedule order (written by the gather)
+    double* ps = nullptr;        // nnz: the gathered entry operands
+    int nch = 0, n = 0;
+    int far = 0;                 // some operands older than the ring
+    long long nnz = 0;
+    long long* prof = nullptr;   // diagnostic: per-chunk phase clocks (time_kernel, IRK_GS_PROF)
 };
 // zout_i = (r_i - sum_{j != i} a_ij z_j) / a_ii in CSR column order, with z_j
-// the updated value (zout) for j before i in sweep order and zin_j otherwise
+// the updated value for j before i in sweep order and zin_j otherwise
 // (zin == nullptr: the zero iterate of a cycle's first sweep).  zin and zout
 // are different vectors (ping-pong), which gives exactly the in-place
-// reference sweep.
+// reference sweep.  Two launches: a parallel gather (r in schedule order;
+// each not-yet-updated operand multiplied by its value -- the same rounded
+// product the row sum subtracts) and the single-CTA sweep.
 void gs_sweep(const GsSweep& S, bool backward, VecRef r, const double* zin, VecRef zout,
               cudaStream_t st);
 // z = wd .* r (first Jacobi sweep from a zero iterate, amg.cpp:119-124).

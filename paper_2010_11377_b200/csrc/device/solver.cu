@@ -512,6 +512,9 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
             if (h.params.smoother != 0 && l + 1 < L) {
                 d.gsf = upload_gs(lev.A, lev.inv_diag, false);
                 d.gsb = upload_gs(lev.A, lev.inv_diag, true);
+                // gather scratch, shared by the level's (sequential) sweeps
+                d.gsf.rs = d.gsb.rs = alloc(d.n);
+                d.gsf.ps = d.gsb.ps = alloc(std::max<long long>(d.gsf.nnz, 1));
             }
             if (l > 0) {
                 d.r = alloc(d.n);
@@ -708,8 +711,9 @@ bool zr_on() { return dev::option("IRK_ZR", 1) != 0; }
 
 // Gauss-Seidel schedule of one level (amg.cpp:125-140): depth(i) = 1 + max
 // depth(j) over the entries a_ij the sweep reads updated (j < i forward, j > i
-// backward); positions sorted by depth (stable in i), entries in column order
-// without the diagonal.
+// backward); positions sorted by depth (stable in i) and cut into chunks of
+// <= kGsRows rows / kGsEnt entries; entries in column order without the
+// diagonal, each with its source code (dev::GsSweep).
 dev::GsSweep DeviceSolver::upload_gs(const Csr& A, const std::vector<double>& inv_diag,
                                      bool backward) {
     const int n = A.rows;
@@ -725,41 +729,94 @@ dev::GsSweep DeviceSolver::upload_gs(const Csr& A, const std::vector<double>& in
         depth[i] = d;
         nlev = std::max(nlev, d + 1);
     }
-    std::vector<int> lptr(nlev + 2, 0);
+    std::vector<int> lptr(nlev + 1, 0);
     for (int i = 0; i < n; ++i) ++lptr[depth[i] + 1];
     for (int l = 0; l < nlev; ++l) lptr[l + 1] += lptr[l];
-    lptr[nlev + 1] = lptr[nlev];
-    std::vector<int> pos(lptr.begin(), lptr.end() - 1), order(n);
-    for (int i = 0; i < n; ++i) order[pos[depth[i]]++] = i;
-    std::vector<int4> hdr(n);
-    std::vector<int> ci;
+    std::vector<int> order(n), pos(n);
+    {
+        std::vector<int> fill(lptr.begin(), lptr.end() - 1);
+        for (int i = 0; i < n; ++i) order[fill[depth[i]]++] = i;
+    }
+    for (int q = 0; q < n; ++q) pos[order[q]] = q;
+    auto offdiag = [&](int i) {
+        int c = 0;
+        for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) c += A.idx[k] != i;
+        return c;
+    };
+    // chunks: each depth cut into pieces within the staging buffers
+    std::vector<int> cptr{0}, ceptr{0};
+    std::vector<int> chunk_end(n);
+    {
+        int e = 0;
+        for (int l = 0; l < nlev; ++l) {
+            int rows = 0, ents = 0;
+            for (int q = lptr[l]; q < lptr[l + 1]; ++q) {
+                const int len = offdiag(order[q]);
+                if (rows > 0 && (rows + 1 > dev::kGsRows || ents + len > dev::kGsEnt)) {
+                    cptr.push_back(q);
+                    ceptr.push_back(e);
+                    rows = ents = 0;
+                }
+                check(len <= dev::kGsEnt, "gauss-seidel: row longer than the staging buffer");
+                ++rows;
+                ents += len;
+                e += len;
+            }
+            cptr.push_back(lptr[l + 1]);
+            ceptr.push_back(e);
+        }
+        for (size_t c = 0; c + 1 < cptr.size(); ++c)
+            for (int q = cptr[c]; q < cptr[c + 1]; ++q) chunk_end[q] = cptr[c + 1];
+    }
+    std::vector<int2> hdr(n);
+    std::vector<int> ref, sref;
     std::vector<double> val, dinv(n);
-    ci.reserve(A.idx.size());
+    ref.reserve(A.idx.size());
+    sref.reserve(A.idx.size());
     val.reserve(A.val.size());
     for (int q = 0; q < n; ++q) {
         const int i = order[q];
-        const int start = static_cast<int>(ci.size());
-        for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k)
-            if (A.idx[k] != i) {
-                ci.push_back(A.idx[k]);
-                val.push_back(A.val[k]);
+        hdr[q] = make_int2(i, static_cast<int>(ref.size()));
+        for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+            const int c = A.idx[k];
+            if (c == i) continue;
+            const bool updated = backward ? c > i : c < i;
+            if (!updated) {
+                ref.push_back(-(2 * c + 1));
+                sref.push_back(dev::kGsRing);  // the gathered product x 1.0
+            } else {
+                ref.push_back(0);
+                // the ring slot survives until q's chunk ends, else zout[c]
+                sref.push_back(pos[c] + dev::kGsRing >= chunk_end[q] ? (pos[c] & (dev::kGsRing - 1))
+                                                                     : -(c + 2));
             }
-        hdr[q] = make_int4(i, start, static_cast<int>(ci.size()) - start, 0);
+            val.push_back(A.val[k]);
+        }
         dinv[q] = inv_diag[i];
     }
-    if (ci.empty()) {  // a diagonal level: keep the entry arrays non-null
-        ci.push_back(0);
+    const long long nnz = static_cast<long long>(ref.size());
+    long long far = 0;
+    for (int v : sref) far += v < 0;
+    if (ref.empty()) {  // a diagonal level: keep the entry arrays non-null
+        ref.push_back(0);
+        sref.push_back(dev::kGsRing);
         val.push_back(0.0);
     }
     dev::GsSweep g;
     g.hdr = upload_array(hdr);
-    g.ci = upload_array(ci);
+    g.ref = upload_array(ref);
+    g.sref = upload_array(sref);
     g.val = upload_array(val);
     g.dinv = upload_array(dinv);
-    g.lptr = upload_array(lptr);
-    g.nlev = nlev;
+    g.cptr = upload_array(cptr);
+    g.ceptr = upload_array(ceptr);
+    g.nch = static_cast<int>(cptr.size()) - 1;
     g.n = n;
-    g.nnz = static_cast<long long>(ci.size());
+    g.nnz = nnz;
+    g.far = far > 0;
+    if (std::getenv("IRK_SETUP_TIMING"))
+        std::fprintf(stderr, "gs %s: n %d, depths %d, chunks %d, entries %lld (%lld beyond the ring)\n",
+                     backward ? "bwd" : "fwd", n, nlev, g.nch, nnz, far);
     return g;
 }
 
@@ -1607,6 +1664,48 @@ double DeviceSolver::time_kernel(int which, int reps) {
             dev::dgs_prof_read(t);
             std::fprintf(stderr, "dgs dot (last launch, ns from CTA 0 start): last CTA arrives %lld, elected %lld, "
                          "reduced %lld, scalars done %lld\n", t[0] - t[4], t[1] - t[4], t[2] - t[4], t[3] - t[4]);
+        }
+        return static_cast<double>(ms) / reps;
+    }
+    if (which >= 60 && which < 80) {
+        // Gauss-Seidel sweep of hierarchy 0, level (which - 60) / 2, forward
+        // (even) or backward (odd), on the level's work vectors
+        DevHier& H = hier_[0];
+        const int l = (which - 60) / 2;
+        const bool back = (which - 60) % 2 == 1;
+        check(H.prm.smoother != 0 && l + 1 < static_cast<int>(H.lv.size()),
+              "time_kernel: no Gauss-Seidel sweep at that level");
+        DevLevel& d = H.lv[l];
+        const double* rr = l == 0 ? d.t : d.r;
+        dev::GsSweep S = back ? d.gsb : d.gsf;
+        DevBuf prof(std::getenv("IRK_GS_PROF") ? 5 * 64 * sizeof(long long) : 0);
+        if (prof.bytes()) {
+            IRK_CUDA_CHECK(cudaMemset(prof.as<void>(), 0, prof.bytes()));
+            S.prof = prof.as<long long>();
+        }
+        auto once = [&]() { dev::gs_sweep(S, back, dev::plain(rr), d.u, dev::plain(d.zp), st_); };
+        IRK_CUDA_CHECK(cudaMemsetAsync(d.u, 0, sizeof(double) * d.n, st_));
+        once();
+        cudaEvent_t e0, e1;
+        IRK_CUDA_CHECK(cudaEventCreate(&e0));
+        IRK_CUDA_CHECK(cudaEventCreate(&e1));
+        IRK_CUDA_CHECK(cudaEventRecord(e0, st_));
+        for (int i = 0; i < reps; ++i) once();
+        IRK_CUDA_CHECK(cudaEventRecord(e1, st_));
+        IRK_CUDA_CHECK(cudaEventSynchronize(e1));
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (prof.bytes()) {
+            std::vector<long long> h(5 * 64);
+            IRK_CUDA_CHECK(cudaMemcpy(h.data(), prof.as<void>(), prof.bytes(), cudaMemcpyDeviceToHost));
+            double a[5] = {0, 0, 0, 0, 0};
+            for (int c = 1; c < 64; ++c)
+                for (int k = 0; k < 5; ++k) a[k] += static_cast<double>(h[5 * c + k]) / 63.0;
+            std::fprintf(stderr, "gs sweep L%d %s: cycles per chunk (thread 0, 63 sampled chunks, mean "
+                         "%.0f rows) after stage loads issued %.0f, compute done %.0f, staged %.0f, "
+                         "barrier %.0f\n", l, back ? "bwd" : "fwd", a[4], a[0], a[1], a[2], a[3]);
         }
         return static_cast<double>(ms) / reps;
     }

@@ -134,7 +134,8 @@ public:
     // returns the mean milliseconds per launch.  which: 0 stage operator,
     // 1 fine-level smoother SpMV, 2 preconditioner apply, 3 V-cycle, 4.. V-cycle
     // below level which-3, 100+j GMRES block-dot at inner index j, 20/21 empty-
-    // kernel launch floor (graph / stream).
+    // kernel launch floor (graph / stream), 60+2l(+1) Gauss-Seidel forward
+    // (backward) sweep of hierarchy 0 at level l.
     double time_kernel(int which, int reps);
     int launches_per_iteration() const { return launches_per_iter_; }
     const std::array<int, 4>& launch_counts() const { return launch_counts_; }

@@ -53,12 +53,18 @@ for _ in range(args.steps):
 L = _abi.lib()
 vc = C.c_double()
 _abi.check(L.irkdev_time_kernel(pc._dev._h, 3, 5, C.byref(vc)))
+sweeps = {}
+for l in range(3):
+    for back in (0, 1):
+        ms = C.c_double()
+        if L.irkdev_time_kernel(pc._dev._h, 60 + 2 * l + back, 5, C.byref(ms)) == 0:
+            sweeps[f"L{l}_{'bwd' if back else 'fwd'}_ms"] = ms.value
 h0 = pc.hierarchy(0)
 out = {"workload": f"heat {args.cells}^2, Radau IIA s=3, h_t=1e-3, P_LD, AMG GS V({args.pre},{args.post}) "
                    f"x{args.psteps} prolongator steps, GMRES(50) rtol 1e-8",
        "levels": h0.sizes(), "tail_from": h0.tail()[0], "iterations": its,
        "ms_per_step": [1e3 * s for s in secs], "solves_per_s": len(secs) / sum(secs),
-       "ms_per_vcycle": vc.value, "setup_s": setup}
+       "ms_per_vcycle": vc.value, "sweep_ms": sweeps, "setup_s": setup}
 if args.ref:
     from refs import RefSolver
     from systems import rel_l2
