@@ -132,6 +132,42 @@ int study() {
         ok = refused && compare_step("heat 32^2 max_coarse 200 (AmgParams passed)", sys, table, 1e-3,
                                      initial(sys.n(), false), P, GmresConfig{}, opt) && ok;
     }
+    // The study driver's own subsolve cycle (ExperimentConfig::amg,
+    // study.hpp:44-47: Gauss-Seidel V(4,4), two prolongator smoothing steps)
+    // and the Custom kind read from a coefficient file (make_coeff,
+    // study.cpp:269-282), as run_cell builds them.
+    {
+        AmgParams study_amg;
+        study_amg.pre_sweeps = 4;
+        study_amg.post_sweeps = 4;
+        study_amg.smoother = AmgSmoother::GaussSeidel;
+        study_amg.prolongation_steps = 2;
+        B200Options opt;
+        opt.amg = study_amg;
+        for (bool dg : {false, true}) {
+            const LinearParabolicSystem sys = make_system(48, dg);
+            const ButcherTable table = make_radau_iia(3);
+            const double ht = dg ? 1e-2 : 1e-3;
+            const BlockPreconditioner P(sys.M, sys.F, precond_coeff(table, CoeffKind::LowerFactor), ht,
+                                        SubsolverKind::AmgVcycle, study_amg);
+            ok = compare_step(dg ? "study cycle GS V(4,4) x2, double glazing 48^2 s=3 LD"
+                                 : "study cycle GS V(4,4) x2, heat 48^2 s=3 LD",
+                              sys, table, ht, initial(sys.n(), dg), P, GmresConfig{}, opt) && ok;
+        }
+        const char* path = "irk_b200_demo_coeff.txt";
+        {
+            std::FILE* f = std::fopen(path, "w");
+            std::fprintf(f, "3\n0.9 0 0\n0.31 0.7 0\n-0.12 0.25 1.1\n");
+            std::fclose(f);
+        }
+        const LinearParabolicSystem sys = make_system(48, false);
+        const ButcherTable table = make_radau_iia(3);
+        const BlockPreconditioner P(sys.M, sys.F, custom_coeff(read_coeff_file(path)), 1e-3,
+                                    SubsolverKind::AmgVcycle);
+        std::remove(path);
+        ok = compare_step("custom coefficient file, heat 48^2 s=3", sys, table, 1e-3,
+                          initial(sys.n(), false), P, GmresConfig{}, B200Options{}) && ok;
+    }
     irk_b200_release();
     std::printf("study %s\n", ok ? "ok" : "FAILED");
     return ok ? 0 : 1;
