@@ -265,6 +265,52 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
     if (a.y2) a.y2[i] = a.wd2[i] * out;
 }
 
+// Row-class DIA (7 diagonals) with the neighbour omega / a_cc table: the
+// operand loads of a row are issued first; a warp whose 32 rows all have the
+// dominant class then takes the stencil from the kernel parameters (no
+// class-table loads), any other warp loads its rows' class tables.  Same
+// products and sums as k_spmv_dia (IRK_DOM_CLASS=0 selects that kernel).
+template <int XM, int EPI, int WDT>
+__global__ void __launch_bounds__(256) k_spmv_cls(Mat A, SpmvArgs a) {
+    pdl_trigger();
+    const int n = A.rows;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) {
+        pdl_wait();
+        return;
+    }
+    const unsigned cls = __ldg(static_cast<const unsigned char*>(A.val) + i);
+    pdl_wait();
+    const double* r = a.r.base ? a.r.get() : nullptr;
+    const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
+    double ov[7];
+#pragma unroll
+    for (int d = 0; d < 7; ++d) {
+        const int c = min(max(i + A.off[d], 0), n - 1);
+        ov[d] = XM == kXWdR ? r[c] : x[c];
+    }
+    double s = 0.0, wdi = 0.0;
+    constexpr bool kWdi = EPI == kESmooth || EPI == kEProlong;
+    if (__all_sync(__activemask(), cls == static_cast<unsigned>(A.dom))) {
+#pragma unroll
+        for (int d = 0; d < 7; ++d) {
+            const double xv = XM == kXWdR ? A.dom_nbwd[d] * ov[d] : ov[d];
+            s += A.dom_tab[d] * xv;
+        }
+        if (kWdi) wdi = WDT == 1 ? A.dom_wd : a.wd[i];
+    } else {
+#pragma unroll
+        for (int d = 0; d < 7; ++d) {
+            const double xv = XM == kXWdR ? __ldg(A.nbwd + cls * 7 + d) * ov[d] : ov[d];
+            s += __ldg(A.tab + cls * 7 + d) * xv;
+        }
+        if (kWdi) wdi = WDT == 1 ? __ldg(A.wdtab + cls) : a.wd[i];
+    }
+    const double out = spmv_epilogue<XM, EPI>(s, wdi, i, a, r, x);
+    a.y.get()[i] = out;
+    if (a.y2) a.y2[i] = a.wd2[i] * out;
+}
+
 // SELL-32: one warp per 32-row slice, entries column-major inside the slice,
 // sequential per-row sums (same order as CSR; padding adds exact zeros).
 template <int XM, int EPI, int VF>
@@ -441,10 +487,16 @@ void launch_spmv(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
     case kCls:
         // DIA row classes (7 diagonals)
         if (A.fmt != kDia || A.nd != 7) throw InvalidArgument("row classes need a 7-diagonal DIA operator");
-        if (A.wdtab)
+        if (A.dom >= 0 && (A.nbwd || XM != kXWdR) && option("IRK_DOM_CLASS", 1) != 0) {
+            if (A.wdtab)
+                launch(k_spmv_cls<XM, EPI, 1>, blocks_for(A.rows, 256), 256, 0, st, A, a);
+            else
+                launch(k_spmv_cls<XM, EPI, 0>, blocks_for(A.rows, 256), 256, 0, st, A, a);
+        } else if (A.wdtab) {
             launch(k_spmv_dia<XM, EPI, kCls, 1, 7>, blocks_for(A.rows, 256), 256, 0, st, A, a);
-        else
+        } else {
             launch(k_spmv_dia<XM, EPI, kCls, 0, 7>, blocks_for(A.rows, 256), 256, 0, st, A, a);
+        }
         break;
     default: launch_spmv_vf<XM, EPI, kF64>(A, a, st); break;
     }

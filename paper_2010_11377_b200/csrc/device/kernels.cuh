@@ -59,6 +59,14 @@ struct Mat {
     // partner row (0 where the coefficient is 0), so wd .* r needs no
     // neighbour class lookups
     const double* nbwd = nullptr;
+    // kCls: the most frequent class (the interior stencil of a uniform grid)
+    // also travels in the kernel parameters -- a warp whose rows all have it
+    // takes its stencil, partner omega / a_cc and omega / a_ii from the
+    // constant bank instead of 15 class-table loads per row
+    int dom = -1;
+    double dom_tab[7] = {};
+    double dom_nbwd[7] = {};
+    double dom_wd = 0.0;
     size_t bytes = 0;               // device bytes of the stored operator
 };
 

@@ -285,10 +285,21 @@ bool DeviceSolver::to_row_classes(std::vector<dev::Mat*> mats, const std::vector
     std::vector<std::vector<double>> tabs;
     if (!row_classes(vals, m0.nd, m0.rows, m0.dstride, cls, tabs)) return false;
     const unsigned char* dcls = upload_array(cls);
+    // the most frequent class rides in the kernel parameters (dev::Mat::dom)
+    int dom = 0;
+    {
+        std::vector<long long> cnt(256, 0);
+        for (unsigned char c : cls) ++cnt[c];
+        for (int c = 1; c < 256; ++c)
+            if (cnt[c] > cnt[dom]) dom = c;
+    }
     // a null entry in `mats`: its table is the neighbour omega / a_cc table
     // of mats[0] (same class array)
     for (size_t q = 0; q < mats.size(); ++q)
-        if (!mats[q]) mats[0]->nbwd = upload_array(tabs[q]);
+        if (!mats[q]) {
+            mats[0]->nbwd = upload_array(tabs[q]);
+            for (int d = 0; d < 7; ++d) mats[0]->dom_nbwd[d] = tabs[q][static_cast<size_t>(dom) * 7 + d];
+        }
     for (size_t q = 0; q < mats.size(); ++q) {
         if (!mats[q]) continue;
         dev::Mat& m = *mats[q];
@@ -299,10 +310,13 @@ bool DeviceSolver::to_row_classes(std::vector<dev::Mat*> mats, const std::vector
         m.tab_smem = 0;
         m.bytes = (q == 0 ? cls.size() : 0) + sizeof(double) * tabs[q].size();
         m.wdtab = nullptr;
+        m.dom = dom;
+        for (int d = 0; d < 7; ++d) m.dom_tab[d] = tabs[q][static_cast<size_t>(dom) * 7 + d];
         if (omega > 0.0 && m.diag0 >= 0) {
             std::vector<double> wd(m.ntab);
             for (int c = 0; c < m.ntab; ++c) wd[c] = omega * (1.0 / tabs[q][static_cast<size_t>(c) * m.nd + m.diag0]);
             m.wdtab = upload_array(wd);
+            m.dom_wd = wd[dom];
         }
     }
     return true;
