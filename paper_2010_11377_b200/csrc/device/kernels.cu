@@ -31,6 +31,7 @@ inline int blocks_for(long long n, int t) { return static_cast<int>((n + t - 1) 
 
 namespace {
 thread_local bool g_pdl_scope = false;
+thread_local bool g_pdl_late = false;
 }
 
 namespace {
@@ -59,8 +60,10 @@ unsigned option_generation() { return g_opt_gen.load(); }
 
 bool pdl_enabled() {
     static const bool on = std::getenv("IRK_PDL") != nullptr;
-    return on || g_pdl_scope;
+    return on || g_pdl_scope || g_pdl_late;
 }
+
+void set_pdl_late(bool on) { g_pdl_late = on; }
 
 void set_pdl_scope(bool on) { g_pdl_scope = on; }
 
@@ -150,8 +153,9 @@ __device__ __forceinline__ double vfetch(const void* v, long long k, const doubl
 // (A.tab_smem), or read in place from global memory through L1 (no per-CTA
 // prologue and barrier before the first row load).
 template <int VF>
-__device__ __forceinline__ const double* load_tab(const Mat& A, double* s_tab, double* s_wd) {
-    pdl_trigger();
+__device__ __forceinline__ const double* load_tab(const Mat& A, double* s_tab, double* s_wd,
+                                                  bool early = true) {
+    if (early) pdl_trigger();
     if constexpr (VF == kU8) {
         if (!A.tab_smem) return A.tab;
         for (int i = threadIdx.x; i < A.ntab; i += blockDim.x) {
@@ -188,7 +192,7 @@ template <int XM, int EPI, int VF, int WDT, int ND>
 __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
     __shared__ double s_tab[VF == kU8 ? 256 : 1];
     __shared__ double s_wd[VF == kU8 ? 256 : 1];
-    const double* tab = load_tab<VF>(A, s_tab, s_wd);
+    const double* tab = load_tab<VF>(A, s_tab, s_wd, !a.late);
     const int n = A.rows;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) {
@@ -263,6 +267,7 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
     const double out = spmv_epilogue<XM, EPI>(s, wdi, i, a, r, x);
     a.y.get()[i] = out;
     if (a.y2) a.y2[i] = a.wd2[i] * out;
+    if (a.late) pdl_trigger();
 }
 
 // Row-class DIA (7 diagonals) with the neighbour omega / a_cc table: the
@@ -272,7 +277,7 @@ __global__ void __launch_bounds__(256) k_spmv_dia(Mat A, SpmvArgs a) {
 // products and sums as k_spmv_dia (IRK_DOM_CLASS=0 selects that kernel).
 template <int XM, int EPI, int WDT>
 __global__ void __launch_bounds__(256) k_spmv_cls(Mat A, SpmvArgs a) {
-    pdl_trigger();
+    if (!a.late) pdl_trigger();
     const int n = A.rows;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) {
@@ -309,6 +314,7 @@ __global__ void __launch_bounds__(256) k_spmv_cls(Mat A, SpmvArgs a) {
     const double out = spmv_epilogue<XM, EPI>(s, wdi, i, a, r, x);
     a.y.get()[i] = out;
     if (a.y2) a.y2[i] = a.wd2[i] * out;
+    if (a.late) pdl_trigger();
 }
 
 // SELL-32: one warp per 32-row slice, entries column-major inside the slice,
@@ -317,7 +323,7 @@ template <int XM, int EPI, int VF>
 __global__ void __launch_bounds__(256) k_spmv_sell(Mat A, SpmvArgs a) {
     __shared__ double s_tab[VF == kU8 ? 256 : 1];
     __shared__ double s_wd[1];
-    const double* tab = load_tab<VF>(A, s_tab, s_wd);
+    const double* tab = load_tab<VF>(A, s_tab, s_wd, !a.late);
     const int slice = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int nslices = (A.rows + 31) >> 5;
@@ -373,6 +379,7 @@ __global__ void __launch_bounds__(256) k_spmv_sell(Mat A, SpmvArgs a) {
     const double out = spmv_epilogue<XM, EPI>(s, wdi, row, a, r, x);
     a.y.get()[row] = out;
     if (a.y2) a.y2[row] = a.wd2[row] * out;
+    if (a.late) pdl_trigger();
 }
 
 // CSR-vector: G lanes per row, each lane loading up to 4 entries of a chunk
@@ -383,7 +390,7 @@ template <int XM, int EPI, int VF, int G>
 __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
     __shared__ double s_tab[VF == kU8 ? 256 : 1];
     __shared__ double s_wd[1];
-    const double* tab = load_tab<VF>(A, s_tab, s_wd);
+    const double* tab = load_tab<VF>(A, s_tab, s_wd, !a.late);
 #ifndef IRK_CSRV_MM
 #define IRK_CSRV_MM 4
 #endif
@@ -445,6 +452,7 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
     const double out = spmv_epilogue<XM, EPI>(s, wdi, row, a, r, x);
     a.y.get()[row] = out;
     if (a.y2) a.y2[row] = a.wd2[row] * out;
+    if (a.late) pdl_trigger();
 }
 
 template <int XM, int EPI, int VF>
@@ -511,12 +519,12 @@ constexpr int stage_op_min_blocks(int S) { return S <= 2 ? 8 : S <= 4 ? 6 : 4; }
 
 template <int S, int VF, int ND>
 __global__ void __launch_bounds__(256, stage_op_min_blocks(S)) k_stage_op_dia(Mat M, Mat K, StageCoef cf, VecRef zr,
-                                                      VecRef yr) {
+                                                      VecRef yr, int late) {
     __shared__ double s_tm[VF == kU8 ? 256 : 1];
     __shared__ double s_tk[VF == kU8 ? 256 : 1];
     __shared__ double s_dummy[1];
-    const double* tm = load_tab<VF>(M, s_tm, s_dummy);
-    const double* tk = load_tab<VF>(K, s_tk, s_dummy);
+    const double* tm = load_tab<VF>(M, s_tm, s_dummy, !late);
+    const double* tk = load_tab<VF>(K, s_tk, s_dummy, false);
     const int n = M.rows;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned ci = 0;  // joint (M, K) row class
@@ -556,15 +564,16 @@ __global__ void __launch_bounds__(256, stage_op_min_blocks(S)) k_stage_op_dia(Ma
         for (int j = 0; j < S; ++j) acc += cf.c[b * S + j] * fk[j];
         y[static_cast<long long>(b) * n + i] = acc;
     }
+    if (late) pdl_trigger();
 }
 
 // ------------------------------------------------------------------ sweep
 template <int VF, int ND>
 __global__ void __launch_bounds__(256) k_sweep_dia(Mat K, VecRef wr, VecRef vr, SweepTerms t,
-                                                   double* __restrict__ store, VecRef outr) {
+                                                   double* __restrict__ store, VecRef outr, int late) {
     __shared__ double s_tk[VF == kU8 ? 256 : 1];
     __shared__ double s_dummy[1];
-    const double* tk = load_tab<VF>(K, s_tk, s_dummy);
+    const double* tk = load_tab<VF>(K, s_tk, s_dummy, !late);
     const int n = K.rows;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     unsigned ci = 0;
@@ -590,6 +599,7 @@ __global__ void __launch_bounds__(256) k_sweep_dia(Mat K, VecRef wr, VecRef vr, 
     for (int q = 0; q < kMaxStages; ++q)
         if (q < t.nt) acc += t.coef[q] * (t.buf[q] ? t.buf[q][i] : f);
     outr.get()[i] = acc;
+    if (late) pdl_trigger();
 }
 
 __global__ void k_combine(int n, VecRef vr, SweepTerms t, VecRef outr) {
@@ -1854,8 +1864,10 @@ __global__ void __launch_bounds__(kRedThreads) k_gm_residual(GmresBufs g, const 
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
-void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st) {
-    if (A.rows > 0) tally(spmv_bytes(A, xmode, epi, a));
+void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a_in, cudaStream_t st) {
+    if (A.rows > 0) tally(spmv_bytes(A, xmode, epi, a_in));
+    SpmvArgs a = a_in;
+    a.late = g_pdl_late && !g_pdl_scope ? 1 : 0;
 #define IRK_SPMV_CASE(X, E)                         \
     if (xmode == X && epi == E) {                   \
         launch_spmv<X, E>(A, a, st);                \
@@ -1873,6 +1885,7 @@ void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st) 
 
 void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecRef y, int n,
                   cudaStream_t st) {
+    const int late = g_pdl_late && !g_pdl_scope ? 1 : 0;
     const int nb = blocks_for(n, 256);
     if (M.vf != K.vf || (M.vf != kF64 && M.vf != kU8 && M.vf != kCls))
         throw InvalidArgument("stage_op: M and K must share a value format (f64, u8 or row classes)");
@@ -1885,13 +1898,13 @@ void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecR
 #define IRK_OP_CASE(S)                                                             \
     case S:                                                                        \
         if (cls)                                                                   \
-            launch(k_stage_op_dia<S, kCls, 7>, nb, 256, 0, st, M, K, c, z, y);         \
+            launch(k_stage_op_dia<S, kCls, 7>, nb, 256, 0, st, M, K, c, z, y, late);         \
         else if (u8 && M.nd == 7)                                                  \
-            launch(k_stage_op_dia<S, kU8, 7>, nb, 256, 0, st, M, K, c, z, y);          \
+            launch(k_stage_op_dia<S, kU8, 7>, nb, 256, 0, st, M, K, c, z, y, late);          \
         else if (u8)                                                               \
-            launch(k_stage_op_dia<S, kU8, 0>, nb, 256, 0, st, M, K, c, z, y);          \
+            launch(k_stage_op_dia<S, kU8, 0>, nb, 256, 0, st, M, K, c, z, y, late);          \
         else                                                                       \
-            launch(k_stage_op_dia<S, kF64, 0>, nb, 256, 0, st, M, K, c, z, y);         \
+            launch(k_stage_op_dia<S, kF64, 0>, nb, 256, 0, st, M, K, c, z, y, late);         \
         break;
         IRK_OP_CASE(1) IRK_OP_CASE(2) IRK_OP_CASE(3) IRK_OP_CASE(4) IRK_OP_CASE(5)
         IRK_OP_CASE(6) IRK_OP_CASE(7)
@@ -1903,6 +1916,7 @@ void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecR
 
 void sweep_dia(const Mat& K, VecRef w, VecRef v, const SweepTerms& t, double* store, VecRef out,
                int n, cudaStream_t st) {
+    const int late = g_pdl_late && !g_pdl_scope ? 1 : 0;
     {
         int terms = 0;
         for (int q = 0; q < t.nt; ++q) terms += t.buf[q] != nullptr;
@@ -1911,16 +1925,16 @@ void sweep_dia(const Mat& K, VecRef w, VecRef v, const SweepTerms& t, double* st
     switch (K.vf) {
     case kCls:
         if (K.nd != 7) throw InvalidArgument("row classes need 7 diagonals");
-        launch(k_sweep_dia<kCls, 7>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out);
+        launch(k_sweep_dia<kCls, 7>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out, late);
         break;
     case kU8:
         if (K.nd == 7)
-            launch(k_sweep_dia<kU8, 7>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out);
+            launch(k_sweep_dia<kU8, 7>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out, late);
         else
-            launch(k_sweep_dia<kU8, 0>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out);
+            launch(k_sweep_dia<kU8, 0>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out, late);
         break;
-    case kU16: launch(k_sweep_dia<kU16, 0>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out); break;
-    default: launch(k_sweep_dia<kF64, 0>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out); break;
+    case kU16: launch(k_sweep_dia<kU16, 0>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out, late); break;
+    default: launch(k_sweep_dia<kF64, 0>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out, late); break;
     }
 }
 

@@ -92,6 +92,10 @@ struct SpmvArgs {
     // gathers one vector instead of two)
     double* y2 = nullptr;
     const double* wd2 = nullptr;
+    // programmatic launch with the trigger at the END of each thread's work
+    // (set by spmv() inside a set_pdl_late scope): the dependent grid's
+    // launch overlaps this grid's last wave instead of taking its slots
+    int late = 0;
 };
 
 // Algorithmic-bytes tally (the roofline's numerator): while a
@@ -112,6 +116,9 @@ bool pdl_enabled();
 // Programmatic launch for the kernels recorded while the scope is on (the
 // latency-bound coarse AMG levels, IRK_PDL_COARSE).
 void set_pdl_scope(bool on);
+// Kernels recorded while on are launched programmatically with the late
+// trigger (SpmvArgs::late): the many-wave level-0/1 SpMVs (IRK_PDL_FINE).
+void set_pdl_late(bool on);
 
 void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st);
 

@@ -900,7 +900,14 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
     // programmatic launches for the latency-bound levels >= 2
     // (IRK_PDL_COARSE=<level> moves the threshold, -1 turns it off)
     static const int pdl_from = std::getenv("IRK_PDL_COARSE") ? std::atoi(std::getenv("IRK_PDL_COARSE")) : 2;
-    auto scope = [&](int l) { dev::set_pdl_scope(pdl_from >= 0 && l >= pdl_from); };
+    // IRK_PDL_FINE=1: the levels below pdl_from are launched programmatically
+    // too, with the trigger at the end of each thread's work (SpmvArgs::late)
+    const bool fine_late = dev::option("IRK_PDL_FINE", 1) != 0;
+    auto scope = [&](int l) {
+        const bool coarse = pdl_from >= 0 && l >= pdl_from;
+        dev::set_pdl_scope(coarse);
+        dev::set_pdl_late(!coarse && fine_late);
+    };
     auto out_of = [&](int l) { return l == first ? z0 : dev::plain(H.lv[l].z); };
     // levels >= bot run in the single-CTA bottom kernel
     // levels >= tail are one dense matvec (IRK_TAIL=0: the recursive cycle)
@@ -912,6 +919,9 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
     for (int l = first; l < down_end; ++l) {
         DevLevel& d = H.lv[l];
         scope(l);
+        // the cycle's first kernel: programmatic only after a late-trigger
+        // kernel (a block sweep), not after one that triggers at its start
+        if (l == first && !vc_pdl_first_) dev::set_pdl_late(false);
         dev::SpmvArgs a;
         a.r = rhs_of(l);
         a.wd = d.wd;
@@ -939,6 +949,7 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
             a.x = dev::plain(d.zp);
             dev::spmv(d.A, dev::kXPlain, dev::kEResid, a, st_);
         }
+        scope(l);
         dev::SpmvArgs ra;
         ra.x = dev::plain(d.t);
         ra.y = dev::plain(H.lv[l + 1].r);
@@ -982,6 +993,7 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
         }
     }
     dev::set_pdl_scope(false);
+    dev::set_pdl_late(false);
 }
 
 // Block preconditioner apply (stage.cpp:138-182): diagonal, forward (LD,
@@ -1039,9 +1051,11 @@ void DeviceSolver::record_precond(VecRef v, VecRef w) {
         return;
     }
     auto e = [&](int j, int k) { return -ht_ * At_[j * s + k]; };
+    const bool fine_late = dev::option("IRK_PDL_FINE", 1) != 0;
     for (int q = 0; q < s; ++q) {
         const int j = structure_ == Structure::Upper ? s - 1 - q : q;
         VecRef in = block(v, j * n);
+        bool swept = false;
         if (structure_ != Structure::Diagonal && q > 0) {
             const int prev = structure_ == Structure::Upper ? j + 1 : j - 1;
             const int k0 = structure_ == Structure::Upper ? j + 1 : 0;
@@ -1064,7 +1078,12 @@ void DeviceSolver::record_precond(VecRef v, VecRef w) {
             if (fresh || later) {
                 double* store = later ? fw_ + prev * n : nullptr;
                 if (K_.fmt == dev::kDia) {
+                    // programmatic, late trigger: it follows the previous
+                    // V-cycle's last (late-trigger) kernel
+                    dev::set_pdl_late(fine_late);
                     dev::sweep_dia(K_, block(w, prev * n), in, t, store, dev::plain(rhs_), n_, st_);
+                    dev::set_pdl_late(false);
+                    swept = true;
                 } else {
                     dev::SpmvArgs a;
                     a.x = block(w, prev * n);
@@ -1080,7 +1099,9 @@ void DeviceSolver::record_precond(VecRef v, VecRef w) {
                 in = dev::plain(rhs_);
             }
         }
+        vc_pdl_first_ = swept;
         record_vcycle(sob_[j], in, block(w, j * n));
+        vc_pdl_first_ = false;
     }
 }
 
@@ -1120,7 +1141,13 @@ void DeviceSolver::record_iteration() {
         record_precond(dev::plain(ax_), slot(gb_.V, jp, stride_, 1));
     } else {
         record_precond(slot(gb_.V, jp, stride_, 0), slot(gb_.Z, jp, stride_, 0));
+        // after the last V-cycle's late-trigger smoother (not after the
+        // block-Jacobi join)
+        const bool late = dev::option("IRK_PDL_FINE", 1) != 0 &&
+                          !(structure_ == Structure::Diagonal && hier_.size() > 1);
+        dev::set_pdl_late(late);
         record_stage_op(slot(gb_.Z, jp, stride_, 0), slot(gb_.V, jp, stride_, 1));
+        dev::set_pdl_late(false);
     }
     if (ortho_ == 1) {
         // programmatic launches: the block-dot's static loads overlap the

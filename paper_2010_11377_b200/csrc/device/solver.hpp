@@ -216,6 +216,9 @@ private:
     bool compress_values_ = true;
     int ortho_ = 1;  // 1 DCGS2 (default), 0 CGS + conditional second pass
     int side_ = 1, g_side_ = -1;  // GMRES preconditioning side (1 right, 0 left)
+    // the next recorded V-cycle's first kernel follows a late-trigger kernel
+    // (a sweep) and may be launched programmatically (IRK_PDL_FINE)
+    bool vc_pdl_first_ = false;
 };
 
 }  // namespace irkb

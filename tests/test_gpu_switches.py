@@ -7,6 +7,7 @@ Switches (irk_set_option, same names as the IRK_* environment variables):
   IRK_ZR           restriction writes wd.*r for the next level vs on-the-fly
   IRK_PDL_DGS      programmatic launches of the DCGS2 block-dot / update
   IRK_PDL_COARSE   first AMG level launched programmatically
+  IRK_PDL_FINE     level-0/1 SpMVs launched programmatically, late trigger
   IRK_DOM_CLASS    row-class SpMV with the dominant class in the kernel
                    parameters vs class-table loads for every row
 """
@@ -20,7 +21,8 @@ from conftest import has_gpu
 pytestmark = [pytest.mark.gpu,
               pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
 
-DEFAULTS = {"IRK_BOTTOM": 1, "IRK_ZR": 1, "IRK_PDL_DGS": 1, "IRK_PDL_COARSE": 2, "IRK_DOM_CLASS": 1}
+DEFAULTS = {"IRK_BOTTOM": 1, "IRK_ZR": 1, "IRK_PDL_DGS": 1, "IRK_PDL_COARSE": 2, "IRK_DOM_CLASS": 1,
+            "IRK_PDL_FINE": 1}
 
 
 def set_opt(name, value):
@@ -52,7 +54,7 @@ def step(case):
 
 @pytest.mark.parametrize("name,off", [("IRK_BOTTOM", 0), ("IRK_ZR", 0), ("IRK_PDL_DGS", 0),
                                       ("IRK_PDL_COARSE", 0), ("IRK_PDL_COARSE", 99),
-                                      ("IRK_DOM_CLASS", 0)])
+                                      ("IRK_DOM_CLASS", 0), ("IRK_PDL_FINE", 0)])
 def test_switch_is_bit_identical(case, name, off):
     a = step(case)
     set_opt(name, off)
