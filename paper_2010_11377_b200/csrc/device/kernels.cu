@@ -582,16 +582,31 @@ __global__ void __launch_bounds__(256) k_sweep_dia(Mat K, VecRef wr, VecRef vr, 
     if (i >= n) return;
     const double* __restrict__ w = wr.get();
     double f = 0.0;
+    if constexpr (VF == kCls && ND == 7) {
+        // operand loads first; a warp whose rows all have the dominant class
+        // takes the stencil from the kernel parameters (k_spmv_cls)
+        double wv[7];
 #pragma unroll
-    for (int d = 0; d < (ND > 0 ? ND : kMaxDiags); ++d) {
-        if (ND == 0 && d >= K.nd) break;
-        const int c = min(max(i + K.off[d], 0), n - 1);
-        double k;
-        if constexpr (VF == kCls)
-            k = __ldg(K.tab + ci * ND + d);
-        else
-            k = vfetch<VF>(K.val, static_cast<long long>(d) * K.dstride + i, tk);
-        f += k * w[c];
+        for (int d = 0; d < 7; ++d) wv[d] = w[min(max(i + K.off[d], 0), n - 1)];
+        if (K.dom >= 0 && __all_sync(__activemask(), ci == static_cast<unsigned>(K.dom))) {
+#pragma unroll
+            for (int d = 0; d < 7; ++d) f += K.dom_tab[d] * wv[d];
+        } else {
+#pragma unroll
+            for (int d = 0; d < 7; ++d) f += __ldg(K.tab + ci * 7 + d) * wv[d];
+        }
+    } else {
+#pragma unroll
+        for (int d = 0; d < (ND > 0 ? ND : kMaxDiags); ++d) {
+            if (ND == 0 && d >= K.nd) break;
+            const int c = min(max(i + K.off[d], 0), n - 1);
+            double k;
+            if constexpr (VF == kCls)
+                k = __ldg(K.tab + ci * ND + d);
+            else
+                k = vfetch<VF>(K.val, static_cast<long long>(d) * K.dstride + i, tk);
+            f += k * w[c];
+        }
     }
     if (store) store[i] = f;
     double acc = vr.get()[i];
@@ -1923,10 +1938,13 @@ void sweep_dia(const Mat& K, VecRef w, VecRef v, const SweepTerms& t, double* st
         tally(mat_bytes(K) + 8.0 * n * (3 + terms) + (store ? 8.0 * n : 0.0));
     }
     switch (K.vf) {
-    case kCls:
+    case kCls: {
         if (K.nd != 7) throw InvalidArgument("row classes need 7 diagonals");
-        launch(k_sweep_dia<kCls, 7>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out, late);
+        Mat Kc = K;
+        if (option("IRK_DOM_CLASS", 1) == 0) Kc.dom = -1;  // class tables for every row
+        launch(k_sweep_dia<kCls, 7>, blocks_for(n, 256), 256, 0, st, Kc, w, v, t, store, out, late);
         break;
+    }
     case kU8:
         if (K.nd == 7)
             launch(k_sweep_dia<kU8, 7>, blocks_for(n, 256), 256, 0, st, K, w, v, t, store, out, late);
