@@ -2094,27 +2094,24 @@ void dot(const double* x, const double* y, long long n, double* partials, unsign
 
 // ------------------------------------------------------------------ Gauss-Seidel
 // One sweep = a parallel gather + ONE CTA stepping through the schedule's
-// chunks, separated by a barrier, one thread per row.  A sweep is a chain of
-// dependent steps (C2 with the study cycle: ~2000 at level 0, ~3100 at level
-// 1) and latency-bound by construction -- the reference's own sweep is
-// sequential (amg.cpp:125-140) -- so a step is kept to shared-memory reads:
-// the gather kernel has already written r and every not-yet-updated operand
-// product in schedule order, so staging chunk C+1 is a set of contiguous,
-// independent loads issued before chunk C computes and stored to the other
-// buffer after it (chunk C+4 is bulk-prefetched into L2); updated operands
-// come from a ring of the last kGsRing computed values.  What bounds a step
-// now is the one SM's load/store issue rate (profiles/r2/gs_sweep.txt).
+// chunks.  A sweep is a chain of dependent steps (C2 with the study cycle:
+// ~2000 depths at level 0, ~3100 at level 1) and latency-bound by
+// construction -- the reference's own sweep is sequential (amg.cpp:125-140).
+//  * k_gs_gather (all SMs): r in schedule order and every not-yet-updated
+//    operand's rounded product a_ij * zin_j, the very product the row sum
+//    subtracts (so the chain reads no global memory);
+//  * k_gs_sweep: warp-specialised -- 4 groups of 7 producer warps copy
+//    chunks (each group every 4th chunk, several in flight) into a ring of
+//    kWsNB shared-memory buffers; 4 consumer warps (one row per thread)
+//    step through the chunks with a 128-thread named barrier between them.
+//    Entries are stored column-major inside a chunk (entry k of the chunk's
+//    row q at k * rows + q, padded to the chunk's longest row), so the
+//    consumers' shared-memory reads are conflict-free; updated operands come
+//    from a ring of the last kGsRing computed values, a not-yet-updated
+//    operand from the ring's constant 1.0 slot times its gathered product
+//    (exact).  Buffers are handed over with sequence flags in shared memory
+//    (fence.cta before the flag store and after its load).
 namespace {
-constexpr int kGsThreads = 1024;
-struct GsBuf {
-    int2 hdr[kGsRows];
-    double dinv[kGsRows];
-    double r[kGsRows];
-    double e[kGsEnt];
-    int ref[kGsEnt];
-};
-constexpr size_t kGsSmem = sizeof(double) * (kGsRing + 2) + 2 * sizeof(GsBuf);
-
 __global__ void __launch_bounds__(256) k_gs_gather(GsSweep S, VecRef rr, const double* zin) {
     pdl_trigger();
     pdl_wait();
@@ -2129,148 +2126,158 @@ __global__ void __launch_bounds__(256) k_gs_gather(GsSweep S, VecRef rr, const d
     }
 }
 
-// Chunk bounds {first position, first entry}: read from global memory one
-// iteration before use (the shared-memory carveout leaves little L1, so
-// every load is an L2 round trip that must not sit on the chunk chain).
-struct GsBounds {
-    int q, e;
+constexpr int kWsCons = 4 * 32, kWsThreads = 1024, kWsProd = kWsThreads - kWsCons;
+constexpr int kWsNB = 6;
+constexpr int kWsGroups = 4, kWsGroupThreads = kWsProd / kWsGroups;  // 224 threads = 7 warps
+struct WsBuf {
+    int meta[4];  // first position, rows, first entry, entries (rows x width)
+    int2 hdr[kGsRows];
+    double dinv[kGsRows];
+    double r[kGsRows];
+    double e[kGsEnt];
+    int ref[kGsEnt];
 };
-__device__ __forceinline__ GsBounds gs_bounds(const GsSweep& S, int C) {
-    const int c = min(C, S.nch);
-    return {__ldg(S.cptr + c), __ldg(S.ceptr + c)};
+constexpr size_t kWsSmem = sizeof(double) * (kGsRing + 2) + kWsNB * sizeof(WsBuf) + 64;
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// chunk [b0, b1): contiguous loads into registers (issued before the
-// current chunk computes), written to the staging buffer after it
-constexpr int kGsRowPer = kGsRows / kGsThreads;
-constexpr int kGsEntPer = kGsEnt / kGsThreads;
-struct GsRegs {
-    int2 h[kGsRowPer];
-    double dinv[kGsRowPer], r[kGsRowPer];
-    double e[kGsEntPer];
-    int ref[kGsEntPer];
-};
-__device__ __forceinline__ void gs_load(const GsSweep& S, GsBounds b0, GsBounds b1, GsRegs& g) {
-    const int nr = b1.q - b0.q, ne = b1.e - b0.e;
-#pragma unroll
-    for (int u = 0; u < kGsRowPer; ++u) {
-        const int q = threadIdx.x + u * kGsThreads;
-        if (q < nr) {
-            g.h[u] = __ldg(S.hdr + b0.q + q);
-            g.dinv[u] = __ldg(S.dinv + b0.q + q);
-            g.r[u] = __ldcg(S.rs + b0.q + q);
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < kGsEntPer; ++u) {
-        const int e = threadIdx.x + u * kGsThreads;
-        if (e < ne) {
-            g.e[u] = __ldcg(S.ps + b0.e + e);
-            g.ref[u] = __ldg(S.sref + b0.e + e);
-        }
-    }
-}
-__device__ __forceinline__ void gs_store(GsBounds b0, GsBounds b1, const GsRegs& g, GsBuf& b) {
-    const int nr = b1.q - b0.q, ne = b1.e - b0.e;
-#pragma unroll
-    for (int u = 0; u < kGsRowPer; ++u) {
-        const int q = threadIdx.x + u * kGsThreads;
-        if (q < nr) {
-            b.hdr[q] = g.h[u];
-            b.dinv[q] = g.dinv[u];
-            b.r[q] = g.r[u];
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < kGsEntPer; ++u) {
-        const int e = threadIdx.x + u * kGsThreads;
-        if (e < ne) {
-            b.e[e] = g.e[u];
-            b.ref[e] = g.ref[u];
-        }
-    }
-}
-
-// a later chunk [p0, p1) into L2: one asynchronous bulk prefetch per array
-// (cp.async.bulk.prefetch.L2, no completion to wait for -- the per-line
-// prefetch.global.L2 of a thread stalls it for an L2 round trip each)
-__device__ __forceinline__ void bulk_prefetch_l2(const void* lo, const void* hi) {
-    const unsigned long long a = reinterpret_cast<unsigned long long>(lo) & ~15ull;
-    const unsigned long long b = reinterpret_cast<unsigned long long>(hi) & ~15ull;
-    if (b > a)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(static_cast<unsigned>(b - a))
-                     : "memory");
-}
-__device__ __forceinline__ void gs_prefetch(const GsSweep& S, GsBounds p0, GsBounds p1) {
-    switch (threadIdx.x) {
-    case 0: bulk_prefetch_l2(S.sref + p0.e, S.sref + p1.e); break;
-    case 32: bulk_prefetch_l2(S.ps + p0.e, S.ps + p1.e); break;
-    case 64: bulk_prefetch_l2(S.hdr + p0.q, S.hdr + p1.q); break;
-    case 96: bulk_prefetch_l2(S.dinv + p0.q, S.dinv + p1.q); break;
-    case 128: bulk_prefetch_l2(S.rs + p0.q, S.rs + p1.q); break;
-    default: break;
-    }
-}
-
-// kFar: some updated operands are older than the ring (read from zout);
-// otherwise every entry is x * ring[ref] -- a not-yet-updated operand's
-// gathered product times the ring's constant 1.0 slot (exact) -- and a row's
-// 8-entry blocks load, multiply and then subtract in column order.
-constexpr int kGsPf = 4;  // L2 prefetch distance (chunks)
 template <bool kFar>
-__global__ void __launch_bounds__(kGsThreads, 1) k_gs_sweep(GsSweep S, VecRef zr) {
+__global__ void __launch_bounds__(kWsThreads, 1) k_gs_sweep(GsSweep S, VecRef zr) {
     pdl_trigger();
     extern __shared__ __align__(16) unsigned char gs_smem[];
     double* ring = reinterpret_cast<double*>(gs_smem);
-    GsBuf* buf = reinterpret_cast<GsBuf*>(gs_smem + sizeof(double) * (kGsRing + 2));
-    // chunk bounds travel through shared memory: thread 0 loads the bounds
-    // of chunk C + kGsPf + 2 while chunk C computes and publishes them with
-    // the barrier (a uniform-register copy of a loaded value would stall
-    // every warp on the load right where it is issued)
-    __shared__ GsBounds sbd[8];
-    if (threadIdx.x == 0) {
-        ring[kGsRing] = 1.0;
-        for (int k = 0; k < kGsPf + 2; ++k) sbd[k] = gs_bounds(S, k);
+    WsBuf* buf = reinterpret_cast<WsBuf*>(gs_smem + sizeof(double) * (kGsRing + 2));
+    volatile int* full = reinterpret_cast<volatile int*>(gs_smem + sizeof(double) * (kGsRing + 2) +
+                                                         kWsNB * sizeof(WsBuf));
+    volatile int* freed = full + 8;
+    if (threadIdx.x < kWsNB) {
+        full[threadIdx.x] = -1;
+        freed[threadIdx.x] = static_cast<int>(threadIdx.x) - kWsNB;
     }
+    if (threadIdx.x == 0) ring[kGsRing] = 1.0;
     pdl_wait();
     __syncthreads();
-    double* zout = zr.get();
-    {
-        GsRegs g;
-        gs_load(S, sbd[0], sbd[1], g);
-        gs_store(sbd[0], sbd[1], g, buf[0]);
+    if (threadIdx.x >= kWsCons) {
+        // ---------------- producers
+        const int pt = threadIdx.x - kWsCons;
+        const int grp = pt / kWsGroupThreads, gt = pt % kWsGroupThreads;
+        int C = grp;
+        int rb = 0, nr = 0, eb = 0, ne = 0;
+        if (C < S.nch) {
+            rb = __ldg(S.cptr + C);
+            nr = __ldg(S.cptr + C + 1) - rb;
+            eb = __ldg(S.ceptr + C);
+            ne = __ldg(S.ceptr + C + 1) - eb;
+        }
+        for (; C < S.nch; C += kWsGroups) {
+            // bounds of this group's next chunk, loaded while this one stages
+            const int Cn = C + kWsGroups;
+            int rbn = 0, nrn = 0, ebn = 0, nen = 0;
+            if (Cn < S.nch) {
+                rbn = __ldg(S.cptr + Cn);
+                nrn = __ldg(S.cptr + Cn + 1) - rbn;
+                ebn = __ldg(S.ceptr + Cn);
+                nen = __ldg(S.ceptr + Cn + 1) - ebn;
+            }
+            const int b = C % kWsNB;
+            if ((threadIdx.x & 31) == 0)
+                while (freed[b] != C - kWsNB) __nanosleep(300);
+            __syncwarp();
+            __threadfence_block();
+            WsBuf& B = buf[b];
+            if (gt == 0) {
+                B.meta[0] = rb;
+                B.meta[1] = nr;
+                B.meta[2] = eb;
+                B.meta[3] = ne;
+            }
+            // all of a thread's loads of the chunk in flight before any store
+            constexpr int kRq = (kGsRows + kWsGroupThreads - 1) / kWsGroupThreads;
+            constexpr int kEq = 4;
+            {
+                int2 h[kRq];
+                double dv[kRq], rv[kRq];
+#pragma unroll
+                for (int u = 0; u < kRq; ++u) {
+                    const int q = gt + u * kWsGroupThreads;
+                    if (q < nr) {
+                        h[u] = __ldg(S.hdr + rb + q);
+                        dv[u] = __ldg(S.dinv + rb + q);
+                        rv[u] = __ldcg(S.rs + rb + q);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kRq; ++u) {
+                    const int q = gt + u * kWsGroupThreads;
+                    if (q < nr) {
+                        B.hdr[q] = h[u];
+                        B.dinv[q] = dv[u];
+                        B.r[q] = rv[u];
+                    }
+                }
+            }
+            for (int e0 = gt; e0 < ne; e0 += kEq * kWsGroupThreads) {
+                double ev[kEq];
+                int fv[kEq];
+#pragma unroll
+                for (int u = 0; u < kEq; ++u) {
+                    const int e = e0 + u * kWsGroupThreads;
+                    if (e < ne) {
+                        ev[u] = __ldcg(S.ps + eb + e);
+                        fv[u] = __ldg(S.sref + eb + e);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kEq; ++u) {
+                    const int e = e0 + u * kWsGroupThreads;
+                    if (e < ne) {
+                        B.e[e] = ev[u];
+                        B.ref[e] = fv[u];
+                    }
+                }
+            }
+            named_bar(2 + grp, kWsGroupThreads);
+            if (gt == 0) {
+                __threadfence_block();
+                full[b] = C;
+            }
+            rb = rbn;
+            nr = nrn;
+            eb = ebn;
+            ne = nen;
+        }
+        return;
     }
-    __syncthreads();
+    // ---------------- consumers
+    double* zout = zr.get();
     long long* prof = S.prof && threadIdx.x == 0 ? S.prof : nullptr;
     const int pstride = S.nch / 64 > 1 ? S.nch / 64 : 1;
     for (int C = 0; C < S.nch; ++C) {
-        long long t0 = 0;
+        const int b = C % kWsNB;
         const bool pr = prof && C % pstride == 0 && C / pstride < 64;
         long long* pp = pr ? prof + 5 * (C / pstride) : nullptr;
+        long long t0 = 0;
         if (pr) t0 = clock64();
-        GsBounds bd[kGsPf + 2];
-#pragma unroll
-        for (int k = 0; k < kGsPf + 2; ++k) bd[k] = sbd[(C + k) & 7];
-        GsBounds nxt{0, 0};
-        if (threadIdx.x == 0) nxt = gs_bounds(S, C + kGsPf + 2);
-        GsRegs g;
-        if (C + 1 < S.nch) gs_load(S, bd[1], bd[2], g);
-        if (C + kGsPf < S.nch) gs_prefetch(S, bd[kGsPf], bd[kGsPf + 1]);
+        if ((threadIdx.x & 31) == 0)
+            while (full[b] != C) {
+            }
+        __syncwarp();
+        __threadfence_block();
         if (pr) pp[0] = clock64() - t0;
-        const GsBuf& b = buf[C & 1];
-        const int rb = bd[0].q, nr = bd[1].q - bd[0].q, eb = bd[0].e, ne = bd[1].e - bd[0].e;
-        for (int q = threadIdx.x; q < nr; q += kGsThreads) {
-            const int2 h = b.hdr[q];
-            const int e0 = h.y - eb;
-            const int e1 = q + 1 < nr ? b.hdr[q + 1].y - eb : ne;
-            double s = b.r[q];
-            for (int e = e0; e < e1; e += 8) {
+        const WsBuf& B = buf[b];
+        const int rb = B.meta[0], nr = B.meta[1];
+        for (int q = threadIdx.x; q < nr; q += kWsCons) {
+            const int2 h = B.hdr[q];  // {row, entries}
+            double s = B.r[q];
+            for (int k = 0; k < h.y; k += 8) {
                 double p[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    const int k = min(e + u, e1 - 1);
-                    const int rf = b.ref[k];
-                    const double x = b.e[k];
+                    const int e = min(k + u, h.y - 1) * nr + q;
+                    const int rf = B.ref[e];
+                    const double x = B.e[e];
                     if (kFar)
                         p[u] = rf >= 0 ? x * ring[rf] : x * zout[-rf - 2];
                     else
@@ -2278,20 +2285,22 @@ __global__ void __launch_bounds__(kGsThreads, 1) k_gs_sweep(GsSweep S, VecRef zr
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
-                    if (e + u < e1) s = s - p[u];
+                    if (k + u < h.y) s = s - p[u];
             }
-            const double z = s * b.dinv[q];
+            const double z = s * B.dinv[q];
             ring[(rb + q) & (kGsRing - 1)] = z;
             zout[h.x] = z;
         }
         if (pr) pp[1] = clock64() - t0;
-        if (C + 1 < S.nch) gs_store(bd[1], bd[2], g, buf[(C + 1) & 1]);
-        if (threadIdx.x == 0) sbd[(C + kGsPf + 2) & 7] = nxt;
-        if (pr) pp[2] = clock64() - t0;
-        __syncthreads();
+        named_bar(1, kWsCons);
         if (pr) {
-            pp[3] = clock64() - t0;
-            pp[4] = bd[1].q - bd[0].q;
+            pp[2] = clock64() - t0;
+            pp[3] = pp[2];
+            pp[4] = nr;
+        }
+        if (threadIdx.x == 0) {
+            __threadfence_block();
+            freed[b] = C;
         }
     }
 }
@@ -2308,9 +2317,9 @@ void gs_sweep(const GsSweep& S, bool backward, VecRef r, const double* zin, VecR
     const int blocks = static_cast<int>(std::min<long long>((work + 255) / 256, 148LL * 8));
     launch(k_gs_gather, std::max(blocks, 1), 256, 0, st, S, r, zin);
     if (S.far)
-        launch(k_gs_sweep<true>, 1, kGsThreads, kGsSmem, st, S, zout);
+        launch(k_gs_sweep<true>, 1, kWsThreads, kWsSmem, st, S, zout);
     else
-        launch(k_gs_sweep<false>, 1, kGsThreads, kGsSmem, st, S, zout);
+        launch(k_gs_sweep<false>, 1, kWsThreads, kWsSmem, st, S, zout);
 }
 
 void set_smem_limits() {
@@ -2320,8 +2329,8 @@ void set_smem_limits() {
     cudaFuncSetAttribute(k_dgs_update<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_dgs_update<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_dense_mv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_gs_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGsSmem));
-    cudaFuncSetAttribute(k_gs_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kGsSmem));
+    cudaFuncSetAttribute(k_gs_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kWsSmem));
+    cudaFuncSetAttribute(k_gs_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kWsSmem));
     const int nv = kMaxRestart + 2;
     cudaFuncSetAttribute(k_gm_blockdot, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(red_smem(nv)));

@@ -193,18 +193,20 @@ void bottom_cycle(const BotDesc& d, const double* r_in, double* z_out, cudaStrea
 // Gauss-Seidel sweep (amg.cpp:125-140) of one level, level-scheduled: the
 // rows are grouped by dependency depth (row i after every row j it reads
 // updated: j < i forward, j > i backward) and stored in that order, the
-// depths cut into chunks of <= kGsRows rows and <= kGsEnt off-diagonal
-// entries (rows of one chunk are independent).  Per schedule position q:
-// hdr[q] = {i, first entry}, dinv[q] = 1 / a_ii; per entry (column order,
-// the diagonal dropped as the reference skips it) its value and two static
-// codes:
+// depths cut into chunks of <= kGsRows rows and <= kGsEnt padded entries
+// (rows of one chunk are independent).  Per schedule position q:
+// hdr[q] = {i, off-diagonal entries}, dinv[q] = 1 / a_ii; a chunk's entries
+// are column-major (entry k of its row q at chunk base + k * rows + q,
+// padded to the chunk's longest row; per row in CSR column order, the
+// diagonal dropped as the reference skips it), each with its value and two
+// static codes:
 //   ref  (the gather)  -(2c+1): the not-yet-updated value of column c, else 0
 //   sref (the sweep)   0 .. kGsRing-1: an updated value still in the
 //                      kernel's ring of the last kGsRing computed rows (slot
 //                      = position mod kGsRing); kGsRing: the gathered product
 //                      (the ring's constant 1.0 slot); -(c+2): an updated
 //                      value too old for the ring (zout[c]; `far` sweeps).
-constexpr int kGsRows = 1024, kGsEnt = 6144, kGsRing = 4096;
+constexpr int kGsRows = 256, kGsEnt = 2048, kGsRing = 4096;
 struct GsSweep {
     const int2* hdr = nullptr;   // n, schedule order
     const int* ref = nullptr;    // nnz gather codes
@@ -212,12 +214,12 @@ struct GsSweep {
     const double* val = nullptr; // nnz values
     const double* dinv = nullptr;
     const int* cptr = nullptr;   // nch + 1 chunk position offsets
-    const int* ceptr = nullptr;  // nch + 1 chunk entry offsets
+    const int* ceptr = nullptr;  // nch + 1 chunk entry offsets (padded, rows x width)
     double* rs = nullptr;        // n: r in schedule order (written by the gather)
     double* ps = nullptr;        // nnz: the gathered entry operands
     int nch = 0, n = 0;
     int far = 0;                 // some operands older than the ring
-    long long nnz = 0;
+    long long nnz = 0;           // stored (padded) entries
     long long* prof = nullptr;   // diagnostic: per-chunk phase clocks (time_kernel, IRK_GS_PROF)
 };
 // zout_i = (r_i - sum_{j != i} a_ij z_j) / a_ii in CSR column order, with z_j

@@ -528,7 +528,7 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
                 d.gsb = upload_gs(lev.A, lev.inv_diag, true);
                 // gather scratch, shared by the level's (sequential) sweeps
                 d.gsf.rs = d.gsb.rs = alloc(d.n);
-                d.gsf.ps = d.gsb.ps = alloc(std::max<long long>(d.gsf.nnz, 1));
+                d.gsf.ps = d.gsb.ps = alloc(std::max<long long>(std::max(d.gsf.nnz, d.gsb.nnz), 1));
             }
             if (l > 0) {
                 d.r = alloc(d.n);
@@ -726,8 +726,9 @@ bool zr_on() { return dev::option("IRK_ZR", 1) != 0; }
 // Gauss-Seidel schedule of one level (amg.cpp:125-140): depth(i) = 1 + max
 // depth(j) over the entries a_ij the sweep reads updated (j < i forward, j > i
 // backward); positions sorted by depth (stable in i) and cut into chunks of
-// <= kGsRows rows / kGsEnt entries; entries in column order without the
-// diagonal, each with its source code (dev::GsSweep).
+// <= kGsRows rows whose entries, padded to the chunk's longest row, fit
+// kGsEnt; a chunk's entries column-major (dev::GsSweep), each row's in CSR
+// column order without the diagonal, with their source codes.
 dev::GsSweep DeviceSolver::upload_gs(const Csr& A, const std::vector<double>& inv_diag,
                                      bool backward) {
     const int n = A.rows;
@@ -752,69 +753,70 @@ dev::GsSweep DeviceSolver::upload_gs(const Csr& A, const std::vector<double>& in
         for (int i = 0; i < n; ++i) order[fill[depth[i]]++] = i;
     }
     for (int q = 0; q < n; ++q) pos[order[q]] = q;
-    auto offdiag = [&](int i) {
-        int c = 0;
-        for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) c += A.idx[k] != i;
-        return c;
-    };
-    // chunks: each depth cut into pieces within the staging buffers
-    std::vector<int> cptr{0}, ceptr{0};
-    std::vector<int> chunk_end(n);
-    {
-        int e = 0;
-        for (int l = 0; l < nlev; ++l) {
-            int rows = 0, ents = 0;
-            for (int q = lptr[l]; q < lptr[l + 1]; ++q) {
-                const int len = offdiag(order[q]);
-                if (rows > 0 && (rows + 1 > dev::kGsRows || ents + len > dev::kGsEnt)) {
-                    cptr.push_back(q);
-                    ceptr.push_back(e);
-                    rows = ents = 0;
-                }
-                check(len <= dev::kGsEnt, "gauss-seidel: row longer than the staging buffer");
-                ++rows;
-                ents += len;
-                e += len;
-            }
-            cptr.push_back(lptr[l + 1]);
-            ceptr.push_back(e);
-        }
-        for (size_t c = 0; c + 1 < cptr.size(); ++c)
-            for (int q = cptr[c]; q < cptr[c + 1]; ++q) chunk_end[q] = cptr[c + 1];
-    }
-    std::vector<int2> hdr(n);
-    std::vector<int> ref, sref;
-    std::vector<double> val, dinv(n);
-    ref.reserve(A.idx.size());
-    sref.reserve(A.idx.size());
-    val.reserve(A.val.size());
+    std::vector<int> len(n);
     for (int q = 0; q < n; ++q) {
         const int i = order[q];
-        hdr[q] = make_int2(i, static_cast<int>(ref.size()));
-        for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
-            const int c = A.idx[k];
-            if (c == i) continue;
-            const bool updated = backward ? c > i : c < i;
-            if (!updated) {
-                ref.push_back(-(2 * c + 1));
-                sref.push_back(dev::kGsRing);  // the gathered product x 1.0
-            } else {
-                ref.push_back(0);
-                // the ring slot survives until q's chunk ends, else zout[c]
-                sref.push_back(pos[c] + dev::kGsRing >= chunk_end[q] ? (pos[c] & (dev::kGsRing - 1))
-                                                                     : -(c + 2));
-            }
-            val.push_back(A.val[k]);
-        }
-        dinv[q] = inv_diag[i];
+        int c = 0;
+        for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) c += A.idx[k] != i;
+        len[q] = c;
+        check(c <= dev::kGsEnt, "gauss-seidel: row longer than the staging buffer");
     }
-    const long long nnz = static_cast<long long>(ref.size());
+    // chunks: each depth cut into pieces whose padded entries fit a buffer
+    std::vector<int> cptr{0}, width;
+    for (int l = 0; l < nlev; ++l) {
+        int rows = 0, w = 0;
+        for (int q = lptr[l]; q < lptr[l + 1]; ++q) {
+            const int w2 = std::max(w, len[q]);
+            if (rows > 0 && (rows + 1 > dev::kGsRows || static_cast<long long>(w2) * (rows + 1) > dev::kGsEnt)) {
+                cptr.push_back(q);
+                width.push_back(w);
+                rows = 0;
+                w = 0;
+            }
+            ++rows;
+            w = std::max(w, len[q]);
+        }
+        cptr.push_back(lptr[l + 1]);
+        width.push_back(w);
+    }
+    const int nch = static_cast<int>(cptr.size()) - 1;
+    std::vector<int> ceptr(nch + 1, 0), chunk_end(n);
+    for (int c = 0; c < nch; ++c) {
+        ceptr[c + 1] = ceptr[c] + width[c] * (cptr[c + 1] - cptr[c]);
+        for (int q = cptr[c]; q < cptr[c + 1]; ++q) chunk_end[q] = cptr[c + 1];
+    }
+    const long long nnz = ceptr[nch];
+    std::vector<int2> hdr(n);
+    // padding entries: value 0, gather code 0, the ring's 1.0 slot (never summed)
+    std::vector<int> ref(std::max<long long>(nnz, 1), 0), sref(std::max<long long>(nnz, 1), dev::kGsRing);
+    std::vector<double> val(std::max<long long>(nnz, 1), 0.0), dinv(n);
     long long far = 0;
-    for (int v : sref) far += v < 0;
-    if (ref.empty()) {  // a diagonal level: keep the entry arrays non-null
-        ref.push_back(0);
-        sref.push_back(dev::kGsRing);
-        val.push_back(0.0);
+    for (int c = 0; c < nch; ++c) {
+        const int nr = cptr[c + 1] - cptr[c];
+        for (int q = cptr[c]; q < cptr[c + 1]; ++q) {
+            const int i = order[q];
+            hdr[q] = make_int2(i, len[q]);
+            dinv[q] = inv_diag[i];
+            int k = 0;
+            for (int kk = A.ptr[i]; kk < A.ptr[i + 1]; ++kk) {
+                const int col = A.idx[kk];
+                if (col == i) continue;
+                const long long e = ceptr[c] + static_cast<long long>(k) * nr + (q - cptr[c]);
+                const bool updated = backward ? col > i : col < i;
+                if (!updated) {
+                    ref[e] = -(2 * col + 1);
+                    sref[e] = dev::kGsRing;  // the gathered product x 1.0
+                } else if (pos[col] + dev::kGsRing >= chunk_end[q]) {
+                    // the ring slot survives until q's chunk ends
+                    sref[e] = pos[col] & (dev::kGsRing - 1);
+                } else {
+                    sref[e] = -(col + 2);  // zout[col]
+                    ++far;
+                }
+                val[e] = A.val[kk];
+                ++k;
+            }
+        }
     }
     dev::GsSweep g;
     g.hdr = upload_array(hdr);
@@ -824,13 +826,16 @@ dev::GsSweep DeviceSolver::upload_gs(const Csr& A, const std::vector<double>& in
     g.dinv = upload_array(dinv);
     g.cptr = upload_array(cptr);
     g.ceptr = upload_array(ceptr);
-    g.nch = static_cast<int>(cptr.size()) - 1;
+    g.nch = nch;
     g.n = n;
     g.nnz = nnz;
     g.far = far > 0;
-    if (std::getenv("IRK_SETUP_TIMING"))
-        std::fprintf(stderr, "gs %s: n %d, depths %d, chunks %d, entries %lld (%lld beyond the ring)\n",
-                     backward ? "bwd" : "fwd", n, nlev, g.nch, nnz, far);
+    if (std::getenv("IRK_SETUP_TIMING")) {
+        long long real = 0;
+        for (int q = 0; q < n; ++q) real += len[q];
+        std::fprintf(stderr, "gs %s: n %d, depths %d, chunks %d, entries %lld (stored %lld), %lld beyond the ring\n",
+                     backward ? "bwd" : "fwd", n, nlev, nch, real, nnz, far);
+    }
     return g;
 }
 
@@ -1745,8 +1750,8 @@ double DeviceSolver::time_kernel(int which, int reps) {
             for (int c = 1; c < 64; ++c)
                 for (int k = 0; k < 5; ++k) a[k] += static_cast<double>(h[5 * c + k]) / 63.0;
             std::fprintf(stderr, "gs sweep L%d %s: cycles per chunk (thread 0, 63 sampled chunks, mean "
-                         "%.0f rows) after stage loads issued %.0f, compute done %.0f, staged %.0f, "
-                         "barrier %.0f\n", l, back ? "bwd" : "fwd", a[4], a[0], a[1], a[2], a[3]);
+                         "%.0f rows) phase clocks %.0f / %.0f / %.0f / %.0f (ws: chunk ready, "
+                         "rows done, consumer barrier)\n", l, back ? "bwd" : "fwd", a[4], a[0], a[1], a[2], a[3]);
         }
         return static_cast<double>(ms) / reps;
     }
