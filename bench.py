@@ -413,7 +413,7 @@ def our_arm(args):
     k_gbs = k_bytes / (kms.value * 1e-3) / 1e9
     traffic = None
     try:  # dram__bytes_read.sum + dram__bytes_write.sum of the same launch (ncu --set full)
-        traffic = json.loads((ROOT / "profiles" / "r1" / "traffic.json").read_text())["k_dgs_dot_j15"]
+        traffic = json.loads((ROOT / "profiles" / "r2" / "traffic.json").read_text())["k_dgs_dot_j15"]
     except Exception:
         pass
     # fine-level smoother: bytes it must move in its own format -- row classes
