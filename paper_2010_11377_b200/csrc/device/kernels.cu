@@ -1624,7 +1624,7 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_dot(GmresBufs g, int fin
 // w' = w - sum_i p_i v_i - h_jj v_j in one pass (element-wise order as the
 // oracle), ||w'||^2, then the provisional stop test on the first-pass column.
 template <bool COND>
-__global__ void __launch_bounds__(kRedThreads, 2) k_dgs_update(GmresBufs g) {
+__global__ void __launch_bounds__(kRedThreads, 2) k_dgs_update(GmresBufs g, int rev) {
     extern __shared__ double red[];
     pdl_trigger();
     // vt_j, w and v_0 are final before the block-dot runs: under a
@@ -1632,7 +1632,10 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_dgs_update(GmresBufs g) {
     // coefficients wait for it
     GmresCtl* ctl = g.ctl;
     const int j = *reinterpret_cast<volatile const int*>(&ctl->j);
-    const int c = blockIdx.x;
+    // rev: chunks in descending order, so the first CTAs re-read what the
+    // block-dot's last wave left in L2 (IRK_DGS_REV; chunk results do not
+    // depend on the order)
+    const int c = rev ? static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x) : static_cast<int>(blockIdx.x);
     const long long n = g.sN;
     const long long stride = (g.sN + 63) / 64 * 64;
     double* ap = g.V + static_cast<long long>(j) * stride;
@@ -2066,7 +2069,8 @@ void gm_dgs_dot(const GmresBufs& g, int finalize, cudaStream_t st) {
 
 void gm_dgs_update(const GmresBufs& g, cudaStream_t st) {
     tally(32.0 * g.sN, 8.0 * g.sN);  // reads v_0..v_{j-1}, vt_j, w; writes v_j, w': (j + 4)
-    launch(g.use_cond ? k_dgs_update<true> : k_dgs_update<false>, g.nchunks, kRedThreads, dgs_smem(g), st, g);
+    const int rev = option("IRK_DGS_REV", 1) != 0;
+    launch(g.use_cond ? k_dgs_update<true> : k_dgs_update<false>, g.nchunks, kRedThreads, dgs_smem(g), st, g, rev);
 }
 
 void gm_normalize(const GmresBufs& g, cudaStream_t st) {
