@@ -120,8 +120,14 @@ int irk_amg_setup(const irk_csr* A, const irk_amg_params* p, irk_hierarchy** out
  * Bit-identical to irk_amg_setup; IRK_ECUDA without a GPU (no fallback). */
 int irk_amg_setup_device(const irk_csr* A, const irk_amg_params* p, int device, irk_hierarchy** out);
 int irk_hierarchy_levels(const irk_hierarchy* h);
-/* which: 0 A, 1 P, 2 R (amg.hpp:35-40). */
+/* which: 0 A, 1 P, 2 R (amg.hpp:35-40); 3 G, 4 U: the composed V(1,1) legs
+ * r_{l+1} = G r_l and z_l = U [r_l; z_{l+1}] the device cycle applies on the
+ * levels above the tail (csrc/host/compose.cpp; 0 rows when not composed). */
 int irk_hierarchy_level(const irk_hierarchy* h, int level, int which, irk_csr* out);
+/* Row-sum association of the composed legs of `level`: L lanes per row (lane
+ * q adds entries q, q+L, ... in order, then an xor butterfly over the lanes);
+ * 1 = the sequential CSR row sum. */
+int irk_hierarchy_compose_lanes(const irk_hierarchy* h, int level, int* g_lanes, int* u_lanes);
 const double* irk_hierarchy_inv_diag(const irk_hierarchy* h, int level);
 const double* irk_hierarchy_coarse_inverse(const irk_hierarchy* h, int* n);
 /* The dense V-cycle tail operator attached by the setup (NULL if none):

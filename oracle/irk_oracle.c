@@ -121,6 +121,31 @@ static void spmv_epi(const or_csr* A, const double* x, const double* r, const do
     }
 }
 
+/* y = A x with the lane-tree row sum of the composed operators
+ * (k_spmv_lt, kernels.cu): lane q of L adds the products of entries q, q+L,
+ * ... in order from 0.0; the lanes are folded by the xor butterfly. */
+static void spmv_lanes(const or_csr* A, int L, const double* x, double* y) {
+    if (L <= 1) {
+        or_spmv(A, x, y);
+        return;
+    }
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < A->rows; ++i) {
+        double p[32], q[32];
+        const int lo = A->ptr[i], len = A->ptr[i + 1] - lo;
+        for (int l = 0; l < L; ++l) {
+            double acc = 0.0;
+            for (int k = l; k < len; k += L) acc = acc + A->val[lo + k] * x[A->idx[lo + k]];
+            p[l] = acc;
+        }
+        for (int o = L / 2; o > 0; o >>= 1) {
+            for (int l = 0; l < L; ++l) q[l] = p[l] + p[l ^ o];
+            memcpy(p, q, sizeof(double) * L);
+        }
+        y[i] = p[0];
+    }
+}
+
 /* ------------------------------------------------------------ V-cycle */
 /* z = B r in k_tail_mv's order (kernels.cu, kTailWarps = 4): per row, 128
  * thread partials -- thread t adds the pairs p = t, t+128, ... (B[2p] r[2p],
@@ -211,6 +236,21 @@ static void vcycle_level(const or_hier* h, double** wd, int l, const double* r, 
         return;
     }
     const int nc = h->A[l + 1].rows;
+    if (h->G && h->U && h->G[l].rows > 0 && h->pre == 1 && h->post == 1) {
+        /* composed level (the device's record_vcycle, solver.cu): the down
+         * leg and the up leg are one sparse product each, every row summed
+         * with the operator's lane tree; the up leg's operand is
+         * [r_l; z_{l+1}] */
+        double* x = (double*)malloc(sizeof(double) * (n + nc));
+        double* rc2 = (double*)malloc(sizeof(double) * nc);
+        memcpy(x, r, sizeof(double) * n);
+        spmv_lanes(&h->G[l], h->g_lanes ? h->g_lanes[l] : 1, r, rc2);
+        vcycle_level(h, wd, l + 1, rc2, x + n);
+        spmv_lanes(&h->U[l], h->u_lanes ? h->u_lanes[l] : 1, x, z);
+        free(x);
+        free(rc2);
+        return;
+    }
     double* t = (double*)malloc(sizeof(double) * n);
     double* zp = NULL;
     double* rc = (double*)malloc(sizeof(double) * nc);

@@ -30,6 +30,16 @@ typedef struct {
     int tail_from, tail_ld;
     const double* tail;
     int smoother;      /* 0 damped Jacobi, 1 Gauss-Seidel (amg.cpp:125-140) */
+    /* composed Jacobi V(1,1) legs (the product's setup, csrc/host/compose.cpp):
+     * on a level l with G[l].rows > 0 the cycle is r_{l+1} = G_l r_l going
+     * down and z_l = U_l [r_l; z_{l+1}] coming up; NULL = recursive form */
+    const or_csr* G;   /* nlev - 1 */
+    const or_csr* U;   /* nlev - 1 */
+    /* row-sum association of G[l], U[l] (part of their definition): L lanes,
+     * lane q adds entries q, q+L, ... of the row in order from 0.0, then the
+     * xor butterfly L/2, ..., 1 folds the lanes; 1 = sequential */
+    const int* g_lanes;
+    const int* u_lanes;
 } or_hier;
 
 typedef struct {

@@ -220,8 +220,14 @@ class AmgHierarchy:
 
     def level(self, l: int, which: str = "A") -> CsrMatrix:
         v = _abi.irk_csr()
-        check(_abi.lib().irk_hierarchy_level(self._h, l, {"A": 0, "P": 1, "R": 2}[which], C.byref(v)))
+        check(_abi.lib().irk_hierarchy_level(self._h, l, {"A": 0, "P": 1, "R": 2, "G": 3, "U": 4}[which], C.byref(v)))
         return CsrMatrix.from_view(v)
+
+    def compose_lanes(self, l: int) -> tuple[int, int]:
+        """Row-sum lanes (G, U) of level l's composed legs (csrc/host/compose.cpp)."""
+        g, u = C.c_int(), C.c_int()
+        check(_abi.lib().irk_hierarchy_compose_lanes(self._h, l, C.byref(g), C.byref(u)))
+        return g.value, u.value
 
     def inv_diag(self, l: int) -> np.ndarray:
         n = self.level(l).n_rows

@@ -72,6 +72,7 @@ _SIGS = {
     "irk_amg_setup_device": (C.c_int, [C.POINTER(irk_csr), C.POINTER(irk_amg_params), C.c_int, C.POINTER(V)]),
     "irk_hierarchy_levels": (C.c_int, [V]),
     "irk_hierarchy_level": (C.c_int, [V, C.c_int, C.c_int, C.POINTER(irk_csr)]),
+    "irk_hierarchy_compose_lanes": (C.c_int, [V, C.c_int, iptr, iptr]),
     "irk_hierarchy_inv_diag": (dptr, [V, C.c_int]),
     "irk_hierarchy_coarse_inverse": (dptr, [V, iptr]),
     "irk_hierarchy_free": (None, [V]),
@@ -199,6 +200,8 @@ def csr_view(rp: np.ndarray, ci: np.ndarray, v: np.ndarray, n_cols: int | None =
 
 def csr_arrays(view: irk_csr):
     n, nnz = view.n_rows, view.nnz
+    if n == 0 or not view.row_ptr:  # an absent operator (e.g. a level without composed legs)
+        return np.zeros(1, np.int32), np.zeros(0, np.int32), np.zeros(0), view.n_cols
     rp = np.ctypeslib.as_array(view.row_ptr, (n + 1,)).copy()
     ci = np.ctypeslib.as_array(view.col_idx, (max(nnz, 1),))[:nnz].copy() if nnz else np.zeros(0, np.int32)
     v = np.ctypeslib.as_array(view.vals, (max(nnz, 1),))[:nnz].copy() if nnz else np.zeros(0)

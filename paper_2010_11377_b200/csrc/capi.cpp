@@ -279,7 +279,16 @@ int irk_hierarchy_level(const irk_hierarchy* h, int level, int which, irk_csr* o
     return guard([&] {
         irkb::check(level >= 0 && level < h->h.n_levels(), "hierarchy: level out of range");
         const irkb::AmgLevel& L = h->h.levels[level];
-        view(which == 0 ? L.A : which == 1 ? L.P : L.R, out);
+        irkb::check(which >= 0 && which <= 4, "hierarchy: which must be 0..4");
+        view(which == 0 ? L.A : which == 1 ? L.P : which == 2 ? L.R : which == 3 ? L.G : L.U, out);
+    });
+}
+
+int irk_hierarchy_compose_lanes(const irk_hierarchy* h, int level, int* g_lanes, int* u_lanes) {
+    return guard([&] {
+        irkb::check(level >= 0 && level < h->h.n_levels(), "hierarchy: level out of range");
+        *g_lanes = h->h.levels[level].g_lanes;
+        *u_lanes = h->h.levels[level].u_lanes;
     });
 }
 

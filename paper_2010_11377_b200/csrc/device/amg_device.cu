@@ -744,7 +744,7 @@ Hierarchy amg_setup_device(const Csr& A, const AmgParams& p, int device) {
             fine.P = S.download(P);
             fine.R = S.download(R);
             DA<double> dc = S.inverse_diagonal(Ac);
-            h.levels.push_back({S.download(Ac), S.download(dc, Ac.rows), {}, {}});
+            h.levels.push_back({S.download(Ac), S.download(dc, Ac.rows), {}, {}, {}, {}});
             clk.lap("download", lv);
             Af = std::move(Ac);
             dinv = std::move(dc);
@@ -752,6 +752,7 @@ Hierarchy amg_setup_device(const Csr& A, const AmgParams& p, int device) {
     }
     h.coarse_inverse = dense_inverse_host(h.levels.back().A);
     attach_tail(h, tail_max_rows());
+    attach_composed(h);
     clk.lap("coarse inv", h.n_levels() - 1);
     return h;
 }

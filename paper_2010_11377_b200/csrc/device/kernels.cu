@@ -354,12 +354,14 @@ __global__ void __launch_bounds__(256) k_spmv_sell(Mat A, SpmvArgs a) {
     const double* r = a.r.base ? a.r.get() : nullptr;
     const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
     const double* __restrict__ wd = a.wd;
+    // kXSplit: x2 rebased so that both halves are indexed by the column
+    const double* x2s = XM == kXSplit ? a.x2.get() - a.split : nullptr;
     double s = 0.0;
 #pragma unroll
     for (int k = 0; k < kPre; ++k)
         if (k < len) {
             const int c = c0[k];
-            const double xv = XM == kXWdR ? wd[c] * r[c] : x[c];
+            const double xv = XM == kXWdR ? wd[c] * r[c] : XM == kXSplit ? (c < a.split ? x : x2s)[c] : x[c];
             s += v0[k] * xv;
         }
 #ifndef IRK_SELL_UNROLL
@@ -369,7 +371,7 @@ __global__ void __launch_bounds__(256) k_spmv_sell(Mat A, SpmvArgs a) {
 #pragma unroll kUnroll
     for (int k = kPre; k < len; ++k) {
         const int c = __ldg(A.idx + base + k * 32 + lane);
-        const double xv = XM == kXWdR ? wd[c] * r[c] : x[c];
+        const double xv = XM == kXWdR ? wd[c] * r[c] : XM == kXSplit ? (c < a.split ? x : x2s)[c] : x[c];
         s += vfetch<VF>(A.val, base + k * 32 + lane, tab) * xv;
     }
     const int row = slice * 32 + lane;
@@ -423,6 +425,7 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
     const double* r = a.r.base ? a.r.get() : nullptr;
     const double* __restrict__ x = a.x.base ? a.x.get() : nullptr;
     const double* __restrict__ wd = a.wd;
+    const double* x2s = XM == kXSplit ? a.x2.get() - a.split : nullptr;
     double s = 0.0;
     for (int ch = 0; ch < chunks; ++ch) {
         double p[MM];
@@ -432,7 +435,8 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
             p[m] = 0.0;
             if (k < len) {
                 const int c = ch == 0 ? c0[m] : __ldg(A.idx + lo + k);
-                const double xv = XM == kXWdR ? wd[c] * r[c] : x[c];
+                const double xv =
+                    XM == kXWdR ? wd[c] * r[c] : XM == kXSplit ? (c < a.split ? x : x2s)[c] : x[c];
                 p[m] = (ch == 0 ? v0[m] : vfetch<VF>(A.val, lo + k, tab)) * xv;
             }
         }
@@ -455,21 +459,322 @@ __global__ void __launch_bounds__(256) k_spmv_csrv(Mat A, SpmvArgs a) {
     if (a.late) pdl_trigger();
 }
 
+
+// Raw stored value of an entry (fp64, or the code that is decoded through
+// the dictionary one pipeline stage later).
+template <int VF> struct RawVal { using type = unsigned; };
+template <> struct RawVal<kF64> { using type = double; };
+
+template <int VF>
+__device__ __forceinline__ typename RawVal<VF>::type raw_fetch(const void* v, long long k) {
+    if constexpr (VF == kF64)
+        return __ldg(static_cast<const double*>(v) + k);
+    else if constexpr (VF == kU8)
+        return __ldg(static_cast<const unsigned char*>(v) + k);
+    else
+        return __ldg(static_cast<const unsigned short*>(v) + k);
+}
+template <int VF>
+__device__ __forceinline__ double raw_decode(typename RawVal<VF>::type r, const double* tab) {
+    if constexpr (VF == kF64)
+        return r;
+    else
+        return __ldg(tab + r);
+}
+
+// Lane-tree CSR: L lanes per row; lane q adds the products of the row's
+// entries q, q+L, q+2L, ... in order from 0.0, then the xor butterfly
+// L/2, ..., 1 folds the lanes.  The association is part of the composed
+// operators' definition (compose.cpp); oracle/irk_oracle.c:spmv_lanes
+// restates it.
+//
+// Persistent and software-pipelined: the grid is one wave of resident CTAs,
+// every lane group walks rows g, g + G, g + 2G, ...; while the operand gathers
+// and dictionary decodes of row i are in flight, the column indices and raw
+// values of row i+1 and the row pointers of row i+2 are loaded, so a row
+// costs one memory round trip instead of the three dependent ones of a
+// thread-per-row launch (pointer -> index -> operand).  MM entries per lane
+// are staged per row (rows longer than L*MM finish in an unpipelined loop).
+template <int XM, int VF, int L, int MM>
+__global__ void __launch_bounds__(256, 4) k_spmv_lt(Mat A, SpmvArgs a) {
+    using Raw = typename RawVal<VF>::type;
+    if (!a.late) pdl_trigger();
+    const double* tab = A.tab;
+    const int n = A.rows;
+    const int stride = gridDim.x * (256 / L);
+    const int lane = threadIdx.x % L;
+    int row = (blockIdx.x * 256 + threadIdx.x) / L;
+    int lo = 0, len = 0, lo1 = 0, len1 = 0;
+    if (row < n) {
+        lo = __ldg(A.ptr + row);
+        len = __ldg(A.ptr + row + 1) - lo;
+    }
+    if (row + stride < n) {
+        lo1 = __ldg(A.ptr + row + stride);
+        len1 = __ldg(A.ptr + row + stride + 1) - lo1;
+    }
+    int c[MM];
+    Raw v[MM];
+#pragma unroll
+    for (int m = 0; m < MM; ++m) {
+        const int k = m * L + lane;
+        c[m] = 0;
+        v[m] = Raw(0);
+        if (k < len) {
+            c[m] = __ldg(A.idx + lo + k);
+            v[m] = raw_fetch<VF>(A.val, lo + k);
+        }
+    }
+    pdl_wait();
+    const double* __restrict__ x = a.x.get();
+    const double* x2s = XM == kXSplit ? a.x2.get() - a.split : nullptr;
+    double* __restrict__ y = a.y.get();
+    while (__any_sync(0xffffffffu, row < n)) {
+        // two rows ahead: row pointers
+        int lo2 = 0, len2 = 0;
+        if (row + 2 * stride < n && row + 2 * stride > 0) {
+            lo2 = __ldg(A.ptr + row + 2 * stride);
+            len2 = __ldg(A.ptr + row + 2 * stride + 1) - lo2;
+        }
+        // one row ahead: indices and raw values
+        int cn[MM];
+        Raw vn[MM];
+#pragma unroll
+        for (int m = 0; m < MM; ++m) {
+            const int k = m * L + lane;
+            cn[m] = 0;
+            vn[m] = Raw(0);
+            if (k < len1) {
+                cn[m] = __ldg(A.idx + lo1 + k);
+                vn[m] = raw_fetch<VF>(A.val, lo1 + k);
+            }
+        }
+        // this row: decode, gather, sum
+        double xv[MM], vv[MM];
+#pragma unroll
+        for (int m = 0; m < MM; ++m) {
+            xv[m] = 0.0;
+            vv[m] = 0.0;
+            if (m * L + lane < len) {
+                vv[m] = raw_decode<VF>(v[m], tab);
+                xv[m] = XM == kXSplit ? (c[m] < a.split ? x : x2s)[c[m]] : x[c[m]];
+            }
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int m = 0; m < MM; ++m)
+            if (m * L + lane < len) s += vv[m] * xv[m];
+        for (int k = MM * L + lane; k < len; k += L) {
+            const int cc = __ldg(A.idx + lo + k);
+            const double xx = XM == kXSplit ? (cc < a.split ? x : x2s)[cc] : x[cc];
+            s += raw_decode<VF>(raw_fetch<VF>(A.val, lo + k), tab) * xx;
+        }
+#pragma unroll
+        for (int o = L / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (row < n && lane == 0) y[row] = s;
+        // rotate the pipeline
+        row += stride;
+        lo = lo1;
+        len = len1;
+        lo1 = lo2;
+        len1 = len2;
+#pragma unroll
+        for (int m = 0; m < MM; ++m) {
+            c[m] = cn[m];
+            v[m] = vn[m];
+        }
+    }
+    if (a.late) pdl_trigger();
+}
+
+// Composed up leg of a 7-point level: y_i = (S x)_i + (Q x2)_i in one
+// sequential row sum, S as row classes (dominant class from the kernel
+// parameters for uniform warps), Q as SELL-32.  Persistent and pipelined like
+// k_spmv_lt: a warp walks the slices w, w + W, ...; while the stencil loads,
+// operand gathers and decodes of one slice are in flight, the next slice's
+// class bytes, column indices and raw values and the slice offsets two ahead
+// are loaded.
+template <int VF>
+__global__ void __launch_bounds__(256, 3) k_up_cls(Mat S, Mat Q, SpmvArgs a) {
+    using Raw = typename RawVal<VF>::type;
+    if (!a.late) pdl_trigger();
+    const double* tab = Q.tab;
+    const int n = S.rows;
+    const int nslices = (n + 31) >> 5;
+    const int stride = gridDim.x * 8;  // warps in the grid
+    const int lane = threadIdx.x & 31;
+    int slice = blockIdx.x * 8 + (threadIdx.x >> 5);
+    constexpr int kPre = 7;
+    const unsigned char* __restrict__ clsp = static_cast<const unsigned char*>(S.val);
+    int base = 0, len = 0, base1 = 0, len1 = 0;
+    if (slice < nslices) {
+        base = __ldg(Q.sptr + slice);
+        len = (__ldg(Q.sptr + slice + 1) - base) >> 5;
+    }
+    if (slice + stride < nslices) {
+        base1 = __ldg(Q.sptr + slice + stride);
+        len1 = (__ldg(Q.sptr + slice + stride + 1) - base1) >> 5;
+    }
+    int c[kPre];
+    Raw v[kPre];
+    unsigned cls = 0;
+    {
+        const int i = min(slice * 32 + lane, n - 1);
+        if (slice < nslices) cls = __ldg(clsp + i);
+#pragma unroll
+        for (int k = 0; k < kPre; ++k) {
+            c[k] = 0;
+            v[k] = Raw(0);
+            if (k < len) {
+                c[k] = __ldg(Q.idx + base + k * 32 + lane);
+                v[k] = raw_fetch<VF>(Q.val, base + k * 32 + lane);
+            }
+        }
+    }
+    pdl_wait();
+    const double* __restrict__ x = a.x.get();
+    const double* __restrict__ z = a.x2.get();
+    double* __restrict__ y = a.y.get();
+    while (slice < nslices) {  // warp-uniform
+        int base2 = 0, len2 = 0;
+        if (slice + 2 * stride < nslices) {
+            base2 = __ldg(Q.sptr + slice + 2 * stride);
+            len2 = (__ldg(Q.sptr + slice + 2 * stride + 1) - base2) >> 5;
+        }
+        int cn[kPre];
+        Raw vn[kPre];
+        unsigned clsn = 0;
+        if (slice + stride < nslices) clsn = __ldg(clsp + min((slice + stride) * 32 + lane, n - 1));
+#pragma unroll
+        for (int k = 0; k < kPre; ++k) {
+            cn[k] = 0;
+            vn[k] = Raw(0);
+            if (k < len1) {
+                cn[k] = __ldg(Q.idx + base1 + k * 32 + lane);
+                vn[k] = raw_fetch<VF>(Q.val, base1 + k * 32 + lane);
+            }
+        }
+        const int row = slice * 32 + lane;
+        const int i = min(row, n - 1);
+        double ov[7];
+#pragma unroll
+        for (int d = 0; d < 7; ++d) ov[d] = x[min(max(i + S.off[d], 0), n - 1)];
+        double zv[kPre], qv[kPre];
+#pragma unroll
+        for (int k = 0; k < kPre; ++k) {
+            zv[k] = 0.0;
+            qv[k] = 0.0;
+            if (k < len) {
+                qv[k] = raw_decode<VF>(v[k], tab);
+                zv[k] = z[c[k]];
+            }
+        }
+        double s = 0.0;
+        if (__all_sync(0xffffffffu, cls == static_cast<unsigned>(S.dom))) {
+#pragma unroll
+            for (int d = 0; d < 7; ++d) s += S.dom_tab[d] * ov[d];
+        } else {
+#pragma unroll
+            for (int d = 0; d < 7; ++d) s += __ldg(S.tab + cls * 7 + d) * ov[d];
+        }
+#pragma unroll
+        for (int k = 0; k < kPre; ++k)
+            if (k < len) s += qv[k] * zv[k];
+        for (int k = kPre; k < len; ++k) {
+            const int cc = __ldg(Q.idx + base + k * 32 + lane);
+            s += raw_decode<VF>(raw_fetch<VF>(Q.val, base + k * 32 + lane), tab) * z[cc];
+        }
+        if (row < n) y[row] = s;
+        slice += stride;
+        base = base1;
+        len = len1;
+        base1 = base2;
+        len1 = len2;
+        cls = clsn;
+#pragma unroll
+        for (int k = 0; k < kPre; ++k) {
+            c[k] = cn[k];
+            v[k] = vn[k];
+        }
+    }
+    if (a.late) pdl_trigger();
+}
+
+// Resident CTAs of a persistent kernel on this device (cached per kernel).
+template <class K>
+int persistent_blocks(K kernel, int want) {
+    static thread_local std::map<const void*, int> cache;
+    const void* key = reinterpret_cast<const void*>(kernel);
+    auto it = cache.find(key);
+    int per_sm = 0;
+    if (it == cache.end()) {
+        int dev_id = 0, sms = 148;
+        IRK_CUDA_CHECK(cudaGetDevice(&dev_id));
+        IRK_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev_id));
+        IRK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0));
+        per_sm = std::max(per_sm, 1) * sms;
+        cache[key] = per_sm;
+    } else {
+        per_sm = it->second;
+    }
+    return std::max(1, std::min(want, per_sm));
+}
+
+template <int XM, int VF, int L>
+void launch_lt_mm(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
+    const int want = blocks_for(static_cast<long long>(A.rows) * L, 256);
+    // entries staged per lane: the stored hint (upload: p95 row length / L)
+    const int mm = A.tree <= 4 ? 4 : A.tree >= 6 ? 6 : 5;
+    if (mm == 4)
+        launch(k_spmv_lt<XM, VF, L, 4>, persistent_blocks(k_spmv_lt<XM, VF, L, 4>, want), 256, 0, st, A, a);
+    else if (mm == 5)
+        launch(k_spmv_lt<XM, VF, L, 5>, persistent_blocks(k_spmv_lt<XM, VF, L, 5>, want), 256, 0, st, A, a);
+    else
+        launch(k_spmv_lt<XM, VF, L, 6>, persistent_blocks(k_spmv_lt<XM, VF, L, 6>, want), 256, 0, st, A, a);
+}
+
+template <int XM, int VF>
+void launch_lt(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
+    switch (A.lanes) {
+    case 2: launch_lt_mm<XM, VF, 2>(A, a, st); break;
+    case 4: launch_lt_mm<XM, VF, 4>(A, a, st); break;
+    case 8: launch_lt_mm<XM, VF, 8>(A, a, st); break;
+    case 16: launch_lt_mm<XM, VF, 16>(A, a, st); break;
+    case 32: launch_lt_mm<XM, VF, 32>(A, a, st); break;
+    default: throw InvalidArgument("spmv: lane-tree operators need 2..32 lanes");
+    }
+}
+
+template <int XM>
+void launch_lt_vf(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
+    if (A.rows == 0) return;
+    switch (A.vf) {
+    case kU8: launch_lt<XM, kU8>(A, a, st); break;
+    case kU16: launch_lt<XM, kU16>(A, a, st); break;
+    case kF64: launch_lt<XM, kF64>(A, a, st); break;
+    default: throw InvalidArgument("spmv: lane-tree operators store fp64 values or codes");
+    }
+}
+
 template <int XM, int EPI, int VF>
 void launch_spmv_vf(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
     if (A.fmt == kDia) {
-        const int nb = blocks_for(A.rows, 256);
-        const bool wdt = VF == kU8 && A.wdtab && A.diag0 >= 0;
-        if (A.nd == 7) {
-            if (wdt)
-                launch(k_spmv_dia<XM, EPI, VF, 1, 7>, nb, 256, 0, st, A, a);
-            else
-                launch(k_spmv_dia<XM, EPI, VF, 0, 7>, nb, 256, 0, st, A, a);
+        if constexpr (XM == kXSplit) {
+            throw InvalidArgument("spmv: a split operand needs a SELL or CSR-vector operator");
         } else {
-            if (wdt)
-                launch(k_spmv_dia<XM, EPI, VF, 1, 0>, nb, 256, 0, st, A, a);
-            else
-                launch(k_spmv_dia<XM, EPI, VF, 0, 0>, nb, 256, 0, st, A, a);
+            const int nb = blocks_for(A.rows, 256);
+            const bool wdt = VF == kU8 && A.wdtab && A.diag0 >= 0;
+            if (A.nd == 7) {
+                if (wdt)
+                    launch(k_spmv_dia<XM, EPI, VF, 1, 7>, nb, 256, 0, st, A, a);
+                else
+                    launch(k_spmv_dia<XM, EPI, VF, 0, 7>, nb, 256, 0, st, A, a);
+            } else {
+                if (wdt)
+                    launch(k_spmv_dia<XM, EPI, VF, 1, 0>, nb, 256, 0, st, A, a);
+                else
+                    launch(k_spmv_dia<XM, EPI, VF, 0, 0>, nb, 256, 0, st, A, a);
+            }
         }
     } else if (A.fmt == kCsrVec) {
         const int nb = blocks_for(static_cast<long long>(A.rows) * A.lanes, 256);
@@ -495,7 +800,9 @@ void launch_spmv(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
     case kCls:
         // DIA row classes (7 diagonals)
         if (A.fmt != kDia || A.nd != 7) throw InvalidArgument("row classes need a 7-diagonal DIA operator");
-        if (A.dom >= 0 && (A.nbwd || XM != kXWdR) && option("IRK_DOM_CLASS", 1) != 0) {
+        if constexpr (XM == kXSplit) {
+            throw InvalidArgument("spmv: a split operand needs a SELL or CSR-vector operator");
+        } else if (A.dom >= 0 && (A.nbwd || XM != kXWdR) && option("IRK_DOM_CLASS", 1) != 0) {
             if (A.wdtab)
                 launch(k_spmv_cls<XM, EPI, 1>, blocks_for(A.rows, 256), 256, 0, st, A, a);
             else
@@ -1886,6 +2193,15 @@ void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a_in, cudaStream_t s
     if (A.rows > 0) tally(spmv_bytes(A, xmode, epi, a_in));
     SpmvArgs a = a_in;
     a.late = g_pdl_late && !g_pdl_scope ? 1 : 0;
+    if (A.tree) {
+        if (epi != kEPlain || (xmode != kXPlain && xmode != kXSplit) || A.fmt != kCsrVec)
+            throw InvalidArgument("spmv: a lane-tree operator is a plain product");
+        if (xmode == kXSplit)
+            launch_lt_vf<kXSplit>(A, a, st);
+        else
+            launch_lt_vf<kXPlain>(A, a, st);
+        return;
+    }
 #define IRK_SPMV_CASE(X, E)                         \
     if (xmode == X && epi == E) {                   \
         launch_spmv<X, E>(A, a, st);                \
@@ -1897,8 +2213,23 @@ void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a_in, cudaStream_t s
     IRK_SPMV_CASE(kXPlain, kEProlong)
     IRK_SPMV_CASE(kXWdR, kEResid)
     IRK_SPMV_CASE(kXWdR, kEPlain)
+    IRK_SPMV_CASE(kXSplit, kEPlain)
 #undef IRK_SPMV_CASE
     throw InvalidArgument("spmv: unsupported mode combination");
+}
+
+void up_cls(const Mat& S, const Mat& Q, const SpmvArgs& a_in, cudaStream_t st) {
+    if (S.vf != kCls || S.fmt != kDia || S.nd != 7 || S.dom < 0 || Q.fmt != kSell || Q.rows != S.rows)
+        throw InvalidArgument("up_cls: S must be 7-diagonal row classes and Q SELL-32 over the same rows");
+    tally(mat_bytes(S) + mat_bytes(Q) + 8.0 * (S.cols + Q.cols) + 8.0 * S.rows);
+    SpmvArgs a = a_in;
+    a.late = g_pdl_late && !g_pdl_scope ? 1 : 0;
+    const int want = blocks_for(S.rows, 256);
+    switch (Q.vf) {
+    case kU8: launch(k_up_cls<kU8>, persistent_blocks(k_up_cls<kU8>, want), 256, 0, st, S, Q, a); break;
+    case kU16: launch(k_up_cls<kU16>, persistent_blocks(k_up_cls<kU16>, want), 256, 0, st, S, Q, a); break;
+    default: launch(k_up_cls<kF64>, persistent_blocks(k_up_cls<kF64>, want), 256, 0, st, S, Q, a); break;
+    }
 }
 
 void stage_op_dia(const Mat& M, const Mat& K, const StageCoef& c, VecRef z, VecRef y, int n,

@@ -44,6 +44,13 @@ struct Mat {
     // accumulated in column order through warp shuffles
     const int* ptr = nullptr;   // row offsets, rows + 1
     int lanes = 1;
+    // lane-tree row sums (the composed V-cycle operators, compose.cpp): each
+    // of the `lanes` lanes adds its strided entries in order, then an xor
+    // butterfly folds the lanes (k_spmv_lt) -- part of the operator's
+    // definition, restated by the oracle.  0: not a lane-tree operator; else the
+    // entries staged per lane and row by the pipelined kernel (4..6, a tuning
+    // hint: about the 95th percentile row length / lanes)
+    int tree = 0;
     // values (both formats): f64 / u8 / u16 per stored entry
     const void* val = nullptr;
     const double* tab = nullptr;  // code dictionary (vf != kF64)
@@ -72,7 +79,10 @@ struct Mat {
 
 // x operand of an SpMV: either a plain vector or the implicit Jacobi
 // pre-smoothed iterate wd .* r (never materialised).
-enum XMode { kXPlain = 0, kXWdR = 1 };
+// kXSplit (SELL / CSR-vector only): the operand is the concatenation
+// [x (split entries); x2] of two vectors -- the composed up leg
+// z_l = [S_l Q_l] [r_l; z_{l+1}] (csrc/host/compose.cpp).
+enum XMode { kXPlain = 0, kXWdR = 1, kXSplit = 2 };
 // Row epilogue applied to s = (A x)_i.
 enum Epi {
     kEPlain = 0,    // y = s
@@ -83,6 +93,8 @@ enum Epi {
 
 struct SpmvArgs {
     VecRef x{};                  // plain x (kXPlain)
+    VecRef x2{};                 // kXSplit: columns >= split read x2[col - split]
+    int split = 0;
     VecRef r{};                  // residual / rhs vector
     const double* wd = nullptr;  // omega * D^-1
     const double* zb = nullptr;  // prolong base (nullptr -> wd .* r)
@@ -121,6 +133,11 @@ void set_pdl_scope(bool on);
 void set_pdl_late(bool on);
 
 void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a, cudaStream_t st);
+// Composed up leg on a 7-point fine level: y = S x + Q x2, S stored as DIA row
+// classes and Q as SELL-32, one thread per row, the row summed sequentially
+// (S's diagonals in ascending offset order, then Q's entries in column order
+// -- the CSR order of U = [S | Q]).
+void up_cls(const Mat& S, const Mat& Q, const SpmvArgs& a, cudaStream_t st);
 
 // Tuning switches: a runtime override (irk_set_option) or the environment
 // variable of the same name, else `dflt`.  Read when a graph is recorded;

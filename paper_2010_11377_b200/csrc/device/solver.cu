@@ -324,11 +324,81 @@ bool DeviceSolver::to_row_classes(std::vector<dev::Mat*> mats, const std::vector
 
 // DIA when the pattern is <= 16 diagonals with <= 15% padding; else SELL-32.
 // `omega` > 0 requests the omega/diag dictionary (hierarchy operators).
-dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
+bool DeviceSolver::upload_up_cls(const Csr& U, int n, dev::Mat& Sm, dev::Mat& Qm) {
+    if (!row_classes_enabled() || dev::option("IRK_UP_CLS", 1) == 0 || U.rows != n || U.cols <= n) return false;
+    Csr S, Q;
+    S.rows = S.cols = n;
+    Q.rows = n;
+    Q.cols = U.cols - n;
+    S.ptr.assign(n + 1, 0);
+    Q.ptr.assign(n + 1, 0);
+    for (int i = 0; i < n; ++i) {
+        int ns = 0;
+        for (int k = U.ptr[i]; k < U.ptr[i + 1]; ++k) ns += U.idx[k] < n ? 1 : 0;
+        S.ptr[i + 1] = S.ptr[i] + ns;
+        Q.ptr[i + 1] = Q.ptr[i] + (U.ptr[i + 1] - U.ptr[i] - ns);
+    }
+    S.idx.resize(S.ptr[n]);
+    S.val.resize(S.ptr[n]);
+    Q.idx.resize(Q.ptr[n]);
+    Q.val.resize(Q.ptr[n]);
+    for (int i = 0; i < n; ++i) {
+        int os = S.ptr[i], oq = Q.ptr[i];
+        for (int k = U.ptr[i]; k < U.ptr[i + 1]; ++k) {
+            if (U.idx[k] < n) {
+                S.idx[os] = U.idx[k];
+                S.val[os++] = U.val[k];
+            } else {
+                Q.idx[oq] = U.idx[k] - n;
+                Q.val[oq++] = U.val[k];
+            }
+        }
+    }
+    const DiaLayout L = dia_layout(S);
+    if (L.offs.size() != 7) return false;
+    dev::Mat m;
+    m.rows = m.cols = n;
+    m.nnz = S.nnz();
+    m.fmt = dev::kDia;
+    m.dstride = L.ds;
+    m.nd = 7;
+    for (int d = 0; d < 7; ++d) {
+        m.off[d] = L.offs[d];
+        if (L.offs[d] == 0) m.diag0 = d;
+    }
+    if (!to_row_classes({&m}, {&L.v}, 0.0)) return false;
+    Sm = m;
+    Qm = upload(Q, false, 0.0, 1);
+    return true;
+}
+
+dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega, int tree_lanes) {
     dev::Mat m;
     m.rows = A.rows;
     m.cols = A.cols;
     m.nnz = A.nnz();
+    if (tree_lanes >= 2) {
+        m.fmt = dev::kCsrVec;
+        m.lanes = tree_lanes;
+        {
+            // staged entries per lane: covers the 95th percentile row length
+            std::vector<int> lens(A.rows);
+            for (int i = 0; i < A.rows; ++i) lens[i] = A.ptr[i + 1] - A.ptr[i];
+            int p95 = 0;
+            if (!lens.empty()) {
+                const size_t q = lens.size() * 95 / 100;
+                std::nth_element(lens.begin(), lens.begin() + q, lens.end());
+                p95 = lens[q];
+            }
+            const int mm = (p95 + tree_lanes - 1) / tree_lanes;
+            m.tree = static_cast<int>(dev::option("IRK_LT_MM", std::min(std::max(mm, 4), 6)));
+        }
+        m.ptr = upload_array(A.ptr);
+        m.idx = upload_array(A.idx);
+        m.bytes += sizeof(int) * (A.ptr.size() + A.idx.size());
+        upload_values(m, A.val, omega);
+        return m;
+    }
     DiaLayout L;
     if (allow_dia) L = dia_layout(A);
     if (!L.offs.empty()) {
@@ -367,7 +437,8 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega) {
     static const double big_avg =
         std::getenv("IRK_CSRV_BIG_AVG") ? std::atof(std::getenv("IRK_CSRV_BIG_AVG")) : 24.0;
     const long long sell_min_rows = dev::option("IRK_SELL_MIN_ROWS", 65536);
-    if ((force < 0 && avg > 4.5 && (A.rows < sell_min_rows || avg > big_avg)) || force == dev::kCsrVec) {
+    if (tree_lanes != 1 &&
+        ((force < 0 && avg > 4.5 && (A.rows < sell_min_rows || avg > big_avg)) || force == dev::kCsrVec)) {
         // entries per lane (tenths; IRK_CSRV_PER_LANE10, default 30 = 3.0)
         const double per_lane = 0.1 * static_cast<double>(dev::option("IRK_CSRV_PER_LANE10", 30));
         int g = 2;
@@ -519,6 +590,11 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
             if (l + 1 < L) {
                 d.P = upload(lev.P, false, 0.0);
                 d.R = upload(lev.R, false, 0.0);
+                if (lev.G.rows > 0 && lev.U.rows > 0) {
+                    d.G = upload(lev.G, false, 0.0, lev.g_lanes);
+                    d.up_cls = lev.u_lanes == 1 && upload_up_cls(lev.U, d.n, d.US, d.UQ);
+                    if (!d.up_cls) d.U = upload(lev.U, false, 0.0, lev.u_lanes);
+                }
             }
             d.t = alloc(d.n);
             d.u = alloc(d.n);
@@ -917,8 +993,11 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
     // levels >= bot run in the single-CTA bottom kernel
     // levels >= tail are one dense matvec (IRK_TAIL=0: the recursive cycle)
     const int tail = dev::option("IRK_TAIL", 1) != 0 && H.tail_from > first ? H.tail_from : -1;
+    // composed levels (compose.cpp): one kernel down (r_{l+1} = G r_l), one up
+    // (z_l = U [r_l; z_{l+1}]); a composed hierarchy has no bottom kernel
+    auto composed = [&](int l) { return pre == 1 && post == 1 && H.lv[l].G.rows > 0; };
     const int bot = tail < 0 && dev::option("IRK_BOTTOM", 1) != 0 && H.bot_from > first && pre == 1 &&
-                            post == 1
+                            post == 1 && !composed(first)
                         ? H.bot_from : -1;
     const int down_end = tail > 0 ? tail : bot > 0 ? bot : L - 1;
     for (int l = first; l < down_end; ++l) {
@@ -927,6 +1006,13 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
         // the cycle's first kernel: programmatic only after a late-trigger
         // kernel (a block sweep), not after one that triggers at its start
         if (l == first && !vc_pdl_first_) dev::set_pdl_late(false);
+        if (composed(l)) {
+            dev::SpmvArgs ga;
+            ga.x = rhs_of(l);
+            ga.y = dev::plain(H.lv[l + 1].r);
+            dev::spmv(d.G, dev::kXPlain, dev::kEPlain, ga, st_);
+            continue;
+        }
         dev::SpmvArgs a;
         a.r = rhs_of(l);
         a.wd = d.wd;
@@ -977,6 +1063,18 @@ void DeviceSolver::record_vcycle(int k, VecRef r0, VecRef z0, int first) {
     for (int l = (tail > 0 ? tail - 1 : bot > 0 ? bot - 1 : L - 2); l >= first; --l) {
         DevLevel& d = H.lv[l];
         scope(l);
+        if (composed(l)) {
+            dev::SpmvArgs ua;
+            ua.x = rhs_of(l);
+            ua.x2 = dev::plain(H.lv[l + 1].z);
+            ua.split = d.n;
+            ua.y = out_of(l);
+            if (d.up_cls)
+                dev::up_cls(d.US, d.UQ, ua, st_);
+            else
+                dev::spmv(d.U, dev::kXSplit, dev::kEPlain, ua, st_);
+            continue;
+        }
         dev::SpmvArgs pa;
         pa.x = dev::plain(H.lv[l + 1].z);
         pa.r = rhs_of(l);

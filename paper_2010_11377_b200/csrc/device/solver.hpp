@@ -53,6 +53,9 @@ struct SolveReport {
 struct DevLevel {
     int n = 0;
     dev::Mat A, P, R;
+    dev::Mat G, U;                // composed V(1,1) legs (compose.cpp); G.rows == 0: recursive level
+    dev::Mat US, UQ;              // up leg of a 7-point level: S as row classes, Q as SELL-32
+    bool up_cls = false;          // (U itself is then not stored)
     double* wd = nullptr;         // omega * D^-1
     double* r = nullptr;          // level rhs (levels >= 1)
     double* z = nullptr;          // level solution (levels >= 1)
@@ -145,7 +148,11 @@ public:
     int graph_mode() const { return graph_mode_; }
 
 private:
-    dev::Mat upload(const Csr& A, bool allow_dia, double omega);
+    // tree_lanes: 0 format by heuristics; 1 SELL-32 (sequential row sums);
+    // >= 2 CSR with lane-tree row sums (composed operators)
+    dev::Mat upload(const Csr& A, bool allow_dia, double omega, int tree_lanes = 0);
+    // U = [S | Q] of a 7-point level as row classes + SELL-32 (false: not that shape)
+    bool upload_up_cls(const Csr& U, int n, dev::Mat& S, dev::Mat& Q);
     void build_bottom(DevHier& dh, const Hierarchy& h);
     // DIA row classes (dev::kCls) for one operator or a pair sharing a pattern
     bool to_row_classes(std::vector<dev::Mat*> mats, const std::vector<const std::vector<double>*>& vals,

@@ -149,7 +149,7 @@ Hierarchy amg_setup(const Csr& A, const AmgParams& p) {
 
     Hierarchy h;
     h.params = p;
-    h.levels.push_back({A, inverse_diagonal(A), {}, {}});
+    h.levels.push_back({A, inverse_diagonal(A), {}, {}, {}, {}});
     while (h.levels.back().A.rows > p.max_coarse && h.n_levels() < p.max_levels) {
         AmgLevel& fine = h.levels.back();
         const int n = fine.A.rows;
@@ -179,10 +179,11 @@ Hierarchy amg_setup(const Csr& A, const AmgParams& p) {
         fine.R = transpose(fine.P);
         Csr Ac = matmul(fine.R, matmul(fine.A, fine.P));
         std::vector<double> dinv = inverse_diagonal(Ac);
-        h.levels.push_back({std::move(Ac), std::move(dinv), {}, {}});
+        h.levels.push_back({std::move(Ac), std::move(dinv), {}, {}, {}, {}});
     }
     h.coarse_inverse = dense_inverse_host(h.levels.back().A);
     attach_tail(h, tail_max_rows());
+    attach_composed(h);
     return h;
 }
 

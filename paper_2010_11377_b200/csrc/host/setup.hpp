@@ -89,6 +89,15 @@ struct AmgLevel {
     Csr A;
     std::vector<double> inv_diag;
     Csr P, R;  // empty on the coarsest level
+    // Composed Jacobi V(1,1) legs (compose.cpp): r_{l+1} = G r_l going down,
+    // z_l = U [r_l; z_{l+1}] coming up (U = [S | Q], Q's columns offset by
+    // A.rows); empty when the level is not composed.
+    Csr G, U;
+    // Row-sum association of G and U (part of their definition, shared with
+    // the oracle): L lanes, lane q adds the row's entries q, q+L, q+2L, ...
+    // in order from 0.0, then the lanes are folded by the xor butterfly
+    // L/2, ..., 1.  L = 1 is the sequential CSR row sum.
+    int g_lanes = 1, u_lanes = 1;
 };
 
 struct Hierarchy {
@@ -110,6 +119,11 @@ Hierarchy amg_setup(const Csr& A, const AmgParams& p);
 // 0 disables).
 void attach_tail(Hierarchy& h, int max_n);
 int tail_max_rows();
+// Attaches the composed operators G_l, U_l of every level above the tail (or
+// the coarsest level) for damped-Jacobi V(1,1) hierarchies (compose.cpp);
+// amg_setup and amg_setup_device call it after attach_tail.  IRK_COMPOSE=0
+// in the environment disables it.
+void attach_composed(Hierarchy& h);
 // Dense inverse of the coarsest operator (Gauss-Jordan, partial pivoting).
 std::vector<double> dense_inverse_host(const Csr& A);
 

@@ -340,7 +340,8 @@ class or_hier(C.Structure):
                 ("R", C.POINTER(or_csr)), ("inv_diag", C.POINTER(dptr)), ("cinv", dptr),
                 ("nc", C.c_int), ("omega", C.c_double), ("pre", C.c_int), ("post", C.c_int),
                 ("tail_from", C.c_int), ("tail_ld", C.c_int), ("tail", dptr),
-                ("smoother", C.c_int)]
+                ("smoother", C.c_int), ("G", C.POINTER(or_csr)), ("U", C.POINTER(or_csr)),
+                ("g_lanes", iptr), ("u_lanes", iptr)]
 
 
 class or_sys(C.Structure):
@@ -415,10 +416,20 @@ class OracleSystem:
             tail_from, tail = h.get("tail", (-1, None))
             tl = None if tail is None else np.ascontiguousarray(tail, np.float64)
             self._keep.append(tl)
+            Garr = Uarr = gl = ul = None
+            if h.get("G") and any(len(g[0]) > 1 for g in h["G"]):
+                gl = np.ascontiguousarray([x[0] for x in h["lanes"]], np.int32)
+                ul = np.ascontiguousarray([x[1] for x in h["lanes"]], np.int32)
+                self._keep.extend([gl, ul])
+                # composed legs (csrc/host/compose.cpp); rows = 0 where absent
+                Garr = (or_csr * max(L - 1, 1))(*[csr(g[:3], g[3]) for g in h["G"]])
+                Uarr = (or_csr * max(L - 1, 1))(*[csr(u[:3], u[3]) for u in h["U"]])
+                self._keep.extend([Garr, Uarr])
             hs.append(or_hier(L, Aarr, Parr, Rarr, idp, _d(cinv), int(round(np.sqrt(cinv.size))),
                               h["omega"], h["pre"], h["post"], tail_from,
                               0 if tl is None else tl.shape[1], None if tl is None else _d(tl),
-                              int(h.get("smoother", 0))))
+                              int(h.get("smoother", 0)), Garr, Uarr,
+                              None if gl is None else _i(gl), None if ul is None else _i(ul)))
         harr = (or_hier * len(hs))(*hs)
         arrs = [np.ascontiguousarray(x, np.float64).ravel() for x in (A, b, At)]
         sobv = np.ascontiguousarray(sob, np.int32)
@@ -479,8 +490,8 @@ def oracle_dot(x, y):
 def hierarchy_dict(h, omega=2.0 / 3.0, pre=1, post=1, smoother=0):
     """Product AmgHierarchy -> oracle hierarchy dict."""
     L = h.n_levels()
-    d = {"A": [], "P": [], "R": [], "inv_diag": [], "omega": omega, "pre": pre, "post": post,
-         "smoother": smoother}
+    d = {"A": [], "P": [], "R": [], "G": [], "U": [], "inv_diag": [], "omega": omega, "pre": pre,
+         "post": post, "smoother": smoother, "lanes": []}
     for l in range(L):
         a = h.level(l, "A")
         d["A"].append((a.row_ptr, a.col_idx, a.vals, a.n_cols))
@@ -489,6 +500,10 @@ def hierarchy_dict(h, omega=2.0 / 3.0, pre=1, post=1, smoother=0):
             p, r = h.level(l, "P"), h.level(l, "R")
             d["P"].append((p.row_ptr, p.col_idx, p.vals, p.n_cols))
             d["R"].append((r.row_ptr, r.col_idx, r.vals, r.n_cols))
+            g, u = h.level(l, "G"), h.level(l, "U")
+            d["G"].append((g.row_ptr, g.col_idx, g.vals, g.n_cols))
+            d["U"].append((u.row_ptr, u.col_idx, u.vals, u.n_cols))
+            d["lanes"].append(h.compose_lanes(l))
     d["cinv"] = h.coarse_inverse()
     d["tail"] = h.tail()
     return d
