@@ -425,6 +425,17 @@ def our_arm(args):
     _abi.check(L.irkdev_level_value_format(dev._h, 0, 0, C.byref(vf0)))
     s_fmt = "row classes" if vf0.value == 3 else "u8 value codes"
     s_bytes = (1 + 8 + 8 + 8) * n if vf0.value == 3 else (7 + 8 + 8 + 1 + 8) * n
+    # the composed V-cycle's level-0 legs (the V-cycle's two biggest kernels):
+    # algorithmic bytes from the kernel's own tally (operands once, stored formats)
+    legs = {}
+    for which, name in ((7, "down leg r_1 = G_0 r_0"), (8, "up leg z_0 = [S_0 Q_0][r_0; z_1]")):
+        lms, lb = C.c_double(), C.c_double()
+        if L.irkdev_time_kernel(dev._h, which, 200, C.byref(lms)) != 0:
+            break  # recursive (uncomposed) hierarchy
+        _abi.check(L.irkdev_last_timed_bytes(dev._h, C.byref(lb)))
+        legs[name] = {"bytes_per_launch": lb.value, "ms_per_launch": lms.value,
+                      "achieved_gbs": lb.value / (lms.value * 1e-3) / 1e9,
+                      "frac": lb.value / (lms.value * 1e-3) / 1e9 / hbm_peak}
     # whole-solve byte models on the actual hierarchies and iterations
     nnz_mk = prob.M.nnz
     mb = (C.c_double * 8)()
@@ -470,10 +481,12 @@ def our_arm(args):
                      "traffic": traffic, "bytes_per_launch": k_bytes, "ms_per_launch": kms.value,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in pk
                      else "fallback 6650 GB/s (B200_PROFILING.md)"},
-        "smoother_roofline": {"kernel": f"fine-level Jacobi smoother k_spmv_dia (DIA, {s_fmt})",
+        "smoother_roofline": {"kernel": f"fine-level Jacobi smoother k_spmv_dia (DIA, {s_fmt}); on the product path only "
+                                        "for recursive hierarchies (IRK_COMPOSE=0, V(pre,post) != V(1,1))",
                               "bytes_per_launch": s_bytes, "ms_per_launch": sms.value,
                               "achieved_gbs": s_bytes / (sms.value * 1e-3) / 1e9,
                               "frac": s_bytes / (sms.value * 1e-3) / 1e9 / hbm_peak},
+        "vcycle_level0_roofline": legs,
         "solve_roofline": {
             "frac": (meas or {}).get("frac", fmt_gbs / hbm_peak),
             "basis": "measured DRAM traffic" if meas else "format model",

@@ -240,9 +240,13 @@ int irkdev_dot(irkdev* d, const double* x, const double* y, long long n, double*
 /* Roofline hook: mean ms per launch of a hot kernel, CUDA events on the
  * solver stream.  which: 0 stage operator, 1 fine smoother SpMV,
  * 2 preconditioner apply, 3 V-cycle, 4+l V-cycle below level l+1,
+ * 7 / 8 the composed level-0 down / up leg of hierarchy 0 alone,
  * 100+j GMRES block-dot at inner index j, 20 / 21 empty-kernel launch
  * floor in a graph / on the stream. */
 int irkdev_time_kernel(irkdev* d, int which, int reps, double* ms);
+/* Algorithmic bytes (operands once, in their stored formats) of one
+ * application of the phase last timed with which < 20. */
+int irkdev_last_timed_bytes(const irkdev* d, double* bytes);
 /* Kernel launches per GMRES iteration in the captured graph body, and the
  * graph mode (1 conditional WHILE nodes, 0 host-driven). */
 int irkdev_graph_info(const irkdev* d, int* launches_per_iteration, int* graph_mode);

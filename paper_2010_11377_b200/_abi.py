@@ -111,6 +111,7 @@ _SIGS = {
     "irkdev_vcycle": (C.c_int, [V, C.c_int, dptr, dptr]),
     "irkdev_dot": (C.c_int, [V, dptr, dptr, C.c_longlong, dptr]),
     "irkdev_time_kernel": (C.c_int, [V, C.c_int, C.c_int, dptr]),
+    "irkdev_last_timed_bytes": (C.c_int, [V, dptr]),
     "irkdev_graph_info": (C.c_int, [V, iptr, iptr]),
     "irkdev_launch_counts": (C.c_int, [V, iptr]),
     "irkdev_model_bytes": (C.c_int, [V, dptr]),

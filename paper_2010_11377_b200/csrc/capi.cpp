@@ -568,6 +568,10 @@ int irkdev_time_kernel(irkdev* d, int which, int reps, double* ms) {
     return guard([&] { *ms = d->s->time_kernel(which, reps); });
 }
 
+int irkdev_last_timed_bytes(const irkdev* d, double* bytes) {
+    return guard([&] { *bytes = d->s->last_timed_bytes(); });
+}
+
 int irkdev_launch_counts(const irkdev* d, int* c) {
     return guard([&] {
         const auto& v = d->s->launch_counts();

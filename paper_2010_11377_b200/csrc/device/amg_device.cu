@@ -751,7 +751,7 @@ Hierarchy amg_setup_device(const Csr& A, const AmgParams& p, int device) {
         }
     }
     h.coarse_inverse = dense_inverse_host(h.levels.back().A);
-    attach_tail(h, tail_max_rows());
+    attach_tail(h, tail_max_rows(h.params));
     attach_composed(h);
     clk.lap("coarse inv", h.n_levels() - 1);
     return h;

@@ -83,6 +83,8 @@ void tally_close() { g_tally = nullptr; }
 double mat_bytes(const Mat& A) {
     const double vb = A.vf == kF64 ? 8.0 : A.vf == kU16 ? 2.0 : 1.0;
     if (A.fmt == kDia) return A.vf == kCls ? static_cast<double>(A.rows) : static_cast<double>(A.nd) * A.rows * vb;
+    if (A.fmt == kRowSig)  // id + base column(s) per row, the signature table once
+        return static_cast<double>(A.rows) * (A.rs_base1 ? 10.0 : 6.0) + static_cast<double>(A.rs_n) * (4.0 + 12.0 * A.rs_w);
     const double rowstruct = A.fmt == kCsrVec ? 4.0 * (A.rows + 1) : 4.0 * ((A.rows + 31) / 32 + 1);
     return static_cast<double>(A.nnz) * (4.0 + vb) + rowstruct;
 }
@@ -700,6 +702,163 @@ __global__ void __launch_bounds__(256, 3) k_up_cls(Mat S, Mat Q, SpmvArgs a) {
     if (a.late) pdl_trigger();
 }
 
+// Lane-tree product of a row-signature operator (RSIG): same row sums as
+// k_spmv_lt on the CSR form (lane q adds entries q, q+L, ... in order, xor
+// butterfly), but a row costs its signature id and base columns (6-10 bytes)
+// instead of 5-12 bytes per entry; offsets and values come from the
+// signature table (L1-resident, shared by all rows of a signature).
+// Persistent and pipelined: the next row's id and bases are loaded while this
+// row's table reads and operand gathers are in flight.
+template <int XM, int L>
+__global__ void __launch_bounds__(256) k_spmv_rs(Mat A, SpmvArgs a) {
+    if (!a.late) pdl_trigger();
+    const int n = A.rows;
+    const int stride = gridDim.x * (256 / L);
+    const int lane = threadIdx.x % L;
+    int row = (blockIdx.x * 256 + threadIdx.x) / L;
+    unsigned sig = 0, sig1 = 0;
+    int b0 = 0, b1 = 0, b0n = 0, b1n = 0;
+    if (row < n) {
+        sig = __ldg(A.rs_sig + row);
+        b0 = __ldg(A.rs_base0 + row);
+        if (XM == kXSplit) b1 = __ldg(A.rs_base1 + row);
+    }
+    if (row + stride < n) {
+        sig1 = __ldg(A.rs_sig + row + stride);
+        b0n = __ldg(A.rs_base0 + row + stride);
+        if (XM == kXSplit) b1n = __ldg(A.rs_base1 + row + stride);
+    }
+    pdl_wait();
+    const double* __restrict__ x = a.x.get();
+    const double* __restrict__ x2 = XM == kXSplit ? a.x2.get() : nullptr;
+    double* __restrict__ y = a.y.get();
+    constexpr int MM = 4;
+    while (__any_sync(0xffffffffu, row < n)) {
+        unsigned sig2 = 0;
+        int b02 = 0, b12 = 0;
+        if (row + 2 * stride < n) {
+            sig2 = __ldg(A.rs_sig + row + 2 * stride);
+            b02 = __ldg(A.rs_base0 + row + 2 * stride);
+            if (XM == kXSplit) b12 = __ldg(A.rs_base1 + row + 2 * stride);
+        }
+        const int len = row < n ? __ldg(A.rs_len + sig) : 0;
+        const int tb = sig * A.rs_w;
+        double s = 0.0;
+        for (int k0 = 0; k0 < len; k0 += MM * L) {
+            int off[MM];
+            double v[MM], xv[MM];
+#pragma unroll
+            for (int m = 0; m < MM; ++m) {
+                const int k = k0 + m * L + lane;
+                off[m] = 0;
+                v[m] = 0.0;
+                if (k < len) {
+                    off[m] = __ldg(A.rs_off + tb + k);
+                    v[m] = __ldg(A.rs_val + tb + k);
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < MM; ++m) {
+                xv[m] = 0.0;
+                if (k0 + m * L + lane < len) {
+                    if (XM == kXSplit && (off[m] & kRsQ))
+                        xv[m] = x2[b1 + (off[m] & ~kRsQ)];
+                    else
+                        xv[m] = x[b0 + off[m]];
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < MM; ++m)
+                if (k0 + m * L + lane < len) s += v[m] * xv[m];
+        }
+#pragma unroll
+        for (int o = L / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (row < n && lane == 0) y[row] = s;
+        row += stride;
+        sig = sig1;
+        b0 = b0n;
+        b1 = b1n;
+        sig1 = sig2;
+        b0n = b02;
+        b1n = b12;
+    }
+    if (a.late) pdl_trigger();
+}
+
+// k_up_cls with Q as row signatures: per row one S class byte, one Q
+// signature id and one base column.
+__global__ void __launch_bounds__(256, 4) k_up_cls_rs(Mat S, Mat Q, SpmvArgs a) {
+    if (!a.late) pdl_trigger();
+    const int n = S.rows;
+    const int stride = gridDim.x * 256;
+    int row = blockIdx.x * 256 + threadIdx.x;
+    const unsigned char* __restrict__ clsp = static_cast<const unsigned char*>(S.val);
+    unsigned cls = 0, sig = 0, clsn = 0, sign = 0;
+    int b = 0, bn = 0;
+    if (row < n) {
+        cls = __ldg(clsp + row);
+        sig = __ldg(Q.rs_sig + row);
+        b = __ldg(Q.rs_base0 + row);
+    }
+    if (row + stride < n) {
+        clsn = __ldg(clsp + row + stride);
+        sign = __ldg(Q.rs_sig + row + stride);
+        bn = __ldg(Q.rs_base0 + row + stride);
+    }
+    pdl_wait();
+    const double* __restrict__ x = a.x.get();
+    const double* __restrict__ z = a.x2.get();
+    double* __restrict__ y = a.y.get();
+    constexpr int kPre = 8;
+    while (__any_sync(0xffffffffu, row < n)) {
+        unsigned cls2 = 0, sig2 = 0;
+        int b2 = 0;
+        if (row + 2 * stride < n) {
+            cls2 = __ldg(clsp + row + 2 * stride);
+            sig2 = __ldg(Q.rs_sig + row + 2 * stride);
+            b2 = __ldg(Q.rs_base0 + row + 2 * stride);
+        }
+        const bool live = row < n;
+        const int i = live ? row : n - 1;
+        double ov[7];
+#pragma unroll
+        for (int d = 0; d < 7; ++d) ov[d] = x[min(max(i + S.off[d], 0), n - 1)];
+        const int len = live ? __ldg(Q.rs_len + sig) : 0;
+        const int tb = sig * Q.rs_w;
+        double qv[kPre], zv[kPre];
+#pragma unroll
+        for (int k = 0; k < kPre; ++k) {
+            qv[k] = 0.0;
+            zv[k] = 0.0;
+            if (k < len) {
+                qv[k] = __ldg(Q.rs_val + tb + k);
+                zv[k] = z[b + __ldg(Q.rs_off + tb + k)];
+            }
+        }
+        double s = 0.0;
+        if (__all_sync(0xffffffffu, cls == static_cast<unsigned>(S.dom))) {
+#pragma unroll
+            for (int d = 0; d < 7; ++d) s += S.dom_tab[d] * ov[d];
+        } else {
+#pragma unroll
+            for (int d = 0; d < 7; ++d) s += __ldg(S.tab + cls * 7 + d) * ov[d];
+        }
+#pragma unroll
+        for (int k = 0; k < kPre; ++k)
+            if (k < len) s += qv[k] * zv[k];
+        for (int k = kPre; k < len; ++k) s += __ldg(Q.rs_val + tb + k) * z[b + __ldg(Q.rs_off + tb + k)];
+        if (live) y[row] = s;
+        row += stride;
+        cls = clsn;
+        sig = sign;
+        b = bn;
+        clsn = cls2;
+        sign = sig2;
+        bn = b2;
+    }
+    if (a.late) pdl_trigger();
+}
+
 // Resident CTAs of a persistent kernel on this device (cached per kernel).
 template <class K>
 int persistent_blocks(K kernel, int want) {
@@ -746,8 +905,25 @@ void launch_lt(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
 }
 
 template <int XM>
+void launch_rs(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
+    const int want = blocks_for(static_cast<long long>(A.rows) * A.lanes, 256);
+    switch (A.lanes) {
+    case 2: launch(k_spmv_rs<XM, 2>, persistent_blocks(k_spmv_rs<XM, 2>, want), 256, 0, st, A, a); break;
+    case 4: launch(k_spmv_rs<XM, 4>, persistent_blocks(k_spmv_rs<XM, 4>, want), 256, 0, st, A, a); break;
+    case 8: launch(k_spmv_rs<XM, 8>, persistent_blocks(k_spmv_rs<XM, 8>, want), 256, 0, st, A, a); break;
+    case 16: launch(k_spmv_rs<XM, 16>, persistent_blocks(k_spmv_rs<XM, 16>, want), 256, 0, st, A, a); break;
+    case 32: launch(k_spmv_rs<XM, 32>, persistent_blocks(k_spmv_rs<XM, 32>, want), 256, 0, st, A, a); break;
+    default: throw InvalidArgument("spmv: lane-tree operators need 2..32 lanes");
+    }
+}
+
+template <int XM>
 void launch_lt_vf(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
     if (A.rows == 0) return;
+    if (A.fmt == kRowSig) {
+        launch_rs<XM>(A, a, st);
+        return;
+    }
     switch (A.vf) {
     case kU8: launch_lt<XM, kU8>(A, a, st); break;
     case kU16: launch_lt<XM, kU16>(A, a, st); break;
@@ -2194,7 +2370,7 @@ void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a_in, cudaStream_t s
     SpmvArgs a = a_in;
     a.late = g_pdl_late && !g_pdl_scope ? 1 : 0;
     if (A.tree) {
-        if (epi != kEPlain || (xmode != kXPlain && xmode != kXSplit) || A.fmt != kCsrVec)
+        if (epi != kEPlain || (xmode != kXPlain && xmode != kXSplit) || (A.fmt != kCsrVec && A.fmt != kRowSig))
             throw InvalidArgument("spmv: a lane-tree operator is a plain product");
         if (xmode == kXSplit)
             launch_lt_vf<kXSplit>(A, a, st);
@@ -2219,12 +2395,17 @@ void spmv(const Mat& A, int xmode, int epi, const SpmvArgs& a_in, cudaStream_t s
 }
 
 void up_cls(const Mat& S, const Mat& Q, const SpmvArgs& a_in, cudaStream_t st) {
-    if (S.vf != kCls || S.fmt != kDia || S.nd != 7 || S.dom < 0 || Q.fmt != kSell || Q.rows != S.rows)
-        throw InvalidArgument("up_cls: S must be 7-diagonal row classes and Q SELL-32 over the same rows");
+    if (S.vf != kCls || S.fmt != kDia || S.nd != 7 || S.dom < 0 || (Q.fmt != kSell && Q.fmt != kRowSig) ||
+        Q.rows != S.rows)
+        throw InvalidArgument("up_cls: S must be 7-diagonal row classes and Q SELL-32 or RSIG over the same rows");
     tally(mat_bytes(S) + mat_bytes(Q) + 8.0 * (S.cols + Q.cols) + 8.0 * S.rows);
     SpmvArgs a = a_in;
     a.late = g_pdl_late && !g_pdl_scope ? 1 : 0;
     const int want = blocks_for(S.rows, 256);
+    if (Q.fmt == kRowSig) {
+        launch(k_up_cls_rs, persistent_blocks(k_up_cls_rs, want), 256, 0, st, S, Q, a);
+        return;
+    }
     switch (Q.vf) {
     case kU8: launch(k_up_cls<kU8>, persistent_blocks(k_up_cls<kU8>, want), 256, 0, st, S, Q, a); break;
     case kU16: launch(k_up_cls<kU16>, persistent_blocks(k_up_cls<kU16>, want), 256, 0, st, S, Q, a); break;

@@ -10,6 +10,7 @@ namespace irkb {
 namespace dev {
 
 constexpr int kMaxDiags = 16;
+constexpr int kRsQ = 1 << 30;  // RSIG offset flag: second operand
 
 // Device matrix formats.  Both keep the reference's per-row summation order
 // (column-ascending, sequential), so results are bit-identical to a CSR row
@@ -25,7 +26,13 @@ constexpr int kMaxDiags = 16;
 // Values are fp64 or, when the matrix has few distinct values, uint8 /
 // uint16 codes into an exact fp64 dictionary (lossless; e.g. 3 distinct
 // values in the fine-level stencils, 14 in the fine prolongator).
-enum MatFmt { kSell = 0, kDia = 1, kCsrVec = 2 };
+//   RSIG -- row signatures (composed operators on structured grids): rows
+//           whose column offsets (relative to the row's first column; for a
+//           split operand relative to the first column of each half) and
+//           fp64 values are identical share one signature, stored once; a
+//           row is its signature id and its base column(s).  Lossless; the
+//           row sums keep the lane-tree order of the CSR form.
+enum MatFmt { kSell = 0, kDia = 1, kCsrVec = 2, kRowSig = 3 };
 // kCls (DIA with 7 diagonals only): one u8 row class per row; rows of one
 // class have the identical stencil, stored once in tab[class * nd + d]
 // (lossless: a class is a distinct tuple of fp64 bit patterns).  On the
@@ -51,6 +58,16 @@ struct Mat {
     // entries staged per lane and row by the pipelined kernel (4..6, a tuning
     // hint: about the 95th percentile row length / lanes)
     int tree = 0;
+    // RSIG: per row the signature id and base columns; per signature its
+    // length and `rs_w` slots of (offset, value); an offset with kRsQ set is
+    // relative to base1 and addresses the second operand (x2) of a split product
+    const unsigned short* rs_sig = nullptr;
+    const int* rs_base0 = nullptr;
+    const int* rs_base1 = nullptr;
+    const int* rs_len = nullptr;
+    const int* rs_off = nullptr;
+    const double* rs_val = nullptr;
+    int rs_w = 0, rs_n = 0;
     // values (both formats): f64 / u8 / u16 per stored entry
     const void* val = nullptr;
     const double* tab = nullptr;  // code dictionary (vf != kF64)

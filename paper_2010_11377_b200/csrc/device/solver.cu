@@ -324,6 +324,108 @@ bool DeviceSolver::to_row_classes(std::vector<dev::Mat*> mats, const std::vector
 
 // DIA when the pattern is <= 16 diagonals with <= 15% padding; else SELL-32.
 // `omega` > 0 requests the omega/diag dictionary (hierarchy operators).
+bool DeviceSolver::upload_rowsig(const Csr& A, int lanes, int split, dev::Mat& out) {
+    // IRK_ROW_SIG bit mask: 1 the Q part of a 7-point up leg (k_up_cls_rs; the
+    // default -- U0 20.0 -> 17.8 us at C2), 2 the down legs G, 4 the split up
+    // legs (both measured slower than the pipelined CSR form: their table reads
+    // are one more dependent level per row; profiles/r2/ab_composed_vcycle.txt)
+    const long long mask = dev::option("IRK_ROW_SIG", 1);
+    const long long need = lanes < 2 ? 1 : split > 0 ? 4 : 2;
+    if ((mask & need) == 0 || A.rows == 0) return false;
+    const int n = A.rows;
+    const int cut = split > 0 ? split : A.cols;  // columns >= cut: second operand
+    std::vector<unsigned short> sig(n);
+    std::vector<int> base0(n, 0), base1(n, 0);
+    // signature store: offsets and value bits of each distinct row, in first-seen order
+    std::vector<int> sptr{0}, soff;
+    std::vector<uint64_t> sval;
+    std::unordered_map<uint64_t, std::vector<int>> by_hash;
+    std::vector<int> ro;
+    std::vector<uint64_t> rv;
+    const size_t max_sigs = std::min<size_t>(65535, static_cast<size_t>(n) / 4 + 1);
+    int prev = -1;
+    for (int i = 0; i < n; ++i) {
+        const int lo = A.ptr[i], hi = A.ptr[i + 1];
+        int b0 = -1, b1 = -1;
+        for (int k = lo; k < hi; ++k) {
+            if (A.idx[k] < cut) {
+                if (b0 < 0) b0 = A.idx[k];
+            } else if (b1 < 0) {
+                b1 = A.idx[k] - cut;
+            }
+        }
+        base0[i] = std::max(b0, 0);
+        base1[i] = std::max(b1, 0);
+        ro.resize(hi - lo);
+        rv.resize(hi - lo);
+        uint64_t h = 1469598103934665603ULL;
+        for (int k = lo; k < hi; ++k) {
+            const int c = A.idx[k];
+            const int o = c < cut ? c - base0[i] : ((c - cut - base1[i]) | dev::kRsQ);
+            uint64_t b;
+            std::memcpy(&b, &A.val[k], sizeof(b));
+            ro[k - lo] = o;
+            rv[k - lo] = b;
+            h = (h ^ static_cast<uint64_t>(static_cast<unsigned>(o))) * 1099511628211ULL;
+            h = (h ^ b) * 1099511628211ULL;
+        }
+        auto same = [&](int c) {
+            return sptr[c + 1] - sptr[c] == hi - lo && std::equal(ro.begin(), ro.end(), soff.begin() + sptr[c]) &&
+                   std::equal(rv.begin(), rv.end(), sval.begin() + sptr[c]);
+        };
+        int c = -1;
+        if (prev >= 0 && same(prev)) {
+            c = prev;
+        } else {
+            std::vector<int>& cand = by_hash[h];
+            for (int q : cand)
+                if (same(q)) c = q;
+            if (c < 0) {
+                c = static_cast<int>(sptr.size()) - 1;
+                if (static_cast<size_t>(c) >= max_sigs) return false;  // the rows do not repeat
+                soff.insert(soff.end(), ro.begin(), ro.end());
+                sval.insert(sval.end(), rv.begin(), rv.end());
+                sptr.push_back(static_cast<int>(soff.size()));
+                cand.push_back(c);
+            }
+        }
+        sig[i] = static_cast<unsigned short>(c);
+        prev = c;
+    }
+    const int ns = static_cast<int>(sptr.size()) - 1;
+    int w = 1;
+    for (int c = 0; c < ns; ++c) w = std::max(w, sptr[c + 1] - sptr[c]);
+    if (static_cast<size_t>(ns) * w * 12 > (size_t(2) << 20)) return false;  // keep the table cache-resident
+    std::vector<int> tlen(ns), toff(static_cast<size_t>(ns) * w, 0);
+    std::vector<double> tval(static_cast<size_t>(ns) * w, 0.0);
+    for (int c = 0; c < ns; ++c) {
+        tlen[c] = sptr[c + 1] - sptr[c];
+        for (int k = 0; k < tlen[c]; ++k) {
+            toff[static_cast<size_t>(c) * w + k] = soff[sptr[c] + k];
+            std::memcpy(&tval[static_cast<size_t>(c) * w + k], &sval[sptr[c] + k], sizeof(double));
+        }
+    }
+    dev::Mat m;
+    m.rows = A.rows;
+    m.cols = A.cols;
+    m.nnz = A.nnz();
+    m.fmt = dev::kRowSig;
+    m.vf = dev::kF64;
+    m.lanes = lanes;
+    m.tree = lanes >= 2 ? 4 : 0;
+    m.rs_sig = upload_array(sig);
+    m.rs_base0 = upload_array(base0);
+    m.rs_base1 = split > 0 ? upload_array(base1) : nullptr;
+    m.rs_len = upload_array(tlen);
+    m.rs_off = upload_array(toff);
+    m.rs_val = upload_array(tval);
+    m.rs_w = w;
+    m.rs_n = ns;
+    m.bytes = static_cast<size_t>(n) * (split > 0 ? 10 : 6) + static_cast<size_t>(ns) * (4 + 12 * static_cast<size_t>(w));
+    out = m;
+    return true;
+}
+
 bool DeviceSolver::upload_up_cls(const Csr& U, int n, dev::Mat& Sm, dev::Mat& Qm) {
     if (!row_classes_enabled() || dev::option("IRK_UP_CLS", 1) == 0 || U.rows != n || U.cols <= n) return false;
     Csr S, Q;
@@ -368,7 +470,7 @@ bool DeviceSolver::upload_up_cls(const Csr& U, int n, dev::Mat& Sm, dev::Mat& Qm
     }
     if (!to_row_classes({&m}, {&L.v}, 0.0)) return false;
     Sm = m;
-    Qm = upload(Q, false, 0.0, 1);
+    if (!upload_rowsig(Q, 1, 0, Qm)) Qm = upload(Q, false, 0.0, 1);
     return true;
 }
 
@@ -591,9 +693,16 @@ DeviceSolver::DeviceSolver(const Csr& M, const Csr& K, int s, const std::vector<
                 d.P = upload(lev.P, false, 0.0);
                 d.R = upload(lev.R, false, 0.0);
                 if (lev.G.rows > 0 && lev.U.rows > 0) {
-                    d.G = upload(lev.G, false, 0.0, lev.g_lanes);
+                    if (lev.g_lanes < 2 || !upload_rowsig(lev.G, lev.g_lanes, 0, d.G))
+                        d.G = upload(lev.G, false, 0.0, lev.g_lanes);
                     d.up_cls = lev.u_lanes == 1 && upload_up_cls(lev.U, d.n, d.US, d.UQ);
-                    if (!d.up_cls) d.U = upload(lev.U, false, 0.0, lev.u_lanes);
+                    if (!d.up_cls && (lev.u_lanes < 2 || !upload_rowsig(lev.U, lev.u_lanes, d.n, d.U)))
+                        d.U = upload(lev.U, false, 0.0, lev.u_lanes);
+                    if (std::getenv("IRK_SETUP_TIMING"))
+                        std::fprintf(stderr, "level %d composed: G fmt %d (%d sigs, w %d)  U %s fmt %d (%d sigs, w %d)\n", l,
+                                     d.G.fmt, d.G.rs_n, d.G.rs_w, d.up_cls ? "cls+Q" : "split",
+                                     d.up_cls ? d.UQ.fmt : d.U.fmt, d.up_cls ? d.UQ.rs_n : d.U.rs_n,
+                                     d.up_cls ? d.UQ.rs_w : d.U.rs_w);
                 }
             }
             d.t = alloc(d.n);
@@ -2014,6 +2123,27 @@ double DeviceSolver::time_kernel(int which, int reps) {
         }
         case 2: record_precond(dev::plain(a.as<double>()), dev::plain(b.as<double>())); break;
         case 3: record_vcycle(0, dev::plain(a.as<double>()), dev::plain(b.as<double>())); break;
+        case 7:
+        case 8: {
+            // the composed level-0 legs alone: r_1 = G_0 r (7), z = U_0 [r; z_1] (8)
+            DevLevel& d = hier_[0].lv[0];
+            check(d.G.rows > 0, "time_kernel: hierarchy 0 is not composed");
+            dev::SpmvArgs sa;
+            sa.x = dev::plain(a.as<double>());
+            if (which == 7) {
+                sa.y = dev::plain(hier_[0].lv[1].r);
+                dev::spmv(d.G, dev::kXPlain, dev::kEPlain, sa, st_);
+            } else {
+                sa.x2 = dev::plain(hier_[0].lv[1].z);
+                sa.split = d.n;
+                sa.y = dev::plain(b.as<double>());
+                if (d.up_cls)
+                    dev::up_cls(d.US, d.UQ, sa, st_);
+                else
+                    dev::spmv(d.U, dev::kXSplit, dev::kEPlain, sa, st_);
+            }
+            break;
+        }
         default: {  // 4, 5, ...: the V-cycle below level which-3
             const int first = std::min<int>(which - 3, static_cast<int>(hier_[0].lv.size()) - 1);
             record_vcycle(0, dev::plain(a.as<double>()), dev::plain(b.as<double>()), first);
@@ -2021,7 +2151,14 @@ double DeviceSolver::time_kernel(int which, int reps) {
         }
         }
     };
-    once();
+    {
+        // algorithmic bytes of one application (stored formats), for the roofline
+        dev::Tally t{};
+        dev::tally_open(&t);
+        once();
+        dev::tally_close();
+        last_timed_bytes_ = t.fixed;
+    }
     cudaEvent_t e0, e1;
     IRK_CUDA_CHECK(cudaEventCreate(&e0));
     IRK_CUDA_CHECK(cudaEventCreate(&e1));

@@ -139,7 +139,11 @@ public:
     // below level which-3, 100+j GMRES block-dot at inner index j, 20/21 empty-
     // kernel launch floor (graph / stream), 60+2l(+1) Gauss-Seidel forward
     // (backward) sweep of hierarchy 0 at level l.
+    // 7 / 8: the composed level-0 down / up leg of hierarchy 0 alone.
     double time_kernel(int which, int reps);
+    // algorithmic bytes (stored formats) of one application of the phase last
+    // timed through the generic path (which < 20)
+    double last_timed_bytes() const { return last_timed_bytes_; }
     int launches_per_iteration() const { return launches_per_iter_; }
     const std::array<int, 4>& launch_counts() const { return launch_counts_; }
     // Algorithmic bytes per phase (pre, cycle, iteration, post) of the last
@@ -151,6 +155,10 @@ private:
     // tree_lanes: 0 format by heuristics; 1 SELL-32 (sequential row sums);
     // >= 2 CSR with lane-tree row sums (composed operators)
     dev::Mat upload(const Csr& A, bool allow_dia, double omega, int tree_lanes = 0);
+    // Row-signature storage (dev::kRowSig) of a composed operator; `split` > 0:
+    // columns >= split address the second operand.  False when the rows do
+    // not repeat (general operators): the caller keeps the CSR form.
+    bool upload_rowsig(const Csr& A, int lanes, int split, dev::Mat& m);
     // U = [S | Q] of a 7-point level as row classes + SELL-32 (false: not that shape)
     bool upload_up_cls(const Csr& U, int n, dev::Mat& S, dev::Mat& Q);
     void build_bottom(DevHier& dh, const Hierarchy& h);
@@ -226,6 +234,7 @@ private:
     // the next recorded V-cycle's first kernel follows a late-trigger kernel
     // (a sweep) and may be launched programmatically (IRK_PDL_FINE)
     bool vc_pdl_first_ = false;
+    double last_timed_bytes_ = 0.0;
 };
 
 }  // namespace irkb

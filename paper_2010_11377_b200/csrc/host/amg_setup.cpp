@@ -182,7 +182,7 @@ Hierarchy amg_setup(const Csr& A, const AmgParams& p) {
         h.levels.push_back({std::move(Ac), std::move(dinv), {}, {}, {}, {}});
     }
     h.coarse_inverse = dense_inverse_host(h.levels.back().A);
-    attach_tail(h, tail_max_rows());
+    attach_tail(h, tail_max_rows(h.params));
     attach_composed(h);
     return h;
 }

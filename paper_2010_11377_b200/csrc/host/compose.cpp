@@ -24,7 +24,11 @@
 // Every product below is a rounded multiply and every sum a rounded add in a
 // fixed order (matmul / add of sparse.cpp), so the operators are reproducible
 // bit for bit from the hierarchy.
+#include <array>
+#include <cstdint>
 #include <cstdlib>
+#include <cstring>
+#include <set>
 #include <vector>
 
 #include "setup.hpp"
@@ -44,15 +48,17 @@ int lanes_for(const Csr& A) {
     return g;
 }
 
-// True when the square operator has at most 7 distinct diagonals (the P1
-// stencil of the structured fine grid): its up leg is summed sequentially, one
-// thread per row (the device stores S as row classes and Q as SELL-32).
-bool stencil7(const Csr& A) {
+// True when the square operator S has exactly 7 distinct diagonals (the P1
+// stencil of the structured fine grid) and at most 256 distinct row stencils
+// (tuples of the 7 fp64 bit patterns, absent entries = 0.0): the device then
+// stores S as one class byte per row, and the up leg is summed sequentially,
+// one thread per row (k_up_cls).
+bool stencil7_classes(const Csr& S) {
     int offs[8];
     int nd = 0;
-    for (int i = 0; i < A.rows; ++i)
-        for (int k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
-            const int o = A.idx[k] - i;
+    for (int i = 0; i < S.rows; ++i)
+        for (int k = S.ptr[i]; k < S.ptr[i + 1]; ++k) {
+            const int o = S.idx[k] - i;
             int q = 0;
             while (q < nd && offs[q] != o) ++q;
             if (q == nd) {
@@ -60,7 +66,20 @@ bool stencil7(const Csr& A) {
                 offs[nd++] = o;
             }
         }
-    return nd == 7;
+    if (nd != 7) return false;
+    std::set<std::array<uint64_t, 7>> seen;
+    for (int i = 0; i < S.rows; ++i) {
+        std::array<uint64_t, 7> t{};
+        for (int k = S.ptr[i]; k < S.ptr[i + 1]; ++k) {
+            const int o = S.idx[k] - i;
+            int q = 0;
+            while (offs[q] != o) ++q;
+            std::memcpy(&t[q], &S.val[k], sizeof(uint64_t));
+        }
+        seen.insert(t);
+        if (seen.size() > 256) return false;
+    }
+    return true;
 }
 
 }  // namespace
@@ -133,7 +152,7 @@ void attach_composed(Hierarchy& h) {
             }
         }
         lev.g_lanes = lanes_for(lev.G);
-        lev.u_lanes = stencil7(A) ? 1 : lanes_for(U);
+        lev.u_lanes = stencil7_classes(S) ? 1 : lanes_for(U);
     }
 }
 

@@ -115,10 +115,12 @@ struct Hierarchy {
 Hierarchy amg_setup(const Csr& A, const AmgParams& p);
 // Attaches the dense tail operator B_l for the first level l >= 1 (above the
 // coarsest) with at most max_n rows (tail.cpp); amg_setup and
-// amg_setup_device call it with tail_max_rows() (IRK_TAIL_MAX, default 3300;
+// amg_setup_device call it with tail_max_rows(params) (IRK_TAIL_MAX; default 1500
+// rows for composed hierarchies, 3300 for recursive ones;
 // 0 disables).
 void attach_tail(Hierarchy& h, int max_n);
-int tail_max_rows();
+int tail_max_rows(const AmgParams& p);
+bool compose_enabled();  // IRK_COMPOSE != 0
 // Attaches the composed operators G_l, U_l of every level above the tail (or
 // the coarsest level) for damped-Jacobi V(1,1) hierarchies (compose.cpp);
 // amg_setup and amg_setup_device call it after attach_tail.  IRK_COMPOSE=0

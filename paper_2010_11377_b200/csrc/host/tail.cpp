@@ -70,9 +70,14 @@ void vcycle_from(const Hierarchy& h, int l, const double* r, std::vector<double>
 
 }  // namespace
 
-int tail_max_rows() {
+int tail_max_rows(const AmgParams& p) {
     const char* v = std::getenv("IRK_TAIL_MAX");
-    const int n = v ? std::atoi(v) : 3300;  // B_l <= ~87 MB
+    // recursive levels (Gauss-Seidel, V(pre,post) != V(1,1), IRK_COMPOSE=0) cost
+    // 4+ dependent launches each: the tail starts at <= 3300 rows (B_l <= ~87
+    // MB); composed levels cost two cheap launches, so there the matvec only
+    // pays below 1500 rows (C2: 2205^2 -> 347^2; profiles/r2/ab_composed_vcycle.txt)
+    const bool composed = compose_enabled() && p.smoother == 0 && p.pre_sweeps == 1 && p.post_sweeps == 1;
+    const int n = v ? std::atoi(v) : composed ? 1500 : 3300;
     return n < 6000 ? n : 6000;             // k_tail_mv stages r in 48 KB of shared memory
 }
 

@@ -120,7 +120,8 @@ def test_device_cycle_bitwise_both_forms(make, compose, tail, monkeypatch):
 def test_storage_switches_are_bit_identical(env, monkeypatch):
     """The up leg as row classes + SELL or as one split SELL operator, and the
     pipelined kernel's staging depth, are storage choices: same row sums."""
-    c = heat_case(192, s=3, ht=1e-3)
+    c = heat_case(256, s=3, ht=1e-3)
+    assert c.hiers[0].compose_lanes(0)[1] == 1  # k_up_cls path (exact grid spacing: few row classes)
     r = np.random.default_rng(12).uniform(-1, 1, c.n)
     base = c.device().vcycle(0, r)
     assert np.array_equal(base, c.oracle.vcycle(0, r))
