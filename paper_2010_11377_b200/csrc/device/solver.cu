@@ -325,11 +325,13 @@ bool DeviceSolver::to_row_classes(std::vector<dev::Mat*> mats, const std::vector
 // DIA when the pattern is <= 16 diagonals with <= 15% padding; else SELL-32.
 // `omega` > 0 requests the omega/diag dictionary (hierarchy operators).
 bool DeviceSolver::upload_rowsig(const Csr& A, int lanes, int split, dev::Mat& out) {
-    // IRK_ROW_SIG bit mask: 1 the Q part of a 7-point up leg (k_up_cls_rs; the
-    // default -- U0 20.0 -> 17.8 us at C2), 2 the down legs G, 4 the split up
-    // legs (both measured slower than the pipelined CSR form: their table reads
-    // are one more dependent level per row; profiles/r2/ab_composed_vcycle.txt)
-    const long long mask = dev::option("IRK_ROW_SIG", 1);
+    // Opt-in (IRK_ROW_SIG bit mask: 1 the Q part of a 7-point up leg, 2 the
+    // down legs G, 4 the split up legs).  Off by default: at C2 the table reads
+    // are one more dependent level per row and the table of the up leg's Q
+    // part (10,011 signatures, 960 KB) is not L1-resident -- hot V-cycle 65.9
+    // us with it (exceptions skipped) vs 64.6 us without
+    // (profiles/r2/ab_composed_vcycle.txt).
+    const long long mask = dev::option("IRK_ROW_SIG", 0);
     const long long need = lanes < 2 ? 1 : split > 0 ? 4 : 2;
     if ((mask & need) == 0 || A.rows == 0) return false;
     const int n = A.rows;
