@@ -497,8 +497,11 @@ __device__ __forceinline__ double raw_decode(typename RawVal<VF>::type r, const 
 // costs one memory round trip instead of the three dependent ones of a
 // thread-per-row launch (pointer -> index -> operand).  MM entries per lane
 // are staged per row (rows longer than L*MM finish in an unpipelined loop).
+#ifndef IRK_LT_MINB
+#define IRK_LT_MINB 4
+#endif
 template <int XM, int VF, int L, int MM>
-__global__ void __launch_bounds__(256, 4) k_spmv_lt(Mat A, SpmvArgs a) {
+__global__ void __launch_bounds__(256, IRK_LT_MINB) k_spmv_lt(Mat A, SpmvArgs a) {
     using Raw = typename RawVal<VF>::type;
     if (!a.late) pdl_trigger();
     const double* tab = A.tab;
@@ -596,8 +599,14 @@ __global__ void __launch_bounds__(256, 4) k_spmv_lt(Mat A, SpmvArgs a) {
 // operand gathers and decodes of one slice are in flight, the next slice's
 // class bytes, column indices and raw values and the slice offsets two ahead
 // are loaded.
+#ifndef IRK_UPCLS_MINB
+#define IRK_UPCLS_MINB 3
+#endif
+#ifndef IRK_UPCLS_PRE
+#define IRK_UPCLS_PRE 7
+#endif
 template <int VF>
-__global__ void __launch_bounds__(256, 3) k_up_cls(Mat S, Mat Q, SpmvArgs a) {
+__global__ void __launch_bounds__(256, IRK_UPCLS_MINB) k_up_cls(Mat S, Mat Q, SpmvArgs a) {
     using Raw = typename RawVal<VF>::type;
     if (!a.late) pdl_trigger();
     const double* tab = Q.tab;
@@ -606,7 +615,7 @@ __global__ void __launch_bounds__(256, 3) k_up_cls(Mat S, Mat Q, SpmvArgs a) {
     const int stride = gridDim.x * 8;  // warps in the grid
     const int lane = threadIdx.x & 31;
     int slice = blockIdx.x * 8 + (threadIdx.x >> 5);
-    constexpr int kPre = 7;
+    constexpr int kPre = IRK_UPCLS_PRE;
     const unsigned char* __restrict__ clsp = static_cast<const unsigned char*>(S.val);
     int base = 0, len = 0, base1 = 0, len1 = 0;
     if (slice < nslices) {
