@@ -81,7 +81,7 @@ void tally_open(Tally* t) { g_tally = t; }
 void tally_close() { g_tally = nullptr; }
 
 double mat_bytes(const Mat& A) {
-    const double vb = A.vf == kF64 ? 8.0 : A.vf == kU16 ? 2.0 : 1.0;
+    const double vb = A.vf == kF64 ? 8.0 : A.vf == kU16 ? 2.0 : A.vf == kP8 ? 0.0 : 1.0;
     if (A.fmt == kDia) return A.vf == kCls ? static_cast<double>(A.rows) : static_cast<double>(A.nd) * A.rows * vb;
     if (A.fmt == kRowSig)  // id + base column(s) per row, the signature table once
         return static_cast<double>(A.rows) * (A.rs_base1 ? 10.0 : 6.0) + static_cast<double>(A.rs_n) * (4.0 + 12.0 * A.rs_w);
@@ -469,7 +469,9 @@ template <> struct RawVal<kF64> { using type = double; };
 
 template <int VF>
 __device__ __forceinline__ typename RawVal<VF>::type raw_fetch(const void* v, long long k) {
-    if constexpr (VF == kF64)
+    if constexpr (VF == kP8)
+        return 0u;  // the code is in the index word
+    else if constexpr (VF == kF64)
         return __ldg(static_cast<const double*>(v) + k);
     else if constexpr (VF == kU8)
         return __ldg(static_cast<const unsigned char*>(v) + k);
@@ -482,6 +484,19 @@ __device__ __forceinline__ double raw_decode(typename RawVal<VF>::type r, const 
         return r;
     else
         return __ldg(tab + r);
+}
+// Column and value of an entry from its index word and raw value (kP8: both
+// from the index word).
+template <int VF>
+__device__ __forceinline__ int ent_col(int w, int shift) {
+    return VF == kP8 ? static_cast<int>(static_cast<unsigned>(w) & ((1u << shift) - 1u)) : w;
+}
+template <int VF>
+__device__ __forceinline__ double ent_val(int w, typename RawVal<VF>::type r, const double* tab, int shift) {
+    if constexpr (VF == kP8)
+        return __ldg(tab + (static_cast<unsigned>(w) >> shift));
+    else
+        return raw_decode<VF>(r, tab);
 }
 
 // Lane-tree CSR: L lanes per row; lane q adds the products of the row's
@@ -561,8 +576,9 @@ __global__ void __launch_bounds__(256, IRK_LT_MINB) k_spmv_lt(Mat A, SpmvArgs a)
             xv[m] = 0.0;
             vv[m] = 0.0;
             if (m * L + lane < len) {
-                vv[m] = raw_decode<VF>(v[m], tab);
-                xv[m] = XM == kXSplit ? (c[m] < a.split ? x : x2s)[c[m]] : x[c[m]];
+                const int col = ent_col<VF>(c[m], A.pk_shift);
+                vv[m] = ent_val<VF>(c[m], v[m], tab, A.pk_shift);
+                xv[m] = XM == kXSplit ? (col < a.split ? x : x2s)[col] : x[col];
             }
         }
         double s = 0.0;
@@ -570,9 +586,10 @@ __global__ void __launch_bounds__(256, IRK_LT_MINB) k_spmv_lt(Mat A, SpmvArgs a)
         for (int m = 0; m < MM; ++m)
             if (m * L + lane < len) s += vv[m] * xv[m];
         for (int k = MM * L + lane; k < len; k += L) {
-            const int cc = __ldg(A.idx + lo + k);
+            const int w = __ldg(A.idx + lo + k);
+            const int cc = ent_col<VF>(w, A.pk_shift);
             const double xx = XM == kXSplit ? (cc < a.split ? x : x2s)[cc] : x[cc];
-            s += raw_decode<VF>(raw_fetch<VF>(A.val, lo + k), tab) * xx;
+            s += ent_val<VF>(w, raw_fetch<VF>(A.val, lo + k), tab, A.pk_shift) * xx;
         }
 #pragma unroll
         for (int o = L / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -668,16 +685,22 @@ __global__ void __launch_bounds__(256, IRK_UPCLS_MINB) k_up_cls(Mat S, Mat Q, Sp
         const int row = slice * 32 + lane;
         const int i = min(row, n - 1);
         double ov[7];
+        // (offsets ascend: off[0] <= ... <= off[6]; a slice away from both ends needs no clamps)
+        if (slice * 32 + S.off[0] >= 0 && slice * 32 + 31 + S.off[6] < n) {
 #pragma unroll
-        for (int d = 0; d < 7; ++d) ov[d] = x[min(max(i + S.off[d], 0), n - 1)];
+            for (int d = 0; d < 7; ++d) ov[d] = x[row + S.off[d]];
+        } else {
+#pragma unroll
+            for (int d = 0; d < 7; ++d) ov[d] = x[min(max(i + S.off[d], 0), n - 1)];
+        }
         double zv[kPre], qv[kPre];
 #pragma unroll
         for (int k = 0; k < kPre; ++k) {
             zv[k] = 0.0;
             qv[k] = 0.0;
             if (k < len) {
-                qv[k] = raw_decode<VF>(v[k], tab);
-                zv[k] = z[c[k]];
+                qv[k] = ent_val<VF>(c[k], v[k], tab, Q.pk_shift);
+                zv[k] = z[ent_col<VF>(c[k], Q.pk_shift)];
             }
         }
         double s = 0.0;
@@ -692,8 +715,8 @@ __global__ void __launch_bounds__(256, IRK_UPCLS_MINB) k_up_cls(Mat S, Mat Q, Sp
         for (int k = 0; k < kPre; ++k)
             if (k < len) s += qv[k] * zv[k];
         for (int k = kPre; k < len; ++k) {
-            const int cc = __ldg(Q.idx + base + k * 32 + lane);
-            s += raw_decode<VF>(raw_fetch<VF>(Q.val, base + k * 32 + lane), tab) * z[cc];
+            const int w = __ldg(Q.idx + base + k * 32 + lane);
+            s += ent_val<VF>(w, raw_fetch<VF>(Q.val, base + k * 32 + lane), tab, Q.pk_shift) * z[ent_col<VF>(w, Q.pk_shift)];
         }
         if (row < n) y[row] = s;
         slice += stride;
@@ -868,24 +891,26 @@ __global__ void __launch_bounds__(256, 4) k_up_cls_rs(Mat S, Mat Q, SpmvArgs a) 
     if (a.late) pdl_trigger();
 }
 
-// Resident CTAs of a persistent kernel on this device (cached per kernel).
+// Resident CTAs of a persistent kernel on the current device (cached per
+// kernel and device).
 template <class K>
 int persistent_blocks(K kernel, int want) {
-    static thread_local std::map<const void*, int> cache;
-    const void* key = reinterpret_cast<const void*>(kernel);
+    static thread_local std::map<std::pair<const void*, int>, int> cache;
+    int dev_id = 0;
+    IRK_CUDA_CHECK(cudaGetDevice(&dev_id));
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), dev_id);
     auto it = cache.find(key);
-    int per_sm = 0;
+    int resident = 0;
     if (it == cache.end()) {
-        int dev_id = 0, sms = 148;
-        IRK_CUDA_CHECK(cudaGetDevice(&dev_id));
+        int sms = 148, per_sm = 0;
         IRK_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev_id));
         IRK_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0));
-        per_sm = std::max(per_sm, 1) * sms;
-        cache[key] = per_sm;
+        resident = std::max(per_sm, 1) * sms;
+        cache[key] = resident;
     } else {
-        per_sm = it->second;
+        resident = it->second;
     }
-    return std::max(1, std::min(want, per_sm));
+    return std::max(1, std::min(want, resident));
 }
 
 template <int XM, int VF, int L>
@@ -935,6 +960,7 @@ void launch_lt_vf(const Mat& A, const SpmvArgs& a, cudaStream_t st) {
     }
     switch (A.vf) {
     case kU8: launch_lt<XM, kU8>(A, a, st); break;
+    case kP8: launch_lt<XM, kP8>(A, a, st); break;
     case kU16: launch_lt<XM, kU16>(A, a, st); break;
     case kF64: launch_lt<XM, kF64>(A, a, st); break;
     default: throw InvalidArgument("spmv: lane-tree operators store fp64 values or codes");
@@ -2417,6 +2443,7 @@ void up_cls(const Mat& S, const Mat& Q, const SpmvArgs& a_in, cudaStream_t st) {
     }
     switch (Q.vf) {
     case kU8: launch(k_up_cls<kU8>, persistent_blocks(k_up_cls<kU8>, want), 256, 0, st, S, Q, a); break;
+    case kP8: launch(k_up_cls<kP8>, persistent_blocks(k_up_cls<kP8>, want), 256, 0, st, S, Q, a); break;
     case kU16: launch(k_up_cls<kU16>, persistent_blocks(k_up_cls<kU16>, want), 256, 0, st, S, Q, a); break;
     default: launch(k_up_cls<kF64>, persistent_blocks(k_up_cls<kF64>, want), 256, 0, st, S, Q, a); break;
     }

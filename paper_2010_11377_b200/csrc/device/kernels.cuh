@@ -38,7 +38,10 @@ enum MatFmt { kSell = 0, kDia = 1, kCsrVec = 2, kRowSig = 3 };
 // (lossless: a class is a distinct tuple of fp64 bit patterns).  On the
 // uniform P1 grid nearly every row is interior, so a row costs one byte and
 // one coalesced load instead of nd codes.
-enum ValFmt { kF64 = 0, kU8 = 1, kU16 = 2, kCls = 3 };
+// kP8 (composed operators with value codes): the dictionary code rides in the
+// top bits of the column index word (Mat::pk_shift = 32 - code bits; the
+// columns fit below), one 4-byte load per entry and no separate value stream.
+enum ValFmt { kF64 = 0, kU8 = 1, kU16 = 2, kCls = 3, kP8 = 4 };
 
 struct Mat {
     int fmt = kSell;
@@ -58,6 +61,7 @@ struct Mat {
     // entries staged per lane and row by the pipelined kernel (4..6, a tuning
     // hint: about the 95th percentile row length / lanes)
     int tree = 0;
+    int pk_shift = 24;  // kP8: column = word & (2^pk_shift - 1), code = word >> pk_shift
     // RSIG: per row the signature id and base columns; per signature its
     // length and `rs_w` slots of (offset, value); an offset with kRsQ set is
     // relative to base1 and addresses the second operand (x2) of a split product

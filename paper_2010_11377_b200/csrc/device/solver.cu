@@ -142,7 +142,8 @@ const T* DeviceSolver::upload_array(const std::vector<T>& h) {
 }
 
 // Stores the entry values (fp64 or dictionary codes) of an operator.
-void DeviceSolver::upload_values(dev::Mat& m, const std::vector<double>& vals, double omega) {
+void DeviceSolver::upload_values(dev::Mat& m, const std::vector<double>& vals, double omega,
+                                 std::vector<unsigned>* codes_out) {
     // Small operators keep fp64 values: their kernels are latency-bound and a
     // dictionary lookup is one more dependent memory trip.
     const long long min_rows = dev::option("IRK_CODES_MIN_ROWS", 100000);
@@ -163,7 +164,17 @@ void DeviceSolver::upload_values(dev::Mat& m, const std::vector<double>& vals, d
     // copy costs a dependent prologue and a barrier; IRK_U8_TAB_SMEM=1 keeps it)
     static const bool tab_smem = std::getenv("IRK_U8_TAB_SMEM") != nullptr;
     m.tab_smem = tab_smem ? 1 : 0;
-    if (d.vf == dev::kU8) {
+    int code_bits = 1;
+    while ((size_t(1) << code_bits) < d.tab.size()) ++code_bits;
+    if (codes_out && dev::option("IRK_PACK8", 1) != 0 && code_bits <= 16 &&
+        static_cast<long long>(m.cols) <= (1LL << (32 - code_bits))) {
+        // code and column share one index word (kP8); the caller packs them
+        m.pk_shift = 32 - code_bits;
+        if (d.vf == dev::kU8)
+            codes_out->assign(d.c8.begin(), d.c8.end());
+        else
+            codes_out->assign(d.c16.begin(), d.c16.end());
+    } else if (d.vf == dev::kU8) {
         m.val = upload_array(d.c8);
         m.bytes += d.c8.size();
     } else {
@@ -177,6 +188,12 @@ void DeviceSolver::upload_values(dev::Mat& m, const std::vector<double>& vals, d
         for (size_t c = 0; c < d.tab.size(); ++c) wd[c] = omega * (1.0 / d.tab[c]);
         m.wdtab = upload_array(wd);
     }
+}
+
+void DeviceSolver::pack_codes(dev::Mat& m, std::vector<int>& idx, const std::vector<unsigned>& codes) {
+    for (size_t e = 0; e < idx.size(); ++e) idx[e] = static_cast<int>(static_cast<unsigned>(idx[e]) | (codes[e] << m.pk_shift));
+    m.vf = dev::kP8;
+    m.val = nullptr;
 }
 
 namespace {
@@ -472,7 +489,11 @@ bool DeviceSolver::upload_up_cls(const Csr& U, int n, dev::Mat& Sm, dev::Mat& Qm
     }
     if (!to_row_classes({&m}, {&L.v}, 0.0)) return false;
     Sm = m;
-    if (!upload_rowsig(Q, 1, 0, Qm)) Qm = upload(Q, false, 0.0, 1);
+    if (!upload_rowsig(Q, 1, 0, Qm)) {
+        pack_sell_ = true;  // k_up_cls reads packed entries
+        Qm = upload(Q, false, 0.0, 1);
+        pack_sell_ = false;
+    }
     return true;
 }
 
@@ -498,9 +519,16 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega, int tr
             m.tree = static_cast<int>(dev::option("IRK_LT_MM", std::min(std::max(mm, 4), 6)));
         }
         m.ptr = upload_array(A.ptr);
-        m.idx = upload_array(A.idx);
         m.bytes += sizeof(int) * (A.ptr.size() + A.idx.size());
-        upload_values(m, A.val, omega);
+        std::vector<unsigned> codes;
+        upload_values(m, A.val, omega, &codes);
+        if (!codes.empty()) {
+            std::vector<int> idx = A.idx;
+            pack_codes(m, idx, codes);
+            m.idx = upload_array(idx);
+        } else {
+            m.idx = upload_array(A.idx);
+        }
         return m;
     }
     DiaLayout L;
@@ -596,9 +624,11 @@ dev::Mat DeviceSolver::upload(const Csr& A, bool allow_dia, double omega, int tr
     }
     m.fmt = dev::kSell;
     m.sptr = upload_array(sptr);
-    m.idx = upload_array(idx);
     m.bytes += sizeof(int) * (sptr.size() + idx.size());
-    upload_values(m, v, omega);
+    std::vector<unsigned> codes;
+    upload_values(m, v, omega, pack_sell_ ? &codes : nullptr);
+    if (!codes.empty()) pack_codes(m, idx, codes);
+    m.idx = upload_array(idx);
     return m;
 }
 

@@ -165,7 +165,12 @@ private:
     // DIA row classes (dev::kCls) for one operator or a pair sharing a pattern
     bool to_row_classes(std::vector<dev::Mat*> mats, const std::vector<const std::vector<double>*>& vals,
                         double omega);
-    void upload_values(dev::Mat& m, const std::vector<double>& vals, double omega);
+    // codes_out (optional): when the values are dictionary codes and code +
+    // column fit one 32-bit word, the codes are returned instead of uploaded
+    // and m.pk_shift is set; the caller packs them with pack_codes (kP8)
+    void upload_values(dev::Mat& m, const std::vector<double>& vals, double omega,
+                       std::vector<unsigned>* codes_out = nullptr);
+    void pack_codes(dev::Mat& m, std::vector<int>& idx, const std::vector<unsigned>& codes);
     template <class T> const T* upload_array(const std::vector<T>& h);
     double* alloc(size_t count);
     void* raw_alloc(size_t bytes);
@@ -235,6 +240,7 @@ private:
     // (a sweep) and may be launched programmatically (IRK_PDL_FINE)
     bool vc_pdl_first_ = false;
     double last_timed_bytes_ = 0.0;
+    bool pack_sell_ = false;  // upload(): pack the next SELL operator's codes (the up leg's Q part)
 };
 
 }  // namespace irkb

@@ -116,7 +116,7 @@ def test_device_cycle_bitwise_both_forms(make, compose, tail, monkeypatch):
 @pytest.mark.gpu
 @pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
 @pytest.mark.parametrize("env", [{"IRK_UP_CLS": "0"}, {"IRK_LT_MM": "4"}, {"IRK_LT_MM": "6"},
-                                 {"IRK_ROW_CLASSES": "0"}, {"IRK_ROW_SIG": "1"}, {"IRK_ROW_SIG": "7"}])
+                                 {"IRK_ROW_CLASSES": "0"}, {"IRK_ROW_SIG": "1"}, {"IRK_ROW_SIG": "7"}, {"IRK_PACK8": "0"}])
 def test_storage_switches_are_bit_identical(env, monkeypatch):
     """The up leg as row classes + SELL or as one split SELL operator, the
     lane-tree operators as CSR or row signatures (opt-in), and the pipelined
