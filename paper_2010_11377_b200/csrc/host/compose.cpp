@@ -38,10 +38,10 @@ namespace irkb {
 namespace {
 
 // Lanes per row of a composed operator: about `per_lane` entries per lane
-// (IRK_LT_PER_LANE10 tenths, default 5.0), a power of two <= 32.
+// (IRK_LT_PER_LANE10 tenths, default 6.0), a power of two <= 32.
 int lanes_for(const Csr& A) {
     const char* v = std::getenv("IRK_LT_PER_LANE10");
-    const double per_lane = 0.1 * (v ? std::atoi(v) : 50);
+    const double per_lane = 0.1 * (v ? std::atoi(v) : 60);
     const double avg = A.rows ? static_cast<double>(A.nnz()) / A.rows : 0.0;
     int g = 1;
     while (g < 32 && per_lane * g < avg) g *= 2;

@@ -58,7 +58,7 @@ def test_lane_rule_and_scope(monkeypatch):
     assert u == 1  # 7-point fine level: sequential row sums (row classes + SELL on the device)
     assert g in (2, 4, 8, 16, 32)
     G = h.level(0, "G")
-    assert 5.0 * g >= G.nnz / G.n_rows > 5.0 * g / 2
+    assert 6.0 * g >= G.nnz / G.n_rows > 6.0 * g / 2
     # levels at or below the tail are not composed
     assert all(h.level(l, "G").n_rows == 0 for l in range(1, h.n_levels()))
     # Gauss-Seidel and V(2,3) hierarchies keep the recursive form
