@@ -144,3 +144,28 @@ def test_recursive_step_still_bitwise(monkeypatch):
     o = c.oracle.step(u, c.f_lift, restart=50, max_iter=500)
     assert d.report.iterations == o["iterations"]
     assert np.array_equal(d.K, o["K"]) and np.array_equal(d.u_next, o["u_next"])
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")
+def test_level0_leg_timing_hooks(monkeypatch):
+    """irkdev_time_kernel(7 | 8) time the composed level-0 legs alone and report
+    their algorithmic bytes (bench.py's vcycle_level0_roofline); a recursive
+    hierarchy rejects them."""
+    import ctypes as C
+    from paper_2010_11377_b200 import _abi
+    L = _abi.lib()
+    c = heat_case(256, s=2, ht=0.01)
+    h = c.device()._dev._h
+    n, nc = c.n, c.hiers[0].level(1, "A").n_rows
+    for which in (7, 8):
+        ms, b = C.c_double(), C.c_double()
+        _abi.check(L.irkdev_time_kernel(h, which, 5, C.byref(ms)))
+        _abi.check(L.irkdev_last_timed_bytes(h, C.byref(b)))
+        assert ms.value > 0.0
+        # at least the operand and result vectors once
+        assert b.value >= 8.0 * (n + nc)
+    monkeypatch.setenv("IRK_COMPOSE", "0")
+    r = heat_case(64, s=2, ht=0.01)
+    ms = C.c_double()
+    assert L.irkdev_time_kernel(r.device()._dev._h, 7, 1, C.byref(ms)) != 0
