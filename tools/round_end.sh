@@ -1,4 +1,5 @@
-# round-end records on the final code: tests, smoke, full-size parity, traffic, benches, launch list
+# Round-end records on the final code (one gpurun call): tests, smoke, full-size parity, whole-step traffic,
+# benches of every BASELINE workload, reference arm, bench launch list, phase times, ncu --set full of a V-cycle, C5 sweep.
 timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/tests_final.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/tests_final.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke_final.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/smoke_final.log
 timeout 1500 python tools/fullsize_parity.py C2 C4 C3 > gpurun_out/fullsize_parity_r2d.jsonl 2> gpurun_out/fullsize_parity_r2d.err; echo "parity rc=$?"
