@@ -113,11 +113,32 @@ Dict encode(const std::vector<double>& v) {
     std::sort(u.begin(), u.end());
     u.erase(std::unique(u.begin(), u.end()), u.end());
     if (u.size() > 65536) return d;
-    d.tab.resize(u.size());
-    std::memcpy(d.tab.data(), u.data(), u.size() * sizeof(double));
-    auto code = [&](uint64_t b) {
+    // Codes in order of first appearance (IRK_DICT_ORDER=0: sorted bit patterns):
+    // the entries a warp decodes together -- consecutive entries of a few rows
+    // with the same stencil -- then sit in adjacent dictionary slots, i.e. in
+    // one or two cache lines instead of scattered over the table.
+    std::vector<int> rank(u.size());
+    for (size_t q = 0; q < u.size(); ++q) rank[q] = static_cast<int>(q);
+    auto slot = [&](uint64_t b) {
         return static_cast<size_t>(std::lower_bound(u.begin(), u.end(), b) - u.begin());
     };
+    if (dev::option("IRK_DICT_ORDER", 1) != 0) {
+        std::vector<int> seen(u.size(), -1);
+        int next = 0;
+        uint64_t last = 0;
+        bool have = false;
+        for (long long i = 0; i < n && next < static_cast<int>(u.size()); ++i) {
+            if (have && bits[i] == last) continue;
+            last = bits[i];
+            have = true;
+            const size_t q = slot(bits[i]);
+            if (seen[q] < 0) seen[q] = next++;
+        }
+        rank = seen;
+    }
+    d.tab.resize(u.size());
+    for (size_t q = 0; q < u.size(); ++q) std::memcpy(&d.tab[rank[q]], &u[q], sizeof(double));
+    auto code = [&](uint64_t b) { return static_cast<size_t>(rank[slot(b)]); };
     if (u.size() <= 256) {
         d.vf = dev::kU8;
         d.c8.resize(v.size());
