@@ -8,6 +8,7 @@
 #include <atomic>
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <utility>
 #include <string>
 
@@ -622,6 +623,9 @@ __global__ void __launch_bounds__(256, IRK_LT_MINB) k_spmv_lt(Mat A, SpmvArgs a)
 #ifndef IRK_UPCLS_PRE
 #define IRK_UPCLS_PRE 7
 #endif
+#ifndef IRK_UPCLS_SPEC
+#define IRK_UPCLS_SPEC 1
+#endif
 template <int VF>
 __global__ void __launch_bounds__(256, IRK_UPCLS_MINB) k_up_cls(Mat S, Mat Q, SpmvArgs a) {
     using Raw = typename RawVal<VF>::type;
@@ -693,30 +697,59 @@ __global__ void __launch_bounds__(256, IRK_UPCLS_MINB) k_up_cls(Mat S, Mat Q, Sp
 #pragma unroll
             for (int d = 0; d < 7; ++d) ov[d] = x[min(max(i + S.off[d], 0), n - 1)];
         }
-        double zv[kPre], qv[kPre];
+        // the slice length is warp-uniform: the common lengths run without
+        // per-entry predicates (IRK_UPCLS_SPEC=0 at build time: predicated form)
+        auto stencil = [&]() {
+            double t = 0.0;
+            if (__all_sync(0xffffffffu, cls == static_cast<unsigned>(S.dom))) {
 #pragma unroll
-        for (int k = 0; k < kPre; ++k) {
-            zv[k] = 0.0;
-            qv[k] = 0.0;
-            if (k < len) {
+                for (int d = 0; d < 7; ++d) t += S.dom_tab[d] * ov[d];
+            } else {
+#pragma unroll
+                for (int d = 0; d < 7; ++d) t += __ldg(S.tab + cls * 7 + d) * ov[d];
+            }
+            return t;
+        };
+        auto fixed = [&](auto lenc) {
+            constexpr int LEN = decltype(lenc)::value;
+            double zv[LEN], qv[LEN];
+#pragma unroll
+            for (int k = 0; k < LEN; ++k) {
                 qv[k] = ent_val<VF>(c[k], v[k], tab, Q.pk_shift);
                 zv[k] = z[ent_col<VF>(c[k], Q.pk_shift)];
             }
-        }
-        double s = 0.0;
-        if (__all_sync(0xffffffffu, cls == static_cast<unsigned>(S.dom))) {
+            double t = stencil();
 #pragma unroll
-            for (int d = 0; d < 7; ++d) s += S.dom_tab[d] * ov[d];
-        } else {
+            for (int k = 0; k < LEN; ++k) t += qv[k] * zv[k];
+            return t;
+        };
+        double s;
+#if IRK_UPCLS_SPEC
+        if (len == 7 && kPre >= 7) {
+            s = fixed(std::integral_constant<int, 7>{});
+        } else if (len == 6 && kPre >= 6) {
+            s = fixed(std::integral_constant<int, 6>{});
+        } else
+#endif
+        {
+            double zv[kPre], qv[kPre];
 #pragma unroll
-            for (int d = 0; d < 7; ++d) s += __ldg(S.tab + cls * 7 + d) * ov[d];
-        }
+            for (int k = 0; k < kPre; ++k) {
+                zv[k] = 0.0;
+                qv[k] = 0.0;
+                if (k < len) {
+                    qv[k] = ent_val<VF>(c[k], v[k], tab, Q.pk_shift);
+                    zv[k] = z[ent_col<VF>(c[k], Q.pk_shift)];
+                }
+            }
+            s = stencil();
 #pragma unroll
-        for (int k = 0; k < kPre; ++k)
-            if (k < len) s += qv[k] * zv[k];
-        for (int k = kPre; k < len; ++k) {
-            const int w = __ldg(Q.idx + base + k * 32 + lane);
-            s += ent_val<VF>(w, raw_fetch<VF>(Q.val, base + k * 32 + lane), tab, Q.pk_shift) * z[ent_col<VF>(w, Q.pk_shift)];
+            for (int k = 0; k < kPre; ++k)
+                if (k < len) s += qv[k] * zv[k];
+            for (int k = kPre; k < len; ++k) {
+                const int w = __ldg(Q.idx + base + k * 32 + lane);
+                s += ent_val<VF>(w, raw_fetch<VF>(Q.val, base + k * 32 + lane), tab, Q.pk_shift) * z[ent_col<VF>(w, Q.pk_shift)];
+            }
         }
         if (row < n) y[row] = s;
         slice += stride;
